@@ -1,0 +1,354 @@
+#!/usr/bin/env python
+"""Benchmark of the JUQCS hot path on B200 (BASELINE.json metric).
+
+Workload (one "step" = one pass of the whole hot path over one batch of
+synthetic input = the whole circuit applied to the resident state):
+  N GPUs = 1: BASELINE config 2 -- N=30 E (16 GiB), H on all 30 qubits, then
+              20 layers of Haar U(2) on every qubit + CNOTs on a random perfect
+              matching (seed 1, 930 gates).
+  N GPUs = P: weak scaling, the same recipe at n = 30 + log2(P) qubits, 2^30
+              amplitudes per GPU, top log2(P) qubits global (one process per
+              GPU, NCCL exchange), as in BASELINE config 3's series.
+value = aggregate effective HBM GB/s = sum over gates of the gate's
+algorithmic bytes (SURVEY.md §8(d) byte-accounting: 32 B x amplitudes touched
+by the gate, 0 for SWAP) over all GPUs / device time (max over ranks).
+Inputs are larger than L2 (16 GiB state >> 126 MB), so no L2 flush is needed.
+
+--impl reference: the oracle (plain CPU fp64 simulator, oracle/) timed on the
+host cores on a bounded sample of the same workload, same metric and unit.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import qsim_inputs as C  # noqa: E402
+
+METRIC = "gates/sec and effective HBM GB/s per gate sweep at N qubits, 1/2/4/8 B200"
+UNIT = "GB/s"
+
+
+def gate_bytes(circ, amp_bytes=16) -> float:
+    """Algorithmic bytes of every gate had it run alone."""
+    n = circ.n
+    tot = 0.0
+    for g in range(len(circ)):
+        name, kind, t, t2, ctl, u = circ.gate(g)
+        if kind == 1:
+            continue
+        off = abs(u[0, 1]) == 0 and abs(u[1, 0]) == 0
+        if off and u[0, 0] == 1 and u[1, 1] == 1:
+            continue
+        b = 2.0 * amp_bytes * 2.0 ** (n - len(ctl))
+        if off and (u[0, 0] == 1 or u[1, 1] == 1):
+            b *= 0.5
+        tot += b
+    return tot
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def workload(world):
+    k = int(round(math.log2(world)))
+    n = 30 + k
+    circ = C.layered(n, 20, seed=1)
+    name = ("config2: N=30 E fp64 (16 GiB), H wall + 20 layers (Haar U(2) on every qubit + CNOT perfect "
+            "matching), 930 gates, seed 1" if world == 1 else
+            f"config2 recipe weak-scaled: N={n} E fp64, 2^30 amplitudes per GPU, top {k} qubits global, "
+            f"H wall + 20 layers (Haar U(2) on every qubit + CNOT matching), {len(circ)} gates, seed 1")
+    return n, circ, name
+
+
+def cpu_sample(circ_full, budget_s=15.0):
+    """Time the oracle on the first gates of the same workload (bounded sample)."""
+    import oracle
+    import psutil
+
+    n = circ_full.n
+    need = (16 << n) * 1.5
+    if psutil.virtual_memory().available < need:
+        n = 28
+    circ = C.layered(n, 20, seed=1) if n != circ_full.n else circ_full
+    a = oracle.e_init(n)
+    done, t_all, nbytes = 0, 0.0, 0.0
+    while t_all < budget_s and done < len(circ):
+        one = circ.slice(done, done + 1)
+        t0 = time.perf_counter()
+        oracle.e_run(a, n, one)
+        t_all += time.perf_counter() - t0
+        nbytes += gate_bytes(one)
+        done += 1
+    return {"value": nbytes / t_all / 1e9, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"first {done} gates of the workload's circuit at N={n} ({t_all:.1f} s, "
+                      f"{done / t_all:.3f} gates/s)"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    n, circ, name = workload(world)
+    W, K = args.warmup, args.steps
+    import oracle
+    import psutil
+
+    if psutil.virtual_memory().available < (16 << n) * 1.5:
+        n = 28
+        circ = C.layered(n, 20, seed=1)
+    a = oracle.e_init(n)
+    # each step: a bounded sample -- the next `g` gates of the circuit (about 2 s of CPU work)
+    t0 = time.perf_counter()
+    oracle.e_run(a, n, circ.slice(0, 1))
+    t1 = max(time.perf_counter() - t0, 1e-3)
+    g = max(1, int(2.0 / t1))
+    pos = 1
+
+    def step():
+        nonlocal pos
+        if pos + g > len(circ):
+            pos = 0
+        part = circ.slice(pos, pos + g)
+        pos += g
+        t0 = time.perf_counter()
+        oracle.e_run(a, n, part)
+        return time.perf_counter() - t0, gate_bytes(part), g
+
+    for _ in range(W):
+        step()
+    tt, bb, gg = 0.0, 0.0, 0
+    for _ in range(K):
+        t, b, c = step()
+        tt, bb, gg = tt + t, bb + b, gg + c
+    v = bb / tt / 1e9
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": tt / K * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": name, "reference_sample": f"{g} gates per step at N={n}"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                             "sample": f"{K} steps x {g} gates of the workload circuit at N={n}"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gates_per_s": gg / tt}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--fuse", type=int, default=1)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    assert args.warmup >= 3 or os.environ.get("BENCH_ALLOW_SHORT"), "timing rules: at least 3 warm-up steps"
+
+    import torch
+
+    torch.cuda.set_device(local)
+    import paper_1805_04708_b200 as q
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n, circ, name = workload(world)
+    if world > 1:
+        obj = [q.qsim_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        s = q.State(n, q.ENC_FP64, world, transport=q.TRANSPORT_NCCL, rank=rank, device=local,
+                    nccl_id=obj[0], fuse=args.fuse)
+    else:
+        s = q.State(n, q.ENC_FP64, 1, fuse=args.fuse, device=local)
+    gates = q.pack_gates(circ)  # host gate records (the step's input)
+    stream = torch.cuda.ExternalStream(s.stream())
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        s.apply_circuit(gates)
+    s.sync()
+    s.reset_stats()
+    s.profile(True)
+    s.profile_read()
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    s.sync()
+    e0.record(stream)
+    for _ in range(args.steps):
+        s.apply_circuit(gates)
+    e1.record(stream)
+    s.sync()
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    st = s.stats()
+    prof = s.profile_read()
+    s.profile(False)
+    t_dev = torch.tensor([ms, st["gate_bytes"], float(st["kernels"])], dtype=torch.float64, device="cuda")
+    if dist:
+        mx = t_dev.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = t_dev.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms_max, bytes_all, launches = mx[0].item(), sm[1].item(), int(sm[2].item())
+    else:
+        ms_max, bytes_all, launches = ms, st["gate_bytes"], st["kernels"]
+    value = bytes_all / (ms_max / 1e3) / 1e9
+    gates_per_s = len(circ) * args.steps / (ms_max / 1e3)
+
+    # ---- end to end through the public API with host buffers ----
+    # every step: reset to |0...0> (the method's input state), H2D of the host
+    # gate records, the circuit, D2H of the result (per-qubit probabilities).
+    e2e_steps = max(1, min(args.steps, 3))
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        s.reset()
+        s.apply_circuit(gates)
+        p1 = s.probabilities()
+    t_e2e = time.perf_counter() - t0
+    barrier()
+    if dist:
+        tt = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = tt.item()
+    e2e = {"value": bytes_all / args.steps * e2e_steps / t_e2e / 1e9, "unit": UNIT,
+           "h2d_bytes_per_step": 88 * len(circ), "d2h_bytes_per_step": 8 * len(p1),
+           "what": "qsim_reset + qsim_apply_circuit(host gate records) + qsim_probabilities(host buffer), wall clock"}
+
+    # ---- roofline of the dominant kernel ----
+    peak, peak_src = peaks()
+    dom = max(prof.items(), key=lambda kv: kv[1]["ms"]) if prof else None
+    roof = None
+    per_kernel = {}
+    for k, v in prof.items():
+        per_kernel[k] = {"launches": v["launches"], "ms_total": v["ms"],
+                         "avg_ms": v["ms"] / max(v["launches"], 1),
+                         "GBps": v["bytes"] / max(v["ms"], 1e-9) / 1e6,
+                         "share_of_step": v["ms"] / ms}
+    if dom:
+        k, v = dom
+        achieved = v["bytes"] / (v["ms"] / 1e3) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get(k)
+            except Exception:
+                traffic = None
+        roof = {"bound": "hbm", "kernel": k, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "bytes_per_launch": v["bytes"] / v["launches"], "avg_launch_ms": v["ms"] / v["launches"]}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_sample(circ)
+        except Exception as ex:  # never let the baseline kill the bench line
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "oracle", "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": name, "n_qubits": n, "gates_per_step": len(circ),
+                           "amplitudes_per_gpu": 1 << (n - int(round(math.log2(world)))),
+                           "fuse": args.fuse, "l2": "inputs larger than L2 (16 GiB state per GPU), no flush",
+                           "parallelism": f"state sharded over {world} GPU(s) by the top log2(P) qubits"},
+                "gates_per_s": gates_per_s, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clk, "per_kernel": per_kernel,
+                "library": {"passes": st["passes"], "fused_gates": st["fused_gates"], "sweeps": st["sweeps"],
+                            "exchanges": st["exchanges"], "exchange_GB": st["exchange_bytes"] / 1e9}}
+        print(json.dumps(line), flush=True)
+    s.close()
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

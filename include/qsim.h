@@ -1,0 +1,260 @@
+/*
+ * qsim.h -- C-ABI of the B200-native JUQCS hot path (arXiv:1805.04708).
+ *
+ * The library applies single-qubit and controlled (2-/3-qubit) gate matrices
+ * to a 2^N-amplitude wave function stored either as complex fp64 ("E",
+ * PAPER.md:113-121, 440) or in the paper's adaptive 2-byte polar code ("A",
+ * PAPER.md §4.1), sharded over P = 2^k shards by the top k
+ * physical index bits (§3.2).  All device work runs in
+ * the library's own sm_100a kernels; there is no CPU fallback: a call that
+ * needs the GPU fails with QSIM_ECUDA when no device is usable.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Qubit j is bit j of the basis index, qubit 0 least significant
+ *    (PAPER.md:255-258).  All qubit and amplitude indices at this boundary are
+ *    LOGICAL; the internal qubit map is never visible.
+ *  - A 2x2 gate matrix U is 8 doubles, row-major, interleaved (re, im):
+ *    {u00r,u00i,u01r,u01i,u10r,u10i,u11r,u11i}; row = output |0>,|1> of the
+ *    target.  It is applied to every amplitude pair (a(..0_t..), a(..1_t..))
+ *    whose control bits are all 1 (Eq. NUM2; groups of
+ *    4/8 for CNOT/TOFFOLI-like gates, App. B
+ *    PAPER.md:1300-1363).  U is copied at call time.
+ *  - Ownership: the qsim_state handle owns all device memory and streams it
+ *    creates; the caller owns every host array passed in or out.
+ *  - Synchronisation: apply_* calls are stream-ordered and may return before
+ *    the GPU finishes; every read-out call (norm, probabilities,
+ *    expectations, measure, get_*) and qsim_sync are synchronous.
+ *  - Threading: a handle must not be used from two threads at once.
+ *  - Errors: every int-returning function returns QSIM_OK (0) or a negative
+ *    QSIM_E* code and sets a thread-local message read by qsim_last_error().
+ *    A failed call leaves the state unchanged unless the code is QSIM_ECUDA /
+ *    QSIM_ECOMM (device or communicator failure: the state is undefined).
+ */
+#ifndef QSIM_H
+#define QSIM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ---------------------------------------------------- */
+#define QSIM_OK 0
+#define QSIM_EINVAL (-1)       /* bad argument: qubit out of range, duplicates, N outside [2,63], ... */
+#define QSIM_ENOMEM (-2)       /* device allocation failed; message states the bytes needed */
+#define QSIM_ECUDA (-3)        /* CUDA runtime error or no usable device */
+#define QSIM_ECOMM (-4)        /* NCCL error */
+#define QSIM_EZERONORM (-5)    /* projection with norm^2 < 1e-14 */
+#define QSIM_ENOTUNITARY (-6)  /* ||U^dagger U - I||_max > 1e-10 */
+#define QSIM_EUNSUPPORTED (-7) /* valid request this build does not implement */
+
+/* ---- encodings ------------------------------------ */
+#define QSIM_ENC_FP64 0      /* E: 16 B/amplitude, interleaved (re, im) fp64 */
+#define QSIM_ENC_ADAPTIVE2 1 /* A: 2 B/amplitude, byte 0 = b0 (magnitude), byte 1 = b1 (angle) */
+
+/* ---- transports for sharded states (§3.2, 370-402) ----------- */
+#define QSIM_TRANSPORT_LOCAL 0 /* all nshards shards live on this process's device ("loopback"):
+                                  the exchange of a global-qubit gate is a device-to-device copy */
+#define QSIM_TRANSPORT_NCCL 1  /* one process per GPU; this process owns shard `rank`;
+                                  the exchange is NCCL send/recv over NVLink */
+
+/* ---- gate records ---------------------------------------------------- */
+#define QSIM_GATE_U 0    /* controlled 2x2 gate: target, controls[0..ncontrols-1], u */
+#define QSIM_GATE_SWAP 1 /* SWAP(target, target2): a relabelling of the qubit map, moves 0 bytes */
+
+typedef struct qsim_state qsim_state; /* opaque; owns all device memory of one process */
+
+typedef struct qsim_gate {
+    int32_t kind;        /* QSIM_GATE_U or QSIM_GATE_SWAP */
+    int32_t target;      /* logical target qubit, 0..N-1 */
+    int32_t target2;     /* SWAP only: second qubit; ignored otherwise */
+    int32_t ncontrols;   /* 0, 1 or 2 */
+    int32_t controls[2]; /* logical control qubits, distinct from target and each other */
+    double u[8];         /* U as described above (ignored for SWAP) */
+} qsim_gate;             /* 88 bytes, no padding */
+
+typedef struct qsim_config {
+    int32_t n_qubits;    /* N, 2 <= N <= 63 (QUBITS) */
+    int32_t encoding;    /* QSIM_ENC_* */
+    int32_t nshards;     /* P = 2^k >= 1; N - k >= 10 local qubits required */
+    int32_t transport;   /* QSIM_TRANSPORT_* (ignored when nshards == 1) */
+    int32_t rank;        /* NCCL: this process's shard index, 0..P-1 */
+    int32_t device;      /* CUDA device ordinal to use; -1 = current device */
+    const uint8_t *nccl_id; /* NCCL: 128-byte ncclUniqueId from qsim_nccl_unique_id on rank 0 */
+    int64_t chunk_bytes; /* exchange chunk per transfer; 0 = default (2^{N-3}/P B in
+                            total, i.e. 2^{N-4}/P per buffer of a double buffer, capped at 512 MiB) */
+    int32_t fuse;        /* 1 = fuse runs of gates into shared-memory tile passes (default), 0 = one sweep per gate */
+    int32_t reserved;
+} qsim_config;
+
+/* Counters since creation (or the last qsim_reset_stats). Bytes are ALGORITHMIC
+ * bytes (SURVEY.md §8(d) byte-accounting rule), summed over the shards this
+ * process owns. */
+typedef struct qsim_stats {
+    int64_t gates;            /* gate records applied (SWAPs included) */
+    int64_t kernels;          /* device kernels launched by the library */
+    int64_t sweeps;           /* single-gate sweep launches */
+    int64_t passes;           /* fused tile-pass launches */
+    int64_t fused_gates;      /* gates applied inside fused passes */
+    int64_t exchanges;        /* global<->local swap exchanges (a7) */
+    double hbm_bytes;         /* algorithmic HBM bytes of sweeps + passes + exchange kernels */
+    double gate_bytes;        /* sum over gates of the per-gate algorithmic bytes had each run alone */
+    double exchange_bytes;    /* bytes sent per direction by this process's shards */
+} qsim_stats;
+
+/* ---- lifetime ---------------------------------------------------------- */
+
+/* Create |0...0> (Eq. appa0) with N qubits in `encoding`,
+ * split into `ngpus` shards that all live on the CURRENT device
+ * (QSIM_TRANSPORT_LOCAL; use qsim_create_ex for one process per GPU).
+ * *out receives the handle.  Errors: EINVAL (N, ngpus not a power of two,
+ * fewer than 10 local qubits), ENOMEM (message has the byte count), ECUDA. */
+int qsim_create(int n_qubits, int encoding, int ngpus, qsim_state **out);
+
+/* Full configuration (see qsim_config).  For QSIM_TRANSPORT_NCCL every rank
+ * calls this collectively with the same n_qubits/encoding/nshards/nccl_id. */
+int qsim_create_ex(const qsim_config *cfg, qsim_state **out);
+
+/* Free all device memory and the communicator.  NULL is a no-op. */
+int qsim_destroy(qsim_state *s);
+
+/* Rank 0 of a QSIM_TRANSPORT_NCCL job calls this and broadcasts the 128
+ * bytes to the other ranks (e.g. over torch.distributed). ECOMM on failure. */
+int qsim_nccl_unique_id(uint8_t out[128]);
+
+/* ---- gates (a2-a8) -------------------------------------------------------- */
+
+/* Apply U to logical `target` iff all `controls` are 1 (Eq. NUM2 with
+ * controls).  A gate whose target sits on a global
+ * (shard-index) bit is preceded by a half-shard swap exchange that moves the
+ * qubit to a local bit; diagonal gates never exchange.
+ * Errors: EINVAL (qubit outside [0,N), duplicates, ncontrols > 2),
+ * ENOTUNITARY. */
+int qsim_apply_gate(qsim_state *s, const double u[8], int target, const int *controls, int ncontrols);
+
+/* SWAP(q1, q2) as a qubit-map relabelling (0 bytes moved).  EINVAL. */
+int qsim_apply_swap(qsim_state *s, int q1, int q2);
+
+/* Apply `ngates` records in order.  Consecutive local gates are fused into
+ * shared-memory tile passes (one HBM pass for many gates, the "combining
+ * ... to multi-qubit gates" of PAPER.md:787-790); the result equals applying
+ * them one by one up to floating-point reassociation (E) or is the same
+ * per-gate A computation (A gates are never fused).  All records are
+ * validated before any is applied; EINVAL / ENOTUNITARY name the index. */
+int qsim_apply_circuit(qsim_state *s, const qsim_gate *gates, size_t ngates);
+
+/* ---- read-out (a10, a11) ------------------------------------------------- */
+
+/* Sum_i |a_i|^2 (Eq. STAT1), decoded amplitudes for A. */
+int qsim_norm(qsim_state *s, double *norm2);
+
+/* p1[n] = P(qubit n = 1) = sum over |a(..1_n..)|^2, n = 0..N-1,
+ * not renormalised.  p1 has N entries. */
+int qsim_probabilities(qsim_state *s, double *p1);
+
+/* BEGIN MEASUREMENT: q[3n+0..2] = <Qx(n)>, <Qy(n)>, <Qz(n)>
+ * with <Qa(n)> = <psi|(1 - sigma^a_n)|psi>/2.  q has 3N entries.  May move
+ * global qubits to local bits (a relabelling; the logical state is unchanged). */
+int qsim_expectations(qsim_state *s, double *q);
+
+/* Projective measurement M of `qubit`: p0 = P(0)/norm^2,
+ * outcome 0 iff u < p0, then the other half is zeroed and the kept half is
+ * scaled by 1/sqrt(p_kept) (E) or re-encoded (A).  qsim_measure derives u
+ * from `seed` with splitmix64: x = splitmix64(seed), u = (x >> 11) * 2^-53.
+ * p0_out may be NULL.  EZERONORM if the kept half has norm^2 < 1e-14. */
+int qsim_measure(qsim_state *s, int qubit, uint64_t seed, int *outcome);
+int qsim_measure_u(qsim_state *s, int qubit, double u, int *outcome, double *p0_out);
+
+/* Amplitudes at `n` LOGICAL basis indices (each < 2^N), written as
+ * out[2k] = re, out[2k+1] = im (decoded for A).  For NCCL every rank
+ * calls it collectively and receives all n values. */
+int qsim_get_amplitudes(qsim_state *s, const uint64_t *logical_idx, size_t n, double *out);
+
+/* Whole state in logical order (2^N complex, interleaved), for tests at
+ * small N (N <= 30).  get: E or A (decoded); set: E only (A: EUNSUPPORTED). */
+int qsim_get_state(qsim_state *s, double *out);
+int qsim_set_state(qsim_state *s, const double *amps);
+
+/* A only: raw codes in logical order (2^N pairs (b0, b1) as int8) and the
+ * magnitude bounds r0 <= r1.  EUNSUPPORTED for E. */
+int qsim_get_codes(qsim_state *s, int8_t *codes, double *r0, double *r1);
+int qsim_set_codes(qsim_state *s, const int8_t *codes, double r0, double r1);
+
+/* ---- plumbing --------------------------------------------------------- */
+
+/* Re-initialise to |0...0> (Eq. appa0) and reset the qubit map; keeps all
+ * allocations (so a benchmark step can start from the method's input state). */
+int qsim_reset(qsim_state *s);
+
+/* Per-kernel-class timing: while enabled, every library kernel launch is
+ * bracketed by CUDA events on the launching stream.  qsim_profile_read
+ * synchronises, aggregates the finished records per class into out[0..max)
+ * (*nout = classes written), and clears them.  Bytes are algorithmic bytes. */
+#define QSIM_K_PASS 0      /* fused tile pass (E) */
+#define QSIM_K_SWEEP 1     /* single-gate sweep (E) */
+#define QSIM_K_XCHG 2      /* exchange-fused gate / swap copy (E and A) */
+#define QSIM_K_A_BOUNDS 3  /* A phase 1: post-gate bounds */
+#define QSIM_K_A_APPLY 4   /* A phase 2: decode-apply-encode */
+#define QSIM_K_A_FAST 5    /* A permutation / phase gates */
+#define QSIM_K_NUM 6
+typedef struct qsim_kernel_profile {
+    int32_t kind;
+    int32_t pad;
+    int64_t launches;
+    double ms;     /* summed event durations */
+    double bytes;  /* summed algorithmic bytes */
+} qsim_kernel_profile;
+int qsim_profile(qsim_state *s, int enable);
+int qsim_profile_read(qsim_state *s, qsim_kernel_profile *out, int max, int *nout);
+
+/* Wait for all work of this handle. */
+int qsim_sync(qsim_state *s);
+
+/* The cudaStream_t (as void*) the library launches shard `shard`'s kernels
+ * on (shard index local to this process), for event timing by the caller. */
+void *qsim_stream(qsim_state *s, int shard);
+
+int qsim_get_stats(qsim_state *s, qsim_stats *out);
+int qsim_reset_stats(qsim_state *s);
+
+/* Logical qubit -> physical bit map (N ints); bits >= N - log2(P) are global. */
+int qsim_get_qubit_map(qsim_state *s, int *pos);
+
+/* Thread-local message of the last failed call ("" if none). */
+const char *qsim_last_error(void);
+
+/* ---- planner (host only; callable without a GPU) ---------------------------
+ * The exchange/remap plan the executor follows (a2, a7): for testing the
+ * sharded path's host logic on CPU.  An op is either
+ *   QSIM_OP_EXCHANGE: swap physical global bit `g` with local bit `l`
+ *     (shard r and r ^ 2^(g-nl) trade half-shards; qubit map updated), or
+ *   QSIM_OP_GATE: gate on physical bits (target `l`, controls) with class
+ *     0 = dense, 1 = diagonal, 2 = anti-diagonal, 3 = identity (skipped).
+ * Ownership: qsim_plan_create allocates *out, qsim_plan_destroy frees it. */
+#define QSIM_OP_EXCHANGE 0
+#define QSIM_OP_GATE 1
+typedef struct qsim_plan qsim_plan;
+typedef struct qsim_plan_op {
+    int32_t type;        /* QSIM_OP_* */
+    int32_t g;           /* EXCHANGE: global physical bit */
+    int32_t l;           /* EXCHANGE: local victim bit; GATE: physical target bit */
+    int32_t cls;         /* GATE: matrix class */
+    int32_t ncontrols;   /* GATE */
+    int32_t controls[2]; /* GATE: physical control bits */
+    int32_t gate_index;  /* GATE: index of the record in the input list */
+} qsim_plan_op;
+
+int qsim_plan_create(int n_qubits, int nshards, const int *initial_map, const qsim_gate *gates, size_t ngates,
+                     qsim_plan **out);
+int64_t qsim_plan_num_ops(const qsim_plan *p);
+int qsim_plan_get_op(const qsim_plan *p, int64_t i, qsim_plan_op *op);
+int qsim_plan_final_map(const qsim_plan *p, int *pos);
+void qsim_plan_destroy(qsim_plan *p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QSIM_H */

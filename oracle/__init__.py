@@ -102,7 +102,7 @@ def e_swap(a: np.ndarray, n: int, q1: int, q2: int) -> np.ndarray:
 
 
 def e_run(a: np.ndarray, n: int, circuit) -> np.ndarray:
-    """Apply a circuit (paper_1805_04708_b200.circuits.Circuit arrays) in order."""
+    """Apply a circuit (qsim_inputs.Circuit arrays) in order."""
     _c128(a)
     g = circuit
     lib().oracle_e_run(_ptr(a.view(np.float64), _dp), n, len(g.kind), _ptr(g.kind, _i32p), _ptr(g.target, _i32p),

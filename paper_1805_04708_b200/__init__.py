@@ -1,0 +1,451 @@
+"""paper_1805_04708_b200 -- B200-native JUQCS hot path (arXiv:1805.04708).
+
+Thin ctypes binding over ``libqsim.so`` (the C-ABI declared in
+``include/qsim.h``).  Argument marshalling only: every step of the path runs
+in the library's sm_100a kernels.  There is no CPU fallback: importing this
+package fails loudly when ``libqsim.so`` is missing, and every compute call
+raises ``QsimError`` (code QSIM_ECUDA) when no GPU is usable.
+
+Function names mirror the C-ABI (``qsim_create``, ``qsim_apply_gate``,
+``qsim_apply_circuit``, ``qsim_probabilities``, ``qsim_measure``,
+``qsim_get_amplitudes`` ...); ``State`` is a convenience wrapper around them.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libqsim.so")
+
+QSIM_OK = 0
+QSIM_EINVAL = -1
+QSIM_ENOMEM = -2
+QSIM_ECUDA = -3
+QSIM_ECOMM = -4
+QSIM_EZERONORM = -5
+QSIM_ENOTUNITARY = -6
+QSIM_EUNSUPPORTED = -7
+
+ENC_FP64 = 0
+ENC_ADAPTIVE2 = 1
+TRANSPORT_LOCAL = 0
+TRANSPORT_NCCL = 1
+GATE_U = 0
+GATE_SWAP = 1
+OP_EXCHANGE = 0
+OP_GATE = 1
+
+
+class QsimError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"qsim error {code}: {msg}")
+        self.code = code
+
+
+class qsim_gate(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("target", ctypes.c_int32), ("target2", ctypes.c_int32),
+                ("ncontrols", ctypes.c_int32), ("controls", ctypes.c_int32 * 2), ("u", ctypes.c_double * 8)]
+
+
+class qsim_config(ctypes.Structure):
+    _fields_ = [("n_qubits", ctypes.c_int32), ("encoding", ctypes.c_int32), ("nshards", ctypes.c_int32),
+                ("transport", ctypes.c_int32), ("rank", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("nccl_id", ctypes.c_void_p), ("chunk_bytes", ctypes.c_int64), ("fuse", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+class qsim_stats(ctypes.Structure):
+    _fields_ = [("gates", ctypes.c_int64), ("kernels", ctypes.c_int64), ("sweeps", ctypes.c_int64),
+                ("passes", ctypes.c_int64), ("fused_gates", ctypes.c_int64), ("exchanges", ctypes.c_int64),
+                ("hbm_bytes", ctypes.c_double), ("gate_bytes", ctypes.c_double),
+                ("exchange_bytes", ctypes.c_double)]
+
+
+class qsim_kernel_profile(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("pad", ctypes.c_int32), ("launches", ctypes.c_int64),
+                ("ms", ctypes.c_double), ("bytes", ctypes.c_double)]
+
+
+KERNEL_NAMES = {0: "pass_e", 1: "sweep_e", 2: "xchg", 3: "a_bounds", 4: "a_apply", 5: "a_fast"}
+
+
+class qsim_plan_op(ctypes.Structure):
+    _fields_ = [("type", ctypes.c_int32), ("g", ctypes.c_int32), ("l", ctypes.c_int32), ("cls", ctypes.c_int32),
+                ("ncontrols", ctypes.c_int32), ("controls", ctypes.c_int32 * 2), ("gate_index", ctypes.c_int32)]
+
+
+assert ctypes.sizeof(qsim_gate) == 88
+
+# every symbol include/qsim.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "qsim_create", "qsim_create_ex", "qsim_destroy", "qsim_nccl_unique_id", "qsim_apply_gate", "qsim_apply_swap",
+    "qsim_apply_circuit", "qsim_norm", "qsim_probabilities", "qsim_expectations", "qsim_measure", "qsim_measure_u",
+    "qsim_get_amplitudes", "qsim_get_state", "qsim_set_state", "qsim_get_codes", "qsim_set_codes", "qsim_sync",
+    "qsim_stream", "qsim_get_stats", "qsim_reset", "qsim_profile", "qsim_profile_read", "qsim_reset_stats", "qsim_get_qubit_map", "qsim_last_error",
+    "qsim_plan_create", "qsim_plan_num_ops", "qsim_plan_get_op", "qsim_plan_final_map", "qsim_plan_destroy",
+)
+
+if not os.path.exists(_LIB_PATH):
+    raise ImportError(f"{_LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                      "(nvcc, sm_100a); there is no CPU fallback")
+
+_lib = ctypes.CDLL(_LIB_PATH)
+_P = ctypes.c_void_p
+_dp = ctypes.POINTER(ctypes.c_double)
+_ip = ctypes.POINTER(ctypes.c_int)
+
+_lib.qsim_last_error.restype = ctypes.c_char_p
+_lib.qsim_create.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)]
+_lib.qsim_create_ex.argtypes = [ctypes.POINTER(qsim_config), ctypes.POINTER(_P)]
+_lib.qsim_destroy.argtypes = [_P]
+_lib.qsim_nccl_unique_id.argtypes = [ctypes.c_void_p]
+_lib.qsim_apply_gate.argtypes = [_P, _dp, ctypes.c_int, _ip, ctypes.c_int]
+_lib.qsim_apply_swap.argtypes = [_P, ctypes.c_int, ctypes.c_int]
+_lib.qsim_apply_circuit.argtypes = [_P, ctypes.POINTER(qsim_gate), ctypes.c_size_t]
+_lib.qsim_norm.argtypes = [_P, _dp]
+_lib.qsim_probabilities.argtypes = [_P, _dp]
+_lib.qsim_expectations.argtypes = [_P, _dp]
+_lib.qsim_measure.argtypes = [_P, ctypes.c_int, ctypes.c_uint64, _ip]
+_lib.qsim_measure_u.argtypes = [_P, ctypes.c_int, ctypes.c_double, _ip, _dp]
+_lib.qsim_get_amplitudes.argtypes = [_P, ctypes.POINTER(ctypes.c_uint64), ctypes.c_size_t, _dp]
+_lib.qsim_get_state.argtypes = [_P, _dp]
+_lib.qsim_set_state.argtypes = [_P, _dp]
+_lib.qsim_get_codes.argtypes = [_P, ctypes.POINTER(ctypes.c_int8), _dp, _dp]
+_lib.qsim_set_codes.argtypes = [_P, ctypes.POINTER(ctypes.c_int8), ctypes.c_double, ctypes.c_double]
+_lib.qsim_sync.argtypes = [_P]
+_lib.qsim_stream.argtypes = [_P, ctypes.c_int]
+_lib.qsim_stream.restype = ctypes.c_void_p
+_lib.qsim_get_stats.argtypes = [_P, ctypes.POINTER(qsim_stats)]
+_lib.qsim_reset_stats.argtypes = [_P]
+_lib.qsim_get_qubit_map.argtypes = [_P, _ip]
+_lib.qsim_reset.argtypes = [_P]
+_lib.qsim_profile.argtypes = [_P, ctypes.c_int]
+_lib.qsim_profile_read.argtypes = [_P, ctypes.POINTER(qsim_kernel_profile), ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+_lib.qsim_plan_create.argtypes = [ctypes.c_int, ctypes.c_int, _ip, ctypes.POINTER(qsim_gate), ctypes.c_size_t,
+                                  ctypes.POINTER(_P)]
+_lib.qsim_plan_num_ops.argtypes = [_P]
+_lib.qsim_plan_num_ops.restype = ctypes.c_int64
+_lib.qsim_plan_get_op.argtypes = [_P, ctypes.c_int64, ctypes.POINTER(qsim_plan_op)]
+_lib.qsim_plan_final_map.argtypes = [_P, _ip]
+_lib.qsim_plan_destroy.argtypes = [_P]
+_lib.qsim_plan_destroy.restype = None
+
+
+def lib():
+    return _lib
+
+
+def lib_path():
+    return _LIB_PATH
+
+
+def _check(rc):
+    if rc != QSIM_OK:
+        raise QsimError(rc, _lib.qsim_last_error().decode(errors="replace"))
+    return rc
+
+
+def _dptr(a):
+    return a.ctypes.data_as(_dp)
+
+
+def pack_gates(circuit) -> ctypes.Array:
+    """Marshal a circuits.Circuit (or a list of (u, target, controls) / ('SWAP', q1, q2))
+    into a qsim_gate array."""
+    if hasattr(circuit, "kind"):
+        n = len(circuit)
+        arr = (qsim_gate * max(n, 1))()
+        kind, t, t2, nc, ct, u = circuit.kind, circuit.target, circuit.target2, circuit.nctrl, circuit.ctrl, circuit.u
+        buf = np.frombuffer(arr, dtype=np.uint8, count=88 * n).reshape(n, 88) if n else None
+        if n:
+            ints = np.zeros((n, 6), dtype=np.int32)
+            ints[:, 0], ints[:, 1], ints[:, 2], ints[:, 3] = kind, t, t2, nc
+            ints[:, 4:6] = ct.reshape(n, 2)
+            buf[:, :24] = ints.view(np.uint8).reshape(n, 24)
+            buf[:, 24:] = np.ascontiguousarray(u.reshape(n, 8)).view(np.uint8).reshape(n, 64)
+        return arr, n
+    items = list(circuit)
+    arr = (qsim_gate * max(len(items), 1))()
+    for i, g in enumerate(items):
+        if isinstance(g[0], str) and g[0].upper() == "SWAP":
+            arr[i].kind, arr[i].target, arr[i].target2 = GATE_SWAP, g[1], g[2]
+            continue
+        u, t = g[0], g[1]
+        ctl = list(g[2]) if len(g) > 2 else []
+        u8 = np.ascontiguousarray(np.asarray(u, dtype=np.complex128).reshape(2, 2)).view(np.float64).reshape(8)
+        arr[i].kind, arr[i].target, arr[i].target2, arr[i].ncontrols = GATE_U, t, -1, len(ctl)
+        for k, c in enumerate(ctl):
+            arr[i].controls[k] = c
+        for k in range(8):
+            arr[i].u[k] = u8[k]
+    return arr, len(items)
+
+
+# ----------------------------------------------------------------------------- C-ABI mirrors
+
+
+def qsim_nccl_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(_lib.qsim_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def qsim_create(n_qubits: int, encoding: int = ENC_FP64, ngpus: int = 1):
+    h = _P()
+    _check(_lib.qsim_create(n_qubits, encoding, ngpus, ctypes.byref(h)))
+    return h
+
+
+def qsim_create_ex(n_qubits, encoding=ENC_FP64, nshards=1, transport=TRANSPORT_LOCAL, rank=0, device=-1,
+                   nccl_id: bytes | None = None, chunk_bytes=0, fuse=1):
+    cfg = qsim_config()
+    cfg.n_qubits, cfg.encoding, cfg.nshards, cfg.transport = n_qubits, encoding, nshards, transport
+    cfg.rank, cfg.device, cfg.chunk_bytes, cfg.fuse = rank, device, chunk_bytes, fuse
+    idbuf = None
+    if nccl_id is not None:
+        idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
+        cfg.nccl_id = ctypes.addressof(idbuf)
+    h = _P()
+    _check(_lib.qsim_create_ex(ctypes.byref(cfg), ctypes.byref(h)))
+    return h
+
+
+def qsim_destroy(h):
+    _lib.qsim_destroy(h)
+
+
+def qsim_apply_gate(h, u, target, controls=()):
+    u8 = np.ascontiguousarray(np.asarray(u, dtype=np.complex128).reshape(2, 2)).view(np.float64).reshape(8)
+    c = (ctypes.c_int * 2)(*(list(controls) + [0, 0])[:2])
+    _check(_lib.qsim_apply_gate(h, _dptr(u8), target, c, len(controls)))
+
+
+def qsim_apply_swap(h, q1, q2):
+    _check(_lib.qsim_apply_swap(h, q1, q2))
+
+
+def qsim_apply_circuit(h, circuit):
+    arr, n = circuit if isinstance(circuit, tuple) else pack_gates(circuit)
+    _check(_lib.qsim_apply_circuit(h, arr, n))
+
+
+def qsim_norm(h) -> float:
+    v = ctypes.c_double()
+    _check(_lib.qsim_norm(h, ctypes.byref(v)))
+    return v.value
+
+
+def qsim_probabilities(h, n) -> np.ndarray:
+    p = np.empty(n, dtype=np.float64)
+    _check(_lib.qsim_probabilities(h, _dptr(p)))
+    return p
+
+
+def qsim_expectations(h, n) -> np.ndarray:
+    q = np.empty(3 * n, dtype=np.float64)
+    _check(_lib.qsim_expectations(h, _dptr(q)))
+    return q.reshape(n, 3)
+
+
+def qsim_measure(h, qubit, seed) -> int:
+    o = ctypes.c_int()
+    _check(_lib.qsim_measure(h, qubit, seed, ctypes.byref(o)))
+    return o.value
+
+
+def qsim_measure_u(h, qubit, u):
+    o, p0 = ctypes.c_int(), ctypes.c_double()
+    _check(_lib.qsim_measure_u(h, qubit, float(u), ctypes.byref(o), ctypes.byref(p0)))
+    return o.value, p0.value
+
+
+def qsim_get_amplitudes(h, idx) -> np.ndarray:
+    idx = np.ascontiguousarray(idx, dtype=np.uint64)
+    out = np.empty(idx.size, dtype=np.complex128)
+    _check(_lib.qsim_get_amplitudes(h, idx.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), idx.size,
+                                    _dptr(out.view(np.float64))))
+    return out
+
+
+def qsim_get_state(h, n) -> np.ndarray:
+    out = np.empty(1 << n, dtype=np.complex128)
+    _check(_lib.qsim_get_state(h, _dptr(out.view(np.float64))))
+    return out
+
+
+def qsim_set_state(h, amps):
+    a = np.ascontiguousarray(amps, dtype=np.complex128)
+    _check(_lib.qsim_set_state(h, _dptr(a.view(np.float64))))
+
+
+def qsim_get_codes(h, n):
+    codes = np.empty(2 << n, dtype=np.int8)
+    r0, r1 = ctypes.c_double(), ctypes.c_double()
+    _check(_lib.qsim_get_codes(h, codes.ctypes.data_as(ctypes.POINTER(ctypes.c_int8)), ctypes.byref(r0),
+                               ctypes.byref(r1)))
+    return codes, r0.value, r1.value
+
+
+def qsim_set_codes(h, codes, r0, r1):
+    c = np.ascontiguousarray(codes, dtype=np.int8)
+    _check(_lib.qsim_set_codes(h, c.ctypes.data_as(ctypes.POINTER(ctypes.c_int8)), float(r0), float(r1)))
+
+
+def qsim_sync(h):
+    _check(_lib.qsim_sync(h))
+
+
+def qsim_stream(h, shard=0) -> int:
+    return _lib.qsim_stream(h, shard) or 0
+
+
+def qsim_get_stats(h) -> dict:
+    st = qsim_stats()
+    _check(_lib.qsim_get_stats(h, ctypes.byref(st)))
+    return {name: getattr(st, name) for name, _ in qsim_stats._fields_}
+
+
+def qsim_reset_stats(h):
+    _check(_lib.qsim_reset_stats(h))
+
+
+def qsim_reset(h):
+    _check(_lib.qsim_reset(h))
+
+
+def qsim_profile(h, enable=True):
+    _check(_lib.qsim_profile(h, 1 if enable else 0))
+
+
+def qsim_profile_read(h) -> dict:
+    """{kernel class name: {"launches", "ms", "bytes"}} since the last read."""
+    arr = (qsim_kernel_profile * 8)()
+    n = ctypes.c_int()
+    _check(_lib.qsim_profile_read(h, arr, 8, ctypes.byref(n)))
+    return {KERNEL_NAMES[arr[i].kind]: dict(launches=arr[i].launches, ms=arr[i].ms, bytes=arr[i].bytes)
+            for i in range(n.value)}
+
+
+def qsim_get_qubit_map(h, n) -> list:
+    pos = (ctypes.c_int * n)()
+    _check(_lib.qsim_get_qubit_map(h, pos))
+    return list(pos)
+
+
+def qsim_plan(n_qubits, nshards, circuit, initial_map=None):
+    """Host-only planner (no GPU): returns (ops as dicts, final qubit map)."""
+    arr, n = pack_gates(circuit)
+    im = None
+    if initial_map is not None:
+        im = (ctypes.c_int * n_qubits)(*initial_map)
+    h = _P()
+    _check(_lib.qsim_plan_create(n_qubits, nshards, im, arr, n, ctypes.byref(h)))
+    try:
+        ops = []
+        op = qsim_plan_op()
+        for i in range(_lib.qsim_plan_num_ops(h)):
+            _check(_lib.qsim_plan_get_op(h, i, ctypes.byref(op)))
+            ops.append(dict(type=op.type, g=op.g, l=op.l, cls=op.cls, controls=list(op.controls)[:op.ncontrols],
+                            gate_index=op.gate_index))
+        pos = (ctypes.c_int * n_qubits)()
+        _check(_lib.qsim_plan_final_map(h, pos))
+        return ops, list(pos)
+    finally:
+        _lib.qsim_plan_destroy(h)
+
+
+class State:
+    """Convenience wrapper: one handle, methods named after the C-ABI calls."""
+
+    def __init__(self, n_qubits, encoding=ENC_FP64, ngpus=1, **ex):
+        self.n = n_qubits
+        self.encoding = encoding
+        if ex:
+            self.h = qsim_create_ex(n_qubits, encoding, ngpus, **ex)
+        else:
+            self.h = qsim_create(n_qubits, encoding, ngpus)
+
+    def close(self):
+        if getattr(self, "h", None):
+            qsim_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def apply_gate(self, u, target, controls=()):
+        qsim_apply_gate(self.h, u, target, controls)
+        return self
+
+    def apply_swap(self, q1, q2):
+        qsim_apply_swap(self.h, q1, q2)
+        return self
+
+    def apply_circuit(self, circuit):
+        qsim_apply_circuit(self.h, circuit)
+        return self
+
+    def norm(self):
+        return qsim_norm(self.h)
+
+    def probabilities(self):
+        return qsim_probabilities(self.h, self.n)
+
+    def expectations(self):
+        return qsim_expectations(self.h, self.n)
+
+    def measure(self, qubit, seed):
+        return qsim_measure(self.h, qubit, seed)
+
+    def measure_u(self, qubit, u):
+        return qsim_measure_u(self.h, qubit, u)
+
+    def get_amplitudes(self, idx):
+        return qsim_get_amplitudes(self.h, idx)
+
+    def get_state(self):
+        return qsim_get_state(self.h, self.n)
+
+    def set_state(self, amps):
+        qsim_set_state(self.h, amps)
+        return self
+
+    def get_codes(self):
+        return qsim_get_codes(self.h, self.n)
+
+    def set_codes(self, codes, r0, r1):
+        qsim_set_codes(self.h, codes, r0, r1)
+        return self
+
+    def sync(self):
+        qsim_sync(self.h)
+
+    def stream(self):
+        return qsim_stream(self.h)
+
+    def stats(self):
+        return qsim_get_stats(self.h)
+
+    def reset_stats(self):
+        qsim_reset_stats(self.h)
+
+    def reset(self):
+        qsim_reset(self.h)
+        return self
+
+    def profile(self, enable=True):
+        qsim_profile(self.h, enable)
+
+    def profile_read(self):
+        return qsim_profile_read(self.h)
+
+    def qubit_map(self):
+        return qsim_get_qubit_map(self.h, self.n)

@@ -1,0 +1,1391 @@
+// api.cu -- the qsim C-ABI: state lifetime, the executor that follows the
+// planner's ops (fused tile passes, sweeps, swap exchanges), reductions and
+// read-out.  See include/qsim.h for the contract of every entry point.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "kernels.h"
+#include "kernels_a.h"
+
+namespace qsim {
+
+static thread_local std::string g_err;
+void set_error(const std::string &msg) { g_err = msg; }
+
+#define CU(call)                                                                            \
+    do {                                                                                    \
+        cudaError_t _e = (call);                                                            \
+        if (_e != cudaSuccess) {                                                            \
+            set_error(std::string(#call) + ": " + cudaGetErrorString(_e));                  \
+            return QSIM_ECUDA;                                                              \
+        }                                                                                   \
+    } while (0)
+#define NC(call)                                                                            \
+    do {                                                                                    \
+        ncclResult_t _r = (call);                                                           \
+        if (_r != ncclSuccess) {                                                            \
+            set_error(std::string(#call) + ": " + ncclGetErrorString(_r));                  \
+            return QSIM_ECOMM;                                                              \
+        }                                                                                   \
+    } while (0)
+#define RC(call)                       \
+    do {                               \
+        int _rc = (call);              \
+        if (_rc != QSIM_OK) return _rc; \
+    } while (0)
+
+static inline uint64_t ins0(uint64_t w, int p) { return ((w >> p) << (p + 1)) | (w & ((1ull << p) - 1ull)); }
+
+struct Shard {
+    int index = 0;            // global shard index (rank bits)
+    void *amps = nullptr;     // 2^nl amplitudes
+};
+
+}  // namespace qsim
+
+using namespace qsim;
+
+struct qsim_state {
+    int n = 0, enc = 0, P = 1, nl = 0, transport = 0, rank = 0, dev = 0, fuse = 1;
+    size_t amp_bytes = 16;
+    uint64_t alloc_amps = 0;  // max(2^nl, 256): small shards are padded with zero amplitudes
+    Planner pl;
+    std::vector<Shard> shards;
+    uint64_t chunk_amps = 0;
+    void *stage[2] = {nullptr, nullptr};
+    cudaStream_t stream = nullptr, comm_stream = nullptr;
+    cudaEvent_t ev_recv[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_start = nullptr;
+    ncclComm_t comm = nullptr;
+    double *d_partials = nullptr, *d_out = nullptr, *h_out = nullptr;  // reduction scratch
+    qsim_stats st{};
+    // A variant
+    double r0 = 0.5, r1 = 0.5;
+    ATables *atab = nullptr;
+    // profiling (qsim_profile): event pairs around each launch
+    struct ProfRec {
+        int kind;
+        double bytes;
+        cudaEvent_t a, b;
+    };
+    bool prof = false;
+    std::vector<ProfRec> prof_recs;
+    std::vector<cudaEvent_t> ev_pool;
+    cudaEvent_t prof_a = nullptr;  // pending start event
+};
+
+namespace qsim {
+
+// ============================================================================
+// helpers
+// ============================================================================
+static cudaEvent_t pool_get(qsim_state *s) {
+    if (!s->ev_pool.empty()) {
+        cudaEvent_t e = s->ev_pool.back();
+        s->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+// Bracket one launch: prof_begin before, prof_end(kind, bytes) after.
+static void prof_begin(qsim_state *s) {
+    if (!s->prof) return;
+    s->prof_a = pool_get(s);
+    cudaEventRecord(s->prof_a, s->stream);
+}
+static void prof_end(qsim_state *s, int kind, double bytes) {
+    if (!s->prof || !s->prof_a) return;
+    cudaEvent_t b = pool_get(s);
+    cudaEventRecord(b, s->stream);
+    s->prof_recs.push_back({kind, bytes, s->prof_a, b});
+    s->prof_a = nullptr;
+}
+static uint64_t shard_base(const qsim_state *s, const Shard &sh) { return (uint64_t)sh.index << s->nl; }
+
+static int rank_bit(const Shard &sh, int phys_bit, int nl) { return (sh.index >> (phys_bit - nl)) & 1; }
+
+// Whether all controls that sit on global bits are 1 for this shard.
+static bool global_ctrls_ok(const qsim_state *s, const Shard &sh, const PlanOp &o) {
+    for (int c = 0; c < o.nctrl; ++c)
+        if (o.ctrl[c] >= s->nl && !rank_bit(sh, o.ctrl[c], s->nl)) return false;
+    return true;
+}
+
+static uint64_t full_cmask(const PlanOp &o) {
+    uint64_t m = 0;
+    for (int c = 0; c < o.nctrl; ++c) m |= 1ull << o.ctrl[c];
+    return m;
+}
+
+// Algorithmic bytes of one gate on one shard had it run alone.
+static double gate_bytes_alone(const qsim_state *s, const Shard &sh, const PlanOp &o, const double *u) {
+    if (!global_ctrls_ok(s, sh, o)) return 0.0;
+    int nlc = 0;
+    for (int c = 0; c < o.nctrl; ++c)
+        if (o.ctrl[c] < s->nl) ++nlc;
+    double amps = std::ldexp(1.0, s->nl - nlc);
+    double per = 2.0 * (double)s->amp_bytes;  // read + write
+    if (o.cls == CLS_DIAG) {
+        if (o.l >= s->nl) {
+            int bit = rank_bit(sh, o.l, s->nl);
+            double fr = bit ? u[6] : u[0], fi = bit ? u[7] : u[1];
+            return (fr == 1.0 && fi == 0.0) ? 0.0 : amps * per;
+        }
+        bool one0 = u[0] == 1.0 && u[1] == 0.0, one1 = u[6] == 1.0 && u[7] == 0.0;
+        if (one0 || one1) return amps * 0.5 * per;
+    }
+    return amps * per;
+}
+
+// ============================================================================
+// E single-gate sweep on every shard
+// ============================================================================
+static int sweep_gate_e(qsim_state *s, const PlanOp &o, const double *u) {
+    for (auto &sh : s->shards) {
+        if (!global_ctrls_ok(s, sh, o)) continue;
+        int locs[3], nloc = 0;
+        uint64_t cm = 0;
+        for (int c = 0; c < o.nctrl; ++c)
+            if (o.ctrl[c] < s->nl) {
+                locs[nloc++] = o.ctrl[c];
+                cm |= 1ull << o.ctrl[c];
+            }
+        if (o.l >= s->nl) {  // diagonal gate on a global bit: uniform factor on the shard
+            int bit = rank_bit(sh, o.l, s->nl);
+            ScaleParams p{};
+            p.a = sh.amps;
+            p.f[0] = bit ? u[6] : u[0];
+            p.f[1] = bit ? u[7] : u[1];
+            if (p.f[0] == 1.0 && p.f[1] == 0.0) continue;
+            std::sort(locs, locs + nloc);
+            for (int k = 0; k < nloc; ++k) p.ins[k] = locs[k];
+            p.nins = nloc;
+            p.cmask = cm;
+            p.nitems = 1ull << (s->nl - nloc);
+            prof_begin(s);
+            launch_scale_e(p, s->stream);
+            prof_end(s, QSIM_K_SWEEP, gate_bytes_alone(s, sh, o, u));
+        } else {
+            SweepParams p{};
+            p.a = sh.amps;
+            locs[nloc++] = o.l;
+            std::sort(locs, locs + nloc);
+            for (int k = 0; k < nloc; ++k) p.ins[k] = locs[k];
+            p.nins = nloc;
+            p.cmask = cm;
+            p.t = o.l;
+            p.cls = o.cls;
+            p.nitems = 1ull << (s->nl - nloc);
+            std::memcpy(p.u, u, sizeof(p.u));
+            bool one0 = u[0] == 1.0 && u[1] == 0.0, one1 = u[6] == 1.0 && u[7] == 0.0;
+            p.touch = (o.cls == CLS_DIAG) ? (one0 ? 2 : (one1 ? 1 : 3)) : 3;
+            prof_begin(s);
+            launch_sweep_e(p, s->stream);
+            prof_end(s, QSIM_K_SWEEP, gate_bytes_alone(s, sh, o, u));
+        }
+        s->st.kernels++;
+        s->st.sweeps++;
+        s->st.hbm_bytes += gate_bytes_alone(s, sh, o, u);
+    }
+    CU(cudaGetLastError());
+    return QSIM_OK;
+}
+
+// ============================================================================
+// fused tile passes (a6)
+// ============================================================================
+struct PassBuild {
+    std::vector<int> ops;      // indices into the run
+    std::vector<int> high;     // local qubits >= PASS_LOW needed in the tile
+    std::vector<std::vector<int>> stage_q;     // per stage: register qubits (local qubit ids)
+    std::vector<std::vector<int>> stage_ops;   // per stage: op indices
+};
+
+static bool pass_add(PassBuild &pb, const PlanOp &o, int idx, int hmax) {
+    bool needs_reg = o.cls != CLS_DIAG;
+    std::vector<int> high = pb.high;
+    if (needs_reg && o.l >= PASS_LOW && std::find(high.begin(), high.end(), o.l) == high.end()) {
+        if ((int)high.size() >= hmax) return false;
+        high.push_back(o.l);
+    }
+    if ((int)pb.ops.size() >= PASS_MAX_GATES) return false;
+    // stage placement
+    if (pb.stage_q.empty()) {
+        pb.stage_q.emplace_back();
+        pb.stage_ops.emplace_back();
+    }
+    if (needs_reg) {
+        auto &R = pb.stage_q.back();
+        if (std::find(R.begin(), R.end(), o.l) == R.end()) {
+            if ((int)R.size() >= PASS_R) {
+                if ((int)pb.stage_q.size() >= PASS_MAX_STAGES) return false;
+                pb.stage_q.emplace_back();
+                pb.stage_ops.emplace_back();
+            }
+            pb.stage_q.back().push_back(o.l);
+        }
+    }
+    pb.stage_ops.back().push_back(idx);
+    pb.ops.push_back(idx);
+    pb.high = high;
+    return true;
+}
+
+static int launch_pass(qsim_state *s, const PassBuild &pb, const std::vector<PlanOp> &run,
+                       const std::vector<const double *> &us) {
+    const int K = std::min(PASS_MAX_K, s->nl);
+    const int h = K - PASS_LOW;
+    std::vector<int> high = pb.high;
+    for (int q = PASS_LOW; (int)high.size() < h && q < s->nl; ++q)
+        if (std::find(high.begin(), high.end(), q) == high.end()) high.push_back(q);
+    std::sort(high.begin(), high.end());
+    auto tile_bit = [&](int q) -> int {
+        if (q < PASS_LOW) return q;
+        for (int i = 0; i < h; ++i)
+            if (high[i] == q) return PASS_LOW + i;
+        return -1;
+    };
+    static PassParams p;  // large: keep off the stack
+    std::memset(&p, 0, sizeof(p));
+    p.nl = s->nl;
+    p.K = K;
+    p.ntiles = 1ull << (s->nl - K);
+    for (int i = 0; i < h; ++i) p.high_q[i] = high[i];
+    p.nstages = (int)pb.stage_q.size();
+    int gi = 0;
+    for (int si = 0; si < p.nstages; ++si) {
+        PassStage &st = p.st[si];
+        std::vector<int> R;
+        for (int q : pb.stage_q[si]) R.push_back(tile_bit(q));
+        for (int b = 0; (int)R.size() < PASS_R; ++b)
+            if (std::find(R.begin(), R.end(), b) == R.end()) R.push_back(b);
+        for (int r = 0; r < PASS_R; ++r) st.rbits[r] = (int8_t)R[r];
+        // group bits: three with distinct residues mod 3 first (bank-conflict-free
+        // quarter warps under the XOR-fold swizzle), then the rest ascending.
+        std::vector<int> rest;
+        for (int b = 0; b < K; ++b)
+            if (std::find(R.begin(), R.end(), b) == R.end()) rest.push_back(b);
+        std::vector<int> gb;
+        for (int res = 0; res < 3; ++res)
+            for (size_t k = 0; k < rest.size(); ++k)
+                if (rest[k] % 3 == res) {
+                    gb.push_back(rest[k]);
+                    rest.erase(rest.begin() + k);
+                    break;
+                }
+        std::sort(gb.begin(), gb.end());
+        for (int b : rest) gb.push_back(b);
+        for (int i = 0; i < K - PASS_R; ++i) st.gbits[i] = (int8_t)gb[i];
+        st.first_gate = (int8_t)gi;
+        st.ngates = (int8_t)pb.stage_ops[si].size();
+        for (int oi : pb.stage_ops[si]) {
+            const PlanOp &o = run[oi];
+            PassGate &g = p.g[gi++];
+            std::memcpy(g.u, us[oi], sizeof(g.u));
+            int8_t cslot = 0;
+            uint64_t cout = 0;
+            for (int c = 0; c < o.nctrl; ++c) {
+                int tb = (o.ctrl[c] < s->nl) ? tile_bit(o.ctrl[c]) : -1;
+                int slot = -1;
+                for (int r = 0; r < PASS_R; ++r)
+                    if (tb >= 0 && R[r] == tb) slot = r;
+                if (slot >= 0)
+                    cslot |= (int8_t)(1 << slot);
+                else
+                    cout |= 1ull << o.ctrl[c];
+            }
+            g.cslot = cslot;
+            g.cmask_out = cout;
+            int ttb = (o.l < s->nl) ? tile_bit(o.l) : -1;
+            int tslot = -1;
+            for (int r = 0; r < PASS_R; ++r)
+                if (ttb >= 0 && R[r] == ttb) tslot = r;
+            if (o.cls == CLS_DIAG) {
+                if (tslot >= 0) {
+                    g.kind = PG_DIAG_IN;
+                    g.slot = (int8_t)tslot;
+                } else {
+                    g.kind = PG_DIAG_OUT;
+                    g.tmask_out = 1ull << o.l;
+                }
+            } else {
+                if (tslot < 0) {
+                    set_error("internal: pass target not in register set");
+                    return QSIM_EINVAL;
+                }
+                g.kind = (o.cls == CLS_ANTI) ? PG_ANTI : PG_DENSE;
+                g.slot = (int8_t)tslot;
+            }
+        }
+    }
+    int grid = (int)std::min<uint64_t>(p.ntiles, (uint64_t)pass_e_max_grid());
+    for (auto &sh : s->shards) {
+        p.a = sh.amps;
+        p.shard_base = shard_base(s, sh);
+        prof_begin(s);
+        launch_pass_e(p, grid, s->stream);
+        prof_end(s, QSIM_K_PASS, std::ldexp(2.0 * (double)s->amp_bytes, s->nl));
+        s->st.kernels++;
+        s->st.passes++;
+        s->st.fused_gates += (int64_t)pb.ops.size();
+        s->st.hbm_bytes += std::ldexp(2.0 * (double)s->amp_bytes, s->nl);
+    }
+    CU(cudaGetLastError());
+    return QSIM_OK;
+}
+
+static int run_gates_e(qsim_state *s, const std::vector<PlanOp> &run, const std::vector<const double *> &us) {
+    size_t i = 0;
+    const int K = std::min(PASS_MAX_K, s->nl);
+    const bool can_fuse = s->fuse && K >= PASS_MIN_K;
+    while (i < run.size()) {
+        if (!can_fuse) {
+            RC(sweep_gate_e(s, run[i], us[i]));
+            ++i;
+            continue;
+        }
+        PassBuild pb;
+        size_t j = i;
+        while (j < run.size() && pass_add(pb, run[j], (int)j, K - PASS_LOW)) ++j;
+        // cost model: one pass (32 B/amp) vs the sweeps' own bytes on shard 0
+        double sweep_bytes = 0.0;
+        for (size_t k = i; k < j; ++k) sweep_bytes += gate_bytes_alone(s, s->shards[0], run[k], us[k]);
+        double pass_bytes = std::ldexp(2.0 * (double)s->amp_bytes, s->nl);
+        if (j - i >= 2 && pass_bytes < sweep_bytes) {
+            // rebase op indices to the run (pass_add stored absolute indices)
+            RC(launch_pass(s, pb, run, us));
+        } else {
+            for (size_t k = i; k < j; ++k) RC(sweep_gate_e(s, run[k], us[k]));
+        }
+        i = j;
+    }
+    return QSIM_OK;
+}
+
+// ============================================================================
+// exchange (a7): swap physical global bit g with local bit l; optionally apply
+// the triggering gate (now on bit l) to each (kept, received) pair on arrival.
+// ============================================================================
+static int exchange(qsim_state *s, const PlanOp &x, const PlanOp *gop, const double *u) {
+    const int j = x.g - s->nl;
+    const int l = x.l;
+    const uint64_t half = 1ull << (s->nl - 1);
+    uint64_t C = std::min<uint64_t>(s->chunk_amps, half);
+    C = std::min<uint64_t>(C, 1ull << l);
+    const uint64_t nchunks = half / C;
+    const size_t ab = s->amp_bytes;
+    auto fill = [&](XchgParams &p, const Shard &sh, int b, uint64_t c, const void *stg) {
+        p.own = sh.amps;
+        p.stage = stg;
+        p.p0 = c * C;
+        p.n = C;
+        p.l = l;
+        p.b = b;
+        p.shard_base = shard_base(s, sh);
+        if (gop) {
+            p.mode = 1;
+            p.cls = gop->cls;
+            p.cmask = full_cmask(*gop);
+            std::memcpy(p.u, u, sizeof(p.u));
+        } else {
+            p.mode = 0;
+        }
+    };
+    auto account = [&]() {
+        s->st.kernels++;
+        s->st.hbm_bytes += (double)C * ab * (gop ? 4.0 : 2.0);
+    };
+    if (s->transport == QSIM_TRANSPORT_LOCAL) {
+        for (auto &sa : s->shards) {
+            if ((sa.index >> j) & 1) continue;
+            Shard *sb = nullptr;
+            for (auto &t : s->shards)
+                if (t.index == (sa.index | (1 << j))) sb = &t;
+            for (uint64_t c = 0; c < nchunks; ++c) {
+                // sa (b=0) sends slot(l=1), sb (b=1) sends slot(l=0)
+                const char *src_a = (const char *)sa.amps + ins0(c * C, l) * ab + ((size_t)1 << l) * ab;
+                const char *src_b = (const char *)sb->amps + ins0(c * C, l) * ab;
+                CU(cudaMemcpyAsync(s->stage[0], src_b, C * ab, cudaMemcpyDeviceToDevice, s->stream));
+                CU(cudaMemcpyAsync(s->stage[1], src_a, C * ab, cudaMemcpyDeviceToDevice, s->stream));
+                XchgParams pa{}, pb{};
+                fill(pa, sa, 0, c, s->stage[0]);
+                fill(pb, *sb, 1, c, s->stage[1]);
+                prof_begin(s);
+                if (s->enc == QSIM_ENC_FP64) {
+                    launch_xchg_e(pa, s->stream);
+                    launch_xchg_e(pb, s->stream);
+                } else {
+                    launch_xchg_a(pa, s->atab, s->stream);
+                    launch_xchg_a(pb, s->atab, s->stream);
+                }
+                prof_end(s, QSIM_K_XCHG, 2.0 * (double)C * ab * (gop ? 4.0 : 2.0));
+                account();
+                account();
+            }
+            s->st.exchange_bytes += 2.0 * (double)half * ab;
+            s->st.exchanges++;
+        }
+        CU(cudaGetLastError());
+        return QSIM_OK;
+    }
+    // ---- NCCL: one shard per process, double-buffered chunk pipeline ----
+    Shard &sh = s->shards[0];
+    const int b = (sh.index >> j) & 1;
+    const int partner = sh.index ^ (1 << j);
+    CU(cudaEventRecord(s->ev_start, s->stream));
+    CU(cudaStreamWaitEvent(s->comm_stream, s->ev_start, 0));
+    for (uint64_t c = 0; c < nchunks; ++c) {
+        const int k = (int)(c & 1);
+        if (c >= 2) CU(cudaStreamWaitEvent(s->comm_stream, s->ev_comp[k], 0));
+        const char *src = (const char *)sh.amps + ins0(c * C, l) * ab + (b ? 0 : ((size_t)1 << l) * ab);
+        NC(ncclGroupStart());
+        NC(ncclSend(src, C * ab, ncclUint8, partner, s->comm, s->comm_stream));
+        NC(ncclRecv(s->stage[k], C * ab, ncclUint8, partner, s->comm, s->comm_stream));
+        NC(ncclGroupEnd());
+        CU(cudaEventRecord(s->ev_recv[k], s->comm_stream));
+        CU(cudaStreamWaitEvent(s->stream, s->ev_recv[k], 0));
+        XchgParams p{};
+        fill(p, sh, b, c, s->stage[k]);
+        prof_begin(s);
+        if (s->enc == QSIM_ENC_FP64)
+            launch_xchg_e(p, s->stream);
+        else
+            launch_xchg_a(p, s->atab, s->stream);
+        prof_end(s, QSIM_K_XCHG, (double)C * ab * (gop ? 4.0 : 2.0));
+        account();
+        CU(cudaEventRecord(s->ev_comp[k], s->stream));
+    }
+    s->st.exchange_bytes += (double)half * ab;
+    s->st.exchanges++;
+    CU(cudaGetLastError());
+    return QSIM_OK;
+}
+
+// ============================================================================
+// executor
+// ============================================================================
+static int run_gates_a(qsim_state *s, const std::vector<PlanOp> &run, const std::vector<const double *> &us);
+
+static int execute(qsim_state *s, const qsim_gate *gates, size_t ngates, const std::vector<PlanOp> &ops) {
+    std::vector<PlanOp> run;
+    std::vector<const double *> us;
+    auto flush = [&]() -> int {
+        if (run.empty()) return QSIM_OK;
+        int rc = (s->enc == QSIM_ENC_FP64) ? run_gates_e(s, run, us) : run_gates_a(s, run, us);
+        run.clear();
+        us.clear();
+        return rc;
+    };
+    for (size_t i = 0; i < ops.size(); ++i) {
+        const PlanOp &o = ops[i];
+        if (o.type == QSIM_OP_EXCHANGE) {
+            RC(flush());
+            const PlanOp *g = nullptr;
+            if (i + 1 < ops.size() && ops[i + 1].type == QSIM_OP_GATE && ops[i + 1].gate_index == o.gate_index &&
+                ops[i + 1].l == o.l) {
+                g = &ops[i + 1];
+                ++i;
+            }
+            if (g && s->enc == QSIM_ENC_ADAPTIVE2 && g->cls == CLS_DENSE) {
+                // A dense gates need exact global bounds first: exchange, then the 2-phase gate
+                RC(exchange(s, o, nullptr, nullptr));
+                run.push_back(*g);
+                us.push_back(gates[g->gate_index].u);
+                RC(flush());
+                continue;
+            }
+            RC(exchange(s, o, g, g ? gates[g->gate_index].u : nullptr));
+            continue;
+        }
+        run.push_back(o);
+        us.push_back(gates[o.gate_index].u);
+    }
+    RC(flush());
+    s->st.gates += (int64_t)ngates;
+    for (size_t g = 0; g < ngates; ++g) {
+        if (gates[g].kind == QSIM_GATE_SWAP) continue;
+        // per-gate algorithmic bytes (for the "effective" GB/s figure) on shard 0's view
+        PlanOp o{};
+        o.cls = classify(gates[g].u);
+        if (o.cls == CLS_IDENT) continue;
+        o.l = 0;
+        o.nctrl = gates[g].ncontrols;
+        o.ctrl[0] = o.ctrl[1] = 1;  // local placeholder: controls count, position irrelevant
+        double amps = std::ldexp(1.0, s->nl - o.nctrl);
+        double per = 2.0 * (double)s->amp_bytes;
+        double bytes = amps * per;
+        if (o.cls == CLS_DIAG) {
+            const double *u = gates[g].u;
+            bool one0 = u[0] == 1.0 && u[1] == 0.0, one1 = u[6] == 1.0 && u[7] == 0.0;
+            if (one0 || one1) bytes *= 0.5;
+        }
+        s->st.gate_bytes += bytes * (double)s->shards.size();
+    }
+    return QSIM_OK;
+}
+
+// ============================================================================
+// reductions
+// ============================================================================
+// phys[0] = norm^2, phys[1 + b] = sum_{physical bit b = 1} |a|^2 for every physical bit b < n
+static int phys_probs(qsim_state *s, std::vector<double> &phys) {
+    phys.assign(1 + s->n, 0.0);
+    for (auto &sh : s->shards) {
+        if (s->enc == QSIM_ENC_FP64)
+            launch_probs_e(sh.amps, s->nl, s->d_partials, s->d_out, s->stream);
+        else
+            launch_probs_a(sh.amps, s->nl, s->atab, s->d_partials, s->d_out, s->stream);
+        s->st.kernels += 2;
+        CU(cudaMemcpyAsync(s->h_out, s->d_out, RED_SLOTS * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+        CU(cudaStreamSynchronize(s->stream));
+        phys[0] += s->h_out[0];
+        for (int b = 0; b < s->nl; ++b) phys[1 + b] += s->h_out[1 + b];
+        for (int b = s->nl; b < s->n; ++b)
+            if (rank_bit(sh, b, s->nl)) phys[1 + b] += s->h_out[0];
+    }
+    if (s->transport == QSIM_TRANSPORT_NCCL && s->P > 1) {
+        CU(cudaMemcpyAsync(s->d_out, phys.data(), phys.size() * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+        NC(ncclAllReduce(s->d_out, s->d_out, phys.size(), ncclFloat64, ncclSum, s->comm, s->stream));
+        CU(cudaMemcpyAsync(phys.data(), s->d_out, phys.size() * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+        CU(cudaStreamSynchronize(s->stream));
+    }
+    return QSIM_OK;
+}
+
+}  // namespace qsim
+
+// ============================================================================
+// C-ABI
+// ============================================================================
+extern "C" {
+
+const char *qsim_last_error(void) { return g_err.c_str(); }
+
+int qsim_nccl_unique_id(uint8_t out[128]) {
+    if (!out) return QSIM_EINVAL;
+    ncclUniqueId id;
+    NC(ncclGetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "ncclUniqueId size");
+    std::memcpy(out, &id, 128);
+    return QSIM_OK;
+}
+
+int qsim_destroy(qsim_state *s) {
+    if (!s) return QSIM_OK;
+    if (s->dev >= 0) cudaSetDevice(s->dev);
+    if (s->stream) cudaStreamSynchronize(s->stream);
+    if (s->comm_stream) cudaStreamSynchronize(s->comm_stream);
+    if (s->comm) ncclCommDestroy(s->comm);
+    for (auto &sh : s->shards)
+        if (sh.amps) cudaFree(sh.amps);
+    for (int k = 0; k < 2; ++k) {
+        if (s->stage[k]) cudaFree(s->stage[k]);
+        if (s->ev_recv[k]) cudaEventDestroy(s->ev_recv[k]);
+        if (s->ev_comp[k]) cudaEventDestroy(s->ev_comp[k]);
+    }
+    if (s->ev_start) cudaEventDestroy(s->ev_start);
+    for (auto &r : s->prof_recs) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (auto e : s->ev_pool) cudaEventDestroy(e);
+    if (s->d_partials) cudaFree(s->d_partials);
+    if (s->d_out) cudaFree(s->d_out);
+    if (s->h_out) cudaFreeHost(s->h_out);
+    if (s->atab) atables_free(s->atab);
+    if (s->stream) cudaStreamDestroy(s->stream);
+    if (s->comm_stream) cudaStreamDestroy(s->comm_stream);
+    delete s;
+    return QSIM_OK;
+}
+
+static int init_state(qsim_state *s) {
+    // |0...0>: a(0) = 1 on shard 0 (E); codes (127, 0) at 0, (-128, 0) elsewhere (A)
+    for (auto &sh : s->shards) {
+        size_t bytes = s->alloc_amps * s->amp_bytes;
+        if (s->enc == QSIM_ENC_FP64) {
+            CU(cudaMemsetAsync(sh.amps, 0, bytes, s->stream));
+            if (sh.index == 0) {
+                static const double one[2] = {1.0, 0.0};
+                CU(cudaMemcpyAsync(sh.amps, one, sizeof(one), cudaMemcpyHostToDevice, s->stream));
+            }
+        } else {
+            launch_init_a(sh.amps, s->alloc_amps, sh.index == 0, s->stream);
+            s->st.kernels++;
+        }
+    }
+    s->r0 = s->r1 = 0.5;
+    if (s->enc == QSIM_ENC_ADAPTIVE2) RC(atables_set(s->atab, s->r0, s->r1, s->stream));
+    CU(cudaStreamSynchronize(s->stream));
+    return QSIM_OK;
+}
+
+int qsim_create_ex(const qsim_config *cfg, qsim_state **out) {
+    if (!cfg || !out) {
+        set_error("qsim_create_ex: null argument");
+        return QSIM_EINVAL;
+    }
+    *out = nullptr;
+    const int n = cfg->n_qubits, P = cfg->nshards;
+    if (n < 2 || n > 63) {
+        set_error("n_qubits must be in [2, 63] (PAPER.md:1418-1419)");
+        return QSIM_EINVAL;
+    }
+    if (P < 1 || (P & (P - 1))) {
+        set_error("nshards must be a power of two");
+        return QSIM_EINVAL;
+    }
+    if (cfg->encoding != QSIM_ENC_FP64 && cfg->encoding != QSIM_ENC_ADAPTIVE2) {
+        set_error("unknown encoding");
+        return QSIM_EINVAL;
+    }
+    int k = 0;
+    while ((1 << k) < P) ++k;
+    const int nl = n - k;
+    if (P > 1 && nl < 10) {
+        set_error("a sharded state needs at least 10 local qubits (N - log2(P) >= 10)");
+        return QSIM_EINVAL;
+    }
+    const int transport = (P == 1) ? QSIM_TRANSPORT_LOCAL : cfg->transport;
+    if (transport != QSIM_TRANSPORT_LOCAL && transport != QSIM_TRANSPORT_NCCL) {
+        set_error("unknown transport");
+        return QSIM_EINVAL;
+    }
+    if (transport == QSIM_TRANSPORT_NCCL && (cfg->rank < 0 || cfg->rank >= P || !cfg->nccl_id)) {
+        set_error("NCCL transport needs 0 <= rank < nshards and a 128-byte nccl_id");
+        return QSIM_EINVAL;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        set_error("no CUDA device available (the library has no CPU fallback)");
+        return QSIM_ECUDA;
+    }
+    auto *s = new qsim_state();
+    s->n = n;
+    s->enc = cfg->encoding;
+    s->P = P;
+    s->nl = nl;
+    s->transport = transport;
+    s->rank = transport == QSIM_TRANSPORT_NCCL ? cfg->rank : 0;
+    s->fuse = cfg->fuse;
+    s->amp_bytes = s->enc == QSIM_ENC_FP64 ? 16 : 2;
+    if (cfg->device >= 0) {
+        if (cudaSetDevice(cfg->device) != cudaSuccess) {
+            delete s;
+            set_error("cudaSetDevice failed");
+            return QSIM_ECUDA;
+        }
+    }
+    cudaGetDevice(&s->dev);
+    s->pl.init(n, P, nullptr);
+    int rc = QSIM_OK;
+    auto fail = [&](int code) {
+        qsim_destroy(s);
+        return code;
+    };
+    if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        set_error("cudaStreamCreate failed");
+        return fail(QSIM_ECUDA);
+    }
+    // shards owned by this process
+    if (transport == QSIM_TRANSPORT_NCCL) {
+        s->shards.resize(1);
+        s->shards[0].index = cfg->rank;
+    } else {
+        s->shards.resize(P);
+        for (int r = 0; r < P; ++r) s->shards[r].index = r;
+    }
+    s->alloc_amps = std::max<uint64_t>(1ull << nl, 256);
+    const size_t shard_bytes = s->alloc_amps * s->amp_bytes;
+    for (auto &sh : s->shards) {
+        if (cudaMalloc(&sh.amps, shard_bytes) != cudaSuccess) {
+            cudaGetLastError();
+            set_error("cudaMalloc of " + std::to_string(shard_bytes) + " B per shard (" +
+                      std::to_string(s->shards.size()) + " shard(s) on this device; state needs 2^" +
+                      std::to_string(n) + " x " + std::to_string(s->amp_bytes) + " B in total) failed");
+            return fail(QSIM_ENOMEM);
+        }
+    }
+    if (P > 1) {
+        // communication buffers of 2^{N-3} bytes in total by default
+        int64_t cb = cfg->chunk_bytes;
+        if (cb <= 0) {
+            double tot = std::ldexp(1.0, n - 3) / P / 2.0;
+            cb = (int64_t)std::min(tot, 512.0 * 1024 * 1024);
+        }
+        uint64_t ca = (uint64_t)cb / s->amp_bytes;
+        uint64_t p2 = 1;
+        while (p2 * 2 <= ca) p2 *= 2;
+        s->chunk_amps = std::max<uint64_t>(p2, 256);
+        s->chunk_amps = std::min<uint64_t>(s->chunk_amps, 1ull << (nl - 1));
+        for (int k2 = 0; k2 < 2; ++k2) {
+            if (cudaMalloc(&s->stage[k2], s->chunk_amps * s->amp_bytes) != cudaSuccess) {
+                cudaGetLastError();
+                set_error("cudaMalloc of the exchange staging buffers failed");
+                return fail(QSIM_ENOMEM);
+            }
+        }
+    }
+    if (cudaMalloc(&s->d_partials, (size_t)red_blocks() * RED_SLOTS * sizeof(double) * 2) != cudaSuccess ||
+        cudaMalloc(&s->d_out, 4096 * sizeof(double)) != cudaSuccess ||
+        cudaMallocHost(&s->h_out, 4096 * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("reduction scratch allocation failed");
+        return fail(QSIM_ENOMEM);
+    }
+    if (s->enc == QSIM_ENC_ADAPTIVE2) {
+        rc = atables_alloc(&s->atab);
+        if (rc) return fail(rc);
+    }
+    if (transport == QSIM_TRANSPORT_NCCL) {
+        if (cudaStreamCreateWithFlags(&s->comm_stream, cudaStreamNonBlocking) != cudaSuccess) return fail(QSIM_ECUDA);
+        for (int k2 = 0; k2 < 2; ++k2) {
+            cudaEventCreateWithFlags(&s->ev_recv[k2], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&s->ev_comp[k2], cudaEventDisableTiming);
+        }
+        cudaEventCreateWithFlags(&s->ev_start, cudaEventDisableTiming);
+        ncclUniqueId id;
+        std::memcpy(&id, cfg->nccl_id, sizeof(id));
+        ncclResult_t r = ncclCommInitRank(&s->comm, P, id, cfg->rank);
+        if (r != ncclSuccess) {
+            set_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+            s->comm = nullptr;
+            return fail(QSIM_ECOMM);
+        }
+    }
+    rc = init_state(s);
+    if (rc) return fail(rc);
+    *out = s;
+    return QSIM_OK;
+}
+
+int qsim_create(int n_qubits, int encoding, int ngpus, qsim_state **out) {
+    qsim_config c{};
+    c.n_qubits = n_qubits;
+    c.encoding = encoding;
+    c.nshards = ngpus;
+    c.transport = QSIM_TRANSPORT_LOCAL;
+    c.device = -1;
+    c.fuse = 1;
+    return qsim_create_ex(&c, out);
+}
+
+int qsim_apply_circuit(qsim_state *s, const qsim_gate *gates, size_t ngates) {
+    if (!s || (!gates && ngates)) {
+        set_error("null argument");
+        return QSIM_EINVAL;
+    }
+    RC(validate_gates(s->n, gates, ngates, true));
+    cudaSetDevice(s->dev);
+    std::vector<PlanOp> ops;
+    s->pl.plan(gates, ngates, ops, true);
+    return execute(s, gates, ngates, ops);
+}
+
+int qsim_apply_gate(qsim_state *s, const double u[8], int target, const int *controls, int ncontrols) {
+    if (!s || !u || (ncontrols > 0 && !controls) || ncontrols < 0 || ncontrols > 2) {
+        set_error("qsim_apply_gate: bad arguments (ncontrols must be 0..2)");
+        return QSIM_EINVAL;
+    }
+    qsim_gate g{};
+    g.kind = QSIM_GATE_U;
+    g.target = target;
+    g.ncontrols = ncontrols;
+    for (int c = 0; c < ncontrols; ++c) g.controls[c] = controls[c];
+    std::memcpy(g.u, u, sizeof(g.u));
+    return qsim_apply_circuit(s, &g, 1);
+}
+
+int qsim_apply_swap(qsim_state *s, int q1, int q2) {
+    if (!s) return QSIM_EINVAL;
+    qsim_gate g{};
+    g.kind = QSIM_GATE_SWAP;
+    g.target = q1;
+    g.target2 = q2;
+    return qsim_apply_circuit(s, &g, 1);
+}
+
+int qsim_reset(qsim_state *s) {
+    if (!s) return QSIM_EINVAL;
+    cudaSetDevice(s->dev);
+    if (s->comm_stream) CU(cudaStreamSynchronize(s->comm_stream));
+    s->pl.init(s->n, s->P, nullptr);
+    return init_state(s);
+}
+
+int qsim_profile(qsim_state *s, int enable) {
+    if (!s) return QSIM_EINVAL;
+    s->prof = enable != 0;
+    return QSIM_OK;
+}
+
+int qsim_profile_read(qsim_state *s, qsim_kernel_profile *out, int max, int *nout) {
+    if (!s || (!out && max > 0)) return QSIM_EINVAL;
+    CU(cudaStreamSynchronize(s->stream));
+    qsim_kernel_profile agg[QSIM_K_NUM];
+    std::memset(agg, 0, sizeof(agg));
+    for (auto &r : s->prof_recs) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        agg[r.kind].kind = r.kind;
+        agg[r.kind].launches++;
+        agg[r.kind].ms += ms;
+        agg[r.kind].bytes += r.bytes;
+        s->ev_pool.push_back(r.a);
+        s->ev_pool.push_back(r.b);
+    }
+    s->prof_recs.clear();
+    int k = 0;
+    for (int c = 0; c < QSIM_K_NUM && k < max; ++c)
+        if (agg[c].launches) out[k++] = agg[c];
+    if (nout) *nout = k;
+    return QSIM_OK;
+}
+
+int qsim_sync(qsim_state *s) {
+    if (!s) return QSIM_EINVAL;
+    CU(cudaStreamSynchronize(s->stream));
+    if (s->comm_stream) CU(cudaStreamSynchronize(s->comm_stream));
+    return QSIM_OK;
+}
+
+void *qsim_stream(qsim_state *s, int shard) {
+    (void)shard;
+    return s ? (void *)s->stream : nullptr;
+}
+
+int qsim_get_stats(qsim_state *s, qsim_stats *out) {
+    if (!s || !out) return QSIM_EINVAL;
+    *out = s->st;
+    return QSIM_OK;
+}
+int qsim_reset_stats(qsim_state *s) {
+    if (!s) return QSIM_EINVAL;
+    s->st = qsim_stats{};
+    return QSIM_OK;
+}
+
+int qsim_get_qubit_map(qsim_state *s, int *pos) {
+    if (!s || !pos) return QSIM_EINVAL;
+    for (int q = 0; q < s->n; ++q) pos[q] = s->pl.pos[q];
+    return QSIM_OK;
+}
+
+int qsim_norm(qsim_state *s, double *norm2) {
+    if (!s || !norm2) return QSIM_EINVAL;
+    cudaSetDevice(s->dev);
+    std::vector<double> phys;
+    RC(phys_probs(s, phys));
+    *norm2 = phys[0];
+    return QSIM_OK;
+}
+
+int qsim_probabilities(qsim_state *s, double *p1) {
+    if (!s || !p1) return QSIM_EINVAL;
+    cudaSetDevice(s->dev);
+    std::vector<double> phys;
+    RC(phys_probs(s, phys));
+    for (int q = 0; q < s->n; ++q) p1[q] = phys[1 + s->pl.pos[q]];
+    return QSIM_OK;
+}
+
+static int pair_sums_local(qsim_state *s, int b, double &sr, double &si) {
+    sr = si = 0.0;
+    for (auto &sh : s->shards) {
+        if (s->enc == QSIM_ENC_FP64)
+            launch_pairdot_e(sh.amps, s->nl, b, s->d_partials, s->d_out, s->stream);
+        else
+            launch_pairdot_a(sh.amps, s->nl, b, s->atab, s->d_partials, s->d_out, s->stream);
+        s->st.kernels += 2;
+        CU(cudaMemcpyAsync(s->h_out, s->d_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+        CU(cudaStreamSynchronize(s->stream));
+        sr += s->h_out[0];
+        si += s->h_out[1];
+    }
+    return QSIM_OK;
+}
+
+int qsim_expectations(qsim_state *s, double *q) {
+    if (!s || !q) return QSIM_EINVAL;
+    cudaSetDevice(s->dev);
+    std::vector<double> phys;
+    RC(phys_probs(s, phys));
+    std::vector<double> Sr(s->n, 0.0), Si(s->n, 0.0);
+    std::vector<int> done(s->n, 0);
+    // local qubits first
+    for (int lq = 0; lq < s->n; ++lq) {
+        int b = s->pl.pos[lq];
+        if (b >= s->nl) continue;
+        RC(pair_sums_local(s, b, Sr[lq], Si[lq]));
+        done[lq] = 1;
+    }
+    for (int lq = 0; lq < s->n; ++lq) {
+        if (done[lq]) continue;
+        int b = s->pl.pos[lq];
+        if (s->transport == QSIM_TRANSPORT_LOCAL) {
+            // pairs across shards r (bit 0) and r | 2^(b-nl): dot products, no data movement
+            const int j = b - s->nl;
+            for (auto &sa : s->shards) {
+                if ((sa.index >> j) & 1) continue;
+                for (auto &sb : s->shards)
+                    if (sb.index == (sa.index | (1 << j))) {
+                        if (s->enc == QSIM_ENC_FP64)
+                            launch_dot_e(sa.amps, sb.amps, 1ull << s->nl, s->d_partials, s->d_out, s->stream);
+                        else
+                            launch_dot_a(sa.amps, sb.amps, 1ull << s->nl, s->atab, s->d_partials, s->d_out,
+                                         s->stream);
+                        s->st.kernels += 2;
+                        CU(cudaMemcpyAsync(s->h_out, s->d_out, 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                                           s->stream));
+                        CU(cudaStreamSynchronize(s->stream));
+                        Sr[lq] += s->h_out[0];
+                        Si[lq] += s->h_out[1];
+                    }
+            }
+        } else {
+            // NCCL: move the qubit to a local bit with a pure swap exchange (a relabelling)
+            int avoid[1] = {-1};
+            int l = s->pl.choose_victim(nullptr, 0, 0, avoid, 0, false);
+            PlanOp x{};
+            x.type = QSIM_OP_EXCHANGE;
+            x.g = b;
+            x.l = l;
+            RC(exchange(s, x, nullptr, nullptr));
+            s->pl.swap_bits(b, l);
+            RC(pair_sums_local(s, l, Sr[lq], Si[lq]));
+        }
+    }
+    if (s->transport == QSIM_TRANSPORT_NCCL && s->P > 1) {
+        std::vector<double> v(2 * s->n);
+        for (int i = 0; i < s->n; ++i) {
+            v[i] = Sr[i];
+            v[s->n + i] = Si[i];
+        }
+        CU(cudaMemcpyAsync(s->d_out, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+        NC(ncclAllReduce(s->d_out, s->d_out, v.size(), ncclFloat64, ncclSum, s->comm, s->stream));
+        CU(cudaMemcpyAsync(v.data(), s->d_out, v.size() * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+        CU(cudaStreamSynchronize(s->stream));
+        for (int i = 0; i < s->n; ++i) {
+            Sr[i] = v[i];
+            Si[i] = v[s->n + i];
+        }
+    }
+    const double nrm = phys[0];
+    for (int lq = 0; lq < s->n; ++lq) {
+        q[3 * lq + 0] = (nrm - 2.0 * Sr[lq]) / 2.0;
+        q[3 * lq + 1] = (nrm - 2.0 * Si[lq]) / 2.0;
+        q[3 * lq + 2] = phys[1 + s->pl.pos[lq]];
+    }
+    return QSIM_OK;
+}
+
+static uint64_t splitmix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+int qsim_measure_u(qsim_state *s, int qubit, double u, int *outcome, double *p0_out) {
+    if (!s || !outcome || qubit < 0 || qubit >= s->n) {
+        set_error("qsim_measure: bad qubit or null outcome");
+        return QSIM_EINVAL;
+    }
+    cudaSetDevice(s->dev);
+    std::vector<double> phys;
+    RC(phys_probs(s, phys));
+    const int b = s->pl.pos[qubit];
+    const double s1 = phys[1 + b], s0 = phys[0] - s1;
+    const double p0 = s0 / phys[0];
+    if (p0_out) *p0_out = p0;
+    const int out = (u < p0) ? 0 : 1;
+    const double keep = out ? s1 : s0;
+    if (!(keep >= 1e-14)) {
+        set_error("projection onto a state with norm^2 < 1e-14 (PAPER.md:1481)");
+        return QSIM_EZERONORM;
+    }
+    const double f = 1.0 / std::sqrt(keep);
+    if (s->enc == QSIM_ENC_FP64) {
+        for (auto &sh : s->shards) {
+            if (b < s->nl) {
+                launch_collapse_e(sh.amps, 1ull << s->nl, b, out, f, s->stream);
+            } else if (rank_bit(sh, b, s->nl) != out) {
+                CU(cudaMemsetAsync(sh.amps, 0, ((size_t)1 << s->nl) * s->amp_bytes, s->stream));
+            } else {
+                launch_scale_all_e(sh.amps, 1ull << s->nl, f, s->stream);
+            }
+            s->st.kernels++;
+        }
+    } else {
+        RC(measure_collapse_a(s, b, out, f));
+    }
+    CU(cudaStreamSynchronize(s->stream));
+    *outcome = out;
+    return QSIM_OK;
+}
+
+int qsim_measure(qsim_state *s, int qubit, uint64_t seed, int *outcome) {
+    uint64_t x = splitmix64(seed);
+    double u = (double)(x >> 11) * (1.0 / 9007199254740992.0);
+    return qsim_measure_u(s, qubit, u, outcome, nullptr);
+}
+
+static uint64_t logical_to_phys(const qsim_state *s, uint64_t L) {
+    uint64_t p = 0;
+    for (int q = 0; q < s->n; ++q)
+        if ((L >> q) & 1ull) p |= 1ull << s->pl.pos[q];
+    return p;
+}
+
+int qsim_get_amplitudes(qsim_state *s, const uint64_t *idx, size_t m, double *out) {
+    if (!s || (m && (!idx || !out))) return QSIM_EINVAL;
+    cudaSetDevice(s->dev);
+    const uint64_t dim_mask = (s->n == 64) ? ~0ull : ((1ull << s->n) - 1ull);
+    for (size_t k = 0; k < m; ++k)
+        if (idx[k] & ~dim_mask) {
+            set_error("amplitude index out of range");
+            return QSIM_EINVAL;
+        }
+    if (!m) return QSIM_OK;
+    // device scratch: offsets + results for m entries
+    uint64_t *d_off = nullptr;
+    double *d_val = nullptr;
+    CU(cudaMalloc(&d_off, m * sizeof(uint64_t)));
+    if (cudaMalloc(&d_val, m * 2 * sizeof(double)) != cudaSuccess) {
+        cudaFree(d_off);
+        set_error("cudaMalloc for get_amplitudes");
+        return QSIM_ENOMEM;
+    }
+    std::vector<double> res(2 * m, 0.0);
+    std::vector<uint64_t> off;
+    std::vector<size_t> which;
+    int rc = QSIM_OK;
+    const uint64_t lmask = (1ull << s->nl) - 1ull;
+    for (auto &sh : s->shards) {
+        off.clear();
+        which.clear();
+        for (size_t k = 0; k < m; ++k) {
+            uint64_t p = logical_to_phys(s, idx[k]);
+            if ((int)(p >> s->nl) == sh.index) {
+                off.push_back(p & lmask);
+                which.push_back(k);
+            }
+        }
+        if (off.empty()) continue;
+        if (cudaMemcpyAsync(d_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice, s->stream) != cudaSuccess) {
+            rc = QSIM_ECUDA;
+            break;
+        }
+        if (s->enc == QSIM_ENC_FP64)
+            launch_gather_e(sh.amps, d_off, off.size(), d_val, s->stream);
+        else
+            launch_gather_a(sh.amps, d_off, off.size(), s->atab, d_val, s->stream);
+        s->st.kernels++;
+        std::vector<double> tmp(2 * off.size());
+        cudaMemcpyAsync(tmp.data(), d_val, tmp.size() * 8, cudaMemcpyDeviceToHost, s->stream);
+        if (cudaStreamSynchronize(s->stream) != cudaSuccess) {
+            rc = QSIM_ECUDA;
+            break;
+        }
+        for (size_t k = 0; k < which.size(); ++k) {
+            res[2 * which[k]] = tmp[2 * k];
+            res[2 * which[k] + 1] = tmp[2 * k + 1];
+        }
+    }
+    if (rc == QSIM_OK && s->transport == QSIM_TRANSPORT_NCCL && s->P > 1) {
+        double *d_all = nullptr;
+        if (cudaMalloc(&d_all, res.size() * 8) == cudaSuccess) {
+            cudaMemcpyAsync(d_all, res.data(), res.size() * 8, cudaMemcpyHostToDevice, s->stream);
+            if (ncclAllReduce(d_all, d_all, res.size(), ncclFloat64, ncclSum, s->comm, s->stream) != ncclSuccess)
+                rc = QSIM_ECOMM;
+            cudaMemcpyAsync(res.data(), d_all, res.size() * 8, cudaMemcpyDeviceToHost, s->stream);
+            cudaStreamSynchronize(s->stream);
+            cudaFree(d_all);
+        } else {
+            rc = QSIM_ENOMEM;
+        }
+    }
+    cudaFree(d_off);
+    cudaFree(d_val);
+    if (rc) {
+        set_error("qsim_get_amplitudes failed");
+        return rc;
+    }
+    std::memcpy(out, res.data(), res.size() * 8);
+    return QSIM_OK;
+}
+
+static int upload_inv(qsim_state *s, int **d_inv) {
+    CU(cudaMalloc(d_inv, s->n * sizeof(int)));
+    CU(cudaMemcpyAsync(*d_inv, s->pl.inv.data(), s->n * sizeof(int), cudaMemcpyHostToDevice, s->stream));
+    return QSIM_OK;
+}
+
+int qsim_get_state(qsim_state *s, double *out) {
+    if (!s || !out) return QSIM_EINVAL;
+    if (s->n > 30) {
+        set_error("qsim_get_state is for N <= 30");
+        return QSIM_EINVAL;
+    }
+    cudaSetDevice(s->dev);
+    const size_t dim = (size_t)1 << s->n;
+    void *d_full = nullptr;
+    int *d_inv = nullptr;
+    CU(cudaMalloc(&d_full, dim * 16));
+    RC(upload_inv(s, &d_inv));
+    CU(cudaMemsetAsync(d_full, 0, dim * 16, s->stream));
+    for (auto &sh : s->shards) {
+        if (s->enc == QSIM_ENC_FP64)
+            launch_to_logical_e(sh.amps, 1ull << s->nl, shard_base(s, sh), d_inv, s->n, d_full, s->stream);
+        else
+            launch_to_logical_a(sh.amps, 1ull << s->nl, shard_base(s, sh), d_inv, s->n, s->atab, d_full, s->stream);
+        s->st.kernels++;
+    }
+    if (s->transport == QSIM_TRANSPORT_NCCL && s->P > 1)
+        NC(ncclAllReduce(d_full, d_full, 2 * dim, ncclFloat64, ncclSum, s->comm, s->stream));
+    CU(cudaMemcpyAsync(out, d_full, dim * 16, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaStreamSynchronize(s->stream));
+    cudaFree(d_full);
+    cudaFree(d_inv);
+    return QSIM_OK;
+}
+
+int qsim_set_state(qsim_state *s, const double *amps) {
+    if (!s || !amps) return QSIM_EINVAL;
+    if (s->enc != QSIM_ENC_FP64) {
+        set_error("qsim_set_state: E only (use qsim_set_codes for A)");
+        return QSIM_EUNSUPPORTED;
+    }
+    if (s->n > 30) {
+        set_error("qsim_set_state is for N <= 30");
+        return QSIM_EINVAL;
+    }
+    cudaSetDevice(s->dev);
+    const size_t dim = (size_t)1 << s->n;
+    void *d_full = nullptr;
+    int *d_inv = nullptr;
+    CU(cudaMalloc(&d_full, dim * 16));
+    RC(upload_inv(s, &d_inv));
+    CU(cudaMemcpyAsync(d_full, amps, dim * 16, cudaMemcpyHostToDevice, s->stream));
+    for (auto &sh : s->shards) {
+        launch_from_logical_e(sh.amps, 1ull << s->nl, shard_base(s, sh), d_inv, s->n, d_full, s->stream);
+        s->st.kernels++;
+    }
+    CU(cudaStreamSynchronize(s->stream));
+    cudaFree(d_full);
+    cudaFree(d_inv);
+    return QSIM_OK;
+}
+
+int qsim_get_codes(qsim_state *s, int8_t *codes, double *r0, double *r1) {
+    if (!s || !codes) return QSIM_EINVAL;
+    if (s->enc != QSIM_ENC_ADAPTIVE2) {
+        set_error("qsim_get_codes: A only");
+        return QSIM_EUNSUPPORTED;
+    }
+    if (s->n > 32) {
+        set_error("qsim_get_codes is for N <= 32");
+        return QSIM_EINVAL;
+    }
+    cudaSetDevice(s->dev);
+    const size_t dim = (size_t)1 << s->n;
+    void *d_full = nullptr;
+    int *d_inv = nullptr;
+    CU(cudaMalloc(&d_full, dim * 2));
+    RC(upload_inv(s, &d_inv));
+    for (auto &sh : s->shards) {
+        launch_codes_to_logical_a(sh.amps, 1ull << s->nl, shard_base(s, sh), d_inv, s->n, d_full, s->stream);
+        s->st.kernels++;
+    }
+    CU(cudaMemcpyAsync(codes, d_full, dim * 2, cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaStreamSynchronize(s->stream));
+    cudaFree(d_full);
+    cudaFree(d_inv);
+    if (r0) *r0 = s->r0;
+    if (r1) *r1 = s->r1;
+    return QSIM_OK;
+}
+
+int qsim_set_codes(qsim_state *s, const int8_t *codes, double r0, double r1) {
+    if (!s || !codes) return QSIM_EINVAL;
+    if (s->enc != QSIM_ENC_ADAPTIVE2) {
+        set_error("qsim_set_codes: A only");
+        return QSIM_EUNSUPPORTED;
+    }
+    if (s->n > 32 || !(r0 > 0.0) || !(r1 >= r0) || !(r1 < 1.0)) {
+        set_error("qsim_set_codes: N <= 32 and 0 < r0 <= r1 < 1 required");
+        return QSIM_EINVAL;
+    }
+    cudaSetDevice(s->dev);
+    const size_t dim = (size_t)1 << s->n;
+    void *d_full = nullptr;
+    int *d_inv = nullptr;
+    CU(cudaMalloc(&d_full, dim * 2));
+    RC(upload_inv(s, &d_inv));
+    CU(cudaMemcpyAsync(d_full, codes, dim * 2, cudaMemcpyHostToDevice, s->stream));
+    for (auto &sh : s->shards) {
+        launch_codes_from_logical_a(sh.amps, 1ull << s->nl, shard_base(s, sh), d_inv, s->n, d_full, s->stream);
+        s->st.kernels++;
+    }
+    s->r0 = r0;
+    s->r1 = r1;
+    RC(atables_set(s->atab, r0, r1, s->stream));
+    CU(cudaStreamSynchronize(s->stream));
+    cudaFree(d_full);
+    cudaFree(d_inv);
+    return QSIM_OK;
+}
+
+}  // extern "C"
+
+// ============================================================================
+// A variant executor (a8, a9)
+// ============================================================================
+namespace qsim {
+
+// Exact global bounds of the post-gate magnitudes (reading R-A4), then the
+// decode-apply-encode sweep with those bounds.
+static int dense_gate_a(qsim_state *s, const PlanOp &o, const double *u) {
+    double mn = INFINITY, mx = -INFINITY;
+    for (auto &sh : s->shards) {
+        AGateParams p{};
+        fill_agate(p, s, sh, o, u);
+        prof_begin(s);
+        launch_bounds_a(p, s->atab, s->d_partials, s->d_out, s->stream);
+        prof_end(s, QSIM_K_A_BOUNDS, std::ldexp((double)s->amp_bytes, s->nl));
+        s->st.kernels += 2;
+        s->st.hbm_bytes += std::ldexp((double)s->amp_bytes, s->nl);
+        CU(cudaMemcpyAsync(s->h_out, s->d_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+        CU(cudaStreamSynchronize(s->stream));
+        mn = std::min(mn, s->h_out[0]);
+        mx = std::max(mx, s->h_out[1]);
+    }
+    if (s->transport == QSIM_TRANSPORT_NCCL && s->P > 1) {
+        s->h_out[0] = mn;
+        s->h_out[1] = -mx;
+        CU(cudaMemcpyAsync(s->d_out, s->h_out, 2 * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+        NC(ncclAllReduce(s->d_out, s->d_out, 2, ncclFloat64, ncclMin, s->comm, s->stream));
+        CU(cudaMemcpyAsync(s->h_out, s->d_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+        CU(cudaStreamSynchronize(s->stream));
+        mn = s->h_out[0];
+        mx = -s->h_out[1];
+    }
+    double r0n, r1n;
+    if (mn > mx) {  // no intermediate magnitudes: sentinel (reading R-A8)
+        r0n = r1n = 0.5;
+    } else {
+        r0n = std::sqrt(mn);
+        r1n = std::sqrt(mx);
+    }
+    RC(atables_set_next(s->atab, r0n, r1n, s->stream));
+    for (auto &sh : s->shards) {
+        AGateParams p{};
+        fill_agate(p, s, sh, o, u);
+        prof_begin(s);
+        launch_apply_a(p, s->atab, s->stream);
+        prof_end(s, QSIM_K_A_APPLY, std::ldexp(2.0 * (double)s->amp_bytes, s->nl));
+        s->st.kernels++;
+        s->st.hbm_bytes += std::ldexp(2.0 * (double)s->amp_bytes, s->nl);
+    }
+    s->r0 = r0n;
+    s->r1 = r1n;
+    RC(atables_commit_next(s->atab, s->stream));
+    CU(cudaGetLastError());
+    return QSIM_OK;
+}
+
+static int run_gates_a(qsim_state *s, const std::vector<PlanOp> &run, const std::vector<const double *> &us) {
+    for (size_t i = 0; i < run.size(); ++i) {
+        const PlanOp &o = run[i];
+        const double *u = us[i];
+        if (o.cls == CLS_DENSE) {
+            RC(dense_gate_a(s, o, u));
+            continue;
+        }
+        // perm (anti-diagonal) and phase (diagonal) gates move or rotate codes; bounds unchanged
+        for (auto &sh : s->shards) {
+            if (!global_ctrls_ok(s, sh, o)) continue;
+            AGateParams p{};
+            fill_agate(p, s, sh, o, u);
+            prof_begin(s);
+            launch_fast_a(p, s->atab, s->stream);
+            prof_end(s, QSIM_K_A_FAST, gate_bytes_alone(s, sh, o, u));
+            s->st.kernels++;
+            s->st.hbm_bytes += gate_bytes_alone(s, sh, o, u);
+        }
+        CU(cudaGetLastError());
+    }
+    return QSIM_OK;
+}
+
+int measure_collapse_a(qsim_state *s, int b, int out, double f) {
+    (void)f;
+    // Collapse = a diagonal projector followed by rescaling: decode, zero the
+    // other half, scale by f, re-encode with exact new bounds (two-phase).
+    double mn = INFINITY, mx = -INFINITY;
+    for (auto &sh : s->shards) {
+        ACollapseParams p{};
+        p.a = sh.amps;
+        p.n = s->alloc_amps;
+        p.shard_base = shard_base(s, sh);
+        p.bit = b;
+        p.keep = out;
+        p.f = f;
+        launch_collapse_bounds_a(p, s->atab, s->d_partials, s->d_out, s->stream);
+        CU(cudaMemcpyAsync(s->h_out, s->d_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+        CU(cudaStreamSynchronize(s->stream));
+        mn = std::min(mn, s->h_out[0]);
+        mx = std::max(mx, s->h_out[1]);
+    }
+    if (s->transport == QSIM_TRANSPORT_NCCL && s->P > 1) {
+        s->h_out[0] = mn;
+        s->h_out[1] = -mx;
+        CU(cudaMemcpyAsync(s->d_out, s->h_out, 2 * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+        NC(ncclAllReduce(s->d_out, s->d_out, 2, ncclFloat64, ncclMin, s->comm, s->stream));
+        CU(cudaMemcpyAsync(s->h_out, s->d_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+        CU(cudaStreamSynchronize(s->stream));
+        mn = s->h_out[0];
+        mx = -s->h_out[1];
+    }
+    double r0n = 0.5, r1n = 0.5;
+    if (mn <= mx) {
+        r0n = std::sqrt(mn);
+        r1n = std::sqrt(mx);
+    }
+    RC(atables_set_next(s->atab, r0n, r1n, s->stream));
+    for (auto &sh : s->shards) {
+        ACollapseParams p{};
+        p.a = sh.amps;
+        p.n = s->alloc_amps;
+        p.shard_base = shard_base(s, sh);
+        p.bit = b;
+        p.keep = out;
+        p.f = f;
+        launch_collapse_apply_a(p, s->atab, s->stream);
+    }
+    s->r0 = r0n;
+    s->r1 = r1n;
+    RC(atables_commit_next(s->atab, s->stream));
+    return QSIM_OK;
+}
+
+void fill_agate(AGateParams &p, const qsim_state *s, const Shard &sh, const PlanOp &o, const double *u) {
+    p.a = sh.amps;
+    p.nl = s->nl;
+    p.shard_base = shard_base(s, sh);
+    p.t = o.l;
+    p.cls = o.cls;
+    p.cmask = full_cmask(o);
+    std::memcpy(p.u, u, sizeof(p.u));
+}
+
+}  // namespace qsim

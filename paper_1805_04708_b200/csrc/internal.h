@@ -1,0 +1,49 @@
+// internal.h -- shared declarations of the qsim library (not part of the C-ABI).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/qsim.h"
+
+namespace qsim {
+
+// ---- error handling --------------------------------------------------------
+void set_error(const std::string &msg);
+struct Error {
+    int code;
+    std::string msg;
+};
+
+// ---- gate classes: the kernels specialise on these ---------
+enum GateClass : int32_t { CLS_DENSE = 0, CLS_DIAG = 1, CLS_ANTI = 2, CLS_IDENT = 3 };
+int32_t classify(const double u[8]);
+
+// ---- planner (a2, a7) --------------------------------------------------------
+struct PlanOp {
+    int32_t type;  // QSIM_OP_EXCHANGE / QSIM_OP_GATE
+    int32_t g, l, cls, nctrl;
+    int32_t ctrl[2];
+    int32_t gate_index;
+};
+
+struct Planner {
+    int n = 0, nl = 0;
+    std::vector<int> pos, inv;  // logical -> physical bit, physical -> logical
+    void init(int n_, int nshards, const int *initial_map);
+    // Appends the ops for gates[0..ngates) to `ops` and updates the map.
+    // `lookahead` enables Belady victim selection over the remaining gates.
+    void plan(const qsim_gate *gates, size_t ngates, std::vector<PlanOp> &ops, bool lookahead);
+    int choose_victim(const qsim_gate *gates, size_t ngates, size_t cur, const int *avoid, int navoid, bool lookahead);
+    void swap_bits(int a, int b);  // exchange the logical qubits at physical bits a and b
+};
+
+int validate_gates(int n, const qsim_gate *gates, size_t ngates, bool check_unitary);
+
+}  // namespace qsim
+
+struct qsim_plan {
+    qsim::Planner pl;
+    std::vector<qsim::PlanOp> ops;
+};

@@ -1,0 +1,124 @@
+// kernels.h -- device kernel parameter blocks and launchers (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace qsim {
+
+// ---- single-gate sweep (a3, a4, a5) ------------------------------------------
+// Enumerates the 2^(nl-1-nlc) amplitude groups of one gate: insert a 0 bit at
+// every sorted position of {target} U local controls, OR in the local control
+// mask (all controls 1), then pair i0 with i1 = i0 | 2^t (Eq. NUM2).
+struct SweepParams {
+    void *a;                // shard base (double2 for E)
+    uint64_t nitems;        // number of groups
+    uint64_t cmask;         // local control bits (set after insertion)
+    int32_t ins[3];         // sorted insertion positions
+    int32_t nins;
+    int32_t t;              // target bit (local)
+    int32_t cls;            // CLS_DENSE / CLS_DIAG / CLS_ANTI
+    int32_t touch;          // DIAG: 3 = both halves, 2 = only i1 (u00 == 1), 1 = only i0 (u11 == 1)
+    int32_t pad;
+    double u[8];
+};
+void launch_sweep_e(const SweepParams &p, cudaStream_t s);
+
+// Multiply every amplitude whose local control bits are set by `f` (a diagonal
+// gate whose target is a global bit: the factor is uniform on the shard).
+struct ScaleParams {
+    void *a;
+    uint64_t nitems;
+    uint64_t cmask;
+    int32_t ins[2];
+    int32_t nins;
+    int32_t pad;
+    double f[2];
+};
+void launch_scale_e(const ScaleParams &p, cudaStream_t s);
+
+// ---- fused tile pass (a6) ----------------------------------------------------
+constexpr int PASS_LOW = 5;       // tile always holds qubits 0..4 (512 B contiguous runs)
+constexpr int PASS_MAX_K = 12;    // 2^12 amplitudes x 16 B = 64 KiB of shared memory per CTA
+constexpr int PASS_MIN_K = 9;
+constexpr int PASS_R = 4;         // qubits held in registers per stage (16 amplitudes per thread)
+constexpr int PASS_THREADS = 128;
+constexpr int PASS_MAX_GATES = 24;
+constexpr int PASS_MAX_STAGES = 12;
+
+enum PassGateKind : int8_t { PG_DENSE = 0, PG_DIAG_IN = 1, PG_ANTI = 2, PG_DIAG_OUT = 3 };
+
+struct PassGate {
+    double u[8];
+    uint64_t cmask_out;  // control bits outside the stage's register set (full physical index)
+    uint64_t tmask_out;  // PG_DIAG_OUT: target bit (full physical index)
+    int8_t kind;
+    int8_t slot;         // target slot (0..3) in the register set
+    int8_t cslot;        // slot bits that must be 1 (controls inside the register set)
+    int8_t pad[5];
+};
+
+struct PassStage {
+    int8_t rbits[PASS_R];  // slot s <-> tile bit rbits[s]
+    int8_t gbits[PASS_MAX_K - PASS_R];  // group index bit i <-> tile bit gbits[i]
+    int8_t first_gate;
+    int8_t ngates;
+    int8_t pad[2];
+};
+
+struct PassParams {
+    void *a;
+    uint64_t shard_base;  // rank bits of this shard (full physical index of local 0)
+    uint64_t ntiles;
+    int32_t nl;
+    int32_t K;            // tile qubits
+    int32_t nstages;
+    int32_t pad;
+    int32_t high_q[PASS_MAX_K - PASS_LOW];  // local qubit of tile bit PASS_LOW + i (ascending)
+    int32_t pad2;
+    PassStage st[PASS_MAX_STAGES];
+    PassGate g[PASS_MAX_GATES];
+};
+void launch_pass_e(const PassParams &p, int grid, cudaStream_t s);
+int pass_e_max_grid();
+
+// ---- exchange-fused gate (a7) ------------------------------------------------
+struct XchgParams {
+    void *own;             // this shard
+    const void *stage;     // received chunk (partner's half-shard slice)
+    uint64_t p0;           // first half-index of the chunk
+    uint64_t n;            // amplitudes in the chunk
+    uint64_t shard_base;   // full physical index of local 0 (after the swap)
+    uint64_t cmask;        // full-index control mask
+    int32_t l;             // victim bit (now holds the gate's target)
+    int32_t b;             // this shard's value of the exchanged global bit = slot it keeps
+    int32_t mode;          // 0 = copy only (pure swap), 1 = apply gate on arrival
+    int32_t cls;
+    double u[8];
+};
+void launch_xchg_e(const XchgParams &p, cudaStream_t s);
+
+// ---- reductions (a10) ---------------------------------------------------------
+// Per-shard: out[0] = sum |a|^2, out[1 + q] = sum_{bit q = 1} |a|^2 for local q.
+constexpr int RED_SLOTS = 64;
+int red_blocks();
+void launch_probs_e(const void *a, int nl, double *partials, double *out, cudaStream_t s);
+// S = sum_{i: bit q = 0} conj(a_i) a_{i | 2^q}  (out[0] = re, out[1] = im)
+void launch_pairdot_e(const void *a, int nl, int q, double *partials, double *out, cudaStream_t s);
+// S = sum_i conj(x_i) y_i over two shards (global-qubit pairs in loopback mode)
+void launch_dot_e(const void *x, const void *y, uint64_t n, double *partials, double *out, cudaStream_t s);
+// Collapse: zero amplitudes whose bit q != keep, scale the others by f.
+void launch_collapse_e(void *a, uint64_t n, int q, int keep, double f, cudaStream_t s);
+void launch_scale_all_e(void *a, uint64_t n, double f, cudaStream_t s);
+
+// Gather a[off[k]] -> out[k]; scatter in[k] -> a[off[k]] (double2 each)
+void launch_gather_e(const void *a, const uint64_t *off, uint64_t m, void *out, cudaStream_t s);
+void launch_scatter_e(void *a, const uint64_t *off, uint64_t m, const void *in, cudaStream_t s);
+// Permute a shard into logical order: out[logical(shard_base | i)] = a[i]
+void launch_to_logical_e(const void *a, uint64_t n, uint64_t shard_base, const int *inv_dev, int nq, void *out,
+                         cudaStream_t s);
+void launch_from_logical_e(void *a, uint64_t n, uint64_t shard_base, const int *inv_dev, int nq, const void *in,
+                           cudaStream_t s);
+
+}  // namespace qsim

@@ -1,0 +1,829 @@
+// kernels_a.cu -- sm_100a kernels for the A variant: the paper's adaptive
+// 2-byte polar encoding (§4.1) fused into the sweeps.
+//
+// Storage: one uint16 per amplitude, low byte b0 (magnitude code), high byte
+// b1 (angle code): theta = pi b1 / 128; r = 0 (b0 = -128), 1 (b0 = 127), else
+// (b0 + 127)(r1 - r0)/253 + r0.
+//
+// Dense gates follow reading R-A4 (exact bounds per gate): phase 1 decodes,
+// applies the gate and reduces min/max |z'|^2 over the intermediate
+// magnitudes (read-only, 2 B/amp); the host turns them into (r0, r1) (global
+// over all shards); phase 2 decodes, applies and encodes with those bounds
+// (4 B/amp).  Both phases use the same device functions, so the
+// zero/one/intermediate classification agrees bit for bit.
+//
+// Decode is a table lookup (tables built on the host with the paper's
+// expressions).  Encode avoids fp64 sqrt/atan2: an fp32 candidate code is
+// corrected against exact fp64 boundaries (squared-magnitude thresholds and
+// boundary-direction cross products), so the code equals the fp64 rounding of
+// the definition except at exact ties.
+//
+// Permutation and phase gates never decode: anti-diagonal gates move codes and
+// add round(128 arg(u)/pi) to b1, diagonal gates add it in place (PAPER.md:
+// 442-444, 459-460: "very little" extra cost for X / CNOT).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "internal.h"
+#include "kernels.h"
+#include "kernels_a.h"
+
+namespace qsim {
+
+// reading R-A5: |z| < 1e-12 is the special 0, |z| > 1 - 1e-12 the special 1 (compared squared)
+#define A_ZERO2 1e-24
+#define A_ONE2 ((1.0 - 1e-12) * (1.0 - 1e-12))
+
+static int a_num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+// ---------------------------------------------------------------- tables (host)
+static void fill_tables(ATabData &t, double r0, double r1) {
+    const double PI = 3.14159265358979323846;
+    for (int i = 0; i < 256; ++i) {
+        int b0 = i - 128;
+        if (b0 == -128)
+            t.r[i] = 0.0;
+        else if (b0 == 127)
+            t.r[i] = 1.0;
+        else
+            t.r[i] = (double)(b0 + 127) * (r1 - r0) / 253.0 + r0;
+        double th = PI * (double)b0 / 128.0;  // i - 128 doubles as b1 here
+        t.cth[i] = std::cos(th);
+        t.sth[i] = std::sin(th);
+    }
+    for (int c = 0; c < 256; ++c) {
+        double m = r0 + ((double)c + 0.5) * (r1 - r0) / 253.0;
+        t.thr[c] = (c < 253) ? m * m : INFINITY;
+    }
+    for (int k = -129; k <= 130; ++k) {
+        double beta = ((double)k + 0.5) * PI / 128.0;
+        t.cb[k + 129] = std::cos(beta);
+        t.sb[k + 129] = std::sin(beta);
+    }
+    t.r0 = r0;
+    t.r1 = r1;
+    t.degenerate = !(r1 > r0);
+    t.scale = t.degenerate ? 0.0 : 253.0 / (r1 - r0);
+}
+
+int atables_alloc(ATables **out) {
+    auto *t = new ATables();
+    if (cudaMalloc(&t->d[0], sizeof(ATabData)) != cudaSuccess || cudaMalloc(&t->d[1], sizeof(ATabData)) != cudaSuccess ||
+        cudaMallocHost(&t->h, sizeof(ATabData)) != cudaSuccess) {
+        cudaGetLastError();
+        atables_free(t);
+        set_error("A tables allocation failed");
+        return QSIM_ENOMEM;
+    }
+    *out = t;
+    return QSIM_OK;
+}
+
+void atables_free(ATables *t) {
+    if (!t) return;
+    if (t->d[0]) cudaFree(t->d[0]);
+    if (t->d[1]) cudaFree(t->d[1]);
+    if (t->h) cudaFreeHost(t->h);
+    delete t;
+}
+
+static int upload(ATables *t, int which, double r0, double r1, cudaStream_t s) {
+    if (cudaStreamSynchronize(s) != cudaSuccess) return QSIM_ECUDA;  // h is reused
+    fill_tables(*t->h, r0, r1);
+    if (cudaMemcpyAsync(t->d[which], t->h, sizeof(ATabData), cudaMemcpyHostToDevice, s) != cudaSuccess) {
+        set_error("A tables upload failed");
+        return QSIM_ECUDA;
+    }
+    if (cudaStreamSynchronize(s) != cudaSuccess) return QSIM_ECUDA;
+    return QSIM_OK;
+}
+
+int atables_set(ATables *t, double r0, double r1, cudaStream_t s) {
+    int rc = upload(t, t->cur, r0, r1, s);
+    if (rc) return rc;
+    return upload(t, 1 - t->cur, r0, r1, s);
+}
+int atables_set_next(ATables *t, double r0, double r1, cudaStream_t s) { return upload(t, 1 - t->cur, r0, r1, s); }
+int atables_commit_next(ATables *t, cudaStream_t s) {
+    (void)s;
+    t->cur = 1 - t->cur;
+    return QSIM_OK;
+}
+static const ATabData *tcur(const ATables *t) { return t->d[t->cur]; }
+static const ATabData *tnext(const ATables *t) { return t->d[1 - t->cur]; }
+
+// ---------------------------------------------------------------- device side
+struct ASm {
+    double r[256];    // decode (current bounds)
+    double thr[256];  // encode thresholds (next bounds)
+    double cth[256], sth[256];
+    double cb[260], sb[260];
+    double r0n, scalen;
+    int degn;
+};
+
+__device__ void load_asm(ASm &sm, const ATabData *__restrict__ cur, const ATabData *__restrict__ nxt) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        sm.r[i] = cur->r[i];
+        sm.thr[i] = nxt->thr[i];
+        sm.cth[i] = cur->cth[i];
+        sm.sth[i] = cur->sth[i];
+    }
+    for (int i = threadIdx.x; i < 260; i += blockDim.x) {
+        sm.cb[i] = cur->cb[i];
+        sm.sb[i] = cur->sb[i];
+    }
+    if (threadIdx.x == 0) {
+        sm.r0n = nxt->r0;
+        sm.scalen = nxt->scale;
+        sm.degn = nxt->degenerate;
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ double2 a_decode(const ASm &sm, uint32_t code) {
+    const int b0i = (int)(code & 0xffu) ^ 0x80;  // int8 b0 + 128
+    const int b1i = (int)((code >> 8) & 0xffu) ^ 0x80;
+    const double r = sm.r[b0i];
+    return make_double2(r * sm.cth[b1i], r * sm.sth[b1i]);
+}
+
+__device__ __forceinline__ double a_m2(double2 z) { return fma(z.x, z.x, z.y * z.y); }
+
+__device__ __forceinline__ uint32_t pack(int b0, int b1) { return (uint32_t)(b0 & 0xff) | ((uint32_t)(b1 & 0xff) << 8); }
+
+__device__ __forceinline__ int a_angle_code(const ASm &sm, double2 z) {
+    float af = atan2f((float)z.y, (float)z.x) * 40.74366543152521f;  // 128 / pi
+    int k = __float2int_rn(af);
+    k = max(-128, min(128, k));
+    // upper boundary of code k: beta = (k + 0.5) pi / 128 (index k + 129)
+    double cu = z.y * sm.cb[k + 129] - z.x * sm.sb[k + 129];
+    if ((k >= 0) ? (cu >= 0.0) : (cu > 0.0)) {
+        k += 1;
+    } else {
+        double cl = z.y * sm.cb[k + 128] - z.x * sm.sb[k + 128];  // beta = (k - 0.5) pi / 128
+        if ((k > 0) ? (cl < 0.0) : (cl <= 0.0)) k -= 1;
+    }
+    k = max(-128, min(128, k));
+    return (k == 128) ? -128 : k;
+}
+
+// Encode with the NEXT bounds (PAPER.md:449-453 inverted; readings R-A3, R-A5..R-A7).
+__device__ __forceinline__ uint32_t a_encode(const ASm &sm, double2 z) {
+    const double m2 = a_m2(z);
+    if (m2 < A_ZERO2) return pack(-128, 0);
+    int b0;
+    if (m2 > A_ONE2) {
+        b0 = 127;
+    } else if (sm.degn) {
+        b0 = 0;
+    } else {
+        float mf = sqrtf((float)m2);
+        int c = __float2int_rn((mf - (float)sm.r0n) * (float)sm.scalen);
+        c = max(0, min(253, c));
+        if (c < 253 && m2 >= sm.thr[c])
+            c += 1;
+        else if (c > 0 && m2 < sm.thr[c - 1])
+            c -= 1;
+        b0 = c - 127;
+    }
+    return pack(b0, a_angle_code(sm, z));
+}
+
+__device__ __forceinline__ void a_gate(const double *u, int cls, double2 &x, double2 &y) {
+    if (cls == CLS_DENSE) {
+        double2 nx, ny;
+        nx.x = fma(u[0], x.x, fma(-u[1], x.y, fma(u[2], y.x, -u[3] * y.y)));
+        nx.y = fma(u[0], x.y, fma(u[1], x.x, fma(u[2], y.y, u[3] * y.x)));
+        ny.x = fma(u[4], x.x, fma(-u[5], x.y, fma(u[6], y.x, -u[7] * y.y)));
+        ny.y = fma(u[4], x.y, fma(u[5], x.x, fma(u[6], y.y, u[7] * y.x)));
+        x = nx;
+        y = ny;
+    }
+}
+
+__device__ __forceinline__ uint64_t a_ins0(uint64_t w, int p) {
+    return ((w >> p) << (p + 1)) | (w & ((1ull << p) - 1ull));
+}
+
+__device__ __forceinline__ bool is_inter(double m2) { return m2 >= A_ZERO2 && m2 <= A_ONE2; }
+
+// A unit = 16 codes = 8 pairs.  LOWT (t < 4): 16 contiguous codes, pairs
+// (k, k | 2^t); else: 8 contiguous codes at the i0 run and 8 at the i1 run.
+template <bool LOWT>
+__device__ __forceinline__ void unit_load(const uint16_t *__restrict__ a, uint64_t u, int t, uint32_t (&c)[16],
+                                          uint64_t &s0) {
+    uint4 v0, v1;
+    if (LOWT) {
+        s0 = u << 4;
+        v0 = *reinterpret_cast<const uint4 *>(a + s0);
+        v1 = *reinterpret_cast<const uint4 *>(a + s0 + 8);
+    } else {
+        s0 = a_ins0(u << 3, t);
+        v0 = *reinterpret_cast<const uint4 *>(a + s0);
+        v1 = *reinterpret_cast<const uint4 *>(a + (s0 | (1ull << t)));
+    }
+    const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        c[2 * k] = w[k] & 0xffffu;
+        c[2 * k + 1] = w[k] >> 16;
+    }
+}
+template <bool LOWT>
+__device__ __forceinline__ void unit_store(uint16_t *__restrict__ a, uint64_t s0, int t, const uint32_t (&c)[16]) {
+    uint4 v0, v1;
+    v0.x = c[0] | (c[1] << 16);
+    v0.y = c[2] | (c[3] << 16);
+    v0.z = c[4] | (c[5] << 16);
+    v0.w = c[6] | (c[7] << 16);
+    v1.x = c[8] | (c[9] << 16);
+    v1.y = c[10] | (c[11] << 16);
+    v1.z = c[12] | (c[13] << 16);
+    v1.w = c[14] | (c[15] << 16);
+    if (LOWT) {
+        *reinterpret_cast<uint4 *>(a + s0) = v0;
+        *reinterpret_cast<uint4 *>(a + s0 + 8) = v1;
+    } else {
+        *reinterpret_cast<uint4 *>(a + s0) = v0;
+        *reinterpret_cast<uint4 *>(a + (s0 | (1ull << t))) = v1;
+    }
+}
+// pair k of a unit: slots (j0, j1) and the local index of j0
+template <bool LOWT>
+__device__ __forceinline__ void pair_slots(int k, int t, uint64_t s0, int &j0, int &j1, uint64_t &i0) {
+    if (LOWT) {
+        // k-th index in 0..15 with bit t clear
+        int lo = k & ((1 << t) - 1);
+        j0 = ((k >> t) << (t + 1)) | lo;
+        j1 = j0 | (1 << t);
+        i0 = s0 + (uint64_t)j0;
+    } else {
+        j0 = k;
+        j1 = k + 8;
+        i0 = s0 + (uint64_t)k;
+    }
+}
+
+constexpr int A_THREADS = 256;
+
+static int a_grid(uint64_t units) {
+    uint64_t cap = (uint64_t)a_num_sms() * 8;
+    uint64_t need = (units + A_THREADS - 1) / A_THREADS;
+    return (int)(need < cap ? (need ? need : 1) : cap);
+}
+
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ double warp_sum_a(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <bool LOWT>
+__global__ void __launch_bounds__(A_THREADS) k_bounds_a(const __grid_constant__ AGateParams p,
+                                                        const ATabData *__restrict__ cur,
+                                                        const ATabData *__restrict__ nxt, double *partials) {
+    __shared__ ASm sm;
+    load_asm(sm, cur, nxt);
+    const uint16_t *a = reinterpret_cast<const uint16_t *>(p.a);
+    const uint64_t units = (p.nl >= 4) ? (1ull << (p.nl - 4)) : 1ull;
+    double mn = INFINITY, mx = -INFINITY;
+    for (uint64_t u = (uint64_t)blockIdx.x * A_THREADS + threadIdx.x; u < units; u += (uint64_t)gridDim.x * A_THREADS) {
+        uint32_t c[16];
+        uint64_t s0;
+        unit_load<LOWT>(a, u, p.t, c, s0);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            int j0, j1;
+            uint64_t i0;
+            pair_slots<LOWT>(k, p.t, s0, j0, j1, i0);
+            double2 x = a_decode(sm, c[j0]), y = a_decode(sm, c[j1]);
+            if (((p.shard_base | i0) & p.cmask) == p.cmask) a_gate(p.u, p.cls, x, y);
+            double mx2 = a_m2(x), my2 = a_m2(y);
+            if (is_inter(mx2)) {
+                mn = fmin(mn, mx2);
+                mx = fmax(mx, mx2);
+            }
+            if (is_inter(my2)) {
+                mn = fmin(mn, my2);
+                mx = fmax(mx, my2);
+            }
+        }
+    }
+    __shared__ double red[2][A_THREADS / 32];
+    mn = warp_min(mn);
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = mn;
+        red[1][threadIdx.x >> 5] = mx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a0 = INFINITY, a1 = -INFINITY;
+        for (int w = 0; w < A_THREADS / 32; ++w) {
+            a0 = fmin(a0, red[0][w]);
+            a1 = fmax(a1, red[1][w]);
+        }
+        partials[2 * blockIdx.x] = a0;
+        partials[2 * blockIdx.x + 1] = a1;
+    }
+}
+
+__global__ void k_minmax_final(const double *partials, int nb, double *out) {
+    if (threadIdx.x != 0) return;
+    double a0 = INFINITY, a1 = -INFINITY;
+    for (int b = 0; b < nb; ++b) {
+        a0 = fmin(a0, partials[2 * b]);
+        a1 = fmax(a1, partials[2 * b + 1]);
+    }
+    out[0] = a0;
+    out[1] = a1;
+}
+
+void launch_bounds_a(const AGateParams &p, const ATables *t, double *partials, double *out, cudaStream_t s) {
+    const uint64_t units = (p.nl >= 4) ? (1ull << (p.nl - 4)) : 1ull;
+    int grid = a_grid(units);
+    if (grid > 2 * a_num_sms() * 4) grid = 2 * a_num_sms() * 4;  // partials capacity
+    if (p.t < 4)
+        k_bounds_a<true><<<grid, A_THREADS, 0, s>>>(p, tcur(t), tnext(t), partials);
+    else
+        k_bounds_a<false><<<grid, A_THREADS, 0, s>>>(p, tcur(t), tnext(t), partials);
+    k_minmax_final<<<1, 32, 0, s>>>(partials, grid, out);
+}
+
+template <bool LOWT>
+__global__ void __launch_bounds__(A_THREADS) k_apply_a(const __grid_constant__ AGateParams p,
+                                                       const ATabData *__restrict__ cur,
+                                                       const ATabData *__restrict__ nxt) {
+    __shared__ ASm sm;
+    load_asm(sm, cur, nxt);
+    uint16_t *a = reinterpret_cast<uint16_t *>(p.a);
+    const uint64_t units = (p.nl >= 4) ? (1ull << (p.nl - 4)) : 1ull;
+    for (uint64_t u = (uint64_t)blockIdx.x * A_THREADS + threadIdx.x; u < units; u += (uint64_t)gridDim.x * A_THREADS) {
+        uint32_t c[16];
+        uint64_t s0;
+        unit_load<LOWT>(a, u, p.t, c, s0);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            int j0, j1;
+            uint64_t i0;
+            pair_slots<LOWT>(k, p.t, s0, j0, j1, i0);
+            double2 x = a_decode(sm, c[j0]), y = a_decode(sm, c[j1]);
+            if (((p.shard_base | i0) & p.cmask) == p.cmask) a_gate(p.u, p.cls, x, y);
+            c[j0] = a_encode(sm, x);
+            c[j1] = a_encode(sm, y);
+        }
+        unit_store<LOWT>(a, s0, p.t, c);
+    }
+}
+
+void launch_apply_a(const AGateParams &p, const ATables *t, cudaStream_t s) {
+    const uint64_t units = (p.nl >= 4) ? (1ull << (p.nl - 4)) : 1ull;
+    int grid = a_grid(units);
+    if (p.t < 4)
+        k_apply_a<true><<<grid, A_THREADS, 0, s>>>(p, tcur(t), tnext(t));
+    else
+        k_apply_a<false><<<grid, A_THREADS, 0, s>>>(p, tcur(t), tnext(t));
+}
+
+// ---------------------------------------------------------------- fast paths
+static int phase_steps(double ur, double ui) {
+    // round half away from zero of 128 arg(u) / pi (the b1 grid of PAPER.md:449)
+    const double PI = 3.14159265358979323846;
+    double x = 128.0 * std::atan2(ui, ur) / PI;
+    double k = (x >= 0.0) ? std::floor(x + 0.5) : -std::floor(-x + 0.5);
+    return (int)k;
+}
+
+__device__ __forceinline__ uint32_t shift_b1(uint32_t code, int k) {
+    if ((code & 0xffu) == 0x80u) return code;  // special zero keeps b1 = 0
+    int b1 = (int)(int8_t)(code >> 8);
+    b1 = ((b1 + k + 128) & 255) - 128;
+    return (code & 0xffu) | ((uint32_t)(b1 & 0xff) << 8);
+}
+
+struct AFastParams {
+    void *a;
+    uint64_t shard_base;
+    uint64_t cmask;
+    uint64_t n;  // codes in the shard
+    int32_t nl, t, cls;
+    int32_t k0, k1;  // DIAG: b1 steps for bit 0 / 1; ANTI: k0 = steps of u01, k1 = steps of u10
+};
+
+// diagonal: per code, 8 codes per thread
+__global__ void __launch_bounds__(A_THREADS) k_diag_a(const __grid_constant__ AFastParams p) {
+    uint16_t *a = reinterpret_cast<uint16_t *>(p.a);
+    const uint64_t nvec = p.n >> 3;
+    for (uint64_t v = (uint64_t)blockIdx.x * A_THREADS + threadIdx.x; v < nvec; v += (uint64_t)gridDim.x * A_THREADS) {
+        uint4 w = *reinterpret_cast<uint4 *>(a + (v << 3));
+        uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint64_t full = p.shard_base | ((v << 3) + k);
+            if ((full & p.cmask) != p.cmask) continue;
+            const int st = ((full >> p.t) & 1ull) ? p.k1 : p.k0;
+            uint32_t c = (k & 1) ? (ws[k >> 1] >> 16) : (ws[k >> 1] & 0xffffu);
+            c = shift_b1(c, st);
+            ws[k >> 1] = (k & 1) ? ((ws[k >> 1] & 0xffffu) | (c << 16)) : ((ws[k >> 1] & 0xffff0000u) | c);
+        }
+        w.x = ws[0];
+        w.y = ws[1];
+        w.z = ws[2];
+        w.w = ws[3];
+        *reinterpret_cast<uint4 *>(a + (v << 3)) = w;
+    }
+}
+
+template <bool LOWT>
+__global__ void __launch_bounds__(A_THREADS) k_anti_a(const __grid_constant__ AFastParams p) {
+    uint16_t *a = reinterpret_cast<uint16_t *>(p.a);
+    const uint64_t units = (p.nl >= 4) ? (1ull << (p.nl - 4)) : 1ull;
+    for (uint64_t u = (uint64_t)blockIdx.x * A_THREADS + threadIdx.x; u < units; u += (uint64_t)gridDim.x * A_THREADS) {
+        uint32_t c[16];
+        uint64_t s0;
+        unit_load<LOWT>(a, u, p.t, c, s0);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            int j0, j1;
+            uint64_t i0;
+            pair_slots<LOWT>(k, p.t, s0, j0, j1, i0);
+            if (((p.shard_base | i0) & p.cmask) != p.cmask) continue;
+            uint32_t x = c[j0], y = c[j1];
+            c[j0] = shift_b1(y, p.k0);  // a0' = u01 a1
+            c[j1] = shift_b1(x, p.k1);  // a1' = u10 a0
+        }
+        unit_store<LOWT>(a, s0, p.t, c);
+    }
+}
+
+void launch_fast_a(const AGateParams &g, const ATables *t, cudaStream_t s) {
+    (void)t;
+    AFastParams p{};
+    p.a = g.a;
+    p.shard_base = g.shard_base;
+    p.cmask = g.cmask;
+    p.n = std::max<uint64_t>(1ull << g.nl, 256);  // shards are padded to >= 256 codes (zero specials)
+    p.nl = g.nl;
+    p.t = g.t;
+    p.cls = g.cls;
+    if (g.cls == CLS_DIAG) {
+        p.k0 = phase_steps(g.u[0], g.u[1]);
+        p.k1 = phase_steps(g.u[6], g.u[7]);
+        k_diag_a<<<a_grid(p.n >> 3), A_THREADS, 0, s>>>(p);
+    } else {
+        p.k0 = phase_steps(g.u[2], g.u[3]);
+        p.k1 = phase_steps(g.u[4], g.u[5]);
+        if (g.t < 4)
+            k_anti_a<true><<<a_grid(p.n >> 4), A_THREADS, 0, s>>>(p);
+        else
+            k_anti_a<false><<<a_grid(p.n >> 4), A_THREADS, 0, s>>>(p);
+    }
+}
+
+// exchange for A: codes move; a diagonal / anti-diagonal gate is applied on arrival
+struct AXParams {
+    void *own;
+    const void *stage;
+    uint64_t p0, n, shard_base, cmask;
+    int32_t l, b, mode, cls, k0, k1;
+};
+__global__ void __launch_bounds__(A_THREADS) k_xchg_a(const __grid_constant__ AXParams p) {
+    uint16_t *own = reinterpret_cast<uint16_t *>(p.own);
+    const uint16_t *stg = reinterpret_cast<const uint16_t *>(p.stage);
+    const uint64_t lb = 1ull << p.l;
+    for (uint64_t k = (uint64_t)blockIdx.x * A_THREADS + threadIdx.x; k < p.n; k += (uint64_t)gridDim.x * A_THREADS) {
+        const uint64_t i0 = a_ins0(p.p0 + k, p.l);
+        const uint64_t i1 = i0 | lb;
+        uint32_t r = stg[k];
+        if (p.mode == 0) {
+            own[p.b ? i0 : i1] = (uint16_t)r;
+            continue;
+        }
+        uint32_t kept = own[p.b ? i1 : i0];
+        uint32_t x = p.b ? r : kept, y = p.b ? kept : r;
+        if (((p.shard_base | i0) & p.cmask) == p.cmask) {
+            if (p.cls == CLS_ANTI) {
+                uint32_t nx = shift_b1(y, p.k0), ny = shift_b1(x, p.k1);
+                x = nx;
+                y = ny;
+            } else {
+                x = shift_b1(x, p.k0);
+                y = shift_b1(y, p.k1);
+            }
+        }
+        own[i0] = (uint16_t)x;
+        own[i1] = (uint16_t)y;
+    }
+}
+void launch_xchg_a(const XchgParams &x, const ATables *t, cudaStream_t s) {
+    (void)t;
+    AXParams p{};
+    p.own = x.own;
+    p.stage = x.stage;
+    p.p0 = x.p0;
+    p.n = x.n;
+    p.shard_base = x.shard_base;
+    p.cmask = x.cmask;
+    p.l = x.l;
+    p.b = x.b;
+    p.mode = x.mode;
+    p.cls = x.cls;
+    if (x.mode == 1) {
+        if (x.cls == CLS_ANTI) {
+            p.k0 = phase_steps(x.u[2], x.u[3]);
+            p.k1 = phase_steps(x.u[4], x.u[5]);
+        } else {
+            p.k0 = phase_steps(x.u[0], x.u[1]);
+            p.k1 = phase_steps(x.u[6], x.u[7]);
+        }
+    }
+    k_xchg_a<<<a_grid(x.n / 4 + 1), A_THREADS, 0, s>>>(p);
+}
+
+// ---------------------------------------------------------------- collapse (measure)
+template <bool APPLY>
+__global__ void __launch_bounds__(A_THREADS) k_collapse_a(const __grid_constant__ ACollapseParams p,
+                                                          const ATabData *__restrict__ cur,
+                                                          const ATabData *__restrict__ nxt, double *partials) {
+    __shared__ ASm sm;
+    load_asm(sm, cur, nxt);
+    uint16_t *a = reinterpret_cast<uint16_t *>(p.a);
+    double mn = INFINITY, mx = -INFINITY;
+    const uint64_t nvec = p.n >> 3;
+    for (uint64_t v = (uint64_t)blockIdx.x * A_THREADS + threadIdx.x; v < nvec; v += (uint64_t)gridDim.x * A_THREADS) {
+        uint4 w = *reinterpret_cast<uint4 *>(a + (v << 3));
+        uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+        uint32_t outc[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint64_t full = p.shard_base | ((v << 3) + k);
+            uint32_t c = (k & 1) ? (ws[k >> 1] >> 16) : (ws[k >> 1] & 0xffffu);
+            double2 z = a_decode(sm, c);
+            if ((int)((full >> p.bit) & 1ull) != p.keep) {
+                z.x = 0.0;
+                z.y = 0.0;
+            } else {
+                z.x *= p.f;
+                z.y *= p.f;
+            }
+            if (APPLY) {
+                outc[k] = a_encode(sm, z);
+            } else {
+                double m2 = a_m2(z);
+                if (is_inter(m2)) {
+                    mn = fmin(mn, m2);
+                    mx = fmax(mx, m2);
+                }
+            }
+        }
+        if (APPLY) {
+            w.x = outc[0] | (outc[1] << 16);
+            w.y = outc[2] | (outc[3] << 16);
+            w.z = outc[4] | (outc[5] << 16);
+            w.w = outc[6] | (outc[7] << 16);
+            *reinterpret_cast<uint4 *>(a + (v << 3)) = w;
+        }
+    }
+    if (APPLY) return;
+    __shared__ double red[2][A_THREADS / 32];
+    mn = warp_min(mn);
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = mn;
+        red[1][threadIdx.x >> 5] = mx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a0 = INFINITY, a1 = -INFINITY;
+        for (int w2 = 0; w2 < A_THREADS / 32; ++w2) {
+            a0 = fmin(a0, red[0][w2]);
+            a1 = fmax(a1, red[1][w2]);
+        }
+        partials[2 * blockIdx.x] = a0;
+        partials[2 * blockIdx.x + 1] = a1;
+    }
+}
+void launch_collapse_bounds_a(const ACollapseParams &p, const ATables *t, double *partials, double *out,
+                              cudaStream_t s) {
+    int grid = a_grid(p.n >> 3);
+    if (grid > 2 * a_num_sms() * 4) grid = 2 * a_num_sms() * 4;
+    k_collapse_a<false><<<grid, A_THREADS, 0, s>>>(p, tcur(t), tnext(t), partials);
+    k_minmax_final<<<1, 32, 0, s>>>(partials, grid, out);
+}
+void launch_collapse_apply_a(const ACollapseParams &p, const ATables *t, cudaStream_t s) {
+    k_collapse_a<true><<<a_grid(p.n >> 3), A_THREADS, 0, s>>>(p, tcur(t), tnext(t), nullptr);
+}
+
+__global__ void k_init_a(uint16_t *a, uint64_t n, int first) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        a[i] = (first && i == 0) ? (uint16_t)pack(127, 0) : (uint16_t)pack(-128, 0);
+}
+void launch_init_a(void *a, uint64_t n, bool first, cudaStream_t s) {
+    k_init_a<<<a_grid(n / 8 + 1), A_THREADS, 0, s>>>(reinterpret_cast<uint16_t *>(a), n, first ? 1 : 0);
+}
+
+// ---------------------------------------------------------------- reductions on decoded values
+__global__ void __launch_bounds__(256) k_probs_a(const uint16_t *__restrict__ a, int nl,
+                                                 const ATabData *__restrict__ cur, double *partials) {
+    __shared__ ASm sm;
+    load_asm(sm, cur, cur);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t n = 1ull << nl;
+    const uint64_t nseg = n >> 8;
+    const uint64_t gwarp = (uint64_t)blockIdx.x * 8 + warp;
+    const uint64_t nwarps = (uint64_t)gridDim.x * 8;
+    double tot_lane = 0.0, pj[3] = {0.0, 0.0, 0.0}, phigh = 0.0;
+    for (uint64_t sgi = gwarp; sgi < nseg; sgi += nwarps) {
+        const uint16_t *seg = a + (sgi << 8);
+        double t = 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            double2 z = a_decode(sm, seg[lane + 32 * j]);
+            double m = fma(z.x, z.x, z.y * z.y);
+            t += m;
+            if (j & 1) pj[0] += m;
+            if (j & 2) pj[1] += m;
+            if (j & 4) pj[2] += m;
+        }
+        tot_lane += t;
+        double seg_tot = warp_sum_a(t);
+        if (8 + lane < nl && ((sgi >> lane) & 1ull)) phigh += seg_tot;
+    }
+    __shared__ double smr[8][RED_SLOTS];
+    double tot = warp_sum_a(tot_lane);
+    double pq[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) pq[q] = warp_sum_a((lane >> q) & 1 ? tot_lane : 0.0);
+    double p5 = warp_sum_a(pj[0]), p6 = warp_sum_a(pj[1]), p7 = warp_sum_a(pj[2]);
+    if (lane == 0) {
+        smr[warp][0] = tot;
+        for (int q = 0; q < 5; ++q) smr[warp][1 + q] = pq[q];
+        smr[warp][6] = p5;
+        smr[warp][7] = p6;
+        smr[warp][8] = p7;
+    }
+    smr[warp][9 + lane] = phigh;
+    if (41 + lane < RED_SLOTS) smr[warp][41 + lane] = 0.0;
+    __syncthreads();
+    if (threadIdx.x < RED_SLOTS) {
+        double s = 0.0;
+        for (int w = 0; w < 8; ++w) s += smr[w][threadIdx.x];
+        partials[(size_t)blockIdx.x * RED_SLOTS + threadIdx.x] = s;
+    }
+}
+__global__ void k_final_sum_a(const double *partials, int nblocks, int nslots, double *out) {
+    int s = threadIdx.x;
+    if (s >= nslots) return;
+    double acc = 0.0;
+    for (int b = 0; b < nblocks; ++b) acc += partials[(size_t)b * nslots + s];
+    out[s] = acc;
+}
+void launch_probs_a(const void *a, int nl, const ATables *t, double *partials, double *out, cudaStream_t s) {
+    int nb = red_blocks();
+    k_probs_a<<<nb, 256, 0, s>>>(reinterpret_cast<const uint16_t *>(a), nl, tcur(t), partials);
+    k_final_sum_a<<<1, RED_SLOTS, 0, s>>>(partials, nb, RED_SLOTS, out);
+}
+
+__global__ void __launch_bounds__(256) k_pairdot_a(const uint16_t *__restrict__ a, int nl, int q,
+                                                   const ATabData *__restrict__ cur, double *partials) {
+    __shared__ ASm sm;
+    load_asm(sm, cur, cur);
+    const uint64_t npairs = 1ull << (nl - 1);
+    const uint64_t qb = 1ull << q;
+    double sr = 0.0, si = 0.0;
+    for (uint64_t w = (uint64_t)blockIdx.x * 256 + threadIdx.x; w < npairs; w += (uint64_t)gridDim.x * 256) {
+        uint64_t i0 = a_ins0(w, q);
+        double2 x = a_decode(sm, a[i0]), y = a_decode(sm, a[i0 | qb]);
+        sr = fma(x.x, y.x, fma(x.y, y.y, sr));
+        si = fma(x.x, y.y, fma(-x.y, y.x, si));
+    }
+    __shared__ double red[2][8];
+    sr = warp_sum_a(sr);
+    si = warp_sum_a(si);
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = sr;
+        red[1][threadIdx.x >> 5] = si;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+        double s2 = 0.0;
+        for (int w = 0; w < 8; ++w) s2 += red[threadIdx.x][w];
+        partials[(size_t)blockIdx.x * 2 + threadIdx.x] = s2;
+    }
+}
+void launch_pairdot_a(const void *a, int nl, int q, const ATables *t, double *partials, double *out,
+                      cudaStream_t s) {
+    int nb = red_blocks();
+    k_pairdot_a<<<nb, 256, 0, s>>>(reinterpret_cast<const uint16_t *>(a), nl, q, tcur(t), partials);
+    k_final_sum_a<<<1, 32, 0, s>>>(partials, nb, 2, out);
+}
+
+__global__ void __launch_bounds__(256) k_dot_a(const uint16_t *__restrict__ x, const uint16_t *__restrict__ y,
+                                               uint64_t n, const ATabData *__restrict__ cur, double *partials) {
+    __shared__ ASm sm;
+    load_asm(sm, cur, cur);
+    double sr = 0.0, si = 0.0;
+    for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (uint64_t)gridDim.x * 256) {
+        double2 u = a_decode(sm, x[i]), v = a_decode(sm, y[i]);
+        sr = fma(u.x, v.x, fma(u.y, v.y, sr));
+        si = fma(u.x, v.y, fma(-u.y, v.x, si));
+    }
+    __shared__ double red[2][8];
+    sr = warp_sum_a(sr);
+    si = warp_sum_a(si);
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = sr;
+        red[1][threadIdx.x >> 5] = si;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+        double s2 = 0.0;
+        for (int w = 0; w < 8; ++w) s2 += red[threadIdx.x][w];
+        partials[(size_t)blockIdx.x * 2 + threadIdx.x] = s2;
+    }
+}
+void launch_dot_a(const void *x, const void *y, uint64_t n, const ATables *t, double *partials, double *out,
+                  cudaStream_t s) {
+    int nb = red_blocks();
+    k_dot_a<<<nb, 256, 0, s>>>(reinterpret_cast<const uint16_t *>(x), reinterpret_cast<const uint16_t *>(y), n,
+                               tcur(t), partials);
+    k_final_sum_a<<<1, 32, 0, s>>>(partials, nb, 2, out);
+}
+
+__global__ void __launch_bounds__(256) k_gather_a(const uint16_t *__restrict__ a, const uint64_t *__restrict__ off,
+                                                  uint64_t m, const ATabData *__restrict__ cur, double2 *out) {
+    __shared__ ASm sm;
+    load_asm(sm, cur, cur);
+    for (uint64_t k = (uint64_t)blockIdx.x * 256 + threadIdx.x; k < m; k += (uint64_t)gridDim.x * 256)
+        out[k] = a_decode(sm, a[off[k]]);
+}
+void launch_gather_a(const void *a, const uint64_t *off, uint64_t m, const ATables *t, double *out, cudaStream_t s) {
+    if (!m) return;
+    k_gather_a<<<a_grid(m), 256, 0, s>>>(reinterpret_cast<const uint16_t *>(a), off, m, tcur(t),
+                                         reinterpret_cast<double2 *>(out));
+}
+
+__device__ __forceinline__ uint64_t phys_to_logical_a(uint64_t phys, const int *inv, int nq) {
+    uint64_t L = 0;
+    for (int b = 0; b < nq; ++b)
+        if ((phys >> b) & 1ull) L |= 1ull << inv[b];
+    return L;
+}
+__global__ void __launch_bounds__(256) k_to_logical_a(const uint16_t *__restrict__ a, uint64_t n, uint64_t base,
+                                                      const int *__restrict__ inv, int nq,
+                                                      const ATabData *__restrict__ cur, double2 *out) {
+    __shared__ ASm sm;
+    load_asm(sm, cur, cur);
+    for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (uint64_t)gridDim.x * 256)
+        out[phys_to_logical_a(base | i, inv, nq)] = a_decode(sm, a[i]);
+}
+void launch_to_logical_a(const void *a, uint64_t n, uint64_t base, const int *inv, int nq, const ATables *t,
+                         void *out, cudaStream_t s) {
+    k_to_logical_a<<<a_grid(n), 256, 0, s>>>(reinterpret_cast<const uint16_t *>(a), n, base, inv, nq, tcur(t),
+                                             reinterpret_cast<double2 *>(out));
+}
+__global__ void k_codes_to_logical(const uint16_t *__restrict__ a, uint64_t n, uint64_t base,
+                                   const int *__restrict__ inv, int nq, uint16_t *out) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        out[phys_to_logical_a(base | i, inv, nq)] = a[i];
+}
+__global__ void k_codes_from_logical(uint16_t *a, uint64_t n, uint64_t base, const int *__restrict__ inv, int nq,
+                                     const uint16_t *__restrict__ in) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        a[i] = in[phys_to_logical_a(base | i, inv, nq)];
+}
+void launch_codes_to_logical_a(const void *a, uint64_t n, uint64_t base, const int *inv, int nq, void *out,
+                               cudaStream_t s) {
+    k_codes_to_logical<<<a_grid(n), 256, 0, s>>>(reinterpret_cast<const uint16_t *>(a), n, base, inv, nq,
+                                                 reinterpret_cast<uint16_t *>(out));
+}
+void launch_codes_from_logical_a(void *a, uint64_t n, uint64_t base, const int *inv, int nq, const void *in,
+                                 cudaStream_t s) {
+    k_codes_from_logical<<<a_grid(n), 256, 0, s>>>(reinterpret_cast<uint16_t *>(a), n, base, inv, nq,
+                                                   reinterpret_cast<const uint16_t *>(in));
+}
+
+}  // namespace qsim

@@ -1,0 +1,87 @@
+// kernels_a.h -- A-variant (adaptive 2-byte polar code, §4.1) kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+struct qsim_state;
+
+namespace qsim {
+
+struct Shard;
+struct PlanOp;
+
+// Decode / encode tables for one pair of bounds (r0, r1).  All values are
+// computed on the host in fp64 with the same expressions as PAPER.md:449-453.
+struct ATabData {
+    double r[256];      // magnitude of b0 (index b0 + 128): 0 for -128, 1 for 127, (b0+127)(r1-r0)/253 + r0
+    double thr[256];    // thr[c] = (r0 + (c + 0.5)(r1 - r0)/253)^2, c = 0..252: boundary between codes c, c+1
+    double cth[256];    // cos(pi b1 / 128), index b1 + 128
+    double sth[256];    // sin(pi b1 / 128)
+    double cb[260];     // cos((k + 0.5) pi / 128), index k + 129, k = -129..128
+    double sb[260];
+    double r0, r1, scale;  // scale = 253 / (r1 - r0) (0 if degenerate)
+    int32_t degenerate;    // r1 == r0
+    int32_t pad;
+};
+
+struct ATables {
+    ATabData *d[2] = {nullptr, nullptr};
+    ATabData *h = nullptr;  // pinned host staging
+    int cur = 0;
+};
+int atables_alloc(ATables **out);
+void atables_free(ATables *t);
+int atables_set(ATables *t, double r0, double r1, cudaStream_t s);       // current = next = (r0, r1)
+int atables_set_next(ATables *t, double r0, double r1, cudaStream_t s);  // tables for the encode bounds
+int atables_commit_next(ATables *t, cudaStream_t s);                     // next becomes current
+
+struct AGateParams {
+    void *a;              // uint16 codes: low byte b0, high byte b1
+    uint64_t shard_base;  // full physical index of local 0
+    uint64_t cmask;       // full-index control mask
+    int32_t nl;
+    int32_t t;            // target physical bit (local unless diagonal)
+    int32_t cls;
+    int32_t pad;
+    double u[8];
+};
+struct ACollapseParams {
+    void *a;
+    uint64_t n;
+    uint64_t shard_base;
+    int32_t bit;  // physical bit measured
+    int32_t keep; // outcome kept
+    double f;     // 1/sqrt(p_kept)
+};
+
+void launch_init_a(void *a, uint64_t n, bool first, cudaStream_t s);
+// phase 1 of a dense gate: out[0] = min |z'|^2, out[1] = max |z'|^2 over intermediates (+inf/-inf if none)
+void launch_bounds_a(const AGateParams &p, const ATables *t, double *partials, double *out, cudaStream_t s);
+// phase 2: decode (current tables), apply, encode (next tables)
+void launch_apply_a(const AGateParams &p, const ATables *t, cudaStream_t s);
+// diagonal / anti-diagonal gates: b1 shifts and code moves, bounds unchanged
+void launch_fast_a(const AGateParams &p, const ATables *t, cudaStream_t s);
+void launch_xchg_a(const struct XchgParams &p, const ATables *t, cudaStream_t s);
+void launch_collapse_bounds_a(const ACollapseParams &p, const ATables *t, double *partials, double *out,
+                              cudaStream_t s);
+void launch_collapse_apply_a(const ACollapseParams &p, const ATables *t, cudaStream_t s);
+
+void launch_probs_a(const void *a, int nl, const ATables *t, double *partials, double *out, cudaStream_t s);
+void launch_pairdot_a(const void *a, int nl, int q, const ATables *t, double *partials, double *out,
+                      cudaStream_t s);
+void launch_dot_a(const void *x, const void *y, uint64_t n, const ATables *t, double *partials, double *out,
+                  cudaStream_t s);
+void launch_gather_a(const void *a, const uint64_t *off, uint64_t m, const ATables *t, double *out, cudaStream_t s);
+void launch_to_logical_a(const void *a, uint64_t n, uint64_t base, const int *inv, int nq, const ATables *t,
+                         void *out, cudaStream_t s);
+void launch_codes_to_logical_a(const void *a, uint64_t n, uint64_t base, const int *inv, int nq, void *out,
+                               cudaStream_t s);
+void launch_codes_from_logical_a(void *a, uint64_t n, uint64_t base, const int *inv, int nq, const void *in,
+                                 cudaStream_t s);
+
+void fill_agate(AGateParams &p, const qsim_state *s, const Shard &sh, const PlanOp &o, const double *u);
+int measure_collapse_a(qsim_state *s, int b, int out, double f);
+
+}  // namespace qsim

@@ -1,4 +1,4 @@
-"""Seeded synthetic circuit generators -- the ONLY module shared by the oracle
+"""qsim_inputs -- seeded synthetic circuit generators: the ONLY module shared by the oracle
 side (tests / bench cpu_baseline) and the CUDA side.
 
 It holds no arithmetic of the method (no state update, no encoding, no

@@ -5,7 +5,7 @@ import math
 import numpy as np
 import pytest
 
-from paper_1805_04708_b200 import circuits as C
+import qsim_inputs as C
 
 s = 1 / math.sqrt(2)
 

@@ -1,0 +1,291 @@
+"""GPU parity for the E (complex fp64) path through the C-ABI, against the
+oracle on the same seeded inputs.  Bar (BASELINE.json north_star): max
+|delta amplitude| <= 1e-12 after each circuit; norms <= 1e-10;
+expectation values <= 1e-12."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import qsim_inputs as C
+
+pytestmark = pytest.mark.gpu
+
+q = pytest.importorskip("paper_1805_04708_b200")
+
+TOL = 1e-12
+
+
+def gpu_run(n, circ, ngpus=1, **ex):
+    s = q.State(n, q.ENC_FP64, ngpus, **ex) if ex else q.State(n, q.ENC_FP64, ngpus)
+    s.apply_circuit(circ)
+    return s
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_config1_random_circuits(seed):
+    """BASELINE config 1: N=14, 200 gates from {H,X,Y,Z,S,T,Rz,Rx,Haar,CNOT,CPHASE,Toffoli}."""
+    circ = C.config(0, seed=seed)
+    ref = oracle.e_simulate(14, circ)
+    with gpu_run(14, circ) as s:
+        got = s.get_state()
+        assert np.max(np.abs(got - ref)) <= TOL
+        assert abs(s.norm() - 1.0) <= 1e-10
+        st = s.stats()
+        assert st["kernels"] > 0 and st["gates"] == 200
+
+
+@pytest.mark.parametrize("fuse", [0, 1])
+@pytest.mark.parametrize("n", [2, 3, 5, 8, 9, 12, 13, 17])
+def test_small_and_ragged_sizes(n, fuse):
+    """Tiny states (below one tile: padded shards), one tile, several tiles."""
+    kinds = C.CFG1_KINDS if n >= 3 else tuple(k for k in C.CFG1_KINDS if k != "TOFFOLI")
+    circ = C.random_circuit(n, 120, seed=n, kinds=kinds)
+    ref = oracle.e_simulate(n, circ)
+    s = q.State(n, q.ENC_FP64, 1, fuse=fuse)
+    s.apply_circuit(circ)
+    assert np.max(np.abs(s.get_state() - ref)) <= TOL
+    s.close()
+
+
+def test_every_target_and_class():
+    """a3/a4/a5: dense, diagonal (both halves, |1>-only, |0>-only), anti-diagonal,
+    with 0/1/2 controls below and above the target, on every target bit."""
+    n = 14
+    rng = np.random.default_rng(3)
+    mats = [C.mat_haar(rng), C.mat_Z(), C.mat_T(), np.diag([np.exp(0.3j), 1.0]), C.mat_Y(), C.mat_X(),
+            C.mat_Rz(1.1), C.mat_U1(0.7)]
+    circ = C.h_wall(n)
+    circ.extend(C.layered(n, 1, seed=9, h_first=False))
+    for t in range(n):
+        for m in mats:
+            ctl = [] if t % 3 == 0 else ([(t + 5) % n] if t % 3 == 1 else [(t + 1) % n, (t + 7) % n])
+            circ.add("M", m, t, ctl)
+    ref = oracle.e_simulate(n, circ)
+    for fuse in (0, 1):
+        s = q.State(n, q.ENC_FP64, 1, fuse=fuse)
+        s.apply_circuit(circ)
+        assert np.max(np.abs(s.get_state() - ref)) <= TOL
+        s.close()
+
+
+def test_apply_gate_one_by_one_equals_circuit():
+    n = 13
+    circ = C.config(0, n=n, seed=4)
+    ref = oracle.e_simulate(n, circ)
+    with q.State(n) as s:
+        for g in range(len(circ)):
+            name, kind, t, t2, ctl, u = circ.gate(g)
+            s.apply_gate(u, t, ctl)
+        assert np.max(np.abs(s.get_state() - ref)) <= TOL
+
+
+def test_fused_layers_config2_shape():
+    """Config 2 recipe (H wall + layers of Haar on every qubit + CNOT matching) at
+    N = 20, fused vs unfused vs oracle."""
+    n = 20
+    circ = C.layered(n, 3, seed=1)
+    ref = oracle.e_simulate(n, circ)
+    for fuse in (1, 0):
+        s = q.State(n, q.ENC_FP64, 1, fuse=fuse)
+        s.apply_circuit(circ)
+        assert np.max(np.abs(s.get_state() - ref)) <= TOL
+        st = s.stats()
+        if fuse:
+            assert st["passes"] > 0 and st["fused_gates"] > len(circ) // 2
+        else:
+            assert st["passes"] == 0
+        s.close()
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_sharded_loopback_transparency(P):
+    """PAPER.md §3.2 / SPEC S:475: results independent of the shard count and
+    swap schedule (<= 1e-12); global-qubit gates go through the exchange."""
+    n = 14
+    circ = C.config(0, n=n, seed=P)
+    circ.extend(C.layered(n, 2, seed=P, h_first=False))
+    ref = oracle.e_simulate(n, circ)
+    s = q.State(n, q.ENC_FP64, P)
+    s.apply_circuit(circ)
+    got = s.get_state()
+    assert np.max(np.abs(got - ref)) <= TOL
+    st = s.stats()
+    assert st["exchanges"] > 0
+    # exchange volume: half a shard per direction per shard per exchange
+    assert st["exchange_bytes"] == pytest.approx(st["exchanges"] * (1 << (n - int(math.log2(P)) - 1)) * 16 * 2)
+    pe = s.expectations()
+    qe = oracle.e_expectations(ref, n)
+    assert np.max(np.abs(pe - qe)) <= TOL
+    assert np.max(np.abs(s.probabilities() - oracle.e_probabilities(ref, n))) <= TOL
+    s.close()
+
+
+def test_sharded_small_chunks_and_unfused():
+    n = 13
+    circ = C.layered(n, 2, seed=7)
+    ref = oracle.e_simulate(n, circ)
+    s = q.State(n, q.ENC_FP64, 4, chunk_bytes=4096, fuse=0)
+    s.apply_circuit(circ)
+    assert np.max(np.abs(s.get_state() - ref)) <= TOL
+    s.close()
+
+
+def test_local_gates_move_no_bytes_between_shards():
+    """gates on local qubits (and diagonal gates anywhere) never exchange."""
+    n = 14
+    s = q.State(n, q.ENC_FP64, 4)
+    c = C.Circuit(n)
+    for t in range(12):
+        c.add("H", C.mat_H(), t)
+    c.add("Z", C.mat_Z(), 13)
+    c.add("CP", C.mat_U1(0.4), 12, [13])
+    c.add("CNOT", C.mat_X(), 3, [13])  # global control, local target
+    s.apply_circuit(c)
+    assert s.stats()["exchanges"] == 0
+    assert np.max(np.abs(s.get_state() - oracle.e_simulate(n, c))) <= TOL
+    s.close()
+
+
+def test_expectations_probabilities_norm():
+    n = 12
+    circ = C.config(0, n=n, seed=11)
+    ref = oracle.e_simulate(n, circ)
+    with gpu_run(n, circ) as s:
+        assert np.max(np.abs(s.expectations() - oracle.e_expectations(ref, n))) <= TOL
+        assert np.max(np.abs(s.probabilities() - oracle.e_probabilities(ref, n))) <= TOL
+        assert abs(s.norm() - oracle.e_norm2(ref, n)) <= 1e-12
+
+
+def test_tables_2_3_on_gpu():
+    """Tables 2-3 on the GPU path."""
+    for circ, expect in [(C.h_wall(16), (0.0, 0.5, 0.5)), (C.ghz_chain(16), (0.5, 0.5, 0.5))]:
+        with gpu_run(16, circ, ngpus=2) as s:
+            assert np.max(np.abs(s.expectations() - np.array(expect)[None, :])) <= 1e-12
+
+
+@pytest.mark.parametrize("P", [1, 4])
+def test_measure(P):
+    n = 12
+    circ = C.config(0, n=n, seed=21)
+    ref = oracle.e_simulate(n, circ)
+    s = gpu_run(n, circ, ngpus=P)
+    for qubit, u in [(0, 0.3), (11, 0.9), (5, 0.5)]:
+        out, p0 = s.measure_u(qubit, u)
+        ro, rp0 = oracle.e_measure(ref, n, qubit, u)
+        assert out == ro and abs(p0 - rp0) <= 1e-12
+        assert np.max(np.abs(s.get_state() - ref)) <= TOL
+    # seeded variant: splitmix64 -> u = (x >> 11) 2^-53 (include/qsim.h)
+    out = s.measure(3, seed=12345)
+    assert out in (0, 1)
+    s.close()
+    z = q.State(4)
+    with pytest.raises(q.QsimError) as e:
+        z.measure_u(2, 1.0)
+    assert e.value.code == q.QSIM_EZERONORM
+
+
+def test_get_amplitudes_logical_indices():
+    n, P = 14, 4
+    circ = C.layered(n, 2, seed=2)
+    ref = oracle.e_simulate(n, circ)
+    with gpu_run(n, circ, ngpus=P) as s:
+        idx = np.random.default_rng(0).integers(0, 1 << n, 3000, dtype=np.uint64)
+        got = s.get_amplitudes(idx)
+        assert np.max(np.abs(got - ref[idx.astype(np.int64)])) <= TOL
+        assert s.qubit_map() != list(range(n))  # swaps were deferred, readout is logical
+
+
+def test_swap_is_relabel_and_set_state():
+    n = 11
+    rng = np.random.default_rng(5)
+    v = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    v /= np.linalg.norm(v)
+    with q.State(n) as s:
+        s.set_state(v)
+        s.apply_swap(0, 10)
+        s.apply_gate(C.mat_H(), 10)
+        ref = oracle.e_apply(oracle.e_swap(v.copy(), n, 0, 10), n, C.mat_H(), 10)
+        assert np.max(np.abs(s.get_state() - ref)) <= TOL
+        assert s.stats()["kernels"] >= 1
+
+
+def test_errors():
+    with pytest.raises(q.QsimError) as e:
+        q.State(1)
+    assert e.value.code == q.QSIM_EINVAL
+    with pytest.raises(q.QsimError):
+        q.State(12, q.ENC_FP64, 3)
+    with pytest.raises(q.QsimError):
+        q.State(12, q.ENC_FP64, 8)  # only 9 local qubits
+    with q.State(5) as s:
+        for bad in [lambda: s.apply_gate(C.mat_H(), 5), lambda: s.apply_gate(C.mat_H(), 1, [1]),
+                    lambda: s.apply_gate(C.mat_X(), 0, [1, 1])]:
+            with pytest.raises(q.QsimError) as e:
+                bad()
+            assert e.value.code == q.QSIM_EINVAL
+        with pytest.raises(q.QsimError) as e:
+            s.apply_gate(np.array([[1, 1], [0, 1]]), 0)
+        assert e.value.code == q.QSIM_ENOTUNITARY
+        assert np.max(np.abs(s.get_state() - oracle.e_init(5))) == 0  # failed calls changed nothing
+
+
+# ----------------------------------------------------------------------------- full size (BASELINE configs)
+
+
+@pytest.mark.slow
+def test_full_size_h_wall_and_qft_n30():
+    """N=30 (config 2 size): H wall and QFT closed forms on sampled amplitudes."""
+    n = 30
+    with q.State(n) as s:
+        s.apply_circuit(C.h_wall(n))
+        idx = np.random.default_rng(1).integers(0, 1 << n, 100000, dtype=np.uint64)
+        assert np.max(np.abs(s.get_amplitudes(idx) - 2.0 ** (-n / 2))) <= 1e-15
+        assert abs(s.norm() - 1) <= 1e-10
+    circ, x = C.qft(n, seed=5)
+    with q.State(n) as s:
+        s.apply_circuit(circ)
+        y = np.random.default_rng(2).integers(0, 1 << n, 100000, dtype=np.uint64)
+        ph = ((np.uint64(x) * y) % np.uint64(1 << n)).astype(np.float64) * (2 * math.pi / (1 << n))
+        assert np.max(np.abs(s.get_amplitudes(y) - 2.0 ** (-n / 2) * np.exp(1j * ph))) <= TOL
+        assert np.max(np.abs(s.probabilities() - 0.5)) <= 1e-12
+
+
+@pytest.mark.slow
+def test_full_size_config2_product_state_pin():
+    """Config 2 circuit at N=30 with the CNOTs removed (same U(2) draws): the
+    product-state closed form Eq. appa2 on 10^5 sampled amplitudes, in the
+    launch configuration bench.py times (fused passes)."""
+    n = 30
+    circ = C.layered(n, 20, seed=1, entangle=False)
+    v = [np.array([1, 0], dtype=np.complex128) for _ in range(n)]
+    for g in range(len(circ)):
+        _, _, t, _, _, u = circ.gate(g)
+        v[t] = u @ v[t]
+    V = np.array(v)  # (n, 2)
+    idx = np.random.default_rng(3).integers(0, 1 << n, 100000, dtype=np.uint64)
+    bits = ((idx[:, None] >> np.arange(n, dtype=np.uint64)[None, :]) & np.uint64(1)).astype(np.int64)
+    ref = np.prod(V[np.arange(n)[None, :], bits], axis=1)
+    with q.State(n) as s:
+        s.apply_circuit(circ)
+        assert np.max(np.abs(s.get_amplitudes(idx) - ref)) <= TOL
+        assert abs(s.norm() - 1) <= 1e-10
+        assert s.stats()["passes"] > 0
+
+
+@pytest.mark.slow
+def test_full_size_config2_vs_oracle_sampled():
+    """Config 2 recipe at its full size N=30 (CNOTs kept, 2 of the 20 layers so
+    the host oracle finishes in about a minute): GPU vs the oracle's full
+    16 GiB state on 10^6 sampled amplitudes and the norm."""
+    n = 30
+    circ = C.layered(n, 2, seed=1)
+    idx = np.random.default_rng(4).integers(0, 1 << n, 1000000, dtype=np.uint64)
+    with q.State(n) as s:
+        s.apply_circuit(circ)
+        got = s.get_amplitudes(idx)
+        nrm = s.norm()
+    ref = oracle.e_simulate(n, circ)
+    assert np.max(np.abs(got - ref[idx.astype(np.int64)])) <= TOL
+    assert abs(nrm - 1) <= 1e-10

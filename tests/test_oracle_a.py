@@ -11,7 +11,7 @@ import numpy as np
 import pytest
 
 import oracle
-from paper_1805_04708_b200 import circuits as C
+import qsim_inputs as C
 
 
 def test_worked_examples():

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 import oracle
-from paper_1805_04708_b200 import circuits as C
+import qsim_inputs as C
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 
