@@ -203,40 +203,90 @@ static int sweep_gate_e(qsim_state *s, const PlanOp &o, const double *u) {
 // fused tile passes (a6)
 // ============================================================================
 struct PassBuild {
-    std::vector<int> ops;      // indices into the run
+    std::vector<int> ops;      // indices into the run, in execution order
     std::vector<int> high;     // local qubits >= PASS_LOW needed in the tile
     std::vector<std::vector<int>> stage_q;     // per stage: register qubits (local qubit ids)
     std::vector<std::vector<int>> stage_ops;   // per stage: op indices
 };
 
+// Qubits a gate acts on non-diagonally (X-type: the target of a dense /
+// anti-diagonal gate) and diagonally (Z-type: controls, diagonal targets).
+// Two gates commute if every shared qubit is Z-type for both.
+static void gate_masks(const PlanOp &o, uint64_t &xq, uint64_t &zq) {
+    xq = zq = 0;
+    if (o.cls == CLS_DIAG)
+        zq |= 1ull << o.l;
+    else
+        xq |= 1ull << o.l;
+    for (int c = 0; c < o.nctrl; ++c) zq |= 1ull << o.ctrl[c];
+}
+
+// Try to append op `idx` to the pass (tile capacity only); false (no change)
+// if it does not fit.  Stages are formed afterwards by stage_pass().
 static bool pass_add(PassBuild &pb, const PlanOp &o, int idx, int hmax) {
-    bool needs_reg = o.cls != CLS_DIAG;
-    std::vector<int> high = pb.high;
-    if (needs_reg && o.l >= PASS_LOW && std::find(high.begin(), high.end(), o.l) == high.end()) {
-        if ((int)high.size() >= hmax) return false;
-        high.push_back(o.l);
-    }
+    const bool needs_reg = o.cls != CLS_DIAG;
     if ((int)pb.ops.size() >= PASS_MAX_GATES) return false;
-    // stage placement
-    if (pb.stage_q.empty()) {
-        pb.stage_q.emplace_back();
-        pb.stage_ops.emplace_back();
-    }
-    if (needs_reg) {
-        auto &R = pb.stage_q.back();
-        if (std::find(R.begin(), R.end(), o.l) == R.end()) {
-            if ((int)R.size() >= PASS_R) {
-                if ((int)pb.stage_q.size() >= PASS_MAX_STAGES) return false;
-                pb.stage_q.emplace_back();
-                pb.stage_ops.emplace_back();
-            }
-            pb.stage_q.back().push_back(o.l);
-        }
-    }
-    pb.stage_ops.back().push_back(idx);
+    bool new_high = needs_reg && o.l >= PASS_LOW && std::find(pb.high.begin(), pb.high.end(), o.l) == pb.high.end();
+    if (new_high && (int)pb.high.size() >= hmax) return false;
+    if (new_high) pb.high.push_back(o.l);
     pb.ops.push_back(idx);
-    pb.high = high;
     return true;
+}
+
+// Split a pass into register stages (<= PASS_R register qubits each) with the
+// same commutation-aware greedy as the pass scheduler: each stage takes, in
+// order, every remaining gate that commutes with all skipped earlier gates and
+// whose target fits the register set.  Returns false if more than
+// PASS_MAX_STAGES stages are needed (the caller then shortens the pass).
+static bool stage_pass(PassBuild &pb, const std::vector<PlanOp> &run) {
+    pb.stage_q.clear();
+    pb.stage_ops.clear();
+    std::vector<int> rem = pb.ops, order;
+    while (!rem.empty()) {
+        if ((int)pb.stage_q.size() >= PASS_MAX_STAGES) return false;
+        std::vector<int> R, taken, left;
+        uint64_t bx = 0, bz = 0;
+        for (int k : rem) {
+            const PlanOp &o = run[k];
+            uint64_t xq, zq;
+            gate_masks(o, xq, zq);
+            bool ok = !((xq & (bx | bz)) || (zq & bx));
+            if (ok && o.cls != CLS_DIAG && std::find(R.begin(), R.end(), o.l) == R.end()) {
+                if ((int)R.size() < PASS_R)
+                    R.push_back(o.l);
+                else
+                    ok = false;
+            }
+            if (ok) {
+                taken.push_back(k);
+            } else {
+                bx |= xq;
+                bz |= zq;
+                left.push_back(k);
+            }
+        }
+        pb.stage_q.push_back(R);
+        pb.stage_ops.push_back(taken);
+        for (int k : taken) order.push_back(k);
+        rem.swap(left);
+    }
+    pb.ops = order;
+    return true;
+}
+
+static void cmatmul2(const double *a, const double *b, double *c) {  // c = a * b (2x2 complex)
+    for (int r = 0; r < 2; ++r)
+        for (int k = 0; k < 2; ++k) {
+            double re = 0.0, im = 0.0;
+            for (int m = 0; m < 2; ++m) {
+                double ar = a[(r * 2 + m) * 2], ai = a[(r * 2 + m) * 2 + 1];
+                double br = b[(m * 2 + k) * 2], bi = b[(m * 2 + k) * 2 + 1];
+                re += ar * br - ai * bi;
+                im += ar * bi + ai * br;
+            }
+            c[(r * 2 + k) * 2] = re;
+            c[(r * 2 + k) * 2 + 1] = im;
+        }
 }
 
 static int launch_pass(qsim_state *s, const PassBuild &pb, const std::vector<PlanOp> &run,
@@ -285,10 +335,30 @@ static int launch_pass(qsim_state *s, const PassBuild &pb, const std::vector<Pla
         for (int b : rest) gb.push_back(b);
         for (int i = 0; i < K - PASS_R; ++i) st.gbits[i] = (int8_t)gb[i];
         st.first_gate = (int8_t)gi;
-        st.ngates = (int8_t)pb.stage_ops[si].size();
+        // last gate (index into p.g) touching each local qubit in this stage, for merging
+        int last_on[64];
+        for (int k2 = 0; k2 < 64; ++k2) last_on[k2] = -1;
+        std::vector<int> merged_ok;  // per gate in this stage: uncontrolled (mergeable)
         for (int oi : pb.stage_ops[si]) {
             const PlanOp &o = run[oi];
-            PassGate &g = p.g[gi++];
+            // merge an uncontrolled gate into the previous uncontrolled gate on the
+            // same target when no gate in between touched that qubit
+            if (o.nctrl == 0 && last_on[o.l] >= 0 && merged_ok[last_on[o.l] - st.first_gate]) {
+                PassGate &m = p.g[last_on[o.l]];
+                double prod[8];
+                cmatmul2(us[oi], m.u, prod);
+                std::memcpy(m.u, prod, sizeof(prod));
+                bool off0 = prod[2] == 0.0 && prod[3] == 0.0 && prod[4] == 0.0 && prod[5] == 0.0;
+                bool dia0 = prod[0] == 0.0 && prod[1] == 0.0 && prod[6] == 0.0 && prod[7] == 0.0;
+                if ((m.kind & 3) != PG_DIAG_OUT || m.kind == PG_SWAP || m.kind == PG_SWAP + PG_PARTIAL) {
+                    int base_kind = off0 ? PG_DIAG_IN : (dia0 ? PG_ANTI : PG_DENSE);
+                    if (dia0 && prod[2] == 1.0 && prod[3] == 0.0 && prod[4] == 1.0 && prod[5] == 0.0) base_kind = PG_SWAP;
+                    m.kind = (int8_t)(base_kind | (m.kind & PG_PARTIAL));
+                }
+                // a DIAG_OUT gate only merges with diagonal gates (target outside the registers)
+                continue;
+            }
+            PassGate &g = p.g[gi];
             std::memcpy(g.u, us[oi], sizeof(g.u));
             int8_t cslot = 0;
             uint64_t cout = 0;
@@ -304,27 +374,49 @@ static int launch_pass(qsim_state *s, const PassBuild &pb, const std::vector<Pla
             }
             g.cslot = cslot;
             g.cmask_out = cout;
+            if (cout) st.needs_full = 1;
             int ttb = (o.l < s->nl) ? tile_bit(o.l) : -1;
             int tslot = -1;
             for (int r = 0; r < PASS_R; ++r)
                 if (ttb >= 0 && R[r] == ttb) tslot = r;
+            int kind;
             if (o.cls == CLS_DIAG) {
                 if (tslot >= 0) {
-                    g.kind = PG_DIAG_IN;
+                    kind = PG_DIAG_IN;
                     g.slot = (int8_t)tslot;
                 } else {
-                    g.kind = PG_DIAG_OUT;
+                    kind = PG_DIAG_OUT;
                     g.tmask_out = 1ull << o.l;
+                    st.needs_full = 1;
                 }
             } else {
                 if (tslot < 0) {
                     set_error("internal: pass target not in register set");
                     return QSIM_EINVAL;
                 }
-                g.kind = (o.cls == CLS_ANTI) ? PG_ANTI : PG_DENSE;
+                kind = (o.cls == CLS_ANTI) ? PG_ANTI : PG_DENSE;
+                const double *uu = us[oi];
+                if (o.cls == CLS_ANTI && uu[2] == 1.0 && uu[3] == 0.0 && uu[4] == 1.0 && uu[5] == 0.0) kind = PG_SWAP;
                 g.slot = (int8_t)tslot;
             }
+            if (cslot) {
+                // a register permutation under an in-register control cannot be a
+                // slot flip: apply it as (exact) dense arithmetic
+                if (kind == PG_ANTI || kind == PG_SWAP) kind = PG_DENSE;
+                kind |= PG_PARTIAL;
+            }
+            g.kind = (int8_t)kind;
+            merged_ok.push_back(o.nctrl == 0 && o.l < s->nl ? 1 : 0);
+            if (o.l < 64) last_on[o.l] = gi;
+            for (int c = 0; c < o.nctrl; ++c)
+                if (o.ctrl[c] < 64) {
+                    // a control use blocks merging across it
+                    if (last_on[o.ctrl[c]] >= 0) merged_ok[last_on[o.ctrl[c]] - st.first_gate] = 0;
+                    last_on[o.ctrl[c]] = -1;
+                }
+            ++gi;
         }
+        st.ngates = (int8_t)(gi - st.first_gate);
     }
     int grid = (int)std::min<uint64_t>(p.ntiles, (uint64_t)pass_e_max_grid());
     for (auto &sh : s->shards) {
@@ -342,30 +434,55 @@ static int launch_pass(qsim_state *s, const PassBuild &pb, const std::vector<Pla
     return QSIM_OK;
 }
 
+// Greedy commutation-aware pass scheduler (a6): each pass takes, in circuit
+// order, every not-yet-applied gate that commutes with all earlier skipped
+// gates and fits the tile (<= K - PASS_LOW high target qubits, <= PASS_MAX_*).
 static int run_gates_e(qsim_state *s, const std::vector<PlanOp> &run, const std::vector<const double *> &us) {
-    size_t i = 0;
     const int K = std::min(PASS_MAX_K, s->nl);
     const bool can_fuse = s->fuse && K >= PASS_MIN_K;
-    while (i < run.size()) {
-        if (!can_fuse) {
-            RC(sweep_gate_e(s, run[i], us[i]));
-            ++i;
-            continue;
-        }
+    if (!can_fuse) {
+        for (size_t i = 0; i < run.size(); ++i) RC(sweep_gate_e(s, run[i], us[i]));
+        return QSIM_OK;
+    }
+    std::vector<char> done(run.size(), 0);
+    size_t first = 0;
+    const double pass_bytes = std::ldexp(2.0 * (double)s->amp_bytes, s->nl);
+    while (first < run.size()) {
         PassBuild pb;
-        size_t j = i;
-        while (j < run.size() && pass_add(pb, run[j], (int)j, K - PASS_LOW)) ++j;
-        // cost model: one pass (32 B/amp) vs the sweeps' own bytes on shard 0
+        uint64_t bx = 0, bz = 0;
+        for (size_t k = first; k < run.size(); ++k) {
+            if (done[k]) continue;
+            uint64_t xq, zq;
+            gate_masks(run[k], xq, zq);
+            const bool conflict = (xq & (bx | bz)) || (zq & bx);
+            if (!conflict && pass_add(pb, run[k], (int)k, K - PASS_LOW)) {
+                done[k] = 1;
+            } else {
+                bx |= xq;
+                bz |= zq;
+            }
+            if ((int)pb.ops.size() >= PASS_MAX_GATES) break;
+        }
+        // form register stages; if the pass needs too many, give back its last gates
+        while (!stage_pass(pb, run)) {
+            int k = pb.ops.back();
+            pb.ops.pop_back();
+            done[k] = 0;
+            if (k < (int)first) first = k;
+            pb.high.clear();
+            for (int k2 : pb.ops)
+                if (run[k2].cls != CLS_DIAG && run[k2].l >= PASS_LOW &&
+                    std::find(pb.high.begin(), pb.high.end(), run[k2].l) == pb.high.end())
+                    pb.high.push_back(run[k2].l);
+        }
         double sweep_bytes = 0.0;
-        for (size_t k = i; k < j; ++k) sweep_bytes += gate_bytes_alone(s, s->shards[0], run[k], us[k]);
-        double pass_bytes = std::ldexp(2.0 * (double)s->amp_bytes, s->nl);
-        if (j - i >= 2 && pass_bytes < sweep_bytes) {
-            // rebase op indices to the run (pass_add stored absolute indices)
+        for (int k : pb.ops) sweep_bytes += gate_bytes_alone(s, s->shards[0], run[k], us[k]);
+        if (pb.ops.size() >= 2 && pass_bytes < sweep_bytes) {
             RC(launch_pass(s, pb, run, us));
         } else {
-            for (size_t k = i; k < j; ++k) RC(sweep_gate_e(s, run[k], us[k]));
+            for (int k : pb.ops) RC(sweep_gate_e(s, run[k], us[k]));
         }
-        i = j;
+        while (first < run.size() && done[first]) ++first;
     }
     return QSIM_OK;
 }

@@ -39,15 +39,17 @@ struct ScaleParams {
 void launch_scale_e(const ScaleParams &p, cudaStream_t s);
 
 // ---- fused tile pass (a6) ----------------------------------------------------
-constexpr int PASS_LOW = 5;       // tile always holds qubits 0..4 (512 B contiguous runs)
+constexpr int PASS_LOW = 3;       // tile always holds qubits 0..2 (128 B contiguous runs = one L2 line)
 constexpr int PASS_MAX_K = 12;    // 2^12 amplitudes x 16 B = 64 KiB of shared memory per CTA
 constexpr int PASS_MIN_K = 9;
 constexpr int PASS_R = 4;         // qubits held in registers per stage (16 amplitudes per thread)
 constexpr int PASS_THREADS = 128;
-constexpr int PASS_MAX_GATES = 24;
-constexpr int PASS_MAX_STAGES = 12;
+constexpr int PASS_MAX_GATES = 32;
+constexpr int PASS_MAX_STAGES = 16;
 
 enum PassGateKind : int8_t { PG_DENSE = 0, PG_DIAG_IN = 1, PG_ANTI = 2, PG_DIAG_OUT = 3 };
+constexpr int PG_SWAP = 8;  // kind value: anti-diagonal with u01 = u10 = 1 (X, CNOT, TOFFOLI): a pure register swap
+constexpr int PG_PARTIAL = 4;  // kind flag: some controls sit in the register set (per-slot predicate)
 
 struct PassGate {
     double u[8];
@@ -64,7 +66,8 @@ struct PassStage {
     int8_t gbits[PASS_MAX_K - PASS_R];  // group index bit i <-> tile bit gbits[i]
     int8_t first_gate;
     int8_t ngates;
-    int8_t pad[2];
+    int8_t needs_full;   // some gate of the stage tests bits outside the register set
+    int8_t pad;
 };
 
 struct PassParams {

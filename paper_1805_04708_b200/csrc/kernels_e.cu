@@ -146,45 +146,93 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-template <int S>
-__device__ __forceinline__ void pg_dense(double2 (&v)[16], const PassGate &g, bool gok, int cslot) {
-    const double u0r = g.u[0], u0i = g.u[1], u1r = g.u[2], u1i = g.u[3];
-    const double u2r = g.u[4], u2i = g.u[5], u3r = g.u[6], u3i = g.u[7];
+// In-place pair updates.  Each output's final FMA is the last use of exactly
+// one input, so the register allocator can write every output over its own
+// input: no register copies at the gate-dispatch merge points (the loop over a
+// stage's gates is a runtime switch).
+//   x' = u00 x + u01 y,  y' = u10 x + u11 y   (u = {u00r,u00i,u01r,u01i,u10r,u10i,u11r,u11i})
+__device__ __forceinline__ void pair_dense(double2 &x, double2 &y, const double (&u)[8]) {
+    const double p0 = fma(u[2], y.x, fma(-u[1], x.y, -u[3] * y.y));  // x'.re - u00r x.re
+    const double p1 = fma(u[2], y.y, fma(u[1], x.x, u[3] * y.x));    // x'.im - u00r x.im
+    const double p2 = fma(u[4], x.x, fma(-u[5], x.y, -u[7] * y.y));  // y'.re - u11r y.re
+    const double p3 = fma(u[4], x.y, fma(u[5], x.x, u[7] * y.x));    // y'.im - u11r y.im
+    x.x = fma(u[0], x.x, p0);
+    x.y = fma(u[0], x.y, p1);
+    y.x = fma(u[6], y.x, p2);
+    y.y = fma(u[6], y.y, p3);
+}
+__device__ __forceinline__ void amp_phase(double2 &x, double ur, double ui) {
+    const double p = -ui * x.y, q = ui * x.x;
+    x.x = fma(ur, x.x, p);
+    x.y = fma(ur, x.y, q);
+}
+
+// Gate application on the 16 register-resident amplitudes of one group.
+// `f` is the group's slot-flip mask: register j holds the amplitude of
+// logical slot j ^ f.  An uncontrolled X / CNOT-like swap on slot S is applied
+// as f ^= 2^S (no data moves); later gates of the stage select conjugated
+// coefficients for flipped slots and the stage's store XORs f into the
+// (GF(2)-linear) smem address.  Every update is in place, so the register
+// allocator never copies the 16 amplitudes at the gate-dispatch merge points.
+// FULL: no control inside the register set.
+template <int S, bool FULL>
+__device__ __forceinline__ void pg_dense(double2 (&v)[16], const PassGate &g, int cslot, uint32_t f) {
+    // flipped target slot: registers hold (y, x), apply X U X, i.e. entry k -> k ^ 6
+    const int fx = ((f >> S) & 1u) ? 6 : 0;
+    double u[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) u[k] = g.u[k ^ fx];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
         if (j & (1 << S)) continue;
-        if (!gok || (j & cslot) != cslot) continue;
-        const int j1 = j | (1 << S);
-        double2 x = v[j], y = v[j1];
-        v[j] = cmad2(u0r, u0i, x, u1r, u1i, y);
-        v[j1] = cmad2(u2r, u2i, x, u3r, u3i, y);
+        if (!FULL && (((uint32_t)j ^ f) & cslot) != (uint32_t)cslot) continue;
+        pair_dense(v[j], v[j | (1 << S)], u);
     }
 }
-template <int S>
-__device__ __forceinline__ void pg_anti(double2 (&v)[16], const PassGate &g, bool gok, int cslot) {
-    const double u1r = g.u[2], u1i = g.u[3], u2r = g.u[4], u2i = g.u[5];
+// diagonal on slot S: logical bit 0 -> (a0r, a0i), logical bit 1 -> (a1r, a1i)
+template <int S, bool FULL>
+__device__ __forceinline__ void pg_phase(double2 (&v)[16], double a0r, double a0i, double a1r, double a1i, int cslot,
+                                         uint32_t f) {
+    const bool fl = (f >> S) & 1u;
+    const double r0 = fl ? a1r : a0r, i0 = fl ? a1i : a0i;  // registers with bit S = 0
+    const double r1 = fl ? a0r : a1r, i1 = fl ? a0i : a1i;  // registers with bit S = 1
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-        if (j & (1 << S)) continue;
-        if (!gok || (j & cslot) != cslot) continue;
-        const int j1 = j | (1 << S);
-        double2 x = v[j], y = v[j1];
-        v[j] = cmul(u1r, u1i, y);
-        v[j1] = cmul(u2r, u2i, x);
-    }
-}
-template <int S>
-__device__ __forceinline__ void pg_diag(double2 (&v)[16], const PassGate &g, bool gok, int cslot) {
-    const double u0r = g.u[0], u0i = g.u[1], u3r = g.u[6], u3i = g.u[7];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        if (!gok || (j & cslot) != cslot) continue;
+        if (!FULL && (((uint32_t)j ^ f) & cslot) != (uint32_t)cslot) continue;
         if (j & (1 << S))
-            v[j] = cmul(u3r, u3i, v[j]);
+            amp_phase(v[j], r1, i1);
         else
-            v[j] = cmul(u0r, u0i, v[j]);
+            amp_phase(v[j], r0, i0);
     }
 }
+template <int S, bool FULL>
+__device__ __forceinline__ void pg_diag(double2 (&v)[16], const PassGate &g, int cslot, uint32_t f) {
+    pg_phase<S, FULL>(v, g.u[0], g.u[1], g.u[6], g.u[7], cslot, f);
+}
+template <bool FULL>
+__device__ __forceinline__ void pg_diag_out(double2 (&v)[16], double fr, double fi, int cslot, uint32_t f) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        if (!FULL && (((uint32_t)j ^ f) & cslot) != (uint32_t)cslot) continue;
+        amp_phase(v[j], fr, fi);
+    }
+}
+template <int S>
+__device__ __forceinline__ void pg_anti_full(double2 (&v)[16], const PassGate &g, uint32_t &f) {
+    // x' = u01 y, y' = u10 x: flip slot S, then logical bit 0 gets u01, bit 1 gets u10
+    f ^= 1u << S;
+    pg_phase<S, true>(v, g.u[2], g.u[3], g.u[4], g.u[5], 0, f);
+}
+
+#define PG_CASES(KIND, FN)                                                   \
+    case (KIND) * 4 + 0: FN<0, true>(v, g, cs, f); break;                    \
+    case (KIND) * 4 + 1: FN<1, true>(v, g, cs, f); break;                    \
+    case (KIND) * 4 + 2: FN<2, true>(v, g, cs, f); break;                    \
+    case (KIND) * 4 + 3: FN<3, true>(v, g, cs, f); break;                    \
+    case ((KIND) + PG_PARTIAL) * 4 + 0: FN<0, false>(v, g, cs, f); break;    \
+    case ((KIND) + PG_PARTIAL) * 4 + 1: FN<1, false>(v, g, cs, f); break;    \
+    case ((KIND) + PG_PARTIAL) * 4 + 2: FN<2, false>(v, g, cs, f); break;    \
+    case ((KIND) + PG_PARTIAL) * 4 + 3: FN<3, false>(v, g, cs, f); break;
 
 __global__ void __launch_bounds__(PASS_THREADS, 3) k_pass_e(const __grid_constant__ PassParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -203,14 +251,15 @@ __global__ void __launch_bounds__(PASS_THREADS, 3) k_pass_e(const __grid_constan
     double2 *__restrict__ a = reinterpret_cast<double2 *>(p.a);
     const uint32_t tid = threadIdx.x;
     const uint32_t ngroups = tsize >> PASS_R;
+    constexpr uint32_t LOWM = (1u << PASS_LOW) - 1u;
 
     for (uint64_t T = blockIdx.x; T < p.ntiles; T += gridDim.x) {
-        // base: insert zeros at the tile's qubits (0..4 and high_q ascending)
+        // base: insert zeros at the tile's qubits (0..PASS_LOW-1 and high_q ascending)
         uint64_t base = T << PASS_LOW;
         for (int i = 0; i < h; ++i) base = insert_zero(base, p.high_q[i]);
-        // ---- load the tile (coalesced 512 B runs) ----
+        // ---- load the tile (coalesced 128 B runs) ----
         for (uint32_t x = tid; x < tsize; x += PASS_THREADS) {
-            uint64_t off = (x & 31u) | dep[x >> PASS_LOW];
+            uint64_t off = (x & LOWM) | dep[x >> PASS_LOW];
             cp_async16(&tile[swz(x)], &a[base | off]);
         }
         cp_async_wait_all();
@@ -218,62 +267,66 @@ __global__ void __launch_bounds__(PASS_THREADS, 3) k_pass_e(const __grid_constan
         // ---- stages ----
         for (int s = 0; s < p.nstages; ++s) {
             const PassStage &st = p.st[s];
-            uint32_t rmask[PASS_R];
-#pragma unroll
-            for (int r = 0; r < PASS_R; ++r) rmask[r] = 1u << st.rbits[r];
+            // swz is linear over GF(2): swz(x0 | slot bits) = swz(x0) ^ xor of swz(slot bit)
+            const uint32_t b0 = swz(1u << st.rbits[0]), b1 = swz(1u << st.rbits[1]);
+            const uint32_t b2 = swz(1u << st.rbits[2]), b3 = swz(1u << st.rbits[3]);
             for (uint32_t grp = tid; grp < ngroups; grp += PASS_THREADS) {
                 uint32_t x0 = 0;
-                for (int i = 0; i < K - PASS_R; ++i)
-                    if (grp & (1u << i)) x0 |= 1u << st.gbits[i];
-                const uint64_t full0 = p.shard_base | base | (x0 & 31u) | dep[x0 >> PASS_LOW];
+                for (int i = 0; i < K - PASS_R; ++i) x0 |= ((grp >> i) & 1u) << st.gbits[i];
+                const uint32_t sx0 = swz(x0);
+                uint64_t full0 = 0;
+                if (st.needs_full) full0 = p.shard_base | base | (x0 & LOWM) | dep[x0 >> PASS_LOW];
                 double2 v[16];
-                uint32_t xs[16];
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
-                    uint32_t x = x0;
-#pragma unroll
-                    for (int r = 0; r < PASS_R; ++r)
-                        if (j & (1 << r)) x |= rmask[r];
-                    xs[j] = swz(x);
-                    v[j] = tile[xs[j]];
+                    const uint32_t xs = sx0 ^ ((j & 1) ? b0 : 0u) ^ ((j & 2) ? b1 : 0u) ^ ((j & 4) ? b2 : 0u) ^
+                                        ((j & 8) ? b3 : 0u);
+                    v[j] = tile[xs];
                 }
+                uint32_t f = 0;
                 for (int gi = st.first_gate; gi < st.first_gate + st.ngates; ++gi) {
                     const PassGate &g = p.g[gi];
-                    const bool gok = (full0 & g.cmask_out) == g.cmask_out;
+                    if ((full0 & g.cmask_out) != g.cmask_out) continue;
                     const int cs = g.cslot;
-                    if (g.kind == PG_DIAG_OUT) {
-                        if (!gok) continue;
-                        const bool bit = (full0 & g.tmask_out) != 0;
-                        const double fr = bit ? g.u[6] : g.u[0], fi = bit ? g.u[7] : g.u[1];
-#pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            if ((j & cs) == cs) v[j] = cmul(fr, fi, v[j]);
+                    const int kind = g.kind;
+                    if (kind == PG_SWAP) {  // uncontrolled (in-register) swap: flip the slot
+                        f ^= 1u << g.slot;
                         continue;
                     }
-                    switch (g.kind * 4 + g.slot) {
-                        case PG_DENSE * 4 + 0: pg_dense<0>(v, g, gok, cs); break;
-                        case PG_DENSE * 4 + 1: pg_dense<1>(v, g, gok, cs); break;
-                        case PG_DENSE * 4 + 2: pg_dense<2>(v, g, gok, cs); break;
-                        case PG_DENSE * 4 + 3: pg_dense<3>(v, g, gok, cs); break;
-                        case PG_DIAG_IN * 4 + 0: pg_diag<0>(v, g, gok, cs); break;
-                        case PG_DIAG_IN * 4 + 1: pg_diag<1>(v, g, gok, cs); break;
-                        case PG_DIAG_IN * 4 + 2: pg_diag<2>(v, g, gok, cs); break;
-                        case PG_DIAG_IN * 4 + 3: pg_diag<3>(v, g, gok, cs); break;
-                        case PG_ANTI * 4 + 0: pg_anti<0>(v, g, gok, cs); break;
-                        case PG_ANTI * 4 + 1: pg_anti<1>(v, g, gok, cs); break;
-                        case PG_ANTI * 4 + 2: pg_anti<2>(v, g, gok, cs); break;
-                        case PG_ANTI * 4 + 3: pg_anti<3>(v, g, gok, cs); break;
+                    if ((kind & 3) == PG_DIAG_OUT) {
+                        const bool bit = (full0 & g.tmask_out) != 0;
+                        const double fr = bit ? g.u[6] : g.u[0], fi = bit ? g.u[7] : g.u[1];
+                        if (kind & PG_PARTIAL)
+                            pg_diag_out<false>(v, fr, fi, cs, f);
+                        else
+                            pg_diag_out<true>(v, fr, fi, cs, f);
+                        continue;
+                    }
+                    switch (kind * 4 + g.slot) {
+                        PG_CASES(PG_DENSE, pg_dense)
+                        PG_CASES(PG_DIAG_IN, pg_diag)
+                        case PG_ANTI * 4 + 0: pg_anti_full<0>(v, g, f); break;
+                        case PG_ANTI * 4 + 1: pg_anti_full<1>(v, g, f); break;
+                        case PG_ANTI * 4 + 2: pg_anti_full<2>(v, g, f); break;
+                        case PG_ANTI * 4 + 3: pg_anti_full<3>(v, g, f); break;
                         default: break;
                     }
                 }
+                // register j holds logical slot j ^ f: store to swz(x0 | slots(j ^ f))
+                const uint32_t sxf = sx0 ^ ((f & 1) ? b0 : 0u) ^ ((f & 2) ? b1 : 0u) ^ ((f & 4) ? b2 : 0u) ^
+                                     ((f & 8) ? b3 : 0u);
 #pragma unroll
-                for (int j = 0; j < 16; ++j) tile[xs[j]] = v[j];
+                for (int j = 0; j < 16; ++j) {
+                    const uint32_t xs = sxf ^ ((j & 1) ? b0 : 0u) ^ ((j & 2) ? b1 : 0u) ^ ((j & 4) ? b2 : 0u) ^
+                                        ((j & 8) ? b3 : 0u);
+                    tile[xs] = v[j];
+                }
             }
             __syncthreads();
         }
         // ---- store the tile ----
         for (uint32_t x = tid; x < tsize; x += PASS_THREADS) {
-            uint64_t off = (x & 31u) | dep[x >> PASS_LOW];
+            uint64_t off = (x & LOWM) | dep[x >> PASS_LOW];
             a[base | off] = tile[swz(x)];
         }
         __syncthreads();
