@@ -45,7 +45,7 @@ constexpr int PASS_MIN_K = 9;
 constexpr int PASS_R = 4;         // qubits held in registers per stage (16 amplitudes per thread)
 constexpr int PASS_THREADS = 128;
 constexpr int PASS_MAX_GATES = 32;
-constexpr int PASS_MAX_STAGES = 16;
+constexpr int PASS_MAX_STAGES = 12;  // smem: 64 KiB tile + 3 KiB gates + 6 KiB group table < 75 KiB (3 CTAs/SM)
 
 enum PassGateKind : int8_t { PG_DENSE = 0, PG_DIAG_IN = 1, PG_ANTI = 2, PG_DIAG_OUT = 3 };
 constexpr int PG_SWAP = 8;  // kind value: anti-diagonal with u01 = u10 = 1 (X, CNOT, TOFFOLI): a pure register swap

@@ -167,6 +167,14 @@ __device__ __forceinline__ void amp_phase(double2 &x, double ur, double ui) {
     x.y = fma(ur, x.y, q);
 }
 
+// Gate table entry as staged in shared memory (one LDS.128 per complex entry).
+struct SmGate {
+    double2 u[4];        // u00, u01, u10, u11
+    uint64_t cmask_out;
+    uint64_t tmask_out;
+    int32_t kind, slot, cslot, pad;
+};
+
 // Gate application on the 16 register-resident amplitudes of one group.
 // `f` is the group's slot-flip mask: register j holds the amplitude of
 // logical slot j ^ f.  An uncontrolled X / CNOT-like swap on slot S is applied
@@ -176,12 +184,11 @@ __device__ __forceinline__ void amp_phase(double2 &x, double ur, double ui) {
 // allocator never copies the 16 amplitudes at the gate-dispatch merge points.
 // FULL: no control inside the register set.
 template <int S, bool FULL>
-__device__ __forceinline__ void pg_dense(double2 (&v)[16], const PassGate &g, int cslot, uint32_t f) {
-    // flipped target slot: registers hold (y, x), apply X U X, i.e. entry k -> k ^ 6
-    const int fx = ((f >> S) & 1u) ? 6 : 0;
-    double u[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) u[k] = g.u[k ^ fx];
+__device__ __forceinline__ void pg_dense(double2 (&v)[16], const SmGate &g, int cslot, uint32_t f) {
+    // flipped target slot: registers hold (y, x): apply X U X (complex entry c -> c ^ 3)
+    const int cx = ((f >> S) & 1u) ? 3 : 0;
+    const double2 e0 = g.u[0 ^ cx], e1 = g.u[1 ^ cx], e2 = g.u[2 ^ cx], e3 = g.u[3 ^ cx];
+    const double u[8] = {e0.x, e0.y, e1.x, e1.y, e2.x, e2.y, e3.x, e3.y};
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
         if (j & (1 << S)) continue;
@@ -189,39 +196,38 @@ __device__ __forceinline__ void pg_dense(double2 (&v)[16], const PassGate &g, in
         pair_dense(v[j], v[j | (1 << S)], u);
     }
 }
-// diagonal on slot S: logical bit 0 -> (a0r, a0i), logical bit 1 -> (a1r, a1i)
+// diagonal on slot S: logical bit 0 -> a0, logical bit 1 -> a1
 template <int S, bool FULL>
-__device__ __forceinline__ void pg_phase(double2 (&v)[16], double a0r, double a0i, double a1r, double a1i, int cslot,
-                                         uint32_t f) {
+__device__ __forceinline__ void pg_phase(double2 (&v)[16], double2 a0, double2 a1, int cslot, uint32_t f) {
     const bool fl = (f >> S) & 1u;
-    const double r0 = fl ? a1r : a0r, i0 = fl ? a1i : a0i;  // registers with bit S = 0
-    const double r1 = fl ? a0r : a1r, i1 = fl ? a0i : a1i;  // registers with bit S = 1
+    const double2 c0 = fl ? a1 : a0;  // registers with bit S = 0
+    const double2 c1 = fl ? a0 : a1;  // registers with bit S = 1
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
         if (!FULL && (((uint32_t)j ^ f) & cslot) != (uint32_t)cslot) continue;
         if (j & (1 << S))
-            amp_phase(v[j], r1, i1);
+            amp_phase(v[j], c1.x, c1.y);
         else
-            amp_phase(v[j], r0, i0);
+            amp_phase(v[j], c0.x, c0.y);
     }
 }
 template <int S, bool FULL>
-__device__ __forceinline__ void pg_diag(double2 (&v)[16], const PassGate &g, int cslot, uint32_t f) {
-    pg_phase<S, FULL>(v, g.u[0], g.u[1], g.u[6], g.u[7], cslot, f);
+__device__ __forceinline__ void pg_diag(double2 (&v)[16], const SmGate &g, int cslot, uint32_t f) {
+    pg_phase<S, FULL>(v, g.u[0], g.u[3], cslot, f);
 }
 template <bool FULL>
-__device__ __forceinline__ void pg_diag_out(double2 (&v)[16], double fr, double fi, int cslot, uint32_t f) {
+__device__ __forceinline__ void pg_diag_out(double2 (&v)[16], double2 c, int cslot, uint32_t f) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
         if (!FULL && (((uint32_t)j ^ f) & cslot) != (uint32_t)cslot) continue;
-        amp_phase(v[j], fr, fi);
+        amp_phase(v[j], c.x, c.y);
     }
 }
 template <int S>
-__device__ __forceinline__ void pg_anti_full(double2 (&v)[16], const PassGate &g, uint32_t &f) {
+__device__ __forceinline__ void pg_anti_full(double2 (&v)[16], const SmGate &g, uint32_t &f) {
     // x' = u01 y, y' = u10 x: flip slot S, then logical bit 0 gets u01, bit 1 gets u10
     f ^= 1u << S;
-    pg_phase<S, true>(v, g.u[2], g.u[3], g.u[4], g.u[5], 0, f);
+    pg_phase<S, true>(v, g.u[1], g.u[2], 0, f);
 }
 
 #define PG_CASES(KIND, FN)                                                   \
@@ -234,34 +240,77 @@ __device__ __forceinline__ void pg_anti_full(double2 (&v)[16], const PassGate &g
     case ((KIND) + PG_PARTIAL) * 4 + 2: FN<2, false>(v, g, cs, f); break;    \
     case ((KIND) + PG_PARTIAL) * 4 + 3: FN<3, false>(v, g, cs, f); break;
 
+// Shared memory of one CTA: the tile (2^K double2, XOR-swizzled), the
+// two-level deposit tables of the high tile bits, the gate table, and per
+// stage the swizzled base address of every register group.
+struct PassSmemLayout {
+    size_t tile, depA, depB, gates, gx, total;
+};
+__host__ __device__ inline PassSmemLayout pass_layout(int K, int nstages) {
+    PassSmemLayout L;
+    L.tile = 0;
+    L.depA = ((size_t)1 << K) * 16;
+    L.depB = L.depA + 32 * 8;
+    L.gates = L.depB + 32 * 8;
+    L.gx = L.gates + PASS_MAX_GATES * sizeof(SmGate);
+    L.total = L.gx + (size_t)nstages * ((size_t)1 << (K - PASS_R)) * 2;
+    return L;
+}
+
 __global__ void __launch_bounds__(PASS_THREADS, 3) k_pass_e(const __grid_constant__ PassParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double2 *tile = reinterpret_cast<double2 *>(smem_raw);
     const int K = p.K;
+    const PassSmemLayout L = pass_layout(K, p.nstages);
+    double2 *tile = reinterpret_cast<double2 *>(smem_raw + L.tile);
+    uint64_t *depA = reinterpret_cast<uint64_t *>(smem_raw + L.depA);  // high tile bits 0..4
+    uint64_t *depB = reinterpret_cast<uint64_t *>(smem_raw + L.depB);  // high tile bits 5..
+    SmGate *gates = reinterpret_cast<SmGate *>(smem_raw + L.gates);
+    uint16_t *gx = reinterpret_cast<uint16_t *>(smem_raw + L.gx);
     const uint32_t tsize = 1u << K;
     const int h = K - PASS_LOW;
-    uint64_t *dep = reinterpret_cast<uint64_t *>(smem_raw + (size_t)tsize * sizeof(double2));
-    for (uint32_t hi = threadIdx.x; hi < (1u << h); hi += PASS_THREADS) {
+    const uint32_t ngroups = tsize >> PASS_R;
+    const uint32_t tid = threadIdx.x;
+    // ---- one-time setup per CTA ----
+    if (tid < 64) {
+        const int lo = tid < 32 ? 0 : 5;
+        const uint32_t hi = tid & 31u;
         uint64_t m = 0;
-        for (int i = 0; i < h; ++i)
-            if (hi & (1u << i)) m |= 1ull << p.high_q[i];
-        dep[hi] = m;
+        for (int i = 0; i < 5 && lo + i < h; ++i)
+            if (hi & (1u << i)) m |= 1ull << p.high_q[lo + i];
+        (tid < 32 ? depA : depB)[hi] = m;
+    }
+    for (int gi = tid; gi < PASS_MAX_GATES; gi += PASS_THREADS) {
+        const PassGate &g = p.g[gi];
+        SmGate sg;
+        for (int c = 0; c < 4; ++c) sg.u[c] = make_double2(g.u[2 * c], g.u[2 * c + 1]);
+        sg.cmask_out = g.cmask_out;
+        sg.tmask_out = g.tmask_out;
+        sg.kind = g.kind;
+        sg.slot = g.slot;
+        sg.cslot = g.cslot;
+        sg.pad = 0;
+        gates[gi] = sg;
+    }
+    for (int s = 0; s < p.nstages; ++s) {
+        const PassStage &st = p.st[s];
+        for (uint32_t grp = tid; grp < ngroups; grp += PASS_THREADS) {
+            uint32_t x0 = 0;
+            for (int i = 0; i < K - PASS_R; ++i) x0 |= ((grp >> i) & 1u) << st.gbits[i];
+            gx[s * ngroups + grp] = (uint16_t)swz(x0);
+        }
     }
     __syncthreads();
     double2 *__restrict__ a = reinterpret_cast<double2 *>(p.a);
-    const uint32_t tid = threadIdx.x;
-    const uint32_t ngroups = tsize >> PASS_R;
     constexpr uint32_t LOWM = (1u << PASS_LOW) - 1u;
+    auto dep = [&](uint32_t hi) -> uint64_t { return depA[hi & 31u] | depB[hi >> 5]; };
 
     for (uint64_t T = blockIdx.x; T < p.ntiles; T += gridDim.x) {
         // base: insert zeros at the tile's qubits (0..PASS_LOW-1 and high_q ascending)
         uint64_t base = T << PASS_LOW;
         for (int i = 0; i < h; ++i) base = insert_zero(base, p.high_q[i]);
         // ---- load the tile (coalesced 128 B runs) ----
-        for (uint32_t x = tid; x < tsize; x += PASS_THREADS) {
-            uint64_t off = (x & LOWM) | dep[x >> PASS_LOW];
-            cp_async16(&tile[swz(x)], &a[base | off]);
-        }
+        for (uint32_t x = tid; x < tsize; x += PASS_THREADS)
+            cp_async16(&tile[swz(x)], &a[base | (x & LOWM) | dep(x >> PASS_LOW)]);
         cp_async_wait_all();
         __syncthreads();
         // ---- stages ----
@@ -270,12 +319,15 @@ __global__ void __launch_bounds__(PASS_THREADS, 3) k_pass_e(const __grid_constan
             // swz is linear over GF(2): swz(x0 | slot bits) = swz(x0) ^ xor of swz(slot bit)
             const uint32_t b0 = swz(1u << st.rbits[0]), b1 = swz(1u << st.rbits[1]);
             const uint32_t b2 = swz(1u << st.rbits[2]), b3 = swz(1u << st.rbits[3]);
+            const int g0 = st.first_gate, g1 = st.first_gate + st.ngates;
+            const bool nf = st.needs_full;
             for (uint32_t grp = tid; grp < ngroups; grp += PASS_THREADS) {
-                uint32_t x0 = 0;
-                for (int i = 0; i < K - PASS_R; ++i) x0 |= ((grp >> i) & 1u) << st.gbits[i];
-                const uint32_t sx0 = swz(x0);
+                const uint32_t sx0 = gx[s * ngroups + grp];
                 uint64_t full0 = 0;
-                if (st.needs_full) full0 = p.shard_base | base | (x0 & LOWM) | dep[x0 >> PASS_LOW];
+                if (nf) {
+                    const uint32_t x0 = swz(sx0);  // swz is an involution
+                    full0 = p.shard_base | base | (x0 & LOWM) | dep(x0 >> PASS_LOW);
+                }
                 double2 v[16];
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
@@ -284,8 +336,8 @@ __global__ void __launch_bounds__(PASS_THREADS, 3) k_pass_e(const __grid_constan
                     v[j] = tile[xs];
                 }
                 uint32_t f = 0;
-                for (int gi = st.first_gate; gi < st.first_gate + st.ngates; ++gi) {
-                    const PassGate &g = p.g[gi];
+                for (int gi = g0; gi < g1; ++gi) {
+                    const SmGate &g = gates[gi];
                     if ((full0 & g.cmask_out) != g.cmask_out) continue;
                     const int cs = g.cslot;
                     const int kind = g.kind;
@@ -295,11 +347,11 @@ __global__ void __launch_bounds__(PASS_THREADS, 3) k_pass_e(const __grid_constan
                     }
                     if ((kind & 3) == PG_DIAG_OUT) {
                         const bool bit = (full0 & g.tmask_out) != 0;
-                        const double fr = bit ? g.u[6] : g.u[0], fi = bit ? g.u[7] : g.u[1];
+                        const double2 c = bit ? g.u[3] : g.u[0];
                         if (kind & PG_PARTIAL)
-                            pg_diag_out<false>(v, fr, fi, cs, f);
+                            pg_diag_out<false>(v, c, cs, f);
                         else
-                            pg_diag_out<true>(v, fr, fi, cs, f);
+                            pg_diag_out<true>(v, c, cs, f);
                         continue;
                     }
                     switch (kind * 4 + g.slot) {
@@ -325,25 +377,25 @@ __global__ void __launch_bounds__(PASS_THREADS, 3) k_pass_e(const __grid_constan
             __syncthreads();
         }
         // ---- store the tile ----
-        for (uint32_t x = tid; x < tsize; x += PASS_THREADS) {
-            uint64_t off = (x & LOWM) | dep[x >> PASS_LOW];
-            a[base | off] = tile[swz(x)];
-        }
+        for (uint32_t x = tid; x < tsize; x += PASS_THREADS)
+            a[base | (x & LOWM) | dep(x >> PASS_LOW)] = tile[swz(x)];
         __syncthreads();
     }
 }
 
-static size_t pass_smem(int K) { return ((size_t)1 << K) * sizeof(double2) + ((size_t)1 << (K - PASS_LOW)) * 8; }
+static size_t pass_smem(int K, int nstages) { return pass_layout(K, nstages).total; }
+
 
 static bool g_pass_attr = false;
 int pass_e_max_grid() { return num_sms() * 3; }
 
 void launch_pass_e(const PassParams &p, int grid, cudaStream_t s) {
     if (!g_pass_attr) {
-        cudaFuncSetAttribute(k_pass_e, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem(PASS_MAX_K));
+        cudaFuncSetAttribute(k_pass_e, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)pass_smem(PASS_MAX_K, PASS_MAX_STAGES));
         g_pass_attr = true;
     }
-    k_pass_e<<<grid, PASS_THREADS, pass_smem(p.K), s>>>(p);
+    k_pass_e<<<grid, PASS_THREADS, pass_smem(p.K, p.nstages), s>>>(p);
 }
 
 // ============================================================================
