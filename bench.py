@@ -37,6 +37,7 @@ import numpy as np  # noqa: E402
 import qsim_inputs as C  # noqa: E402
 
 METRIC = "gates/sec and effective HBM GB/s per gate sweep at N qubits, 1/2/4/8 B200"
+ALU_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # fp64 FMA peak from unit counts and max clock
 UNIT = "GB/s"
 
 
@@ -301,7 +302,12 @@ def main():
            "what": "qsim_reset + qsim_apply_circuit(host gate records) + qsim_probabilities(host buffer), wall clock"}
 
     # ---- roofline of the dominant kernel ----
+    # Each launch has algorithmic bytes (HBM) and algorithmic fp64 flops; the
+    # binding roofline is the one with the larger ideal time.  HBM peak:
+    # MEASURED_PEAKS.json; fp64 peak: derived from unit counts and clock
+    # (DESIGN.md "Rooflines"): 148 SMs x 64 FP64 FMA/clk x 2 flop x 1.965 GHz.
     peak, peak_src = peaks()
+    peak_fp64 = ALU_PEAK_TFLOPS
     dom = max(prof.items(), key=lambda kv: kv[1]["ms"]) if prof else None
     roof = None
     per_kernel = {}
@@ -309,20 +315,34 @@ def main():
         per_kernel[k] = {"launches": v["launches"], "ms_total": v["ms"],
                          "avg_ms": v["ms"] / max(v["launches"], 1),
                          "GBps": v["bytes"] / max(v["ms"], 1e-9) / 1e6,
+                         "TFLOPs": v["flops"] / max(v["ms"], 1e-9) / 1e9,
                          "share_of_step": v["ms"] / ms}
     if dom:
         k, v = dom
-        achieved = v["bytes"] / (v["ms"] / 1e3) / 1e9
+        sec = v["ms"] / 1e3
+        gbs = v["bytes"] / sec / 1e9
+        tfl = v["flops"] / sec / 1e12
+        t_hbm = v["bytes"] / (peak * 1e9)
+        t_alu = v["flops"] / (peak_fp64 * 1e12)
         traffic = None
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
             try:
-                traffic = json.load(open(tp)).get(k)
+                t = json.load(open(tp)).get(k)
+                traffic = t["dram_over_algorithmic"] * v["bytes"] / v["launches"] if t else None
             except Exception:
                 traffic = None
-        roof = {"bound": "hbm", "kernel": k, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                "bytes_per_launch": v["bytes"] / v["launches"], "avg_launch_ms": v["ms"] / v["launches"]}
+        common = {"kernel": k, "traffic": traffic, "bytes_per_launch": v["bytes"] / v["launches"],
+                  "flops_per_launch": v["flops"] / v["launches"], "avg_launch_ms": v["ms"] / v["launches"],
+                  "hbm": {"achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak, "peak_source": peak_src},
+                  "fp64": {"achieved": tfl, "peak": peak_fp64, "unit": "TFLOP/s", "frac": tfl / peak_fp64,
+                           "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (measured DFMA "
+                                          "microbenchmark: 33.6 TFLOP/s)"}}
+        if t_alu > t_hbm:
+            roof = {"bound": "alu", "achieved": tfl, "peak": peak_fp64, "unit": "TFLOP/s", "frac": tfl / peak_fp64,
+                    **common}
+        else:
+            roof = {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak, **common}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

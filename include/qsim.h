@@ -206,6 +206,8 @@ typedef struct qsim_kernel_profile {
     int64_t launches;
     double ms;     /* summed event durations */
     double bytes;  /* summed algorithmic bytes */
+    double flops;  /* summed algorithmic fp64 flops (14 per amplitude of a dense
+                      gate, 6 per touched amplitude of a phase gate, 0 for permutations) */
 } qsim_kernel_profile;
 int qsim_profile(qsim_state *s, int enable);
 int qsim_profile_read(qsim_state *s, qsim_kernel_profile *out, int max, int *nout);

@@ -66,7 +66,7 @@ class qsim_stats(ctypes.Structure):
 
 class qsim_kernel_profile(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("pad", ctypes.c_int32), ("launches", ctypes.c_int64),
-                ("ms", ctypes.c_double), ("bytes", ctypes.c_double)]
+                ("ms", ctypes.c_double), ("bytes", ctypes.c_double), ("flops", ctypes.c_double)]
 
 
 KERNEL_NAMES = {0: "pass_e", 1: "sweep_e", 2: "xchg", 3: "a_bounds", 4: "a_apply", 5: "a_fast"}
@@ -325,7 +325,8 @@ def qsim_profile_read(h) -> dict:
     arr = (qsim_kernel_profile * 8)()
     n = ctypes.c_int()
     _check(_lib.qsim_profile_read(h, arr, 8, ctypes.byref(n)))
-    return {KERNEL_NAMES[arr[i].kind]: dict(launches=arr[i].launches, ms=arr[i].ms, bytes=arr[i].bytes)
+    return {KERNEL_NAMES[arr[i].kind]: dict(launches=arr[i].launches, ms=arr[i].ms, bytes=arr[i].bytes,
+                                            flops=arr[i].flops)
             for i in range(n.value)}
 
 

@@ -71,7 +71,7 @@ struct qsim_state {
     // profiling (qsim_profile): event pairs around each launch
     struct ProfRec {
         int kind;
-        double bytes;
+        double bytes, flops;
         cudaEvent_t a, b;
     };
     bool prof = false;
@@ -101,11 +101,11 @@ static void prof_begin(qsim_state *s) {
     s->prof_a = pool_get(s);
     cudaEventRecord(s->prof_a, s->stream);
 }
-static void prof_end(qsim_state *s, int kind, double bytes) {
+static void prof_end(qsim_state *s, int kind, double bytes, double flops = 0.0) {
     if (!s->prof || !s->prof_a) return;
     cudaEvent_t b = pool_get(s);
     cudaEventRecord(b, s->stream);
-    s->prof_recs.push_back({kind, bytes, s->prof_a, b});
+    s->prof_recs.push_back({kind, bytes, flops, s->prof_a, b});
     s->prof_a = nullptr;
 }
 static uint64_t shard_base(const qsim_state *s, const Shard &sh) { return (uint64_t)sh.index << s->nl; }
@@ -145,6 +145,31 @@ static double gate_bytes_alone(const qsim_state *s, const Shard &sh, const PlanO
     return amps * per;
 }
 
+// Algorithmic fp64 flops of one gate on one shard: a dense 2x2
+// is 14 flops per amplitude it updates (4 complex multiplies + 2 complex adds
+// per pair), a phase 6 per amplitude whose factor is not 1, a permutation 0.
+static double gate_flops(const qsim_state *s, const Shard &sh, const PlanOp &o, const double *u) {
+    if (!global_ctrls_ok(s, sh, o)) return 0.0;
+    int nlc = 0;
+    for (int c = 0; c < o.nctrl; ++c)
+        if (o.ctrl[c] < s->nl) ++nlc;
+    double amps = std::ldexp(1.0, s->nl - nlc);
+    if (o.cls == CLS_DENSE) return 14.0 * amps;
+    if (o.cls == CLS_ANTI) {
+        bool perm = u[2] == 1.0 && u[3] == 0.0 && u[4] == 1.0 && u[5] == 0.0;
+        return perm ? 0.0 : 6.0 * amps;
+    }
+    if (o.cls == CLS_DIAG) {
+        bool one0 = u[0] == 1.0 && u[1] == 0.0, one1 = u[6] == 1.0 && u[7] == 0.0;
+        if (o.l >= s->nl) {
+            int bit = rank_bit(sh, o.l, s->nl);
+            return (bit ? one1 : one0) ? 0.0 : 6.0 * amps;
+        }
+        return 6.0 * amps * ((one0 ? 0.0 : 0.5) + (one1 ? 0.0 : 0.5));
+    }
+    return 0.0;
+}
+
 // ============================================================================
 // E single-gate sweep on every shard
 // ============================================================================
@@ -172,7 +197,7 @@ static int sweep_gate_e(qsim_state *s, const PlanOp &o, const double *u) {
             p.nitems = 1ull << (s->nl - nloc);
             prof_begin(s);
             launch_scale_e(p, s->stream);
-            prof_end(s, QSIM_K_SWEEP, gate_bytes_alone(s, sh, o, u));
+            prof_end(s, QSIM_K_SWEEP, gate_bytes_alone(s, sh, o, u), gate_flops(s, sh, o, u));
         } else {
             SweepParams p{};
             p.a = sh.amps;
@@ -189,7 +214,7 @@ static int sweep_gate_e(qsim_state *s, const PlanOp &o, const double *u) {
             p.touch = (o.cls == CLS_DIAG) ? (one0 ? 2 : (one1 ? 1 : 3)) : 3;
             prof_begin(s);
             launch_sweep_e(p, s->stream);
-            prof_end(s, QSIM_K_SWEEP, gate_bytes_alone(s, sh, o, u));
+            prof_end(s, QSIM_K_SWEEP, gate_bytes_alone(s, sh, o, u), gate_flops(s, sh, o, u));
         }
         s->st.kernels++;
         s->st.sweeps++;
@@ -422,9 +447,11 @@ static int launch_pass(qsim_state *s, const PassBuild &pb, const std::vector<Pla
     for (auto &sh : s->shards) {
         p.a = sh.amps;
         p.shard_base = shard_base(s, sh);
+        double fl = 0.0;
+        for (int k : pb.ops) fl += gate_flops(s, sh, run[k], us[k]);
         prof_begin(s);
         launch_pass_e(p, grid, s->stream);
-        prof_end(s, QSIM_K_PASS, std::ldexp(2.0 * (double)s->amp_bytes, s->nl));
+        prof_end(s, QSIM_K_PASS, std::ldexp(2.0 * (double)s->amp_bytes, s->nl), fl);
         s->st.kernels++;
         s->st.passes++;
         s->st.fused_gates += (int64_t)pb.ops.size();
@@ -957,6 +984,7 @@ int qsim_profile_read(qsim_state *s, qsim_kernel_profile *out, int max, int *nou
         agg[r.kind].launches++;
         agg[r.kind].ms += ms;
         agg[r.kind].bytes += r.bytes;
+        agg[r.kind].flops += r.flops;
         s->ev_pool.push_back(r.a);
         s->ev_pool.push_back(r.b);
     }
