@@ -103,6 +103,7 @@ typedef struct qsim_stats {
     double hbm_bytes;         /* algorithmic HBM bytes of sweeps + passes + exchange kernels */
     double gate_bytes;        /* sum over gates of the per-gate algorithmic bytes had each run alone */
     double exchange_bytes;    /* bytes sent per direction by this process's shards */
+    int64_t stages;           /* register stages summed over fused passes */
 } qsim_stats;
 
 /* ---- lifetime ---------------------------------------------------------- */

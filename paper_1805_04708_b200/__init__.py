@@ -61,7 +61,7 @@ class qsim_stats(ctypes.Structure):
     _fields_ = [("gates", ctypes.c_int64), ("kernels", ctypes.c_int64), ("sweeps", ctypes.c_int64),
                 ("passes", ctypes.c_int64), ("fused_gates", ctypes.c_int64), ("exchanges", ctypes.c_int64),
                 ("hbm_bytes", ctypes.c_double), ("gate_bytes", ctypes.c_double),
-                ("exchange_bytes", ctypes.c_double)]
+                ("exchange_bytes", ctypes.c_double), ("stages", ctypes.c_int64)]
 
 
 class qsim_kernel_profile(ctypes.Structure):

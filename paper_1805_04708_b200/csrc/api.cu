@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -54,6 +55,7 @@ using namespace qsim;
 
 struct qsim_state {
     int n = 0, enc = 0, P = 1, nl = 0, transport = 0, rank = 0, dev = 0, fuse = 1;
+    int pass_r = 4;  // register qubits per pass stage (QSIM_PASS_R=5 selects 32-amplitude groups)
     size_t amp_bytes = 16;
     uint64_t alloc_amps = 0;  // max(2^nl, 256): small shards are padded with zero amplitudes
     Planner pl;
@@ -263,7 +265,7 @@ static bool pass_add(PassBuild &pb, const PlanOp &o, int idx, int hmax) {
 // order, every remaining gate that commutes with all skipped earlier gates and
 // whose target fits the register set.  Returns false if more than
 // PASS_MAX_STAGES stages are needed (the caller then shortens the pass).
-static bool stage_pass(PassBuild &pb, const std::vector<PlanOp> &run) {
+static bool stage_pass(PassBuild &pb, const std::vector<PlanOp> &run, int RR) {
     pb.stage_q.clear();
     pb.stage_ops.clear();
     std::vector<int> rem = pb.ops, order;
@@ -277,7 +279,7 @@ static bool stage_pass(PassBuild &pb, const std::vector<PlanOp> &run) {
             gate_masks(o, xq, zq);
             bool ok = !((xq & (bx | bz)) || (zq & bx));
             if (ok && o.cls != CLS_DIAG && std::find(R.begin(), R.end(), o.l) == R.end()) {
-                if ((int)R.size() < PASS_R)
+                if ((int)R.size() < RR)
                     R.push_back(o.l);
                 else
                     ok = false;
@@ -316,7 +318,7 @@ static void cmatmul2(const double *a, const double *b, double *c) {  // c = a * 
 
 static int launch_pass(qsim_state *s, const PassBuild &pb, const std::vector<PlanOp> &run,
                        const std::vector<const double *> &us) {
-    const int K = std::min(PASS_MAX_K, s->nl);
+    const int K = std::min(pass_e_max_k(), s->nl);
     const int h = K - PASS_LOW;
     std::vector<int> high = pb.high;
     for (int q = PASS_LOW; (int)high.size() < h && q < s->nl; ++q)
@@ -335,14 +337,16 @@ static int launch_pass(qsim_state *s, const PassBuild &pb, const std::vector<Pla
     p.ntiles = 1ull << (s->nl - K);
     for (int i = 0; i < h; ++i) p.high_q[i] = high[i];
     p.nstages = (int)pb.stage_q.size();
+    const int RR = s->pass_r;
+    p.R = RR;
     int gi = 0;
     for (int si = 0; si < p.nstages; ++si) {
         PassStage &st = p.st[si];
         std::vector<int> R;
         for (int q : pb.stage_q[si]) R.push_back(tile_bit(q));
-        for (int b = 0; (int)R.size() < PASS_R; ++b)
+        for (int b = 0; (int)R.size() < RR; ++b)
             if (std::find(R.begin(), R.end(), b) == R.end()) R.push_back(b);
-        for (int r = 0; r < PASS_R; ++r) st.rbits[r] = (int8_t)R[r];
+        for (int r = 0; r < RR; ++r) st.rbits[r] = (int8_t)R[r];
         // group bits: three with distinct residues mod 3 first (bank-conflict-free
         // quarter warps under the XOR-fold swizzle), then the rest ascending.
         std::vector<int> rest;
@@ -358,7 +362,7 @@ static int launch_pass(qsim_state *s, const PassBuild &pb, const std::vector<Pla
                 }
         std::sort(gb.begin(), gb.end());
         for (int b : rest) gb.push_back(b);
-        for (int i = 0; i < K - PASS_R; ++i) st.gbits[i] = (int8_t)gb[i];
+        for (int i = 0; i < K - RR; ++i) st.gbits[i] = (int8_t)gb[i];
         st.first_gate = (int8_t)gi;
         // last gate (index into p.g) touching each local qubit in this stage, for merging
         int last_on[64];
@@ -379,6 +383,7 @@ static int launch_pass(qsim_state *s, const PassBuild &pb, const std::vector<Pla
                     int base_kind = off0 ? PG_DIAG_IN : (dia0 ? PG_ANTI : PG_DENSE);
                     if (dia0 && prod[2] == 1.0 && prod[3] == 0.0 && prod[4] == 1.0 && prod[5] == 0.0) base_kind = PG_SWAP;
                     m.kind = (int8_t)(base_kind | (m.kind & PG_PARTIAL));
+                    m.op = (int8_t)pass_op(m.kind, m.slot, RR);
                 }
                 // a DIAG_OUT gate only merges with diagonal gates (target outside the registers)
                 continue;
@@ -390,7 +395,7 @@ static int launch_pass(qsim_state *s, const PassBuild &pb, const std::vector<Pla
             for (int c = 0; c < o.nctrl; ++c) {
                 int tb = (o.ctrl[c] < s->nl) ? tile_bit(o.ctrl[c]) : -1;
                 int slot = -1;
-                for (int r = 0; r < PASS_R; ++r)
+                for (int r = 0; r < RR; ++r)
                     if (tb >= 0 && R[r] == tb) slot = r;
                 if (slot >= 0)
                     cslot |= (int8_t)(1 << slot);
@@ -402,7 +407,7 @@ static int launch_pass(qsim_state *s, const PassBuild &pb, const std::vector<Pla
             if (cout) st.needs_full = 1;
             int ttb = (o.l < s->nl) ? tile_bit(o.l) : -1;
             int tslot = -1;
-            for (int r = 0; r < PASS_R; ++r)
+            for (int r = 0; r < RR; ++r)
                 if (ttb >= 0 && R[r] == ttb) tslot = r;
             int kind;
             if (o.cls == CLS_DIAG) {
@@ -431,6 +436,7 @@ static int launch_pass(qsim_state *s, const PassBuild &pb, const std::vector<Pla
                 kind |= PG_PARTIAL;
             }
             g.kind = (int8_t)kind;
+            g.op = (int8_t)pass_op(kind, g.slot, RR);
             merged_ok.push_back(o.nctrl == 0 && o.l < s->nl ? 1 : 0);
             if (o.l < 64) last_on[o.l] = gi;
             for (int c = 0; c < o.nctrl; ++c)
@@ -443,7 +449,8 @@ static int launch_pass(qsim_state *s, const PassBuild &pb, const std::vector<Pla
         }
         st.ngates = (int8_t)(gi - st.first_gate);
     }
-    int grid = (int)std::min<uint64_t>(p.ntiles, (uint64_t)pass_e_max_grid());
+    int grid = (int)std::min<uint64_t>(p.ntiles, (uint64_t)pass_e_max_grid(RR));
+    s->st.stages += p.nstages;
     for (auto &sh : s->shards) {
         p.a = sh.amps;
         p.shard_base = shard_base(s, sh);
@@ -465,7 +472,7 @@ static int launch_pass(qsim_state *s, const PassBuild &pb, const std::vector<Pla
 // order, every not-yet-applied gate that commutes with all earlier skipped
 // gates and fits the tile (<= K - PASS_LOW high target qubits, <= PASS_MAX_*).
 static int run_gates_e(qsim_state *s, const std::vector<PlanOp> &run, const std::vector<const double *> &us) {
-    const int K = std::min(PASS_MAX_K, s->nl);
+    const int K = std::min(pass_e_max_k(), s->nl);
     const bool can_fuse = s->fuse && K >= PASS_MIN_K;
     if (!can_fuse) {
         for (size_t i = 0; i < run.size(); ++i) RC(sweep_gate_e(s, run[i], us[i]));
@@ -491,7 +498,7 @@ static int run_gates_e(qsim_state *s, const std::vector<PlanOp> &run, const std:
             if ((int)pb.ops.size() >= PASS_MAX_GATES) break;
         }
         // form register stages; if the pass needs too many, give back its last gates
-        while (!stage_pass(pb, run)) {
+        while (!stage_pass(pb, run, s->pass_r)) {
             int k = pb.ops.back();
             pb.ops.pop_back();
             done[k] = 0;
@@ -821,6 +828,7 @@ int qsim_create_ex(const qsim_config *cfg, qsim_state **out) {
     s->transport = transport;
     s->rank = transport == QSIM_TRANSPORT_NCCL ? cfg->rank : 0;
     s->fuse = cfg->fuse;
+    if (const char *pr = getenv("QSIM_PASS_R")) s->pass_r = (atoi(pr) == 4) ? 4 : 5;
     s->amp_bytes = s->enc == QSIM_ENC_FP64 ? 16 : 2;
     if (cfg->device >= 0) {
         if (cudaSetDevice(cfg->device) != cudaSuccess) {

@@ -42,7 +42,7 @@ void launch_scale_e(const ScaleParams &p, cudaStream_t s);
 constexpr int PASS_LOW = 3;       // tile always holds qubits 0..2 (128 B contiguous runs = one L2 line)
 constexpr int PASS_MAX_K = 12;    // 2^12 amplitudes x 16 B = 64 KiB of shared memory per CTA
 constexpr int PASS_MIN_K = 9;
-constexpr int PASS_R = 4;         // qubits held in registers per stage (16 amplitudes per thread)
+constexpr int PASS_R_MAX = 5;     // qubits held in registers per stage: R = 4 (16 amplitudes / thread) or 5 (32)
 constexpr int PASS_THREADS = 128;
 constexpr int PASS_MAX_GATES = 32;
 constexpr int PASS_MAX_STAGES = 12;  // smem: 64 KiB tile + 3 KiB gates + 6 KiB group table < 75 KiB (3 CTAs/SM)
@@ -58,12 +58,26 @@ struct PassGate {
     int8_t kind;
     int8_t slot;         // target slot (0..3) in the register set
     int8_t cslot;        // slot bits that must be 1 (controls inside the register set)
-    int8_t pad[5];
+    int8_t op;           // dense dispatch index (pass_op()), computed on the host
+    int8_t pad[4];
 };
+// Dense dispatch index of a pass gate: slot * 6 + {0 dense, 1 dense-partial,
+// 2 diag, 3 diag-partial, 4 anti, 5 swap}, or 6 * R + {0, 1} for a diagonal
+// gate whose target is outside the register set (full / partial).
+__host__ __device__ inline int pass_op(int kind, int slot, int R) {
+    const bool part = (kind & PG_PARTIAL) != 0;
+    if (kind == PG_SWAP) return slot * 6 + 5;
+    switch (kind & 3) {
+        case PG_DENSE: return slot * 6 + (part ? 1 : 0);
+        case PG_DIAG_IN: return slot * 6 + (part ? 3 : 2);
+        case PG_ANTI: return slot * 6 + 4;
+        default: return 6 * R + (part ? 1 : 0);
+    }
+}
 
 struct PassStage {
-    int8_t rbits[PASS_R];  // slot s <-> tile bit rbits[s]
-    int8_t gbits[PASS_MAX_K - PASS_R];  // group index bit i <-> tile bit gbits[i]
+    int8_t rbits[PASS_R_MAX];  // slot s <-> tile bit rbits[s] (first R used)
+    int8_t gbits[PASS_MAX_K];  // group index bit i <-> tile bit gbits[i] (first K - R used)
     int8_t first_gate;
     int8_t ngates;
     int8_t needs_full;   // some gate of the stage tests bits outside the register set
@@ -77,14 +91,15 @@ struct PassParams {
     int32_t nl;
     int32_t K;            // tile qubits
     int32_t nstages;
-    int32_t pad;
+    int32_t R;            // register qubits per stage (4 or 5)
     int32_t high_q[PASS_MAX_K - PASS_LOW];  // local qubit of tile bit PASS_LOW + i (ascending)
     int32_t pad2;
     PassStage st[PASS_MAX_STAGES];
     PassGate g[PASS_MAX_GATES];
 };
 void launch_pass_e(const PassParams &p, int grid, cudaStream_t s);
-int pass_e_max_grid();
+int pass_e_max_grid(int R);
+int pass_e_max_k();  // tile qubits of the selected pass-kernel occupancy
 
 // ---- exchange-fused gate (a7) ------------------------------------------------
 struct XchgParams {

@@ -132,6 +132,7 @@ struct ASm {
     double cb[260], sb[260];
     double r0n, scalen;
     int degn;
+    float mmargin;  // magnitude-candidate margin (steps) below which the fp64 check is skipped
 };
 
 __device__ void load_asm(ASm &sm, const ATabData *__restrict__ cur, const ATabData *__restrict__ nxt) {
@@ -149,6 +150,10 @@ __device__ void load_asm(ASm &sm, const ATabData *__restrict__ cur, const ATabDa
         sm.r0n = nxt->r0;
         sm.scalen = nxt->scale;
         sm.degn = nxt->degenerate;
+        // fp32 candidate error in steps: |d tf| <= (eps32 (|m| + r0) + |m - m_f|) * scale,
+        // bounded by 4e-7 * (r1 + r0) * scale + 1e-3; above 0.5 -> always check
+        const double e = 4e-7 * (nxt->r1 + nxt->r0) * nxt->scale + 1e-3;
+        sm.mmargin = (float)(e < 0.49 ? e : 0.5);
     }
     __syncthreads();
 }
@@ -164,23 +169,48 @@ __device__ __forceinline__ double a_m2(double2 z) { return fma(z.x, z.x, z.y * z
 
 __device__ __forceinline__ uint32_t pack(int b0, int b1) { return (uint32_t)(b0 & 0xff) | ((uint32_t)(b1 & 0xff) << 8); }
 
+// fp32 atan2 candidate in units of the b1 step (128/pi per radian): octant
+// reduction + the odd minimax polynomial of Abramowitz & Stegun 4.4.49
+// (|error| <= 1e-5 rad = 4e-4 steps).
+__device__ __forceinline__ float atan2_steps(float y, float x) {
+    const float ax = fabsf(x), ay = fabsf(y);
+    const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+    const float t = __fdividef(mn, mx);
+    const float s = t * t;
+    float p = fmaf(fmaf(fmaf(fmaf(0.0208351f, s, -0.0851330f), s, 0.1801410f), s, -0.3302995f), s, 0.9998660f) * t;
+    if (ay > ax) p = 1.57079632679f - p;
+    if (x < 0.f) p = 3.14159265359f - p;
+    if (y < 0.f) p = -p;
+    return p * 40.74366543152521f;  // 128 / pi
+}
+
+// Angle code: round half away from zero of 128 atan2(y, x) / pi, computed in
+// fp64 terms.  The fp32 candidate is exact unless it lies within A_MARGIN
+// steps of a rounding boundary; only then the exact fp64 boundary-direction
+// cross products decide (ties away from zero, reading R-A6).
+#define A_MARGIN 0.02f
 __device__ __forceinline__ int a_angle_code(const ASm &sm, double2 z) {
-    float af = atan2f((float)z.y, (float)z.x) * 40.74366543152521f;  // 128 / pi
+    const float af = atan2_steps((float)z.y, (float)z.x);
     int k = __float2int_rn(af);
+    const float fr = af - (float)k;
     k = max(-128, min(128, k));
-    // upper boundary of code k: beta = (k + 0.5) pi / 128 (index k + 129)
-    double cu = z.y * sm.cb[k + 129] - z.x * sm.sb[k + 129];
-    if ((k >= 0) ? (cu >= 0.0) : (cu > 0.0)) {
-        k += 1;
-    } else {
-        double cl = z.y * sm.cb[k + 128] - z.x * sm.sb[k + 128];  // beta = (k - 0.5) pi / 128
-        if ((k > 0) ? (cl < 0.0) : (cl <= 0.0)) k -= 1;
+    if (fabsf(fr) > 0.5f - A_MARGIN) {
+        // upper boundary of code k: beta = (k + 0.5) pi / 128 (index k + 129)
+        double cu = z.y * sm.cb[k + 129] - z.x * sm.sb[k + 129];
+        if ((k >= 0) ? (cu >= 0.0) : (cu > 0.0)) {
+            k += 1;
+        } else {
+            double cl = z.y * sm.cb[k + 128] - z.x * sm.sb[k + 128];  // beta = (k - 0.5) pi / 128
+            if ((k > 0) ? (cl < 0.0) : (cl <= 0.0)) k -= 1;
+        }
+        k = max(-128, min(128, k));
     }
-    k = max(-128, min(128, k));
     return (k == 128) ? -128 : k;
 }
 
 // Encode with the NEXT bounds (PAPER.md:449-453 inverted; readings R-A3, R-A5..R-A7).
+// Magnitude: fp32 candidate, exact fp64 squared-threshold check only near a
+// rounding boundary (sm.mmargin steps, derived from the fp32 error bound).
 __device__ __forceinline__ uint32_t a_encode(const ASm &sm, double2 z) {
     const double m2 = a_m2(z);
     if (m2 < A_ZERO2) return pack(-128, 0);
@@ -190,13 +220,17 @@ __device__ __forceinline__ uint32_t a_encode(const ASm &sm, double2 z) {
     } else if (sm.degn) {
         b0 = 0;
     } else {
-        float mf = sqrtf((float)m2);
-        int c = __float2int_rn((mf - (float)sm.r0n) * (float)sm.scalen);
+        const float mf = sqrtf((float)m2);
+        const float tf = (mf - (float)sm.r0n) * (float)sm.scalen;
+        int c = __float2int_rn(tf);
+        const float fr = tf - (float)c;
         c = max(0, min(253, c));
-        if (c < 253 && m2 >= sm.thr[c])
-            c += 1;
-        else if (c > 0 && m2 < sm.thr[c - 1])
-            c -= 1;
+        if (fabsf(fr) > 0.5f - sm.mmargin) {
+            if (c < 253 && m2 >= sm.thr[c])
+                c += 1;
+            else if (c > 0 && m2 < sm.thr[c - 1])
+                c -= 1;
+        }
         b0 = c - 127;
     }
     return pack(b0, a_angle_code(sm, z));

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "internal.h"
 #include "kernels.h"
@@ -172,38 +173,38 @@ struct SmGate {
     double2 u[4];        // u00, u01, u10, u11
     uint64_t cmask_out;
     uint64_t tmask_out;
-    int32_t kind, slot, cslot, pad;
+    int32_t kind, slot, cslot, op;
 };
 
-// Gate application on the 16 register-resident amplitudes of one group.
+// Gate application on the NS = 2^R register-resident amplitudes of one group.
 // `f` is the group's slot-flip mask: register j holds the amplitude of
 // logical slot j ^ f.  An uncontrolled X / CNOT-like swap on slot S is applied
 // as f ^= 2^S (no data moves); later gates of the stage select conjugated
 // coefficients for flipped slots and the stage's store XORs f into the
 // (GF(2)-linear) smem address.  Every update is in place, so the register
-// allocator never copies the 16 amplitudes at the gate-dispatch merge points.
+// allocator never copies the amplitudes at the gate-dispatch merge points.
 // FULL: no control inside the register set.
-template <int S, bool FULL>
-__device__ __forceinline__ void pg_dense(double2 (&v)[16], const SmGate &g, int cslot, uint32_t f) {
+template <int NS, int S, bool FULL>
+__device__ __forceinline__ void pg_dense(double2 (&v)[NS], const SmGate &g, int cslot, uint32_t f) {
     // flipped target slot: registers hold (y, x): apply X U X (complex entry c -> c ^ 3)
     const int cx = ((f >> S) & 1u) ? 3 : 0;
     const double2 e0 = g.u[0 ^ cx], e1 = g.u[1 ^ cx], e2 = g.u[2 ^ cx], e3 = g.u[3 ^ cx];
     const double u[8] = {e0.x, e0.y, e1.x, e1.y, e2.x, e2.y, e3.x, e3.y};
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < NS; ++j) {
         if (j & (1 << S)) continue;
         if (!FULL && (((uint32_t)j ^ f) & cslot) != (uint32_t)cslot) continue;
         pair_dense(v[j], v[j | (1 << S)], u);
     }
 }
 // diagonal on slot S: logical bit 0 -> a0, logical bit 1 -> a1
-template <int S, bool FULL>
-__device__ __forceinline__ void pg_phase(double2 (&v)[16], double2 a0, double2 a1, int cslot, uint32_t f) {
+template <int NS, int S, bool FULL>
+__device__ __forceinline__ void pg_phase(double2 (&v)[NS], double2 a0, double2 a1, int cslot, uint32_t f) {
     const bool fl = (f >> S) & 1u;
     const double2 c0 = fl ? a1 : a0;  // registers with bit S = 0
     const double2 c1 = fl ? a0 : a1;  // registers with bit S = 1
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < NS; ++j) {
         if (!FULL && (((uint32_t)j ^ f) & cslot) != (uint32_t)cslot) continue;
         if (j & (1 << S))
             amp_phase(v[j], c1.x, c1.y);
@@ -211,56 +212,58 @@ __device__ __forceinline__ void pg_phase(double2 (&v)[16], double2 a0, double2 a
             amp_phase(v[j], c0.x, c0.y);
     }
 }
-template <int S, bool FULL>
-__device__ __forceinline__ void pg_diag(double2 (&v)[16], const SmGate &g, int cslot, uint32_t f) {
-    pg_phase<S, FULL>(v, g.u[0], g.u[3], cslot, f);
-}
-template <bool FULL>
-__device__ __forceinline__ void pg_diag_out(double2 (&v)[16], double2 c, int cslot, uint32_t f) {
+template <int NS>
+__device__ __forceinline__ void pg_diag_out(double2 (&v)[NS], double2 c, int cslot, uint32_t f, bool full) {
+    if (full) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        if (!FULL && (((uint32_t)j ^ f) & cslot) != (uint32_t)cslot) continue;
-        amp_phase(v[j], c.x, c.y);
+        for (int j = 0; j < NS; ++j) amp_phase(v[j], c.x, c.y);
+    } else {
+#pragma unroll
+        for (int j = 0; j < NS; ++j)
+            if ((((uint32_t)j ^ f) & cslot) == (uint32_t)cslot) amp_phase(v[j], c.x, c.y);
     }
 }
-template <int S>
-__device__ __forceinline__ void pg_anti_full(double2 (&v)[16], const SmGate &g, uint32_t &f) {
-    // x' = u01 y, y' = u10 x: flip slot S, then logical bit 0 gets u01, bit 1 gets u10
-    f ^= 1u << S;
-    pg_phase<S, true>(v, g.u[1], g.u[2], 0, f);
-}
 
-#define PG_CASES(KIND, FN)                                                   \
-    case (KIND) * 4 + 0: FN<0, true>(v, g, cs, f); break;                    \
-    case (KIND) * 4 + 1: FN<1, true>(v, g, cs, f); break;                    \
-    case (KIND) * 4 + 2: FN<2, true>(v, g, cs, f); break;                    \
-    case (KIND) * 4 + 3: FN<3, true>(v, g, cs, f); break;                    \
-    case ((KIND) + PG_PARTIAL) * 4 + 0: FN<0, false>(v, g, cs, f); break;    \
-    case ((KIND) + PG_PARTIAL) * 4 + 1: FN<1, false>(v, g, cs, f); break;    \
-    case ((KIND) + PG_PARTIAL) * 4 + 2: FN<2, false>(v, g, cs, f); break;    \
-    case ((KIND) + PG_PARTIAL) * 4 + 3: FN<3, false>(v, g, cs, f); break;
+// one gate on slot S (compile time) of a group; sub = op % 6
+template <int NS, int S>
+__device__ __forceinline__ void pg_slot(double2 (&v)[NS], const SmGate &g, int sub, int cs, uint32_t &f) {
+    switch (sub) {
+        case 0: pg_dense<NS, S, true>(v, g, cs, f); break;
+        case 1: pg_dense<NS, S, false>(v, g, cs, f); break;
+        case 2: pg_phase<NS, S, true>(v, g.u[0], g.u[3], cs, f); break;
+        case 3: pg_phase<NS, S, false>(v, g.u[0], g.u[3], cs, f); break;
+        case 4:  // x' = u01 y, y' = u10 x: flip slot S, then bit 0 gets u01, bit 1 gets u10
+            f ^= 1u << S;
+            pg_phase<NS, S, true>(v, g.u[1], g.u[2], 0, f);
+            break;
+        default: f ^= 1u << S; break;  // 5: uncontrolled in-register swap = slot flip
+    }
+}
 
 // Shared memory of one CTA: the tile (2^K double2, XOR-swizzled), the
 // two-level deposit tables of the high tile bits, the gate table, and per
 // stage the swizzled base address of every register group.
 struct PassSmemLayout {
-    size_t tile, depA, depB, gates, gx, total;
+    size_t tile, depA, depB, depJ, gates, gx, total;
 };
-__host__ __device__ inline PassSmemLayout pass_layout(int K, int nstages) {
+__host__ __device__ inline PassSmemLayout pass_layout(int K, int R, int nstages) {
     PassSmemLayout L;
     L.tile = 0;
     L.depA = ((size_t)1 << K) * 16;
     L.depB = L.depA + 32 * 8;
-    L.gates = L.depB + 32 * 8;
+    L.depJ = L.depB + 32 * 8;
+    L.gates = L.depJ + 32 * 8;
     L.gx = L.gates + PASS_MAX_GATES * sizeof(SmGate);
-    L.total = L.gx + (size_t)nstages * ((size_t)1 << (K - PASS_R)) * 2;
+    L.total = L.gx + (size_t)nstages * ((size_t)1 << (K - R)) * 2;
     return L;
 }
 
-__global__ void __launch_bounds__(PASS_THREADS, 3) k_pass_e(const __grid_constant__ PassParams p) {
+template <int R, int MINB>
+__global__ void __launch_bounds__(PASS_THREADS, MINB) k_pass_e(const __grid_constant__ PassParams p) {
+    constexpr int NS = 1 << R;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int K = p.K;
-    const PassSmemLayout L = pass_layout(K, p.nstages);
+    const PassSmemLayout L = pass_layout(K, R, p.nstages);
     double2 *tile = reinterpret_cast<double2 *>(smem_raw + L.tile);
     uint64_t *depA = reinterpret_cast<uint64_t *>(smem_raw + L.depA);  // high tile bits 0..4
     uint64_t *depB = reinterpret_cast<uint64_t *>(smem_raw + L.depB);  // high tile bits 5..
@@ -268,7 +271,7 @@ __global__ void __launch_bounds__(PASS_THREADS, 3) k_pass_e(const __grid_constan
     uint16_t *gx = reinterpret_cast<uint16_t *>(smem_raw + L.gx);
     const uint32_t tsize = 1u << K;
     const int h = K - PASS_LOW;
-    const uint32_t ngroups = tsize >> PASS_R;
+    const uint32_t ngroups = tsize >> R;
     const uint32_t tid = threadIdx.x;
     // ---- one-time setup per CTA ----
     if (tid < 64) {
@@ -288,14 +291,14 @@ __global__ void __launch_bounds__(PASS_THREADS, 3) k_pass_e(const __grid_constan
         sg.kind = g.kind;
         sg.slot = g.slot;
         sg.cslot = g.cslot;
-        sg.pad = 0;
+        sg.op = g.op;
         gates[gi] = sg;
     }
     for (int s = 0; s < p.nstages; ++s) {
         const PassStage &st = p.st[s];
         for (uint32_t grp = tid; grp < ngroups; grp += PASS_THREADS) {
             uint32_t x0 = 0;
-            for (int i = 0; i < K - PASS_R; ++i) x0 |= ((grp >> i) & 1u) << st.gbits[i];
+            for (int i = 0; i < K - R; ++i) x0 |= ((grp >> i) & 1u) << st.gbits[i];
             gx[s * ngroups + grp] = (uint16_t)swz(x0);
         }
     }
@@ -303,22 +306,33 @@ __global__ void __launch_bounds__(PASS_THREADS, 3) k_pass_e(const __grid_constan
     double2 *__restrict__ a = reinterpret_cast<double2 *>(p.a);
     constexpr uint32_t LOWM = (1u << PASS_LOW) - 1u;
     auto dep = [&](uint32_t hi) -> uint64_t { return depA[hi & 31u] | depB[hi >> 5]; };
+    static_assert(PASS_THREADS == 128, "load/store addressing assumes x = tid + 128 j");
+    const uint32_t njt = tsize >> 7;  // elements per thread in the load / store loops
+    const uint32_t s_tid = swz(tid);
+    const uint64_t d_tid = (tid & LOWM) | dep(tid >> PASS_LOW);
+    uint64_t *depJ = reinterpret_cast<uint64_t *>(smem_raw + L.depJ);  // dep(16 j): high tile bits >= 4
+    for (uint32_t j = tid; j < njt; j += PASS_THREADS) depJ[j] = dep(j << 4);
+    __syncthreads();
 
     for (uint64_t T = blockIdx.x; T < p.ntiles; T += gridDim.x) {
         // base: insert zeros at the tile's qubits (0..PASS_LOW-1 and high_q ascending)
         uint64_t base = T << PASS_LOW;
         for (int i = 0; i < h; ++i) base = insert_zero(base, p.high_q[i]);
         // ---- load the tile (coalesced 128 B runs) ----
-        for (uint32_t x = tid; x < tsize; x += PASS_THREADS)
-            cp_async16(&tile[swz(x)], &a[base | (x & LOWM) | dep(x >> PASS_LOW)]);
+        // x = tid + 128 j: swz and the deposit are GF(2)-linear on disjoint
+        // bits, so address = a[(base | d_tid) + depJ[j]] and smem = s_tid ^ swz(128 j).
+        const double2 *pt = a + (base | d_tid);
+#pragma unroll 8
+        for (uint32_t j = 0; j < njt; ++j) cp_async16(&tile[s_tid ^ swz(j << 7)], pt + depJ[j]);
         cp_async_wait_all();
         __syncthreads();
         // ---- stages ----
         for (int s = 0; s < p.nstages; ++s) {
             const PassStage &st = p.st[s];
             // swz is linear over GF(2): swz(x0 | slot bits) = swz(x0) ^ xor of swz(slot bit)
-            const uint32_t b0 = swz(1u << st.rbits[0]), b1 = swz(1u << st.rbits[1]);
-            const uint32_t b2 = swz(1u << st.rbits[2]), b3 = swz(1u << st.rbits[3]);
+            uint32_t sb[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) sb[r] = swz(1u << st.rbits[r]);
             const int g0 = st.first_gate, g1 = st.first_gate + st.ngates;
             const bool nf = st.needs_full;
             for (uint32_t grp = tid; grp < ngroups; grp += PASS_THREADS) {
@@ -328,11 +342,13 @@ __global__ void __launch_bounds__(PASS_THREADS, 3) k_pass_e(const __grid_constan
                     const uint32_t x0 = swz(sx0);  // swz is an involution
                     full0 = p.shard_base | base | (x0 & LOWM) | dep(x0 >> PASS_LOW);
                 }
-                double2 v[16];
+                double2 v[NS];
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const uint32_t xs = sx0 ^ ((j & 1) ? b0 : 0u) ^ ((j & 2) ? b1 : 0u) ^ ((j & 4) ? b2 : 0u) ^
-                                        ((j & 8) ? b3 : 0u);
+                for (int j = 0; j < NS; ++j) {
+                    uint32_t xs = sx0;
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        if (j & (1 << r)) xs ^= sb[r];
                     v[j] = tile[xs];
                 }
                 uint32_t f = 0;
@@ -340,62 +356,85 @@ __global__ void __launch_bounds__(PASS_THREADS, 3) k_pass_e(const __grid_constan
                     const SmGate &g = gates[gi];
                     if ((full0 & g.cmask_out) != g.cmask_out) continue;
                     const int cs = g.cslot;
-                    const int kind = g.kind;
-                    if (kind == PG_SWAP) {  // uncontrolled (in-register) swap: flip the slot
-                        f ^= 1u << g.slot;
-                        continue;
-                    }
-                    if ((kind & 3) == PG_DIAG_OUT) {
+                    const int op = g.op;
+                    if (op >= 6 * R) {  // diagonal gate whose target is outside the registers
                         const bool bit = (full0 & g.tmask_out) != 0;
-                        const double2 c = bit ? g.u[3] : g.u[0];
-                        if (kind & PG_PARTIAL)
-                            pg_diag_out<false>(v, c, cs, f);
-                        else
-                            pg_diag_out<true>(v, c, cs, f);
+                        pg_diag_out<NS>(v, bit ? g.u[3] : g.u[0], cs, f, op == 6 * R);
                         continue;
                     }
-                    switch (kind * 4 + g.slot) {
-                        PG_CASES(PG_DENSE, pg_dense)
-                        PG_CASES(PG_DIAG_IN, pg_diag)
-                        case PG_ANTI * 4 + 0: pg_anti_full<0>(v, g, f); break;
-                        case PG_ANTI * 4 + 1: pg_anti_full<1>(v, g, f); break;
-                        case PG_ANTI * 4 + 2: pg_anti_full<2>(v, g, f); break;
-                        case PG_ANTI * 4 + 3: pg_anti_full<3>(v, g, f); break;
-                        default: break;
+                    const int slot = op / 6, sub = op - 6 * slot;
+                    switch (slot) {
+                        case 0: pg_slot<NS, 0>(v, g, sub, cs, f); break;
+                        case 1: pg_slot<NS, 1>(v, g, sub, cs, f); break;
+                        case 2: pg_slot<NS, 2>(v, g, sub, cs, f); break;
+                        case 3: pg_slot<NS, 3>(v, g, sub, cs, f); break;
+                        default:
+                            if constexpr (R > 4) pg_slot<NS, (R > 4 ? 4 : 0)>(v, g, sub, cs, f);
+                            break;
                     }
                 }
                 // register j holds logical slot j ^ f: store to swz(x0 | slots(j ^ f))
-                const uint32_t sxf = sx0 ^ ((f & 1) ? b0 : 0u) ^ ((f & 2) ? b1 : 0u) ^ ((f & 4) ? b2 : 0u) ^
-                                     ((f & 8) ? b3 : 0u);
+                uint32_t sxf = sx0;
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const uint32_t xs = sxf ^ ((j & 1) ? b0 : 0u) ^ ((j & 2) ? b1 : 0u) ^ ((j & 4) ? b2 : 0u) ^
-                                        ((j & 8) ? b3 : 0u);
+                for (int r = 0; r < R; ++r)
+                    if (f & (1u << r)) sxf ^= sb[r];
+#pragma unroll
+                for (int j = 0; j < NS; ++j) {
+                    uint32_t xs = sxf;
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        if (j & (1 << r)) xs ^= sb[r];
                     tile[xs] = v[j];
                 }
             }
             __syncthreads();
         }
         // ---- store the tile ----
-        for (uint32_t x = tid; x < tsize; x += PASS_THREADS)
-            a[base | (x & LOWM) | dep(x >> PASS_LOW)] = tile[swz(x)];
+        double2 *ps = a + (base | d_tid);
+#pragma unroll 8
+        for (uint32_t j = 0; j < njt; ++j) ps[depJ[j]] = tile[s_tid ^ swz(j << 7)];
         __syncthreads();
     }
 }
 
-static size_t pass_smem(int K, int nstages) { return pass_layout(K, nstages).total; }
+static size_t pass_smem(int K, int R, int nstages) { return pass_layout(K, R, nstages).total; }
 
 
 static bool g_pass_attr = false;
-int pass_e_max_grid() { return num_sms() * 3; }
+// CTAs per SM of the R = 4 kernel: 3 (164 registers, K = 12 tiles), or 4 / 5
+// (register-capped, K = 11 tiles) -- selected with QSIM_PASS_OCC for tuning.
+static int pass_occ() {
+    static int occ = 0;
+    if (!occ) {
+        const char *e = getenv("QSIM_PASS_OCC");
+        occ = e ? atoi(e) : 3;
+        if (occ < 3 || occ > 5) occ = 3;
+    }
+    return occ;
+}
+int pass_e_max_k() { return pass_occ() == 3 ? 12 : 11; }
+int pass_e_max_grid(int R) { return num_sms() * (R >= 5 ? 2 : pass_occ()); }
 
 void launch_pass_e(const PassParams &p, int grid, cudaStream_t s) {
     if (!g_pass_attr) {
-        cudaFuncSetAttribute(k_pass_e, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)pass_smem(PASS_MAX_K, PASS_MAX_STAGES));
+        cudaFuncSetAttribute(k_pass_e<4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)pass_smem(PASS_MAX_K, 4, PASS_MAX_STAGES));
+        cudaFuncSetAttribute(k_pass_e<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)pass_smem(PASS_MAX_K, 4, PASS_MAX_STAGES));
+        cudaFuncSetAttribute(k_pass_e<4, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)pass_smem(PASS_MAX_K, 4, PASS_MAX_STAGES));
+        cudaFuncSetAttribute(k_pass_e<5, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)pass_smem(PASS_MAX_K, 5, PASS_MAX_STAGES));
         g_pass_attr = true;
     }
-    k_pass_e<<<grid, PASS_THREADS, pass_smem(p.K, p.nstages), s>>>(p);
+    if (p.R >= 5)
+        k_pass_e<5, 2><<<grid, PASS_THREADS, pass_smem(p.K, 5, p.nstages), s>>>(p);
+    else if (pass_occ() == 4)
+        k_pass_e<4, 4><<<grid, PASS_THREADS, pass_smem(p.K, 4, p.nstages), s>>>(p);
+    else if (pass_occ() == 5)
+        k_pass_e<4, 5><<<grid, PASS_THREADS, pass_smem(p.K, 4, p.nstages), s>>>(p);
+    else
+        k_pass_e<4, 3><<<grid, PASS_THREADS, pass_smem(p.K, 4, p.nstages), s>>>(p);
 }
 
 // ============================================================================
