@@ -352,24 +352,44 @@ __global__ void __launch_bounds__(PASS_THREADS, MINB) k_pass_e(const __grid_cons
                     v[j] = tile[xs];
                 }
                 uint32_t f = 0;
+                // software-pipelined dispatch: the next gate's descriptor is
+                // loaded while the current gate's FMA block runs
+                int op_n = g0 < g1 ? gates[g0].op : 0;
+                int cs_n = g0 < g1 ? gates[g0].cslot : 0;
+                uint64_t cm_n = g0 < g1 ? gates[g0].cmask_out : 0;
                 for (int gi = g0; gi < g1; ++gi) {
                     const SmGate &g = gates[gi];
-                    if ((full0 & g.cmask_out) != g.cmask_out) continue;
-                    const int cs = g.cslot;
-                    const int op = g.op;
-                    if (op >= 6 * R) {  // diagonal gate whose target is outside the registers
-                        const bool bit = (full0 & g.tmask_out) != 0;
-                        pg_diag_out<NS>(v, bit ? g.u[3] : g.u[0], cs, f, op == 6 * R);
-                        continue;
+                    const int op = op_n, cs = cs_n;
+                    const uint64_t cm = cm_n;
+                    if (gi + 1 < g1) {
+                        op_n = gates[gi + 1].op;
+                        cs_n = gates[gi + 1].cslot;
+                        cm_n = gates[gi + 1].cmask_out;
                     }
-                    const int slot = op / 6, sub = op - 6 * slot;
-                    switch (slot) {
-                        case 0: pg_slot<NS, 0>(v, g, sub, cs, f); break;
-                        case 1: pg_slot<NS, 1>(v, g, sub, cs, f); break;
-                        case 2: pg_slot<NS, 2>(v, g, sub, cs, f); break;
-                        case 3: pg_slot<NS, 3>(v, g, sub, cs, f); break;
+                    if ((full0 & cm) != cm) continue;
+                    switch (op) {
+#define PG_OPS(S)                                                                            \
+    case (S) * 6 + 0: pg_dense<NS, (S), true>(v, g, cs, f); break;                           \
+    case (S) * 6 + 1: pg_dense<NS, (S), false>(v, g, cs, f); break;                          \
+    case (S) * 6 + 2: pg_phase<NS, (S), true>(v, g.u[0], g.u[3], cs, f); break;              \
+    case (S) * 6 + 3: pg_phase<NS, (S), false>(v, g.u[0], g.u[3], cs, f); break;             \
+    case (S) * 6 + 4:                                                                        \
+        f ^= 1u << (S);                                                                      \
+        pg_phase<NS, (S), true>(v, g.u[1], g.u[2], 0, f);                                    \
+        break;                                                                               \
+    case (S) * 6 + 5: f ^= 1u << (S); break;
+                        PG_OPS(0)
+                        PG_OPS(1)
+                        PG_OPS(2)
+                        PG_OPS(3)
+#undef PG_OPS
                         default:
-                            if constexpr (R > 4) pg_slot<NS, (R > 4 ? 4 : 0)>(v, g, sub, cs, f);
+                            if (op >= 6 * R) {  // diagonal gate whose target is outside the registers
+                                const bool bit = (full0 & g.tmask_out) != 0;
+                                pg_diag_out<NS>(v, bit ? g.u[3] : g.u[0], cs, f, op == 6 * R);
+                            } else if constexpr (R > 4) {
+                                pg_slot<NS, (R > 4 ? 4 : 0)>(v, g, op - 24, cs, f);
+                            }
                             break;
                     }
                 }
