@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -56,6 +57,7 @@ using namespace qsim;
 struct qsim_state {
     int n = 0, enc = 0, P = 1, nl = 0, transport = 0, rank = 0, dev = 0, fuse = 1;
     int pass_r = 4;  // register qubits per pass stage (QSIM_PASS_R=5 selects 32-amplitude groups)
+    int use_mma = 1; // tensor-core (DMMA) pair stages in fused passes (QSIM_PASS_MMA=0 disables)
     size_t amp_bytes = 16;
     uint64_t alloc_amps = 0;  // max(2^nl, 256): small shards are padded with zero amplitudes
     Planner pl;
@@ -232,8 +234,9 @@ static int sweep_gate_e(qsim_state *s, const PlanOp &o, const double *u) {
 struct PassBuild {
     std::vector<int> ops;      // indices into the run, in execution order
     std::vector<int> high;     // local qubits >= PASS_LOW needed in the tile
-    std::vector<std::vector<int>> stage_q;     // per stage: register qubits (local qubit ids)
+    std::vector<std::vector<int>> stage_q;     // per stage: register qubits, or the pair (type 1)
     std::vector<std::vector<int>> stage_ops;   // per stage: op indices
+    std::vector<int> stage_type;               // 0 register stage, 1 tensor-core pair stage
 };
 
 // Qubits a gate acts on non-diagonally (X-type: the target of a dense /
@@ -265,14 +268,82 @@ static bool pass_add(PassBuild &pb, const PlanOp &o, int idx, int hmax) {
 // order, every remaining gate that commutes with all skipped earlier gates and
 // whose target fits the register set.  Returns false if more than
 // PASS_MAX_STAGES stages are needed (the caller then shortens the pass).
-static bool stage_pass(PassBuild &pb, const std::vector<PlanOp> &run, int RR) {
+static bool in_tile(const PassBuild &pb, int q, int nl) {
+    if (q < 0 || q >= nl) return false;
+    return q < PASS_LOW || std::find(pb.high.begin(), pb.high.end(), q) != pb.high.end();
+}
+// Qubits (target and controls) of a gate if it can join a tensor-core pair
+// stage: at most two, all in the tile.  Returns the count (0 = not pairable).
+static int pair_qubits(const PassBuild &pb, const PlanOp &o, int nl, int *q) {
+    int n = 0;
+    if (!in_tile(pb, o.l, nl)) return 0;
+    q[n++] = o.l;
+    for (int c = 0; c < o.nctrl; ++c) {
+        if (!in_tile(pb, o.ctrl[c], nl) || n >= 2) return 0;
+        q[n++] = o.ctrl[c];
+    }
+    return n;
+}
+
+static bool stage_pass(PassBuild &pb, const std::vector<PlanOp> &run, int RR, bool use_mma, int nl) {
     pb.stage_q.clear();
     pb.stage_ops.clear();
+    pb.stage_type.clear();
     std::vector<int> rem = pb.ops, order;
     while (!rem.empty()) {
         if ((int)pb.stage_q.size() >= PASS_MAX_STAGES) return false;
-        std::vector<int> R, taken, left;
+        std::vector<int> taken, left;
         uint64_t bx = 0, bz = 0;
+        // ---- tensor-core pair stage: every remaining gate acting only on the pair ----
+        int q0[2];
+        const int n0 = use_mma ? pair_qubits(pb, run[rem[0]], nl, q0) : 0;
+        if (n0 > 0) {
+            int a = q0[0], b = n0 == 2 ? q0[1] : -1;
+            if (b < 0) {  // partner: first commuting 2-qubit gate on a, else another 1-qubit gate's qubit
+                uint64_t sx = 0, sz = 0;
+                int alt = -1;
+                for (int k : rem) {
+                    const PlanOp &o = run[k];
+                    uint64_t xq, zq;
+                    gate_masks(o, xq, zq);
+                    const bool ok = !((xq & (sx | sz)) || (zq & sx));
+                    int q[2];
+                    const int nq = pair_qubits(pb, o, nl, q);
+                    if (ok && nq == 2 && (q[0] == a || q[1] == a)) {
+                        b = q[0] == a ? q[1] : q[0];
+                        break;
+                    }
+                    if (ok && nq == 1 && q[0] != a && alt < 0) alt = q[0];
+                    sx |= xq;
+                    sz |= zq;
+                }
+                if (b < 0) b = alt;
+                for (int t = 0; b < 0 && t < nl; ++t)
+                    if (t != a && in_tile(pb, t, nl)) b = t;
+            }
+            const uint64_t pm = (1ull << a) | (1ull << b);
+            for (int k : rem) {
+                const PlanOp &o = run[k];
+                uint64_t xq, zq;
+                gate_masks(o, xq, zq);
+                bool ok = !((xq & (bx | bz)) || (zq & bx)) && ((xq | zq) & ~pm) == 0 && o.l < nl;
+                if (ok) {
+                    taken.push_back(k);
+                } else {
+                    bx |= xq;
+                    bz |= zq;
+                    left.push_back(k);
+                }
+            }
+            pb.stage_q.push_back({a, b});
+            pb.stage_ops.push_back(taken);
+            pb.stage_type.push_back(1);
+            for (int k : taken) order.push_back(k);
+            rem.swap(left);
+            continue;
+        }
+        // ---- register stage: gates whose targets fit RR register qubits ----
+        std::vector<int> R;
         for (int k : rem) {
             const PlanOp &o = run[k];
             uint64_t xq, zq;
@@ -294,6 +365,7 @@ static bool stage_pass(PassBuild &pb, const std::vector<PlanOp> &run, int RR) {
         }
         pb.stage_q.push_back(R);
         pb.stage_ops.push_back(taken);
+        pb.stage_type.push_back(0);
         for (int k : taken) order.push_back(k);
         rem.swap(left);
     }
@@ -340,8 +412,69 @@ static int launch_pass(qsim_state *s, const PassBuild &pb, const std::vector<Pla
     const int RR = s->pass_r;
     p.R = RR;
     int gi = 0;
+    int nops4 = 0;
     for (int si = 0; si < p.nstages; ++si) {
         PassStage &st = p.st[si];
+        if (pb.stage_type[si] == 1) {
+            // tensor-core pair stage: lane bits 0,1 = the pair, lane bits 2-4 items,
+            // warp bits, fragment bits
+            const int a = pb.stage_q[si][0], b = pb.stage_q[si][1];
+            const int ta = tile_bit(a), tb = tile_bit(b);
+            std::vector<int> rest;
+            for (int t = 0; t < K; ++t)
+                if (t != ta && t != tb) rest.push_back(t);
+            // first item bit: residue mod 3 distinct from the pair's (conflict-free quarter warps)
+            int pick = 0;
+            for (size_t k2 = 0; k2 < rest.size(); ++k2)
+                if (rest[k2] % 3 != ta % 3 && rest[k2] % 3 != tb % 3) {
+                    pick = (int)k2;
+                    break;
+                }
+            std::vector<int> mb = {ta, tb, rest[pick]};
+            rest.erase(rest.begin() + pick);
+            for (int t : rest) mb.push_back(t);
+            for (int i = 0; i < K; ++i) st.mbits[i] = (int8_t)mb[i];
+            st.type = 1;
+            st.opi = (int8_t)nops4;
+            st.first_gate = (int8_t)gi;
+            st.ngates = 0;
+            // G = product of the stage's gates embedded in the pair basis c = bit(a) + 2 bit(b)
+            double G[4][4][2] = {};
+            for (int c = 0; c < 4; ++c) G[c][c][0] = 1.0;
+            for (int oi : pb.stage_ops[si]) {
+                const PlanOp &o = run[oi];
+                const double *u = us[oi];
+                double M[4][4][2] = {};
+                for (int c = 0; c < 4; ++c) M[c][c][0] = 1.0;
+                const int tm = (o.l == a) ? 1 : 2;
+                int cm = 0;
+                for (int c = 0; c < o.nctrl; ++c) cm |= (o.ctrl[c] == a) ? 1 : 2;
+                for (int c = 0; c < 4; ++c) {
+                    if ((c & tm) || (c & cm) != cm) continue;
+                    const int c1 = c | tm;
+                    M[c][c][0] = u[0]; M[c][c][1] = u[1];
+                    M[c][c1][0] = u[2]; M[c][c1][1] = u[3];
+                    M[c1][c][0] = u[4]; M[c1][c][1] = u[5];
+                    M[c1][c1][0] = u[6]; M[c1][c1][1] = u[7];
+                }
+                double N[4][4][2];
+                for (int r = 0; r < 4; ++r)
+                    for (int c = 0; c < 4; ++c) {
+                        double re = 0.0, im = 0.0;
+                        for (int m = 0; m < 4; ++m) {
+                            re += M[r][m][0] * G[m][c][0] - M[r][m][1] * G[m][c][1];
+                            im += M[r][m][0] * G[m][c][1] + M[r][m][1] * G[m][c][0];
+                        }
+                        N[r][c][0] = re;
+                        N[r][c][1] = im;
+                    }
+                std::memcpy(G, N, sizeof(G));
+            }
+            for (int r = 0; r < 4; ++r)
+                for (int c = 0; c < 4; ++c) p.op4[nops4][r * 4 + c] = make_double2(G[r][c][0], G[r][c][1]);
+            ++nops4;
+            continue;
+        }
         std::vector<int> R;
         for (int q : pb.stage_q[si]) R.push_back(tile_bit(q));
         for (int b = 0; (int)R.size() < RR; ++b)
@@ -449,6 +582,12 @@ static int launch_pass(qsim_state *s, const PassBuild &pb, const std::vector<Pla
         }
         st.ngates = (int8_t)(gi - st.first_gate);
     }
+    if (getenv("QSIM_DEBUG_PASSES")) {
+        std::string d = "pass: " + std::to_string(pb.ops.size()) + " gates, stages:";
+        for (int si = 0; si < p.nstages; ++si)
+            d += (pb.stage_type[si] ? " M" : " R") + std::to_string(pb.stage_ops[si].size());
+        fprintf(stderr, "%s\n", d.c_str());
+    }
     int grid = (int)std::min<uint64_t>(p.ntiles, (uint64_t)pass_e_max_grid(RR));
     s->st.stages += p.nstages;
     for (auto &sh : s->shards) {
@@ -498,7 +637,7 @@ static int run_gates_e(qsim_state *s, const std::vector<PlanOp> &run, const std:
             if ((int)pb.ops.size() >= PASS_MAX_GATES) break;
         }
         // form register stages; if the pass needs too many, give back its last gates
-        while (!stage_pass(pb, run, s->pass_r)) {
+        while (!stage_pass(pb, run, s->pass_r, s->use_mma && K >= 11 && s->pass_r == 4, s->nl)) {
             int k = pb.ops.back();
             pb.ops.pop_back();
             done[k] = 0;
@@ -829,6 +968,7 @@ int qsim_create_ex(const qsim_config *cfg, qsim_state **out) {
     s->rank = transport == QSIM_TRANSPORT_NCCL ? cfg->rank : 0;
     s->fuse = cfg->fuse;
     if (const char *pr = getenv("QSIM_PASS_R")) s->pass_r = (atoi(pr) == 4) ? 4 : 5;
+    if (const char *pm = getenv("QSIM_PASS_MMA")) s->use_mma = atoi(pm) != 0;
     s->amp_bytes = s->enc == QSIM_ENC_FP64 ? 16 : 2;
     if (cfg->device >= 0) {
         if (cudaSetDevice(cfg->device) != cudaSuccess) {

@@ -75,13 +75,20 @@ __host__ __device__ inline int pass_op(int kind, int slot, int R) {
     }
 }
 
+// A pass stage is either a register stage (type 0: gates applied with fp64
+// FMAs on 2^R register-resident amplitudes per thread) or a tensor-core pair
+// stage (type 1: one 4x4 complex operator on two tile qubits, applied with
+// mma.sync.m8n8k4.f64 -- lanes = 4 amplitudes of a quad x 8 items).
 struct PassStage {
-    int8_t rbits[PASS_R_MAX];  // slot s <-> tile bit rbits[s] (first R used)
-    int8_t gbits[PASS_MAX_K];  // group index bit i <-> tile bit gbits[i] (first K - R used)
+    int8_t rbits[PASS_R_MAX];  // type 0: slot s <-> tile bit rbits[s] (first R used)
+    int8_t gbits[PASS_MAX_K];  // type 0: group index bit i <-> tile bit gbits[i] (first K - R used)
+    int8_t mbits[PASS_MAX_K];  // type 1: lane bits 0-4, warp bits 5-6, fragment bits 7.. <-> tile bits
     int8_t first_gate;
     int8_t ngates;
-    int8_t needs_full;   // some gate of the stage tests bits outside the register set
-    int8_t pad;
+    int8_t needs_full;   // type 0: some gate of the stage tests bits outside the register set
+    int8_t type;
+    int8_t opi;          // type 1: index into PassParams::op4
+    int8_t pad[3];
 };
 
 struct PassParams {
@@ -96,7 +103,9 @@ struct PassParams {
     int32_t pad2;
     PassStage st[PASS_MAX_STAGES];
     PassGate g[PASS_MAX_GATES];
+    double2 op4[PASS_MAX_STAGES][16];  // type-1 operators G[c'][c], c = bit(qa) + 2 bit(qb)
 };
+static_assert(sizeof(PassParams) <= 32000, "kernel parameter block too large");
 void launch_pass_e(const PassParams &p, int grid, cudaStream_t s);
 int pass_e_max_grid(int R);
 int pass_e_max_k();  // tile qubits of the selected pass-kernel occupancy

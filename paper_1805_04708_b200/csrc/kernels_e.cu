@@ -240,11 +240,22 @@ __device__ __forceinline__ void pg_slot(double2 (&v)[NS], const SmGate &g, int s
     }
 }
 
+// D = A B + C for one m8n8k4 f64 tile (A: lane (r = lane>>2, k = lane&3);
+// B: lane (k = lane&3, n = lane>>2); D: lane (r, n = 2 (lane&3) + {0,1})).
+__device__ __forceinline__ void dmma_first(double &d0, double &d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%4};\n"
+                 : "=d"(d0), "=d"(d1) : "d"(a), "d"(b), "d"(0.0));
+}
+__device__ __forceinline__ void dmma_acc(double &d0, double &d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
 // Shared memory of one CTA: the tile (2^K double2, XOR-swizzled), the
 // two-level deposit tables of the high tile bits, the gate table, and per
 // stage the swizzled base address of every register group.
 struct PassSmemLayout {
-    size_t tile, depA, depB, depJ, gates, gx, total;
+    size_t tile, depA, depB, depJ, gates, gx, fbt, total;
 };
 __host__ __device__ inline PassSmemLayout pass_layout(int K, int R, int nstages) {
     PassSmemLayout L;
@@ -254,7 +265,8 @@ __host__ __device__ inline PassSmemLayout pass_layout(int K, int R, int nstages)
     L.depJ = L.depB + 32 * 8;
     L.gates = L.depJ + 32 * 8;
     L.gx = L.gates + PASS_MAX_GATES * sizeof(SmGate);
-    L.total = L.gx + (size_t)nstages * ((size_t)1 << (K - R)) * 2;
+    L.fbt = L.gx + (size_t)nstages * ((size_t)1 << (K - R)) * 2;
+    L.total = L.fbt + (size_t)nstages * 8 * 2;
     return L;
 }
 
@@ -269,6 +281,7 @@ __global__ void __launch_bounds__(PASS_THREADS, MINB) k_pass_e(const __grid_cons
     uint64_t *depB = reinterpret_cast<uint64_t *>(smem_raw + L.depB);  // high tile bits 5..
     SmGate *gates = reinterpret_cast<SmGate *>(smem_raw + L.gates);
     uint16_t *gx = reinterpret_cast<uint16_t *>(smem_raw + L.gx);
+    uint16_t *fbt = reinterpret_cast<uint16_t *>(smem_raw + L.fbt);
     const uint32_t tsize = 1u << K;
     const int h = K - PASS_LOW;
     const uint32_t ngroups = tsize >> R;
@@ -296,6 +309,13 @@ __global__ void __launch_bounds__(PASS_THREADS, MINB) k_pass_e(const __grid_cons
     }
     for (int s = 0; s < p.nstages; ++s) {
         const PassStage &st = p.st[s];
+        if (st.type == 1) {  // pair stage: thread base address (lane, warp bits) + fragment basis
+            uint32_t xl = 0;
+            for (int i = 0; i < 7; ++i) xl |= ((tid >> i) & 1u) << st.mbits[i];
+            gx[s * ngroups + tid] = (uint16_t)swz(xl);
+            if (tid < 8) fbt[s * 8 + tid] = (tid < 5 && 7 + (int)tid < K) ? (uint16_t)swz(1u << st.mbits[7 + tid]) : 0;
+            continue;
+        }
         for (uint32_t grp = tid; grp < ngroups; grp += PASS_THREADS) {
             uint32_t x0 = 0;
             for (int i = 0; i < K - R; ++i) x0 |= ((grp >> i) & 1u) << st.gbits[i];
@@ -329,6 +349,40 @@ __global__ void __launch_bounds__(PASS_THREADS, MINB) k_pass_e(const __grid_cons
         // ---- stages ----
         for (int s = 0; s < p.nstages; ++s) {
             const PassStage &st = p.st[s];
+            if (st.type == 1) {
+                // ---- tensor-core pair stage: amp' = G amp on the quad (lane bits 0,1) ----
+                // Real 8x8 form: k = c <-> Re(in_c), k = 4 + c <-> Im(in_c);
+                // n = 2c' <-> Re(out_c'), n = 2c' + 1 <-> Im(out_c').  A lane holds
+                // amp c of item r as (A chunk 0, A chunk 1) and receives amp'_c as (d0, d1).
+                // Per-thread base address and fragment-bit basis come from the
+                // per-CTA tables built at kernel start (GF(2)-linear swizzle).
+                const uint32_t sl = gx[s * ngroups + tid];
+                const uint16_t *fbs = fbt + s * 8;
+                const uint32_t fb0 = fbs[0], fb1 = fbs[1], fb2 = fbs[2], fb3 = fbs[3], fb4 = fbs[4];
+                const uint32_t off[8] = {0u, fb0, fb1, fb0 ^ fb1, fb2, fb0 ^ fb2, fb1 ^ fb2, fb0 ^ fb1 ^ fb2};
+                const uint32_t c = tid & 3u, nn = (tid & 31u) >> 2;
+                const double2 gcc = p.op4[st.opi][(nn >> 1) * 4 + c];  // G[c'][c]
+                const double b0 = (nn & 1u) ? gcc.y : gcc.x;            // B[c][n]
+                const double b1 = (nn & 1u) ? gcc.x : -gcc.y;           // B[4 + c][n]
+                const uint32_t nch = 1u << (K - 10);                     // chunks of 8 fragments
+                for (uint32_t ch = 0; ch < nch; ++ch) {
+                    const uint32_t cb = sl ^ ((ch & 1u) ? fb3 : 0u) ^ ((ch & 2u) ? fb4 : 0u);
+                    double2 v8[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) v8[j] = tile[cb ^ off[j]];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        double d0, d1;
+                        dmma_first(d0, d1, v8[j].x, b0);
+                        dmma_acc(d0, d1, v8[j].y, b1);
+                        v8[j] = make_double2(d0, d1);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) tile[cb ^ off[j]] = v8[j];
+                }
+                __syncthreads();
+                continue;
+            }
             // swz is linear over GF(2): swz(x0 | slot bits) = swz(x0) ^ xor of swz(slot bit)
             uint32_t sb[R];
 #pragma unroll
