@@ -253,12 +253,20 @@ static void gate_masks(const PlanOp &o, uint64_t &xq, uint64_t &zq) {
 
 // Try to append op `idx` to the pass (tile capacity only); false (no change)
 // if it does not fit.  Stages are formed afterwards by stage_pass().
-static bool pass_add(PassBuild &pb, const PlanOp &o, int idx, int hmax) {
+static bool pass_add(PassBuild &pb, const PlanOp &o, int idx, int hmax, int nl) {
     const bool needs_reg = o.cls != CLS_DIAG;
     if ((int)pb.ops.size() >= PASS_MAX_GATES) return false;
     bool new_high = needs_reg && o.l >= PASS_LOW && std::find(pb.high.begin(), pb.high.end(), o.l) == pb.high.end();
     if (new_high && (int)pb.high.size() >= hmax) return false;
     if (new_high) pb.high.push_back(o.l);
+    // bring a local control into the tile too when there is room: a controlled
+    // gate with all its qubits in the tile can join a tensor-core pair stage
+    if (needs_reg && o.nctrl == 1) {
+        const int c = o.ctrl[0];
+        if (c >= PASS_LOW && c < nl && (int)pb.high.size() < hmax &&
+            std::find(pb.high.begin(), pb.high.end(), c) == pb.high.end())
+            pb.high.push_back(c);
+    }
     pb.ops.push_back(idx);
     return true;
 }
@@ -628,7 +636,7 @@ static int run_gates_e(qsim_state *s, const std::vector<PlanOp> &run, const std:
             uint64_t xq, zq;
             gate_masks(run[k], xq, zq);
             const bool conflict = (xq & (bx | bz)) || (zq & bx);
-            if (!conflict && pass_add(pb, run[k], (int)k, K - PASS_LOW)) {
+            if (!conflict && pass_add(pb, run[k], (int)k, K - PASS_LOW, s->nl)) {
                 done[k] = 1;
             } else {
                 bx |= xq;
