@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(PASS_THREADS, MINB) k_pass_e(const __grid_cons
     const uint32_t s_tid = swz(tid);
     const uint64_t d_tid = (tid & LOWM) | dep(tid >> PASS_LOW);
     uint64_t *depJ = reinterpret_cast<uint64_t *>(smem_raw + L.depJ);  // dep(16 j): high tile bits >= 4
-    for (uint32_t j = tid; j < njt; j += PASS_THREADS) depJ[j] = dep(j << 4);
+    for (uint32_t j = tid; j < njt; j += PASS_THREADS) depJ[j] = dep(j << (7 - PASS_LOW));
     __syncthreads();
 
     for (uint64_t T = blockIdx.x; T < p.ntiles; T += gridDim.x) {

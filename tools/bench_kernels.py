@@ -15,7 +15,8 @@ n, layers = int(sys.argv[2]), int(sys.argv[3])
 fuse = int(sys.argv[4]) if len(sys.argv) > 4 else 1
 recipe = sys.argv[5] if len(sys.argv) > 5 else ("rzrx" if enc == q.ENC_ADAPTIVE2 else "layered")
 circ = {"layered": lambda: C.layered(n, layers, seed=1), "rzrx": lambda: C.rz_rx_cphase(n, layers, seed=4),
-        "qft": lambda: C.qft(n, seed=5)[0], "hwall": lambda: C.h_wall(n)}[recipe]()
+        "qft": lambda: C.qft(n, seed=5)[0], "hwall": lambda: C.h_wall(n), "ghz": lambda: C.ghz_chain(n),
+        "cfg1": lambda: C.random_circuit(n, 200 * layers, seed=0)}[recipe]()
 s = q.State(n, enc, 1, fuse=fuse)
 gates = q.pack_gates(circ)
 s.apply_circuit(gates)  # warm-up (also: the state is non-trivial for the timed run)
@@ -23,16 +24,16 @@ s.sync()
 s.reset_stats()
 s.profile(True)
 s.profile_read()
+reps = int(os.environ.get("REPS", "1"))
 t0 = time.perf_counter()
-s.apply_circuit(gates)
+for _ in range(reps):
+    s.apply_circuit(gates)
 s.sync()
-wall = time.perf_counter() - t0
+wall = (time.perf_counter() - t0) / reps
 prof = s.profile_read()
 st = s.stats()
-out = {"enc": sys.argv[1], "n": n, "recipe": recipe, "gates": len(circ), "wall_s": wall,
+out = {"enc": sys.argv[1], "n": n, "recipe": recipe, "gates": len(circ), "wall_s": wall, "reps": reps,
        "gates_per_s": len(circ) / wall, "stats": st,
        "kernels": {k: dict(v, avg_ms=v["ms"] / v["launches"], GBps=v["bytes"] / v["ms"] / 1e6,
                            TFLOPs=v["flops"] / v["ms"] / 1e9) for k, v in prof.items()}}
-if enc == q.ENC_ADAPTIVE2:
-    _, r0, r1 = (None, None, None)
 print(json.dumps(out))
