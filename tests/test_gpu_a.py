@@ -159,3 +159,22 @@ def test_a_readout_and_measure():
         mask = ((np.arange(1 << n) >> 4) & 1) == out
         assert np.all(zc[~mask] == 0)
         assert abs(np.vdot(zc, zc).real - 1) <= 0.02
+
+
+@pytest.mark.slow
+def test_max_size_a_n36_paper_workloads():
+    """BASELINE config 4's per-GPU size (2^36 codes = 128 GiB): the H wall and the
+    GHZ chain are exact in A (Tables 2-3 captions),
+    checked on sampled amplitudes and the per-qubit expectation values."""
+    n = 36
+    idx = np.random.default_rng(7).integers(0, 1 << n, 100000, dtype=np.uint64)
+    with q.State(n, q.ENC_ADAPTIVE2) as s:
+        s.apply_circuit(C.h_wall(n))
+        assert np.max(np.abs(s.get_amplitudes(idx) - 2.0 ** (-n / 2))) <= 1e-15
+        p = s.probabilities()
+        assert np.max(np.abs(p - 0.5)) <= 1e-12
+        s.reset()
+        s.apply_circuit(C.ghz_chain(n))
+        z = s.get_amplitudes(np.array([0, (1 << n) - 1, 12345, 1 << 35], dtype=np.uint64))
+        assert np.max(np.abs(z - np.array([1, 1, 0, 0]) / math.sqrt(2))) <= 1e-15
+        assert np.max(np.abs(s.probabilities() - 0.5)) <= 1e-15

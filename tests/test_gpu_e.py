@@ -289,3 +289,32 @@ def test_full_size_config2_vs_oracle_sampled():
     ref = oracle.e_simulate(n, circ)
     assert np.max(np.abs(got - ref[idx.astype(np.int64)])) <= TOL
     assert abs(nrm - 1) <= 1e-10
+
+
+@pytest.mark.slow
+def test_max_size_config3_n33_product_pin_and_qft():
+    """BASELINE config 3's per-GPU size (2^33 amplitudes = 128 GiB of HBM): the
+    config-3 recipe (H wall + 10 layers of Haar U(2), CNOTs removed) against the
+    product-state closed form (Eq. appa2) on 10^5 sampled amplitudes, then the
+    QFT closed form at the same size (the largest E state one B200 holds)."""
+    n = 33
+    circ = C.layered(n, 10, seed=3, entangle=False)
+    v = [np.array([1, 0], dtype=np.complex128) for _ in range(n)]
+    for g in range(len(circ)):
+        _, _, t, _, _, u = circ.gate(g)
+        v[t] = u @ v[t]
+    V = np.array(v)
+    idx = np.random.default_rng(5).integers(0, 1 << n, 100000, dtype=np.uint64)
+    bits = ((idx[:, None] >> np.arange(n, dtype=np.uint64)[None, :]) & np.uint64(1)).astype(np.int64)
+    ref = np.prod(V[np.arange(n)[None, :], bits], axis=1)
+    with q.State(n) as s:
+        s.apply_circuit(circ)
+        assert np.max(np.abs(s.get_amplitudes(idx) - ref)) <= TOL
+        assert abs(s.norm() - 1) <= 1e-10
+        s.reset()
+        qc, x = C.qft(n, seed=5)
+        s.apply_circuit(qc)
+        y = np.random.default_rng(6).integers(0, 1 << n, 100000, dtype=np.uint64)
+        ph = ((np.uint64(x) * y) % np.uint64(1 << n)).astype(np.float64) * (2 * math.pi / (1 << n))
+        assert np.max(np.abs(s.get_amplitudes(y) - 2.0 ** (-n / 2) * np.exp(1j * ph))) <= TOL
+        assert np.max(np.abs(s.probabilities() - 0.5)) <= 1e-12
