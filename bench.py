@@ -225,12 +225,15 @@ def main():
     import paper_1805_04708_b200 as q
 
     dist = None
-    if world > 1:
+    # BENCH_FORCE_DIST=1 takes the multi-GPU code path (process group, NCCL
+    # transport) even with one rank -- a one-GPU check of the N>1 plumbing.
+    use_dist = world > 1 or os.environ.get("BENCH_FORCE_DIST") == "1"
+    if use_dist:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n, circ, name = workload(world)
-    if world > 1:
+    if use_dist:
         obj = [q.qsim_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         s = q.State(n, q.ENC_FP64, world, transport=q.TRANSPORT_NCCL, rank=rank, device=local,

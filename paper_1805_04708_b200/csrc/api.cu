@@ -849,7 +849,7 @@ static int phys_probs(qsim_state *s, std::vector<double> &phys) {
         for (int b = s->nl; b < s->n; ++b)
             if (rank_bit(sh, b, s->nl)) phys[1 + b] += s->h_out[0];
     }
-    if (s->transport == QSIM_TRANSPORT_NCCL && s->P > 1) {
+    if (s->transport == QSIM_TRANSPORT_NCCL) {
         CU(cudaMemcpyAsync(s->d_out, phys.data(), phys.size() * sizeof(double), cudaMemcpyHostToDevice, s->stream));
         NC(ncclAllReduce(s->d_out, s->d_out, phys.size(), ncclFloat64, ncclSum, s->comm, s->stream));
         CU(cudaMemcpyAsync(phys.data(), s->d_out, phys.size() * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
@@ -952,7 +952,9 @@ int qsim_create_ex(const qsim_config *cfg, qsim_state **out) {
         set_error("a sharded state needs at least 10 local qubits (N - log2(P) >= 10)");
         return QSIM_EINVAL;
     }
-    const int transport = (P == 1) ? QSIM_TRANSPORT_LOCAL : cfg->transport;
+    // nshards = 1 defaults to LOCAL; an explicit NCCL request with one rank is honoured
+    // (communicator + collective read-out paths, used to test NCCL on one GPU)
+    const int transport = (P == 1 && cfg->transport != QSIM_TRANSPORT_NCCL) ? QSIM_TRANSPORT_LOCAL : cfg->transport;
     if (transport != QSIM_TRANSPORT_LOCAL && transport != QSIM_TRANSPORT_NCCL) {
         set_error("unknown transport");
         return QSIM_EINVAL;
@@ -1265,7 +1267,7 @@ int qsim_expectations(qsim_state *s, double *q) {
             RC(pair_sums_local(s, l, Sr[lq], Si[lq]));
         }
     }
-    if (s->transport == QSIM_TRANSPORT_NCCL && s->P > 1) {
+    if (s->transport == QSIM_TRANSPORT_NCCL) {
         std::vector<double> v(2 * s->n);
         for (int i = 0; i < s->n; ++i) {
             v[i] = Sr[i];
@@ -1402,7 +1404,7 @@ int qsim_get_amplitudes(qsim_state *s, const uint64_t *idx, size_t m, double *ou
             res[2 * which[k] + 1] = tmp[2 * k + 1];
         }
     }
-    if (rc == QSIM_OK && s->transport == QSIM_TRANSPORT_NCCL && s->P > 1) {
+    if (rc == QSIM_OK && s->transport == QSIM_TRANSPORT_NCCL) {
         double *d_all = nullptr;
         if (cudaMalloc(&d_all, res.size() * 8) == cudaSuccess) {
             cudaMemcpyAsync(d_all, res.data(), res.size() * 8, cudaMemcpyHostToDevice, s->stream);
@@ -1451,7 +1453,7 @@ int qsim_get_state(qsim_state *s, double *out) {
             launch_to_logical_a(sh.amps, 1ull << s->nl, shard_base(s, sh), d_inv, s->n, s->atab, d_full, s->stream);
         s->st.kernels++;
     }
-    if (s->transport == QSIM_TRANSPORT_NCCL && s->P > 1)
+    if (s->transport == QSIM_TRANSPORT_NCCL)
         NC(ncclAllReduce(d_full, d_full, 2 * dim, ncclFloat64, ncclSum, s->comm, s->stream));
     CU(cudaMemcpyAsync(out, d_full, dim * 16, cudaMemcpyDeviceToHost, s->stream));
     CU(cudaStreamSynchronize(s->stream));
@@ -1570,7 +1572,7 @@ static int dense_gate_a(qsim_state *s, const PlanOp &o, const double *u) {
         mn = std::min(mn, s->h_out[0]);
         mx = std::max(mx, s->h_out[1]);
     }
-    if (s->transport == QSIM_TRANSPORT_NCCL && s->P > 1) {
+    if (s->transport == QSIM_TRANSPORT_NCCL) {
         s->h_out[0] = mn;
         s->h_out[1] = -mx;
         CU(cudaMemcpyAsync(s->d_out, s->h_out, 2 * sizeof(double), cudaMemcpyHostToDevice, s->stream));
@@ -1647,7 +1649,7 @@ int measure_collapse_a(qsim_state *s, int b, int out, double f) {
         mn = std::min(mn, s->h_out[0]);
         mx = std::max(mx, s->h_out[1]);
     }
-    if (s->transport == QSIM_TRANSPORT_NCCL && s->P > 1) {
+    if (s->transport == QSIM_TRANSPORT_NCCL) {
         s->h_out[0] = mn;
         s->h_out[1] = -mx;
         CU(cudaMemcpyAsync(s->d_out, s->h_out, 2 * sizeof(double), cudaMemcpyHostToDevice, s->stream));

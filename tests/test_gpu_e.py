@@ -318,3 +318,32 @@ def test_max_size_config3_n33_product_pin_and_qft():
         ph = ((np.uint64(x) * y) % np.uint64(1 << n)).astype(np.float64) * (2 * math.pi / (1 << n))
         assert np.max(np.abs(s.get_amplitudes(y) - 2.0 ** (-n / 2) * np.exp(1j * ph))) <= TOL
         assert np.max(np.abs(s.probabilities() - 0.5)) <= 1e-12
+
+
+def test_nccl_transport_single_rank():
+    """The NCCL transport with one rank on one GPU: communicator creation from a
+    qsim_nccl_unique_id, and every collective read-out path (probabilities,
+    expectations, amplitudes, state, measure; A bounds all-reduce)."""
+    uid = q.qsim_nccl_unique_id()
+    assert len(uid) == 128
+    n = 14
+    circ = C.config(0, seed=3)
+    ref = oracle.e_simulate(n, circ)
+    s = q.State(n, q.ENC_FP64, 1, transport=q.TRANSPORT_NCCL, rank=0, nccl_id=uid)
+    s.apply_circuit(circ)
+    assert np.max(np.abs(s.get_state() - ref)) <= TOL
+    assert np.max(np.abs(s.probabilities() - oracle.e_probabilities(ref, n))) <= TOL
+    assert np.max(np.abs(s.expectations() - oracle.e_expectations(ref, n))) <= TOL
+    idx = np.arange(0, 1 << n, 7, dtype=np.uint64)
+    assert np.max(np.abs(s.get_amplitudes(idx) - ref[idx.astype(np.int64)])) <= TOL
+    out, p0 = s.measure_u(2, 0.4)
+    ro, rp0 = oracle.e_measure(ref, n, 2, 0.4)
+    assert out == ro and abs(p0 - rp0) <= 1e-12
+    s.close()
+    a = q.State(12, q.ENC_ADAPTIVE2, 1, transport=q.TRANSPORT_NCCL, rank=0, nccl_id=q.qsim_nccl_unique_id())
+    ca = C.rz_rx_cphase(12, 2, seed=4)
+    a.apply_circuit(ca)
+    codes, r0, r1 = a.get_codes()
+    ra = oracle.AState(12).run(ca)
+    assert r0 == pytest.approx(ra.r0, rel=1e-12) and r1 == pytest.approx(ra.r1, rel=1e-12)
+    a.close()
