@@ -169,6 +169,12 @@ int qsim_expectations(qsim_state *s, double *q);
 int qsim_measure(qsim_state *s, int qubit, uint64_t seed, int *outcome);
 int qsim_measure_u(qsim_state *s, int qubit, double u, int *outcome, double *p0_out);
 
+/* CLEAR (value 0) / SET (value 1) of App. B: project
+ * `qubit` onto |value> and renormalise.  EZERONORM if the projected state has
+ * norm^2 < 1e-14 ("fails if the projection results in a state with amplitude
+ * zero"); the state is then unchanged. */
+int qsim_project(qsim_state *s, int qubit, int value);
+
 /* Amplitudes at `n` LOGICAL basis indices (each < 2^N), written as
  * out[2k] = re, out[2k+1] = im (decoded for A).  For NCCL every rank
  * calls it collectively and receives all n values. */

@@ -52,6 +52,7 @@ def lib():
         L.oracle_e_expectations.argtypes = [_dp, ctypes.c_int, _dp]
         L.oracle_e_probabilities.argtypes = [_dp, ctypes.c_int, _dp]
         L.oracle_e_measure.argtypes = [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_double, _dp]
+        L.oracle_e_project.argtypes = [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         L.oracle_a_decode.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double, _dp, _dp]
         L.oracle_a_encode.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                       ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
@@ -136,6 +137,11 @@ def e_measure(a: np.ndarray, n: int, qubit: int, u_draw: float):
     p0 = ctypes.c_double(0.0)
     out = lib().oracle_e_measure(_ptr(_c128(a).view(np.float64), _dp), n, qubit, float(u_draw), ctypes.byref(p0))
     return out, p0.value
+
+
+def e_project(a: np.ndarray, n: int, qubit: int, value: int) -> int:
+    """CLEAR / SET: project onto |value> of qubit, renormalise; -5 on zero norm."""
+    return lib().oracle_e_project(_ptr(_c128(a).view(np.float64), _dp), n, qubit, value)
 
 
 # ----------------------------------------------------------------------------- A

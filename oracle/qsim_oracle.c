@@ -201,6 +201,31 @@ int oracle_e_measure(double *a, int n, int qubit, double u_draw, double *p0_out)
     return outcome;
 }
 
+/* CLEAR / SET (App. B): the projector |v><v| on qubit n,
+ * followed by renormalisation; returns -5 if the projected norm^2 < 1e-14
+ * ("fails if the projection results in a state with amplitude zero"), leaving
+ * the state unchanged. */
+int oracle_e_project(double *a, int n, int qubit, int value)
+{
+    uint64_t dim = (uint64_t)1 << n;
+    uint64_t b = (uint64_t)1 << qubit;
+    long double keep = 0.0L;
+    for (uint64_t i = 0; i < dim; ++i)
+        if (((i & b) ? 1 : 0) == value) keep += (long double)a[2 * i] * a[2 * i] + (long double)a[2 * i + 1] * a[2 * i + 1];
+    if (keep < 1e-14L) return -5;
+    double scale = (double)(1.0L / sqrtl(keep));
+    for (uint64_t i = 0; i < dim; ++i) {
+        if (((i & b) ? 1 : 0) != value) {
+            a[2 * i] = 0.0;
+            a[2 * i + 1] = 0.0;
+        } else {
+            a[2 * i] *= scale;
+            a[2 * i + 1] *= scale;
+        }
+    }
+    return 0;
+}
+
 /* ------------------------------------------------------------------------ */
 /* A: adaptive 2-byte polar encoding, §4.1             */
 /* Codes are stored interleaved: code[2i] = b0 (magnitude), code[2i+1] = b1   */

@@ -84,7 +84,7 @@ EXPORTS = (
     "qsim_create", "qsim_create_ex", "qsim_destroy", "qsim_nccl_unique_id", "qsim_apply_gate", "qsim_apply_swap",
     "qsim_apply_circuit", "qsim_norm", "qsim_probabilities", "qsim_expectations", "qsim_measure", "qsim_measure_u",
     "qsim_get_amplitudes", "qsim_get_state", "qsim_set_state", "qsim_get_codes", "qsim_set_codes", "qsim_sync",
-    "qsim_stream", "qsim_get_stats", "qsim_reset", "qsim_profile", "qsim_profile_read", "qsim_reset_stats", "qsim_get_qubit_map", "qsim_last_error",
+    "qsim_project", "qsim_stream", "qsim_get_stats", "qsim_reset", "qsim_profile", "qsim_profile_read", "qsim_reset_stats", "qsim_get_qubit_map", "qsim_last_error",
     "qsim_plan_create", "qsim_plan_num_ops", "qsim_plan_get_op", "qsim_plan_final_map", "qsim_plan_destroy",
 )
 
@@ -110,6 +110,7 @@ _lib.qsim_probabilities.argtypes = [_P, _dp]
 _lib.qsim_expectations.argtypes = [_P, _dp]
 _lib.qsim_measure.argtypes = [_P, ctypes.c_int, ctypes.c_uint64, _ip]
 _lib.qsim_measure_u.argtypes = [_P, ctypes.c_int, ctypes.c_double, _ip, _dp]
+_lib.qsim_project.argtypes = [_P, ctypes.c_int, ctypes.c_int]
 _lib.qsim_get_amplitudes.argtypes = [_P, ctypes.POINTER(ctypes.c_uint64), ctypes.c_size_t, _dp]
 _lib.qsim_get_state.argtypes = [_P, _dp]
 _lib.qsim_set_state.argtypes = [_P, _dp]
@@ -262,6 +263,11 @@ def qsim_measure_u(h, qubit, u):
     return o.value, p0.value
 
 
+def qsim_project(h, qubit, value):
+    """CLEAR (value=0) / SET (value=1): project and renormalise (PAPER.md:1474-1493)."""
+    _check(_lib.qsim_project(h, qubit, value))
+
+
 def qsim_get_amplitudes(h, idx) -> np.ndarray:
     idx = np.ascontiguousarray(idx, dtype=np.uint64)
     out = np.empty(idx.size, dtype=np.complex128)
@@ -408,6 +414,10 @@ class State:
 
     def measure_u(self, qubit, u):
         return qsim_measure_u(self.h, qubit, u)
+
+    def project(self, qubit, value):
+        qsim_project(self.h, qubit, value)
+        return self
 
     def get_amplitudes(self, idx):
         return qsim_get_amplitudes(self.h, idx)

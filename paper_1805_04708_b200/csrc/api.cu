@@ -1006,6 +1006,18 @@ int qsim_create_ex(const qsim_config *cfg, qsim_state **out) {
         s->shards.resize(P);
         for (int r = 0; r < P; ++r) s->shards[r].index = r;
     }
+    // capacity check before any allocation (also guards 2^nl * bytes overflow)
+    {
+        size_t free_b = 0, total_b = 0;
+        cudaMemGetInfo(&free_b, &total_b);
+        const double need = std::ldexp((double)s->amp_bytes, nl) * (double)s->shards.size();
+        if (nl > 40 || need > (double)total_b) {
+            set_error("state needs " + std::to_string(need) + " B on this device (2^" + std::to_string(nl) + " x " +
+                      std::to_string(s->amp_bytes) + " B x " + std::to_string(s->shards.size()) +
+                      " shard(s)); the device has " + std::to_string((double)total_b) + " B");
+            return fail(QSIM_ENOMEM);
+        }
+    }
     s->alloc_amps = std::max<uint64_t>(1ull << nl, 256);
     const size_t shard_bytes = s->alloc_amps * s->amp_bytes;
     for (auto &sh : s->shards) {
@@ -1298,20 +1310,8 @@ static uint64_t splitmix64(uint64_t x) {
     return x ^ (x >> 31);
 }
 
-int qsim_measure_u(qsim_state *s, int qubit, double u, int *outcome, double *p0_out) {
-    if (!s || !outcome || qubit < 0 || qubit >= s->n) {
-        set_error("qsim_measure: bad qubit or null outcome");
-        return QSIM_EINVAL;
-    }
-    cudaSetDevice(s->dev);
-    std::vector<double> phys;
-    RC(phys_probs(s, phys));
-    const int b = s->pl.pos[qubit];
-    const double s1 = phys[1 + b], s0 = phys[0] - s1;
-    const double p0 = s0 / phys[0];
-    if (p0_out) *p0_out = p0;
-    const int out = (u < p0) ? 0 : 1;
-    const double keep = out ? s1 : s0;
+// Project qubit onto `out` and renormalise (M's collapse, CLEAR / SET).
+static int collapse(qsim_state *s, int b, int out, double keep) {
     if (!(keep >= 1e-14)) {
         set_error("projection onto a state with norm^2 < 1e-14 (PAPER.md:1481)");
         return QSIM_EZERONORM;
@@ -1332,8 +1332,38 @@ int qsim_measure_u(qsim_state *s, int qubit, double u, int *outcome, double *p0_
         RC(measure_collapse_a(s, b, out, f));
     }
     CU(cudaStreamSynchronize(s->stream));
+    return QSIM_OK;
+}
+
+int qsim_measure_u(qsim_state *s, int qubit, double u, int *outcome, double *p0_out) {
+    if (!s || !outcome || qubit < 0 || qubit >= s->n) {
+        set_error("qsim_measure: bad qubit or null outcome");
+        return QSIM_EINVAL;
+    }
+    cudaSetDevice(s->dev);
+    std::vector<double> phys;
+    RC(phys_probs(s, phys));
+    const int b = s->pl.pos[qubit];
+    const double s1 = phys[1 + b], s0 = phys[0] - s1;
+    const double p0 = s0 / phys[0];
+    if (p0_out) *p0_out = p0;
+    const int out = (u < p0) ? 0 : 1;
+    RC(collapse(s, b, out, out ? s1 : s0));
     *outcome = out;
     return QSIM_OK;
+}
+
+int qsim_project(qsim_state *s, int qubit, int value) {
+    if (!s || qubit < 0 || qubit >= s->n || (value != 0 && value != 1)) {
+        set_error("qsim_project: bad qubit or value (0 = CLEAR, 1 = SET)");
+        return QSIM_EINVAL;
+    }
+    cudaSetDevice(s->dev);
+    std::vector<double> phys;
+    RC(phys_probs(s, phys));
+    const int b = s->pl.pos[qubit];
+    const double s1 = phys[1 + b], s0 = phys[0] - s1;
+    return collapse(s, b, value, value ? s1 : s0);
 }
 
 int qsim_measure(qsim_state *s, int qubit, uint64_t seed, int *outcome) {

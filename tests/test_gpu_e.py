@@ -347,3 +347,26 @@ def test_nccl_transport_single_rank():
     ra = oracle.AState(12).run(ca)
     assert r0 == pytest.approx(ra.r0, rel=1e-12) and r1 == pytest.approx(ra.r1, rel=1e-12)
     a.close()
+
+
+@pytest.mark.parametrize("P", [1, 4])
+def test_clear_set(P):
+    """CLEAR / SET through qsim_project (incl. a global qubit when sharded)."""
+    n = 12
+    circ = C.config(0, n=n, seed=31)
+    ref = oracle.e_simulate(n, circ)
+    with gpu_run(n, circ, ngpus=P) as s:
+        for qubit, value in [(0, 1), (11, 0), (6, 1)]:
+            s.project(qubit, value)
+            assert oracle.e_project(ref, n, qubit, value) == 0
+            assert np.max(np.abs(s.get_state() - ref)) <= TOL
+        with pytest.raises(q.QsimError) as e:
+            s.project(0, 0)  # qubit 0 is already |1>
+        assert e.value.code == q.QSIM_EZERONORM
+        assert np.max(np.abs(s.get_state() - ref)) <= TOL
+
+
+def test_too_large_state_is_enomem():
+    with pytest.raises(q.QsimError) as e:
+        q.State(40)  # 16 TiB
+    assert e.value.code == q.QSIM_ENOMEM

@@ -220,3 +220,19 @@ def test_measure_projects_and_renormalises():
     # zero-norm projection fails
     z = oracle.e_init(n)
     assert oracle.e_measure(z, n, 0, 1.0)[0] == -5  # u = 1 forces outcome 1, p1 = 0
+
+
+def test_clear_set_vs_dense_projector():
+    """CLEAR / SET: (|v><v|_n x I) psi / ||...||; failure on zero norm."""
+    n = 6
+    a = oracle.e_simulate(n, C.layered(n, 2, seed=12))  # every qubit in superposition
+    for qubit in (0, 3, 5):
+        for value in (0, 1):
+            P = np.diag([1.0 - value, float(value)]).astype(np.complex128)
+            ref = kron_ops(n, {qubit: P}) @ a
+            ref /= np.linalg.norm(ref)
+            b = a.copy()
+            assert oracle.e_project(b, n, qubit, value) == 0
+            assert np.max(np.abs(b - ref)) <= 1e-14
+    z = oracle.e_init(n)
+    assert oracle.e_project(z, n, 2, 1) == -5 and z[0] == 1

@@ -10,13 +10,38 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1805_04708_b200 as q  # noqa: E402
 import qsim_inputs as C  # noqa: E402
 
+def pairs(n, layers):
+    """Synthetic: layers x (Haar on qubits 0..11, CNOT 2i -> 2i+1): pure pair blocks."""
+    import numpy as np
+    rng = np.random.default_rng(0)
+    c = C.Circuit(n)
+    for _ in range(layers):
+        for i in range(6):
+            c.add("Haar", C.mat_haar(rng), 2 * i)
+            c.add("Haar", C.mat_haar(rng), 2 * i + 1)
+            c.add("CNOT", C.mat_X(), 2 * i + 1, [2 * i])
+    return c
+
+
+def singles(n, layers):
+    """Synthetic: layers x Haar on qubits 0..11 (no entanglers)."""
+    import numpy as np
+    rng = np.random.default_rng(0)
+    c = C.Circuit(n)
+    for _ in range(layers):
+        for i in range(12):
+            c.add("Haar", C.mat_haar(rng), i)
+    return c
+
+
 enc = q.ENC_ADAPTIVE2 if sys.argv[1] == "A" else q.ENC_FP64
 n, layers = int(sys.argv[2]), int(sys.argv[3])
 fuse = int(sys.argv[4]) if len(sys.argv) > 4 else 1
 recipe = sys.argv[5] if len(sys.argv) > 5 else ("rzrx" if enc == q.ENC_ADAPTIVE2 else "layered")
 circ = {"layered": lambda: C.layered(n, layers, seed=1), "rzrx": lambda: C.rz_rx_cphase(n, layers, seed=4),
         "qft": lambda: C.qft(n, seed=5)[0], "hwall": lambda: C.h_wall(n), "ghz": lambda: C.ghz_chain(n),
-        "cfg1": lambda: C.random_circuit(n, 200 * layers, seed=0)}[recipe]()
+        "cfg1": lambda: C.random_circuit(n, 200 * layers, seed=0), "pairs": lambda: pairs(n, layers),
+        "single": lambda: singles(n, layers)}[recipe]()
 s = q.State(n, enc, 1, fuse=fuse)
 gates = q.pack_gates(circ)
 s.apply_circuit(gates)  # warm-up (also: the state is non-trivial for the timed run)
