@@ -169,6 +169,14 @@ int qsim_expectations(qsim_state *s, double *q);
 int qsim_measure(qsim_state *s, int qubit, uint64_t seed, int *outcome);
 int qsim_measure_u(qsim_state *s, int qubit, double u, int *outcome, double *p0_out);
 
+/* GENERATE EVENTS (App. B): draw `nsamples` basis states
+ * (LOGICAL indices, written to out[0..nsamples)) from |a|^2, without changing
+ * the state.  Event k uses u_k = (splitmix64(seed + k) >> 11) * 2^-53 and is the
+ * smallest logical index L with cumsum_{L' <= L} |a_L'|^2 > u_k * norm^2
+ * (inverse CDF in logical order).  Needs 8 B x 2^N of scratch (N <= 34);
+ * EUNSUPPORTED for the multi-process NCCL transport; EZERONORM for a zero state. */
+int qsim_sample(qsim_state *s, size_t nsamples, uint64_t seed, uint64_t *out);
+
 /* CLEAR (value 0) / SET (value 1) of App. B: project
  * `qubit` onto |value> and renormalise.  EZERONORM if the projected state has
  * norm^2 < 1e-14 ("fails if the projection results in a state with amplitude

@@ -52,6 +52,7 @@ def lib():
         L.oracle_e_expectations.argtypes = [_dp, ctypes.c_int, _dp]
         L.oracle_e_probabilities.argtypes = [_dp, ctypes.c_int, _dp]
         L.oracle_e_measure.argtypes = [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_double, _dp]
+        L.oracle_e_sample.argtypes = [_dp, ctypes.c_int, _dp, ctypes.c_int64, ctypes.POINTER(ctypes.c_uint64)]
         L.oracle_e_project.argtypes = [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         L.oracle_a_decode.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double, _dp, _dp]
         L.oracle_a_encode.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
@@ -137,6 +138,15 @@ def e_measure(a: np.ndarray, n: int, qubit: int, u_draw: float):
     p0 = ctypes.c_double(0.0)
     out = lib().oracle_e_measure(_ptr(_c128(a).view(np.float64), _dp), n, qubit, float(u_draw), ctypes.byref(p0))
     return out, p0.value
+
+
+def e_sample(a: np.ndarray, n: int, u) -> np.ndarray:
+    """GENERATE EVENTS: inverse-CDF indices for caller-drawn u in [0,1)."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    out = np.empty(u.size, dtype=np.uint64)
+    lib().oracle_e_sample(_ptr(_c128(a).view(np.float64), _dp), n, _ptr(u, _dp), u.size,
+                          out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)))
+    return out
 
 
 def e_project(a: np.ndarray, n: int, qubit: int, value: int) -> int:

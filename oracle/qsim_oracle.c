@@ -201,6 +201,30 @@ int oracle_e_measure(double *a, int n, int qubit, double u_draw, double *p0_out)
     return outcome;
 }
 
+/* GENERATE EVENTS (App. B): for each caller-drawn
+ * u_k in [0,1), the smallest index L with sum_{L' <= L} |a_L'|^2 > u_k * total
+ * (inverse CDF over the basis index order; cumulative sums in long double). */
+void oracle_e_sample(const double *a, int n, const double *u, int64_t nsamp, uint64_t *out)
+{
+    uint64_t dim = (uint64_t)1 << n;
+    long double *cum = (long double *)malloc(sizeof(long double) * dim);
+    long double run = 0.0L;
+    for (uint64_t i = 0; i < dim; ++i) {
+        run += (long double)a[2 * i] * a[2 * i] + (long double)a[2 * i + 1] * a[2 * i + 1];
+        cum[i] = run;
+    }
+    for (int64_t k = 0; k < nsamp; ++k) {
+        long double t = (long double)u[k] * run;
+        uint64_t lo = 0, hi = dim - 1; /* first i with cum[i] > t */
+        while (lo < hi) {
+            uint64_t mid = lo + (hi - lo) / 2;
+            if (cum[mid] > t) hi = mid; else lo = mid + 1;
+        }
+        out[k] = lo;
+    }
+    free(cum);
+}
+
 /* CLEAR / SET (App. B): the projector |v><v| on qubit n,
  * followed by renormalisation; returns -5 if the projected norm^2 < 1e-14
  * ("fails if the projection results in a state with amplitude zero"), leaving

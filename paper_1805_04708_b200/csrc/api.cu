@@ -1366,6 +1366,28 @@ int qsim_project(qsim_state *s, int qubit, int value) {
     return collapse(s, b, value, value ? s1 : s0);
 }
 
+int qsim_sample(qsim_state *s, size_t nsamples, uint64_t seed, uint64_t *out) {
+    if (!s || (nsamples && !out)) return QSIM_EINVAL;
+    if (s->transport == QSIM_TRANSPORT_NCCL && s->P > 1) {
+        set_error("qsim_sample: not implemented for the multi-process NCCL transport");
+        return QSIM_EUNSUPPORTED;
+    }
+    if (s->n > 34) {
+        set_error("qsim_sample needs an 8 B x 2^N probability array (N <= 34)");
+        return QSIM_EINVAL;
+    }
+    cudaSetDevice(s->dev);
+    std::vector<void *> amps;
+    std::vector<uint64_t> bases;
+    for (auto &sh : s->shards) {
+        amps.push_back(sh.amps);
+        bases.push_back(shard_base(s, sh));
+    }
+    s->st.kernels += 4;
+    return sample_logical(amps.data(), bases.data(), (int)amps.size(), s->nl, s->n, s->pl.inv.data(), s->enc, s->atab,
+                          nsamples, seed, out, s->stream);
+}
+
 int qsim_measure(qsim_state *s, int qubit, uint64_t seed, int *outcome) {
     uint64_t x = splitmix64(seed);
     double u = (double)(x >> 11) * (1.0 / 9007199254740992.0);

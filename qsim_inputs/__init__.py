@@ -347,3 +347,18 @@ def random_codes(n: int, seed: int, frac_zero: float = 0.05, frac_one: float = 0
     r0 = float(rng.uniform(0.05, 0.2)) * 2.0 ** (-n / 2)
     r1 = r0 + float(rng.uniform(1.0, 4.0)) * 2.0 ** (-n / 2)
     return codes, r0, r1
+
+
+def splitmix_uniform(seed: int, count: int) -> np.ndarray:
+    """The counter-based draws of qsim_measure / qsim_sample (include/qsim.h):
+    u_k = (splitmix64(seed + k) >> 11) * 2^-53, k = 0..count-1.  Both the CUDA
+    side and the oracle side use exactly these numbers."""
+    M = (1 << 64) - 1
+    out = np.empty(count, dtype=np.float64)
+    for i in range(count):
+        x = (seed + i + 0x9E3779B97F4A7C15) & M
+        x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M
+        x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & M
+        x ^= x >> 31
+        out[i] = (x >> 11) * (1.0 / 9007199254740992.0)
+    return out

@@ -370,3 +370,24 @@ def test_too_large_state_is_enomem():
     with pytest.raises(q.QsimError) as e:
         q.State(40)  # 16 TiB
     assert e.value.code == q.QSIM_ENOMEM
+
+
+@pytest.mark.parametrize("P", [1, 4])
+def test_generate_events(P):
+    """GENERATE EVENTS on the GPU == the oracle's inverse CDF for the same
+    counter-based draws (up to draws within 1e-12 of a CDF boundary), in
+    logical order even after deferred swaps."""
+    n = 13
+    circ = C.layered(n, 2, seed=8)
+    circ.swap(0, 12)
+    ref = oracle.e_simulate(n, circ)
+    with gpu_run(n, circ, ngpus=P) as s:
+        got = s.sample(20000, seed=99)
+        assert s.qubit_map() != list(range(n))
+        st = s.get_state()
+    assert np.max(np.abs(st - ref)) <= TOL  # sampling leaves the state unchanged
+    u = C.splitmix_uniform(99, 20000)
+    want = oracle.e_sample(ref, n, u)
+    cum = np.cumsum(np.abs(ref) ** 2)
+    near = np.abs(cum[want.astype(np.int64)] - u * cum[-1]) < 1e-12
+    assert np.all((got == want) | near)

@@ -236,3 +236,21 @@ def test_clear_set_vs_dense_projector():
             assert np.max(np.abs(b - ref)) <= 1e-14
     z = oracle.e_init(n)
     assert oracle.e_project(z, n, 2, 1) == -5 and z[0] == 1
+
+
+def test_generate_events_inverse_cdf():
+    """GENERATE EVENTS: inverse CDF in index order, checked
+    against numpy cumsum + searchsorted, and GHZ events are only |0..0> / |1..1>."""
+    n = 9
+    a = oracle.e_simulate(n, C.layered(n, 2, seed=4))
+    u = C.splitmix_uniform(77, 3000)
+    got = oracle.e_sample(a, n, u)
+    cum = np.cumsum(np.abs(a) ** 2)
+    ref = np.searchsorted(cum, u * cum[-1], side="right")
+    close = np.abs(cum[np.minimum(ref, (1 << n) - 1)] - u * cum[-1]) < 1e-12
+    assert np.all((got == ref) | close)
+    g = oracle.e_simulate(n, C.ghz_chain(n))
+    ev = oracle.e_sample(g, n, u)
+    assert set(np.unique(ev).tolist()) == {0, (1 << n) - 1}
+    frac1 = np.mean(ev == (1 << n) - 1)
+    assert abs(frac1 - 0.5) < 0.05
