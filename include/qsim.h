@@ -157,7 +157,9 @@ int qsim_norm(qsim_state *s, double *norm2);
 int qsim_probabilities(qsim_state *s, double *p1);
 
 /* BEGIN MEASUREMENT: q[3n+0..2] = <Qx(n)>, <Qy(n)>, <Qz(n)>
- * with <Qa(n)> = <psi|(1 - sigma^a_n)|psi>/2.  q has 3N entries.  May move
+ * with <Qa(n)> = <psi|(1 - sigma^a_n)|psi> / (2 <psi|psi>), i.e. of the
+ * normalised state (Eq. STAT1; matters for A, whose encoding drifts the norm).
+ * q has 3N entries.  May move
  * global qubits to local bits (a relabelling; the logical state is unchanged). */
 int qsim_expectations(qsim_state *s, double *q);
 
@@ -176,6 +178,13 @@ int qsim_measure_u(qsim_state *s, int qubit, double u, int *outcome, double *p0_
  * (inverse CDF in logical order).  Needs 8 B x 2^N of scratch (N <= 34);
  * EUNSUPPORTED for the multi-process NCCL transport; EZERONORM for a zero state. */
 int qsim_sample(qsim_state *s, size_t nsamples, uint64_t seed, uint64_t *out);
+
+/* SHORBOX n_x G y (App. B; §5.4):
+ * replace the state by 2^{-nx/2} sum_{x=0}^{2^nx - 1} |x>|y^x mod G>, the
+ * x-register on logical qubits 0..nx-1 and the f-register on nx..N-1 (the
+ * logical index is x + 2^nx f).  Direct preparation: no gates, no exchange.
+ * EINVAL unless 0 <= nx < N, 2 <= G <= 2^(N-nx) and 1 <= y < G. */
+int qsim_prepare_shorbox(qsim_state *s, int nx, uint64_t G, uint64_t y);
 
 /* CLEAR (value 0) / SET (value 1) of App. B: project
  * `qubit` onto |value> and renormalise.  EZERONORM if the projected state has

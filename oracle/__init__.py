@@ -52,6 +52,7 @@ def lib():
         L.oracle_e_expectations.argtypes = [_dp, ctypes.c_int, _dp]
         L.oracle_e_probabilities.argtypes = [_dp, ctypes.c_int, _dp]
         L.oracle_e_measure.argtypes = [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_double, _dp]
+        L.oracle_e_shorbox.argtypes = [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64]
         L.oracle_e_sample.argtypes = [_dp, ctypes.c_int, _dp, ctypes.c_int64, ctypes.POINTER(ctypes.c_uint64)]
         L.oracle_e_project.argtypes = [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         L.oracle_a_decode.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double, _dp, _dp]
@@ -138,6 +139,13 @@ def e_measure(a: np.ndarray, n: int, qubit: int, u_draw: float):
     p0 = ctypes.c_double(0.0)
     out = lib().oracle_e_measure(_ptr(_c128(a).view(np.float64), _dp), n, qubit, float(u_draw), ctypes.byref(p0))
     return out, p0.value
+
+
+def e_shorbox(n: int, nx: int, G: int, y: int) -> np.ndarray:
+    """SHORBOX: 2^{-nx/2} sum_x |x>|y^x mod G>, x on qubits 0..nx-1."""
+    a = np.empty(1 << n, dtype=np.complex128)
+    lib().oracle_e_shorbox(_ptr(a.view(np.float64), _dp), n, nx, G, y)
+    return a
 
 
 def e_sample(a: np.ndarray, n: int, u) -> np.ndarray:

@@ -128,7 +128,8 @@ double oracle_e_norm2(const double *a, int n)
  * With S_n = sum_{i: bit n = 0} conj(a_i) a_{i|2^n}:
  *   <sigma^x_n> = 2 Re S_n, <sigma^y_n> = 2 Im S_n,
  *   <sigma^z_n> = sum |a(bit n = 0)|^2 - sum |a(bit n = 1)|^2.
- * Output q[3n+0..2] = <Qx(n)>, <Qy(n)>, <Qz(n)>.  Not renormalised. */
+ * Output q[3n+0..2] = <Qx(n)>, <Qy(n)>, <Qz(n)> of the normalised state
+ * (divided by sum |a|^2; reading R-B7). */
 void oracle_e_expectations(const double *a, int n, double *q)
 {
     uint64_t dim = (uint64_t)1 << n;
@@ -148,9 +149,12 @@ void oracle_e_expectations(const double *a, int n, double *q)
                 p0 += m;
             }
         }
-        q[3 * k + 0] = (double)((p0 + p1 - 2.0L * sr) / 2.0L);
-        q[3 * k + 1] = (double)((p0 + p1 - 2.0L * si) / 2.0L);
-        q[3 * k + 2] = (double)((p0 + p1 - (p0 - p1)) / 2.0L);
+        /* expectation values of the normalised state (Eq. STAT1; reading R-B7:
+         * the A encoding does not preserve the norm, R-A11) */
+        long double nrm = p0 + p1;
+        q[3 * k + 0] = (double)((nrm - 2.0L * sr) / (2.0L * nrm));
+        q[3 * k + 1] = (double)((nrm - 2.0L * si) / (2.0L * nrm));
+        q[3 * k + 2] = (double)((nrm - (p0 - p1)) / (2.0L * nrm));
     }
 }
 
@@ -199,6 +203,23 @@ int oracle_e_measure(double *a, int n, int qubit, double u_draw, double *p0_out)
         }
     }
     return outcome;
+}
+
+/* SHORBOX n_x G y (App. B; §5.4):
+ * 2^{-n_x/2} sum_{x=0}^{2^{n_x}-1} |x>|y^x mod G>, the x-register on qubits
+ * 0..n_x-1 and the f-register above it: a(x + 2^{n_x} f) = 2^{-n_x/2} iff
+ * f = y^x mod G (sum limit: reading A21).  Replaces the state. */
+void oracle_e_shorbox(double *a, int n, int nx, uint64_t G, uint64_t y)
+{
+    uint64_t dim = (uint64_t)1 << n;
+    memset(a, 0, sizeof(double) * 2 * dim);
+    double amp = pow(2.0, -0.5 * nx);
+    uint64_t f = 1 % G; /* y^0 mod G */
+    for (uint64_t x = 0; x < ((uint64_t)1 << nx); ++x) {
+        uint64_t i = x + (f << nx);
+        a[2 * i] = amp;
+        f = (f * y) % G;
+    }
 }
 
 /* GENERATE EVENTS (App. B): for each caller-drawn

@@ -84,7 +84,7 @@ EXPORTS = (
     "qsim_create", "qsim_create_ex", "qsim_destroy", "qsim_nccl_unique_id", "qsim_apply_gate", "qsim_apply_swap",
     "qsim_apply_circuit", "qsim_norm", "qsim_probabilities", "qsim_expectations", "qsim_measure", "qsim_measure_u",
     "qsim_get_amplitudes", "qsim_get_state", "qsim_set_state", "qsim_get_codes", "qsim_set_codes", "qsim_sync",
-    "qsim_project", "qsim_sample", "qsim_stream", "qsim_get_stats", "qsim_reset", "qsim_profile", "qsim_profile_read", "qsim_reset_stats", "qsim_get_qubit_map", "qsim_last_error",
+    "qsim_project", "qsim_sample", "qsim_prepare_shorbox", "qsim_stream", "qsim_get_stats", "qsim_reset", "qsim_profile", "qsim_profile_read", "qsim_reset_stats", "qsim_get_qubit_map", "qsim_last_error",
     "qsim_plan_create", "qsim_plan_num_ops", "qsim_plan_get_op", "qsim_plan_final_map", "qsim_plan_destroy",
 )
 
@@ -111,6 +111,7 @@ _lib.qsim_expectations.argtypes = [_P, _dp]
 _lib.qsim_measure.argtypes = [_P, ctypes.c_int, ctypes.c_uint64, _ip]
 _lib.qsim_measure_u.argtypes = [_P, ctypes.c_int, ctypes.c_double, _ip, _dp]
 _lib.qsim_project.argtypes = [_P, ctypes.c_int, ctypes.c_int]
+_lib.qsim_prepare_shorbox.argtypes = [_P, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64]
 _lib.qsim_sample.argtypes = [_P, ctypes.c_size_t, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
 _lib.qsim_get_amplitudes.argtypes = [_P, ctypes.POINTER(ctypes.c_uint64), ctypes.c_size_t, _dp]
 _lib.qsim_get_state.argtypes = [_P, _dp]
@@ -269,6 +270,11 @@ def qsim_project(h, qubit, value):
     _check(_lib.qsim_project(h, qubit, value))
 
 
+def qsim_prepare_shorbox(h, nx, G, y):
+    """SHORBOX: 2^{-nx/2} sum_x |x>|y^x mod G>, x-register = qubits 0..nx-1."""
+    _check(_lib.qsim_prepare_shorbox(h, nx, G, y))
+
+
 def qsim_sample(h, nsamples, seed) -> np.ndarray:
     """GENERATE EVENTS: logical basis indices drawn from |a|^2."""
     out = np.empty(max(int(nsamples), 1), dtype=np.uint64)
@@ -422,6 +428,10 @@ class State:
 
     def measure_u(self, qubit, u):
         return qsim_measure_u(self.h, qubit, u)
+
+    def prepare_shorbox(self, nx, G, y):
+        qsim_prepare_shorbox(self.h, nx, G, y)
+        return self
 
     def sample(self, nsamples, seed):
         return qsim_sample(self.h, nsamples, seed)

@@ -1294,11 +1294,12 @@ int qsim_expectations(qsim_state *s, double *q) {
             Si[i] = v[s->n + i];
         }
     }
+    // expectation values of the normalised state (Eq. STAT1; reading R-B7)
     const double nrm = phys[0];
     for (int lq = 0; lq < s->n; ++lq) {
-        q[3 * lq + 0] = (nrm - 2.0 * Sr[lq]) / 2.0;
-        q[3 * lq + 1] = (nrm - 2.0 * Si[lq]) / 2.0;
-        q[3 * lq + 2] = phys[1 + s->pl.pos[lq]];
+        q[3 * lq + 0] = (nrm - 2.0 * Sr[lq]) / (2.0 * nrm);
+        q[3 * lq + 1] = (nrm - 2.0 * Si[lq]) / (2.0 * nrm);
+        q[3 * lq + 2] = phys[1 + s->pl.pos[lq]] / nrm;
     }
     return QSIM_OK;
 }
@@ -1386,6 +1387,33 @@ int qsim_sample(qsim_state *s, size_t nsamples, uint64_t seed, uint64_t *out) {
     s->st.kernels += 4;
     return sample_logical(amps.data(), bases.data(), (int)amps.size(), s->nl, s->n, s->pl.inv.data(), s->enc, s->atab,
                           nsamples, seed, out, s->stream);
+}
+
+int qsim_prepare_shorbox(qsim_state *s, int nx, uint64_t G, uint64_t y) {
+    if (!s || nx < 0 || nx >= s->n || G < 2 || y < 1 || y >= G) {
+        set_error("qsim_prepare_shorbox: need 0 <= nx < N, G >= 2, 1 <= y < G");
+        return QSIM_EINVAL;
+    }
+    if (s->n - nx < 64 && G > (1ull << (s->n - nx))) {
+        set_error("qsim_prepare_shorbox: G does not fit the f-register (N - nx qubits)");
+        return QSIM_EINVAL;
+    }
+    cudaSetDevice(s->dev);
+    if (s->comm_stream) CU(cudaStreamSynchronize(s->comm_stream));
+    std::vector<void *> amps;
+    std::vector<uint64_t> bases;
+    for (auto &sh : s->shards) {
+        amps.push_back(sh.amps);
+        bases.push_back(shard_base(s, sh));
+    }
+    RC(shorbox(amps.data(), bases.data(), (int)amps.size(), s->nl, s->n, s->pl.inv.data(), s->enc, nx, G, y, s->stream));
+    s->st.kernels += (int64_t)amps.size();
+    if (s->enc == QSIM_ENC_ADAPTIVE2) {
+        const double r = (nx == 0) ? 0.5 : std::ldexp(1.0, -nx / 2) * ((nx & 1) ? 0.70710678118654752440 : 1.0);
+        s->r0 = s->r1 = r;  // every non-zero amplitude has magnitude 2^{-nx/2} (reading R-A7/R-A8)
+        RC(atables_set(s->atab, s->r0, s->r1, s->stream));
+    }
+    return QSIM_OK;
 }
 
 int qsim_measure(qsim_state *s, int qubit, uint64_t seed, int *outcome) {

@@ -84,6 +84,9 @@ void launch_codes_from_logical_a(void *a, uint64_t n, uint64_t base, const int *
 int sample_logical(void *const *shard_amps, const uint64_t *shard_base, int nshards, int nl, int nq, const int *inv_host,
                    int enc, const ATables *at, uint64_t nsamp, uint64_t seed, uint64_t *out_host, cudaStream_t s);
 
+int shorbox(void *const *shard_amps, const uint64_t *shard_base, int nshards, int nl, int nq, const int *inv_host,
+            int enc, int nx, uint64_t G, uint64_t y, cudaStream_t s);
+
 void fill_agate(AGateParams &p, const qsim_state *s, const Shard &sh, const PlanOp &o, const double *u);
 int measure_collapse_a(qsim_state *s, int b, int out, double f);
 

@@ -11,7 +11,9 @@
 // Deterministic for a given state, seed and count.
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
+#include <string>
 #include <vector>
 
 #include "internal.h"
@@ -224,6 +226,61 @@ int sample_logical(void *const *shard_amps, const uint64_t *shard_base, int nsha
     cleanup();
     if (e != cudaSuccess) {
         set_error(std::string("qsim_sample: ") + cudaGetErrorString(e));
+        return QSIM_ECUDA;
+    }
+    return QSIM_OK;
+}
+
+// ---- SHORBOX (App. B) ---------------------------------
+__device__ __forceinline__ uint64_t mulmod(uint64_t a, uint64_t b, uint64_t m) {
+    return (uint64_t)(((unsigned __int128)a * b) % m);
+}
+__device__ __forceinline__ uint64_t powmod(uint64_t y, uint64_t x, uint64_t m) {
+    uint64_t r = 1 % m, b = y % m;
+    while (x) {
+        if (x & 1) r = mulmod(r, b, m);
+        b = mulmod(b, b, m);
+        x >>= 1;
+    }
+    return r;
+}
+// E: a(phys) = 2^{-nx/2} iff f == y^x mod G for the logical index x + 2^nx f
+__global__ void k_shorbox_e(double2 *__restrict__ a, uint64_t n, uint64_t base, const int *__restrict__ inv, int nq,
+                            int nx, uint64_t G, uint64_t y, double amp) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t L = phys_to_logical_s(base | i, inv, nq);
+        const uint64_t x = L & ((1ull << nx) - 1ull), f = L >> nx;
+        a[i] = make_double2((f == powmod(y, x, G)) ? amp : 0.0, 0.0);
+    }
+}
+// A: the same state as codes: (b0, b1) = (0, 0) -> r0 = r1 = 2^{-nx/2} (degenerate bounds), or
+// (127, 0) when nx = 0 (a basis state), special zero elsewhere
+__global__ void k_shorbox_a(uint16_t *__restrict__ a, uint64_t n, uint64_t base, const int *__restrict__ inv, int nq,
+                            int nx, uint64_t G, uint64_t y, uint16_t code) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t L = phys_to_logical_s(base | i, inv, nq);
+        const uint64_t x = L & ((1ull << nx) - 1ull), f = L >> nx;
+        a[i] = (f == powmod(y, x, G)) ? code : (uint16_t)0x0080u;  // 0x0080 = (b0 -128, b1 0)
+    }
+}
+int shorbox(void *const *shard_amps, const uint64_t *shard_base, int nshards, int nl, int nq, const int *inv_host,
+            int enc, int nx, uint64_t G, uint64_t y, cudaStream_t s) {
+    int *d_inv = nullptr;
+    if (cudaMalloc(&d_inv, nq * sizeof(int)) != cudaSuccess) return QSIM_ENOMEM;
+    cudaMemcpyAsync(d_inv, inv_host, nq * sizeof(int), cudaMemcpyHostToDevice, s);
+    const double amp = ldexp(1.0, -nx / 2) * ((nx & 1) ? 0.70710678118654752440 : 1.0);
+    for (int r = 0; r < nshards; ++r) {
+        if (enc == QSIM_ENC_FP64)
+            k_shorbox_e<<<148 * 8, 256, 0, s>>>((double2 *)shard_amps[r], 1ull << nl, shard_base[r], d_inv, nq, nx, G, y,
+                                                amp);
+        else
+            k_shorbox_a<<<148 * 8, 256, 0, s>>>((uint16_t *)shard_amps[r], 1ull << nl, shard_base[r], d_inv, nq, nx, G,
+                                                y, (uint16_t)(nx == 0 ? 0x007Fu : 0x0000u));
+    }
+    cudaError_t e = cudaStreamSynchronize(s);
+    cudaFree(d_inv);
+    if (e != cudaSuccess) {
+        set_error(std::string("shorbox: ") + cudaGetErrorString(e));
         return QSIM_ECUDA;
     }
     return QSIM_OK;

@@ -316,6 +316,21 @@ def qft(n: int, x: int | None = None, seed: int = 5) -> tuple[Circuit, int]:
     return c, x
 
 
+def qft_register(n: int, m: int, swaps: bool = True) -> Circuit:
+    """The QFT of reading A15 on qubits 0..m-1 of an n-qubit register (no input
+    preparation): for j = m-1..0 { H(j); CPHASE(k -> j, 2pi/2^(j-k+1)), k = j-1..0 },
+    then (if swaps) SWAP(i, m-1-i) for i < m/2."""
+    c = Circuit(n)
+    for j in range(m - 1, -1, -1):
+        c.add("H", mat_H(), j)
+        for k in range(j - 1, -1, -1):
+            c.add("CPHASE", mat_R(j - k + 1), j, [k])
+    if swaps:
+        for i in range(m // 2):
+            c.swap(i, m - 1 - i)
+    return c
+
+
 def config(idx: int, n: int | None = None, seed: int | None = None, layers: int | None = None) -> Circuit:
     """BASELINE.json configs by index (0-based as in the JSON list)."""
     if idx == 0:

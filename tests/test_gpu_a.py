@@ -178,3 +178,22 @@ def test_max_size_a_n36_paper_workloads():
         z = s.get_amplitudes(np.array([0, (1 << n) - 1, 12345, 1 << 35], dtype=np.uint64))
         assert np.max(np.abs(z - np.array([1, 1, 0, 0]) / math.sqrt(2))) <= 1e-15
         assert np.max(np.abs(s.probabilities() - 0.5)) <= 1e-15
+
+
+@pytest.mark.slow
+def test_table5_shor_n30_in_a():
+    """PAPER.md Table 5: the A encoding (our exact-bounds policy, reading R-A4)
+    agrees with the printed exact columns to about 3 digits, like the paper's A
+    columns (worst printed A deviation 0.006 there; bound 0.011 of Table 4)."""
+    import os
+    rows = [l.split() for l in open(os.path.join(os.path.dirname(__file__), "golden", "table5_shor.txt"))
+            if l.strip() and not l.startswith("#")]
+    t = np.array(rows, dtype=float)
+    with q.State(30, q.ENC_ADAPTIVE2) as s:
+        s.prepare_shorbox(20, 1007, 529)
+        z = s.get_amplitudes(np.array([0, 1 << 20, 1 + (529 << 20)], dtype=np.uint64))
+        # SHORBOX is exact in A: |0>|1> and |1>|529> carry 2^-10, |0>|0> is empty
+        assert z[0] == 0 and np.max(np.abs(np.abs(z[1:]) - 2.0 ** -10)) <= 1e-15
+        s.apply_circuit(C.qft_register(30, 20))
+        e = s.expectations()[:20]
+    assert np.max(np.abs(e - t[:, 4:7])) <= 0.011

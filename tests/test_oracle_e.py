@@ -254,3 +254,18 @@ def test_generate_events_inverse_cdf():
     assert set(np.unique(ev).tolist()) == {0, (1 << n) - 1}
     frac1 = np.mean(ev == (1 << n) - 1)
     assert abs(frac1 - 0.5) < 0.05
+
+
+def test_shorbox_closed_form_and_period():
+    """SHORBOX (PAPER.md:1452-1471): amplitude 2^{-nx/2} exactly at x + 2^nx (y^x mod G);
+    after the QFT on the x-register the x-distribution sits on multiples of 2^nx / r
+    (G = 15, y = 7: period r = 4 divides 2^nx, so the peaks are exact)."""
+    n, nx, G, y = 8, 4, 15, 7
+    a = oracle.e_shorbox(n, nx, G, y)
+    nz = np.flatnonzero(np.abs(a) > 0)
+    want = sorted(x + (pow(y, x, G) << nx) for x in range(1 << nx))
+    assert nz.tolist() == want
+    assert np.allclose(a[nz], 2.0 ** (-nx / 2), atol=0) and abs(oracle.e_norm2(a, n) - 1) <= 1e-15
+    oracle.e_run(a, n, C.qft_register(n, nx))
+    px = (np.abs(a.reshape(1 << (n - nx), 1 << nx)) ** 2).sum(axis=0)
+    assert np.all(px[[0, 4, 8, 12]] > 0.2) and px[[k for k in range(16) if k % 4]].max() <= 1e-15
