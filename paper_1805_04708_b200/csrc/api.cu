@@ -419,6 +419,7 @@ static int launch_pass(qsim_state *s, const PassBuild &pb, const std::vector<Pla
     p.nstages = (int)pb.stage_q.size();
     const int RR = s->pass_r;
     p.R = RR;
+    p.noio = getenv("QSIM_DEBUG_PASS_NOIO") ? 1 : 0;
     int gi = 0;
     int nops4 = 0;
     for (int si = 0; si < p.nstages; ++si) {

@@ -99,6 +99,8 @@ struct PassParams {
     int32_t K;            // tile qubits
     int32_t nstages;
     int32_t R;            // register qubits per stage (4 or 5)
+    int32_t noio;         // debug: skip the HBM tile load / store (timing experiments only)
+    int32_t pad_noio;
     int32_t high_q[PASS_MAX_K - PASS_LOW];  // local qubit of tile bit PASS_LOW + i (ascending)
     int32_t pad2;
     PassStage st[PASS_MAX_STAGES];

@@ -342,8 +342,10 @@ __global__ void __launch_bounds__(PASS_THREADS, MINB) k_pass_e(const __grid_cons
         // x = tid + 128 j: swz and the deposit are GF(2)-linear on disjoint
         // bits, so address = a[(base | d_tid) + depJ[j]] and smem = s_tid ^ swz(128 j).
         const double2 *pt = a + (base | d_tid);
+        if (!p.noio) {
 #pragma unroll 8
-        for (uint32_t j = 0; j < njt; ++j) cp_async16(&tile[s_tid ^ swz(j << 7)], pt + depJ[j]);
+            for (uint32_t j = 0; j < njt; ++j) cp_async16(&tile[s_tid ^ swz(j << 7)], pt + depJ[j]);
+        }
         cp_async_wait_all();
         __syncthreads();
         // ---- stages ----
@@ -465,8 +467,10 @@ __global__ void __launch_bounds__(PASS_THREADS, MINB) k_pass_e(const __grid_cons
         }
         // ---- store the tile ----
         double2 *ps = a + (base | d_tid);
+        if (!p.noio) {
 #pragma unroll 8
-        for (uint32_t j = 0; j < njt; ++j) ps[depJ[j]] = tile[s_tid ^ swz(j << 7)];
+            for (uint32_t j = 0; j < njt; ++j) ps[depJ[j]] = tile[s_tid ^ swz(j << 7)];
+        }
         __syncthreads();
     }
 }
