@@ -128,7 +128,7 @@ static const ATabData *tnext(const ATables *t) { return t->d[1 - t->cur]; }
 struct ASm {
     double r[256];    // decode (current bounds)
     double thr[256];  // encode thresholds (next bounds)
-    double cth[256], sth[256];
+    double2 cs[256];  // (cos, sin)(pi b1 / 128), one 128-bit load per decode
     double cb[260], sb[260];
     double r0n, scalen;
     int degn;
@@ -139,8 +139,7 @@ __device__ void load_asm(ASm &sm, const ATabData *__restrict__ cur, const ATabDa
     for (int i = threadIdx.x; i < 256; i += blockDim.x) {
         sm.r[i] = cur->r[i];
         sm.thr[i] = nxt->thr[i];
-        sm.cth[i] = cur->cth[i];
-        sm.sth[i] = cur->sth[i];
+        sm.cs[i] = make_double2(cur->cth[i], cur->sth[i]);
     }
     for (int i = threadIdx.x; i < 260; i += blockDim.x) {
         sm.cb[i] = cur->cb[i];
@@ -152,7 +151,7 @@ __device__ void load_asm(ASm &sm, const ATabData *__restrict__ cur, const ATabDa
         sm.degn = nxt->degenerate;
         // fp32 candidate error in steps: |d tf| <= (eps32 (|m| + r0) + |m - m_f|) * scale,
         // bounded by 4e-7 * (r1 + r0) * scale + 1e-3; above 0.5 -> always check
-        const double e = 4e-7 * (nxt->r1 + nxt->r0) * nxt->scale + 1e-3;
+        const double e = 4e-7 * (nxt->r1 + nxt->r0) * nxt->scale + 1e-4;
         sm.mmargin = (float)(e < 0.49 ? e : 0.5);
     }
     __syncthreads();
@@ -162,7 +161,8 @@ __device__ __forceinline__ double2 a_decode(const ASm &sm, uint32_t code) {
     const int b0i = (int)(code & 0xffu) ^ 0x80;  // int8 b0 + 128
     const int b1i = (int)((code >> 8) & 0xffu) ^ 0x80;
     const double r = sm.r[b0i];
-    return make_double2(r * sm.cth[b1i], r * sm.sth[b1i]);
+    const double2 cs = sm.cs[b1i];
+    return make_double2(r * cs.x, r * cs.y);
 }
 
 __device__ __forceinline__ double a_m2(double2 z) { return fma(z.x, z.x, z.y * z.y); }
@@ -187,8 +187,10 @@ __device__ __forceinline__ float atan2_steps(float y, float x) {
 // Angle code: round half away from zero of 128 atan2(y, x) / pi, computed in
 // fp64 terms.  The fp32 candidate is exact unless it lies within A_MARGIN
 // steps of a rounding boundary; only then the exact fp64 boundary-direction
-// cross products decide (ties away from zero, reading R-A6).
-#define A_MARGIN 0.02f
+// cross products decide (ties away from zero, reading R-A6).  Candidate error:
+// polynomial <= 4e-4 steps + fp32 rounding ~3e-6 steps, so 1e-3 is safe; a
+// small margin keeps the (divergent) fp64 path rare per warp.
+#define A_MARGIN 1e-3f
 __device__ __forceinline__ int a_angle_code(const ASm &sm, double2 z) {
     const float af = atan2_steps((float)z.y, (float)z.x);
     int k = __float2int_rn(af);
