@@ -5,6 +5,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
+#include <deque>
 #include <cstdlib>
 #include <cmath>
 #include <cstdio>
@@ -15,6 +17,7 @@
 #include "internal.h"
 #include "kernels.h"
 #include "kernels_a.h"
+#include "lpass.h"
 
 namespace qsim {
 
@@ -58,6 +61,7 @@ struct qsim_state {
     int n = 0, enc = 0, P = 1, nl = 0, transport = 0, rank = 0, dev = 0, fuse = 1;
     int pass_r = 4;  // register qubits per pass stage (QSIM_PASS_R=5 selects 32-amplitude groups)
     int use_mma = 1; // tensor-core (DMMA) pair stages in fused passes (QSIM_PASS_MMA=0 disables)
+    int pass_kernel = 1;  // 1: relabelling pass k_lpass_e (lpass.h); 0: k_pass_e (QSIM_PASS_KERNEL=0)
     size_t amp_bytes = 16;
     uint64_t alloc_amps = 0;  // max(2^nl, 256): small shards are padded with zero amplitudes
     Planner pl;
@@ -253,9 +257,9 @@ static void gate_masks(const PlanOp &o, uint64_t &xq, uint64_t &zq) {
 
 // Try to append op `idx` to the pass (tile capacity only); false (no change)
 // if it does not fit.  Stages are formed afterwards by stage_pass().
-static bool pass_add(PassBuild &pb, const PlanOp &o, int idx, int hmax, int nl) {
+static bool pass_add(PassBuild &pb, const PlanOp &o, int idx, int hmax, int nl, int max_gates = PASS_MAX_GATES) {
     const bool needs_reg = o.cls != CLS_DIAG;
-    if ((int)pb.ops.size() >= PASS_MAX_GATES) return false;
+    if ((int)pb.ops.size() >= max_gates) return false;
     bool new_high = needs_reg && o.l >= PASS_LOW && std::find(pb.high.begin(), pb.high.end(), o.l) == pb.high.end();
     if (new_high && (int)pb.high.size() >= hmax) return false;
     if (new_high) pb.high.push_back(o.l);
@@ -616,10 +620,99 @@ static int launch_pass(qsim_state *s, const PassBuild &pb, const std::vector<Pla
     return QSIM_OK;
 }
 
+// ---- relabelling tile pass (lpass.h) ----
+static PlanOp plan_op_of(const LGate &g) {
+    PlanOp o{};
+    o.type = QSIM_OP_GATE;
+    o.g = -1;
+    o.l = g.t;
+    o.cls = classify(g.u);
+    o.nctrl = g.nctl;
+    o.ctrl[0] = g.nctl > 0 ? g.ctl[0] : 0;
+    o.ctrl[1] = g.nctl > 1 ? g.ctl[1] : 0;
+    o.gate_index = -1;
+    return o;
+}
+
+// lpass_run's callbacks: launch k_lpass_e on every shard / a single-gate sweep.
+// Synthetic (deferred) diagonals are excluded from the algorithmic flops.
+struct LaunchSink : LPassSink {
+    qsim_state *s;
+    const std::vector<PlanOp> *run;
+    const std::vector<const double *> *us;
+    int pass(const LPassParams &p, const LCompileStats &cs, const std::vector<int> &ids) override {
+        int nreal = 0;
+        for (int id : ids) nreal += id >= 0;
+        if (getenv("QSIM_DEBUG_PASSES"))
+            fprintf(stderr, "lpass: %zu gates (%d circuit), %d stages, %d ops (%d tables, %d shears, %d dense, %d flips, "
+                            "%d relabels, %d swaps), %d tile-level permutations, %d events, %d coefficients, "
+                            "%d carried, %d deferred\n",
+                    ids.size(), nreal, cs.stages, cs.ops, cs.diagt, cs.shears, cs.dense, cs.flips, cs.relabels,
+                    cs.cswaps, cs.tile_free, cs.events, p.ncoef, cs.carried, cs.deferred);
+        static LPassParams q;  // large: keep off the stack
+        std::memcpy(&q, &p, sizeof(q));
+        q.noio = getenv("QSIM_DEBUG_PASS_NOIO") ? 1 : 0;
+        s->st.stages += p.nstages;
+        for (auto &sh : s->shards) {
+            q.a = sh.amps;
+            q.shard_base = shard_base(s, sh);
+            double fl = 0.0;
+            for (int id : ids)
+                if (id >= 0) fl += gate_flops(s, sh, (*run)[id], (*us)[id]);
+            prof_begin(s);
+            launch_lpass_e(q, s->stream);
+            prof_end(s, QSIM_K_PASS, std::ldexp(2.0 * (double)s->amp_bytes, s->nl), fl);
+            s->st.kernels++;
+            s->st.passes++;
+            s->st.fused_gates += nreal;
+            s->st.hbm_bytes += std::ldexp(2.0 * (double)s->amp_bytes, s->nl);
+        }
+        CU(cudaGetLastError());
+        return QSIM_OK;
+    }
+    int sweep(const LGate &g, int id) override {
+        if (id >= 0) return sweep_gate_e(s, (*run)[id], (*us)[id]);
+        return sweep_gate_e(s, plan_op_of(g), g.u);
+    }
+    double gate_bytes(const LGate &g) override { return gate_bytes_alone(s, s->shards[0], plan_op_of(g), g.u); }
+};
+
+static int run_gates_lpass(qsim_state *s, const std::vector<PlanOp> &run, const std::vector<const double *> &us) {
+    std::vector<LGate> lg(run.size());
+    for (size_t k = 0; k < run.size(); ++k) {
+        const PlanOp &o = run[k];
+        LGate &g = lg[k];
+        g.t = o.l;
+        g.nctl = o.nctrl;
+        g.ctl[0] = o.nctrl > 0 ? o.ctrl[0] : 0;
+        g.ctl[1] = o.nctrl > 1 ? o.ctrl[1] : 0;
+        std::memcpy(g.u, us[k], sizeof(g.u));
+    }
+    LRunConfig cfg;
+    cfg.nl = s->nl;
+    cfg.K = std::min(LP_MAX_K, s->nl);
+    cfg.R = s->pass_r;
+    cfg.max_coef = lpass_max_coef(cfg.R);
+    cfg.defer = getenv("QSIM_LPASS_NODEFER") == nullptr;
+    cfg.pass_bytes = std::ldexp(2.0 * (double)s->amp_bytes, s->nl);
+    LaunchSink sink;
+    sink.s = s;
+    sink.run = &run;
+    sink.us = &us;
+    std::string err;
+    const int rc = lpass_run(lg.data(), (int)lg.size(), cfg, sink, &err);
+    if (rc == -1) {
+        set_error("lpass: " + err);
+        return QSIM_EINVAL;
+    }
+    return rc;
+}
+
 // Greedy commutation-aware pass scheduler (a6): each pass takes, in circuit
 // order, every not-yet-applied gate that commutes with all earlier skipped
 // gates and fits the tile (<= K - PASS_LOW high target qubits, <= PASS_MAX_*).
 static int run_gates_e(qsim_state *s, const std::vector<PlanOp> &run, const std::vector<const double *> &us) {
+    if (s->pass_kernel == 1 && s->fuse && std::min(LP_MAX_K, s->nl) >= LP_MIN_K) return run_gates_lpass(s, run, us);
     const int K = std::min(pass_e_max_k(), s->nl);
     const bool can_fuse = s->fuse && K >= PASS_MIN_K;
     if (!can_fuse) {
@@ -980,6 +1073,7 @@ int qsim_create_ex(const qsim_config *cfg, qsim_state **out) {
     s->fuse = cfg->fuse;
     if (const char *pr = getenv("QSIM_PASS_R")) s->pass_r = (atoi(pr) == 4) ? 4 : 5;
     if (const char *pm = getenv("QSIM_PASS_MMA")) s->use_mma = atoi(pm) != 0;
+    if (const char *pk = getenv("QSIM_PASS_KERNEL")) s->pass_kernel = atoi(pk) != 0 ? 1 : 0;
     s->amp_bytes = s->enc == QSIM_ENC_FP64 ? 16 : 2;
     if (cfg->device >= 0) {
         if (cudaSetDevice(cfg->device) != cudaSuccess) {

@@ -1,0 +1,403 @@
+// lpass.cu -- k_lpass_e: the relabelling tile pass (lpass.h), sm_100a.
+//
+// One persistent CTA of 128 threads per tile slot; 3 (R = 4) or 2 (R = 5)
+// CTAs per SM.  Per tile: cp.async load of 2^K amplitudes (128 B runs) into
+// XOR-swizzled shared memory, the program's register stages (each a
+// shared-memory round trip of the tile; ops in registers), and a store that
+// reads logical x from physical M x ^ b.  The op semantics are exactly those
+// of the host-side emulator tools/lpass_emu.cpp, which validates the
+// compiler; every address below is an XOR of host-provided GF(2) basis
+// vectors.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "lpass.h"
+
+namespace qsim {
+
+__device__ __forceinline__ uint64_t lp_ins0(uint64_t w, int p) {
+    return ((w >> p) << (p + 1)) | (w & ((1ull << p) - 1ull));
+}
+__device__ __forceinline__ uint32_t lp_par(uint32_t x) { return __popc(x) & 1u; }
+__host__ __device__ constexpr int lp_ctz5(int i) { return (i & 1) ? 0 : (i & 2) ? 1 : (i & 4) ? 2 : (i & 8) ? 3 : 4; }
+__host__ __device__ constexpr int lp_hibit(int v) { return v >= 16 ? 4 : v >= 8 ? 3 : v >= 4 ? 2 : v >= 2 ? 1 : 0; }
+
+__device__ __forceinline__ void lp_cp_async16(void *smem, const void *gmem) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void lp_cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// x' = x - t y, y' = y + t x  (2 FMAs per amplitude component)
+__device__ __forceinline__ void lp_shear_pair(double2 &x, double2 &y, double t) {
+    const double2 x0 = x;
+    x.x = fma(-t, y.x, x.x);
+    x.y = fma(-t, y.y, x.y);
+    y.x = fma(t, x0.x, y.x);
+    y.y = fma(t, x0.y, y.y);
+}
+
+template <int NS, int V>
+__device__ __forceinline__ void lp_shearu(double2 (&v)[NS], double te) {
+    constexpr int HB = lp_hibit(V);
+#pragma unroll
+    for (int j0 = 0; j0 < NS; ++j0) {
+        if (j0 & (1 << HB)) continue;
+        lp_shear_pair(v[j0], v[j0 ^ V], te);
+    }
+}
+template <int NS, int V>
+__device__ __forceinline__ void lp_shear(double2 (&v)[NS], double t, uint32_t pm, uint32_t gp) {
+    constexpr int HB = lp_hibit(V);
+    const uint32_t q = pm ^ (gp ? 0xffffffffu : 0u);
+#pragma unroll
+    for (int j0 = 0; j0 < NS; ++j0) {
+        if (j0 & (1 << HB)) continue;
+        const double te = ((q >> j0) & 1u) ? -t : t;
+        lp_shear_pair(v[j0], v[j0 ^ V], te);
+    }
+}
+// per-pair control predicate: all in-register controls of sigma(j0) are 1
+__device__ __forceinline__ uint32_t lp_ctl_mask(const LOp &o, uint32_t g) {
+    uint32_t m = 0xffffffffu;
+    const int nc = o.nctl;
+    if (nc > 0) m &= o.pmc[0] ^ (lp_par(o.rowc[0] & g) ? 0xffffffffu : 0u);
+    if (nc > 1) m &= o.pmc[1] ^ (lp_par(o.rowc[1] & g) ? 0xffffffffu : 0u);
+    return m;  // bit j0 = 1 iff the pair at j0 is selected
+}
+template <int NS, int V>
+__device__ __forceinline__ void lp_cshear(double2 (&v)[NS], double t, uint32_t pm, uint32_t gp, uint32_t cm) {
+    constexpr int HB = lp_hibit(V);
+    const uint32_t q = pm ^ (gp ? 0xffffffffu : 0u);
+#pragma unroll
+    for (int j0 = 0; j0 < NS; ++j0) {
+        if (j0 & (1 << HB)) continue;
+        double te = ((q >> j0) & 1u) ? -t : t;
+        te = ((cm >> j0) & 1u) ? te : 0.0;
+        lp_shear_pair(v[j0], v[j0 ^ V], te);
+    }
+}
+template <int NS, int V>
+__device__ __forceinline__ void lp_dense(double2 (&v)[NS], const double2 *u, uint32_t pm, uint32_t gp, uint32_t cm) {
+    constexpr int HB = lp_hibit(V);
+    const uint32_t q = pm ^ (gp ? 0xffffffffu : 0u);
+    const double2 a = u[0], b = u[1], c = u[2], d = u[3];
+#pragma unroll
+    for (int j0 = 0; j0 < NS; ++j0) {
+        if (j0 & (1 << HB)) continue;
+        if (!((cm >> j0) & 1u)) continue;
+        // register j0 holds the logical-1 member when the bit is set: apply X U X
+        const bool s = (q >> j0) & 1u;
+        const double2 e00 = s ? d : a, e01 = s ? c : b, e10 = s ? b : c, e11 = s ? a : d;
+        const double2 x = v[j0], y = v[j0 ^ V];
+        v[j0] = make_double2(e00.x * x.x - e00.y * x.y + e01.x * y.x - e01.y * y.y,
+                             e00.x * x.y + e00.y * x.x + e01.x * y.y + e01.y * y.x);
+        v[j0 ^ V] = make_double2(e10.x * x.x - e10.y * x.y + e11.x * y.x - e11.y * y.y,
+                                 e10.x * x.y + e10.y * x.x + e11.x * y.y + e11.y * y.x);
+    }
+}
+template <int NS, int V>
+__device__ __forceinline__ void lp_cswap(double2 (&v)[NS], uint32_t cm) {
+    constexpr int HB = lp_hibit(V);
+#pragma unroll
+    for (int j0 = 0; j0 < NS; ++j0) {
+        if (j0 & (1 << HB)) continue;
+        const bool s = (cm >> j0) & 1u;
+        const double2 x = v[j0], y = v[j0 ^ V];
+        v[j0] = s ? y : x;
+        v[j0 ^ V] = s ? x : y;
+    }
+}
+
+struct LPSmem {
+    size_t tile, cpool, total;
+};
+// tables sit right after the tile: both offsets are multiples of a table's
+// size (2^R x 16 B), so entry j ^ g of a table is at (base + g*16) ^ (j*16)
+__host__ __device__ inline LPSmem lp_smem(int K, int ncoef) {
+    LPSmem L;
+    L.tile = 0;
+    L.cpool = ((size_t)1 << K) * 16;
+    L.total = L.cpool + (size_t)((ncoef + 1) & ~1) * 8;
+    return L;
+}
+
+// lifted shear on register bit r (L D U factorisation, D already applied by
+// the table): logical x += a y; y += t x -- every FMA writes its own input
+template <int NS, int RB, bool FLIP>
+__device__ __forceinline__ void lp_lift(double2 (&v)[NS], double t, double a) {
+#pragma unroll
+    for (int j0 = 0; j0 < NS; ++j0) {
+        if (j0 & (1 << RB)) continue;
+        double2 &x = FLIP ? v[j0 | (1 << RB)] : v[j0];
+        double2 &y = FLIP ? v[j0] : v[j0 | (1 << RB)];
+        x.x = fma(a, y.x, x.x);
+        x.y = fma(a, y.y, x.y);
+        y.x = fma(t, x.x, y.x);
+        y.y = fma(t, x.y, y.y);
+    }
+}
+
+// v[j] *= T[j ^ g]; tb = byte offset of the table in shared memory + 16 g
+template <int NS>
+__device__ __forceinline__ void lp_table(double2 (&v)[NS], const unsigned char *smem, uint32_t tb) {
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+        const double2 c = *reinterpret_cast<const double2 *>(smem + (tb ^ (uint32_t)(j << 4)));
+        const double2 x = v[j];
+        const double p = c.y * x.y, q = c.y * x.x;
+        v[j].x = fma(c.x, x.x, -p);
+        v[j].y = fma(c.x, x.y, q);
+    }
+}
+
+template <int R, int MINB>
+__global__ void __launch_bounds__(LP_THREADS, MINB) k_lpass_e(const __grid_constant__ LPassParams p) {
+    constexpr int NS = 1 << R;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int K = p.K;
+    const LPSmem L = lp_smem(K, p.ncoef);
+    double *cpool = reinterpret_cast<double *>(smem_raw + L.cpool);
+    const uint32_t cpool_off = (uint32_t)L.cpool;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t ngroups = 1u << (K - R);
+    // ---- one-time setup per CTA ----
+    for (int i = tid; i < p.ncoef; i += LP_THREADS) cpool[i] = p.coef[i];
+    // load / store addressing: logical x = tid + 128 j; smem byte offset of x
+    // at load = XOR of scol over its bits (store: smcol, plus S b); HBM offset
+    // = deposit of its bits.  Bits 0..6 are this thread's, bits 7.. come from j.
+    uint32_t s_tid = 0, m_tid = 0;
+    uint64_t d_tid = tid & 7u;
+#pragma unroll
+    for (int i = 0; i < 7; ++i)
+        if ((tid >> i) & 1u) {
+            s_tid ^= (uint32_t)p.scol[i] << 4;
+            m_tid ^= (uint32_t)p.smcol[i] << 4;
+            if (i >= LP_LOW) d_tid |= 1ull << p.high_q[i - LP_LOW];
+        }
+    uint32_t s_hi[5], m_hi[5];
+    uint64_t d_hi[5];
+#pragma unroll
+    for (int b = 0; b < 5; ++b) {
+        const bool on = 7 + b < K;
+        s_hi[b] = on ? (uint32_t)p.scol[7 + b] << 4 : 0u;
+        m_hi[b] = on ? (uint32_t)p.smcol[7 + b] << 4 : 0u;
+        d_hi[b] = on ? (1ull << p.high_q[7 + b - LP_LOW]) : 0ull;
+    }
+    __syncthreads();
+    double2 *__restrict__ a = reinterpret_cast<double2 *>(p.a);
+
+    for (uint64_t T = blockIdx.x; T < p.ntiles; T += gridDim.x) {
+        uint64_t base = T << LP_LOW;
+        for (int i = 0; i < K - LP_LOW; ++i) base = lp_ins0(base, p.high_q[i]);
+        const uint64_t full = p.shard_base | base;
+        uint32_t fired = 0;
+        for (int e = 0; e < p.nevents; ++e)
+            if ((full & p.ev_full[e]) == p.ev_full[e]) fired |= 1u << e;
+        // ---- load the tile: logical x = tid + 128 j at S x ----
+        if (!p.noio) {
+            // j in Gray-code order: one column changes per element
+            const double2 *pt = a + (base | d_tid);
+            uint32_t so = s_tid;
+            uint64_t dj = 0;
+            const int nj = 1 << (K - 7);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                if (i >= nj) break;
+                if (i) {
+                    const int b = lp_ctz5(i);
+                    so ^= s_hi[b];
+                    dj ^= d_hi[b];
+                }
+                lp_cp_async16(smem_raw + so, pt + dj);
+            }
+        }
+        lp_cp_async_wait_all();
+        __syncthreads();
+        // ---- register stages ----
+        for (int s = 0; s < p.nstages; ++s) {
+            const LStage &st = p.st[s];
+            uint32_t y = st.y_static;
+            for (uint32_t m = fired & st.ev_mask; m; m &= m - 1) y ^= st.y_ev[__ffs(m) - 1];
+            uint32_t g0 = 0;
+#pragma unroll
+            for (int r = 0; r < R; ++r) g0 |= ((y >> st.qbit[r]) & 1u) << r;
+            const uint32_t yrest = y & ~(uint32_t)st.qmask;
+            uint32_t rp[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) rp[r] = (uint32_t)st.reg_phys[r] << 4;
+            const int op0 = st.first_op, op1 = st.first_op + st.nops;
+            const bool nxq = st.needs_xq;
+            for (uint32_t grp = tid; grp < ngroups; grp += LP_THREADS) {
+                uint32_t a0 = 0, xq = yrest;
+                for (int i = 0; i < K - R; ++i)
+                    if ((grp >> i) & 1u) {
+                        a0 ^= (uint32_t)st.grp_phys[i] << 4;
+                        if (nxq) xq ^= st.grp_log[i];
+                    }
+                double2 v[NS];
+#pragma unroll
+                for (int j = 0; j < NS; ++j) {
+                    uint32_t ad = a0;
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        if (j & (1 << r)) ad ^= rp[r];
+                    v[j] = *reinterpret_cast<const double2 *>(smem_raw + ad);
+                }
+                uint32_t g = g0;
+                const uint64_t *oph = reinterpret_cast<const uint64_t *>(p.op);
+                uint64_t hn = op0 < op1 ? oph[op0 * (sizeof(LOp) / 8)] : 0;
+                for (int oi = op0; oi < op1; ++oi) {
+                    const LOp &o = p.op[oi];
+                    const uint64_t h = hn;  // header: code | flags | rowS | gvec | coef
+                    if (oi + 1 < op1) hn = oph[(oi + 1) * (sizeof(LOp) / 8)];
+                    const uint32_t code = (uint32_t)h & 0xffu;
+                    const uint32_t coef = (uint32_t)(h >> 32) & 0xffffu;
+                    if ((h >> 8) & LF_COND) {
+                        if (((xq & o.tmask) != o.tval) || ((full & o.omask) != o.oval)) continue;
+                    }
+                    // table variant: the group's values of up to 2 condition bits
+                    uint32_t toff = cpool_off + coef * 8u;
+                    if ((h >> 48) & 0xffu) {
+                        const uint32_t nv = (uint32_t)(h >> 48) & 0xffu;
+#pragma unroll
+                        for (int i = 0; i < 2; ++i)
+                            if (i < (int)nv) {
+                                const uint32_t c = o.rowc[i];
+                                const uint32_t bit = c < 64 ? (xq >> c) & 1u : (uint32_t)(full >> (c - 64)) & 1u;
+                                toff += bit << (i + R + 4);  // variant stride: one table, 2^R x 16 bytes
+                            }
+                    }
+                    if (code == LOP_CODE_ROUND) {
+                        lp_table<NS>(v, smem_raw, toff | (g << 4));
+                        const uint32_t mask = (uint32_t)(h >> 24) & 0xffu;
+                        const double *sp = p.sc + o.pm;
+                        int k = 0;
+#define LP_ROUND_BIT(RB)                                                          \
+    if constexpr ((RB) < R) {                                                     \
+        if ((mask >> (RB)) & 1u) {                                                \
+            const double t = sp[2 * k], aa = sp[2 * k + 1];                       \
+            ++k;                                                                  \
+            if ((g >> (RB)) & 1u)                                                 \
+                lp_lift<NS, ((RB) < R ? (RB) : 0), true>(v, t, aa);               \
+            else                                                                  \
+                lp_lift<NS, ((RB) < R ? (RB) : 0), false>(v, t, aa);              \
+        }                                                                         \
+    }
+                        LP_ROUND_BIT(0) LP_ROUND_BIT(1) LP_ROUND_BIT(2) LP_ROUND_BIT(3) LP_ROUND_BIT(4)
+#undef LP_ROUND_BIT
+                        continue;
+                    }
+                    if (code == LOP_CODE_DIAGT) {
+                        lp_table<NS>(v, smem_raw, toff | (g << 4));
+                        continue;
+                    }
+                    if (code == LOP_CODE_FLIP) {
+                        g ^= (uint32_t)(h >> 24) & 0xffu;
+                        continue;
+                    }
+                    const uint32_t gp = lp_par(((uint32_t)(h >> 16) & 0xffu) & g);
+                    switch (code) {
+#define LP_V_CASES(VS)                                                                                    \
+    case LOP_SHEARU * 16 + (VS):                                                                          \
+        if constexpr ((VS) < lp_nv(R)) {                                                                  \
+            const double t = p.sc[coef];                                                                  \
+            lp_shearu<NS, lp_vec(R, (VS))>(v, ((o.pm ^ gp) & 1u) ? -t : t);                               \
+        }                                                                                                 \
+        break;                                                                                            \
+    case LOP_SHEAR * 16 + (VS):                                                                           \
+        if constexpr ((VS) < lp_nv(R)) lp_shear<NS, lp_vec(R, (VS))>(v, p.sc[coef], o.pm, gp);             \
+        break;
+#define LP_W1_CASES(VS)                                                                                   \
+    case LOP_CSHEAR * 16 + (VS):                                                                          \
+        if constexpr ((VS) < R) lp_cshear<NS, (1 << (VS))>(v, p.sc[coef], o.pm, gp, lp_ctl_mask(o, g));    \
+        break;                                                                                            \
+    case LOP_DENSE * 16 + (VS):                                                                           \
+        if constexpr ((VS) < R)                                                                           \
+            lp_dense<NS, (1 << (VS))>(v, reinterpret_cast<const double2 *>(p.sc + coef), o.pm, gp,        \
+                                      lp_ctl_mask(o, g));                                                 \
+        break;                                                                                            \
+    case LOP_CSWAP * 16 + (VS):                                                                           \
+        if constexpr ((VS) < R) lp_cswap<NS, (1 << (VS))>(v, lp_ctl_mask(o, g));                          \
+        break;
+                        LP_V_CASES(0) LP_V_CASES(1) LP_V_CASES(2) LP_V_CASES(3) LP_V_CASES(4)
+                        LP_V_CASES(5) LP_V_CASES(6) LP_V_CASES(7) LP_V_CASES(8) LP_V_CASES(9)
+                        LP_V_CASES(10) LP_V_CASES(11) LP_V_CASES(12) LP_V_CASES(13) LP_V_CASES(14)
+                        LP_W1_CASES(0) LP_W1_CASES(1) LP_W1_CASES(2) LP_W1_CASES(3) LP_W1_CASES(4)
+#undef LP_V_CASES
+#undef LP_W1_CASES
+                        default:
+                            break;
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < NS; ++j) {
+                    uint32_t ad = a0;
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        if (j & (1 << r)) ad ^= rp[r];
+                    *reinterpret_cast<double2 *>(smem_raw + ad) = v[j];
+                }
+            }
+            __syncthreads();
+        }
+        // ---- store: logical x = tid + 128 j from S (M x ^ b) ----
+        uint32_t sbt = p.sb_static;
+        for (uint32_t m = fired; m; m &= m - 1) sbt ^= p.sv_ev[__ffs(m) - 1];
+        if (!p.noio) {
+            double2 *ps = a + (base | d_tid);
+            uint32_t mo = m_tid ^ (sbt << 4);
+            uint64_t dj = 0;
+            const int nj = 1 << (K - 7);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                if (i >= nj) break;
+                if (i) {
+                    const int b = lp_ctz5(i);
+                    mo ^= m_hi[b];
+                    dj ^= d_hi[b];
+                }
+                ps[dj] = *reinterpret_cast<const double2 *>(smem_raw + mo);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+size_t lpass_smem_bytes(int K, int ncoef) { return lp_smem(K, ncoef).total; }
+
+static int lp_num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+// CTAs per SM: 3 for R = 4 (64 KiB tile + <= 7.5 KiB coefficients each), 2 for R = 5
+int lpass_ctas_per_sm(int R) { return R == 4 ? 3 : 2; }
+int lpass_max_coef(int R) { return R == 4 ? 960 : LP_MAX_COEF; }
+
+void launch_lpass_e(const LPassParams &p, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_lpass_e<4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)lp_smem(LP_MAX_K, 960).total);
+        cudaFuncSetAttribute(k_lpass_e<5, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)lp_smem(LP_MAX_K, LP_MAX_COEF).total);
+        attr = true;
+    }
+    const uint64_t cap = (uint64_t)lp_num_sms() * lpass_ctas_per_sm(p.R);
+    const int grid = (int)(p.ntiles < cap ? p.ntiles : cap);
+    const size_t sm = lp_smem(p.K, p.ncoef).total;
+    if (p.R == 5)
+        k_lpass_e<5, 2><<<grid, LP_THREADS, sm, s>>>(p);
+    else
+        k_lpass_e<4, 3><<<grid, LP_THREADS, sm, s>>>(p);
+}
+
+}  // namespace qsim
