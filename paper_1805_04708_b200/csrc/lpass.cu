@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "lpass.h"
 
@@ -127,13 +128,20 @@ __host__ __device__ inline LPSmem lp_smem(int K, int ncoef) {
 // the table): logical x += a y; y += t x -- every FMA writes its own input
 template <int NS, int RB, bool FLIP>
 __device__ __forceinline__ void lp_lift(double2 (&v)[NS], double t, double a) {
+    // all x updates first, then all y updates: dependent FMAs NS/2 apart
 #pragma unroll
     for (int j0 = 0; j0 < NS; ++j0) {
         if (j0 & (1 << RB)) continue;
         double2 &x = FLIP ? v[j0 | (1 << RB)] : v[j0];
-        double2 &y = FLIP ? v[j0] : v[j0 | (1 << RB)];
+        const double2 &y = FLIP ? v[j0] : v[j0 | (1 << RB)];
         x.x = fma(a, y.x, x.x);
         x.y = fma(a, y.y, x.y);
+    }
+#pragma unroll
+    for (int j0 = 0; j0 < NS; ++j0) {
+        if (j0 & (1 << RB)) continue;
+        const double2 &x = FLIP ? v[j0 | (1 << RB)] : v[j0];
+        double2 &y = FLIP ? v[j0] : v[j0 | (1 << RB)];
         y.x = fma(t, x.x, y.x);
         y.y = fma(t, x.y, y.y);
     }
@@ -142,17 +150,197 @@ __device__ __forceinline__ void lp_lift(double2 (&v)[NS], double t, double a) {
 // v[j] *= T[j ^ g]; tb = byte offset of the table in shared memory + 16 g
 template <int NS>
 __device__ __forceinline__ void lp_table(double2 (&v)[NS], const unsigned char *smem, uint32_t tb) {
+    double2 c[NS];
+#pragma unroll
+    for (int j = 0; j < NS; ++j) c[j] = *reinterpret_cast<const double2 *>(smem + (tb ^ (uint32_t)(j << 4)));
+    double p[NS], q[NS];
 #pragma unroll
     for (int j = 0; j < NS; ++j) {
-        const double2 c = *reinterpret_cast<const double2 *>(smem + (tb ^ (uint32_t)(j << 4)));
-        const double2 x = v[j];
-        const double p = c.y * x.y, q = c.y * x.x;
-        v[j].x = fma(c.x, x.x, -p);
-        v[j].y = fma(c.x, x.y, q);
+        p[j] = c[j].y * v[j].y;
+        q[j] = c[j].y * v[j].x;
+    }
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+        v[j].x = fma(c[j].x, v[j].x, -p[j]);
+        v[j].y = fma(c[j].x, v[j].y, q[j]);
     }
 }
 
-template <int R, int MINB>
+// tile load (cp.async) / store of the NJ = 2^(K-7) elements of this thread:
+// logical x = tid + 128 j, j in Gray-code order (one column changes per step)
+template <int NJ>
+__device__ __forceinline__ void lp_tile_load(unsigned char *smem, const char *gp, uint32_t so, const uint32_t *s_hi,
+                                             const uint64_t *d_hi) {
+    uint64_t dj = 0;
+#pragma unroll
+    for (int i = 0; i < NJ; ++i) {
+        if (i) {
+            so ^= s_hi[lp_ctz5(i)];
+            dj ^= d_hi[lp_ctz5(i)];
+        }
+        lp_cp_async16(smem + so, gp + dj);
+    }
+}
+template <int NJ>
+__device__ __forceinline__ void lp_tile_store(const unsigned char *smem, char *gp, uint32_t mo, const uint32_t *m_hi,
+                                              const uint64_t *d_hi) {
+    uint64_t dj = 0;
+#pragma unroll
+    for (int i = 0; i < NJ; ++i) {
+        if (i) {
+            mo ^= m_hi[lp_ctz5(i)];
+            dj ^= d_hi[lp_ctz5(i)];
+        }
+        *reinterpret_cast<double2 *>(gp + dj) = *reinterpret_cast<const double2 *>(smem + mo);
+    }
+}
+
+// table variant offset (bytes in shared memory) of a group: the group's
+// values of up to 2 condition bits select among the op's consecutive tables
+template <int R>
+__device__ __forceinline__ uint32_t lp_toff(uint64_t h, const LOp &o, uint32_t xq, uint64_t full, uint32_t cpool_off) {
+    uint32_t toff = cpool_off + (uint32_t)((h >> 32) & 0xffffu) * 8u;
+    const uint32_t nv = (uint32_t)(h >> 48) & 0xffu;
+    if (nv) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+            if (i < (int)nv) {
+                const uint32_t c = o.rowc[i];
+                const uint32_t bit = c < 64 ? (xq >> c) & 1u : (uint32_t)(full >> (c - 64)) & 1u;
+                toff += bit << (i + R + 4);
+            }
+    }
+    return toff;
+}
+
+// One op of the stage program on one register group (v, g: its register
+// values and flip vector; xq: its logical tile bits outside the registers).
+template <int R>
+__device__ __forceinline__ void lp_op1(double2 (&v)[1 << R], uint32_t &g, uint32_t xq, uint64_t full, uint64_t h,
+                                       const LOp &o, const LPassParams &p, const unsigned char *smem_raw,
+                                       uint32_t cpool_off) {
+    constexpr int NS = 1 << R;
+    const uint32_t code = (uint32_t)h & 0xffu;
+    const uint32_t coef = (uint32_t)(h >> 32) & 0xffffu;
+    if ((h >> 8) & LF_COND) {
+        if (((xq & o.tmask) != o.tval) || ((full & o.omask) != o.oval)) return;
+    }
+    const uint32_t toff = lp_toff<R>(h, o, xq, full, cpool_off);
+    if (code == LOP_CODE_ROUND) {
+        lp_table<NS>(v, smem_raw, toff | (g << 4));
+        const uint32_t mask = (uint32_t)(h >> 24) & 0xffu;
+        const double *sp = p.sc + o.pm;
+        int k = 0;
+#define LP_ROUND_BIT(RB)                                                          \
+    if constexpr ((RB) < R) {                                                     \
+        if ((mask >> (RB)) & 1u) {                                                \
+            const double t = sp[2 * k], aa = sp[2 * k + 1];                       \
+            ++k;                                                                  \
+            if ((g >> (RB)) & 1u)                                                 \
+lp_lift<NS, ((RB) < R ? (RB) : 0), true>(v, t, aa);               \
+            else                                                                  \
+lp_lift<NS, ((RB) < R ? (RB) : 0), false>(v, t, aa);              \
+        }                                                                         \
+    }
+        LP_ROUND_BIT(0) LP_ROUND_BIT(1) LP_ROUND_BIT(2) LP_ROUND_BIT(3) LP_ROUND_BIT(4)
+#undef LP_ROUND_BIT
+        return;
+    }
+    if (code == LOP_CODE_DIAGT) {
+        lp_table<NS>(v, smem_raw, toff | (g << 4));
+        return;
+    }
+    if (code == LOP_CODE_FLIP) {
+        g ^= (uint32_t)(h >> 24) & 0xffu;
+        return;
+    }
+    const uint32_t gp = lp_par(((uint32_t)(h >> 16) & 0xffu) & g);
+    switch (code) {
+#define LP_V_CASES(VS)                                                                                    \
+    case LOP_SHEARU * 16 + (VS):                                                                          \
+        if constexpr ((VS) < lp_nv(R)) {                                                                  \
+            const double t = p.sc[coef];                                                                  \
+            lp_shearu<NS, lp_vec(R, (VS))>(v, ((o.pm ^ gp) & 1u) ? -t : t);                               \
+        }                                                                                                 \
+        break;                                                                                            \
+    case LOP_SHEAR * 16 + (VS):                                                                           \
+        if constexpr ((VS) < lp_nv(R)) lp_shear<NS, lp_vec(R, (VS))>(v, p.sc[coef], o.pm, gp);             \
+        break;
+#define LP_W1_CASES(VS)                                                                                   \
+    case LOP_CSHEAR * 16 + (VS):                                                                          \
+        if constexpr ((VS) < R) lp_cshear<NS, (1 << (VS))>(v, p.sc[coef], o.pm, gp, lp_ctl_mask(o, g));    \
+        break;                                                                                            \
+    case LOP_DENSE * 16 + (VS):                                                                           \
+        if constexpr ((VS) < R)                                                                           \
+            lp_dense<NS, (1 << (VS))>(v, reinterpret_cast<const double2 *>(p.sc + coef), o.pm, gp,        \
+                      lp_ctl_mask(o, g));                                                 \
+        break;                                                                                            \
+    case LOP_CSWAP * 16 + (VS):                                                                           \
+        if constexpr ((VS) < R) lp_cswap<NS, (1 << (VS))>(v, lp_ctl_mask(o, g));                          \
+        break;
+        LP_V_CASES(0) LP_V_CASES(1) LP_V_CASES(2) LP_V_CASES(3) LP_V_CASES(4)
+        LP_V_CASES(5) LP_V_CASES(6) LP_V_CASES(7) LP_V_CASES(8) LP_V_CASES(9)
+        LP_V_CASES(10) LP_V_CASES(11) LP_V_CASES(12) LP_V_CASES(13) LP_V_CASES(14)
+        LP_W1_CASES(0) LP_W1_CASES(1) LP_W1_CASES(2) LP_W1_CASES(3) LP_W1_CASES(4)
+#undef LP_V_CASES
+#undef LP_W1_CASES
+        default:
+            break;
+    }
+}
+
+// two groups at once (same op, independent data): interleaved for ILP
+template <int NS>
+__device__ __forceinline__ void lp_table2(double2 (&v0)[NS], double2 (&v1)[NS], const unsigned char *smem, uint32_t tb0,
+                                          uint32_t tb1) {
+    double2 c0[NS], c1[NS];
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+        c0[j] = *reinterpret_cast<const double2 *>(smem + (tb0 ^ (uint32_t)(j << 4)));
+        c1[j] = *reinterpret_cast<const double2 *>(smem + (tb1 ^ (uint32_t)(j << 4)));
+    }
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+        const double p0 = c0[j].y * v0[j].y, q0 = c0[j].y * v0[j].x;
+        const double p1 = c1[j].y * v1[j].y, q1 = c1[j].y * v1[j].x;
+        v0[j].x = fma(c0[j].x, v0[j].x, -p0);
+        v0[j].y = fma(c0[j].x, v0[j].y, q0);
+        v1[j].x = fma(c1[j].x, v1[j].x, -p1);
+        v1[j].y = fma(c1[j].x, v1[j].y, q1);
+    }
+}
+template <int NS, int RB, bool FLIP>
+__device__ __forceinline__ void lp_lift2(double2 (&v0)[NS], double2 (&v1)[NS], double t, double a) {
+#pragma unroll
+    for (int j0 = 0; j0 < NS; ++j0) {
+        if (j0 & (1 << RB)) continue;
+        double2 &x0 = FLIP ? v0[j0 | (1 << RB)] : v0[j0];
+        const double2 &y0 = FLIP ? v0[j0] : v0[j0 | (1 << RB)];
+        double2 &x1 = FLIP ? v1[j0 | (1 << RB)] : v1[j0];
+        const double2 &y1 = FLIP ? v1[j0] : v1[j0 | (1 << RB)];
+        x0.x = fma(a, y0.x, x0.x);
+        x0.y = fma(a, y0.y, x0.y);
+        x1.x = fma(a, y1.x, x1.x);
+        x1.y = fma(a, y1.y, x1.y);
+    }
+#pragma unroll
+    for (int j0 = 0; j0 < NS; ++j0) {
+        if (j0 & (1 << RB)) continue;
+        const double2 &x0 = FLIP ? v0[j0 | (1 << RB)] : v0[j0];
+        double2 &y0 = FLIP ? v0[j0] : v0[j0 | (1 << RB)];
+        const double2 &x1 = FLIP ? v1[j0 | (1 << RB)] : v1[j0];
+        double2 &y1 = FLIP ? v1[j0] : v1[j0 | (1 << RB)];
+        y0.x = fma(t, x0.x, y0.x);
+        y0.y = fma(t, x0.y, y0.y);
+        y1.x = fma(t, x1.x, y1.x);
+        y1.y = fma(t, x1.y, y1.y);
+    }
+}
+
+// G = register groups a thread processes together (G = 2 needs 2^(K-R) = 256
+// groups: both groups of a thread go through each op at once -- twice the
+// independent work per dispatched op)
+template <int R, int G, int MINB>
 __global__ void __launch_bounds__(LP_THREADS, MINB) k_lpass_e(const __grid_constant__ LPassParams p) {
     constexpr int NS = 1 << R;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -183,7 +371,7 @@ __global__ void __launch_bounds__(LP_THREADS, MINB) k_lpass_e(const __grid_const
         const bool on = 7 + b < K;
         s_hi[b] = on ? (uint32_t)p.scol[7 + b] << 4 : 0u;
         m_hi[b] = on ? (uint32_t)p.smcol[7 + b] << 4 : 0u;
-        d_hi[b] = on ? (1ull << p.high_q[7 + b - LP_LOW]) : 0ull;
+        d_hi[b] = on ? (16ull << p.high_q[7 + b - LP_LOW]) : 0ull;  // bytes
     }
     __syncthreads();
     double2 *__restrict__ a = reinterpret_cast<double2 *>(p.a);
@@ -197,20 +385,12 @@ __global__ void __launch_bounds__(LP_THREADS, MINB) k_lpass_e(const __grid_const
             if ((full & p.ev_full[e]) == p.ev_full[e]) fired |= 1u << e;
         // ---- load the tile: logical x = tid + 128 j at S x ----
         if (!p.noio) {
-            // j in Gray-code order: one column changes per element
-            const double2 *pt = a + (base | d_tid);
-            uint32_t so = s_tid;
-            uint64_t dj = 0;
-            const int nj = 1 << (K - 7);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                if (i >= nj) break;
-                if (i) {
-                    const int b = lp_ctz5(i);
-                    so ^= s_hi[b];
-                    dj ^= d_hi[b];
-                }
-                lp_cp_async16(smem_raw + so, pt + dj);
+            const char *gp = reinterpret_cast<const char *>(a + (base | d_tid));
+            switch (K) {
+                case 12: lp_tile_load<32>(smem_raw, gp, s_tid, s_hi, d_hi); break;
+                case 11: lp_tile_load<16>(smem_raw, gp, s_tid, s_hi, d_hi); break;
+                case 10: lp_tile_load<8>(smem_raw, gp, s_tid, s_hi, d_hi); break;
+                default: lp_tile_load<4>(smem_raw, gp, s_tid, s_hi, d_hi); break;
             }
         }
         lp_cp_async_wait_all();
@@ -229,6 +409,96 @@ __global__ void __launch_bounds__(LP_THREADS, MINB) k_lpass_e(const __grid_const
             for (int r = 0; r < R; ++r) rp[r] = (uint32_t)st.reg_phys[r] << 4;
             const int op0 = st.first_op, op1 = st.first_op + st.nops;
             const bool nxq = st.needs_xq;
+            if constexpr (G == 2) {
+                uint32_t a0[2], xq[2], gg[2];
+                double2 v[2][NS];
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const uint32_t grp = tid + k * LP_THREADS;
+                    a0[k] = 0;
+                    xq[k] = yrest;
+                    for (int i = 0; i < K - R; ++i)
+                        if ((grp >> i) & 1u) {
+                            a0[k] ^= (uint32_t)st.grp_phys[i] << 4;
+                            if (nxq) xq[k] ^= st.grp_log[i];
+                        }
+                    gg[k] = g0;
+                }
+#pragma unroll
+                for (int k = 0; k < 2; ++k)
+#pragma unroll
+                    for (int j = 0; j < NS; ++j) {
+                        uint32_t ad = a0[k];
+#pragma unroll
+                        for (int r = 0; r < R; ++r)
+                            if (j & (1 << r)) ad ^= rp[r];
+                        v[k][j] = *reinterpret_cast<const double2 *>(smem_raw + ad);
+                    }
+                const uint64_t *oph = reinterpret_cast<const uint64_t *>(p.op);
+                uint64_t hn = op0 < op1 ? oph[op0 * (sizeof(LOp) / 8)] : 0;
+                for (int oi = op0; oi < op1; ++oi) {
+                    const uint64_t h = hn;
+                    if (oi + 1 < op1) hn = oph[(oi + 1) * (sizeof(LOp) / 8)];
+                    const LOp &o = p.op[oi];
+                    const uint32_t code = (uint32_t)h & 0xffu;
+                    const bool fast = !((h >> 8) & LF_COND) &&
+                                      (code == LOP_CODE_ROUND || code == LOP_CODE_DIAGT || code == LOP_CODE_FLIP);
+                    if (!fast) {
+                        lp_op1<R>(v[0], gg[0], xq[0], full, h, o, p, smem_raw, cpool_off);
+                        lp_op1<R>(v[1], gg[1], xq[1], full, h, o, p, smem_raw, cpool_off);
+                        continue;
+                    }
+                    if (code == LOP_CODE_FLIP) {
+                        gg[0] ^= (uint32_t)(h >> 24) & 0xffu;
+                        gg[1] ^= (uint32_t)(h >> 24) & 0xffu;
+                        continue;
+                    }
+                    lp_table2<NS>(v[0], v[1], smem_raw, lp_toff<R>(h, o, xq[0], full, cpool_off) | (gg[0] << 4),
+                                  lp_toff<R>(h, o, xq[1], full, cpool_off) | (gg[1] << 4));
+                    if (code == LOP_CODE_DIAGT) continue;
+                    const uint32_t mask = (uint32_t)(h >> 24) & 0xffu;
+                    const double *sp = p.sc + o.pm;
+                    int kk = 0;
+#define LP_ROUND_BIT2(RB)                                                              \
+    if constexpr ((RB) < R) {                                                          \
+        if ((mask >> (RB)) & 1u) {                                                     \
+            const double t = sp[2 * kk], aa = sp[2 * kk + 1];                          \
+            ++kk;                                                                      \
+            const uint32_t f0 = (gg[0] >> (RB)) & 1u, f1 = (gg[1] >> (RB)) & 1u;       \
+            constexpr int RBc = (RB) < R ? (RB) : 0;                                   \
+            if (f0 == f1) {                                                            \
+                if (f0)                                                                \
+                    lp_lift2<NS, RBc, true>(v[0], v[1], t, aa);                        \
+                else                                                                   \
+                    lp_lift2<NS, RBc, false>(v[0], v[1], t, aa);                       \
+            } else {                                                                   \
+                if (f0)                                                                \
+                    lp_lift<NS, RBc, true>(v[0], t, aa);                               \
+                else                                                                   \
+                    lp_lift<NS, RBc, false>(v[0], t, aa);                              \
+                if (f1)                                                                \
+                    lp_lift<NS, RBc, true>(v[1], t, aa);                               \
+                else                                                                   \
+                    lp_lift<NS, RBc, false>(v[1], t, aa);                              \
+            }                                                                          \
+        }                                                                              \
+    }
+                    LP_ROUND_BIT2(0) LP_ROUND_BIT2(1) LP_ROUND_BIT2(2) LP_ROUND_BIT2(3) LP_ROUND_BIT2(4)
+#undef LP_ROUND_BIT2
+                }
+#pragma unroll
+                for (int k = 0; k < 2; ++k)
+#pragma unroll
+                    for (int j = 0; j < NS; ++j) {
+                        uint32_t ad = a0[k];
+#pragma unroll
+                        for (int r = 0; r < R; ++r)
+                            if (j & (1 << r)) ad ^= rp[r];
+                        *reinterpret_cast<double2 *>(smem_raw + ad) = v[k][j];
+                    }
+                __syncthreads();
+                continue;
+            }
             for (uint32_t grp = tid; grp < ngroups; grp += LP_THREADS) {
                 uint32_t a0 = 0, xq = yrest;
                 for (int i = 0; i < K - R; ++i)
@@ -249,87 +519,9 @@ __global__ void __launch_bounds__(LP_THREADS, MINB) k_lpass_e(const __grid_const
                 const uint64_t *oph = reinterpret_cast<const uint64_t *>(p.op);
                 uint64_t hn = op0 < op1 ? oph[op0 * (sizeof(LOp) / 8)] : 0;
                 for (int oi = op0; oi < op1; ++oi) {
-                    const LOp &o = p.op[oi];
-                    const uint64_t h = hn;  // header: code | flags | rowS | gvec | coef
+                    const uint64_t h = hn;  // header: code | flags | rowS | gvec | coef | nvariants
                     if (oi + 1 < op1) hn = oph[(oi + 1) * (sizeof(LOp) / 8)];
-                    const uint32_t code = (uint32_t)h & 0xffu;
-                    const uint32_t coef = (uint32_t)(h >> 32) & 0xffffu;
-                    if ((h >> 8) & LF_COND) {
-                        if (((xq & o.tmask) != o.tval) || ((full & o.omask) != o.oval)) continue;
-                    }
-                    // table variant: the group's values of up to 2 condition bits
-                    uint32_t toff = cpool_off + coef * 8u;
-                    if ((h >> 48) & 0xffu) {
-                        const uint32_t nv = (uint32_t)(h >> 48) & 0xffu;
-#pragma unroll
-                        for (int i = 0; i < 2; ++i)
-                            if (i < (int)nv) {
-                                const uint32_t c = o.rowc[i];
-                                const uint32_t bit = c < 64 ? (xq >> c) & 1u : (uint32_t)(full >> (c - 64)) & 1u;
-                                toff += bit << (i + R + 4);  // variant stride: one table, 2^R x 16 bytes
-                            }
-                    }
-                    if (code == LOP_CODE_ROUND) {
-                        lp_table<NS>(v, smem_raw, toff | (g << 4));
-                        const uint32_t mask = (uint32_t)(h >> 24) & 0xffu;
-                        const double *sp = p.sc + o.pm;
-                        int k = 0;
-#define LP_ROUND_BIT(RB)                                                          \
-    if constexpr ((RB) < R) {                                                     \
-        if ((mask >> (RB)) & 1u) {                                                \
-            const double t = sp[2 * k], aa = sp[2 * k + 1];                       \
-            ++k;                                                                  \
-            if ((g >> (RB)) & 1u)                                                 \
-                lp_lift<NS, ((RB) < R ? (RB) : 0), true>(v, t, aa);               \
-            else                                                                  \
-                lp_lift<NS, ((RB) < R ? (RB) : 0), false>(v, t, aa);              \
-        }                                                                         \
-    }
-                        LP_ROUND_BIT(0) LP_ROUND_BIT(1) LP_ROUND_BIT(2) LP_ROUND_BIT(3) LP_ROUND_BIT(4)
-#undef LP_ROUND_BIT
-                        continue;
-                    }
-                    if (code == LOP_CODE_DIAGT) {
-                        lp_table<NS>(v, smem_raw, toff | (g << 4));
-                        continue;
-                    }
-                    if (code == LOP_CODE_FLIP) {
-                        g ^= (uint32_t)(h >> 24) & 0xffu;
-                        continue;
-                    }
-                    const uint32_t gp = lp_par(((uint32_t)(h >> 16) & 0xffu) & g);
-                    switch (code) {
-#define LP_V_CASES(VS)                                                                                    \
-    case LOP_SHEARU * 16 + (VS):                                                                          \
-        if constexpr ((VS) < lp_nv(R)) {                                                                  \
-            const double t = p.sc[coef];                                                                  \
-            lp_shearu<NS, lp_vec(R, (VS))>(v, ((o.pm ^ gp) & 1u) ? -t : t);                               \
-        }                                                                                                 \
-        break;                                                                                            \
-    case LOP_SHEAR * 16 + (VS):                                                                           \
-        if constexpr ((VS) < lp_nv(R)) lp_shear<NS, lp_vec(R, (VS))>(v, p.sc[coef], o.pm, gp);             \
-        break;
-#define LP_W1_CASES(VS)                                                                                   \
-    case LOP_CSHEAR * 16 + (VS):                                                                          \
-        if constexpr ((VS) < R) lp_cshear<NS, (1 << (VS))>(v, p.sc[coef], o.pm, gp, lp_ctl_mask(o, g));    \
-        break;                                                                                            \
-    case LOP_DENSE * 16 + (VS):                                                                           \
-        if constexpr ((VS) < R)                                                                           \
-            lp_dense<NS, (1 << (VS))>(v, reinterpret_cast<const double2 *>(p.sc + coef), o.pm, gp,        \
-                                      lp_ctl_mask(o, g));                                                 \
-        break;                                                                                            \
-    case LOP_CSWAP * 16 + (VS):                                                                           \
-        if constexpr ((VS) < R) lp_cswap<NS, (1 << (VS))>(v, lp_ctl_mask(o, g));                          \
-        break;
-                        LP_V_CASES(0) LP_V_CASES(1) LP_V_CASES(2) LP_V_CASES(3) LP_V_CASES(4)
-                        LP_V_CASES(5) LP_V_CASES(6) LP_V_CASES(7) LP_V_CASES(8) LP_V_CASES(9)
-                        LP_V_CASES(10) LP_V_CASES(11) LP_V_CASES(12) LP_V_CASES(13) LP_V_CASES(14)
-                        LP_W1_CASES(0) LP_W1_CASES(1) LP_W1_CASES(2) LP_W1_CASES(3) LP_W1_CASES(4)
-#undef LP_V_CASES
-#undef LP_W1_CASES
-                        default:
-                            break;
-                    }
+                    lp_op1<R>(v, g, xq, full, h, p.op[oi], p, smem_raw, cpool_off);
                 }
 #pragma unroll
                 for (int j = 0; j < NS; ++j) {
@@ -346,19 +538,13 @@ __global__ void __launch_bounds__(LP_THREADS, MINB) k_lpass_e(const __grid_const
         uint32_t sbt = p.sb_static;
         for (uint32_t m = fired; m; m &= m - 1) sbt ^= p.sv_ev[__ffs(m) - 1];
         if (!p.noio) {
-            double2 *ps = a + (base | d_tid);
-            uint32_t mo = m_tid ^ (sbt << 4);
-            uint64_t dj = 0;
-            const int nj = 1 << (K - 7);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                if (i >= nj) break;
-                if (i) {
-                    const int b = lp_ctz5(i);
-                    mo ^= m_hi[b];
-                    dj ^= d_hi[b];
-                }
-                ps[dj] = *reinterpret_cast<const double2 *>(smem_raw + mo);
+            char *gp = reinterpret_cast<char *>(a + (base | d_tid));
+            const uint32_t mo = m_tid ^ (sbt << 4);
+            switch (K) {
+                case 12: lp_tile_store<32>(smem_raw, gp, mo, m_hi, d_hi); break;
+                case 11: lp_tile_store<16>(smem_raw, gp, mo, m_hi, d_hi); break;
+                case 10: lp_tile_store<8>(smem_raw, gp, mo, m_hi, d_hi); break;
+                default: lp_tile_store<4>(smem_raw, gp, mo, m_hi, d_hi); break;
             }
         }
         __syncthreads();
@@ -384,20 +570,28 @@ int lpass_max_coef(int R) { return R == 4 ? 960 : LP_MAX_COEF; }
 
 void launch_lpass_e(const LPassParams &p, cudaStream_t s) {
     static bool attr = false;
+    static int g2 = -1;
     if (!attr) {
-        cudaFuncSetAttribute(k_lpass_e<4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_lpass_e<4, 1, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)lp_smem(LP_MAX_K, 960).total);
-        cudaFuncSetAttribute(k_lpass_e<5, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_lpass_e<4, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)lp_smem(LP_MAX_K, LP_MAX_COEF).total);
+        cudaFuncSetAttribute(k_lpass_e<5, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)lp_smem(LP_MAX_K, LP_MAX_COEF).total);
+        const char *e = getenv("QSIM_LPASS_G2");
+        g2 = e ? atoi(e) : 0;
         attr = true;
     }
-    const uint64_t cap = (uint64_t)lp_num_sms() * lpass_ctas_per_sm(p.R);
+    const bool use_g2 = g2 && p.R == 4 && p.K - p.R == 8;
+    const uint64_t cap = (uint64_t)lp_num_sms() * (use_g2 ? 2 : lpass_ctas_per_sm(p.R));
     const int grid = (int)(p.ntiles < cap ? p.ntiles : cap);
     const size_t sm = lp_smem(p.K, p.ncoef).total;
     if (p.R == 5)
-        k_lpass_e<5, 2><<<grid, LP_THREADS, sm, s>>>(p);
+        k_lpass_e<5, 1, 2><<<grid, LP_THREADS, sm, s>>>(p);
+    else if (use_g2)
+        k_lpass_e<4, 2, 2><<<grid, LP_THREADS, sm, s>>>(p);
     else
-        k_lpass_e<4, 3><<<grid, LP_THREADS, sm, s>>>(p);
+        k_lpass_e<4, 1, 3><<<grid, LP_THREADS, sm, s>>>(p);
 }
 
 }  // namespace qsim
