@@ -62,6 +62,7 @@ struct qsim_state {
     int pass_r = 4;  // register qubits per pass stage (QSIM_PASS_R=5 selects 32-amplitude groups)
     int use_mma = 1; // tensor-core (DMMA) pair stages in fused passes (QSIM_PASS_MMA=0 disables)
     int pass_kernel = 1;  // 1: relabelling pass k_lpass_e (lpass.h); 0: k_pass_e (QSIM_PASS_KERNEL=0)
+    int pass_k = LP_MAX_K;  // tile qubits of the relabelling pass (QSIM_LPASS_K = 9..12)
     size_t amp_bytes = 16;
     uint64_t alloc_amps = 0;  // max(2^nl, 256): small shards are padded with zero amplitudes
     Planner pl;
@@ -690,7 +691,7 @@ static int run_gates_lpass(qsim_state *s, const std::vector<PlanOp> &run, const 
     }
     LRunConfig cfg;
     cfg.nl = s->nl;
-    cfg.K = std::min(LP_MAX_K, s->nl);
+    cfg.K = std::min(s->pass_k, s->nl);
     cfg.R = s->pass_r;
     cfg.max_coef = lpass_max_coef(cfg.R);
     cfg.defer = getenv("QSIM_LPASS_NODEFER") == nullptr;
@@ -1074,6 +1075,7 @@ int qsim_create_ex(const qsim_config *cfg, qsim_state **out) {
     if (const char *pr = getenv("QSIM_PASS_R")) s->pass_r = (atoi(pr) == 4) ? 4 : 5;
     if (const char *pm = getenv("QSIM_PASS_MMA")) s->use_mma = atoi(pm) != 0;
     if (const char *pk = getenv("QSIM_PASS_KERNEL")) s->pass_kernel = atoi(pk) != 0 ? 1 : 0;
+    if (const char *lk = getenv("QSIM_LPASS_K")) s->pass_k = std::max(LP_MIN_K, std::min(LP_MAX_K, atoi(lk)));
     s->amp_bytes = s->enc == QSIM_ENC_FP64 ? 16 : 2;
     if (cfg->device >= 0) {
         if (cudaSetDevice(cfg->device) != cudaSuccess) {

@@ -150,19 +150,19 @@ __device__ __forceinline__ void lp_lift(double2 (&v)[NS], double t, double a) {
 // v[j] *= T[j ^ g]; tb = byte offset of the table in shared memory + 16 g
 template <int NS>
 __device__ __forceinline__ void lp_table(double2 (&v)[NS], const unsigned char *smem, uint32_t tb) {
-    double2 c[NS];
+    // chunks of 8 entries: bounded register pressure, loads still ahead of the math
+    constexpr int CH = NS < 8 ? NS : 8;
 #pragma unroll
-    for (int j = 0; j < NS; ++j) c[j] = *reinterpret_cast<const double2 *>(smem + (tb ^ (uint32_t)(j << 4)));
-    double p[NS], q[NS];
+    for (int j0 = 0; j0 < NS; j0 += CH) {
+        double2 c[CH];
 #pragma unroll
-    for (int j = 0; j < NS; ++j) {
-        p[j] = c[j].y * v[j].y;
-        q[j] = c[j].y * v[j].x;
-    }
+        for (int j = 0; j < CH; ++j) c[j] = *reinterpret_cast<const double2 *>(smem + (tb ^ (uint32_t)((j0 + j) << 4)));
 #pragma unroll
-    for (int j = 0; j < NS; ++j) {
-        v[j].x = fma(c[j].x, v[j].x, -p[j]);
-        v[j].y = fma(c[j].x, v[j].y, q[j]);
+        for (int j = 0; j < CH; ++j) {
+            const double p = c[j].y * v[j0 + j].y, q = c[j].y * v[j0 + j].x;
+            v[j0 + j].x = fma(c[j].x, v[j0 + j].x, -p);
+            v[j0 + j].y = fma(c[j].x, v[j0 + j].y, q);
+        }
     }
 }
 
@@ -576,6 +576,8 @@ void launch_lpass_e(const LPassParams &p, cudaStream_t s) {
                              (int)lp_smem(LP_MAX_K, 960).total);
         cudaFuncSetAttribute(k_lpass_e<4, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)lp_smem(LP_MAX_K, LP_MAX_COEF).total);
+        cudaFuncSetAttribute(k_lpass_e<4, 1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)lp_smem(11, 960).total);
         cudaFuncSetAttribute(k_lpass_e<5, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)lp_smem(LP_MAX_K, LP_MAX_COEF).total);
         const char *e = getenv("QSIM_LPASS_G2");
@@ -583,13 +585,16 @@ void launch_lpass_e(const LPassParams &p, cudaStream_t s) {
         attr = true;
     }
     const bool use_g2 = g2 && p.R == 4 && p.K - p.R == 8;
-    const uint64_t cap = (uint64_t)lp_num_sms() * (use_g2 ? 2 : lpass_ctas_per_sm(p.R));
+    const bool use_4 = !use_g2 && p.R == 4 && p.K <= 11;  // 32 KiB tiles: 4 CTAs per SM
+    const uint64_t cap = (uint64_t)lp_num_sms() * (use_g2 ? 2 : use_4 ? 4 : lpass_ctas_per_sm(p.R));
     const int grid = (int)(p.ntiles < cap ? p.ntiles : cap);
     const size_t sm = lp_smem(p.K, p.ncoef).total;
     if (p.R == 5)
         k_lpass_e<5, 1, 2><<<grid, LP_THREADS, sm, s>>>(p);
     else if (use_g2)
         k_lpass_e<4, 2, 2><<<grid, LP_THREADS, sm, s>>>(p);
+    else if (use_4)
+        k_lpass_e<4, 1, 4><<<grid, LP_THREADS, sm, s>>>(p);
     else
         k_lpass_e<4, 1, 3><<<grid, LP_THREADS, sm, s>>>(p);
 }
