@@ -256,12 +256,20 @@ const char *qsim_last_error(void);
  * The exchange/remap plan the executor follows (a2, a7): for testing the
  * sharded path's host logic on CPU.  An op is either
  *   QSIM_OP_EXCHANGE: swap physical global bit `g` with local bit `l`
- *     (shard r and r ^ 2^(g-nl) trade half-shards; qubit map updated), or
+ *     (the shards holding global bits G and G ^ 2^(g-nl) trade half-shards;
+ *     qubit map updated),
  *   QSIM_OP_GATE: gate on physical bits (target `l`, controls) with class
- *     0 = dense, 1 = diagonal, 2 = anti-diagonal, 3 = identity (skipped).
+ *     0 = dense, 1 = diagonal, 2 = anti-diagonal, 3 = identity (skipped), or
+ *   QSIM_OP_RELABEL: an anti-diagonal gate (X, CNOT, Toffoli, Y, ...) whose
+ *     target `l` and controls are all global bits: its phase part runs as a
+ *     diagonal gate and its permutation part only relabels which shard holds
+ *     which global bits -- no data moves (PAPER.md:389-392 does this for
+ *     SWAP; CNOT "can be implemented without having to exchange data",
+ *     P:395-400).
  * Ownership: qsim_plan_create allocates *out, qsim_plan_destroy frees it. */
 #define QSIM_OP_EXCHANGE 0
 #define QSIM_OP_GATE 1
+#define QSIM_OP_RELABEL 2
 typedef struct qsim_plan qsim_plan;
 typedef struct qsim_plan_op {
     int32_t type;        /* QSIM_OP_* */

@@ -37,6 +37,7 @@ GATE_U = 0
 GATE_SWAP = 1
 OP_EXCHANGE = 0
 OP_GATE = 1
+OP_RELABEL = 2  # permutation gate on global bits: shard relabelling, no data movement
 
 
 class QsimError(RuntimeError):

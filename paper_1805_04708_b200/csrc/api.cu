@@ -86,6 +86,7 @@ struct qsim_state {
     bool prof = false;
     std::vector<ProfRec> prof_recs;
     std::vector<cudaEvent_t> ev_pool;
+    std::vector<uint32_t> gphys, ginv;  // storage index -> physical global bits (phi) and inverse
     cudaEvent_t prof_a = nullptr;  // pending start event
 };
 
@@ -117,14 +118,25 @@ static void prof_end(qsim_state *s, int kind, double bytes, double flops = 0.0) 
     s->prof_recs.push_back({kind, bytes, flops, s->prof_a, b});
     s->prof_a = nullptr;
 }
-static uint64_t shard_base(const qsim_state *s, const Shard &sh) { return (uint64_t)sh.index << s->nl; }
+// Physical global bits held by a shard's storage: phi(index).  Permutation
+// gates on global qubits (planner op QSIM_OP_RELABEL) permute phi instead of
+// moving data.
+static uint32_t shard_phys(const qsim_state *s, const Shard &sh) { return s->gphys[sh.index]; }
+static uint64_t shard_base(const qsim_state *s, const Shard &sh) { return (uint64_t)shard_phys(s, sh) << s->nl; }
 
-static int rank_bit(const Shard &sh, int phys_bit, int nl) { return (sh.index >> (phys_bit - nl)) & 1; }
+static int rank_bit(const qsim_state *s, const Shard &sh, int phys_bit) {
+    return (shard_phys(s, sh) >> (phys_bit - s->nl)) & 1;
+}
+static void reset_labels(qsim_state *s) {
+    s->gphys.resize(s->P);
+    s->ginv.resize(s->P);
+    for (int r = 0; r < s->P; ++r) s->gphys[r] = s->ginv[r] = (uint32_t)r;
+}
 
 // Whether all controls that sit on global bits are 1 for this shard.
 static bool global_ctrls_ok(const qsim_state *s, const Shard &sh, const PlanOp &o) {
     for (int c = 0; c < o.nctrl; ++c)
-        if (o.ctrl[c] >= s->nl && !rank_bit(sh, o.ctrl[c], s->nl)) return false;
+        if (o.ctrl[c] >= s->nl && !rank_bit(s, sh, o.ctrl[c])) return false;
     return true;
 }
 
@@ -144,7 +156,7 @@ static double gate_bytes_alone(const qsim_state *s, const Shard &sh, const PlanO
     double per = 2.0 * (double)s->amp_bytes;  // read + write
     if (o.cls == CLS_DIAG) {
         if (o.l >= s->nl) {
-            int bit = rank_bit(sh, o.l, s->nl);
+            int bit = rank_bit(s, sh, o.l);
             double fr = bit ? u[6] : u[0], fi = bit ? u[7] : u[1];
             return (fr == 1.0 && fi == 0.0) ? 0.0 : amps * per;
         }
@@ -171,7 +183,7 @@ static double gate_flops(const qsim_state *s, const Shard &sh, const PlanOp &o, 
     if (o.cls == CLS_DIAG) {
         bool one0 = u[0] == 1.0 && u[1] == 0.0, one1 = u[6] == 1.0 && u[7] == 0.0;
         if (o.l >= s->nl) {
-            int bit = rank_bit(sh, o.l, s->nl);
+            int bit = rank_bit(s, sh, o.l);
             return (bit ? one1 : one0) ? 0.0 : 6.0 * amps;
         }
         return 6.0 * amps * ((one0 ? 0.0 : 0.5) + (one1 ? 0.0 : 0.5));
@@ -193,7 +205,7 @@ static int sweep_gate_e(qsim_state *s, const PlanOp &o, const double *u) {
                 cm |= 1ull << o.ctrl[c];
             }
         if (o.l >= s->nl) {  // diagonal gate on a global bit: uniform factor on the shard
-            int bit = rank_bit(sh, o.l, s->nl);
+            int bit = rank_bit(s, sh, o.l);
             ScaleParams p{};
             p.a = sh.amps;
             p.f[0] = bit ? u[6] : u[0];
@@ -798,10 +810,11 @@ static int exchange(qsim_state *s, const PlanOp &x, const PlanOp *gop, const dou
     };
     if (s->transport == QSIM_TRANSPORT_LOCAL) {
         for (auto &sa : s->shards) {
-            if ((sa.index >> j) & 1) continue;
+            if ((shard_phys(s, sa) >> j) & 1) continue;
             Shard *sb = nullptr;
+            const uint32_t want = s->ginv[shard_phys(s, sa) | (1u << j)];
             for (auto &t : s->shards)
-                if (t.index == (sa.index | (1 << j))) sb = &t;
+                if ((uint32_t)t.index == want) sb = &t;
             for (uint64_t c = 0; c < nchunks; ++c) {
                 // sa (b=0) sends slot(l=1), sb (b=1) sends slot(l=0)
                 const char *src_a = (const char *)sa.amps + ins0(c * C, l) * ab + ((size_t)1 << l) * ab;
@@ -831,8 +844,8 @@ static int exchange(qsim_state *s, const PlanOp &x, const PlanOp *gop, const dou
     }
     // ---- NCCL: one shard per process, double-buffered chunk pipeline ----
     Shard &sh = s->shards[0];
-    const int b = (sh.index >> j) & 1;
-    const int partner = sh.index ^ (1 << j);
+    const int b = (shard_phys(s, sh) >> j) & 1;
+    const int partner = (int)s->ginv[shard_phys(s, sh) ^ (1u << j)];
     CU(cudaEventRecord(s->ev_start, s->stream));
     CU(cudaStreamWaitEvent(s->comm_stream, s->ev_start, 0));
     for (uint64_t c = 0; c < nchunks; ++c) {
@@ -870,6 +883,7 @@ static int run_gates_a(qsim_state *s, const std::vector<PlanOp> &run, const std:
 static int execute(qsim_state *s, const qsim_gate *gates, size_t ngates, const std::vector<PlanOp> &ops) {
     std::vector<PlanOp> run;
     std::vector<const double *> us;
+    std::deque<std::array<double, 8>> synth;  // phase parts of relabelled anti-diagonal gates
     auto flush = [&]() -> int {
         if (run.empty()) return QSIM_OK;
         int rc = (s->enc == QSIM_ENC_FP64) ? run_gates_e(s, run, us) : run_gates_a(s, run, us);
@@ -879,6 +893,31 @@ static int execute(qsim_state *s, const qsim_gate *gates, size_t ngates, const s
     };
     for (size_t i = 0; i < ops.size(); ++i) {
         const PlanOp &o = ops[i];
+        if (o.type == QSIM_OP_RELABEL) {
+            // anti-diagonal U = X . diag(u10, u01) with target and controls on global
+            // bits: the phase part is a diagonal gate (per-shard factor), the X part
+            // permutes the shards' physical labels -- no data moves
+            const double *u = gates[o.gate_index].u;
+            if (!(u[2] == 1.0 && u[3] == 0.0 && u[4] == 1.0 && u[5] == 0.0)) {
+                synth.push_back({u[4], u[5], 0.0, 0.0, 0.0, 0.0, u[2], u[3]});
+                PlanOp d = o;
+                d.type = QSIM_OP_GATE;
+                d.cls = classify(synth.back().data());
+                if (d.cls != CLS_IDENT) {
+                    run.push_back(d);
+                    us.push_back(synth.back().data());
+                }
+            }
+            RC(flush());
+            const uint32_t tb = 1u << (o.l - s->nl);
+            for (int r = 0; r < s->P; ++r) {
+                bool on = true;
+                for (int c = 0; c < o.nctrl; ++c) on = on && ((s->gphys[r] >> (o.ctrl[c] - s->nl)) & 1u);
+                if (on) s->gphys[r] ^= tb;
+            }
+            for (int r = 0; r < s->P; ++r) s->ginv[s->gphys[r]] = (uint32_t)r;
+            continue;
+        }
         if (o.type == QSIM_OP_EXCHANGE) {
             RC(flush());
             const PlanOp *g = nullptr;
@@ -942,7 +981,7 @@ static int phys_probs(qsim_state *s, std::vector<double> &phys) {
         phys[0] += s->h_out[0];
         for (int b = 0; b < s->nl; ++b) phys[1 + b] += s->h_out[1 + b];
         for (int b = s->nl; b < s->n; ++b)
-            if (rank_bit(sh, b, s->nl)) phys[1 + b] += s->h_out[0];
+            if (rank_bit(s, sh, b)) phys[1 + b] += s->h_out[0];
     }
     if (s->transport == QSIM_TRANSPORT_NCCL) {
         CU(cudaMemcpyAsync(s->d_out, phys.data(), phys.size() * sizeof(double), cudaMemcpyHostToDevice, s->stream));
@@ -1002,6 +1041,7 @@ int qsim_destroy(qsim_state *s) {
 
 static int init_state(qsim_state *s) {
     // |0...0>: a(0) = 1 on shard 0 (E); codes (127, 0) at 0, (-128, 0) elsewhere (A)
+    reset_labels(s);
     for (auto &sh : s->shards) {
         size_t bytes = s->alloc_amps * s->amp_bytes;
         if (s->enc == QSIM_ENC_FP64) {
@@ -1347,9 +1387,9 @@ int qsim_expectations(qsim_state *s, double *q) {
             // pairs across shards r (bit 0) and r | 2^(b-nl): dot products, no data movement
             const int j = b - s->nl;
             for (auto &sa : s->shards) {
-                if ((sa.index >> j) & 1) continue;
+                if ((shard_phys(s, sa) >> j) & 1) continue;
                 for (auto &sb : s->shards)
-                    if (sb.index == (sa.index | (1 << j))) {
+                    if ((uint32_t)sb.index == s->ginv[shard_phys(s, sa) | (1u << j)]) {
                         if (s->enc == QSIM_ENC_FP64)
                             launch_dot_e(sa.amps, sb.amps, 1ull << s->nl, s->d_partials, s->d_out, s->stream);
                         else
@@ -1419,7 +1459,7 @@ static int collapse(qsim_state *s, int b, int out, double keep) {
         for (auto &sh : s->shards) {
             if (b < s->nl) {
                 launch_collapse_e(sh.amps, 1ull << s->nl, b, out, f, s->stream);
-            } else if (rank_bit(sh, b, s->nl) != out) {
+            } else if (rank_bit(s, sh, b) != out) {
                 CU(cudaMemsetAsync(sh.amps, 0, ((size_t)1 << s->nl) * s->amp_bytes, s->stream));
             } else {
                 launch_scale_all_e(sh.amps, 1ull << s->nl, f, s->stream);
@@ -1555,7 +1595,7 @@ int qsim_get_amplitudes(qsim_state *s, const uint64_t *idx, size_t m, double *ou
         which.clear();
         for (size_t k = 0; k < m; ++k) {
             uint64_t p = logical_to_phys(s, idx[k]);
-            if ((int)(p >> s->nl) == sh.index) {
+            if ((p >> s->nl) == (uint64_t)shard_phys(s, sh)) {
                 off.push_back(p & lmask);
                 which.push_back(k);
             }

@@ -146,6 +146,23 @@ void Planner::plan(const qsim_gate *gates, size_t ngates, std::vector<PlanOp> &o
         int32_t cls = classify(x.u);
         if (cls == CLS_IDENT) continue;
         int pt = pos[x.target];
+        if (pt >= nl && cls == CLS_ANTI && relabel_global) {
+            // a permutation gate on global bits only: relabel the shards (no exchange)
+            bool all_global = true;
+            for (int c = 0; c < x.ncontrols; ++c) all_global = all_global && pos[x.controls[c]] >= nl;
+            if (all_global) {
+                PlanOp r{};
+                r.type = QSIM_OP_RELABEL;
+                r.l = pt;
+                r.cls = cls;
+                r.nctrl = x.ncontrols;
+                r.ctrl[0] = x.ncontrols > 0 ? pos[x.controls[0]] : -1;
+                r.ctrl[1] = x.ncontrols > 1 ? pos[x.controls[1]] : -1;
+                r.gate_index = (int32_t)g;
+                ops.push_back(r);
+                continue;
+            }
+        }
         if (pt >= nl && cls != CLS_DIAG) {
             int avoid[2];
             int navoid = 0;

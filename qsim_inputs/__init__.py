@@ -239,6 +239,31 @@ def random_circuit(n: int = 14, ngates: int = 200, seed: int = 0, kinds=CFG1_KIN
     return c
 
 
+def global_permutations(n: int, nshards: int, seed: int) -> Circuit:
+    """Permutation gates whose target and controls are all among the top
+    log2(nshards) qubits (the global qubits of a fresh state): X, Y, and, when
+    there are enough global qubits, CNOT and Toffoli (App. B, PAPER.md:1141,
+    1151, 1300-1363), each after an H on a random local qubit so the state is
+    not a basis state.  Seeded (PCG64)."""
+    rng = np.random.default_rng(seed)
+    k = int(round(np.log2(nshards)))
+    top = list(range(n - k, n))
+    c = Circuit(n)
+    for _ in range(6):
+        c.add("H", mat_H(), int(rng.integers(0, n - k)))
+        kind = int(rng.integers(0, 4))
+        perm = [int(q) for q in rng.permutation(top)]
+        if kind == 0 or k == 1 and kind >= 2:
+            c.add("X", mat_X(), perm[0])
+        elif kind == 1:
+            c.add("Y", mat_Y(), perm[0])
+        elif kind == 2 or k == 2:
+            c.add("CNOT", mat_X(), perm[0], [perm[1]])
+        else:
+            c.add("TOFFOLI", mat_X(), perm[0], [perm[1], perm[2]])
+    return c
+
+
 def h_wall(n: int) -> Circuit:
     """PAPER.md §5.1 (653-657): H on every qubit of |0...0>."""
     c = Circuit(n)

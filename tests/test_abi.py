@@ -69,7 +69,11 @@ def _apply_plan_numpy(n, P, circ, ops, final_map):
         else:
             _, kind, t, t2, ctl, u = circ.gate(o["gate_index"])
             pt = o["l"]
-            assert o["cls"] == 1 or pt < nl  # only diagonal gates stay on global bits
+            # only diagonal gates and relabels (permutations among global bits) stay on global bits;
+            # in the physical-index view a relabel is the gate itself
+            assert o["cls"] == 1 or pt < nl or o["type"] == q.OP_RELABEL
+            if o["type"] == q.OP_RELABEL:
+                assert pt >= nl and all(c >= nl for c in o["controls"]) and o["cls"] == 2
             cm = 0
             for c in o["controls"]:
                 cm |= 1 << c
@@ -93,12 +97,15 @@ def test_planner_plan_reproduces_the_circuit(P):
     import oracle
 
     n = 11
-    circ = C.config(0, n=n, seed=P)
+    circ = C.global_permutations(n, P, seed=P)
+    circ.extend(C.config(0, n=n, seed=P))
     circ.extend(C.layered(n, 1, seed=P, h_first=False))
     circ.swap(0, n - 1)
+    circ.extend(C.global_permutations(n, P, seed=P + 1))
     ops, fmap = q.qsim_plan(n, P, circ)
     nex = sum(o["type"] == q.OP_EXCHANGE for o in ops)
     assert nex > 0
+    assert sum(o["type"] == q.OP_RELABEL for o in ops) > 0
     got = _apply_plan_numpy(n, P, circ, ops, fmap)
     assert np.max(np.abs(got - oracle.e_simulate(n, circ))) <= 1e-12
 

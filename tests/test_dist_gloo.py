@@ -43,9 +43,7 @@ def _worker(rank, world, port, n, seed, chunk, out_q):
         obj = [b"x" * 128 if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         assert obj[0] == b"x" * 128
-        circ = C.config(0, n=n, seed=seed)
-        circ.extend(C.layered(n, 2, seed=seed, h_first=False))
-        circ.swap(1, n - 1)
+        circ = _circuit(n, world, seed)
         ops, fmap = q.qsim_plan(n, world, circ)
         k = int(np.log2(world))
         nl = n - k
@@ -54,12 +52,22 @@ def _worker(rank, world, port, n, seed, chunk, out_q):
             a[0] = 1
         idx = np.arange(1 << nl)
         nex = 0
+        # phi[r]: physical global bits held by rank r (permuted by QSIM_OP_RELABEL)
+        phi = list(range(world))
         for o in ops:
+            if o["type"] == q.OP_RELABEL:
+                _, kind, t, t2, ctl, u = circ.gate(o["gate_index"])
+                jt = o["l"] - nl
+                on = [all((phi[r] >> (c - nl)) & 1 for c in o["controls"]) for r in range(world)]
+                if on[rank]:  # phase part diag(u10, u01) on the global target: a factor on the shard
+                    a *= u[0, 1] if (phi[rank] >> jt) & 1 else u[1, 0]
+                phi = [phi[r] ^ (1 << jt) if on[r] else phi[r] for r in range(world)]
+                continue
             if o["type"] == q.OP_EXCHANGE:
                 g, l = o["g"], o["l"]
                 j = g - nl
-                b = (rank >> j) & 1
-                partner = rank ^ (1 << j)
+                b = (phi[rank] >> j) & 1
+                partner = phi.index(phi[rank] ^ (1 << j))
                 half = 1 << (nl - 1)
                 C_ = min(chunk, half, 1 << l)
                 for c in range(half // C_):
@@ -74,7 +82,7 @@ def _worker(rank, world, port, n, seed, chunk, out_q):
                 continue
             _, kind, t, t2, ctl, u = circ.gate(o["gate_index"])
             pt = o["l"]
-            ok = all(((rank >> (c - nl)) & 1) for c in o["controls"] if c >= nl)
+            ok = all(((phi[rank] >> (c - nl)) & 1) for c in o["controls"] if c >= nl)
             if not ok:
                 continue
             cm = 0
@@ -83,7 +91,7 @@ def _worker(rank, world, port, n, seed, chunk, out_q):
                     cm |= 1 << c
             if pt >= nl:  # diagonal gate on a global bit: uniform factor on the shard
                 assert o["cls"] == 1
-                f = u[1, 1] if (rank >> (pt - nl)) & 1 else u[0, 0]
+                f = u[1, 1] if (phi[rank] >> (pt - nl)) & 1 else u[0, 0]
                 sel = (idx & cm) == cm
                 a[sel] *= f
                 continue
@@ -97,7 +105,10 @@ def _worker(rank, world, port, n, seed, chunk, out_q):
         full = [torch.zeros(1 << nl, dtype=torch.complex128) for _ in range(world)]
         dist.all_gather(full, torch.from_numpy(a))
         if rank == 0:
-            phys = np.concatenate([f.numpy() for f in full])
+            blocks = [None] * world
+            for r in range(world):
+                blocks[phi[r]] = full[r].numpy()  # rank r holds physical global bits phi[r]
+            phys = np.concatenate(blocks)
             pidx = np.arange(1 << n)
             L = np.zeros(1 << n, dtype=np.int64)
             for qq in range(n):
@@ -107,6 +118,15 @@ def _worker(rank, world, port, n, seed, chunk, out_q):
             out_q.put((logical, nex))
     finally:
         dist.destroy_process_group()
+
+
+def _circuit(n, world, seed):
+    circ = C.global_permutations(n, world, seed)
+    circ.extend(C.config(0, n=n, seed=seed))
+    circ.extend(C.layered(n, 2, seed=seed, h_first=False))
+    circ.swap(1, n - 1)
+    circ.extend(C.global_permutations(n, world, seed + 1))
+    return circ
 
 
 @pytest.mark.parametrize("chunk", [1 << 30, 64])
@@ -124,9 +144,7 @@ def test_two_rank_exchange_protocol_matches_oracle(chunk):
     for p in procs:
         p.join(timeout=300)
         assert p.exitcode == 0
-    circ = C.config(0, n=n, seed=seed)
-    circ.extend(C.layered(n, 2, seed=seed, h_first=False))
-    circ.swap(1, n - 1)
+    circ = _circuit(n, world, seed)
     ref = oracle.e_simulate(n, circ)
     assert nex > 0
     assert np.max(np.abs(logical - ref)) <= 1e-12

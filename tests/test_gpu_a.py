@@ -140,6 +140,22 @@ def test_sharding_is_bit_exact_in_a():
         assert np.array_equal(c, out[0][0]) and r0 == out[0][1] and r1 == out[0][2]
 
 
+def test_global_relabel_is_bit_exact_in_a():
+    """Relabelled permutation gates move A codes exactly:
+    codes with global permutations are the same for P = 1 and P = 8."""
+    n = 13
+    circ = C.rz_rx_cphase(n, 2, seed=7)
+    circ.extend(C.global_permutations(n, 8, seed=7))
+    circ.extend(C.rz_rx_cphase(n, 1, seed=8))
+    out = []
+    for P in (1, 8):
+        with q.State(n, q.ENC_ADAPTIVE2, P) as s:
+            s.apply_circuit(circ)
+            out.append(s.get_codes())
+    c8, r0, r1 = out[1]
+    assert np.array_equal(c8, out[0][0]) and r0 == out[0][1] and r1 == out[0][2]
+
+
 def test_a_readout_and_measure():
     n = 12
     circ = C.rz_rx_cphase(n, 2, seed=6)

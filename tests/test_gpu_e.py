@@ -122,6 +122,37 @@ def test_sharded_loopback_transparency(P):
     s.close()
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_global_permutation_gates_relabel_shards(P):
+    """X / Y / CNOT / Toffoli whose target and controls are
+    all global bits relabel the shards (which shard holds which global bits)
+    instead of exchanging half-shards; the result, the expectations and the
+    logical read-out are unchanged."""
+    n = 14
+    k = int(math.log2(P))
+    perm_only = C.global_permutations(n, P, seed=P)
+    nrelabel = sum(1 for o in q.qsim_plan(n, P, perm_only)[0] if o["type"] == q.OP_RELABEL)
+    assert nrelabel > 0
+    circ = C.global_permutations(n, P, seed=P)
+    circ.extend(C.config(0, n=n, seed=P))
+    circ.extend(C.layered(n, 1, seed=P, h_first=False))
+    circ.extend(C.global_permutations(n, P, seed=P + 10))
+    ref = oracle.e_simulate(n, circ)
+    with q.State(n, q.ENC_FP64, P) as s:
+        s.apply_circuit(perm_only)
+        assert s.stats()["exchanges"] == 0  # permutations among global bits move no data
+        s.reset()
+        s.apply_circuit(circ)
+        got = s.get_state()
+        assert np.max(np.abs(got - ref)) <= TOL
+        idx = np.array([0, 1, (1 << n) - 1, 12345, 1 << (n - 1), (1 << (n - k)) + 7], dtype=np.uint64)
+        assert np.max(np.abs(s.get_amplitudes(idx) - ref[idx.astype(np.int64)])) <= TOL
+        assert np.max(np.abs(s.expectations() - oracle.e_expectations(ref, n))) <= TOL
+        assert abs(s.norm() - 1.0) <= 1e-10
+
+
+@pytest.mark.gpu
 def test_sharded_small_chunks_and_unfused():
     n = 13
     circ = C.layered(n, 2, seed=7)
