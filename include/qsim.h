@@ -186,6 +186,28 @@ int qsim_sample(qsim_state *s, size_t nsamples, uint64_t seed, uint64_t *out);
  * EINVAL unless 0 <= nx < N, 2 <= G <= 2^(N-nx) and 1 <= y < G. */
 int qsim_prepare_shorbox(qsim_state *s, int nx, uint64_t G, uint64_t y);
 
+/* ---- auxiliary-variable method (§4.2) -------------
+ * Stateless: no qsim_state, no 2^N vector.  out[2k], out[2k+1] = <y_k|psi>
+ * (re, im) for the LOGICAL indices y_k = idx[k] (< 2^N), psi = the gate list
+ * applied to |0...0> (Eq. appa0), by
+ *     <y|psi> = 2^{-P} sum_{s_1..s_P = +-1} prod_j <y_j| W_j(s) |0>_j   (Eq. appa7)
+ * where every CNOT is H_t U_ct(pi) H_t and every controlled phase
+ * U_ct(a) (Eq. appa4) becomes a sum over one auxiliary variable by the
+ * discrete Hubbard-Stratonovich identity, cos 2x = e^{ia/2} (Eqs. appa5-6).
+ * Gates: single-qubit gates, and one-control gates whose 2x2 is diagonal or
+ * anti-diagonal (reading R-B9: diag(1, d0) on the control and U_ct(arg
+ * d1/d0), then a CNOT for the anti-diagonal case).  abs_sum (nullable, m
+ * doubles) receives 2^{-P} sum_s |term_s|: the HS terms are not bounded by
+ * 1 (x is complex), so the rounding error of the sum scales with it.  Runs on
+ * the current CUDA device; work O(2^P (number of qubits with variables) m).
+ * Errors: EINVAL (N outside [2,63], bad qubits / indices), EUNSUPPORTED
+ * (SWAP records, two controls, a controlled dense 2x2, P > 40, more than 2^20
+ * values on one qubit), ECUDA. */
+int qsim_aux_amplitudes(int n_qubits, const qsim_gate *gates, size_t ngates, const uint64_t *idx, size_t m,
+                        double *out, double *abs_sum);
+/* Number P of auxiliary variables of a gate list (host only, no GPU). */
+int qsim_aux_num_vars(int n_qubits, const qsim_gate *gates, size_t ngates, int *P);
+
 /* CLEAR (value 0) / SET (value 1) of App. B: project
  * `qubit` onto |value> and renormalise.  EZERONORM if the projected state has
  * norm^2 < 1e-14 ("fails if the projection results in a state with amplitude

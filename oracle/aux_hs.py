@@ -7,7 +7,9 @@ by step in the paper's notation, in plain numpy fp64/complex128:
    Reading R-B9 (the paper names single-qubit gates, controlled phase shifts
    and CNOT): a controlled diagonal gate diag(d0, d1) on t with
    control c is diag(1, d0) on c followed by U_{c t}(a), e^{ia} = d1 / d0
-   (d0 != 0); a controlled anti-diagonal [[0, u01], [u10, 0]] is the
+   (d0 != 0; no variable when d1 = d0, U_ct(0) = I, so a CNOT or a
+   controlled phase costs exactly one variable); a controlled
+   anti-diagonal [[0, u01], [u10, 0]] is the
    controlled diagonal diag(u10, u01) followed by CNOT_{c t}.  Gates with two
    controls or a controlled dense 2x2 are outside the method (ValueError).
 2. Each U_{c t}(a_p) (Eq. appa4) gets an auxiliary variable
@@ -48,11 +50,13 @@ def _rewrite(circuit):
         if diag:
             d0, d1 = u[0, 0], u[1, 1]
             ops.append(("u", c, np.diag([1.0, d0])))
-            ops.append(("cp", c, t, float(np.angle(d1 / d0))))
+            if d1 != d0:  # U_ct(0) = I needs no variable
+                ops.append(("cp", c, t, float(np.angle(d1 / d0))))
         elif anti:
             d0, d1 = u[1, 0], u[0, 1]  # U = X diag(u10, u01)
             ops.append(("u", c, np.diag([1.0, d0])))
-            ops.append(("cp", c, t, float(np.angle(d1 / d0))))
+            if d1 != d0:
+                ops.append(("cp", c, t, float(np.angle(d1 / d0))))
             h = np.array([[1, 1], [1, -1]], dtype=np.complex128) / np.sqrt(2.0)
             ops.append(("u", t, h))
             ops.append(("cp", c, t, np.pi))

@@ -87,6 +87,7 @@ EXPORTS = (
     "qsim_get_amplitudes", "qsim_get_state", "qsim_set_state", "qsim_get_codes", "qsim_set_codes", "qsim_sync",
     "qsim_project", "qsim_sample", "qsim_prepare_shorbox", "qsim_stream", "qsim_get_stats", "qsim_reset", "qsim_profile", "qsim_profile_read", "qsim_reset_stats", "qsim_get_qubit_map", "qsim_last_error",
     "qsim_plan_create", "qsim_plan_num_ops", "qsim_plan_get_op", "qsim_plan_final_map", "qsim_plan_destroy",
+    "qsim_aux_amplitudes", "qsim_aux_num_vars",
 )
 
 if not os.path.exists(_LIB_PATH):
@@ -113,6 +114,11 @@ _lib.qsim_measure.argtypes = [_P, ctypes.c_int, ctypes.c_uint64, _ip]
 _lib.qsim_measure_u.argtypes = [_P, ctypes.c_int, ctypes.c_double, _ip, _dp]
 _lib.qsim_project.argtypes = [_P, ctypes.c_int, ctypes.c_int]
 _lib.qsim_prepare_shorbox.argtypes = [_P, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64]
+_lib.qsim_aux_amplitudes.argtypes = [ctypes.c_int, ctypes.POINTER(qsim_gate), ctypes.c_size_t,
+                                     ctypes.POINTER(ctypes.c_uint64), ctypes.c_size_t,
+                                     ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+_lib.qsim_aux_num_vars.argtypes = [ctypes.c_int, ctypes.POINTER(qsim_gate), ctypes.c_size_t,
+                                   ctypes.POINTER(ctypes.c_int)]
 _lib.qsim_sample.argtypes = [_P, ctypes.c_size_t, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
 _lib.qsim_get_amplitudes.argtypes = [_P, ctypes.POINTER(ctypes.c_uint64), ctypes.c_size_t, _dp]
 _lib.qsim_get_state.argtypes = [_P, _dp]
@@ -269,6 +275,29 @@ def qsim_measure_u(h, qubit, u):
 def qsim_project(h, qubit, value):
     """CLEAR (value=0) / SET (value=1): project and renormalise (PAPER.md:1474-1493)."""
     _check(_lib.qsim_project(h, qubit, value))
+
+
+def qsim_aux_num_vars(n_qubits, circuit) -> int:
+    """Number of auxiliary variables of the circuit (§4.2; host only)."""
+    arr, n = pack_gates(circuit)
+    P = ctypes.c_int()
+    _check(_lib.qsim_aux_num_vars(n_qubits, arr, n, ctypes.byref(P)))
+    return P.value
+
+
+def qsim_aux_amplitudes(n_qubits, circuit, idx, return_abs_sum=False):
+    """<y|psi> at logical indices idx by the auxiliary-variable method
+    (§4.2, Eq. appa7) on the current CUDA device; optionally also
+    2^-P sum_s |term_s| per amplitude."""
+    arr, n = pack_gates(circuit)
+    y = np.ascontiguousarray(np.asarray(idx, dtype=np.uint64))
+    out = np.empty(2 * len(y))
+    ab = np.empty(len(y))
+    _check(_lib.qsim_aux_amplitudes(n_qubits, arr, n, y.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), len(y),
+                                    out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                    ab.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+    z = out[0::2] + 1j * out[1::2]
+    return (z, ab) if return_abs_sum else z
 
 
 def qsim_prepare_shorbox(h, nx, G, y):

@@ -1526,6 +1526,21 @@ int qsim_sample(qsim_state *s, size_t nsamples, uint64_t seed, uint64_t *out) {
                           nsamples, seed, out, s->stream);
 }
 
+int qsim_aux_amplitudes(int n_qubits, const qsim_gate *gates, size_t ngates, const uint64_t *idx, size_t m,
+                        double *out, double *abs_sum) {
+    if ((ngates && !gates) || (m && (!idx || !out)) || n_qubits < 2 || n_qubits > 63) {
+        set_error("qsim_aux_amplitudes: bad arguments");
+        return QSIM_EINVAL;
+    }
+    RC(validate_gates(n_qubits, gates, ngates, true));
+    for (size_t k = 0; k < m; ++k)
+        if (idx[k] >> n_qubits) {
+            set_error("qsim_aux_amplitudes: index out of range");
+            return QSIM_EINVAL;
+        }
+    return aux_amplitudes(n_qubits, gates, ngates, idx, m, out, abs_sum, 40);
+}
+
 int qsim_prepare_shorbox(qsim_state *s, int nx, uint64_t G, uint64_t y) {
     if (!s || nx < 0 || nx >= s->n || G < 2 || y < 1 || y >= G) {
         set_error("qsim_prepare_shorbox: need 0 <= nx < N, G >= 2, 1 <= y < G");

@@ -42,6 +42,11 @@ struct Planner {
 
 int validate_gates(int n, const qsim_gate *gates, size_t ngates, bool check_unitary);
 
+// ---- auxiliary-variable evaluator (aux.cu) ----
+int aux_num_vars(int n, const qsim_gate *gates, size_t ngates, int *P);
+int aux_amplitudes(int n, const qsim_gate *gates, size_t ngates, const uint64_t *idx, size_t m, double *out,
+                   double *abs_sum, int max_vars);
+
 }  // namespace qsim
 
 struct qsim_plan {

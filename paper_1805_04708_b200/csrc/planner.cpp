@@ -242,4 +242,14 @@ int qsim_plan_final_map(const qsim_plan *p, int *pos) {
 }
 
 void qsim_plan_destroy(qsim_plan *p) { delete p; }
+
+int qsim_aux_num_vars(int n_qubits, const qsim_gate *gates, size_t ngates, int *P) {
+    if (!P || (ngates && !gates) || n_qubits < 2 || n_qubits > 63) {
+        qsim::set_error("qsim_aux_num_vars: bad arguments");
+        return QSIM_EINVAL;
+    }
+    int rc = qsim::validate_gates(n_qubits, gates, ngates, true);
+    if (rc) return rc;
+    return qsim::aux_num_vars(n_qubits, gates, ngates, P);
+}
 }

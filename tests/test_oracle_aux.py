@@ -102,3 +102,12 @@ def test_outside_the_method_is_rejected():
     c.add("CH", C.mat_H(), 1, [0])
     with pytest.raises(ValueError):
         aux_hs.amplitudes(2, c, [0])
+
+
+def test_library_counts_the_same_auxiliary_variables():
+    """Host-only C-ABI planner (no GPU): P of qsim_aux_num_vars = the oracle's."""
+    import paper_1805_04708_b200 as q
+
+    for seed in range(4):
+        c = _hs_circuit(9, 40, seed)
+        assert q.qsim_aux_num_vars(9, c) == aux_hs.num_aux(c)
