@@ -186,6 +186,57 @@ int qsim_sample(qsim_state *s, size_t nsamples, uint64_t seed, uint64_t *out);
  * EINVAL unless 0 <= nx < N, 2 <= G <= 2^(N-nx) and 1 <= y < G. */
 int qsim_prepare_shorbox(qsim_state *s, int nx, uint64_t G, uint64_t y);
 
+/* Set the logical -> physical qubit map (pos[q] = physical bit of logical
+ * qubit q, a permutation of 0..N-1): BIT ASSIGNMENT (App. B, PAPER.md:
+ * 1424-1449), a performance choice that leaves results unchanged when issued
+ * on |0...0> (right after qsim_create / qsim_reset); on another state it
+ * relabels the qubits.  EINVAL unless pos is a permutation. */
+int qsim_set_qubit_map(qsim_state *s, const int *pos);
+
+/* ---- the assembler-like instruction language (App. B) --
+ * qsim_asm_parse compiles a program text (host only, no GPU): one instruction
+ * per line, '!' starts a comment, mnemonics case-insensitive; QUBITS N first;
+ * BIT ASSIGNMENT and DEPOLARIZING CHANNEL before the first gate; gates I H X Y
+ * Z S S+ T T+ U1 U2 U3 +X -X +Y -Y R CNOT U TOFFOLI with the matrices of
+ * App. B; BEGIN MEASUREMENT, GENERATE EVENTS, M, SHORBOX, CLEAR, SET, EXIT.
+ * Errors: EINVAL with "line L: ..." in qsim_last_error().  qsim_asm_run
+ * executes it on a fresh state (encoding, ngpus as qsim_create): runs of gates
+ * go to qsim_apply_circuit; BEGIN MEASUREMENT appends the 3N expectations of
+ * qsim_expectations to the result; M n appends (n, outcome) drawn by
+ * qsim_measure with seed = seed + (measurement index); GENERATE EVENTS draws
+ * with qsim_sample (its own seed if > 0, else `seed`) and ends the run;
+ * EXIT measures qubits 0..N-1 and ends the run; the depolarising channel
+ * inserts X/Y/Z after every gate (reading R-B11).  The result object owns its
+ * arrays; qsim_asm_result_get copies min(cap, count) items into buf and
+ * returns the full count. */
+typedef struct qsim_asm qsim_asm;
+typedef struct qsim_asm_result qsim_asm_result;
+#define QSIM_ASM_GATE 0        /* `gate` holds the record */
+#define QSIM_ASM_MEASURE_ALL 1 /* BEGIN MEASUREMENT */
+#define QSIM_ASM_EVENTS 2      /* GENERATE EVENTS args[0] = events, args[1] = seed */
+#define QSIM_ASM_M 3           /* M args[0] */
+#define QSIM_ASM_SHORBOX 4     /* args = nx, G, y */
+#define QSIM_ASM_CLEAR 5       /* args[0] = qubit */
+#define QSIM_ASM_SET 6         /* args[0] = qubit */
+#define QSIM_ASM_EXIT 7
+typedef struct qsim_asm_op {
+    int32_t type;    /* QSIM_ASM_* */
+    int32_t line;    /* source line */
+    int64_t args[3];
+    qsim_gate gate;  /* QSIM_ASM_GATE */
+} qsim_asm_op;
+#define QSIM_ASM_R_TABLES 0   /* double: 3N per BEGIN MEASUREMENT (<Qx>,<Qy>,<Qz> per qubit) */
+#define QSIM_ASM_R_OUTCOMES 1 /* int32 pairs (qubit, outcome) per measured qubit */
+#define QSIM_ASM_R_EVENTS 2   /* uint64 logical basis indices */
+int qsim_asm_parse(const char *text, qsim_asm **out);
+int qsim_asm_info(const qsim_asm *a, int *n_qubits, int64_t *nops, int *perm /* N, nullable */,
+                  double *depol /* 4: p_x, p_y, p_z, seed; nullable */);
+int qsim_asm_get_op(const qsim_asm *a, int64_t i, qsim_asm_op *op);
+void qsim_asm_destroy(qsim_asm *a);
+int qsim_asm_run(const qsim_asm *a, int encoding, int ngpus, uint64_t seed, qsim_asm_result **out);
+int qsim_asm_result_get(const qsim_asm_result *r, int what, void *buf, int64_t cap, int64_t *count);
+void qsim_asm_result_destroy(qsim_asm_result *r);
+
 /* ---- auxiliary-variable method (§4.2) -------------
  * Stateless: no qsim_state, no 2^N vector.  out[2k], out[2k+1] = <y_k|psi>
  * (re, im) for the LOGICAL indices y_k = idx[k] (< 2^N), psi = the gate list

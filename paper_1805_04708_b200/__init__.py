@@ -87,7 +87,9 @@ EXPORTS = (
     "qsim_get_amplitudes", "qsim_get_state", "qsim_set_state", "qsim_get_codes", "qsim_set_codes", "qsim_sync",
     "qsim_project", "qsim_sample", "qsim_prepare_shorbox", "qsim_stream", "qsim_get_stats", "qsim_reset", "qsim_profile", "qsim_profile_read", "qsim_reset_stats", "qsim_get_qubit_map", "qsim_last_error",
     "qsim_plan_create", "qsim_plan_num_ops", "qsim_plan_get_op", "qsim_plan_final_map", "qsim_plan_destroy",
-    "qsim_aux_amplitudes", "qsim_aux_num_vars",
+    "qsim_aux_amplitudes", "qsim_aux_num_vars", "qsim_set_qubit_map",
+    "qsim_asm_parse", "qsim_asm_info", "qsim_asm_get_op", "qsim_asm_destroy", "qsim_asm_run",
+    "qsim_asm_result_get", "qsim_asm_result_destroy",
 )
 
 if not os.path.exists(_LIB_PATH):
@@ -117,6 +119,19 @@ _lib.qsim_prepare_shorbox.argtypes = [_P, ctypes.c_int, ctypes.c_uint64, ctypes.
 _lib.qsim_aux_amplitudes.argtypes = [ctypes.c_int, ctypes.POINTER(qsim_gate), ctypes.c_size_t,
                                      ctypes.POINTER(ctypes.c_uint64), ctypes.c_size_t,
                                      ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+_lib.qsim_set_qubit_map.argtypes = [_P, ctypes.POINTER(ctypes.c_int)]
+_lib.qsim_asm_parse.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
+_lib.qsim_asm_info.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int64),
+                               ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)]
+_lib.qsim_asm_get_op.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+_lib.qsim_asm_destroy.argtypes = [ctypes.c_void_p]
+_lib.qsim_asm_destroy.restype = None
+_lib.qsim_asm_run.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_uint64,
+                              ctypes.POINTER(ctypes.c_void_p)]
+_lib.qsim_asm_result_get.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64,
+                                     ctypes.POINTER(ctypes.c_int64)]
+_lib.qsim_asm_result_destroy.argtypes = [ctypes.c_void_p]
+_lib.qsim_asm_result_destroy.restype = None
 _lib.qsim_aux_num_vars.argtypes = [ctypes.c_int, ctypes.POINTER(qsim_gate), ctypes.c_size_t,
                                    ctypes.POINTER(ctypes.c_int)]
 _lib.qsim_sample.argtypes = [_P, ctypes.c_size_t, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
@@ -298,6 +313,66 @@ def qsim_aux_amplitudes(n_qubits, circuit, idx, return_abs_sum=False):
                                     ab.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
     z = out[0::2] + 1j * out[1::2]
     return (z, ab) if return_abs_sum else z
+
+
+ASM_GATE, ASM_MEASURE_ALL, ASM_EVENTS, ASM_M, ASM_SHORBOX, ASM_CLEAR, ASM_SET, ASM_EXIT = range(8)
+
+
+class qsim_asm_op(ctypes.Structure):
+    _fields_ = [("type", ctypes.c_int32), ("line", ctypes.c_int32), ("args", ctypes.c_int64 * 3),
+                ("gate", qsim_gate)]
+
+
+def asm_parse(text: str) -> dict:
+    """Compile an App. B program (host only): N, the BIT
+    ASSIGNMENT map, the depolarising-channel parameters and the op list."""
+    h = ctypes.c_void_p()
+    _check(_lib.qsim_asm_parse(text.encode(), ctypes.byref(h)))
+    try:
+        n, nops = ctypes.c_int(), ctypes.c_int64()
+        _check(_lib.qsim_asm_info(h, ctypes.byref(n), ctypes.byref(nops), None, None))
+        perm = (ctypes.c_int * n.value)()
+        dep = (ctypes.c_double * 4)()
+        _check(_lib.qsim_asm_info(h, None, None, perm, dep))
+        ops = []
+        op = qsim_asm_op()
+        for i in range(nops.value):
+            _check(_lib.qsim_asm_get_op(h, i, ctypes.byref(op)))
+            g = op.gate
+            ops.append(dict(type=op.type, line=op.line, args=list(op.args), target=g.target,
+                            controls=[g.controls[k] for k in range(g.ncontrols)],
+                            u=np.array(list(g.u)).view(np.complex128).reshape(2, 2)))
+        return dict(n=n.value, perm=list(perm), depol=list(dep), ops=ops)
+    finally:
+        _lib.qsim_asm_destroy(h)
+
+
+def asm_run(text: str, encoding=ENC_FP64, ngpus=1, seed=0) -> dict:
+    """Run an App. B program on a fresh state: BEGIN MEASUREMENT tables
+    (K x N x 3: <Qx>, <Qy>, <Qz>), M outcomes [(qubit, outcome)], events."""
+    h = ctypes.c_void_p()
+    _check(_lib.qsim_asm_parse(text.encode(), ctypes.byref(h)))
+    r = ctypes.c_void_p()
+    try:
+        n = ctypes.c_int()
+        _check(_lib.qsim_asm_info(h, ctypes.byref(n), None, None, None))
+        _check(_lib.qsim_asm_run(h, encoding, ngpus, seed, ctypes.byref(r)))
+    finally:
+        _lib.qsim_asm_destroy(h)
+    try:
+        out = {}
+        for what, dt, key in ((0, np.float64, "tables"), (1, np.int32, "outcomes"), (2, np.uint64, "events")):
+            cnt = ctypes.c_int64()
+            _check(_lib.qsim_asm_result_get(r, what, None, 0, ctypes.byref(cnt)))
+            buf = np.empty(cnt.value, dtype=dt)
+            _check(_lib.qsim_asm_result_get(r, what, buf.ctypes.data_as(ctypes.c_void_p), cnt.value,
+                                            ctypes.byref(cnt)))
+            out[key] = buf
+        out["tables"] = out["tables"].reshape(-1, n.value, 3)
+        out["outcomes"] = [tuple(x) for x in out["outcomes"].reshape(-1, 2).tolist()]
+        return out
+    finally:
+        _lib.qsim_asm_result_destroy(r)
 
 
 def qsim_prepare_shorbox(h, nx, G, y):

@@ -971,10 +971,13 @@ static int execute(qsim_state *s, const qsim_gate *gates, size_t ngates, const s
 static int phys_probs(qsim_state *s, std::vector<double> &phys) {
     phys.assign(1 + s->n, 0.0);
     for (auto &sh : s->shards) {
+        // the reduction walks 256-amplitude segments: shards below 2^8 amplitudes
+        // are zero-padded to 256 (alloc_amps), so reduce over the padded size
+        const int nr = std::max(s->nl, 8);
         if (s->enc == QSIM_ENC_FP64)
-            launch_probs_e(sh.amps, s->nl, s->d_partials, s->d_out, s->stream);
+            launch_probs_e(sh.amps, nr, s->d_partials, s->d_out, s->stream);
         else
-            launch_probs_a(sh.amps, s->nl, s->atab, s->d_partials, s->d_out, s->stream);
+            launch_probs_a(sh.amps, nr, s->atab, s->d_partials, s->d_out, s->stream);
         s->st.kernels += 2;
         CU(cudaMemcpyAsync(s->h_out, s->d_out, RED_SLOTS * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
         CU(cudaStreamSynchronize(s->stream));
@@ -1524,6 +1527,23 @@ int qsim_sample(qsim_state *s, size_t nsamples, uint64_t seed, uint64_t *out) {
     s->st.kernels += 4;
     return sample_logical(amps.data(), bases.data(), (int)amps.size(), s->nl, s->n, s->pl.inv.data(), s->enc, s->atab,
                           nsamples, seed, out, s->stream);
+}
+
+int qsim_set_qubit_map(qsim_state *s, const int *pos) {
+    if (!s || !pos) return QSIM_EINVAL;
+    std::vector<int> seen(s->n, 0);
+    for (int q = 0; q < s->n; ++q) {
+        if (pos[q] < 0 || pos[q] >= s->n || seen[pos[q]]) {
+            set_error("qsim_set_qubit_map: not a permutation of 0..N-1");
+            return QSIM_EINVAL;
+        }
+        seen[pos[q]] = 1;
+    }
+    for (int q = 0; q < s->n; ++q) {
+        s->pl.pos[q] = pos[q];
+        s->pl.inv[pos[q]] = q;
+    }
+    return QSIM_OK;
 }
 
 int qsim_aux_amplitudes(int n_qubits, const qsim_gate *gates, size_t ngates, const uint64_t *idx, size_t m,

@@ -460,3 +460,18 @@ def test_table5_shor_n30_exact_columns():
     # between the printed exact and A columns (reading R-B6) -- bounded by the
     # paper's own A-vs-exact level 0.011
     assert np.max(np.abs(e[:, :2] - t[:, 4:6])) <= 0.011
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [2, 3, 5, 7])
+def test_small_states_below_256_amplitudes(n):
+    """N < 8: shards are zero-padded to 256 amplitudes; every read-out still
+    covers exactly the 2^N logical amplitudes."""
+    circ = C.config(0, n=n, seed=n, layers=None) if n >= 3 else C.h_wall(n)
+    ref = oracle.e_simulate(n, circ)
+    with q.State(n) as s:
+        s.apply_circuit(circ)
+        assert np.max(np.abs(s.get_state() - ref)) <= TOL
+        assert abs(s.norm() - 1.0) <= 1e-10
+        assert np.max(np.abs(s.probabilities() - oracle.e_probabilities(ref, n))) <= TOL
+        assert np.max(np.abs(s.expectations() - oracle.e_expectations(ref, n))) <= TOL
