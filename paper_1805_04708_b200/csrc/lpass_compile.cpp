@@ -181,6 +181,9 @@ struct Compiler {
 
     int run();
     int compile_stage(const std::vector<int> &take, const int *Q);
+    // stage register sets: greedy lookahead (LPASS_LOOKAHEAD=1) with a score
+    // penalty per in-stage flip (LPASS_FLIP_PENALTY), or first-come (0, default)
+    int lookahead = 0, flip_penalty = 2;
 };
 
 // Build the register-stage prims of one gate.  `slot_of` maps tile bit -> slot.
@@ -792,104 +795,196 @@ int Compiler::run() {
         if (rem.empty()) break;
         if ((int)stages.size() >= LP_MAX_STAGES) return 1;
         // (2) one register stage: every remaining gate that commutes with the
-        // skipped ones and whose non-diagonal target fits the R register slots
-        int Q[5];
-        int nq = 0;
-        int slot_of[LP_MAX_K];
-        for (int i = 0; i < LP_MAX_K; ++i) slot_of[i] = -1;
-        uint8_t ainv[5];
-        for (int r = 0; r < R; ++r) ainv[r] = (uint8_t)(1u << r);
-        int nev_avail = LP_MAX_EVENTS - (int)ts.ev_v.size();
-        uint32_t used_out = 0;  // tile bits the stage tests outside the registers (conditions)
-        std::vector<int> take, left;
-        std::vector<Prim> tmp;
-        uint64_t bx = 0, bz = 0;
-        bool carried_any = false;
-        for (int k : rem) {
-            const GInfo &g = G[k];
-            bool ok = !((g.xq & (bx | bz)) || (g.zq & bx));
-            // an uncontrolled 1-qubit diagonal on a qubit outside the registers
-            // commutes with the whole stage: carry it (or defer it out of the
-            // pass when its qubit is not in the tile) -- no op, no table
-            if (ok && allow_carry && g.cls == GC_DIAG && g.nci == 0 && g.om == 0 &&
-                (g.tt < 0 || slot_of[g.tt] < 0)) {
-                const cd d0(g.u[0], g.u[1]), d1(g.u[6], g.u[7]);
-                if (g.tt >= 0) {
-                    if (!has_carry[g.tt]) {
-                        carry[g.tt][0] = carry[g.tt][1] = cd(1.0, 0.0);
-                        has_carry[g.tt] = true;
+        // skipped ones and whose non-diagonal target fits the R register slots.
+        // scan(): the selection for a given initial register set; with grow,
+        // gates may claim free slots first-come; dry runs change no state.
+        struct Scan {
+            int Q[5];
+            int nq = 0;
+            int slot_of[LP_MAX_K];
+            uint32_t used_out = 0;
+            std::vector<int> take, left;
+            bool carried_any = false;
+            int score = 0;
+        };
+        auto scan = [&](const int *Qi, int nqi, bool grow, bool dry, Scan &S) {
+            int *Q = S.Q;
+            int &nq = S.nq;
+            int *slot_of = S.slot_of;
+            uint32_t &used_out = S.used_out;
+            std::vector<int> &take = S.take, &left = S.left;
+            bool &carried_any = S.carried_any;
+            nq = 0;
+            for (int i = 0; i < LP_MAX_K; ++i) slot_of[i] = -1;
+            for (int i = 0; i < nqi; ++i) {
+                Q[nq] = Qi[i];
+                slot_of[Qi[i]] = nq++;
+            }
+            uint8_t ainv[5];
+            for (int r = 0; r < R; ++r) ainv[r] = (uint8_t)(1u << r);
+            int nev_avail = LP_MAX_EVENTS - (int)ts.ev_v.size();
+            used_out = 0;  // tile bits the stage tests outside the registers (conditions)
+            std::vector<Prim> tmp;
+            uint64_t bx = 0, bz = 0;
+            for (int k : rem) {
+                const GInfo &g = G[k];
+                bool ok = !((g.xq & (bx | bz)) || (g.zq & bx));
+                // an uncontrolled 1-qubit diagonal on a qubit outside the registers
+                // commutes with the whole stage: carry it (or defer it out of the
+                // pass when its qubit is not in the tile) -- no op, no table
+                if (ok && allow_carry && g.cls == GC_DIAG && g.nci == 0 && g.om == 0 &&
+                    (g.tt < 0 || slot_of[g.tt] < 0)) {
+                    carried_any = true;
+                    if (dry) continue;
+                    const cd d0(g.u[0], g.u[1]), d1(g.u[6], g.u[7]);
+                    if (g.tt >= 0) {
+                        if (!has_carry[g.tt]) {
+                            carry[g.tt][0] = carry[g.tt][1] = cd(1.0, 0.0);
+                            has_carry[g.tt] = true;
+                        }
+                        carry[g.tt][0] *= d0;
+                        carry[g.tt][1] *= d1;
+                    } else {
+                        LGate x{};
+                        x.t = gates[k].t;
+                        std::memcpy(x.u, g.u, sizeof(x.u));
+                        out_deferred.push_back(x);
                     }
-                    carry[g.tt][0] *= d0;
-                    carry[g.tt][1] *= d1;
-                } else {
-                    LGate x{};
-                    x.t = gates[k].t;
-                    std::memcpy(x.u, g.u, sizeof(x.u));
-                    out_deferred.push_back(x);
+                    st.carried++;
+                    carried_any = true;
+                    continue;
                 }
-                st.carried++;
-                carried_any = true;
-                continue;
-            }
-            int added = -1;
-            // a diagonal gate takes a free register slot for its (tile) target:
-            // then it merges into the stage's table instead of needing its own
-            if (ok && g.cls == GC_DIAG && g.tt >= 0 && slot_of[g.tt] < 0 && nq < R && !((used_out >> g.tt) & 1)) {
-                Q[nq] = g.tt;
-                slot_of[g.tt] = nq;
-                added = nq++;
-            }
-            if (ok && (g.cls == GC_ANTI || g.cls == GC_DENSE) && slot_of[g.tt] < 0) {
-                // a new register qubit: not for a free permutation (done at tile
-                // level), not a bit already tested outside the registers, room left
-                if ((is_free(g) && !take.empty()) || nq >= R || ((used_out >> g.tt) & 1))
-                    ok = false;
-                else {
+                int added = -1;
+                // a diagonal gate takes a free register slot for its (tile) target:
+                // then it merges into the stage's table instead of needing its own
+                if (ok && grow && g.cls == GC_DIAG && g.tt >= 0 && slot_of[g.tt] < 0 && nq < R &&
+                    !((used_out >> g.tt) & 1)) {
                     Q[nq] = g.tt;
                     slot_of[g.tt] = nq;
                     added = nq++;
                 }
-            }
-            uint32_t uo = used_out;
-            if (ok) {
-                for (int c = 0; c < g.nci; ++c)
-                    if (slot_of[g.ci[c]] < 0) uo |= 1u << g.ci[c];
-                if (g.cls == GC_DIAG && g.tt >= 0 && slot_of[g.tt] < 0) uo |= 1u << g.tt;
-                if (__builtin_popcount(uo) + R > K) ok = false;  // padding must find untested bits
-            }
-            int nev2 = nev_avail;
-            uint8_t ainv2[5];
-            std::memcpy(ainv2, ainv, sizeof(ainv2));
-            if (ok) {
-                // the prims this gate becomes: every register pair vector must have weight <= 2
-                tmp.clear();
-                PrimBuilder pb{R, NS, slot_of, nev_avail, &tmp};
-                pb.gate(g);
-                nev2 = pb.nev_avail;
-                for (const Prim &p : tmp) {
-                    // shears take pair vectors of weight <= 2; the rare controlled
-                    // ops (general 2x2, controlled shear / swap) weight 1
-                    const bool w1 = p.kind == PK_DENSE || p.kind == PK_CSWAP || (p.kind == PK_SHEAR && p.cs);
-                    if (p.kind == PK_SHEAR && vidx[ainv2[p.S]] < 0) ok = false;
-                    if (w1 && __builtin_popcount(ainv2[p.S]) != 1) ok = false;
-                    if (p.kind == PK_RELABEL) ainv2[p.rc] ^= ainv2[p.S];
+                if (ok && (g.cls == GC_ANTI || g.cls == GC_DENSE) && slot_of[g.tt] < 0) {
+                    // a new register qubit: not for a free permutation (done at tile
+                    // level), not a bit already tested outside the registers, room left
+                    if (!grow || (is_free(g) && !take.empty()) || nq >= R || ((used_out >> g.tt) & 1))
+                        ok = false;
+                    else {
+                        Q[nq] = g.tt;
+                        slot_of[g.tt] = nq;
+                        added = nq++;
+                    }
+                }
+                uint32_t uo = used_out;
+                if (ok) {
+                    for (int c = 0; c < g.nci; ++c)
+                        if (slot_of[g.ci[c]] < 0) uo |= 1u << g.ci[c];
+                    if (g.cls == GC_DIAG && g.tt >= 0 && slot_of[g.tt] < 0) uo |= 1u << g.tt;
+                    if (__builtin_popcount(uo) + R > K) ok = false;  // padding must find untested bits
+                }
+                int nev2 = nev_avail;
+                uint8_t ainv2[5];
+                std::memcpy(ainv2, ainv, sizeof(ainv2));
+                if (ok) {
+                    // the prims this gate becomes: every register pair vector must have weight <= 2
+                    tmp.clear();
+                    PrimBuilder pb{R, NS, slot_of, nev_avail, &tmp};
+                    pb.gate(g);
+                    nev2 = pb.nev_avail;
+                    for (const Prim &p : tmp) {
+                        // shears take pair vectors of weight <= 2; the rare controlled
+                        // ops (general 2x2, controlled shear / swap) weight 1
+                        const bool w1 = p.kind == PK_DENSE || p.kind == PK_CSWAP || (p.kind == PK_SHEAR && p.cs);
+                        if (p.kind == PK_SHEAR && vidx[ainv2[p.S]] < 0) ok = false;
+                        if (w1 && __builtin_popcount(ainv2[p.S]) != 1) ok = false;
+                        if (p.kind == PK_RELABEL) ainv2[p.rc] ^= ainv2[p.S];
+                    }
+                }
+                if (ok) {
+                    take.push_back(k);
+                    S.score += g.cls == GC_DENSE ? 4 : (g.cls == GC_ANTI ? 1 : 0);
+                    if (g.cls == GC_ANTI && g.tt >= 0 && slot_of[g.tt] >= 0) {  // an in-stage flip costs an op
+                        bool inq = false;
+                        for (int c = 0; c < g.nci; ++c) inq = inq || slot_of[g.ci[c]] >= 0;
+                        if (!inq && (g.nci > 0 || g.om)) S.score -= flip_penalty;
+                    }
+                    used_out = uo;
+                    nev_avail = nev2;
+                    std::memcpy(ainv, ainv2, sizeof(ainv));
+                } else {
+                    if (added >= 0) {
+                        slot_of[Q[added]] = -1;
+                        --nq;
+                    }
+                    bx |= g.xq;
+                    bz |= g.zq;
+                    left.push_back(k);
                 }
             }
-            if (ok) {
-                take.push_back(k);
-                used_out = uo;
-                nev_avail = nev2;
-                std::memcpy(ainv, ainv2, sizeof(ainv));
-            } else {
-                if (added >= 0) {
-                    slot_of[Q[added]] = -1;
-                    --nq;
+        };
+        // register set by greedy lookahead: add the tile qubit that lets the
+        // stage take the most gates (dense gates weigh most: they share tables)
+        int Qsel[5];
+        int nsel = 0;
+        if (lookahead) {
+            Scan base;
+            scan(Qsel, 0, false, true, base);
+            int best_score = base.score;
+            uint32_t cand = 0;
+            for (int k : rem)
+                if ((G[k].cls == GC_DENSE || G[k].cls == GC_ANTI) && G[k].tt >= 0) cand |= 1u << G[k].tt;
+            while (nsel < R) {
+                int best = -1;
+                for (int c = 0; c < K; ++c) {
+                    if (!((cand >> c) & 1)) continue;
+                    bool in = false;
+                    for (int i = 0; i < nsel; ++i) in = in || Qsel[i] == c;
+                    if (in) continue;
+                    Qsel[nsel] = c;
+                    Scan tr;
+                    scan(Qsel, nsel + 1, false, true, tr);
+                    if (tr.score > best_score) {
+                        best_score = tr.score;
+                        best = c;
+                    }
                 }
-                bx |= g.xq;
-                bz |= g.zq;
-                left.push_back(k);
+                if (best < 0) break;
+                Qsel[nsel++] = best;
             }
         }
+        Scan S;
+        scan(Qsel, nsel, true, false, S);
+        {
+            // a permutation gate the tile level can apply for free (is_free) that
+            // no later gate of the stage depends on goes back to the remaining
+            // gates: it is then a relabelling after the stage, not an in-stage
+            // flip (one op per group, and divergent flip vectors)
+            std::vector<int> keep, back;
+            uint64_t lx = 0, lz = 0;  // qubits used by the later kept gates
+            for (int i = (int)S.take.size() - 1; i >= 0; --i) {
+                const int k = S.take[i];
+                const GInfo &g = G[k];
+                const bool later_dep = (g.xq & (lx | lz)) || (g.zq & lx);
+                if (g.pure && is_free(g) && !later_dep && !(g.nci == 1 && S.slot_of[g.ci[0]] >= 0)) {
+                    back.push_back(k);
+                    continue;
+                }
+                keep.push_back(k);
+                lx |= g.xq;
+                lz |= g.zq;
+            }
+            if (!back.empty()) {
+                std::reverse(keep.begin(), keep.end());
+                S.take.swap(keep);
+                S.left.insert(S.left.end(), back.begin(), back.end());
+                std::sort(S.left.begin(), S.left.end());
+            }
+        }
+        int *Q = S.Q;
+        int &nq = S.nq;
+        int *slot_of = S.slot_of;
+        const uint32_t used_out = S.used_out;
+        std::vector<int> &take = S.take, &left = S.left;
+        const bool carried_any = S.carried_any;
         if (take.empty()) {
             if (carried_any) {
                 rem.swap(left);
@@ -947,6 +1042,8 @@ int lpass_compile(const LGate *gates, int ng, int nl, int K, int R, const int *t
     c.R = R;
     c.max_coef = max_coef;
     c.allow_carry = deferred != nullptr;
+    if (const char *e = getenv("LPASS_LOOKAHEAD")) c.lookahead = atoi(e);
+    if (const char *e = getenv("LPASS_FLIP_PENALTY")) c.flip_penalty = atoi(e);
     for (int q = 0; q < 64; ++q) c.tbit_of[q] = -1;
     for (int i = 0; i < K; ++i) c.tbit_of[tile_q[i]] = i;
     c.G.resize(ng);
