@@ -213,6 +213,18 @@ __device__ __forceinline__ uint32_t lp_toff(uint64_t h, const LOp &o, uint32_t x
     return toff;
 }
 
+// flips folded into a table op (compiler): g ^= gvec where the condition bit is 1
+__device__ __forceinline__ void lp_preflip(uint32_t &g, const LOp &o, uint32_t xq, uint64_t full) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const uint32_t f = o.pmc[k];
+        if (!(f >> 16)) break;
+        const uint32_t c = (f >> 8) & 255u;
+        const uint32_t bit = c == 255u ? 1u : c < 64u ? (xq >> c) & 1u : (uint32_t)(full >> (c - 64u)) & 1u;
+        g ^= bit ? (f & 255u) : 0u;
+    }
+}
+
 // One op of the stage program on one register group (v, g: its register
 // values and flip vector; xq: its logical tile bits outside the registers).
 template <int R>
@@ -225,6 +237,7 @@ __device__ __forceinline__ void lp_op1(double2 (&v)[1 << R], uint32_t &g, uint32
     if ((h >> 8) & LF_COND) {
         if (((xq & o.tmask) != o.tval) || ((full & o.omask) != o.oval)) return;
     }
+    if (code == LOP_CODE_ROUND || code == LOP_CODE_DIAGT) lp_preflip(g, o, xq, full);
     const uint32_t toff = lp_toff<R>(h, o, xq, full, cpool_off);
     if (code == LOP_CODE_ROUND) {
         lp_table<NS>(v, smem_raw, toff | (g << 4));
@@ -453,6 +466,8 @@ __global__ void __launch_bounds__(LP_THREADS, MINB) k_lpass_e(const __grid_const
                         gg[1] ^= (uint32_t)(h >> 24) & 0xffu;
                         continue;
                     }
+                    lp_preflip(gg[0], o, xq[0], full);
+                    lp_preflip(gg[1], o, xq[1], full);
                     lp_table2<NS>(v[0], v[1], smem_raw, lp_toff<R>(h, o, xq[0], full, cpool_off) | (gg[0] << 4),
                                   lp_toff<R>(h, o, xq[1], full, cpool_off) | (gg[1] << 4));
                     if (code == LOP_CODE_DIAGT) continue;

@@ -104,6 +104,9 @@ struct LOp {
     uint8_t pad0;
     uint32_t pm;       // bit j = par(rowS & j) (SHEARU: bit 0 = the uniform parity; ROUND: offset in sc[])
     uint32_t pmc[2];   // the same for each in-register control row
+                       // DIAGT / ROUND: up to 2 pre-flips applied before the op:
+                       // bit 16 valid, bits 8-15 condition code (tile bit b -> b,
+                       // full-index bit b -> 64 + b, 255 = always), bits 0-7 gvec
     uint8_t rowc[2];
     uint16_t pad1;
     uint16_t tmask, tval;  // condition on the group's logical tile bits outside the registers

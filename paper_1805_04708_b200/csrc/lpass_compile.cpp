@@ -747,6 +747,57 @@ int Compiler::compile_stage(const std::vector<int> &take, const int *Q) {
         if (!carried && flush_P()) return 1;
     }
     if ((int)ops.size() > LP_MAX_OPS) return 1;
+    // fold FLIP ops into the table op that follows them (<= 2 per op): a flip
+    // only updates the group's vector g, so applying it right before the next
+    // op is the same program with one dispatch less
+    {
+        std::vector<LOp> merged;
+        std::vector<LOp> pend;
+        for (int i = sr.op0; i < (int)ops.size(); ++i) {
+            const LOp &o = ops[i];
+            int code = -1;
+            if (o.code == LOP_CODE_FLIP) {
+                if (!(o.flags & LF_COND))
+                    code = 255;
+                else if (o.tmask && !o.omask && __builtin_popcount(o.tmask) == 1 && o.tval == o.tmask)
+                    code = __builtin_ctz(o.tmask);
+                else if (!o.tmask && o.omask && __builtin_popcountll(o.omask) == 1 && o.oval == o.omask)
+                    code = 64 + __builtin_ctzll(o.omask);
+            }
+            if (code >= 0 && pend.size() < 2) {
+                LOp f = o;
+                f.pm = (uint32_t)code;  // stash
+                pend.push_back(f);
+                continue;
+            }
+            const bool table = (o.code == LOP_CODE_DIAGT || o.code == LOP_CODE_ROUND) && !(o.flags & LF_COND);
+            if (table && !pend.empty()) {
+                LOp t = o;
+                for (size_t k = 0; k < pend.size(); ++k)
+                    t.pmc[k] = (1u << 16) | (pend[k].pm << 8) | pend[k].gvec;
+                merged.push_back(t);
+                pend.clear();
+                continue;
+            }
+            for (const LOp &f : pend) {  // no table op next: keep them as ops
+                LOp x = f;
+                x.pm = 0;
+                merged.push_back(x);
+            }
+            pend.clear();
+            if (code >= 0) {  // a third flip in a row
+                LOp f = o;
+                f.pm = (uint32_t)code;
+                pend.push_back(f);
+                continue;
+            }
+            merged.push_back(o);
+        }
+        // flips after the stage's last table op: g is not read again -- the
+        // tile-level relabelling (replay below) carries their effect
+        ops.resize(sr.op0);
+        ops.insert(ops.end(), merged.begin(), merged.end());
+    }
     sr.nops = (int)ops.size() - sr.op0;
     stages.push_back(sr);
     // tile-level effect of the stage's relabels and flips

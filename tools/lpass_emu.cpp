@@ -90,6 +90,15 @@ static void emu_pass(const LPassParams &p, cd *a) {
                 for (int oi = st.first_op; oi < st.first_op + st.nops; ++oi) {
                     const LOp &o = p.op[oi];
                     if ((o.flags & LF_COND) && (((xq & o.tmask) != o.tval) || ((full & o.omask) != o.oval))) continue;
+                    if (o.code == LOP_CODE_ROUND || o.code == LOP_CODE_DIAGT)
+                        for (int k = 0; k < 2; ++k) {  // pre-flips folded into the table op
+                            const uint32_t f = o.pmc[k];
+                            if (!(f >> 16)) continue;
+                            const uint32_t c = (f >> 8) & 255u;
+                            const uint32_t bit =
+                                c == 255 ? 1u : c < 64 ? (xq >> c) & 1u : (uint32_t)((full >> (c - 64)) & 1u);
+                            if (bit) g ^= f & 255u;
+                        }
                     uint32_t toff = o.coef;  // table variant selected by the group's condition bits
                     if (o.code == LOP_CODE_ROUND || o.code == LOP_CODE_DIAGT)
                         for (int i = 0; i < o.nctl; ++i) {
@@ -331,7 +340,65 @@ static int run_circuits(int ncases, uint64_t seed) {
     return 0;
 }
 
+// compile-only statistics of a gate file (t nctl c0 c1 u0..u7 per line) at nl
+// local qubits: the program the runtime would launch, without a state
+struct StatSink : LPassSink {
+    long passes = 0, sweeps = 0, stages = 0, ops = 0, tables = 0, shears = 0, flips = 0, relabels = 0,
+         tile_free = 0, events = 0;
+    int nl = 30;
+    int pass(const LPassParams &, const LCompileStats &cs, const std::vector<int> &) override {
+        ++passes;
+        stages += cs.stages;
+        ops += cs.ops;
+        tables += cs.diagt;
+        shears += cs.shears;
+        flips += cs.flips;
+        relabels += cs.relabels;
+        tile_free += cs.tile_free;
+        events += cs.events;
+        return 0;
+    }
+    int sweep(const LGate &, int) override {
+        ++sweeps;
+        return 0;
+    }
+    double gate_bytes(const LGate &g) override {
+        const bool diag = g.u[2] == 0 && g.u[3] == 0 && g.u[4] == 0 && g.u[5] == 0;
+        return std::ldexp(32.0, nl - g.nctl) * (diag ? 0.5 : 1.0);
+    }
+};
+
+static int stats_file(const char *path, int nl, int R) {
+    FILE *f = fopen(path, "r");
+    if (!f) return 2;
+    std::vector<LGate> gs;
+    LGate g{};
+    while (fscanf(f, "%d %d %d %d %lf %lf %lf %lf %lf %lf %lf %lf", &g.t, &g.nctl, &g.ctl[0], &g.ctl[1], &g.u[0],
+                  &g.u[1], &g.u[2], &g.u[3], &g.u[4], &g.u[5], &g.u[6], &g.u[7]) == 12)
+        gs.push_back(g);
+    fclose(f);
+    StatSink sink;
+    sink.nl = nl;
+    LRunConfig cfg;
+    cfg.nl = nl;
+    cfg.K = std::min(LP_MAX_K, nl);
+    cfg.R = R;
+    cfg.max_coef = R == 4 ? 960 : LP_MAX_COEF;
+    cfg.pass_bytes = std::ldexp(32.0, nl);
+    std::string err;
+    if (lpass_run(gs.data(), (int)gs.size(), cfg, sink, &err)) {
+        printf("error %s\n", err.c_str());
+        return 1;
+    }
+    printf("gates=%zu passes=%ld sweeps=%ld stages=%ld ops=%ld tables=%ld shears=%ld flips=%ld relabels=%ld "
+           "tile_free=%ld events=%ld\n",
+           gs.size(), sink.passes, sink.sweeps, sink.stages, sink.ops, sink.tables, sink.shears, sink.flips,
+           sink.relabels, sink.tile_free, sink.events);
+    return 0;
+}
+
 int main(int argc, char **argv) {
+    if (argc > 3 && std::string(argv[1]) == "stats") return stats_file(argv[2], atoi(argv[3]), argc > 4 ? atoi(argv[4]) : 4);
     const int ncases = argc > 1 ? atoi(argv[1]) : 300;
     const uint64_t seed = argc > 2 ? strtoull(argv[2], nullptr, 10) : 1;
     if (argc > 3 && std::string(argv[3]) == "run") return run_circuits(ncases, seed);
