@@ -152,6 +152,15 @@ int qsim_apply_circuit(qsim_state *s, const qsim_gate *gates, size_t ngates);
 /* Sum_i |a_i|^2 (Eq. STAT1), decoded amplitudes for A. */
 int qsim_norm(qsim_state *s, double *norm2);
 
+/* out[0] + i out[1] = <a|b> = sum_x conj(a_x) b_x over the logical basis
+ * (decoded amplitudes for an A side), e.g. the fidelity |<A|E>|^2 / (<A|A><E|E>)
+ * of an A run against an E run of the same circuit (SURVEY.md §8(d) config 4,
+ * BASELINE north_star "fidelity against fp64 reported").  Both handles must
+ * live in this process on the same device with the same N and shard count,
+ * the loopback transport, and the same qubit map and shard labels (as two
+ * runs of one circuit have): QSIM_EUNSUPPORTED otherwise.  Synchronous. */
+int qsim_overlap(qsim_state *a, qsim_state *b, double *out);
+
 /* p1[n] = P(qubit n = 1) = sum over |a(..1_n..)|^2, n = 0..N-1,
  * not renormalised.  p1 has N entries. */
 int qsim_probabilities(qsim_state *s, double *p1);
@@ -311,6 +320,31 @@ int qsim_profile_read(qsim_state *s, qsim_kernel_profile *out, int max, int *nou
 
 /* Wait for all work of this handle. */
 int qsim_sync(qsim_state *s);
+
+/* ---- CUDA graphs of a gate sequence (the
+ * latency-bound N=14 circuit with "per-gate launch, a CUDA Graph, and a
+ * single persistent kernel") ----------------------------------------------
+ * qsim_graph_begin starts capturing every launch this handle makes on its
+ * stream (nothing runs); the gate calls that follow (qsim_apply_gate /
+ * qsim_apply_circuit) are planned and compiled on the host as usual;
+ * qsim_graph_end stops the capture and instantiates the graph (*out, owned
+ * by the caller, freed with qsim_graph_destroy).  qsim_graph_launch replays
+ * it on the handle's stream: the same kernels with the same parameters,
+ * i.e. the captured gate sequence applied again to the CURRENT state, with
+ * no host planning.  Valid only when the captured sequence leaves the
+ * logical->physical qubit map and the shard labels unchanged (so a replay
+ * sees the layout the capture saw); otherwise qsim_graph_end returns
+ * QSIM_EUNSUPPORTED and the state is in an unspecified (but allocated)
+ * condition -- call qsim_reset.  E encoding and the loopback transport only
+ * (the A encoding synchronises with the host for its bounds; NCCL uses a
+ * second stream): QSIM_EUNSUPPORTED otherwise.  Read-out calls between
+ * begin and end return QSIM_EINVAL.  Profiling records are not taken while
+ * capturing. */
+typedef struct qsim_graph qsim_graph;
+int qsim_graph_begin(qsim_state *s);
+int qsim_graph_end(qsim_state *s, qsim_graph **out);
+int qsim_graph_launch(qsim_state *s, qsim_graph *g);
+int qsim_graph_destroy(qsim_graph *g);
 
 /* The cudaStream_t (as void*) the library launches shard `shard`'s kernels
  * on (shard index local to this process), for event timing by the caller. */

@@ -90,6 +90,7 @@ EXPORTS = (
     "qsim_aux_amplitudes", "qsim_aux_num_vars", "qsim_set_qubit_map",
     "qsim_asm_parse", "qsim_asm_info", "qsim_asm_get_op", "qsim_asm_destroy", "qsim_asm_run",
     "qsim_asm_result_get", "qsim_asm_result_destroy",
+    "qsim_overlap", "qsim_graph_begin", "qsim_graph_end", "qsim_graph_launch", "qsim_graph_destroy",
 )
 
 if not os.path.exists(_LIB_PATH):
@@ -141,6 +142,11 @@ _lib.qsim_set_state.argtypes = [_P, _dp]
 _lib.qsim_get_codes.argtypes = [_P, ctypes.POINTER(ctypes.c_int8), _dp, _dp]
 _lib.qsim_set_codes.argtypes = [_P, ctypes.POINTER(ctypes.c_int8), ctypes.c_double, ctypes.c_double]
 _lib.qsim_sync.argtypes = [_P]
+_lib.qsim_overlap.argtypes = [_P, _P, _dp]
+_lib.qsim_graph_begin.argtypes = [_P]
+_lib.qsim_graph_end.argtypes = [_P, ctypes.POINTER(_P)]
+_lib.qsim_graph_launch.argtypes = [_P, _P]
+_lib.qsim_graph_destroy.argtypes = [_P]
 _lib.qsim_stream.argtypes = [_P, ctypes.c_int]
 _lib.qsim_stream.restype = ctypes.c_void_p
 _lib.qsim_get_stats.argtypes = [_P, ctypes.POINTER(qsim_stats)]
@@ -423,6 +429,30 @@ def qsim_sync(h):
     _check(_lib.qsim_sync(h))
 
 
+def qsim_overlap(ha, hb) -> complex:
+    out = (ctypes.c_double * 2)()
+    _check(_lib.qsim_overlap(ha, hb, out))
+    return complex(out[0], out[1])
+
+
+def qsim_graph_begin(h):
+    _check(_lib.qsim_graph_begin(h))
+
+
+def qsim_graph_end(h):
+    g = _P()
+    _check(_lib.qsim_graph_end(h, ctypes.byref(g)))
+    return g
+
+
+def qsim_graph_launch(h, g):
+    _check(_lib.qsim_graph_launch(h, g))
+
+
+def qsim_graph_destroy(g):
+    _check(_lib.qsim_graph_destroy(g))
+
+
 def qsim_stream(h, shard=0) -> int:
     return _lib.qsim_stream(h, shard) or 0
 
@@ -568,6 +598,24 @@ class State:
     def stream(self):
         return qsim_stream(self.h)
 
+    def overlap(self, other):
+        """<self|other> (qsim_overlap)."""
+        return qsim_overlap(self.h, other.h)
+
+    def capture(self, fn):
+        """Capture the launches fn(self) makes into a CUDA graph (qsim_graph_*);
+        returns a Graph whose launch() replays them on the current state."""
+        qsim_graph_begin(self.h)
+        try:
+            fn(self)
+        except BaseException:
+            try:
+                qsim_graph_destroy(qsim_graph_end(self.h))
+            except QsimError:
+                pass
+            raise
+        return Graph(self, qsim_graph_end(self.h))
+
     def stats(self):
         return qsim_get_stats(self.h)
 
@@ -586,3 +634,25 @@ class State:
 
     def qubit_map(self):
         return qsim_get_qubit_map(self.h, self.n)
+
+
+class Graph:
+    """A captured gate sequence (qsim_graph_*): launch() replays it on the
+    owning State's stream with no host planning."""
+
+    def __init__(self, state, g):
+        self.state, self.g = state, g
+
+    def launch(self):
+        qsim_graph_launch(self.state.h, self.g)
+
+    def close(self):
+        if self.g:
+            qsim_graph_destroy(self.g)
+            self.g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

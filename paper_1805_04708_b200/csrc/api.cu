@@ -76,6 +76,8 @@ struct qsim_state {
     qsim_stats st{};
     // A variant
     double r0 = 0.5, r1 = 0.5;
+    bool r_stale = false;  // dense gates update (r0, r1) in the device tables only (read back on demand)
+    double *d_acc = nullptr;  // (min, -max) of |z|^2 of a dense A gate
     ATables *atab = nullptr;
     // profiling (qsim_profile): event pairs around each launch
     struct ProfRec {
@@ -84,6 +86,10 @@ struct qsim_state {
         cudaEvent_t a, b;
     };
     bool prof = false;
+    bool capturing = false;      // qsim_graph_begin .. qsim_graph_end
+    bool prof_saved = false;
+    std::vector<int> cap_pos;    // qubit map at qsim_graph_begin
+    std::vector<uint32_t> cap_gphys;
     std::vector<ProfRec> prof_recs;
     std::vector<cudaEvent_t> ev_pool;
     std::vector<uint32_t> gphys, ginv;  // storage index -> physical global bits (phi) and inverse
@@ -1034,6 +1040,7 @@ int qsim_destroy(qsim_state *s) {
     for (auto e : s->ev_pool) cudaEventDestroy(e);
     if (s->d_partials) cudaFree(s->d_partials);
     if (s->d_out) cudaFree(s->d_out);
+    if (s->d_acc) cudaFree(s->d_acc);
     if (s->h_out) cudaFreeHost(s->h_out);
     if (s->atab) atables_free(s->atab);
     if (s->stream) cudaStreamDestroy(s->stream);
@@ -1059,6 +1066,7 @@ static int init_state(qsim_state *s) {
         }
     }
     s->r0 = s->r1 = 0.5;
+    s->r_stale = false;
     if (s->enc == QSIM_ENC_ADAPTIVE2) RC(atables_set(s->atab, s->r0, s->r1, s->stream));
     CU(cudaStreamSynchronize(s->stream));
     return QSIM_OK;
@@ -1191,6 +1199,7 @@ int qsim_create_ex(const qsim_config *cfg, qsim_state **out) {
     }
     if (cudaMalloc(&s->d_partials, (size_t)red_blocks() * RED_SLOTS * sizeof(double) * 2) != cudaSuccess ||
         cudaMalloc(&s->d_out, 4096 * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&s->d_acc, 2 * sizeof(double)) != cudaSuccess ||
         cudaMallocHost(&s->h_out, 4096 * sizeof(double)) != cudaSuccess) {
         cudaGetLastError();
         set_error("reduction scratch allocation failed");
@@ -1269,6 +1278,10 @@ int qsim_apply_swap(qsim_state *s, int q1, int q2) {
 }
 
 int qsim_reset(qsim_state *s) {
+    if (s && s->capturing) {
+        set_error("qsim_reset: not allowed while a graph capture is open");
+        return QSIM_EINVAL;
+    }
     if (!s) return QSIM_EINVAL;
     cudaSetDevice(s->dev);
     if (s->comm_stream) CU(cudaStreamSynchronize(s->comm_stream));
@@ -1283,6 +1296,10 @@ int qsim_profile(qsim_state *s, int enable) {
 }
 
 int qsim_profile_read(qsim_state *s, qsim_kernel_profile *out, int max, int *nout) {
+    if (s && s->capturing) {
+        set_error("qsim_profile_read: not allowed while a graph capture is open");
+        return QSIM_EINVAL;
+    }
     if (!s || (!out && max > 0)) return QSIM_EINVAL;
     CU(cudaStreamSynchronize(s->stream));
     qsim_kernel_profile agg[QSIM_K_NUM];
@@ -1308,8 +1325,92 @@ int qsim_profile_read(qsim_state *s, qsim_kernel_profile *out, int max, int *nou
 
 int qsim_sync(qsim_state *s) {
     if (!s) return QSIM_EINVAL;
+    if (s->capturing) {
+        set_error("qsim_sync: not allowed while a graph capture is open");
+        return QSIM_EINVAL;
+    }
     CU(cudaStreamSynchronize(s->stream));
     if (s->comm_stream) CU(cudaStreamSynchronize(s->comm_stream));
+    return QSIM_OK;
+}
+
+struct qsim_graph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    qsim_state *owner = nullptr;
+};
+
+int qsim_graph_begin(qsim_state *s) {
+    if (!s) return QSIM_EINVAL;
+    if (s->capturing) {
+        set_error("qsim_graph_begin: a capture is already open");
+        return QSIM_EINVAL;
+    }
+    if (s->enc != QSIM_ENC_FP64 || (s->P > 1 && s->transport != QSIM_TRANSPORT_LOCAL)) {
+        set_error("qsim_graph_begin: graphs need the E encoding and the loopback transport");
+        return QSIM_EUNSUPPORTED;
+    }
+    CU(cudaStreamSynchronize(s->stream));
+    s->cap_pos = s->pl.pos;
+    s->cap_gphys = s->gphys;
+    s->prof_saved = s->prof;
+    s->prof = false;
+    CU(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+    s->capturing = true;
+    return QSIM_OK;
+}
+
+int qsim_graph_end(qsim_state *s, qsim_graph **out) {
+    if (!s || !out) return QSIM_EINVAL;
+    *out = nullptr;
+    if (!s->capturing) {
+        set_error("qsim_graph_end: no capture open");
+        return QSIM_EINVAL;
+    }
+    s->capturing = false;
+    s->prof = s->prof_saved;
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(s->stream, &g);
+    if (e != cudaSuccess || !g) {
+        cudaGetLastError();
+        set_error(std::string("qsim_graph_end: capture failed: ") + cudaGetErrorString(e));
+        if (g) cudaGraphDestroy(g);
+        return QSIM_ECUDA;
+    }
+    if (s->pl.pos != s->cap_pos || s->gphys != s->cap_gphys) {
+        cudaGraphDestroy(g);
+        set_error("qsim_graph_end: the captured gates change the qubit map / shard labels; a replay would see "
+                  "another layout (call qsim_reset)");
+        return QSIM_EUNSUPPORTED;
+    }
+    auto *G = new qsim_graph();
+    G->graph = g;
+    G->owner = s;
+    if (cudaGraphInstantiate(&G->exec, g, 0) != cudaSuccess) {
+        cudaGetLastError();
+        cudaGraphDestroy(g);
+        delete G;
+        set_error("qsim_graph_end: cudaGraphInstantiate failed");
+        return QSIM_ECUDA;
+    }
+    *out = G;
+    return QSIM_OK;
+}
+
+int qsim_graph_launch(qsim_state *s, qsim_graph *g) {
+    if (!s || !g || g->owner != s || s->capturing) {
+        set_error("qsim_graph_launch: graph / handle mismatch or capture open");
+        return QSIM_EINVAL;
+    }
+    CU(cudaGraphLaunch(g->exec, s->stream));
+    return QSIM_OK;
+}
+
+int qsim_graph_destroy(qsim_graph *g) {
+    if (!g) return QSIM_OK;
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
     return QSIM_OK;
 }
 
@@ -1336,6 +1437,10 @@ int qsim_get_qubit_map(qsim_state *s, int *pos) {
 }
 
 int qsim_norm(qsim_state *s, double *norm2) {
+    if (s && s->capturing) {
+        set_error("qsim_norm: not allowed while a graph capture is open");
+        return QSIM_EINVAL;
+    }
     if (!s || !norm2) return QSIM_EINVAL;
     cudaSetDevice(s->dev);
     std::vector<double> phys;
@@ -1344,7 +1449,43 @@ int qsim_norm(qsim_state *s, double *norm2) {
     return QSIM_OK;
 }
 
+int qsim_overlap(qsim_state *a, qsim_state *b, double *out) {
+    if (!a || !b || !out) return QSIM_EINVAL;
+    if (a->capturing || b->capturing) {
+        set_error("qsim_overlap: not allowed while a graph capture is open");
+        return QSIM_EINVAL;
+    }
+    if (a->n != b->n || a->P != b->P || a->dev != b->dev || (a->P > 1 && (a->transport != QSIM_TRANSPORT_LOCAL ||
+                                                                         b->transport != QSIM_TRANSPORT_LOCAL))) {
+        set_error("qsim_overlap: the handles need the same N, shard count and device, loopback transport");
+        return QSIM_EUNSUPPORTED;
+    }
+    if (a->pl.pos != b->pl.pos || a->gphys != b->gphys) {
+        set_error("qsim_overlap: the handles have different qubit maps / shard labels");
+        return QSIM_EUNSUPPORTED;
+    }
+    cudaSetDevice(a->dev);
+    CU(cudaStreamSynchronize(b->stream));
+    double sr = 0.0, si = 0.0;
+    for (size_t k = 0; k < a->shards.size(); ++k) {
+        launch_overlap(a->shards[k].amps, a->enc == QSIM_ENC_FP64 ? nullptr : a->atab, b->shards[k].amps,
+                       b->enc == QSIM_ENC_FP64 ? nullptr : b->atab, 1ull << a->nl, a->d_partials, a->d_out, a->stream);
+        a->st.kernels += 2;
+        CU(cudaMemcpyAsync(a->h_out, a->d_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, a->stream));
+        CU(cudaStreamSynchronize(a->stream));
+        sr += a->h_out[0];
+        si += a->h_out[1];
+    }
+    out[0] = sr;
+    out[1] = si;
+    return QSIM_OK;
+}
+
 int qsim_probabilities(qsim_state *s, double *p1) {
+    if (s && s->capturing) {
+        set_error("qsim_probabilities: not allowed while a graph capture is open");
+        return QSIM_EINVAL;
+    }
     if (!s || !p1) return QSIM_EINVAL;
     cudaSetDevice(s->dev);
     std::vector<double> phys;
@@ -1370,6 +1511,10 @@ static int pair_sums_local(qsim_state *s, int b, double &sr, double &si) {
 }
 
 int qsim_expectations(qsim_state *s, double *q) {
+    if (s && s->capturing) {
+        set_error("qsim_expectations: not allowed while a graph capture is open");
+        return QSIM_EINVAL;
+    }
     if (!s || !q) return QSIM_EINVAL;
     cudaSetDevice(s->dev);
     std::vector<double> phys;
@@ -1477,6 +1622,10 @@ static int collapse(qsim_state *s, int b, int out, double keep) {
 }
 
 int qsim_measure_u(qsim_state *s, int qubit, double u, int *outcome, double *p0_out) {
+    if (s && s->capturing) {
+        set_error("qsim_measure_u: not allowed while a graph capture is open");
+        return QSIM_EINVAL;
+    }
     if (!s || !outcome || qubit < 0 || qubit >= s->n) {
         set_error("qsim_measure: bad qubit or null outcome");
         return QSIM_EINVAL;
@@ -1495,6 +1644,10 @@ int qsim_measure_u(qsim_state *s, int qubit, double u, int *outcome, double *p0_
 }
 
 int qsim_project(qsim_state *s, int qubit, int value) {
+    if (s && s->capturing) {
+        set_error("qsim_project: not allowed while a graph capture is open");
+        return QSIM_EINVAL;
+    }
     if (!s || qubit < 0 || qubit >= s->n || (value != 0 && value != 1)) {
         set_error("qsim_project: bad qubit or value (0 = CLEAR, 1 = SET)");
         return QSIM_EINVAL;
@@ -1508,6 +1661,10 @@ int qsim_project(qsim_state *s, int qubit, int value) {
 }
 
 int qsim_sample(qsim_state *s, size_t nsamples, uint64_t seed, uint64_t *out) {
+    if (s && s->capturing) {
+        set_error("qsim_sample: not allowed while a graph capture is open");
+        return QSIM_EINVAL;
+    }
     if (!s || (nsamples && !out)) return QSIM_EINVAL;
     if (s->transport == QSIM_TRANSPORT_NCCL && s->P > 1) {
         set_error("qsim_sample: not implemented for the multi-process NCCL transport");
@@ -1583,12 +1740,17 @@ int qsim_prepare_shorbox(qsim_state *s, int nx, uint64_t G, uint64_t y) {
     if (s->enc == QSIM_ENC_ADAPTIVE2) {
         const double r = (nx == 0) ? 0.5 : std::ldexp(1.0, -nx / 2) * ((nx & 1) ? 0.70710678118654752440 : 1.0);
         s->r0 = s->r1 = r;  // every non-zero amplitude has magnitude 2^{-nx/2} (reading R-A7/R-A8)
+        s->r_stale = false;
         RC(atables_set(s->atab, s->r0, s->r1, s->stream));
     }
     return QSIM_OK;
 }
 
 int qsim_measure(qsim_state *s, int qubit, uint64_t seed, int *outcome) {
+    if (s && s->capturing) {
+        set_error("qsim_measure: not allowed while a graph capture is open");
+        return QSIM_EINVAL;
+    }
     uint64_t x = splitmix64(seed);
     double u = (double)(x >> 11) * (1.0 / 9007199254740992.0);
     return qsim_measure_u(s, qubit, u, outcome, nullptr);
@@ -1602,6 +1764,10 @@ static uint64_t logical_to_phys(const qsim_state *s, uint64_t L) {
 }
 
 int qsim_get_amplitudes(qsim_state *s, const uint64_t *idx, size_t m, double *out) {
+    if (s && s->capturing) {
+        set_error("qsim_get_amplitudes: not allowed while a graph capture is open");
+        return QSIM_EINVAL;
+    }
     if (!s || (m && (!idx || !out))) return QSIM_EINVAL;
     cudaSetDevice(s->dev);
     const uint64_t dim_mask = (s->n == 64) ? ~0ull : ((1ull << s->n) - 1ull);
@@ -1686,6 +1852,10 @@ static int upload_inv(qsim_state *s, int **d_inv) {
 }
 
 int qsim_get_state(qsim_state *s, double *out) {
+    if (s && s->capturing) {
+        set_error("qsim_get_state: not allowed while a graph capture is open");
+        return QSIM_EINVAL;
+    }
     if (!s || !out) return QSIM_EINVAL;
     if (s->n > 30) {
         set_error("qsim_get_state is for N <= 30");
@@ -1715,6 +1885,10 @@ int qsim_get_state(qsim_state *s, double *out) {
 }
 
 int qsim_set_state(qsim_state *s, const double *amps) {
+    if (s && s->capturing) {
+        set_error("qsim_set_state: not allowed while a graph capture is open");
+        return QSIM_EINVAL;
+    }
     if (!s || !amps) return QSIM_EINVAL;
     if (s->enc != QSIM_ENC_FP64) {
         set_error("qsim_set_state: E only (use qsim_set_codes for A)");
@@ -1741,7 +1915,24 @@ int qsim_set_state(qsim_state *s, const double *amps) {
     return QSIM_OK;
 }
 
+// (r0, r1) of the current A tables back to the host after dense gates built them on the device
+static int sync_bounds(qsim_state *s) {
+    if (!s->r_stale) return QSIM_OK;
+    double rr[2];
+    CU(cudaMemcpyAsync(rr, reinterpret_cast<const char *>(s->atab->d[s->atab->cur]) + offsetof(ATabData, r0),
+                       sizeof(rr), cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaStreamSynchronize(s->stream));
+    s->r0 = rr[0];
+    s->r1 = rr[1];
+    s->r_stale = false;
+    return QSIM_OK;
+}
+
 int qsim_get_codes(qsim_state *s, int8_t *codes, double *r0, double *r1) {
+    if (s && s->capturing) {
+        set_error("qsim_get_codes: not allowed while a graph capture is open");
+        return QSIM_EINVAL;
+    }
     if (!s || !codes) return QSIM_EINVAL;
     if (s->enc != QSIM_ENC_ADAPTIVE2) {
         set_error("qsim_get_codes: A only");
@@ -1765,12 +1956,17 @@ int qsim_get_codes(qsim_state *s, int8_t *codes, double *r0, double *r1) {
     CU(cudaStreamSynchronize(s->stream));
     cudaFree(d_full);
     cudaFree(d_inv);
+    RC(sync_bounds(s));
     if (r0) *r0 = s->r0;
     if (r1) *r1 = s->r1;
     return QSIM_OK;
 }
 
 int qsim_set_codes(qsim_state *s, const int8_t *codes, double r0, double r1) {
+    if (s && s->capturing) {
+        set_error("qsim_set_codes: not allowed while a graph capture is open");
+        return QSIM_EINVAL;
+    }
     if (!s || !codes) return QSIM_EINVAL;
     if (s->enc != QSIM_ENC_ADAPTIVE2) {
         set_error("qsim_set_codes: A only");
@@ -1793,6 +1989,7 @@ int qsim_set_codes(qsim_state *s, const int8_t *codes, double r0, double r1) {
     }
     s->r0 = r0;
     s->r1 = r1;
+    s->r_stale = false;
     RC(atables_set(s->atab, r0, r1, s->stream));
     CU(cudaStreamSynchronize(s->stream));
     cudaFree(d_full);
@@ -1810,38 +2007,24 @@ namespace qsim {
 // Exact global bounds of the post-gate magnitudes (reading R-A4), then the
 // decode-apply-encode sweep with those bounds.
 static int dense_gate_a(qsim_state *s, const PlanOp &o, const double *u) {
-    double mn = INFINITY, mx = -INFINITY;
+    // phase 1 on every shard: (min, -max) of the post-gate |z|^2 merged on the
+    // device; across ranks one ncclAllReduce(min); the next tables are built
+    // on the device from the result -- no host round trip per gate
+    bool first = true;
     for (auto &sh : s->shards) {
         AGateParams p{};
         fill_agate(p, s, sh, o, u);
         prof_begin(s);
-        launch_bounds_a(p, s->atab, s->d_partials, s->d_out, s->stream);
+        launch_bounds_a(p, s->atab, s->d_partials, s->d_acc, first, s->stream);
         prof_end(s, QSIM_K_A_BOUNDS, std::ldexp((double)s->amp_bytes, s->nl));
+        first = false;
         s->st.kernels += 2;
         s->st.hbm_bytes += std::ldexp((double)s->amp_bytes, s->nl);
-        CU(cudaMemcpyAsync(s->h_out, s->d_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
-        CU(cudaStreamSynchronize(s->stream));
-        mn = std::min(mn, s->h_out[0]);
-        mx = std::max(mx, s->h_out[1]);
     }
-    if (s->transport == QSIM_TRANSPORT_NCCL) {
-        s->h_out[0] = mn;
-        s->h_out[1] = -mx;
-        CU(cudaMemcpyAsync(s->d_out, s->h_out, 2 * sizeof(double), cudaMemcpyHostToDevice, s->stream));
-        NC(ncclAllReduce(s->d_out, s->d_out, 2, ncclFloat64, ncclMin, s->comm, s->stream));
-        CU(cudaMemcpyAsync(s->h_out, s->d_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
-        CU(cudaStreamSynchronize(s->stream));
-        mn = s->h_out[0];
-        mx = -s->h_out[1];
-    }
-    double r0n, r1n;
-    if (mn > mx) {  // no intermediate magnitudes: sentinel (reading R-A8)
-        r0n = r1n = 0.5;
-    } else {
-        r0n = std::sqrt(mn);
-        r1n = std::sqrt(mx);
-    }
-    RC(atables_set_next(s->atab, r0n, r1n, s->stream));
+    if (s->transport == QSIM_TRANSPORT_NCCL)
+        NC(ncclAllReduce(s->d_acc, s->d_acc, 2, ncclFloat64, ncclMin, s->comm, s->stream));
+    launch_tables_next(s->d_acc, s->atab, s->stream);
+    s->st.kernels++;
     for (auto &sh : s->shards) {
         AGateParams p{};
         fill_agate(p, s, sh, o, u);
@@ -1851,8 +2034,7 @@ static int dense_gate_a(qsim_state *s, const PlanOp &o, const double *u) {
         s->st.kernels++;
         s->st.hbm_bytes += std::ldexp(2.0 * (double)s->amp_bytes, s->nl);
     }
-    s->r0 = r0n;
-    s->r1 = r1n;
+    s->r_stale = true;  // (r0, r1) now live in the device tables only
     RC(atables_commit_next(s->atab, s->stream));
     CU(cudaGetLastError());
     return QSIM_OK;
@@ -1899,7 +2081,7 @@ int measure_collapse_a(qsim_state *s, int b, int out, double f) {
         CU(cudaMemcpyAsync(s->h_out, s->d_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
         CU(cudaStreamSynchronize(s->stream));
         mn = std::min(mn, s->h_out[0]);
-        mx = std::max(mx, s->h_out[1]);
+        mx = std::max(mx, -s->h_out[1]);
     }
     if (s->transport == QSIM_TRANSPORT_NCCL) {
         s->h_out[0] = mn;
@@ -1929,6 +2111,7 @@ int measure_collapse_a(qsim_state *s, int b, int out, double f) {
     }
     s->r0 = r0n;
     s->r1 = r1n;
+    s->r_stale = false;
     RC(atables_commit_next(s->atab, s->stream));
     return QSIM_OK;
 }

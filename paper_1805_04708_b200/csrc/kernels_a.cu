@@ -133,6 +133,7 @@ struct ASm {
     double r0n, scalen;
     int degn;
     float mmargin;  // magnitude-candidate margin (steps) below which the fp64 check is skipped
+    float scalef, r0s;  // fp32 253/(r1-r0) and r0 * that (next bounds), for the candidate
 };
 
 __device__ void load_asm(ASm &sm, const ATabData *__restrict__ cur, const ATabData *__restrict__ nxt) {
@@ -151,8 +152,11 @@ __device__ void load_asm(ASm &sm, const ATabData *__restrict__ cur, const ATabDa
         sm.degn = nxt->degenerate;
         // fp32 candidate error in steps: |d tf| <= (eps32 (|m| + r0) + |m - m_f|) * scale,
         // bounded by 4e-7 * (r1 + r0) * scale + 1e-3; above 0.5 -> always check
-        const double e = 4e-7 * (nxt->r1 + nxt->r0) * nxt->scale + 1e-4;
+        // (a_encode2: fp32 copies of (x, y), |z|^2 and rsqrt in fp32: relative error <= 6e-7)
+        const double e = 6e-7 * (nxt->r1 + nxt->r0) * nxt->scale + 1e-4;
         sm.mmargin = (float)(e < 0.49 ? e : 0.5);
+        sm.scalef = (float)nxt->scale;
+        sm.r0s = (float)(nxt->r0 * nxt->scale);
     }
     __syncthreads();
 }
@@ -337,40 +341,154 @@ __device__ __forceinline__ double warp_sum_a(double v) {
     return v;
 }
 
-template <bool LOWT>
+// ---------------------------------------------------------------- dense gates
+// A unit = 16 codes = 8 pairs, one per thread per iteration.  TL = 0..3: the
+// target is bit TL of 16 contiguous codes (pairs (j, j | 2^TL)); TL = 4: the
+// target t >= 4 is a runtime bit, the unit is 8 contiguous codes at s0 and 8
+// at s0 | 2^t (pairs (k, k + 8)).  All register indexing is compile-time.
+// Controls: a pair is selected iff its full index has every cmask bit; the
+// unit's low bits (0..3, resp. 0..2) are the only ones that differ inside a
+// unit, so the test is (hi part of the unit) && ((slot & cl) == cl).
+template <int TL>
+struct AUnit {
+    static constexpr int LOWB = TL < 4 ? 4 : 3;
+    __device__ static __forceinline__ int j0(int k) { return TL < 4 ? (((k >> TL) << (TL + 1)) | (k & ((1 << TL) - 1))) : k; }
+    __device__ static __forceinline__ int j1(int k) { return TL < 4 ? (j0(k) | (1 << TL)) : k + 8; }
+    __device__ static __forceinline__ uint64_t s0(uint64_t u, int t) { return TL < 4 ? (u << 4) : a_ins0(u << 3, t); }
+    __device__ static __forceinline__ void load(const uint16_t *__restrict__ a, uint64_t s0, int t, uint32_t (&c)[16]) {
+        const uint4 v0 = __ldcs(reinterpret_cast<const uint4 *>(a + s0));
+        const uint4 v1 = __ldcs(reinterpret_cast<const uint4 *>(a + (TL < 4 ? s0 + 8 : (s0 | (1ull << t)))));
+        const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            c[2 * k] = w[k] & 0xffffu;
+            c[2 * k + 1] = w[k] >> 16;
+        }
+    }
+    __device__ static __forceinline__ void store(uint16_t *__restrict__ a, uint64_t s0, int t, const uint32_t (&c)[16]) {
+        uint4 v0, v1;
+        v0.x = c[0] | (c[1] << 16);
+        v0.y = c[2] | (c[3] << 16);
+        v0.z = c[4] | (c[5] << 16);
+        v0.w = c[6] | (c[7] << 16);
+        v1.x = c[8] | (c[9] << 16);
+        v1.y = c[10] | (c[11] << 16);
+        v1.z = c[12] | (c[13] << 16);
+        v1.w = c[14] | (c[15] << 16);
+        __stcs(reinterpret_cast<uint4 *>(a + s0), v0);
+        __stcs(reinterpret_cast<uint4 *>(a + (TL < 4 ? s0 + 8 : (s0 | (1ull << t)))), v1);
+    }
+};
+
+__device__ __forceinline__ void a_gate2(const double (&u)[8], double2 &x, double2 &y) {
+    const double2 x0 = x, y0 = y;
+    x.x = fma(u[0], x0.x, fma(-u[1], x0.y, fma(u[2], y0.x, -u[3] * y0.y)));
+    x.y = fma(u[0], x0.y, fma(u[1], x0.x, fma(u[2], y0.y, u[3] * y0.x)));
+    y.x = fma(u[4], x0.x, fma(-u[5], x0.y, fma(u[6], y0.x, -u[7] * y0.y)));
+    y.y = fma(u[4], x0.y, fma(u[5], x0.x, fma(u[6], y0.y, u[7] * y0.x)));
+}
+
+// hi words of A_ZERO2 = 1e-24 and A_ONE2 = (1 - 1e-12)^2: an m2 >= A_ZERO2 has
+// hi(m2) >= A_ZHI, an m2 <= A_ONE2 has hi(m2) <= A_OHI (m2 >= 0: hi words order
+// like the values); the fast paths below only ever widen to the exact tests.
+#define A_ZHI 0x3af357c2u
+#define A_OHI 0x3fefffffu
+
+// Running exact min / max of the intermediate m2 = |z|^2 (reading R-A4/R-A5)
+// with a hi-word pre-filter: a value can change mn (mx) only if its hi word is
+// <= hi(mn) (>= hi(mx)) and it can be intermediate; only those take the exact
+// fp64 path.
+struct ABnd {
+    double mn, mx;
+    uint32_t mnh, mxh;
+    __device__ __forceinline__ void init() {
+        mn = INFINITY;
+        mx = -INFINITY;
+        mnh = 0x7ff00000u;
+        mxh = 0u;
+    }
+    __device__ __forceinline__ void add(double m2) {
+        const uint32_t h = (uint32_t)__double2hiint(m2);
+        const bool cand = ((h <= mnh) & (h >= A_ZHI)) | ((h >= mxh) & (h <= A_OHI));
+        if (cand) {
+            if (m2 >= A_ZERO2 && m2 <= A_ONE2) {
+                if (m2 < mn) {
+                    mn = m2;
+                    mnh = h;
+                }
+                if (m2 > mx) {
+                    mx = m2;
+                    mxh = h;
+                }
+            }
+        }
+    }
+};
+
+// encode with the fp32 candidate computed from fp32 copies of (x, y)
+__device__ __forceinline__ uint32_t a_encode2(const ASm &sm, double2 z) {
+    const double m2 = a_m2(z);
+    const uint32_t h = (uint32_t)__double2hiint(m2);
+    int b0;
+    if (h <= A_ZHI || h >= A_OHI) {  // near or beyond the special thresholds: exact tests
+        if (m2 < A_ZERO2) return pack(-128, 0);
+        if (m2 > A_ONE2) return pack(127, a_angle_code(sm, z));
+    }
+    if (sm.degn) {
+        b0 = 0;
+    } else {
+        const float xf = (float)z.x, yf = (float)z.y;
+        const float m2f = fmaf(xf, xf, yf * yf);
+        const float mf = m2f * rsqrtf(m2f);
+        const float tf = fmaf(mf, sm.scalef, -sm.r0s);
+        int c = __float2int_rn(tf);
+        const float fr = tf - (float)c;
+        c = max(0, min(253, c));
+        if (fabsf(fr) > 0.5f - sm.mmargin) {
+            if (c < 253 && m2 >= sm.thr[c])
+                c += 1;
+            else if (c > 0 && m2 < sm.thr[c - 1])
+                c -= 1;
+        }
+        b0 = c - 127;
+    }
+    return pack(b0, a_angle_code(sm, z));
+}
+
+template <int TL, bool CTRL>
 __global__ void __launch_bounds__(A_THREADS) k_bounds_a(const __grid_constant__ AGateParams p,
                                                         const ATabData *__restrict__ cur,
                                                         const ATabData *__restrict__ nxt, double *partials) {
+    using U = AUnit<TL>;
     __shared__ ASm sm;
     load_asm(sm, cur, nxt);
     const uint16_t *a = reinterpret_cast<const uint16_t *>(p.a);
     const uint64_t units = (p.nl >= 4) ? (1ull << (p.nl - 4)) : 1ull;
-    double mn = INFINITY, mx = -INFINITY;
-    for (uint64_t u = (uint64_t)blockIdx.x * A_THREADS + threadIdx.x; u < units; u += (uint64_t)gridDim.x * A_THREADS) {
+    const uint64_t lowm = (1ull << U::LOWB) - 1ull;
+    const uint64_t chi = p.cmask & ~lowm;
+    const uint32_t cl = (uint32_t)(p.cmask & lowm);
+    double u[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) u[i] = p.u[i];
+    ABnd b;
+    b.init();
+    for (uint64_t v = (uint64_t)blockIdx.x * A_THREADS + threadIdx.x; v < units; v += (uint64_t)gridDim.x * A_THREADS) {
         uint32_t c[16];
-        uint64_t s0;
-        unit_load<LOWT>(a, u, p.t, c, s0);
+        const uint64_t s0 = U::s0(v, p.t);
+        U::load(a, s0, p.t, c);
+        const bool hi_ok = !CTRL || (((p.shard_base | s0) & chi) == chi);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            int j0, j1;
-            uint64_t i0;
-            pair_slots<LOWT>(k, p.t, s0, j0, j1, i0);
+            const int j0 = U::j0(k), j1 = U::j1(k);
             double2 x = a_decode(sm, c[j0]), y = a_decode(sm, c[j1]);
-            if (((p.shard_base | i0) & p.cmask) == p.cmask) a_gate(p.u, p.cls, x, y);
-            double mx2 = a_m2(x), my2 = a_m2(y);
-            if (is_inter(mx2)) {
-                mn = fmin(mn, mx2);
-                mx = fmax(mx, mx2);
-            }
-            if (is_inter(my2)) {
-                mn = fmin(mn, my2);
-                mx = fmax(mx, my2);
-            }
+            const int off = TL < 4 ? j0 : k;
+            if (!CTRL || (hi_ok && ((uint32_t)off & cl) == cl)) a_gate2(u, x, y);
+            b.add(a_m2(x));
+            b.add(a_m2(y));
         }
     }
     __shared__ double red[2][A_THREADS / 32];
-    mn = warp_min(mn);
-    mx = warp_max(mx);
+    const double mn = warp_min(b.mn), mx = warp_max(b.mx);
     if ((threadIdx.x & 31) == 0) {
         red[0][threadIdx.x >> 5] = mn;
         red[1][threadIdx.x >> 5] = mx;
@@ -387,61 +505,142 @@ __global__ void __launch_bounds__(A_THREADS) k_bounds_a(const __grid_constant__ 
     }
 }
 
-__global__ void k_minmax_final(const double *partials, int nb, double *out) {
-    if (threadIdx.x != 0) return;
+// merge the per-block partials into acc = (min m2, -max m2) (first shard:
+// overwrite), the form one ncclAllReduce(ncclMin) combines across ranks
+__global__ void k_minmax_final(const double *partials, int nb, double *acc, int first) {
+    __shared__ double r0[32], r1[32];
     double a0 = INFINITY, a1 = -INFINITY;
-    for (int b = 0; b < nb; ++b) {
-        a0 = fmin(a0, partials[2 * b]);
-        a1 = fmax(a1, partials[2 * b + 1]);
+    for (int i = threadIdx.x; i < nb; i += 32) {
+        a0 = fmin(a0, partials[2 * i]);
+        a1 = fmax(a1, partials[2 * i + 1]);
     }
-    out[0] = a0;
-    out[1] = a1;
+    r0[threadIdx.x] = a0;
+    r1[threadIdx.x] = a1;
+    __syncwarp();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 32; ++w) {
+            a0 = fmin(a0, r0[w]);
+            a1 = fmax(a1, r1[w]);
+        }
+        if (first) {
+            acc[0] = a0;
+            acc[1] = -a1;
+        } else {
+            acc[0] = fmin(acc[0], a0);
+            acc[1] = fmin(acc[1], -a1);
+        }
+    }
 }
 
-void launch_bounds_a(const AGateParams &p, const ATables *t, double *partials, double *out, cudaStream_t s) {
+// next tables from acc = (min m2, -max m2): r0 = sqrt(min), r1 = sqrt(max), or
+// the sentinel 0.5 when no magnitude is intermediate (reading R-A8).  The same
+// expressions as fill_tables on the host, with explicit IEEE roundings (no
+// FMA contraction), so device- and host-built tables are bit-identical.
+__global__ void k_tables_next(const double *acc, ATabData *t) {
+    const double mn = acc[0], mx = -acc[1];
+    const bool none = !(mn <= mx);
+    const double r0 = none ? 0.5 : __dsqrt_rn(mn), r1 = none ? 0.5 : __dsqrt_rn(mx);
+    const double d = __dsub_rn(r1, r0);
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        const int b0 = i - 128;
+        t->r[i] = b0 == -128 ? 0.0 : b0 == 127 ? 1.0 : __dadd_rn(__ddiv_rn(__dmul_rn((double)(b0 + 127), d), 253.0), r0);
+        if (i < 253) {
+            const double m = __dadd_rn(r0, __ddiv_rn(__dmul_rn((double)i + 0.5, d), 253.0));
+            t->thr[i] = __dmul_rn(m, m);
+        } else {
+            t->thr[i] = INFINITY;
+        }
+    }
+    if (threadIdx.x == 0) {
+        t->r0 = r0;
+        t->r1 = r1;
+        t->degenerate = !(r1 > r0);
+        t->scale = !(r1 > r0) ? 0.0 : __ddiv_rn(253.0, d);
+    }
+}
+
+template <int TL, bool CTRL>
+static void launch_bounds_tl(const AGateParams &p, const ATables *t, double *partials, int grid, cudaStream_t s) {
+    k_bounds_a<TL, CTRL><<<grid, A_THREADS, 0, s>>>(p, tcur(t), tnext(t), partials);
+}
+template <int TL>
+static void launch_bounds_c(const AGateParams &p, const ATables *t, double *partials, int grid, cudaStream_t s) {
+    if (p.cmask)
+        launch_bounds_tl<TL, true>(p, t, partials, grid, s);
+    else
+        launch_bounds_tl<TL, false>(p, t, partials, grid, s);
+}
+
+void launch_bounds_a(const AGateParams &p, const ATables *t, double *partials, double *acc, bool first,
+                     cudaStream_t s) {
     const uint64_t units = (p.nl >= 4) ? (1ull << (p.nl - 4)) : 1ull;
     int grid = a_grid(units);
     if (grid > 2 * a_num_sms() * 4) grid = 2 * a_num_sms() * 4;  // partials capacity
-    if (p.t < 4)
-        k_bounds_a<true><<<grid, A_THREADS, 0, s>>>(p, tcur(t), tnext(t), partials);
-    else
-        k_bounds_a<false><<<grid, A_THREADS, 0, s>>>(p, tcur(t), tnext(t), partials);
-    k_minmax_final<<<1, 32, 0, s>>>(partials, grid, out);
+    switch (p.t < 4 ? p.t : 4) {
+        case 0: launch_bounds_c<0>(p, t, partials, grid, s); break;
+        case 1: launch_bounds_c<1>(p, t, partials, grid, s); break;
+        case 2: launch_bounds_c<2>(p, t, partials, grid, s); break;
+        case 3: launch_bounds_c<3>(p, t, partials, grid, s); break;
+        default: launch_bounds_c<4>(p, t, partials, grid, s); break;
+    }
+    k_minmax_final<<<1, 32, 0, s>>>(partials, grid, acc, first ? 1 : 0);
 }
 
-template <bool LOWT>
+void launch_tables_next(const double *acc, ATables *t, cudaStream_t s) {
+    k_tables_next<<<1, 256, 0, s>>>(acc, t->d[1 - t->cur]);
+}
+
+template <int TL, bool CTRL>
 __global__ void __launch_bounds__(A_THREADS) k_apply_a(const __grid_constant__ AGateParams p,
                                                        const ATabData *__restrict__ cur,
                                                        const ATabData *__restrict__ nxt) {
+    using U = AUnit<TL>;
     __shared__ ASm sm;
     load_asm(sm, cur, nxt);
     uint16_t *a = reinterpret_cast<uint16_t *>(p.a);
     const uint64_t units = (p.nl >= 4) ? (1ull << (p.nl - 4)) : 1ull;
-    for (uint64_t u = (uint64_t)blockIdx.x * A_THREADS + threadIdx.x; u < units; u += (uint64_t)gridDim.x * A_THREADS) {
+    const uint64_t lowm = (1ull << U::LOWB) - 1ull;
+    const uint64_t chi = p.cmask & ~lowm;
+    const uint32_t cl = (uint32_t)(p.cmask & lowm);
+    double u[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) u[i] = p.u[i];
+    for (uint64_t v = (uint64_t)blockIdx.x * A_THREADS + threadIdx.x; v < units; v += (uint64_t)gridDim.x * A_THREADS) {
         uint32_t c[16];
-        uint64_t s0;
-        unit_load<LOWT>(a, u, p.t, c, s0);
+        const uint64_t s0 = U::s0(v, p.t);
+        U::load(a, s0, p.t, c);
+        const bool hi_ok = !CTRL || (((p.shard_base | s0) & chi) == chi);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            int j0, j1;
-            uint64_t i0;
-            pair_slots<LOWT>(k, p.t, s0, j0, j1, i0);
+            const int j0 = U::j0(k), j1 = U::j1(k);
             double2 x = a_decode(sm, c[j0]), y = a_decode(sm, c[j1]);
-            if (((p.shard_base | i0) & p.cmask) == p.cmask) a_gate(p.u, p.cls, x, y);
-            c[j0] = a_encode(sm, x);
-            c[j1] = a_encode(sm, y);
+            const int off = TL < 4 ? j0 : k;
+            if (!CTRL || (hi_ok && ((uint32_t)off & cl) == cl)) a_gate2(u, x, y);
+            c[j0] = a_encode2(sm, x);
+            c[j1] = a_encode2(sm, y);
         }
-        unit_store<LOWT>(a, s0, p.t, c);
+        U::store(a, s0, p.t, c);
     }
+}
+
+template <int TL>
+static void launch_apply_c(const AGateParams &p, const ATables *t, int grid, cudaStream_t s) {
+    if (p.cmask)
+        k_apply_a<TL, true><<<grid, A_THREADS, 0, s>>>(p, tcur(t), tnext(t));
+    else
+        k_apply_a<TL, false><<<grid, A_THREADS, 0, s>>>(p, tcur(t), tnext(t));
 }
 
 void launch_apply_a(const AGateParams &p, const ATables *t, cudaStream_t s) {
     const uint64_t units = (p.nl >= 4) ? (1ull << (p.nl - 4)) : 1ull;
-    int grid = a_grid(units);
-    if (p.t < 4)
-        k_apply_a<true><<<grid, A_THREADS, 0, s>>>(p, tcur(t), tnext(t));
-    else
-        k_apply_a<false><<<grid, A_THREADS, 0, s>>>(p, tcur(t), tnext(t));
+    const int grid = a_grid(units);
+    switch (p.t < 4 ? p.t : 4) {
+        case 0: launch_apply_c<0>(p, t, grid, s); break;
+        case 1: launch_apply_c<1>(p, t, grid, s); break;
+        case 2: launch_apply_c<2>(p, t, grid, s); break;
+        case 3: launch_apply_c<3>(p, t, grid, s); break;
+        default: launch_apply_c<4>(p, t, grid, s); break;
+    }
 }
 
 // ---------------------------------------------------------------- fast paths
@@ -667,7 +866,7 @@ void launch_collapse_bounds_a(const ACollapseParams &p, const ATables *t, double
     int grid = a_grid(p.n >> 3);
     if (grid > 2 * a_num_sms() * 4) grid = 2 * a_num_sms() * 4;
     k_collapse_a<false><<<grid, A_THREADS, 0, s>>>(p, tcur(t), tnext(t), partials);
-    k_minmax_final<<<1, 32, 0, s>>>(partials, grid, out);
+    k_minmax_final<<<1, 32, 0, s>>>(partials, grid, out, 1);  // out = (min, -max)
 }
 void launch_collapse_apply_a(const ACollapseParams &p, const ATables *t, cudaStream_t s) {
     k_collapse_a<true><<<a_grid(p.n >> 3), A_THREADS, 0, s>>>(p, tcur(t), tnext(t), nullptr);
@@ -806,6 +1005,80 @@ void launch_dot_a(const void *x, const void *y, uint64_t n, const ATables *t, do
     int nb = red_blocks();
     k_dot_a<<<nb, 256, 0, s>>>(reinterpret_cast<const uint16_t *>(x), reinterpret_cast<const uint16_t *>(y), n,
                                tcur(t), partials);
+    k_final_sum_a<<<1, 32, 0, s>>>(partials, nb, 2, out);
+}
+
+// <x|y> = sum conj(x_i) y_i over one shard pair, each side E (complex fp64)
+// or A (decoded with its own current tables): the fidelity of an A run
+// against an E run of the same circuit.
+struct AOvSm {
+    double r[2][256];
+    double2 cs[2][256];
+};
+template <bool XA, bool YA>
+__global__ void __launch_bounds__(256) k_overlap(const void *__restrict__ xv, const void *__restrict__ yv, uint64_t n,
+                                                 const ATabData *__restrict__ tx, const ATabData *__restrict__ ty,
+                                                 double *partials) {
+    __shared__ AOvSm sm;
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        if (XA) {
+            sm.r[0][i] = tx->r[i];
+            sm.cs[0][i] = make_double2(tx->cth[i], tx->sth[i]);
+        }
+        if (YA) {
+            sm.r[1][i] = ty->r[i];
+            sm.cs[1][i] = make_double2(ty->cth[i], ty->sth[i]);
+        }
+    }
+    __syncthreads();
+    double sr = 0.0, si = 0.0;
+    for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (uint64_t)gridDim.x * 256) {
+        double2 u, v;
+        if (XA) {
+            const uint32_t c = reinterpret_cast<const uint16_t *>(xv)[i];
+            const double r = sm.r[0][(c & 0xffu) ^ 0x80u];
+            const double2 e = sm.cs[0][((c >> 8) & 0xffu) ^ 0x80u];
+            u = make_double2(r * e.x, r * e.y);
+        } else {
+            u = reinterpret_cast<const double2 *>(xv)[i];
+        }
+        if (YA) {
+            const uint32_t c = reinterpret_cast<const uint16_t *>(yv)[i];
+            const double r = sm.r[1][(c & 0xffu) ^ 0x80u];
+            const double2 e = sm.cs[1][((c >> 8) & 0xffu) ^ 0x80u];
+            v = make_double2(r * e.x, r * e.y);
+        } else {
+            v = reinterpret_cast<const double2 *>(yv)[i];
+        }
+        sr = fma(u.x, v.x, fma(u.y, v.y, sr));
+        si = fma(u.x, v.y, fma(-u.y, v.x, si));
+    }
+    __shared__ double red[2][8];
+    sr = warp_sum_a(sr);
+    si = warp_sum_a(si);
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = sr;
+        red[1][threadIdx.x >> 5] = si;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+        double s2 = 0.0;
+        for (int w = 0; w < 8; ++w) s2 += red[threadIdx.x][w];
+        partials[(size_t)blockIdx.x * 2 + threadIdx.x] = s2;
+    }
+}
+void launch_overlap(const void *x, const ATables *tx, const void *y, const ATables *ty, uint64_t n, double *partials,
+                    double *out, cudaStream_t s) {
+    const int nb = red_blocks();
+    const ATabData *dx = tx ? tcur(tx) : nullptr, *dy = ty ? tcur(ty) : nullptr;
+    if (tx && ty)
+        k_overlap<true, true><<<nb, 256, 0, s>>>(x, y, n, dx, dy, partials);
+    else if (tx)
+        k_overlap<true, false><<<nb, 256, 0, s>>>(x, y, n, dx, dy, partials);
+    else if (ty)
+        k_overlap<false, true><<<nb, 256, 0, s>>>(x, y, n, dx, dy, partials);
+    else
+        k_overlap<false, false><<<nb, 256, 0, s>>>(x, y, n, dx, dy, partials);
     k_final_sum_a<<<1, 32, 0, s>>>(partials, nb, 2, out);
 }
 

@@ -57,13 +57,18 @@ struct ACollapseParams {
 };
 
 void launch_init_a(void *a, uint64_t n, bool first, cudaStream_t s);
-// phase 1 of a dense gate: out[0] = min |z'|^2, out[1] = max |z'|^2 over intermediates (+inf/-inf if none)
-void launch_bounds_a(const AGateParams &p, const ATables *t, double *partials, double *out, cudaStream_t s);
+// phase 1 of a dense gate: acc = (min |z'|^2, -max |z'|^2) over intermediates (+inf/+inf if none),
+// merged into acc unless `first` (several shards on one device); ncclMin-reducible across ranks
+void launch_bounds_a(const AGateParams &p, const ATables *t, double *partials, double *acc, bool first,
+                     cudaStream_t s);
+// the next tables (r, thr, r0, r1, scale) built on the device from acc (no host round trip)
+void launch_tables_next(const double *acc, ATables *t, cudaStream_t s);
 // phase 2: decode (current tables), apply, encode (next tables)
 void launch_apply_a(const AGateParams &p, const ATables *t, cudaStream_t s);
 // diagonal / anti-diagonal gates: b1 shifts and code moves, bounds unchanged
 void launch_fast_a(const AGateParams &p, const ATables *t, cudaStream_t s);
 void launch_xchg_a(const struct XchgParams &p, const ATables *t, cudaStream_t s);
+// collapse phase 1: out = (min |z'|^2, -max |z'|^2)
 void launch_collapse_bounds_a(const ACollapseParams &p, const ATables *t, double *partials, double *out,
                               cudaStream_t s);
 void launch_collapse_apply_a(const ACollapseParams &p, const ATables *t, cudaStream_t s);
@@ -73,6 +78,9 @@ void launch_pairdot_a(const void *a, int nl, int q, const ATables *t, double *pa
                       cudaStream_t s);
 void launch_dot_a(const void *x, const void *y, uint64_t n, const ATables *t, double *partials, double *out,
                   cudaStream_t s);
+// <x|y> over n amplitudes; tx / ty: the A tables of an A side, nullptr for an E side
+void launch_overlap(const void *x, const ATables *tx, const void *y, const ATables *ty, uint64_t n, double *partials,
+                    double *out, cudaStream_t s);
 void launch_gather_a(const void *a, const uint64_t *off, uint64_t m, const ATables *t, double *out, cudaStream_t s);
 void launch_to_logical_a(const void *a, uint64_t n, uint64_t base, const int *inv, int nq, const ATables *t,
                          void *out, cudaStream_t s);

@@ -213,3 +213,49 @@ def test_table5_shor_n30_in_a():
         s.apply_circuit(C.qft_register(30, 20))
         e = s.expectations()[:20]
     assert np.max(np.abs(e - t[:, 4:7])) <= 0.011
+
+
+@pytest.mark.parametrize("P", [1, 4])
+def test_overlap_a_vs_e_on_device(P):
+    """qsim_overlap: <A|E>, <E|A>, <A|A>, <E|E> computed on the device equal
+    np.vdot of the two decoded states read back (1e-12), so the config-4
+    fidelity |<A|E>|^2 / (<A|A><E|E>) can be taken at full size."""
+    n = 13
+    circ = C.rz_rx_cphase(n, 3, seed=4)
+    with q.State(n, q.ENC_ADAPTIVE2, P) as a, q.State(n, q.ENC_FP64, P) as e:
+        a.apply_circuit(circ)
+        e.apply_circuit(circ)
+        za, ze = a.get_state(), e.get_state()
+        assert abs(a.overlap(e) - np.vdot(za, ze)) <= 1e-12
+        assert abs(e.overlap(a) - np.vdot(ze, za)) <= 1e-12
+        assert abs(a.overlap(a) - np.vdot(za, za)) <= 1e-12
+        assert abs(e.overlap(e) - 1.0) <= 1e-12
+        fid = abs(a.overlap(e)) ** 2 / (a.overlap(a).real * e.overlap(e).real)
+        assert fid >= 0.95
+    with q.State(n, q.ENC_FP64, 2) as x, q.State(n, q.ENC_FP64, 2) as y:
+        x.apply_gate(C.mat_H(), n - 1)  # exchange: x's qubit map differs from y's
+        with pytest.raises(q.QsimError) as err:
+            x.overlap(y)
+        assert err.value.code == -7
+
+
+def test_config4_fidelity_and_norm_drift_match_the_oracle():
+    """Config 4 recipe, 10 layers, N=16: the A run's fidelity against E and
+    its norm drift equal the oracle-A's (the loss of fidelity with N is a
+    property of the linear magnitude code with exact global bounds, not of
+    the kernels: r1 grows to many times the rms amplitude)."""
+    n = 16
+    circ = C.rz_rx_cphase(n, 10, seed=4)
+    ref = oracle.AState(n).run(circ)
+    zr = ref.decoded()
+    e = oracle.e_simulate(n, circ)
+    f_or = abs(np.vdot(zr, e)) ** 2 / (np.vdot(zr, zr).real * np.vdot(e, e).real)
+    with q.State(n, q.ENC_ADAPTIVE2, 1) as a, q.State(n, q.ENC_FP64, 1) as s:
+        a.apply_circuit(circ)
+        s.apply_circuit(circ)
+        f = abs(a.overlap(s)) ** 2 / (a.overlap(a).real * s.overlap(s).real)
+        nrm = a.norm()
+        _, r0, r1 = a.get_codes()
+    assert abs(f - f_or) <= 2e-3
+    assert abs(nrm - np.vdot(zr, zr).real) <= 2e-3
+    assert r1 == pytest.approx(ref.r1, rel=1e-6)

@@ -475,3 +475,57 @@ def test_small_states_below_256_amplitudes(n):
         assert abs(s.norm() - 1.0) <= 1e-10
         assert np.max(np.abs(s.probabilities() - oracle.e_probabilities(ref, n))) <= TOL
         assert np.max(np.abs(s.expectations() - oracle.e_expectations(ref, n))) <= TOL
+
+
+
+@pytest.mark.parametrize("fuse", [0, 1])
+@pytest.mark.parametrize("P", [1, 2])
+def test_graph_replay_applies_the_captured_circuit(fuse, P):
+    """qsim_graph_*: capturing a config-1 circuit runs nothing; each replay
+    applies the circuit again to the current state (oracle: the circuit
+    applied once, then three times).  P = 2 (loopback shards): the circuit
+    avoids the global qubit, so the capture leaves the map unchanged."""
+    n = 14
+    if P == 1:
+        circ = C.config(0, seed=3)
+    else:
+        circ, sub = C.Circuit(n), C.random_circuit(n - 1, 200, seed=3)
+        for i in range(len(sub)):
+            name, kind, t, t2, ctl, u = sub.gate(i)
+            circ.add(name, u, t, ctl)
+    s = q.State(n, q.ENC_FP64, P, fuse=fuse)
+    g = s.capture(lambda st: st.apply_circuit(circ))
+    assert np.array_equal(s.get_state(), oracle.e_init(n))  # capturing ran nothing
+    g.launch()
+    ref = oracle.e_simulate(n, circ)
+    assert np.max(np.abs(s.get_state() - ref)) <= TOL
+    g.launch()
+    g.launch()
+    for _ in range(2):
+        ref = oracle.e_run(ref.copy(), n, circ)
+    assert np.max(np.abs(s.get_state() - ref)) <= TOL
+    g.close()
+    s.close()
+
+
+def test_graph_capture_rejects_layout_changes_and_readouts():
+    """A capture whose gates move a qubit across the shard boundary (an
+    exchange changes the qubit map) cannot be replayed: EUNSUPPORTED; read-out
+    calls inside a capture: EINVAL; A encoding: EUNSUPPORTED."""
+    n = 12
+    s = q.State(n, q.ENC_FP64, 2)
+    with pytest.raises(q.QsimError) as e:
+        s.capture(lambda st: st.apply_gate(C.mat_H(), n - 1))
+    assert e.value.code == -7
+    s.reset()
+    with pytest.raises(q.QsimError) as e:
+        s.capture(lambda st: st.norm())
+    assert e.value.code == -1
+    s.reset()
+    assert abs(s.norm() - 1.0) <= 1e-15  # the handle is usable after a failed capture
+    s.close()
+    a = q.State(n, q.ENC_ADAPTIVE2, 1)
+    with pytest.raises(q.QsimError) as e:
+        a.capture(lambda st: st.apply_gate(C.mat_H(), 0))
+    assert e.value.code == -7
+    a.close()
