@@ -152,7 +152,6 @@ __device__ void load_asm(ASm &sm, const ATabData *__restrict__ cur, const ATabDa
         sm.degn = nxt->degenerate;
         // fp32 candidate error in steps: |d tf| <= (eps32 (|m| + r0) + |m - m_f|) * scale,
         // bounded by 4e-7 * (r1 + r0) * scale + 1e-3; above 0.5 -> always check
-        // (a_encode2: fp32 copies of (x, y), |z|^2 and rsqrt in fp32: relative error <= 6e-7)
         const double e = 6e-7 * (nxt->r1 + nxt->r0) * nxt->scale + 1e-4;
         sm.mmargin = (float)(e < 0.49 ? e : 0.5);
         sm.scalef = (float)nxt->scale;
@@ -425,34 +424,102 @@ struct ABnd {
     }
 };
 
-// encode with the fp32 candidate computed from fp32 copies of (x, y)
-__device__ __forceinline__ uint32_t a_encode2(const ASm &sm, double2 z) {
-    const double m2 = a_m2(z);
-    const uint32_t h = (uint32_t)__double2hiint(m2);
-    int b0;
-    if (h <= A_ZHI || h >= A_OHI) {  // near or beyond the special thresholds: exact tests
-        if (m2 < A_ZERO2) return pack(-128, 0);
-        if (m2 > A_ONE2) return pack(127, a_angle_code(sm, z));
+
+// ---- fp32 fast path with a certified fallback ------------------------------
+// The dense A gate decides codes and bounds from fp32 copies of the decode
+// tables, of U and of the gate arithmetic, together with a rigorous bound on
+// how far each fp32 output can be from the fp64 reference (a_decode, a_gate2,
+// a_m2 -- the functions the fallback and the oracle's definition use).  A code
+// (or a bounds candidate) is committed from fp32 only when that bound proves
+// the fp64 reference decides the same way; otherwise the pair is recomputed in
+// fp64 exactly as before.  So the result is the fp64 reference's, bit for bit,
+// while most pairs cost fp32 (FMA pipe) instead of fp64 + conversions.
+//
+// Error bound (u = 2^-24): the fp32 decode has |zf - z| <= 3u r per component
+// (table value r, cos / sin and the product each rounded once); one output
+// component is 4 products summed by an fma chain, with |Re u_ij| + |Im u_ij|
+// <= sqrt2: sum_j sqrt2 (3u + u) r_j for the inputs and coefficients plus 4
+// roundings of partial sums <= 4u sqrt2 (r0 + r1) -- in all <= 11.4u (r0 + r1)
+// = 6.8e-7 (r0 + r1).  A_KF = 1e-6 > that, so per output component
+// |xf - x| <= E = A_KF (r0 + r1) with r the pair's decoded magnitudes.
+#define A_KF 1e-6f
+struct ASmF {
+    float rf[256];
+    float2 csf[256];
+    float scalef, r0s, r0f;
+};
+__device__ __forceinline__ void load_asmf(ASmF &f, const ASm &sm) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        f.rf[i] = (float)sm.r[i];
+        f.csf[i] = make_float2((float)sm.cs[i].x, (float)sm.cs[i].y);
     }
-    if (sm.degn) {
-        b0 = 0;
-    } else {
-        const float xf = (float)z.x, yf = (float)z.y;
-        const float m2f = fmaf(xf, xf, yf * yf);
-        const float mf = m2f * rsqrtf(m2f);
-        const float tf = fmaf(mf, sm.scalef, -sm.r0s);
-        int c = __float2int_rn(tf);
-        const float fr = tf - (float)c;
-        c = max(0, min(253, c));
-        if (fabsf(fr) > 0.5f - sm.mmargin) {
-            if (c < 253 && m2 >= sm.thr[c])
-                c += 1;
-            else if (c > 0 && m2 < sm.thr[c - 1])
-                c -= 1;
-        }
-        b0 = c - 127;
+    if (threadIdx.x == 0) {
+        f.scalef = (float)sm.scalen;
+        f.r0s = (float)(sm.r0n * sm.scalen);
+        f.r0f = (float)sm.r0n;
     }
-    return pack(b0, a_angle_code(sm, z));
+    __syncthreads();
+}
+__device__ __forceinline__ float2 a_decode_f(const ASmF &f, uint32_t code, float &r) {
+    r = f.rf[(code & 0xffu) ^ 0x80u];
+    const float2 cs = f.csf[((code >> 8) & 0xffu) ^ 0x80u];
+    return make_float2(r * cs.x, r * cs.y);
+}
+__device__ __forceinline__ void a_gate_f(const float (&u)[8], float2 &x, float2 &y) {
+    const float2 x0 = x, y0 = y;
+    x.x = fmaf(u[0], x0.x, fmaf(-u[1], x0.y, fmaf(u[2], y0.x, -u[3] * y0.y)));
+    x.y = fmaf(u[0], x0.y, fmaf(u[1], x0.x, fmaf(u[2], y0.y, u[3] * y0.x)));
+    y.x = fmaf(u[4], x0.x, fmaf(-u[5], x0.y, fmaf(u[6], y0.x, -u[7] * y0.y)));
+    y.y = fmaf(u[4], x0.y, fmaf(u[5], x0.x, fmaf(u[6], y0.y, u[7] * y0.x)));
+}
+// nearest integer of t (|t| < 2^22) without the conversion unit: k and t - k
+__device__ __forceinline__ int a_rnd(float t, float &fr) {
+    const float m = t + 12582912.0f;  // 1.5 * 2^23
+    fr = t - (m - 12582912.0f);
+    return __float_as_int(m) - 0x4B400000;
+}
+// The code of one fp32 output x (component error bound E); ok = false when
+// the fp32 value cannot decide it.  Branch-free.
+__device__ __forceinline__ uint32_t a_encode_f(const ASm &sm, const ASmF &f, float2 x, float E, bool &ok) {
+    const float m2f = fmaf(x.x, x.x, x.y * x.y);
+    const float rs = rsqrtf(m2f);
+    const float mf = m2f > 0.f ? m2f * rs : 0.f;
+    const float Em = fmaf(1.4143f, E, 4e-7f * mf);  // | |z| - mf |
+    const bool zero = mf + Em < 0.99999e-12f;    // certainly the special zero (reading R-A5)
+    // certainly intermediate, and the direction known to within 1 %
+    const bool inter = (mf - Em > 1.00001e-12f) & (mf + Em < 0.999999f) & (Em < 0.01f * mf);
+    float fr;
+    const float tf = fminf(fmaxf(fmaf(mf, f.scalef, -f.r0s), -2.f), 256.f);
+    const int c = a_rnd(tf, fr);
+    const float errm = fmaf(Em + 1.2e-7f * (mf + f.r0f), f.scalef, 2e-5f);
+    const bool okm = sm.degn || (fabsf(fr) < 0.5f - errm);
+    const int b0 = sm.degn ? 0 : max(0, min(253, c)) - 127;
+    float fa;
+    int k = a_rnd(atan2_steps(x.y, x.x), fa);
+    // direction error <= sqrt(2) E / |z| (|z| >= 0.99 mf) rad, polynomial 1e-5 rad + fp32 rounding
+    const float erra = fmaf(1.4143f * 1.0102f * 40.7437f, E * rs, 6e-4f);
+    const bool oka = fabsf(fa) < 0.5f - erra;
+    k = max(-128, min(128, k));
+    ok = zero | (inter & okm & oka);
+    return zero ? pack(-128, 0) : pack(b0, k == 128 ? -128 : k);
+}
+
+// fp64 reference for the pairs of a unit whose fp32 decision failed (rare;
+// out of line so the hot loop stays small)
+template <int TL>
+__device__ __noinline__ void a_unit_exact(const ASm &sm, const double *u, const uint32_t *c, uint32_t *nc,
+                                          uint32_t fail, uint32_t selm) {
+    double uu[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) uu[i] = u[i];
+    for (int k = 0; k < 8; ++k) {
+        if (!((fail >> k) & 1u)) continue;
+        const int j0 = AUnit<TL>::j0(k), j1 = AUnit<TL>::j1(k);
+        double2 x = a_decode(sm, c[j0]), y = a_decode(sm, c[j1]);
+        if ((selm >> k) & 1u) a_gate2(uu, x, y);
+        nc[j0] = a_encode(sm, x);
+        nc[j1] = a_encode(sm, y);
+    }
 }
 
 template <int TL, bool CTRL>
@@ -602,24 +669,38 @@ __global__ void __launch_bounds__(A_THREADS) k_apply_a(const __grid_constant__ A
     const uint64_t lowm = (1ull << U::LOWB) - 1ull;
     const uint64_t chi = p.cmask & ~lowm;
     const uint32_t cl = (uint32_t)(p.cmask & lowm);
+    __shared__ ASmF f;
+    load_asmf(f, sm);
     double u[8];
+    float uf[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) u[i] = p.u[i];
+    for (int i = 0; i < 8; ++i) {
+        u[i] = p.u[i];
+        uf[i] = (float)p.u[i];
+    }
     for (uint64_t v = (uint64_t)blockIdx.x * A_THREADS + threadIdx.x; v < units; v += (uint64_t)gridDim.x * A_THREADS) {
         uint32_t c[16];
         const uint64_t s0 = U::s0(v, p.t);
         U::load(a, s0, p.t, c);
         const bool hi_ok = !CTRL || (((p.shard_base | s0) & chi) == chi);
+        uint32_t nc[16], fail = 0, selm = 0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const int j0 = U::j0(k), j1 = U::j1(k);
-            double2 x = a_decode(sm, c[j0]), y = a_decode(sm, c[j1]);
             const int off = TL < 4 ? j0 : k;
-            if (!CTRL || (hi_ok && ((uint32_t)off & cl) == cl)) a_gate2(u, x, y);
-            c[j0] = a_encode2(sm, x);
-            c[j1] = a_encode2(sm, y);
+            const bool sel = !CTRL || (hi_ok && ((uint32_t)off & cl) == cl);
+            selm |= (uint32_t)sel << k;
+            float ra, rb;
+            float2 xf = a_decode_f(f, c[j0], ra), yf = a_decode_f(f, c[j1], rb);
+            if (sel) a_gate_f(uf, xf, yf);
+            const float E = A_KF * (ra + rb);
+            bool okx, oky;
+            nc[j0] = a_encode_f(sm, f, xf, E, okx);
+            nc[j1] = a_encode_f(sm, f, yf, E, oky);
+            fail |= (uint32_t)!(okx && oky) << k;
         }
-        U::store(a, s0, p.t, c);
+        if (fail) a_unit_exact<TL>(sm, u, c, nc, fail, selm);
+        U::store(a, s0, p.t, nc);
     }
 }
 
