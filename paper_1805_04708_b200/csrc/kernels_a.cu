@@ -749,27 +749,52 @@ struct AFastParams {
     int32_t k0, k1;  // DIAG: b1 steps for bit 0 / 1; ANTI: k0 = steps of u01, k1 = steps of u10
 };
 
-// diagonal: per code, 8 codes per thread
-__global__ void __launch_bounds__(A_THREADS) k_diag_a(const __grid_constant__ AFastParams p) {
+// Diagonal gates visit only the 16-byte vectors (8 codes) that hold touched
+// codes: the touched set is "control bits = 1" plus, when one diagonal entry
+// has no phase step (CPHASE, S, T, Z ...: k0 = 0), "target bit = 1" -- the
+// fixed bits at or above bit 3 are inserted into the vector index (like the E
+// sweep), those below bit 3 select lanes.  b1 += k (mod 256) for the
+// touched codes, the special zero keeps b1 = 0; b0 never changes.
+struct ADiagParams {
+    void *a;
+    uint64_t nvec;      // vectors visited
+    uint64_t orv;       // vector-index bits fixed to 1
+    int32_t ins[4];     // vector-index positions of the fixed bits (ascending)
+    int32_t nins;
+    uint32_t lowmask, lowval;  // fixed bits of the lane index (code bits 0..2)
+    int32_t tlow;       // target bit < 3 (lane bit), else -1
+    int32_t tvec;       // target bit >= 3 and not fixed: vector-index bit, else -1
+    int32_t tconst;     // target bit value when it is neither (fixed or global)
+    int32_t k0, k1;
+};
+__device__ __forceinline__ uint32_t shift_b1_fast(uint32_t code, uint32_t k8) {
+    const uint32_t moved = (code & 0xffu) | ((code + k8) & 0xff00u);
+    return (code & 0xffu) == 0x80u ? code : moved;
+}
+__global__ void __launch_bounds__(A_THREADS) k_diag_a(const __grid_constant__ ADiagParams p) {
     uint16_t *a = reinterpret_cast<uint16_t *>(p.a);
-    const uint64_t nvec = p.n >> 3;
-    for (uint64_t v = (uint64_t)blockIdx.x * A_THREADS + threadIdx.x; v < nvec; v += (uint64_t)gridDim.x * A_THREADS) {
-        uint4 w = *reinterpret_cast<uint4 *>(a + (v << 3));
-        uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    const uint32_t k08 = (uint32_t)p.k0 << 8, k18 = (uint32_t)p.k1 << 8;
+    for (uint64_t w = (uint64_t)blockIdx.x * A_THREADS + threadIdx.x; w < p.nvec; w += (uint64_t)gridDim.x * A_THREADS) {
+        uint64_t v = w;
+        for (int q = 0; q < p.nins; ++q) v = a_ins0(v, p.ins[q]);
+        v |= p.orv;
+        uint4 x = __ldcs(reinterpret_cast<const uint4 *>(a + (v << 3)));
+        uint32_t ws[4] = {x.x, x.y, x.z, x.w};
+        const uint32_t tv = p.tvec >= 0 ? (uint32_t)(v >> p.tvec) & 1u : (uint32_t)p.tconst;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const uint64_t full = p.shard_base | ((v << 3) + k);
-            if ((full & p.cmask) != p.cmask) continue;
-            const int st = ((full >> p.t) & 1ull) ? p.k1 : p.k0;
-            uint32_t c = (k & 1) ? (ws[k >> 1] >> 16) : (ws[k >> 1] & 0xffffu);
-            c = shift_b1(c, st);
-            ws[k >> 1] = (k & 1) ? ((ws[k >> 1] & 0xffffu) | (c << 16)) : ((ws[k >> 1] & 0xffff0000u) | c);
+        for (int j = 0; j < 8; ++j) {
+            if (((uint32_t)j & p.lowmask) != p.lowval) continue;
+            const uint32_t bit = p.tlow >= 0 ? ((uint32_t)j >> p.tlow) & 1u : tv;
+            const uint32_t k8 = bit ? k18 : k08;
+            const uint32_t c = (j & 1) ? (ws[j >> 1] >> 16) : (ws[j >> 1] & 0xffffu);
+            const uint32_t n = shift_b1_fast(c, k8);
+            ws[j >> 1] = (j & 1) ? ((ws[j >> 1] & 0xffffu) | (n << 16)) : ((ws[j >> 1] & 0xffff0000u) | n);
         }
-        w.x = ws[0];
-        w.y = ws[1];
-        w.z = ws[2];
-        w.w = ws[3];
-        *reinterpret_cast<uint4 *>(a + (v << 3)) = w;
+        x.x = ws[0];
+        x.y = ws[1];
+        x.z = ws[2];
+        x.w = ws[3];
+        __stcs(reinterpret_cast<uint4 *>(a + (v << 3)), x);
     }
 }
 
@@ -806,9 +831,43 @@ void launch_fast_a(const AGateParams &g, const ATables *t, cudaStream_t s) {
     p.t = g.t;
     p.cls = g.cls;
     if (g.cls == CLS_DIAG) {
-        p.k0 = phase_steps(g.u[0], g.u[1]);
-        p.k1 = phase_steps(g.u[6], g.u[7]);
-        k_diag_a<<<a_grid(p.n >> 3), A_THREADS, 0, s>>>(p);
+        const int k0 = phase_steps(g.u[0], g.u[1]), k1 = phase_steps(g.u[6], g.u[7]);
+        const int nl = g.nl >= 3 ? g.nl : 3;  // shards are padded to >= 256 codes (zero specials)
+        const uint64_t lmask = (nl >= 64) ? ~0ull : ((1ull << nl) - 1ull);
+        uint64_t fixed = g.cmask & lmask, val = fixed;  // global controls: checked by the caller
+        ADiagParams d{};
+        d.a = g.a;
+        d.k0 = k0;
+        d.k1 = k1;
+        d.tlow = d.tvec = -1;
+        if (g.t >= g.nl) {  // global target: one step for the whole shard
+            d.tconst = (int)((g.shard_base >> g.t) & 1ull);
+            if ((d.tconst ? k1 : k0) == 0) return;
+        } else if (k0 == 0 || k1 == 0) {  // only one value of the target bit moves
+            if (k0 == 0 && k1 == 0) return;
+            fixed |= 1ull << g.t;
+            if (k1 != 0) val |= 1ull << g.t;
+            d.tconst = k1 != 0 ? 1 : 0;
+        } else if (g.t < 3) {
+            d.tlow = g.t;
+        } else {
+            d.tconst = 0;
+        }
+        d.lowmask = (uint32_t)(fixed & 7u);
+        d.lowval = (uint32_t)(val & 7u);
+        int nf = 0;
+        for (int b = 3; b < nl; ++b)
+            if ((fixed >> b) & 1ull) {
+                d.ins[nf++] = b - 3;
+                if ((val >> b) & 1ull) d.orv |= 1ull << (b - 3);
+            }
+        d.nins = nf;
+        if (g.t >= 3 && g.t < nl && !((fixed >> g.t) & 1ull)) {
+            d.tvec = g.t - 3;  // bit of the (inserted) vector index
+        }
+        d.nvec = (1ull << (nl - 3)) >> nf;
+        k_diag_a<<<a_grid(d.nvec), A_THREADS, 0, s>>>(d);
+        return;
     } else {
         p.k0 = phase_steps(g.u[2], g.u[3]);
         p.k1 = phase_steps(g.u[4], g.u[5]);
