@@ -372,16 +372,25 @@ const char *qsim_last_error(void);
  *     diagonal gate and its permutation part only relabels which shard holds
  *     which global bits -- no data moves (PAPER.md:389-392 does this for
  *     SWAP; CNOT "can be implemented without having to exchange data",
- *     P:395-400).
+ *     P:395-400), or
+ *   QSIM_OP_REMAP: one (global bit `g`, local bit `l`) pair of a
+ *     simultaneous swap of m >= 2 global bits with m local bits (SURVEY.md
+ *     §8(f) NEXT-1 (i)); the m consecutive REMAP ops with the same
+ *     gate_index form ONE all-to-all: every shard trades 2^nl (1 - 2^-m)
+ *     amplitudes with the 2^m - 1 shards that differ from it in those global
+ *     bits, instead of m pairwise half-shard exchanges (m/2 of a shard).  The
+ *     planner emits it when the gate that needs a global target is followed,
+ *     within 2N gates, by non-diagonal gates on other global targets.
  * Ownership: qsim_plan_create allocates *out, qsim_plan_destroy frees it. */
 #define QSIM_OP_EXCHANGE 0
 #define QSIM_OP_GATE 1
 #define QSIM_OP_RELABEL 2
+#define QSIM_OP_REMAP 3
 typedef struct qsim_plan qsim_plan;
 typedef struct qsim_plan_op {
     int32_t type;        /* QSIM_OP_* */
-    int32_t g;           /* EXCHANGE: global physical bit */
-    int32_t l;           /* EXCHANGE: local victim bit; GATE: physical target bit */
+    int32_t g;           /* EXCHANGE / REMAP: global physical bit */
+    int32_t l;           /* EXCHANGE / REMAP: local victim bit; GATE: physical target bit */
     int32_t cls;         /* GATE: matrix class */
     int32_t ncontrols;   /* GATE */
     int32_t controls[2]; /* GATE: physical control bits */

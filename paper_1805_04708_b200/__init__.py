@@ -38,6 +38,7 @@ GATE_SWAP = 1
 OP_EXCHANGE = 0
 OP_GATE = 1
 OP_RELABEL = 2  # permutation gate on global bits: shard relabelling, no data movement
+OP_REMAP = 3  # one (g, l) pair of a multi-bit all-to-all remap (consecutive ops, same gate_index)
 
 
 class QsimError(RuntimeError):

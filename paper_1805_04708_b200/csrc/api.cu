@@ -881,6 +881,98 @@ static int exchange(qsim_state *s, const PlanOp &x, const PlanOp *gop, const dou
     return QSIM_OK;
 }
 
+// All-to-all remap (planner QSIM_OP_REMAP group, remap.cu): m (global g_i,
+// local l_i) pairs swapped at once.  Shard phi trades its block B(t) (l bits
+// = t) with block B(phi[j]) of the shard phi with j bits := t, for every
+// t != phi[j].  The qubit map was updated by the planner.
+static int remap(qsim_state *s, std::vector<std::pair<int, int>> pairs) {
+    std::sort(pairs.begin(), pairs.end(), [](const std::pair<int, int> &x, const std::pair<int, int> &y) {
+        return x.second < y.second;  // by local bit
+    });
+    const int m = (int)pairs.size();
+    RemapBlock blk{};
+    blk.m = m;
+    int jb[8];
+    for (int i = 0; i < m; ++i) {
+        blk.pos[i] = pairs[i].second;
+        jb[i] = pairs[i].first - s->nl;
+    }
+    const uint64_t nblock = 1ull << (s->nl - m);
+    const size_t ab = s->amp_bytes;
+    auto jval = [&](uint32_t phi) {  // phi's j bits as a block value
+        uint32_t v = 0;
+        for (int i = 0; i < m; ++i) v |= ((phi >> jb[i]) & 1u) << i;
+        return v;
+    };
+    auto with_j = [&](uint32_t phi, uint32_t t) {
+        for (int i = 0; i < m; ++i) phi = (phi & ~(1u << jb[i])) | (((t >> i) & 1u) << jb[i]);
+        return phi;
+    };
+    const uint32_t nt = 1u << m;
+    if (s->transport == QSIM_TRANSPORT_LOCAL) {
+        prof_begin(s);
+        for (auto &sa : s->shards) {
+            const uint32_t pa = shard_phys(s, sa), ta = jval(pa);
+            for (uint32_t t = 0; t < nt; ++t) {
+                if (t == ta) continue;
+                const uint32_t idxb = s->ginv[with_j(pa, t)];
+                if (idxb < (uint32_t)sa.index) continue;  // each pair once
+                Shard *sb = nullptr;
+                for (auto &x : s->shards)
+                    if ((uint32_t)x.index == idxb) sb = &x;
+                launch_blockswap(sa.amps, sb->amps, nblock, blk, t, ta, ab, s->stream);
+                s->st.kernels++;
+                s->st.hbm_bytes += 4.0 * (double)nblock * ab;
+            }
+            s->st.exchange_bytes += (double)(nt - 1) * (double)nblock * ab;
+        }
+        prof_end(s, QSIM_K_XCHG, 2.0 * (double)s->P * (double)(nt - 1) * (double)nblock * ab);
+        s->st.exchanges++;
+        CU(cudaGetLastError());
+        return QSIM_OK;
+    }
+    // ---- NCCL: one shard per process; every chunk round trades one slice of
+    // each of the 2^m - 1 blocks with its partner (grouped sends / receives)
+    Shard &sh = s->shards[0];
+    const uint32_t pa = shard_phys(s, sh), ta = jval(pa);
+    uint64_t C = 1;
+    while (C * 2 * (nt - 1) <= s->chunk_amps && C * 2 <= nblock) C *= 2;
+    const uint64_t nch = nblock / C;
+    char *sendb = (char *)s->stage[0], *recvb = (char *)s->stage[1];
+    prof_begin(s);
+    for (uint64_t c = 0; c < nch; ++c) {
+        int slot = 0;
+        for (uint32_t t = 0; t < nt; ++t) {
+            if (t == ta) continue;
+            launch_pack(sh.amps, sendb + (size_t)slot * C * ab, c * C, C, blk, t, ab, s->stream);
+            ++slot;
+        }
+        NC(ncclGroupStart());
+        slot = 0;
+        for (uint32_t t = 0; t < nt; ++t) {
+            if (t == ta) continue;
+            const int peer = (int)s->ginv[with_j(pa, t)];
+            NC(ncclSend(sendb + (size_t)slot * C * ab, C * ab, ncclUint8, peer, s->comm, s->stream));
+            NC(ncclRecv(recvb + (size_t)slot * C * ab, C * ab, ncclUint8, peer, s->comm, s->stream));
+            ++slot;
+        }
+        NC(ncclGroupEnd());
+        slot = 0;
+        for (uint32_t t = 0; t < nt; ++t) {
+            if (t == ta) continue;
+            launch_unpack(sh.amps, recvb + (size_t)slot * C * ab, c * C, C, blk, t, ab, s->stream);
+            ++slot;
+        }
+        s->st.kernels += 2 * (nt - 1);
+        s->st.hbm_bytes += 4.0 * (double)(nt - 1) * (double)C * ab;
+    }
+    prof_end(s, QSIM_K_XCHG, 2.0 * (double)(nt - 1) * (double)nblock * ab);
+    s->st.exchange_bytes += (double)(nt - 1) * (double)nblock * ab;
+    s->st.exchanges++;
+    CU(cudaGetLastError());
+    return QSIM_OK;
+}
+
 // ============================================================================
 // executor
 // ============================================================================
@@ -922,6 +1014,18 @@ static int execute(qsim_state *s, const qsim_gate *gates, size_t ngates, const s
                 if (on) s->gphys[r] ^= tb;
             }
             for (int r = 0; r < s->P; ++r) s->ginv[s->gphys[r]] = (uint32_t)r;
+            continue;
+        }
+        if (o.type == QSIM_OP_REMAP) {
+            RC(flush());
+            std::vector<std::pair<int, int>> pairs;
+            size_t k = i;
+            while (k < ops.size() && ops[k].type == QSIM_OP_REMAP && ops[k].gate_index == o.gate_index) {
+                pairs.push_back({ops[k].g, ops[k].l});
+                ++k;
+            }
+            i = k - 1;
+            RC(remap(s, pairs));
             continue;
         }
         if (o.type == QSIM_OP_EXCHANGE) {
@@ -1137,6 +1241,7 @@ int qsim_create_ex(const qsim_config *cfg, qsim_state **out) {
     }
     cudaGetDevice(&s->dev);
     s->pl.init(n, P, nullptr);
+    s->pl.remap = getenv("QSIM_NO_REMAP") == nullptr;  // all-to-all remaps (NEXT-1 (i)); off: pairwise only
     int rc = QSIM_OK;
     auto fail = [&](int code) {
         qsim_destroy(s);

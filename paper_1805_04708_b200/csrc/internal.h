@@ -32,6 +32,7 @@ struct Planner {
     int n = 0, nl = 0;
     std::vector<int> pos, inv;  // logical -> physical bit, physical -> logical
     bool relabel_global = true; // permutation gates on global bits only -> QSIM_OP_RELABEL
+    bool remap = true;          // several global targets ahead -> one all-to-all (QSIM_OP_REMAP)
     void init(int n_, int nshards, const int *initial_map);
     // Appends the ops for gates[0..ngates) to `ops` and updates the map.
     // `lookahead` enables Belady victim selection over the remaining gates.

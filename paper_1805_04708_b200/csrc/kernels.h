@@ -128,6 +128,23 @@ struct XchgParams {
 };
 void launch_xchg_e(const XchgParams &p, cudaStream_t s);
 
+// ---- all-to-all remap (remap.cu, NEXT-1 (i)) ---------------------------------
+// A block of a shard: the elements whose local bits pos[0] < ... < pos[m-1]
+// equal the bits of a value v (bit i of v at pos[i]); element x of the block
+// is the x-th such index in increasing order.
+struct RemapBlock {
+    int32_t m;
+    int32_t pos[8];
+};
+// swap block va of shard a with block vb of shard b (same device), nblock elements each
+void launch_blockswap(void *a, void *b, uint64_t nblock, const RemapBlock &blk, uint32_t va, uint32_t vb,
+                      size_t elem, cudaStream_t s);
+// elements [base, base + count) of block v of src -> out[0 .. count), and back
+void launch_pack(const void *src, void *out, uint64_t base, uint64_t count, const RemapBlock &blk, uint32_t v,
+                 size_t elem, cudaStream_t s);
+void launch_unpack(void *dst, const void *in, uint64_t base, uint64_t count, const RemapBlock &blk, uint32_t v,
+                   size_t elem, cudaStream_t s);
+
 // ---- reductions (a10) ---------------------------------------------------------
 // Per-shard: out[0] = sum |a|^2, out[1 + q] = sum_{bit q = 1} |a|^2 for local q.
 constexpr int RED_SLOTS = 64;

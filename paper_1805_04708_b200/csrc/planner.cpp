@@ -9,6 +9,7 @@
 // indices".  Swaps are never undone ("defers swaps").
 // Diagonal gates never exchange: their phase depends only on index bits,
 // rank bits included.  Controls on global bits become a per-shard predicate.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -164,10 +165,50 @@ void Planner::plan(const qsim_gate *gates, size_t ngates, std::vector<PlanOp> &o
             }
         }
         if (pt >= nl && cls != CLS_DIAG) {
-            int avoid[2];
+            int avoid[2 + 64];
             int navoid = 0;
             for (int c = 0; c < x.ncontrols; ++c)
                 if (pos[x.controls[c]] < nl) avoid[navoid++] = pos[x.controls[c]];
+            // NEXT-1 (i): the other global bits that non-diagonal gates will
+            // target within the next 2N gates join this exchange as one
+            // all-to-all (m bits: 1 - 2^-m of a shard per GPU instead of m/2)
+            int gl[64];
+            int m = 0;
+            gl[m++] = pt;
+            if (remap && n - nl >= 2) {
+                const size_t end = std::min(ngates, g + 1 + 2 * (size_t)n);
+                for (size_t h = g + 1; h < end && m < n - nl; ++h) {
+                    const qsim_gate &y = gates[h];
+                    if (y.kind == QSIM_GATE_SWAP) break;  // relabels: stop looking (rare)
+                    const int32_t yc = classify(y.u);
+                    if (yc == CLS_DIAG || yc == CLS_IDENT) continue;
+                    const int py = pos[y.target];
+                    if (py < nl) continue;
+                    bool allg = yc == CLS_ANTI && relabel_global;  // would relabel: no data moves
+                    for (int c = 0; c < y.ncontrols && allg; ++c) allg = pos[y.controls[c]] >= nl;
+                    if (allg) continue;
+                    bool dup = false;
+                    for (int i = 0; i < m; ++i) dup = dup || gl[i] == py;
+                    if (!dup) gl[m++] = py;
+                }
+            }
+            if (m >= 2) {
+                int lv[64];
+                for (int i = 0; i < m; ++i) {
+                    lv[i] = choose_victim(gates, ngates, g, avoid, navoid, lookahead);
+                    avoid[navoid++] = lv[i];
+                }
+                for (int i = 0; i < m; ++i) {
+                    PlanOp e{};
+                    e.type = QSIM_OP_REMAP;
+                    e.g = gl[i];
+                    e.l = lv[i];
+                    e.gate_index = (int32_t)g;
+                    ops.push_back(e);
+                }
+                for (int i = 0; i < m; ++i) swap_bits(gl[i], lv[i]);
+                pt = pos[x.target];
+            } else {
             int l = choose_victim(gates, ngates, g, avoid, navoid, lookahead);
             PlanOp e{};
             e.type = QSIM_OP_EXCHANGE;
@@ -177,6 +218,7 @@ void Planner::plan(const qsim_gate *gates, size_t ngates, std::vector<PlanOp> &o
             ops.push_back(e);
             swap_bits(pt, l);
             pt = l;
+            }
         }
         PlanOp o{};
         o.type = QSIM_OP_GATE;

@@ -60,7 +60,7 @@ def _apply_plan_numpy(n, P, circ, ops, final_map):
     v[0] = 1
     idx = np.arange(1 << n)
     for o in ops:
-        if o["type"] == q.OP_EXCHANGE:
+        if o["type"] in (q.OP_EXCHANGE, q.OP_REMAP):  # a REMAP group = disjoint bit transpositions
             g, l = o["g"], o["l"]
             assert g >= nl and l < nl
             bg, bl = (idx >> g) & 1, (idx >> l) & 1
@@ -103,9 +103,38 @@ def test_planner_plan_reproduces_the_circuit(P):
     circ.swap(0, n - 1)
     circ.extend(C.global_permutations(n, P, seed=P + 1))
     ops, fmap = q.qsim_plan(n, P, circ)
-    nex = sum(o["type"] == q.OP_EXCHANGE for o in ops)
+    nex = sum(o["type"] in (q.OP_EXCHANGE, q.OP_REMAP) for o in ops)
     assert nex > 0
     assert sum(o["type"] == q.OP_RELABEL for o in ops) > 0
+    if P >= 4:  # the layered part targets every global qubit: one all-to-all remap
+        assert sum(o["type"] == q.OP_REMAP for o in ops) >= 2
+    got = _apply_plan_numpy(n, P, circ, ops, fmap)
+    assert np.max(np.abs(got - oracle.e_simulate(n, circ))) <= 1e-12
+
+
+@pytest.mark.parametrize("P", [4, 8])
+def test_planner_remap_groups(P):
+    """Config-3 recipe: every layer hits all log2(P) global qubits with dense
+    gates; the planner swaps them in with one all-to-all per layer (REMAP
+    groups of m = log2(P) disjoint (global, local) pairs, distinct bits, the
+    gate that triggered it then local), and the plan reproduces the circuit."""
+    import oracle
+
+    n = 12
+    k = int(np.log2(P))
+    circ = C.layered(n, 3, seed=3)
+    ops, fmap = q.qsim_plan(n, P, circ)
+    nl = n - k
+    groups = {}
+    for o in ops:
+        if o["type"] == q.OP_REMAP:
+            groups.setdefault(o["gate_index"], []).append((o["g"], o["l"]))
+    nx = sum(o["type"] == q.OP_EXCHANGE for o in ops)
+    assert len(groups) >= 3 and len(groups) > nx
+    for gi, pairs in groups.items():
+        gs, ls = [p[0] for p in pairs], [p[1] for p in pairs]
+        assert 2 <= len(pairs) <= k and len(set(gs)) == len(gs) and all(nl <= x < n for x in gs)
+        assert len(set(ls)) == len(ls) and all(x < nl for x in ls)
     got = _apply_plan_numpy(n, P, circ, ops, fmap)
     assert np.max(np.abs(got - oracle.e_simulate(n, circ))) <= 1e-12
 

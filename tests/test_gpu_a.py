@@ -259,3 +259,21 @@ def test_config4_fidelity_and_norm_drift_match_the_oracle():
     assert abs(f - f_or) <= 2e-3
     assert abs(nrm - np.vdot(zr, zr).real) <= 2e-3
     assert r1 == pytest.approx(ref.r1, rel=1e-6)
+
+
+def test_all_to_all_remap_is_bit_exact_in_a():
+    """A codes after a circuit whose plan holds all-to-all remaps (P = 4, 8
+    loopback shards) equal the single-shard run's bit for bit: remaps only
+    move codes, bounds are global."""
+    n = 13
+    circ = C.layered(n, 2, seed=7)
+    circ.extend(C.rz_rx_cphase(n, 2, seed=7))
+    out = []
+    for P in (1, 4, 8):
+        ops, _ = q.qsim_plan(n, P, circ)
+        assert P == 1 or sum(o["type"] == q.OP_REMAP for o in ops) > 0
+        with q.State(n, q.ENC_ADAPTIVE2, P) as s:
+            s.apply_circuit(circ)
+            out.append(s.get_codes())
+    for c, r0, r1 in out[1:]:
+        assert np.array_equal(c, out[0][0]) and r0 == out[0][1] and r1 == out[0][2]

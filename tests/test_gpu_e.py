@@ -113,8 +113,18 @@ def test_sharded_loopback_transparency(P):
     assert np.max(np.abs(got - ref)) <= TOL
     st = s.stats()
     assert st["exchanges"] > 0
-    # exchange volume: half a shard per direction per shard per exchange
-    assert st["exchange_bytes"] == pytest.approx(st["exchanges"] * (1 << (n - int(math.log2(P)) - 1)) * 16 * 2)
+    # exchange volume: a pairwise exchange moves half a shard per direction per
+    # shard; an m-bit all-to-all remap moves 1 - 2^-m of every shard
+    nl = n - int(math.log2(P))
+    ops, _ = q.qsim_plan(n, P, circ)
+    npair = sum(o["type"] == q.OP_EXCHANGE for o in ops)
+    groups = {}
+    for o in ops:
+        if o["type"] == q.OP_REMAP:
+            groups[o["gate_index"]] = groups.get(o["gate_index"], 0) + 1
+    want = npair * P * (1 << (nl - 1)) * 16
+    want += sum(P * ((1 << m) - 1) * (1 << (nl - m)) * 16 for m in groups.values())
+    assert st["exchange_bytes"] == pytest.approx(want)
     pe = s.expectations()
     qe = oracle.e_expectations(ref, n)
     assert np.max(np.abs(pe - qe)) <= TOL
@@ -529,3 +539,25 @@ def test_graph_capture_rejects_layout_changes_and_readouts():
         a.capture(lambda st: st.apply_gate(C.mat_H(), 0))
     assert e.value.code == -7
     a.close()
+
+
+@pytest.mark.parametrize("P", [4, 8])
+def test_all_to_all_remap_loopback(P, monkeypatch):
+    """NEXT-1 (i): a config-3 shaped circuit (every layer hits all global
+    qubits with dense gates) on P loopback shards: the plan holds all-to-all
+    remaps; the state equals the oracle's, and the remaps move fewer bytes
+    than the pairwise exchanges of the same circuit (QSIM_NO_REMAP=1)."""
+    n = 14
+    circ = C.layered(n, 3, seed=3)
+    ref = oracle.e_simulate(n, circ)
+    with q.State(n, q.ENC_FP64, P) as s:
+        s.apply_circuit(circ)
+        assert np.max(np.abs(s.get_state() - ref)) <= TOL
+        st = s.stats()
+    monkeypatch.setenv("QSIM_NO_REMAP", "1")
+    with q.State(n, q.ENC_FP64, P) as s:
+        s.apply_circuit(circ)
+        assert np.max(np.abs(s.get_state() - ref)) <= TOL
+        st0 = s.stats()
+    assert st["exchanges"] < st0["exchanges"]
+    assert st["exchange_bytes"] < st0["exchange_bytes"]
