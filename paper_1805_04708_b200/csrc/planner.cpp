@@ -11,6 +11,7 @@
 // rank bits included.  Controls on global bits become a per-shard predicate.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 
@@ -253,6 +254,7 @@ int qsim_plan_create(int n_qubits, int nshards, const int *initial_map, const qs
         qsim::set_error("qsim_plan_create: no local qubits");
         return QSIM_EINVAL;
     }
+    p->pl.remap = getenv("QSIM_NO_REMAP") == nullptr;  // same switch as qsim_create
     p->pl.plan(gates, ngates, p->ops, true);
     *out = p;
     return QSIM_OK;
