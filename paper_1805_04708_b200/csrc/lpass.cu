@@ -225,6 +225,27 @@ __device__ __forceinline__ void lp_preflip(uint32_t &g, const LOp &o, uint32_t x
     }
 }
 
+// the lifted shears of a ROUND op on the register bits in mask (ascending),
+// coefficients (t, a) pairs at sp
+template <int R>
+__device__ __forceinline__ void lp_lifts(double2 (&v)[1 << R], uint32_t g, uint32_t mask, const double *sp) {
+    constexpr int NS = 1 << R;
+    int k = 0;
+#define LP_ROUND_BIT(RB)                                                          \
+    if constexpr ((RB) < R) {                                                     \
+        if ((mask >> (RB)) & 1u) {                                                \
+            const double t = sp[2 * k], aa = sp[2 * k + 1];                       \
+            ++k;                                                                  \
+            if ((g >> (RB)) & 1u)                                                 \
+                lp_lift<NS, ((RB) < R ? (RB) : 0), true>(v, t, aa);               \
+            else                                                                  \
+                lp_lift<NS, ((RB) < R ? (RB) : 0), false>(v, t, aa);              \
+        }                                                                         \
+    }
+    LP_ROUND_BIT(0) LP_ROUND_BIT(1) LP_ROUND_BIT(2) LP_ROUND_BIT(3) LP_ROUND_BIT(4)
+#undef LP_ROUND_BIT
+}
+
 // One op of the stage program on one register group (v, g: its register
 // values and flip vector; xq: its logical tile bits outside the registers).
 template <int R>
@@ -241,22 +262,7 @@ __device__ __forceinline__ void lp_op1(double2 (&v)[1 << R], uint32_t &g, uint32
     const uint32_t toff = lp_toff<R>(h, o, xq, full, cpool_off);
     if (code == LOP_CODE_ROUND) {
         lp_table<NS>(v, smem_raw, toff | (g << 4));
-        const uint32_t mask = (uint32_t)(h >> 24) & 0xffu;
-        const double *sp = p.sc + o.pm;
-        int k = 0;
-#define LP_ROUND_BIT(RB)                                                          \
-    if constexpr ((RB) < R) {                                                     \
-        if ((mask >> (RB)) & 1u) {                                                \
-            const double t = sp[2 * k], aa = sp[2 * k + 1];                       \
-            ++k;                                                                  \
-            if ((g >> (RB)) & 1u)                                                 \
-lp_lift<NS, ((RB) < R ? (RB) : 0), true>(v, t, aa);               \
-            else                                                                  \
-lp_lift<NS, ((RB) < R ? (RB) : 0), false>(v, t, aa);              \
-        }                                                                         \
-    }
-        LP_ROUND_BIT(0) LP_ROUND_BIT(1) LP_ROUND_BIT(2) LP_ROUND_BIT(3) LP_ROUND_BIT(4)
-#undef LP_ROUND_BIT
+        lp_lifts<R>(v, g, (uint32_t)(h >> 24) & 0xffu, p.sc + o.pm);
         return;
     }
     if (code == LOP_CODE_DIAGT) {
@@ -514,9 +520,18 @@ __global__ void __launch_bounds__(LP_THREADS, MINB) k_lpass_e(const __grid_const
                 __syncthreads();
                 continue;
             }
+            // group bits 0..6 = this thread's index (LP_THREADS = 128): their
+            // address / logical parts once per stage; bits >= 7 per group below
+            uint32_t a0t = 0, xqt = yrest;
+#pragma unroll
+            for (int i = 0; i < 7; ++i)
+                if (i < K - R && ((tid >> i) & 1u)) {
+                    a0t ^= (uint32_t)st.grp_phys[i] << 4;
+                    xqt ^= st.grp_log[i];
+                }
             for (uint32_t grp = tid; grp < ngroups; grp += LP_THREADS) {
-                uint32_t a0 = 0, xq = yrest;
-                for (int i = 0; i < K - R; ++i)
+                uint32_t a0 = a0t, xq = nxq ? xqt : yrest;
+                for (int i = 7; i < K - R; ++i)
                     if ((grp >> i) & 1u) {
                         a0 ^= (uint32_t)st.grp_phys[i] << 4;
                         if (nxq) xq ^= st.grp_log[i];
@@ -534,7 +549,7 @@ __global__ void __launch_bounds__(LP_THREADS, MINB) k_lpass_e(const __grid_const
                 const uint64_t *oph = reinterpret_cast<const uint64_t *>(p.op);
                 uint64_t hn = op0 < op1 ? oph[op0 * (sizeof(LOp) / 8)] : 0;
                 for (int oi = op0; oi < op1; ++oi) {
-                    const uint64_t h = hn;  // header: code | flags | rowS | gvec | coef | nvariants
+                    const uint64_t h = hn;  // header: code | flags | rowS | gvec | coef | nvariants | simple
                     if (oi + 1 < op1) hn = oph[(oi + 1) * (sizeof(LOp) / 8)];
                     lp_op1<R>(v, g, xq, full, h, p.op[oi], p, smem_raw, cpool_off);
                 }

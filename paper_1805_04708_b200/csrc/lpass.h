@@ -100,7 +100,7 @@ struct LOp {
     uint8_t rowS;      // row S of A: bit S of sigma(j) = par(rowS & (j ^ g))
     uint8_t gvec;      // FLIP: A^-1 e_t;  ROUND: register bits sheared
     uint16_t coef;     // DIAGT / ROUND: table offset in coef[]; SHEAR*/DENSE: offset in sc[]
-    uint8_t nctl;      // in-register controls (CSHEAR / DENSE / CSWAP)
+    uint8_t nctl;      // in-register controls (CSHEAR / DENSE / CSWAP); DIAGT / ROUND: table variants
     uint8_t pad0;
     uint32_t pm;       // bit j = par(rowS & j) (SHEARU: bit 0 = the uniform parity; ROUND: offset in sc[])
     uint32_t pmc[2];   // the same for each in-register control row
