@@ -104,6 +104,7 @@ typedef struct qsim_stats {
     double gate_bytes;        /* sum over gates of the per-gate algorithmic bytes had each run alone */
     double exchange_bytes;    /* bytes sent per direction by this process's shards */
     int64_t stages;           /* register stages summed over fused passes */
+    int64_t jit_passes;       /* fused passes run by a run-time specialised kernel (the rest interpreted) */
 } qsim_stats;
 
 /* ---- lifetime ---------------------------------------------------------- */
@@ -320,6 +321,15 @@ int qsim_profile_read(qsim_state *s, qsim_kernel_profile *out, int max, int *nou
 
 /* Wait for all work of this handle. */
 int qsim_sync(qsim_state *s);
+
+/* The fused pass runs a compiled gate program either in the interpreter
+ * kernel or in a kernel specialised to that program (NVRTC, sm_100a, cached
+ * per program shape, compiled in background threads; the two run the same
+ * device functions, so results do not depend on which ran).  This call
+ * waits until every specialisation queued so far has been compiled (or has
+ * failed: such programs keep running interpreted).  QSIM_LPASS_JIT = 0 / 1
+ * (default) / 2 selects off / background / compile-at-first-launch. */
+int qsim_jit_sync(void);
 
 /* ---- CUDA graphs of a gate sequence (the
  * latency-bound N=14 circuit with "per-gate launch, a CUDA Graph, and a

@@ -63,7 +63,7 @@ class qsim_stats(ctypes.Structure):
     _fields_ = [("gates", ctypes.c_int64), ("kernels", ctypes.c_int64), ("sweeps", ctypes.c_int64),
                 ("passes", ctypes.c_int64), ("fused_gates", ctypes.c_int64), ("exchanges", ctypes.c_int64),
                 ("hbm_bytes", ctypes.c_double), ("gate_bytes", ctypes.c_double),
-                ("exchange_bytes", ctypes.c_double), ("stages", ctypes.c_int64)]
+                ("exchange_bytes", ctypes.c_double), ("stages", ctypes.c_int64), ("jit_passes", ctypes.c_int64)]
 
 
 class qsim_kernel_profile(ctypes.Structure):
@@ -91,7 +91,7 @@ EXPORTS = (
     "qsim_aux_amplitudes", "qsim_aux_num_vars", "qsim_set_qubit_map",
     "qsim_asm_parse", "qsim_asm_info", "qsim_asm_get_op", "qsim_asm_destroy", "qsim_asm_run",
     "qsim_asm_result_get", "qsim_asm_result_destroy",
-    "qsim_overlap", "qsim_graph_begin", "qsim_graph_end", "qsim_graph_launch", "qsim_graph_destroy",
+    "qsim_overlap", "qsim_jit_sync", "qsim_graph_begin", "qsim_graph_end", "qsim_graph_launch", "qsim_graph_destroy",
 )
 
 if not os.path.exists(_LIB_PATH):
@@ -144,6 +144,7 @@ _lib.qsim_get_codes.argtypes = [_P, ctypes.POINTER(ctypes.c_int8), _dp, _dp]
 _lib.qsim_set_codes.argtypes = [_P, ctypes.POINTER(ctypes.c_int8), ctypes.c_double, ctypes.c_double]
 _lib.qsim_sync.argtypes = [_P]
 _lib.qsim_overlap.argtypes = [_P, _P, _dp]
+_lib.qsim_jit_sync.argtypes = []
 _lib.qsim_graph_begin.argtypes = [_P]
 _lib.qsim_graph_end.argtypes = [_P, ctypes.POINTER(_P)]
 _lib.qsim_graph_launch.argtypes = [_P, _P]
@@ -428,6 +429,11 @@ def qsim_set_codes(h, codes, r0, r1):
 
 def qsim_sync(h):
     _check(_lib.qsim_sync(h))
+
+
+def qsim_jit_sync():
+    """Wait for the queued run-time specialisations of the fused pass (qsim_jit_sync)."""
+    _check(_lib.qsim_jit_sync())
 
 
 def qsim_overlap(ha, hb) -> complex:

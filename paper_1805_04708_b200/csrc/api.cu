@@ -679,7 +679,7 @@ struct LaunchSink : LPassSink {
             for (int id : ids)
                 if (id >= 0) fl += gate_flops(s, sh, (*run)[id], (*us)[id]);
             prof_begin(s);
-            launch_lpass_e(q, s->stream);
+            s->st.jit_passes += launch_lpass_e(q, s->stream);
             prof_end(s, QSIM_K_PASS, std::ldexp(2.0 * (double)s->amp_bytes, s->nl), fl);
             s->st.kernels++;
             s->st.passes++;
@@ -1425,6 +1425,11 @@ int qsim_profile_read(qsim_state *s, qsim_kernel_profile *out, int max, int *nou
     for (int c = 0; c < QSIM_K_NUM && k < max; ++c)
         if (agg[c].launches) out[k++] = agg[c];
     if (nout) *nout = k;
+    return QSIM_OK;
+}
+
+int qsim_jit_sync(void) {
+    lpass_jit_sync();
     return QSIM_OK;
 }
 

@@ -1,0 +1,431 @@
+// lpass_dev.cuh -- device code of the relabelling tile pass (lpass.h): the
+// op semantics (exactly those of the host emulator tools/lpass_emu.cpp) and
+// the kernel body.  Included by lpass.cu (the interpreter kernel) and, as
+// source text, by the run-time specialised kernels NVRTC compiles (lpass.cu,
+// lpass_jit_*): both run the same device functions.
+#pragma once
+
+#include "lpass_types.h"
+
+namespace qsim {
+
+__device__ __forceinline__ uint64_t lp_ins0(uint64_t w, int p) {
+    return ((w >> p) << (p + 1)) | (w & ((1ull << p) - 1ull));
+}
+__device__ __forceinline__ uint32_t lp_par(uint32_t x) { return __popc(x) & 1u; }
+__host__ __device__ constexpr int lp_ctz5(int i) { return (i & 1) ? 0 : (i & 2) ? 1 : (i & 4) ? 2 : (i & 8) ? 3 : 4; }
+__host__ __device__ constexpr int lp_hibit(int v) { return v >= 16 ? 4 : v >= 8 ? 3 : v >= 4 ? 2 : v >= 2 ? 1 : 0; }
+
+__device__ __forceinline__ void lp_cp_async16(void *smem, const void *gmem) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void lp_cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// x' = x - t y, y' = y + t x  (2 FMAs per amplitude component)
+__device__ __forceinline__ void lp_shear_pair(double2 &x, double2 &y, double t) {
+    const double2 x0 = x;
+    x.x = fma(-t, y.x, x.x);
+    x.y = fma(-t, y.y, x.y);
+    y.x = fma(t, x0.x, y.x);
+    y.y = fma(t, x0.y, y.y);
+}
+
+template <int NS, int V>
+__device__ __forceinline__ void lp_shearu(double2 (&v)[NS], double te) {
+    constexpr int HB = lp_hibit(V);
+#pragma unroll
+    for (int j0 = 0; j0 < NS; ++j0) {
+        if (j0 & (1 << HB)) continue;
+        lp_shear_pair(v[j0], v[j0 ^ V], te);
+    }
+}
+template <int NS, int V>
+__device__ __forceinline__ void lp_shear(double2 (&v)[NS], double t, uint32_t pm, uint32_t gp) {
+    constexpr int HB = lp_hibit(V);
+    const uint32_t q = pm ^ (gp ? 0xffffffffu : 0u);
+#pragma unroll
+    for (int j0 = 0; j0 < NS; ++j0) {
+        if (j0 & (1 << HB)) continue;
+        const double te = ((q >> j0) & 1u) ? -t : t;
+        lp_shear_pair(v[j0], v[j0 ^ V], te);
+    }
+}
+// per-pair control predicate: all in-register controls of sigma(j0) are 1
+__device__ __forceinline__ uint32_t lp_ctl_mask(const LOp &o, uint32_t g) {
+    uint32_t m = 0xffffffffu;
+    const int nc = o.nctl;
+    if (nc > 0) m &= o.pmc[0] ^ (lp_par(o.rowc[0] & g) ? 0xffffffffu : 0u);
+    if (nc > 1) m &= o.pmc[1] ^ (lp_par(o.rowc[1] & g) ? 0xffffffffu : 0u);
+    return m;  // bit j0 = 1 iff the pair at j0 is selected
+}
+template <int NS, int V>
+__device__ __forceinline__ void lp_cshear(double2 (&v)[NS], double t, uint32_t pm, uint32_t gp, uint32_t cm) {
+    constexpr int HB = lp_hibit(V);
+    const uint32_t q = pm ^ (gp ? 0xffffffffu : 0u);
+#pragma unroll
+    for (int j0 = 0; j0 < NS; ++j0) {
+        if (j0 & (1 << HB)) continue;
+        double te = ((q >> j0) & 1u) ? -t : t;
+        te = ((cm >> j0) & 1u) ? te : 0.0;
+        lp_shear_pair(v[j0], v[j0 ^ V], te);
+    }
+}
+template <int NS, int V>
+__device__ __forceinline__ void lp_dense(double2 (&v)[NS], const double2 *u, uint32_t pm, uint32_t gp, uint32_t cm) {
+    constexpr int HB = lp_hibit(V);
+    const uint32_t q = pm ^ (gp ? 0xffffffffu : 0u);
+    const double2 a = u[0], b = u[1], c = u[2], d = u[3];
+#pragma unroll
+    for (int j0 = 0; j0 < NS; ++j0) {
+        if (j0 & (1 << HB)) continue;
+        if (!((cm >> j0) & 1u)) continue;
+        // register j0 holds the logical-1 member when the bit is set: apply X U X
+        const bool s = (q >> j0) & 1u;
+        const double2 e00 = s ? d : a, e01 = s ? c : b, e10 = s ? b : c, e11 = s ? a : d;
+        const double2 x = v[j0], y = v[j0 ^ V];
+        v[j0] = make_double2(e00.x * x.x - e00.y * x.y + e01.x * y.x - e01.y * y.y,
+                             e00.x * x.y + e00.y * x.x + e01.x * y.y + e01.y * y.x);
+        v[j0 ^ V] = make_double2(e10.x * x.x - e10.y * x.y + e11.x * y.x - e11.y * y.y,
+                                 e10.x * x.y + e10.y * x.x + e11.x * y.y + e11.y * y.x);
+    }
+}
+template <int NS, int V>
+__device__ __forceinline__ void lp_cswap(double2 (&v)[NS], uint32_t cm) {
+    constexpr int HB = lp_hibit(V);
+#pragma unroll
+    for (int j0 = 0; j0 < NS; ++j0) {
+        if (j0 & (1 << HB)) continue;
+        const bool s = (cm >> j0) & 1u;
+        const double2 x = v[j0], y = v[j0 ^ V];
+        v[j0] = s ? y : x;
+        v[j0 ^ V] = s ? x : y;
+    }
+}
+
+struct LPSmem {
+    size_t tile, cpool, total;
+};
+// tables sit right after the tile: both offsets are multiples of a table's
+// size (2^R x 16 B), so entry j ^ g of a table is at (base + g*16) ^ (j*16)
+__host__ __device__ inline LPSmem lp_smem(int K, int ncoef) {
+    LPSmem L;
+    L.tile = 0;
+    L.cpool = ((size_t)1 << K) * 16;
+    L.total = L.cpool + (size_t)((ncoef + 1) & ~1) * 8;
+    return L;
+}
+
+// lifted shear on register bit r (L D U factorisation, D already applied by
+// the table): logical x += a y; y += t x -- every FMA writes its own input
+template <int NS, int RB, bool FLIP>
+__device__ __forceinline__ void lp_lift(double2 (&v)[NS], double t, double a) {
+    // all x updates first, then all y updates: dependent FMAs NS/2 apart
+#pragma unroll
+    for (int j0 = 0; j0 < NS; ++j0) {
+        if (j0 & (1 << RB)) continue;
+        double2 &x = FLIP ? v[j0 | (1 << RB)] : v[j0];
+        const double2 &y = FLIP ? v[j0] : v[j0 | (1 << RB)];
+        x.x = fma(a, y.x, x.x);
+        x.y = fma(a, y.y, x.y);
+    }
+#pragma unroll
+    for (int j0 = 0; j0 < NS; ++j0) {
+        if (j0 & (1 << RB)) continue;
+        const double2 &x = FLIP ? v[j0 | (1 << RB)] : v[j0];
+        double2 &y = FLIP ? v[j0] : v[j0 | (1 << RB)];
+        y.x = fma(t, x.x, y.x);
+        y.y = fma(t, x.y, y.y);
+    }
+}
+
+// v[j] *= T[j ^ g]; tb = byte offset of the table in shared memory + 16 g
+template <int NS>
+__device__ __forceinline__ void lp_table(double2 (&v)[NS], const unsigned char *smem, uint32_t tb) {
+    // chunks of 8 entries: bounded register pressure, loads still ahead of the math
+    constexpr int CH = NS < 8 ? NS : 8;
+#pragma unroll
+    for (int j0 = 0; j0 < NS; j0 += CH) {
+        double2 c[CH];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) c[j] = *reinterpret_cast<const double2 *>(smem + (tb ^ (uint32_t)((j0 + j) << 4)));
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+            const double p = c[j].y * v[j0 + j].y, q = c[j].y * v[j0 + j].x;
+            v[j0 + j].x = fma(c[j].x, v[j0 + j].x, -p);
+            v[j0 + j].y = fma(c[j].x, v[j0 + j].y, q);
+        }
+    }
+}
+
+// tile load (cp.async) / store of the NJ = 2^(K-7) elements of this thread:
+// logical x = tid + 128 j, j in Gray-code order (one column changes per step)
+template <int NJ>
+__device__ __forceinline__ void lp_tile_load(unsigned char *smem, const char *gp, uint32_t so, const uint32_t *s_hi,
+                                             const uint64_t *d_hi) {
+    uint64_t dj = 0;
+#pragma unroll
+    for (int i = 0; i < NJ; ++i) {
+        if (i) {
+            so ^= s_hi[lp_ctz5(i)];
+            dj ^= d_hi[lp_ctz5(i)];
+        }
+        lp_cp_async16(smem + so, gp + dj);
+    }
+}
+template <int NJ>
+__device__ __forceinline__ void lp_tile_store(const unsigned char *smem, char *gp, uint32_t mo, const uint32_t *m_hi,
+                                              const uint64_t *d_hi) {
+    uint64_t dj = 0;
+#pragma unroll
+    for (int i = 0; i < NJ; ++i) {
+        if (i) {
+            mo ^= m_hi[lp_ctz5(i)];
+            dj ^= d_hi[lp_ctz5(i)];
+        }
+        *reinterpret_cast<double2 *>(gp + dj) = *reinterpret_cast<const double2 *>(smem + mo);
+    }
+}
+
+// table variant offset (bytes in shared memory) of a group: the group's
+// values of up to 2 condition bits select among the op's consecutive tables
+template <int R>
+__device__ __forceinline__ uint32_t lp_toff(uint64_t h, const LOp &o, uint32_t xq, uint64_t full, uint32_t cpool_off) {
+    uint32_t toff = cpool_off + (uint32_t)((h >> 32) & 0xffffu) * 8u;
+    const uint32_t nv = (uint32_t)(h >> 48) & 0xffu;
+    if (nv) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+            if (i < (int)nv) {
+                const uint32_t c = o.rowc[i];
+                const uint32_t bit = c < 64 ? (xq >> c) & 1u : (uint32_t)(full >> (c - 64)) & 1u;
+                toff += bit << (i + R + 4);
+            }
+    }
+    return toff;
+}
+
+// flips folded into a table op (compiler): g ^= gvec where the condition bit is 1
+__device__ __forceinline__ void lp_preflip(uint32_t &g, const LOp &o, uint32_t xq, uint64_t full) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const uint32_t f = o.pmc[k];
+        if (!(f >> 16)) break;
+        const uint32_t c = (f >> 8) & 255u;
+        const uint32_t bit = c == 255u ? 1u : c < 64u ? (xq >> c) & 1u : (uint32_t)(full >> (c - 64u)) & 1u;
+        g ^= bit ? (f & 255u) : 0u;
+    }
+}
+
+// the lifted shears of a ROUND op on the register bits in mask (ascending),
+// coefficients (t, a) pairs at sp
+template <int R>
+__device__ __forceinline__ void lp_lifts(double2 (&v)[1 << R], uint32_t g, uint32_t mask, const double *sp) {
+    constexpr int NS = 1 << R;
+    int k = 0;
+#define LP_ROUND_BIT(RB)                                                          \
+    if constexpr ((RB) < R) {                                                     \
+        if ((mask >> (RB)) & 1u) {                                                \
+            const double t = sp[2 * k], aa = sp[2 * k + 1];                       \
+            ++k;                                                                  \
+            if ((g >> (RB)) & 1u)                                                 \
+                lp_lift<NS, ((RB) < R ? (RB) : 0), true>(v, t, aa);               \
+            else                                                                  \
+                lp_lift<NS, ((RB) < R ? (RB) : 0), false>(v, t, aa);              \
+        }                                                                         \
+    }
+    LP_ROUND_BIT(0) LP_ROUND_BIT(1) LP_ROUND_BIT(2) LP_ROUND_BIT(3) LP_ROUND_BIT(4)
+#undef LP_ROUND_BIT
+}
+
+// One op of the stage program on one register group (v, g: its register
+// values and flip vector; xq: its logical tile bits outside the registers).
+template <int R>
+__device__ __forceinline__ void lp_op1(double2 (&v)[1 << R], uint32_t &g, uint32_t xq, uint64_t full, uint64_t h,
+                                       const LOp &o, const LPassParams &p, const unsigned char *smem_raw,
+                                       uint32_t cpool_off) {
+    constexpr int NS = 1 << R;
+    const uint32_t code = (uint32_t)h & 0xffu;
+    const uint32_t coef = (uint32_t)(h >> 32) & 0xffffu;
+    if ((h >> 8) & LF_COND) {
+        if (((xq & o.tmask) != o.tval) || ((full & o.omask) != o.oval)) return;
+    }
+    if (code == LOP_CODE_ROUND || code == LOP_CODE_DIAGT) lp_preflip(g, o, xq, full);
+    const uint32_t toff = lp_toff<R>(h, o, xq, full, cpool_off);
+    if (code == LOP_CODE_ROUND) {
+        lp_table<NS>(v, smem_raw, toff | (g << 4));
+        lp_lifts<R>(v, g, (uint32_t)(h >> 24) & 0xffu, p.sc + o.pm);
+        return;
+    }
+    if (code == LOP_CODE_DIAGT) {
+        lp_table<NS>(v, smem_raw, toff | (g << 4));
+        return;
+    }
+    if (code == LOP_CODE_FLIP) {
+        g ^= (uint32_t)(h >> 24) & 0xffu;
+        return;
+    }
+    const uint32_t gp = lp_par(((uint32_t)(h >> 16) & 0xffu) & g);
+    switch (code) {
+#define LP_V_CASES(VS)                                                                                    \
+    case LOP_SHEARU * 16 + (VS):                                                                          \
+        if constexpr ((VS) < lp_nv(R)) {                                                                  \
+            const double t = p.sc[coef];                                                                  \
+            lp_shearu<NS, lp_vec(R, (VS))>(v, ((o.pm ^ gp) & 1u) ? -t : t);                               \
+        }                                                                                                 \
+        break;                                                                                            \
+    case LOP_SHEAR * 16 + (VS):                                                                           \
+        if constexpr ((VS) < lp_nv(R)) lp_shear<NS, lp_vec(R, (VS))>(v, p.sc[coef], o.pm, gp);             \
+        break;
+#define LP_W1_CASES(VS)                                                                                   \
+    case LOP_CSHEAR * 16 + (VS):                                                                          \
+        if constexpr ((VS) < R) lp_cshear<NS, (1 << (VS))>(v, p.sc[coef], o.pm, gp, lp_ctl_mask(o, g));    \
+        break;                                                                                            \
+    case LOP_DENSE * 16 + (VS):                                                                           \
+        if constexpr ((VS) < R)                                                                           \
+            lp_dense<NS, (1 << (VS))>(v, reinterpret_cast<const double2 *>(p.sc + coef), o.pm, gp,        \
+                      lp_ctl_mask(o, g));                                                 \
+        break;                                                                                            \
+    case LOP_CSWAP * 16 + (VS):                                                                           \
+        if constexpr ((VS) < R) lp_cswap<NS, (1 << (VS))>(v, lp_ctl_mask(o, g));                          \
+        break;
+        LP_V_CASES(0) LP_V_CASES(1) LP_V_CASES(2) LP_V_CASES(3) LP_V_CASES(4)
+        LP_V_CASES(5) LP_V_CASES(6) LP_V_CASES(7) LP_V_CASES(8) LP_V_CASES(9)
+        LP_V_CASES(10) LP_V_CASES(11) LP_V_CASES(12) LP_V_CASES(13) LP_V_CASES(14)
+        LP_W1_CASES(0) LP_W1_CASES(1) LP_W1_CASES(2) LP_W1_CASES(3) LP_W1_CASES(4)
+#undef LP_V_CASES
+#undef LP_W1_CASES
+        default:
+            break;
+    }
+}
+
+// The pass kernel body.  `ops(s, v, g, xq, full, p, smem, cpool_off)` applies
+// the ops of stage s to one register group; the interpreter (lpass.cu,
+// LpInterp) walks the program, a run-time specialised kernel (NVRTC, the same
+// lp_op1 calls with literal headers) switches on s.  Everything else --
+// tile load / store, group addressing, stage round trips -- is this code.
+template <int R, class Ops>
+__device__ __forceinline__ void lp_body(const LPassParams &p, const Ops &ops) {
+    constexpr int NS = 1 << R;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int K = p.K;
+    const LPSmem L = lp_smem(K, p.ncoef);
+    double *cpool = reinterpret_cast<double *>(smem_raw + L.cpool);
+    const uint32_t cpool_off = (uint32_t)L.cpool;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t ngroups = 1u << (K - R);
+    // ---- one-time setup per CTA ----
+    for (int i = tid; i < p.ncoef; i += LP_THREADS) cpool[i] = p.coef[i];
+    // load / store addressing: logical x = tid + 128 j; smem byte offset of x
+    // at load = XOR of scol over its bits (store: smcol, plus S b); HBM offset
+    // = deposit of its bits.  Bits 0..6 are this thread's, bits 7.. come from j.
+    uint32_t s_tid = 0, m_tid = 0;
+    uint64_t d_tid = tid & 7u;
+#pragma unroll
+    for (int i = 0; i < 7; ++i)
+        if ((tid >> i) & 1u) {
+            s_tid ^= (uint32_t)p.scol[i] << 4;
+            m_tid ^= (uint32_t)p.smcol[i] << 4;
+            if (i >= LP_LOW) d_tid |= 1ull << p.high_q[i - LP_LOW];
+        }
+    uint32_t s_hi[5], m_hi[5];
+    uint64_t d_hi[5];
+#pragma unroll
+    for (int b = 0; b < 5; ++b) {
+        const bool on = 7 + b < K;
+        s_hi[b] = on ? (uint32_t)p.scol[7 + b] << 4 : 0u;
+        m_hi[b] = on ? (uint32_t)p.smcol[7 + b] << 4 : 0u;
+        d_hi[b] = on ? (16ull << p.high_q[7 + b - LP_LOW]) : 0ull;  // bytes
+    }
+    __syncthreads();
+    double2 *__restrict__ a = reinterpret_cast<double2 *>(p.a);
+
+    for (uint64_t T = blockIdx.x; T < p.ntiles; T += gridDim.x) {
+        uint64_t base = T << LP_LOW;
+        for (int i = 0; i < K - LP_LOW; ++i) base = lp_ins0(base, p.high_q[i]);
+        const uint64_t full = p.shard_base | base;
+        uint32_t fired = 0;
+        for (int e = 0; e < p.nevents; ++e)
+            if ((full & p.ev_full[e]) == p.ev_full[e]) fired |= 1u << e;
+        // ---- load the tile: logical x = tid + 128 j at S x ----
+        if (!p.noio) {
+            const char *gp = reinterpret_cast<const char *>(a + (base | d_tid));
+            switch (K) {
+                case 12: lp_tile_load<32>(smem_raw, gp, s_tid, s_hi, d_hi); break;
+                case 11: lp_tile_load<16>(smem_raw, gp, s_tid, s_hi, d_hi); break;
+                case 10: lp_tile_load<8>(smem_raw, gp, s_tid, s_hi, d_hi); break;
+                default: lp_tile_load<4>(smem_raw, gp, s_tid, s_hi, d_hi); break;
+            }
+        }
+        lp_cp_async_wait_all();
+        __syncthreads();
+        // ---- register stages ----
+        for (int s = 0; s < p.nstages; ++s) {
+            const LStage &st = p.st[s];
+            uint32_t y = st.y_static;
+            for (uint32_t m = fired & st.ev_mask; m; m &= m - 1) y ^= st.y_ev[__ffs(m) - 1];
+            uint32_t g0 = 0;
+#pragma unroll
+            for (int r = 0; r < R; ++r) g0 |= ((y >> st.qbit[r]) & 1u) << r;
+            const uint32_t yrest = y & ~(uint32_t)st.qmask;
+            uint32_t rp[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) rp[r] = (uint32_t)st.reg_phys[r] << 4;
+            const bool nxq = st.needs_xq;
+            // group bits 0..6 = this thread's index (LP_THREADS = 128): their
+            // address / logical parts once per stage; bits >= 7 per group below
+            uint32_t a0t = 0, xqt = yrest;
+#pragma unroll
+            for (int i = 0; i < 7; ++i)
+                if (i < K - R && ((tid >> i) & 1u)) {
+                    a0t ^= (uint32_t)st.grp_phys[i] << 4;
+                    xqt ^= st.grp_log[i];
+                }
+            for (uint32_t grp = tid; grp < ngroups; grp += LP_THREADS) {
+                uint32_t a0 = a0t, xq = nxq ? xqt : yrest;
+                for (int i = 7; i < K - R; ++i)
+                    if ((grp >> i) & 1u) {
+                        a0 ^= (uint32_t)st.grp_phys[i] << 4;
+                        if (nxq) xq ^= st.grp_log[i];
+                    }
+                double2 v[NS];
+#pragma unroll
+                for (int j = 0; j < NS; ++j) {
+                    uint32_t ad = a0;
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        if (j & (1 << r)) ad ^= rp[r];
+                    v[j] = *reinterpret_cast<const double2 *>(smem_raw + ad);
+                }
+                uint32_t g = g0;
+                ops(s, v, g, xq, full, p, smem_raw, cpool_off);
+#pragma unroll
+                for (int j = 0; j < NS; ++j) {
+                    uint32_t ad = a0;
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        if (j & (1 << r)) ad ^= rp[r];
+                    *reinterpret_cast<double2 *>(smem_raw + ad) = v[j];
+                }
+            }
+            __syncthreads();
+        }
+        // ---- store: logical x = tid + 128 j from S (M x ^ b) ----
+        uint32_t sbt = p.sb_static;
+        for (uint32_t m = fired; m; m &= m - 1) sbt ^= p.sv_ev[__ffs(m) - 1];
+        if (!p.noio) {
+            char *gp = reinterpret_cast<char *>(a + (base | d_tid));
+            const uint32_t mo = m_tid ^ (sbt << 4);
+            switch (K) {
+                case 12: lp_tile_store<32>(smem_raw, gp, mo, m_hi, d_hi); break;
+                case 11: lp_tile_store<16>(smem_raw, gp, mo, m_hi, d_hi); break;
+                case 10: lp_tile_store<8>(smem_raw, gp, mo, m_hi, d_hi); break;
+                default: lp_tile_store<4>(smem_raw, gp, mo, m_hi, d_hi); break;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace qsim

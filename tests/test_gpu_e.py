@@ -561,3 +561,33 @@ def test_all_to_all_remap_loopback(P, monkeypatch):
         st0 = s.stats()
     assert st["exchanges"] < st0["exchanges"]
     assert st["exchange_bytes"] < st0["exchange_bytes"]
+
+
+def _run_n22(mode, tmp_path):
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = str(tmp_path / f"state_{mode}.npy")
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); import paper_1805_04708_b200 as q, qsim_inputs as C; "
+            "n = 22; s = q.State(n, q.ENC_FP64, 1); s.apply_circuit(C.layered(n, 3, seed=1)); st = s.stats(); "
+            "np.save(%r, s.get_state()); print(st['jit_passes'], st['passes'])" % (root, out))
+    env = dict(os.environ, QSIM_LPASS_JIT=str(mode))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    jit, passes = (int(x) for x in r.stdout.split()[-2:])
+    return np.load(out), jit, passes
+
+
+def test_specialised_pass_kernels_match_the_interpreter_and_the_oracle(tmp_path):
+    """The run-time specialised pass kernels (NVRTC, QSIM_LPASS_JIT=2: compiled
+    before their first launch) run every pass of a config-2 shaped circuit at
+    N = 22 (1024 tiles); the state equals the interpreter's (QSIM_LPASS_JIT=0)
+    and the oracle's."""
+    a, jit, passes = _run_n22(2, tmp_path)
+    b, jit0, passes0 = _run_n22(0, tmp_path)
+    assert passes > 0 and jit == passes and jit0 == 0 and passes0 == passes
+    assert np.max(np.abs(a - b)) <= 1e-14
+    ref = oracle.e_simulate(22, C.layered(22, 3, seed=1))
+    assert np.max(np.abs(a - ref)) <= TOL
