@@ -1379,4 +1379,66 @@ int lpass_run(const LGate *gates, int ng, const LRunConfig &cfg, LPassSink &sink
     return 0;
 }
 
+// The specialised kernel: the tile's stages in order, each an lp_stage call
+// with the stage as a literal LStage and a functor holding its ops as literal
+// LOps (lp_op1 folds to straight-line code); the tile width is a template
+// constant.
+std::string lpass_jit_source(const LPassParams &p, int R, int minb) {
+    std::string s;
+    s.reserve(8192);
+    s += "#include \"lpass_dev.cuh\"\n";
+    char buf[640];
+    for (int st = 0; st < p.nstages; ++st) {
+        snprintf(buf, sizeof buf,
+                 "template <int R>\nstruct JitOps%d {\n  __device__ __forceinline__ void operator()(double2 (&v)[1 << R], "
+                 "uint32_t &g, uint32_t xq, uint64_t full, const qsim::LPassParams &p, const unsigned char *smem, "
+                 "uint32_t cpool_off) const {\n",
+                 st);
+        s += buf;
+        for (int i = p.st[st].first_op; i < p.st[st].first_op + p.st[st].nops; ++i) {
+            // the whole op as a literal: conditions, parities, pre-flips and
+            // coefficient offsets fold into the code
+            const LOp &o = p.op[i];
+            uint64_t h;
+            std::memcpy(&h, &o, 8);
+            snprintf(buf, sizeof buf,
+                     "    { constexpr qsim::LOp o{%u, %u, %u, %u, %u, %u, %u, %uu, {%uu, %uu}, {%u, %u}, 0, %u, %u, 0, "
+                     "0x%llxull, 0x%llxull};\n",
+                     o.code, o.flags, o.rowS, o.gvec, o.coef, o.nctl, o.pad0, o.pm, o.pmc[0], o.pmc[1], o.rowc[0],
+                     o.rowc[1], o.tmask, o.tval, (unsigned long long)o.omask, (unsigned long long)o.oval);
+            s += buf;
+            snprintf(buf, sizeof buf, "      qsim::lp_op1<R>(v, g, xq, full, 0x%016llxull, o, p, smem, cpool_off); }\n",
+                     (unsigned long long)h);
+            s += buf;
+        }
+        s += "  }\n};\n";
+    }
+    s += "struct JitStages {\n  const qsim::LPassParams &p;\n  __device__ __forceinline__ void operator()(const "
+         "qsim::LpTile &t) const {\n";
+    for (int st = 0; st < p.nstages; ++st) {
+        const LStage &S = p.st[st];
+        std::string ev = "{";
+        for (int e = 0; e < LP_MAX_EVENTS; ++e) ev += std::to_string(S.y_ev[e]) + (e + 1 < LP_MAX_EVENTS ? "," : "}");
+        snprintf(buf, sizeof buf,
+                 "    { constexpr qsim::LStage S{{%u,%u,%u,%u,%u}, {%u,%u,%u,%u,%u,%u,%u,%u}, {%u,%u,%u,%u,%u,%u,%u,%u}, "
+                 "%u, %u, {%u,%u,%u,%u,%u}, %u, %u, %u, %uu, ",
+                 S.reg_phys[0], S.reg_phys[1], S.reg_phys[2], S.reg_phys[3], S.reg_phys[4], S.grp_phys[0],
+                 S.grp_phys[1], S.grp_phys[2], S.grp_phys[3], S.grp_phys[4], S.grp_phys[5], S.grp_phys[6],
+                 S.grp_phys[7], S.grp_log[0], S.grp_log[1], S.grp_log[2], S.grp_log[3], S.grp_log[4], S.grp_log[5],
+                 S.grp_log[6], S.grp_log[7], S.y_static, S.qmask, S.qbit[0], S.qbit[1], S.qbit[2], S.qbit[3],
+                 S.qbit[4], S.needs_xq, S.first_op, S.nops, S.ev_mask);
+        s += buf;
+        s += ev + "};\n";
+        snprintf(buf, sizeof buf, "      qsim::lp_stage<%d, %d>(p, t, S, JitOps%d<%d>{}); }\n", R, p.K, st, R);
+        s += buf;
+    }
+    s += "  }\n};\n";
+    snprintf(buf, sizeof buf,
+             "extern \"C\" __global__ void __launch_bounds__(%d, %d) k_lpass_jit(const __grid_constant__ "
+             "qsim::LPassParams p) { qsim::lp_body<%d, %d>(p, JitStages{p}); }\n",
+             LP_THREADS, minb, R, p.K);
+    s += buf;
+    return s;
+}
+
 }  // namespace qsim

@@ -300,21 +300,85 @@ __device__ __forceinline__ void lp_op1(double2 (&v)[1 << R], uint32_t &g, uint32
     }
 }
 
-// The pass kernel body.  `ops(s, v, g, xq, full, p, smem, cpool_off)` applies
-// the ops of stage s to one register group; the interpreter (lpass.cu,
-// LpInterp) walks the program, a run-time specialised kernel (NVRTC, the same
-// lp_op1 calls with literal headers) switches on s.  Everything else --
-// tile load / store, group addressing, stage round trips -- is this code.
-template <int R, class Ops>
-__device__ __forceinline__ void lp_body(const LPassParams &p, const Ops &ops) {
+// Per-tile context of the stage loop.
+struct LpTile {
+    unsigned char *smem_raw;
+    uint64_t full;    // full physical index of the tile's base
+    uint32_t fired;   // events of this tile
+    uint32_t cpool_off;
+};
+
+// One register stage: every group of 2^R amplitudes (a coset of the stage's
+// register basis) is loaded from shared memory, `ops(v, g, xq, full, p,
+// smem, cpool_off)` applies the stage's ops, and it is stored back.  KK: the
+// tile width when known at compile time (0: p.K).
+template <int R, int KK, class Ops>
+__device__ __forceinline__ void lp_stage(const LPassParams &p, const LpTile &t, const LStage &st, const Ops &ops) {
     constexpr int NS = 1 << R;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int K = p.K;
-    const LPSmem L = lp_smem(K, p.ncoef);
-    double *cpool = reinterpret_cast<double *>(smem_raw + L.cpool);
-    const uint32_t cpool_off = (uint32_t)L.cpool;
+    const int K = KK ? KK : p.K;
     const uint32_t tid = threadIdx.x;
     const uint32_t ngroups = 1u << (K - R);
+    unsigned char *smem_raw = t.smem_raw;
+    uint32_t y = st.y_static;
+    for (uint32_t m = t.fired & st.ev_mask; m; m &= m - 1) y ^= st.y_ev[__ffs(m) - 1];
+    uint32_t g0 = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) g0 |= ((y >> st.qbit[r]) & 1u) << r;
+    const uint32_t yrest = y & ~(uint32_t)st.qmask;
+    uint32_t rp[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) rp[r] = (uint32_t)st.reg_phys[r] << 4;
+    const bool nxq = st.needs_xq;
+    // group bits 0..6 = this thread's index (LP_THREADS = 128): their
+    // address / logical parts once per stage; bits >= 7 per group below
+    uint32_t a0t = 0, xqt = yrest;
+#pragma unroll
+    for (int i = 0; i < 7; ++i)
+        if (i < K - R && ((tid >> i) & 1u)) {
+            a0t ^= (uint32_t)st.grp_phys[i] << 4;
+            xqt ^= st.grp_log[i];
+        }
+    for (uint32_t grp = tid; grp < ngroups; grp += LP_THREADS) {
+        uint32_t a0 = a0t, xq = nxq ? xqt : yrest;
+        for (int i = 7; i < K - R; ++i)
+            if ((grp >> i) & 1u) {
+                a0 ^= (uint32_t)st.grp_phys[i] << 4;
+                if (nxq) xq ^= st.grp_log[i];
+            }
+        double2 v[NS];
+#pragma unroll
+        for (int j = 0; j < NS; ++j) {
+            uint32_t ad = a0;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (j & (1 << r)) ad ^= rp[r];
+            v[j] = *reinterpret_cast<const double2 *>(smem_raw + ad);
+        }
+        uint32_t g = g0;
+        ops(v, g, xq, t.full, p, smem_raw, t.cpool_off);
+#pragma unroll
+        for (int j = 0; j < NS; ++j) {
+            uint32_t ad = a0;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (j & (1 << r)) ad ^= rp[r];
+            *reinterpret_cast<double2 *>(smem_raw + ad) = v[j];
+        }
+    }
+    __syncthreads();
+}
+
+// The pass kernel body.  `stages(t)` runs the register stages of one tile
+// (lp_stage per stage): the interpreter (lpass.cu) walks p.st / p.op, a
+// run-time specialised kernel (NVRTC) calls lp_stage with literal stages and
+// ops.  Everything else -- tile load / store, addressing -- is this code.
+template <int R, int KK, class Stages>
+__device__ __forceinline__ void lp_body(const LPassParams &p, const Stages &stages) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int K = KK ? KK : p.K;
+    const LPSmem L = lp_smem(K, p.ncoef);
+    double *cpool = reinterpret_cast<double *>(smem_raw + L.cpool);
+    const uint32_t tid = threadIdx.x;
     // ---- one-time setup per CTA ----
     for (int i = tid; i < p.ncoef; i += LP_THREADS) cpool[i] = p.coef[i];
     // load / store addressing: logical x = tid + 128 j; smem byte offset of x
@@ -344,10 +408,13 @@ __device__ __forceinline__ void lp_body(const LPassParams &p, const Ops &ops) {
     for (uint64_t T = blockIdx.x; T < p.ntiles; T += gridDim.x) {
         uint64_t base = T << LP_LOW;
         for (int i = 0; i < K - LP_LOW; ++i) base = lp_ins0(base, p.high_q[i]);
-        const uint64_t full = p.shard_base | base;
-        uint32_t fired = 0;
+        LpTile t;
+        t.smem_raw = smem_raw;
+        t.full = p.shard_base | base;
+        t.cpool_off = (uint32_t)L.cpool;
+        t.fired = 0;
         for (int e = 0; e < p.nevents; ++e)
-            if ((full & p.ev_full[e]) == p.ev_full[e]) fired |= 1u << e;
+            if ((t.full & p.ev_full[e]) == p.ev_full[e]) t.fired |= 1u << e;
         // ---- load the tile: logical x = tid + 128 j at S x ----
         if (!p.noio) {
             const char *gp = reinterpret_cast<const char *>(a + (base | d_tid));
@@ -361,59 +428,10 @@ __device__ __forceinline__ void lp_body(const LPassParams &p, const Ops &ops) {
         lp_cp_async_wait_all();
         __syncthreads();
         // ---- register stages ----
-        for (int s = 0; s < p.nstages; ++s) {
-            const LStage &st = p.st[s];
-            uint32_t y = st.y_static;
-            for (uint32_t m = fired & st.ev_mask; m; m &= m - 1) y ^= st.y_ev[__ffs(m) - 1];
-            uint32_t g0 = 0;
-#pragma unroll
-            for (int r = 0; r < R; ++r) g0 |= ((y >> st.qbit[r]) & 1u) << r;
-            const uint32_t yrest = y & ~(uint32_t)st.qmask;
-            uint32_t rp[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r) rp[r] = (uint32_t)st.reg_phys[r] << 4;
-            const bool nxq = st.needs_xq;
-            // group bits 0..6 = this thread's index (LP_THREADS = 128): their
-            // address / logical parts once per stage; bits >= 7 per group below
-            uint32_t a0t = 0, xqt = yrest;
-#pragma unroll
-            for (int i = 0; i < 7; ++i)
-                if (i < K - R && ((tid >> i) & 1u)) {
-                    a0t ^= (uint32_t)st.grp_phys[i] << 4;
-                    xqt ^= st.grp_log[i];
-                }
-            for (uint32_t grp = tid; grp < ngroups; grp += LP_THREADS) {
-                uint32_t a0 = a0t, xq = nxq ? xqt : yrest;
-                for (int i = 7; i < K - R; ++i)
-                    if ((grp >> i) & 1u) {
-                        a0 ^= (uint32_t)st.grp_phys[i] << 4;
-                        if (nxq) xq ^= st.grp_log[i];
-                    }
-                double2 v[NS];
-#pragma unroll
-                for (int j = 0; j < NS; ++j) {
-                    uint32_t ad = a0;
-#pragma unroll
-                    for (int r = 0; r < R; ++r)
-                        if (j & (1 << r)) ad ^= rp[r];
-                    v[j] = *reinterpret_cast<const double2 *>(smem_raw + ad);
-                }
-                uint32_t g = g0;
-                ops(s, v, g, xq, full, p, smem_raw, cpool_off);
-#pragma unroll
-                for (int j = 0; j < NS; ++j) {
-                    uint32_t ad = a0;
-#pragma unroll
-                    for (int r = 0; r < R; ++r)
-                        if (j & (1 << r)) ad ^= rp[r];
-                    *reinterpret_cast<double2 *>(smem_raw + ad) = v[j];
-                }
-            }
-            __syncthreads();
-        }
+        stages(t);
         // ---- store: logical x = tid + 128 j from S (M x ^ b) ----
         uint32_t sbt = p.sb_static;
-        for (uint32_t m = fired; m; m &= m - 1) sbt ^= p.sv_ev[__ffs(m) - 1];
+        for (uint32_t m = t.fired; m; m &= m - 1) sbt ^= p.sv_ev[__ffs(m) - 1];
         if (!p.noio) {
             char *gp = reinterpret_cast<char *>(a + (base | d_tid));
             const uint32_t mo = m_tid ^ (sbt << 4);

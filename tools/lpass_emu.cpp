@@ -397,7 +397,55 @@ static int stats_file(const char *path, int nl, int R) {
     return 0;
 }
 
+// the CUDA sources of the specialised kernels of a gate file's passes
+// (lpass_jit_source), one file per pass: jit_<k>.cu in outdir
+struct SrcSink : LPassSink {
+    std::string dir;
+    int R = 4, k = 0, maxn = 1 << 30;
+    int pass(const LPassParams &p, const LCompileStats &, const std::vector<int> &) override {
+        if (k >= maxn) return 0;
+        const int minb = p.R == 5 ? 2 : (p.R == 4 && p.K <= 11) ? 4 : 3;
+        const std::string src = lpass_jit_source(p, p.R, minb);
+        FILE *f = fopen((dir + "/jit_" + std::to_string(k++) + ".cu").c_str(), "w");
+        if (!f) return 1;
+        fputs(src.c_str(), f);
+        fclose(f);
+        return 0;
+    }
+    int sweep(const LGate &, int) override { return 0; }
+    double gate_bytes(const LGate &) override { return 1e30; }
+};
+
+static int jit_sources(const char *path, int nl, const char *dir, int maxn) {
+    FILE *f = fopen(path, "r");
+    if (!f) return 2;
+    std::vector<LGate> gs;
+    LGate g{};
+    while (fscanf(f, "%d %d %d %d %lf %lf %lf %lf %lf %lf %lf %lf", &g.t, &g.nctl, &g.ctl[0], &g.ctl[1], &g.u[0],
+                  &g.u[1], &g.u[2], &g.u[3], &g.u[4], &g.u[5], &g.u[6], &g.u[7]) == 12)
+        gs.push_back(g);
+    fclose(f);
+    SrcSink sink;
+    sink.dir = dir;
+    sink.maxn = maxn;
+    LRunConfig cfg;
+    cfg.nl = nl;
+    cfg.K = std::min(LP_MAX_K, nl);
+    cfg.R = 4;
+    cfg.max_coef = 960;
+    cfg.pass_bytes = std::ldexp(32.0, nl);
+    std::string err;
+    if (lpass_run(gs.data(), (int)gs.size(), cfg, sink, &err)) {
+        printf("error %s\n", err.c_str());
+        return 1;
+    }
+    printf("ok sources=%d\n", sink.k);
+    return 0;
+}
+
 int main(int argc, char **argv) {
+    if (argc > 4 && std::string(argv[1]) == "jitsrc")
+        return jit_sources(argv[2], atoi(argv[3]), argv[4], argc > 5 ? atoi(argv[5]) : 1 << 30);
     if (argc > 3 && std::string(argv[1]) == "stats") return stats_file(argv[2], atoi(argv[3]), argc > 4 ? atoi(argv[4]) : 4);
     const int ncases = argc > 1 ? atoi(argv[1]) : 300;
     const uint64_t seed = argc > 2 ? strtoull(argv[2], nullptr, 10) : 1;
