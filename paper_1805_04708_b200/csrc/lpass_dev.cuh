@@ -316,11 +316,19 @@ template <int R, int KK, class Ops>
 __device__ __forceinline__ void lp_stage(const LPassParams &p, const LpTile &t, const LStage &st, const Ops &ops) {
     constexpr int NS = 1 << R;
     const int K = KK ? KK : p.K;
-    const uint32_t tid = threadIdx.x;
+    // read %tid.x through volatile asm: the per-stage group addressing below is
+    // recomputed per tile instead of being hoisted out of the tile loop for
+    // every stage at once (register pressure -> spills in specialised kernels)
+    uint32_t tid;
+    asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
     const uint32_t ngroups = 1u << (K - R);
     unsigned char *smem_raw = t.smem_raw;
     uint32_t y = st.y_static;
-    for (uint32_t m = t.fired & st.ev_mask; m; m &= m - 1) y ^= st.y_ev[__ffs(m) - 1];
+    // static event indices (a literal stage keeps only its events, no indexed array)
+#pragma unroll
+    for (int e = 0; e < LP_MAX_EVENTS; ++e)
+        if ((st.ev_mask >> e) & 1u)
+            if ((t.fired >> e) & 1u) y ^= st.y_ev[e];
     uint32_t g0 = 0;
 #pragma unroll
     for (int r = 0; r < R; ++r) g0 |= ((y >> st.qbit[r]) & 1u) << r;
