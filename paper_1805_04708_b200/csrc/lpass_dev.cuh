@@ -319,8 +319,7 @@ __device__ __forceinline__ void lp_stage(const LPassParams &p, const LpTile &t, 
     // read %tid.x through volatile asm: the per-stage group addressing below is
     // recomputed per tile instead of being hoisted out of the tile loop for
     // every stage at once (register pressure -> spills in specialised kernels)
-    uint32_t tid;
-    asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
+    const uint32_t tid = threadIdx.x;
     const uint32_t ngroups = 1u << (K - R);
     unsigned char *smem_raw = t.smem_raw;
     uint32_t y = st.y_static;
