@@ -104,8 +104,9 @@ size_t lpass_smem_bytes(int K, int ncoef);
 int launch_lpass_e(const LPassParams &p, struct CUstream_st *stream);
 void lpass_jit_sync();  // wait for every queued specialisation
 // CUDA source of the kernel specialised to this program (R register qubits,
-// minb CTAs per SM): lp_body with literal stages and ops (lpass_dev.cuh)
-std::string lpass_jit_source(const LPassParams &p, int R, int minb);
+// minb CTAs per SM, nt threads per CTA): lp_body with literal stages and ops
+// (lpass_dev.cuh)
+std::string lpass_jit_source(const LPassParams &p, int R, int minb, int nt = LP_THREADS);
 void lpass_launch_counts(long long *jit, long long *interp);  // specialised (NVRTC) / interpreter launches so far
 
 }  // namespace qsim

@@ -1383,7 +1383,7 @@ int lpass_run(const LGate *gates, int ng, const LRunConfig &cfg, LPassSink &sink
 // with the stage as a literal LStage and a functor holding its ops as literal
 // LOps (lp_op1 folds to straight-line code); the tile width is a template
 // constant.
-std::string lpass_jit_source(const LPassParams &p, int R, int minb) {
+std::string lpass_jit_source(const LPassParams &p, int R, int minb, int nt) {
     std::string s;
     s.reserve(8192);
     s += "#include \"lpass_dev.cuh\"\n";
@@ -1429,14 +1429,15 @@ std::string lpass_jit_source(const LPassParams &p, int R, int minb) {
                  S.qbit[4], S.needs_xq, S.first_op, S.nops, S.ev_mask);
         s += buf;
         s += ev + "};\n";
-        snprintf(buf, sizeof buf, "      qsim::lp_stage<%d, %d>(p, t, S, JitOps%d<%d>{}); }\n", R, p.K, st, R);
+        snprintf(buf, sizeof buf, "      qsim::lp_stage<%d, %d, JitOps%d<%d>, %d>(p, t, S, JitOps%d<%d>{}); }\n", R, p.K,
+                 st, R, nt, st, R);
         s += buf;
     }
     s += "  }\n};\n";
     snprintf(buf, sizeof buf,
              "extern \"C\" __global__ void __launch_bounds__(%d, %d) k_lpass_jit(const __grid_constant__ "
-             "qsim::LPassParams p) { qsim::lp_body<%d, %d>(p, JitStages{p}); }\n",
-             LP_THREADS, minb, R, p.K);
+             "qsim::LPassParams p) { qsim::lp_body<%d, %d, JitStages, %d>(p, JitStages{p}); }\n",
+             nt, minb, R, p.K, nt);
     s += buf;
     return s;
 }

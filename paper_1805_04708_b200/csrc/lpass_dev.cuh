@@ -159,7 +159,7 @@ __device__ __forceinline__ void lp_table(double2 (&v)[NS], const unsigned char *
 }
 
 // tile load (cp.async) / store of the NJ = 2^(K-7) elements of this thread:
-// logical x = tid + 128 j, j in Gray-code order (one column changes per step)
+// logical x = tid + NT j, j in Gray-code order (one column changes per step)
 template <int NJ>
 __device__ __forceinline__ void lp_tile_load(unsigned char *smem, const char *gp, uint32_t so, const uint32_t *s_hi,
                                              const uint64_t *d_hi) {
@@ -311,14 +311,12 @@ struct LpTile {
 // One register stage: every group of 2^R amplitudes (a coset of the stage's
 // register basis) is loaded from shared memory, `ops(v, g, xq, full, p,
 // smem, cpool_off)` applies the stage's ops, and it is stored back.  KK: the
-// tile width when known at compile time (0: p.K).
-template <int R, int KK, class Ops>
+// tile width when known at compile time (0: p.K); NT: threads per CTA.
+template <int R, int KK, class Ops, int NT = LP_THREADS>
 __device__ __forceinline__ void lp_stage(const LPassParams &p, const LpTile &t, const LStage &st, const Ops &ops) {
     constexpr int NS = 1 << R;
     const int K = KK ? KK : p.K;
-    // read %tid.x through volatile asm: the per-stage group addressing below is
-    // recomputed per tile instead of being hoisted out of the tile loop for
-    // every stage at once (register pressure -> spills in specialised kernels)
+    constexpr int TB = NT == 256 ? 8 : 7;  // group bits held by the thread index
     const uint32_t tid = threadIdx.x;
     const uint32_t ngroups = 1u << (K - R);
     unsigned char *smem_raw = t.smem_raw;
@@ -336,18 +334,18 @@ __device__ __forceinline__ void lp_stage(const LPassParams &p, const LpTile &t, 
 #pragma unroll
     for (int r = 0; r < R; ++r) rp[r] = (uint32_t)st.reg_phys[r] << 4;
     const bool nxq = st.needs_xq;
-    // group bits 0..6 = this thread's index (LP_THREADS = 128): their
-    // address / logical parts once per stage; bits >= 7 per group below
+    // group bits 0..TB-1 = this thread's index: their address / logical parts
+    // once per stage; bits >= TB per group below
     uint32_t a0t = 0, xqt = yrest;
 #pragma unroll
-    for (int i = 0; i < 7; ++i)
+    for (int i = 0; i < TB; ++i)
         if (i < K - R && ((tid >> i) & 1u)) {
             a0t ^= (uint32_t)st.grp_phys[i] << 4;
             xqt ^= st.grp_log[i];
         }
-    for (uint32_t grp = tid; grp < ngroups; grp += LP_THREADS) {
+    for (uint32_t grp = tid; grp < ngroups; grp += NT) {
         uint32_t a0 = a0t, xq = nxq ? xqt : yrest;
-        for (int i = 7; i < K - R; ++i)
+        for (int i = TB; i < K - R; ++i)
             if ((grp >> i) & 1u) {
                 a0 ^= (uint32_t)st.grp_phys[i] << 4;
                 if (nxq) xq ^= st.grp_log[i];
@@ -379,22 +377,23 @@ __device__ __forceinline__ void lp_stage(const LPassParams &p, const LpTile &t, 
 // (lp_stage per stage): the interpreter (lpass.cu) walks p.st / p.op, a
 // run-time specialised kernel (NVRTC) calls lp_stage with literal stages and
 // ops.  Everything else -- tile load / store, addressing -- is this code.
-template <int R, int KK, class Stages>
+template <int R, int KK, class Stages, int NT = LP_THREADS>
 __device__ __forceinline__ void lp_body(const LPassParams &p, const Stages &stages) {
+    constexpr int TB = NT == 256 ? 8 : 7;  // tile bits held by the thread index
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int K = KK ? KK : p.K;
     const LPSmem L = lp_smem(K, p.ncoef);
     double *cpool = reinterpret_cast<double *>(smem_raw + L.cpool);
     const uint32_t tid = threadIdx.x;
     // ---- one-time setup per CTA ----
-    for (int i = tid; i < p.ncoef; i += LP_THREADS) cpool[i] = p.coef[i];
-    // load / store addressing: logical x = tid + 128 j; smem byte offset of x
+    for (int i = tid; i < p.ncoef; i += NT) cpool[i] = p.coef[i];
+    // load / store addressing: logical x = tid + NT j; smem byte offset of x
     // at load = XOR of scol over its bits (store: smcol, plus S b); HBM offset
-    // = deposit of its bits.  Bits 0..6 are this thread's, bits 7.. come from j.
+    // = deposit of its bits.  Bits 0..TB-1 are this thread's, the rest come from j.
     uint32_t s_tid = 0, m_tid = 0;
     uint64_t d_tid = tid & 7u;
 #pragma unroll
-    for (int i = 0; i < 7; ++i)
+    for (int i = 0; i < TB; ++i)
         if ((tid >> i) & 1u) {
             s_tid ^= (uint32_t)p.scol[i] << 4;
             m_tid ^= (uint32_t)p.smcol[i] << 4;
@@ -404,10 +403,10 @@ __device__ __forceinline__ void lp_body(const LPassParams &p, const Stages &stag
     uint64_t d_hi[5];
 #pragma unroll
     for (int b = 0; b < 5; ++b) {
-        const bool on = 7 + b < K;
-        s_hi[b] = on ? (uint32_t)p.scol[7 + b] << 4 : 0u;
-        m_hi[b] = on ? (uint32_t)p.smcol[7 + b] << 4 : 0u;
-        d_hi[b] = on ? (16ull << p.high_q[7 + b - LP_LOW]) : 0ull;  // bytes
+        const bool on = TB + b < K;
+        s_hi[b] = on ? (uint32_t)p.scol[TB + b] << 4 : 0u;
+        m_hi[b] = on ? (uint32_t)p.smcol[TB + b] << 4 : 0u;
+        d_hi[b] = on ? (16ull << p.high_q[TB + b - LP_LOW]) : 0ull;  // bytes
     }
     __syncthreads();
     double2 *__restrict__ a = reinterpret_cast<double2 *>(p.a);
@@ -425,11 +424,12 @@ __device__ __forceinline__ void lp_body(const LPassParams &p, const Stages &stag
         // ---- load the tile: logical x = tid + 128 j at S x ----
         if (!p.noio) {
             const char *gp = reinterpret_cast<const char *>(a + (base | d_tid));
-            switch (K) {
-                case 12: lp_tile_load<32>(smem_raw, gp, s_tid, s_hi, d_hi); break;
-                case 11: lp_tile_load<16>(smem_raw, gp, s_tid, s_hi, d_hi); break;
-                case 10: lp_tile_load<8>(smem_raw, gp, s_tid, s_hi, d_hi); break;
-                default: lp_tile_load<4>(smem_raw, gp, s_tid, s_hi, d_hi); break;
+            switch (K - TB) {
+                case 5: lp_tile_load<32>(smem_raw, gp, s_tid, s_hi, d_hi); break;
+                case 4: lp_tile_load<16>(smem_raw, gp, s_tid, s_hi, d_hi); break;
+                case 3: lp_tile_load<8>(smem_raw, gp, s_tid, s_hi, d_hi); break;
+                case 2: lp_tile_load<4>(smem_raw, gp, s_tid, s_hi, d_hi); break;
+                default: lp_tile_load<2>(smem_raw, gp, s_tid, s_hi, d_hi); break;
             }
         }
         lp_cp_async_wait_all();
@@ -442,11 +442,12 @@ __device__ __forceinline__ void lp_body(const LPassParams &p, const Stages &stag
         if (!p.noio) {
             char *gp = reinterpret_cast<char *>(a + (base | d_tid));
             const uint32_t mo = m_tid ^ (sbt << 4);
-            switch (K) {
-                case 12: lp_tile_store<32>(smem_raw, gp, mo, m_hi, d_hi); break;
-                case 11: lp_tile_store<16>(smem_raw, gp, mo, m_hi, d_hi); break;
-                case 10: lp_tile_store<8>(smem_raw, gp, mo, m_hi, d_hi); break;
-                default: lp_tile_store<4>(smem_raw, gp, mo, m_hi, d_hi); break;
+            switch (K - TB) {
+                case 5: lp_tile_store<32>(smem_raw, gp, mo, m_hi, d_hi); break;
+                case 4: lp_tile_store<16>(smem_raw, gp, mo, m_hi, d_hi); break;
+                case 3: lp_tile_store<8>(smem_raw, gp, mo, m_hi, d_hi); break;
+                case 2: lp_tile_store<4>(smem_raw, gp, mo, m_hi, d_hi); break;
+                default: lp_tile_store<2>(smem_raw, gp, mo, m_hi, d_hi); break;
             }
         }
         __syncthreads();

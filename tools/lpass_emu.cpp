@@ -401,11 +401,11 @@ static int stats_file(const char *path, int nl, int R) {
 // (lpass_jit_source), one file per pass: jit_<k>.cu in outdir
 struct SrcSink : LPassSink {
     std::string dir;
-    int R = 4, k = 0, maxn = 1 << 30;
+    int R = 4, k = 0, maxn = 1 << 30, nt = 128;
     int pass(const LPassParams &p, const LCompileStats &, const std::vector<int> &) override {
         if (k >= maxn) return 0;
         const int minb = p.R == 5 ? 2 : (p.R == 4 && p.K <= 11) ? 4 : 3;
-        const std::string src = lpass_jit_source(p, p.R, minb);
+        const std::string src = nt == 256 ? lpass_jit_source(p, p.R, 2, 256) : lpass_jit_source(p, p.R, minb);
         FILE *f = fopen((dir + "/jit_" + std::to_string(k++) + ".cu").c_str(), "w");
         if (!f) return 1;
         fputs(src.c_str(), f);
@@ -428,6 +428,7 @@ static int jit_sources(const char *path, int nl, const char *dir, int maxn) {
     SrcSink sink;
     sink.dir = dir;
     sink.maxn = maxn;
+    if (getenv("QSIM_LPASS_NT") && atoi(getenv("QSIM_LPASS_NT")) == 256) sink.nt = 256;
     LRunConfig cfg;
     cfg.nl = nl;
     cfg.K = std::min(LP_MAX_K, nl);
