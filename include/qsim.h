@@ -331,6 +331,13 @@ int qsim_sync(qsim_state *s);
  * (default) / 2 selects off / background / compile-at-first-launch. */
 int qsim_jit_sync(void);
 
+/* Stop the compile threads of the specialisations and wait for their
+ * in-flight compiles; later passes run interpreted.  Call it before the
+ * process exits while compiles may be running (the Python binding registers
+ * it with atexit): exit handlers must not wait for threads that may need the
+ * dynamic loader. */
+int qsim_jit_shutdown(void);
+
 /* ---- CUDA graphs of a gate sequence (the
  * latency-bound N=14 circuit with "per-gate launch, a CUDA Graph, and a
  * single persistent kernel") ----------------------------------------------

@@ -12,6 +12,7 @@ Function names mirror the C-ABI (``qsim_create``, ``qsim_apply_gate``,
 """
 from __future__ import annotations
 
+import atexit
 import ctypes
 import os
 
@@ -91,7 +92,7 @@ EXPORTS = (
     "qsim_aux_amplitudes", "qsim_aux_num_vars", "qsim_set_qubit_map",
     "qsim_asm_parse", "qsim_asm_info", "qsim_asm_get_op", "qsim_asm_destroy", "qsim_asm_run",
     "qsim_asm_result_get", "qsim_asm_result_destroy",
-    "qsim_overlap", "qsim_jit_sync", "qsim_graph_begin", "qsim_graph_end", "qsim_graph_launch", "qsim_graph_destroy",
+    "qsim_overlap", "qsim_jit_sync", "qsim_jit_shutdown", "qsim_graph_begin", "qsim_graph_end", "qsim_graph_launch", "qsim_graph_destroy",
 )
 
 if not os.path.exists(_LIB_PATH):
@@ -145,6 +146,9 @@ _lib.qsim_set_codes.argtypes = [_P, ctypes.POINTER(ctypes.c_int8), ctypes.c_doub
 _lib.qsim_sync.argtypes = [_P]
 _lib.qsim_overlap.argtypes = [_P, _P, _dp]
 _lib.qsim_jit_sync.argtypes = []
+_lib.qsim_jit_shutdown.argtypes = []
+# stop the fused-pass compile threads before the C exit handlers run (qsim.h)
+atexit.register(_lib.qsim_jit_shutdown)
 _lib.qsim_graph_begin.argtypes = [_P]
 _lib.qsim_graph_end.argtypes = [_P, ctypes.POINTER(_P)]
 _lib.qsim_graph_launch.argtypes = [_P, _P]

@@ -1433,6 +1433,11 @@ int qsim_jit_sync(void) {
     return QSIM_OK;
 }
 
+int qsim_jit_shutdown(void) {
+    lpass_jit_shutdown();
+    return QSIM_OK;
+}
+
 int qsim_sync(qsim_state *s) {
     if (!s) return QSIM_EINVAL;
     if (s->capturing) {

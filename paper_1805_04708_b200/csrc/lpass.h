@@ -102,7 +102,8 @@ int lpass_ctas_per_sm(int R);
 size_t lpass_smem_bytes(int K, int ncoef);
 // grid = min(ntiles, CTAs/SM x SMs); returns 1 if a run-time specialised (NVRTC) kernel ran, 0 the interpreter
 int launch_lpass_e(const LPassParams &p, struct CUstream_st *stream);
-void lpass_jit_sync();  // wait for every queued specialisation
+void lpass_jit_sync();      // wait for every queued specialisation
+void lpass_jit_shutdown();  // stop and join the compile threads (before process exit)
 // CUDA source of the kernel specialised to this program (R register qubits,
 // minb CTAs per SM, nt threads per CTA): lp_body with literal stages and ops
 // (lpass_dev.cuh)
