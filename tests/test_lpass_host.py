@@ -78,7 +78,7 @@ def test_specialised_kernel_sources_compile(emu, tmp_path):
                "typedef int int32_t;\ntypedef long long int64_t;\n")
     for k in range(2):
         src = prelude + open(tmp_path / f"jit_{k}.cu").read()
-        assert "lp_stage<4, 12>" in src and "constexpr qsim::LOp" in src
+        assert "lp_stage<4, 12, JitOps0<4>, 128>" in src and "constexpr qsim::LOp" in src
         err, prog = nvrtc.nvrtcCreateProgram(src.encode(), b"lpass_jit.cu", 2, hdrs,
                                              [b"lpass_types.h", b"lpass_dev.cuh"])
         opts = [b"--gpu-architecture=sm_100a", b"-std=c++17", b"-default-device"]
