@@ -13,6 +13,10 @@ value = aggregate effective HBM GB/s = sum over gates of the gate's
 algorithmic bytes (SURVEY.md §8(d) byte-accounting: 32 B x amplitudes touched
 by the gate, 0 for SWAP) over all GPUs / device time (max over ranks).
 Inputs are larger than L2 (16 GiB state >> 126 MB), so no L2 flush is needed.
+Warm-up: the first warm-up step queues the NVRTC specialisation of every pass
+program of the circuit; bench.py waits for them (qsim_jit_sync) before the
+remaining warm-up steps, so the timed steps run the specialised pass kernels
+(reported as library.jit_passes).
 
 --impl reference: the oracle (plain CPU fp64 simulator, oracle/) timed on the
 host cores on a bounded sample of the same workload, same metric and unit.
