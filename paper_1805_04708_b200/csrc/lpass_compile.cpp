@@ -1288,36 +1288,72 @@ int lpass_run(const LGate *gates, int ng, const LRunConfig &cfg, LPassSink &sink
     static thread_local LPassParams prog;
     std::vector<LGate> lg, dfr;
     std::vector<int> sel, ids;
-    while (!pend.empty()) {
-        std::vector<char> done(pend.size(), 0);
-        std::vector<int> high;
-        sel.clear();
-        auto in_high = [&](int q) { return std::find(high.begin(), high.end(), q) != high.end(); };
+    // Greedy pass selection: every pending gate (in order) that commutes with
+    // all skipped earlier ones and whose non-diagonal target fits the tile's
+    // hmax free qubits (first come, first served), qubits in `forbid` never
+    // joining the tile.  Score: dense / permutation gates 1, others 0.3.
+    auto select = [&](uint64_t forbid, std::vector<int> &sel_, std::vector<int> &high_, std::vector<char> &done_) {
+        done_.assign(pend.size(), 0);
+        high_.clear();
+        sel_.clear();
+        auto in_high = [&](int q) { return std::find(high_.begin(), high_.end(), q) != high_.end(); };
         uint64_t bx = 0, bz = 0;
-        for (size_t k = 0; k < pend.size() && (int)sel.size() < LP_MAX_PASS_GATES; ++k) {
+        double score = 0.0;
+        for (size_t k = 0; k < pend.size() && (int)sel_.size() < LP_MAX_PASS_GATES; ++k) {
             const Item &it = pend[k];
             bool ok = !((it.xq & (bx | bz)) || (it.zq & bx));
             if (ok && it.needs_reg) {
                 const int t = it.g.t;
                 if (t >= LP_LOW && !in_high(t)) {
-                    if ((int)high.size() >= hmax)
+                    if ((int)high_.size() >= hmax || ((forbid >> t) & 1ull))
                         ok = false;
                     else
-                        high.push_back(t);
+                        high_.push_back(t);
                 }
                 // a local control in the tile makes a CNOT a tile relabelling
                 if (ok && it.g.nctl == 1) {
                     const int c = it.g.ctl[0];
-                    if (c >= LP_LOW && c < nl && (int)high.size() < hmax && !in_high(c)) high.push_back(c);
+                    if (c >= LP_LOW && c < nl && (int)high_.size() < hmax && !in_high(c) && !((forbid >> c) & 1ull))
+                        high_.push_back(c);
                 }
             }
             if (ok) {
-                done[k] = 1;
-                sel.push_back((int)k);
+                done_[k] = 1;
+                sel_.push_back((int)k);
+                score += it.needs_reg ? 1.0 : 0.3;
             } else {
                 bx |= it.xq;
                 bz |= it.zq;
             }
+        }
+        return score;
+    };
+    static const int search = getenv("LPASS_SEARCH") ? atoi(getenv("LPASS_SEARCH")) : 2;
+    while (!pend.empty()) {
+        std::vector<char> done;
+        std::vector<int> high;
+        double best = select(0, sel, high, done);
+        // local search over the tile's qubits: keep one of them out when that
+        // lets more gates into the pass (a qubit whose gates come early but
+        // block many others), a few rounds
+        uint64_t forbid = 0;
+        for (int round = 0; round < search; ++round) {
+            bool improved = false;
+            const std::vector<int> h0 = high;
+            for (int q : h0) {
+                std::vector<int> s2, h2;
+                std::vector<char> d2;
+                const double sc = select(forbid | (1ull << q), s2, h2, d2);
+                if (sc > best + 1e-9) {
+                    best = sc;
+                    sel.swap(s2);
+                    high.swap(h2);
+                    done.swap(d2);
+                    forbid |= 1ull << q;
+                    improved = true;
+                }
+            }
+            if (!improved) break;
         }
         if (getenv("LPASS_TRACE")) fprintf(stderr, "lpass_run: pending %zu, pass %zu\n", pend.size(), sel.size());
         LCompileStats cs;
