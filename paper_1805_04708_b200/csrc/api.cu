@@ -2155,13 +2155,64 @@ static int dense_gate_a(qsim_state *s, const PlanOp &o, const double *u) {
     return QSIM_OK;
 }
 
+// Consecutive diagonal gates [i, j) as one sweep per shard (k_diag_run_a):
+// each gate contributes the integer b1 steps it would add alone, so the
+// codes equal gate-by-gate application bit for bit (mod 256 addition).
+static int diag_run_a(qsim_state *s, const std::vector<PlanOp> &run, const std::vector<const double *> &us, size_t i,
+                      size_t j) {
+    for (auto &sh : s->shards) {
+        ADiagRunParams p{};
+        p.a = sh.amps;
+        p.n = s->alloc_amps;
+        double bytes = 0.0;
+        for (size_t k = i; k < j; ++k) {
+            const PlanOp &o = run[k];
+            const double *u = us[k];
+            if (!global_ctrls_ok(s, sh, o)) continue;
+            ADiagRunGate g{};
+            for (int c = 0; c < o.nctrl; ++c)
+                if (o.ctrl[c] < s->nl) g.cmask |= 1u << o.ctrl[c];
+            const int k0 = a_phase_steps(u[0], u[1]), k1 = a_phase_steps(u[6], u[7]);
+            if (o.l >= s->nl) {
+                g.t = -1;
+                g.k0 = (int8_t)(rank_bit(s, sh, o.l) ? k1 : k0);
+                g.k1 = g.k0;
+            } else {
+                g.t = (int16_t)o.l;
+                g.k0 = (int8_t)k0;
+                g.k1 = (int8_t)k1;
+            }
+            p.g[p.ngates++] = g;
+            bytes += gate_bytes_alone(s, sh, o, u);
+        }
+        if (!p.ngates) continue;
+        prof_begin(s);
+        launch_diag_run_a(p, s->stream);
+        prof_end(s, QSIM_K_A_FAST, bytes);
+        s->st.kernels++;
+        s->st.hbm_bytes += std::ldexp(2.0 * (double)s->amp_bytes, s->nl);
+    }
+    CU(cudaGetLastError());
+    return QSIM_OK;
+}
+
 static int run_gates_a(qsim_state *s, const std::vector<PlanOp> &run, const std::vector<const double *> &us) {
+    static const bool fuse_diag = getenv("QSIM_A_NO_DIAG_RUN") == nullptr;
     for (size_t i = 0; i < run.size(); ++i) {
         const PlanOp &o = run[i];
         const double *u = us[i];
         if (o.cls == CLS_DENSE) {
             RC(dense_gate_a(s, o, u));
             continue;
+        }
+        if (fuse_diag && o.cls == CLS_DIAG && s->nl <= 32) {
+            size_t j = i;
+            while (j < run.size() && run[j].cls == CLS_DIAG && (int)(j - i) < A_MAX_DIAG_RUN) ++j;
+            if (j - i >= 2) {
+                RC(diag_run_a(s, run, us, i, j));
+                i = j - 1;
+                continue;
+            }
         }
         // perm (anti-diagonal) and phase (diagonal) gates move or rotate codes; bounds unchanged
         for (auto &sh : s->shards) {

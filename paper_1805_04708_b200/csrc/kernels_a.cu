@@ -878,6 +878,45 @@ void launch_fast_a(const AGateParams &g, const ATables *t, cudaStream_t s) {
     }
 }
 
+// a run of diagonal gates: per code, the sum of the gates' b1 steps (mod 256)
+__global__ void __launch_bounds__(A_THREADS) k_diag_run_a(const __grid_constant__ ADiagRunParams p) {
+    uint16_t *a = reinterpret_cast<uint16_t *>(p.a);
+    const uint64_t nvec = p.n >> 3;
+    for (uint64_t v = (uint64_t)blockIdx.x * A_THREADS + threadIdx.x; v < nvec; v += (uint64_t)gridDim.x * A_THREADS) {
+        uint4 w = __ldcs(reinterpret_cast<const uint4 *>(a + (v << 3)));
+        uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+        const uint32_t hi = (uint32_t)(v << 3);  // local index bits >= 3 of the 8 codes (bits < 32 suffice:
+                                                  // the gates' local bits are < 32 -- checked by the caller)
+        uint32_t sh[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int gi = 0; gi < p.ngates; ++gi) {
+            const ADiagRunGate g = p.g[gi];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t idx = hi | (uint32_t)j;
+                const bool on = (idx & g.cmask) == g.cmask;
+                const bool bit = g.t >= 0 && ((idx >> g.t) & 1u);
+                sh[j] += on ? (uint32_t)(int)(bit ? g.k1 : g.k0) : 0u;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t c = (j & 1) ? (ws[j >> 1] >> 16) : (ws[j >> 1] & 0xffffu);
+            const uint32_t n = shift_b1_fast(c, (sh[j] & 0xffu) << 8);
+            ws[j >> 1] = (j & 1) ? ((ws[j >> 1] & 0xffffu) | (n << 16)) : ((ws[j >> 1] & 0xffff0000u) | n);
+        }
+        w.x = ws[0];
+        w.y = ws[1];
+        w.z = ws[2];
+        w.w = ws[3];
+        __stcs(reinterpret_cast<uint4 *>(a + (v << 3)), w);
+    }
+}
+
+void launch_diag_run_a(const ADiagRunParams &p, cudaStream_t s) {
+    k_diag_run_a<<<a_grid(p.n >> 3), A_THREADS, 0, s>>>(p);
+}
+int a_phase_steps(double ur, double ui) { return phase_steps(ur, ui); }
+
 // exchange for A: codes move; a diagonal / anti-diagonal gate is applied on arrival
 struct AXParams {
     void *own;

@@ -67,6 +67,25 @@ void launch_tables_next(const double *acc, ATables *t, cudaStream_t s);
 void launch_apply_a(const AGateParams &p, const ATables *t, cudaStream_t s);
 // diagonal / anti-diagonal gates: b1 shifts and code moves, bounds unchanged
 void launch_fast_a(const AGateParams &p, const ATables *t, cudaStream_t s);
+// A run of consecutive diagonal gates in one sweep: each gate's b1 step
+// round(128 arg(u)/pi) per value of its target bit, added under its local
+// controls (global targets / controls resolved per shard by the caller into
+// constant steps / dropped gates) -- the same integers, summed mod 256, the
+// gates add one by one (exact).
+constexpr int A_MAX_DIAG_RUN = 48;
+struct ADiagRunGate {
+    uint32_t cmask;   // local control bits
+    int16_t t;        // local target bit, or -1: constant step k0 for the whole shard
+    int8_t k0, k1;    // b1 steps for target bit 0 / 1
+};
+struct ADiagRunParams {
+    void *a;
+    uint64_t n;       // codes in the shard
+    int32_t ngates, pad;
+    ADiagRunGate g[A_MAX_DIAG_RUN];
+};
+void launch_diag_run_a(const ADiagRunParams &p, cudaStream_t s);
+int a_phase_steps(double ur, double ui);
 void launch_xchg_a(const struct XchgParams &p, const ATables *t, cudaStream_t s);
 // collapse phase 1: out = (min |z'|^2, -max |z'|^2)
 void launch_collapse_bounds_a(const ACollapseParams &p, const ATables *t, double *partials, double *out,

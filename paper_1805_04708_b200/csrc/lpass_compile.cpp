@@ -1292,6 +1292,8 @@ int lpass_run(const LGate *gates, int ng, const LRunConfig &cfg, LPassSink &sink
     // all skipped earlier ones and whose non-diagonal target fits the tile's
     // hmax free qubits (first come, first served), qubits in `forbid` never
     // joining the tile.  Score: dense / permutation gates 1, others 0.3.
+    static const double w_other = getenv("LPASS_W") ? atof(getenv("LPASS_W")) : 0.3;
+    static const int best_impr = getenv("LPASS_BEST") ? atoi(getenv("LPASS_BEST")) : 0;
     auto select = [&](uint64_t forbid, std::vector<int> &sel_, std::vector<int> &high_, std::vector<char> &done_) {
         done_.assign(pend.size(), 0);
         high_.clear();
@@ -1320,7 +1322,7 @@ int lpass_run(const LGate *gates, int ng, const LRunConfig &cfg, LPassSink &sink
             if (ok) {
                 done_[k] = 1;
                 sel_.push_back((int)k);
-                score += it.needs_reg ? 1.0 : 0.3;
+                score += it.needs_reg ? 1.0 : w_other;
             } else {
                 bx |= it.xq;
                 bz |= it.zq;
@@ -1328,7 +1330,7 @@ int lpass_run(const LGate *gates, int ng, const LRunConfig &cfg, LPassSink &sink
         }
         return score;
     };
-    static const int search = getenv("LPASS_SEARCH") ? atoi(getenv("LPASS_SEARCH")) : 2;
+    static const int search = getenv("LPASS_SEARCH") ? atoi(getenv("LPASS_SEARCH")) : 3;
     while (!pend.empty()) {
         std::vector<char> done;
         std::vector<int> high;
@@ -1340,19 +1342,22 @@ int lpass_run(const LGate *gates, int ng, const LRunConfig &cfg, LPassSink &sink
         for (int round = 0; round < search; ++round) {
             bool improved = false;
             const std::vector<int> h0 = high;
+            uint64_t fbest = forbid;
             for (int q : h0) {
                 std::vector<int> s2, h2;
                 std::vector<char> d2;
-                const double sc = select(forbid | (1ull << q), s2, h2, d2);
+                const uint64_t f = (best_impr ? forbid : fbest) | (1ull << q);
+                const double sc = select(f, s2, h2, d2);
                 if (sc > best + 1e-9) {
                     best = sc;
                     sel.swap(s2);
                     high.swap(h2);
                     done.swap(d2);
-                    forbid |= 1ull << q;
+                    fbest = f;
                     improved = true;
                 }
             }
+            forbid = fbest;
             if (!improved) break;
         }
         if (getenv("LPASS_TRACE")) fprintf(stderr, "lpass_run: pending %zu, pass %zu\n", pend.size(), sel.size());

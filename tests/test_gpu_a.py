@@ -277,3 +277,30 @@ def test_all_to_all_remap_is_bit_exact_in_a():
             out.append(s.get_codes())
     for c, r0, r1 in out[1:]:
         assert np.array_equal(c, out[0][0]) and r0 == out[0][1] and r1 == out[0][2]
+
+
+def test_fused_diagonal_runs_are_bit_exact(tmp_path):
+    """Consecutive diagonal gates run as one sweep (k_diag_run_a) give the
+    same codes, bit for bit, as one sweep per gate (QSIM_A_NO_DIAG_RUN=1):
+    the per-gate b1 steps are integers summed mod 256.  Config-4 recipe (its
+    CPHASE matchings and Rz streaks are the runs), P = 1 and 4."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env_off in (False, True):
+        for P in (1, 4):
+            out = str(tmp_path / f"c_{int(env_off)}_{P}.npy")
+            code = ("import sys, numpy as np; sys.path.insert(0, %r); import paper_1805_04708_b200 as q, "
+                    "qsim_inputs as C; s = q.State(14, q.ENC_ADAPTIVE2, %d); s.apply_circuit(C.rz_rx_cphase(14, 4, "
+                    "seed=9)); c, r0, r1 = s.get_codes(); np.save(%r, c); print(r0, r1)" % (root, P, out))
+            env = dict(os.environ)
+            if env_off:
+                env["QSIM_A_NO_DIAG_RUN"] = "1"
+            r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+            assert r.returncode == 0, r.stderr
+            outs.append((np.load(out), r.stdout.split()))
+    for c, b in outs[1:]:
+        assert np.array_equal(c, outs[0][0]) and b == outs[0][1]

@@ -381,7 +381,7 @@ static int stats_file(const char *path, int nl, int R) {
     sink.nl = nl;
     LRunConfig cfg;
     cfg.nl = nl;
-    cfg.K = std::min(LP_MAX_K, nl);
+    cfg.K = std::min(getenv("QSIM_LPASS_K") ? atoi(getenv("QSIM_LPASS_K")) : LP_MAX_K, nl);
     cfg.R = R;
     cfg.max_coef = R == 4 ? 960 : LP_MAX_COEF;
     cfg.pass_bytes = std::ldexp(32.0, nl);
