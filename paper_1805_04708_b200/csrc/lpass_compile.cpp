@@ -1294,6 +1294,7 @@ int lpass_run(const LGate *gates, int ng, const LRunConfig &cfg, LPassSink &sink
     // joining the tile.  Score: dense / permutation gates 1, others 0.3.
     static const double w_other = getenv("LPASS_W") ? atof(getenv("LPASS_W")) : 0.3;
     static const int best_impr = getenv("LPASS_BEST") ? atoi(getenv("LPASS_BEST")) : 0;
+    static const bool pairs_ok = getenv("LPASS_PAIRS") ? atoi(getenv("LPASS_PAIRS")) != 0 : true;
     auto select = [&](uint64_t forbid, std::vector<int> &sel_, std::vector<int> &high_, std::vector<char> &done_) {
         done_.assign(pend.size(), 0);
         high_.clear();
@@ -1358,6 +1359,24 @@ int lpass_run(const LGate *gates, int ng, const LRunConfig &cfg, LPassSink &sink
                 }
             }
             forbid = fbest;
+            if (!improved && pairs_ok) {  // no single exclusion helps: try pairs
+                for (size_t a = 0; a < h0.size() && !improved; ++a)
+                    for (size_t b2 = a + 1; b2 < h0.size(); ++b2) {
+                        std::vector<int> s2, h2;
+                        std::vector<char> d2;
+                        const uint64_t f = forbid | (1ull << h0[a]) | (1ull << h0[b2]);
+                        const double sc = select(f, s2, h2, d2);
+                        if (sc > best + 1e-9) {
+                            best = sc;
+                            sel.swap(s2);
+                            high.swap(h2);
+                            done.swap(d2);
+                            fbest = f;
+                            improved = true;
+                        }
+                    }
+                forbid = fbest;
+            }
             if (!improved) break;
         }
         if (getenv("LPASS_TRACE")) fprintf(stderr, "lpass_run: pending %zu, pass %zu\n", pend.size(), sel.size());
