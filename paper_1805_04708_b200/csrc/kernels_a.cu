@@ -379,6 +379,42 @@ struct AUnit {
     }
 };
 
+// Matrix classes of a dense U for the A kernels (host: a_ukind): 0 general,
+// 1 every entry real (H, Ry), 2 real diagonal and imaginary off-diagonal (Rx).
+// The class formulas are the general one with its exactly-zero terms dropped
+// (fma(0, b, c) = c, fma(a, b, +-0) = a b rounded once), so the fp64 results
+// are the same bits.
+template <int UK>
+__device__ __forceinline__ void a_gate2k(const double (&u)[8], double2 &x, double2 &y) {
+    const double2 x0 = x, y0 = y;
+    if (UK == 1) {
+        x.x = fma(u[0], x0.x, u[2] * y0.x);
+        x.y = fma(u[0], x0.y, u[2] * y0.y);
+        y.x = fma(u[4], x0.x, u[6] * y0.x);
+        y.y = fma(u[4], x0.y, u[6] * y0.y);
+    } else {
+        x.x = fma(u[0], x0.x, -(u[3] * y0.y));
+        x.y = fma(u[0], x0.y, u[3] * y0.x);
+        y.x = fma(-u[5], x0.y, u[6] * y0.x);
+        y.y = fma(u[5], x0.x, u[6] * y0.y);
+    }
+}
+template <int UK>
+__device__ __forceinline__ void a_gate_fk(const float (&u)[8], float2 &x, float2 &y) {
+    const float2 x0 = x, y0 = y;
+    if (UK == 1) {
+        x.x = fmaf(u[0], x0.x, u[2] * y0.x);
+        x.y = fmaf(u[0], x0.y, u[2] * y0.y);
+        y.x = fmaf(u[4], x0.x, u[6] * y0.x);
+        y.y = fmaf(u[4], x0.y, u[6] * y0.y);
+    } else {
+        x.x = fmaf(u[0], x0.x, -(u[3] * y0.y));
+        x.y = fmaf(u[0], x0.y, u[3] * y0.x);
+        y.x = fmaf(-u[5], x0.y, u[6] * y0.x);
+        y.y = fmaf(u[5], x0.x, u[6] * y0.y);
+    }
+}
+
 __device__ __forceinline__ void a_gate2(const double (&u)[8], double2 &x, double2 &y) {
     const double2 x0 = x, y0 = y;
     x.x = fma(u[0], x0.x, fma(-u[1], x0.y, fma(u[2], y0.x, -u[3] * y0.y)));
@@ -472,6 +508,21 @@ __device__ __forceinline__ void a_gate_f(const float (&u)[8], float2 &x, float2 
     y.x = fmaf(u[4], x0.x, fmaf(-u[5], x0.y, fmaf(u[6], y0.x, -u[7] * y0.y)));
     y.y = fmaf(u[4], x0.y, fmaf(u[5], x0.x, fmaf(u[6], y0.y, u[7] * y0.x)));
 }
+template <int UK>
+__device__ __forceinline__ void a_gate2u(const double (&u)[8], double2 &x, double2 &y) {
+    if (UK == 0)
+        a_gate2(u, x, y);
+    else
+        a_gate2k<UK>(u, x, y);
+}
+template <int UK>
+__device__ __forceinline__ void a_gate_fu(const float (&u)[8], float2 &x, float2 &y) {
+    if (UK == 0)
+        a_gate_f(u, x, y);
+    else
+        a_gate_fk<UK>(u, x, y);
+}
+
 // nearest integer of t (|t| < 2^22) without the conversion unit: k and t - k
 __device__ __forceinline__ int a_rnd(float t, float &fr) {
     const float m = t + 12582912.0f;  // 1.5 * 2^23
@@ -506,7 +557,7 @@ __device__ __forceinline__ uint32_t a_encode_f(const ASm &sm, const ASmF &f, flo
 
 // fp64 reference for the pairs of a unit whose fp32 decision failed (rare;
 // out of line so the hot loop stays small)
-template <int TL>
+template <int TL, int UK>
 __device__ __noinline__ void a_unit_exact(const ASm &sm, const double *u, const uint32_t *c, uint32_t *nc,
                                           uint32_t fail, uint32_t selm) {
     double uu[8];
@@ -516,13 +567,13 @@ __device__ __noinline__ void a_unit_exact(const ASm &sm, const double *u, const 
         if (!((fail >> k) & 1u)) continue;
         const int j0 = AUnit<TL>::j0(k), j1 = AUnit<TL>::j1(k);
         double2 x = a_decode(sm, c[j0]), y = a_decode(sm, c[j1]);
-        if ((selm >> k) & 1u) a_gate2(uu, x, y);
+        if ((selm >> k) & 1u) a_gate2u<UK>(uu, x, y);
         nc[j0] = a_encode(sm, x);
         nc[j1] = a_encode(sm, y);
     }
 }
 
-template <int TL, bool CTRL>
+template <int TL, bool CTRL, int UK>
 __global__ void __launch_bounds__(A_THREADS) k_bounds_a(const __grid_constant__ AGateParams p,
                                                         const ATabData *__restrict__ cur,
                                                         const ATabData *__restrict__ nxt, double *partials) {
@@ -549,7 +600,7 @@ __global__ void __launch_bounds__(A_THREADS) k_bounds_a(const __grid_constant__ 
             const int j0 = U::j0(k), j1 = U::j1(k);
             double2 x = a_decode(sm, c[j0]), y = a_decode(sm, c[j1]);
             const int off = TL < 4 ? j0 : k;
-            if (!CTRL || (hi_ok && ((uint32_t)off & cl) == cl)) a_gate2(u, x, y);
+            if (!CTRL || (hi_ok && ((uint32_t)off & cl) == cl)) a_gate2u<UK>(u, x, y);
             b.add(a_m2(x));
             b.add(a_m2(y));
         }
@@ -626,16 +677,32 @@ __global__ void k_tables_next(const double *acc, ATabData *t) {
     }
 }
 
-template <int TL, bool CTRL>
+template <int TL, bool CTRL, int UK>
 static void launch_bounds_tl(const AGateParams &p, const ATables *t, double *partials, int grid, cudaStream_t s) {
-    k_bounds_a<TL, CTRL><<<grid, A_THREADS, 0, s>>>(p, tcur(t), tnext(t), partials);
+    k_bounds_a<TL, CTRL, UK><<<grid, A_THREADS, 0, s>>>(p, tcur(t), tnext(t), partials);
 }
-template <int TL>
+template <int TL, int UK>
 static void launch_bounds_c(const AGateParams &p, const ATables *t, double *partials, int grid, cudaStream_t s) {
     if (p.cmask)
-        launch_bounds_tl<TL, true>(p, t, partials, grid, s);
+        launch_bounds_tl<TL, true, UK>(p, t, partials, grid, s);
     else
-        launch_bounds_tl<TL, false>(p, t, partials, grid, s);
+        launch_bounds_tl<TL, false, UK>(p, t, partials, grid, s);
+}
+template <int UK>
+static void launch_bounds_k(const AGateParams &p, const ATables *t, double *partials, int grid, cudaStream_t s) {
+    switch (p.t < 4 ? p.t : 4) {
+        case 0: launch_bounds_c<0, UK>(p, t, partials, grid, s); break;
+        case 1: launch_bounds_c<1, UK>(p, t, partials, grid, s); break;
+        case 2: launch_bounds_c<2, UK>(p, t, partials, grid, s); break;
+        case 3: launch_bounds_c<3, UK>(p, t, partials, grid, s); break;
+        default: launch_bounds_c<4, UK>(p, t, partials, grid, s); break;
+    }
+}
+// matrix class of U (see a_gate2k)
+static int a_ukind(const double *u) {
+    if (u[1] == 0.0 && u[3] == 0.0 && u[5] == 0.0 && u[7] == 0.0) return 1;
+    if (u[1] == 0.0 && u[7] == 0.0 && u[2] == 0.0 && u[4] == 0.0) return 2;
+    return 0;
 }
 
 void launch_bounds_a(const AGateParams &p, const ATables *t, double *partials, double *acc, bool first,
@@ -643,12 +710,10 @@ void launch_bounds_a(const AGateParams &p, const ATables *t, double *partials, d
     const uint64_t units = (p.nl >= 4) ? (1ull << (p.nl - 4)) : 1ull;
     int grid = a_grid(units);
     if (grid > 2 * a_num_sms() * 4) grid = 2 * a_num_sms() * 4;  // partials capacity
-    switch (p.t < 4 ? p.t : 4) {
-        case 0: launch_bounds_c<0>(p, t, partials, grid, s); break;
-        case 1: launch_bounds_c<1>(p, t, partials, grid, s); break;
-        case 2: launch_bounds_c<2>(p, t, partials, grid, s); break;
-        case 3: launch_bounds_c<3>(p, t, partials, grid, s); break;
-        default: launch_bounds_c<4>(p, t, partials, grid, s); break;
+    switch (a_ukind(p.u)) {
+        case 1: launch_bounds_k<1>(p, t, partials, grid, s); break;
+        case 2: launch_bounds_k<2>(p, t, partials, grid, s); break;
+        default: launch_bounds_k<0>(p, t, partials, grid, s); break;
     }
     k_minmax_final<<<1, 32, 0, s>>>(partials, grid, acc, first ? 1 : 0);
 }
@@ -657,7 +722,7 @@ void launch_tables_next(const double *acc, ATables *t, cudaStream_t s) {
     k_tables_next<<<1, 256, 0, s>>>(acc, t->d[1 - t->cur]);
 }
 
-template <int TL, bool CTRL>
+template <int TL, bool CTRL, int UK>
 __global__ void __launch_bounds__(A_THREADS) k_apply_a(const __grid_constant__ AGateParams p,
                                                        const ATabData *__restrict__ cur,
                                                        const ATabData *__restrict__ nxt) {
@@ -692,35 +757,43 @@ __global__ void __launch_bounds__(A_THREADS) k_apply_a(const __grid_constant__ A
             selm |= (uint32_t)sel << k;
             float ra, rb;
             float2 xf = a_decode_f(f, c[j0], ra), yf = a_decode_f(f, c[j1], rb);
-            if (sel) a_gate_f(uf, xf, yf);
+            if (sel) a_gate_fu<UK>(uf, xf, yf);
             const float E = A_KF * (ra + rb);
             bool okx, oky;
             nc[j0] = a_encode_f(sm, f, xf, E, okx);
             nc[j1] = a_encode_f(sm, f, yf, E, oky);
             fail |= (uint32_t)!(okx && oky) << k;
         }
-        if (fail) a_unit_exact<TL>(sm, u, c, nc, fail, selm);
+        if (fail) a_unit_exact<TL, UK>(sm, u, c, nc, fail, selm);
         U::store(a, s0, p.t, nc);
     }
 }
 
-template <int TL>
+template <int TL, int UK>
 static void launch_apply_c(const AGateParams &p, const ATables *t, int grid, cudaStream_t s) {
     if (p.cmask)
-        k_apply_a<TL, true><<<grid, A_THREADS, 0, s>>>(p, tcur(t), tnext(t));
+        k_apply_a<TL, true, UK><<<grid, A_THREADS, 0, s>>>(p, tcur(t), tnext(t));
     else
-        k_apply_a<TL, false><<<grid, A_THREADS, 0, s>>>(p, tcur(t), tnext(t));
+        k_apply_a<TL, false, UK><<<grid, A_THREADS, 0, s>>>(p, tcur(t), tnext(t));
+}
+template <int UK>
+static void launch_apply_k(const AGateParams &p, const ATables *t, int grid, cudaStream_t s) {
+    switch (p.t < 4 ? p.t : 4) {
+        case 0: launch_apply_c<0, UK>(p, t, grid, s); break;
+        case 1: launch_apply_c<1, UK>(p, t, grid, s); break;
+        case 2: launch_apply_c<2, UK>(p, t, grid, s); break;
+        case 3: launch_apply_c<3, UK>(p, t, grid, s); break;
+        default: launch_apply_c<4, UK>(p, t, grid, s); break;
+    }
 }
 
 void launch_apply_a(const AGateParams &p, const ATables *t, cudaStream_t s) {
     const uint64_t units = (p.nl >= 4) ? (1ull << (p.nl - 4)) : 1ull;
     const int grid = a_grid(units);
-    switch (p.t < 4 ? p.t : 4) {
-        case 0: launch_apply_c<0>(p, t, grid, s); break;
-        case 1: launch_apply_c<1>(p, t, grid, s); break;
-        case 2: launch_apply_c<2>(p, t, grid, s); break;
-        case 3: launch_apply_c<3>(p, t, grid, s); break;
-        default: launch_apply_c<4>(p, t, grid, s); break;
+    switch (a_ukind(p.u)) {
+        case 1: launch_apply_k<1>(p, t, grid, s); break;
+        case 2: launch_apply_k<2>(p, t, grid, s); break;
+        default: launch_apply_k<0>(p, t, grid, s); break;
     }
 }
 
