@@ -154,9 +154,26 @@ def cpu_sample(circ_full, budget_s=15.0):
         t_all += time.perf_counter() - t0
         nbytes += gate_bytes(one)
         done += 1
-    return {"value": nbytes / t_all / 1e9, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"first {done} gates of the workload's circuit at N={n} ({t_all:.1f} s, "
-                      f"{done / t_all:.3f} gates/s)"}
+    out = {"value": nbytes / t_all / 1e9, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+           "sample": f"first {done} gates of the workload's circuit at N={n} ({t_all:.1f} s, "
+                     f"{done / t_all:.3f} gates/s)"}
+    # the same oracle on one thread (1 thread and all cores), a short sample
+    cores = oracle.num_threads()
+    try:
+        oracle.set_num_threads(1)
+        done1, t1, b1 = 0, 0.0, 0.0
+        while t1 < budget_s / 3 and done1 < len(circ):
+            one = circ.slice(done1, done1 + 1)
+            t0 = time.perf_counter()
+            oracle.e_run(a, n, one)
+            t1 += time.perf_counter() - t0
+            b1 += gate_bytes(one)
+            done1 += 1
+        out["one_thread"] = {"value": b1 / t1 / 1e9, "unit": UNIT, "cores": 1,
+                             "sample": f"first {done1} gates at N={n} ({t1:.1f} s)"}
+    finally:
+        oracle.set_num_threads(cores)
+    return out
 
 
 def run_reference(args, rank, world):

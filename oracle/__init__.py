@@ -67,6 +67,8 @@ def lib():
         L.oracle_a_run.argtypes = [_i8p, ctypes.c_int, _dp, _dp, ctypes.c_int64, _i32p, _i32p, _i32p, _i32p, _i32p,
                                    _dp, _dp]
         L.oracle_num_threads.restype = ctypes.c_int
+        L.oracle_set_num_threads.argtypes = [ctypes.c_int]
+        L.oracle_set_num_threads.restype = None
     return _lib
 
 
@@ -235,3 +237,8 @@ class AState:
 
 def num_threads() -> int:
     return lib().oracle_num_threads()
+
+
+def set_num_threads(n: int) -> None:
+    """OpenMP thread count of the oracle's loops (timing only; results unchanged)."""
+    lib().oracle_set_num_threads(int(n))

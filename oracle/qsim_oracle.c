@@ -434,3 +434,15 @@ int oracle_num_threads(void)
     return 1;
 #endif
 }
+
+/* thread count of the OpenMP loops (timing harness: SURVEY.md §8(d) times the
+ * oracle on 1 thread and on all cores); no effect on the results */
+void oracle_set_num_threads(int n)
+{
+#ifdef _OPENMP
+    extern void omp_set_num_threads(int);
+    omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
