@@ -166,7 +166,10 @@ struct Compiler {
     }
 
     std::vector<double> sc;
-    int add_table(const double *v, int n) {  // n = 2^(R+1): tables stay aligned to their size
+    int add_table(const double *v, int n, bool reuse = false) {  // n = 2^(R+1): tables stay aligned to their size
+        if (reuse)  // an identical table already in the pool (bitwise): share it
+            for (int at = 0; at + n <= (int)coef.size(); at += n)
+                if (std::memcmp(coef.data() + at, v, sizeof(double) * (size_t)n) == 0) return at;
         if ((int)coef.size() + n > max_coef) return -1;
         const int at = (int)coef.size();
         coef.insert(coef.end(), v, v + n);
@@ -452,20 +455,20 @@ int Compiler::compile_stage(const std::vector<int> &take, const int *Q) {
             if (p.tmask) sr.needs_xq = true;
         }
     };
-    auto table_at = [&](const std::vector<cd> &T) -> int {
+    auto table_at = [&](const std::vector<cd> &T, bool reuse) -> int {
         std::vector<double> buf(2 * NS);
         for (int k = 0; k < NS; ++k) {
             const cd e = T[A_apply(k)];
             buf[2 * k] = e.real();
             buf[2 * k + 1] = e.imag();
         }
-        return add_table(buf.data(), 2 * NS);
+        return add_table(buf.data(), 2 * NS, reuse);
     };
     // the pending tables (all variants, consecutive); fills the variant fields of o
     auto pending_tables = [&](LOp &o) -> int {
         int first = -1;
         for (const auto &P : PV) {
-            const int at = table_at(P);
+            const int at = table_at(P, PV.size() == 1);  // variants must stay consecutive
             if (at < 0) return -1;
             if (first < 0) first = at;
         }
@@ -478,7 +481,7 @@ int Compiler::compile_stage(const std::vector<int> &take, const int *Q) {
         return 0;
     };
     auto emit_table = [&](const std::vector<cd> &T, const Prim *cp) -> int {
-        const int at = table_at(T);
+        const int at = table_at(T, true);
         if (at < 0) return 1;
         LOp o{};
         o.code = LOP_CODE_DIAGT;
@@ -572,6 +575,32 @@ int Compiler::compile_stage(const std::vector<int> &take, const int *Q) {
                             for (int s = 0; s < NS; ++s) P[s] *= p.tab[s];
                         break;
                     case PK_DIAGC: {
+                        // a conditional diagonal on one logical slot (CPHASE / controlled
+                        // phase with its control outside the registers): two coefficients
+                        // in sc, no 2^R table in the coefficient pool
+                        int S1 = -1;
+                        for (int b = 0; b < R && S1 < 0; ++b) {
+                            bool ok1 = true;
+                            for (int sv = 0; sv < NS && ok1; ++sv)
+                                ok1 = p.tab[sv] == p.tab[((sv >> b) & 1) ? (1 << b) : 0];
+                            if (ok1) S1 = b;
+                        }
+                        if (S1 >= 0) {
+                            const double tv[4] = {p.tab[0].real(), p.tab[0].imag(), p.tab[1 << S1].real(),
+                                                  p.tab[1 << S1].imag()};
+                            const int at = add_sc(tv, 4);
+                            if (at < 0) return 1;
+                            LOp o{};
+                            o.code = LOP_CODE_DIAG1;
+                            o.rowS = Arow[S1];
+                            o.pm = pmask(Arow[S1]);
+                            o.coef = (uint16_t)at;
+                            o.gvec = (uint8_t)(p.tab[0] == cd(1.0, 0.0) ? 1 : 0);
+                            set_cond(o, p);
+                            ops.push_back(o);
+                            st.diagt++;
+                            break;
+                        }
                         const int rc = emit_table(p.tab, &p);
                         if (rc) return rc;
                         break;

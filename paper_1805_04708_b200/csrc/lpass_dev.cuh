@@ -265,6 +265,31 @@ __device__ __forceinline__ void lp_op1(double2 (&v)[1 << R], uint32_t &g, uint32
         g ^= (uint32_t)(h >> 24) & 0xffu;
         return;
     }
+    if (code == LOP_CODE_DIAG1) {
+        const uint32_t gp = lp_par(((uint32_t)(h >> 16) & 0xffu) & g);
+        const double *T = p.sc + coef;
+        const double t0r = T[0], t0i = T[1], t1r = T[2], t1i = T[3];
+        if ((h >> 24) & 1u) {  // T0 == 1: multiply the half with b = 1 only (uniform branch on gp)
+            const uint32_t want = gp ? 0u : 1u;
+#pragma unroll
+            for (int j = 0; j < NS; ++j) {
+                if (((o.pm >> j) & 1u) != want) continue;
+                const double pp = t1i * v[j].y, qq = t1i * v[j].x;
+                v[j].x = fma(t1r, v[j].x, -pp);
+                v[j].y = fma(t1r, v[j].y, qq);
+            }
+            return;
+        }
+#pragma unroll
+        for (int j = 0; j < NS; ++j) {
+            const bool b = (((o.pm >> j) & 1u) ^ gp) != 0;
+            const double cr = b ? t1r : t0r, ci = b ? t1i : t0i;
+            const double pp = ci * v[j].y, qq = ci * v[j].x;
+            v[j].x = fma(cr, v[j].x, -pp);
+            v[j].y = fma(cr, v[j].y, qq);
+        }
+        return;
+    }
     const uint32_t gp = lp_par(((uint32_t)(h >> 16) & 0xffu) & g);
     switch (code) {
 #define LP_V_CASES(VS)                                                                                    \

@@ -40,6 +40,11 @@ enum : uint8_t {
 };
 constexpr uint8_t LOP_CODE_DIAGT = 250;  // v[j] *= T[j ^ g]
 constexpr uint8_t LOP_CODE_FLIP = 251;   // g ^= gvec
+// DIAG1: a (conditional) diagonal that depends on one logical register slot S
+// only: v[j] *= T[b], b = par(rowS & (j ^ g)) (pm: bit j = par(rowS & j)),
+// T = (T0, T1) complex at sc[coef .. coef + 4) -- no 2^R table in the pool;
+// gvec bit 0 set: T0 == 1 exactly (controlled phases), only the b = 1 half moves
+constexpr uint8_t LOP_CODE_DIAG1 = 253;
 // ROUND: v[j] *= T[j ^ g] (T at coef, 2^R complex), then for every register bit
 // r in gvec (ascending) a lifted shear on the pairs (j0, j0 | 2^r) with
 // (t_r, a_r) = coef[2^(R+1) + 2k], coef[2^(R+1) + 2k + 1]:

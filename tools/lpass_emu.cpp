@@ -138,6 +138,12 @@ static void emu_pass(const LPassParams &p, cd *a) {
                         g ^= o.gvec;
                         continue;
                     }
+                    if (o.code == LOP_CODE_DIAG1) {
+                        const int gp = __builtin_popcount(o.rowS & g) & 1;
+                        const cd t0(p.sc[o.coef], p.sc[o.coef + 1]), t1(p.sc[o.coef + 2], p.sc[o.coef + 3]);
+                        for (int j = 0; j < NS; ++j) v[j] *= ((((o.pm >> j) & 1) ^ gp) ? t1 : t0);
+                        continue;
+                    }
                     const int type = o.code >> 4, V = lp_vec(R, o.code & 15);
                     const int hb = 31 - __builtin_clz((unsigned)V);
                     const uint32_t gp = par(o.rowS & g);
