@@ -585,6 +585,38 @@ int Compiler::compile_stage(const std::vector<int> &take, const int *Q) {
                                 ok1 = p.tab[sv] == p.tab[((sv >> b) & 1) ? (1 << b) : 0];
                             if (ok1) S1 = b;
                         }
+                        // T0 = 1 under one condition bit (= 1): a PHASES term, merged into the
+                        // previous op when that is a PHASES op on the same slot whose terms end
+                        // the scalar array
+                        int pcode = -1;
+                        if (S1 >= 0 && p.tab[0] == cd(1.0, 0.0)) {
+                            if (p.tmask && !p.omask && __builtin_popcount(p.tmask) == 1 && p.tval == p.tmask)
+                                pcode = __builtin_ctz(p.tmask);
+                            else if (!p.tmask && p.omask && __builtin_popcountll(p.omask) == 1 && p.oval == p.omask)
+                                pcode = 64 + __builtin_ctzll(p.omask);
+                        }
+                        if (pcode >= 0) {
+                            const double term[3] = {(double)pcode, p.tab[1 << S1].real(), p.tab[1 << S1].imag()};
+                            LOp *last = ops.size() > (size_t)sr.op0 ? &ops.back() : nullptr;
+                            if (last && last->code == LOP_CODE_PHASES && last->rowS == Arow[S1] && last->nctl < 255 &&
+                                (int)sc.size() == last->coef + 3 * last->nctl) {
+                                if (add_sc(term, 3) < 0) return 1;
+                                last->nctl++;
+                            } else {
+                                const int at = add_sc(term, 3);
+                                if (at < 0) return 1;
+                                LOp o{};
+                                o.code = LOP_CODE_PHASES;
+                                o.rowS = Arow[S1];
+                                o.pm = pmask(Arow[S1]);
+                                o.coef = (uint16_t)at;
+                                o.nctl = 1;
+                                ops.push_back(o);
+                            }
+                            if (pcode < 64) sr.needs_xq = true;
+                            st.diagt++;
+                            break;
+                        }
                         if (S1 >= 0) {
                             const double tv[4] = {p.tab[0].real(), p.tab[0].imag(), p.tab[1 << S1].real(),
                                                   p.tab[1 << S1].imag()};

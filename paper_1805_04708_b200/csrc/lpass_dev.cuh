@@ -265,6 +265,31 @@ __device__ __forceinline__ void lp_op1(double2 (&v)[1 << R], uint32_t &g, uint32
         g ^= (uint32_t)(h >> 24) & 0xffu;
         return;
     }
+    if (code == LOP_CODE_PHASES) {
+        const double *T = p.sc + coef;
+        const int nt = (int)((h >> 48) & 0xffu);
+        double cr = 1.0, ci = 0.0;
+        for (int k = 0; k < nt; ++k) {
+            const int c = (int)T[3 * k];
+            const uint32_t bit = c < 64 ? (xq >> c) & 1u : (uint32_t)(full >> (c - 64)) & 1u;
+            if (bit) {
+                const double er = T[3 * k + 1], ei = T[3 * k + 2];
+                const double nr = fma(cr, er, -ci * ei);
+                ci = fma(cr, ei, ci * er);
+                cr = nr;
+            }
+        }
+        const uint32_t gp = lp_par(((uint32_t)(h >> 16) & 0xffu) & g);
+        const uint32_t want = gp ? 0u : 1u;
+#pragma unroll
+        for (int j = 0; j < NS; ++j) {
+            if (((o.pm >> j) & 1u) != want) continue;
+            const double pp = ci * v[j].y, qq = ci * v[j].x;
+            v[j].x = fma(cr, v[j].x, -pp);
+            v[j].y = fma(cr, v[j].y, qq);
+        }
+        return;
+    }
     if (code == LOP_CODE_DIAG1) {
         const uint32_t gp = lp_par(((uint32_t)(h >> 16) & 0xffu) & g);
         const double *T = p.sc + coef;

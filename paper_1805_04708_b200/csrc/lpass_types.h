@@ -45,6 +45,13 @@ constexpr uint8_t LOP_CODE_FLIP = 251;   // g ^= gvec
 // T = (T0, T1) complex at sc[coef .. coef + 4) -- no 2^R table in the pool;
 // gvec bit 0 set: T0 == 1 exactly (controlled phases), only the b = 1 half moves
 constexpr uint8_t LOP_CODE_DIAG1 = 253;
+// PHASES: adjacent controlled phases on one logical register slot S, each
+// under one condition bit outside the registers: per group the product
+// c = prod_k (bit_k ? e_k : 1) over the nctl terms at sc[coef + 3k] = (code,
+// re, im) (code: tile bit b -> b, full-index bit b -> 64 + b), then v[j] *= c
+// where par(rowS & (j ^ g)) = 1 -- one complex multiply per term per group
+// instead of per amplitude (the QFT's CPHASE ladders)
+constexpr uint8_t LOP_CODE_PHASES = 254;
 // ROUND: v[j] *= T[j ^ g] (T at coef, 2^R complex), then for every register bit
 // r in gvec (ascending) a lifted shear on the pairs (j0, j0 | 2^r) with
 // (t_r, a_r) = coef[2^(R+1) + 2k], coef[2^(R+1) + 2k + 1]:

@@ -138,6 +138,19 @@ static void emu_pass(const LPassParams &p, cd *a) {
                         g ^= o.gvec;
                         continue;
                     }
+                    if (o.code == LOP_CODE_PHASES) {
+                        cd c(1.0, 0.0);
+                        for (int k = 0; k < o.nctl; ++k) {
+                            const int cc = (int)p.sc[o.coef + 3 * k];
+                            const uint32_t bit =
+                                cc < 64 ? (xq >> cc) & 1u : (uint32_t)((full >> (cc - 64)) & 1u);
+                            if (bit) c *= cd(p.sc[o.coef + 3 * k + 1], p.sc[o.coef + 3 * k + 2]);
+                        }
+                        const int gp = __builtin_popcount(o.rowS & g) & 1;
+                        for (int j = 0; j < NS; ++j)
+                            if (((o.pm >> j) & 1) ^ gp) v[j] *= c;
+                        continue;
+                    }
                     if (o.code == LOP_CODE_DIAG1) {
                         const int gp = __builtin_popcount(o.rowS & g) & 1;
                         const cd t0(p.sc[o.coef], p.sc[o.coef + 1]), t1(p.sc[o.coef + 2], p.sc[o.coef + 3]);
