@@ -563,7 +563,7 @@ def test_all_to_all_remap_loopback(P, monkeypatch):
     assert st["exchange_bytes"] < st0["exchange_bytes"]
 
 
-def _run_n22(mode, tmp_path):
+def _run_n22(mode, tmp_path, recipe="C.layered(n, 3, seed=1)", n=22):
     import os
     import subprocess
     import sys
@@ -571,8 +571,8 @@ def _run_n22(mode, tmp_path):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = str(tmp_path / f"state_{mode}.npy")
     code = ("import sys, numpy as np; sys.path.insert(0, %r); import paper_1805_04708_b200 as q, qsim_inputs as C; "
-            "n = 22; s = q.State(n, q.ENC_FP64, 1); s.apply_circuit(C.layered(n, 3, seed=1)); st = s.stats(); "
-            "np.save(%r, s.get_state()); print(st['jit_passes'], st['passes'])" % (root, out))
+            "n = %d; s = q.State(n, q.ENC_FP64, 1); s.apply_circuit(%s); st = s.stats(); "
+            "np.save(%r, s.get_state()); print(st['jit_passes'], st['passes'])" % (root, n, recipe, out))
     env = dict(os.environ, QSIM_LPASS_JIT=str(mode))
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr
@@ -591,3 +591,18 @@ def test_specialised_pass_kernels_match_the_interpreter_and_the_oracle(tmp_path)
     assert np.max(np.abs(a - b)) <= 1e-14
     ref = oracle.e_simulate(22, C.layered(22, 3, seed=1))
     assert np.max(np.abs(a - ref)) <= TOL
+
+
+@pytest.mark.parametrize("recipe,n", [("C.qft(n, seed=5)[0]", 20), ("C.random_circuit(n, 400, seed=11)", 16),
+                                      ("C.config(3, n=n)", 18)])
+def test_specialised_kernels_with_phase_ops_match_the_oracle(tmp_path, recipe, n):
+    """Specialised pass kernels compiled before their first launch
+    (QSIM_LPASS_JIT=2) on programs with DIAG1 / PHASES ops (QFT ladders,
+    controlled phases with outside controls, random gate mixes, the config-4
+    recipe in E): the state equals the interpreter's and the oracle's."""
+    a, jit, passes = _run_n22(2, tmp_path, recipe, n)
+    b, jit0, _ = _run_n22(0, tmp_path, recipe, n)
+    assert passes > 0 and jit == passes and jit0 == 0
+    assert np.max(np.abs(a - b)) <= 1e-14
+    circ = eval(recipe, {"C": C, "n": n})
+    assert np.max(np.abs(a - oracle.e_simulate(n, circ))) <= TOL
