@@ -105,9 +105,10 @@ int launch_lpass_e(const LPassParams &p, struct CUstream_st *stream);
 void lpass_jit_sync();      // wait for every queued specialisation
 void lpass_jit_shutdown();  // stop and join the compile threads (before process exit)
 // CUDA source of the kernel specialised to this program (R register qubits,
-// minb CTAs per SM, nt threads per CTA): lp_body with literal stages and ops
+// minb CTAs per SM, nt threads per CTA, ng register groups per thread at
+// once): lp_body with literal stages and ops
 // (lpass_dev.cuh)
-std::string lpass_jit_source(const LPassParams &p, int R, int minb, int nt = LP_THREADS);
+std::string lpass_jit_source(const LPassParams &p, int R, int minb, int nt = LP_THREADS, int ng = 1);
 void lpass_launch_counts(long long *jit, long long *interp);  // specialised (NVRTC) / interpreter launches so far
 
 }  // namespace qsim

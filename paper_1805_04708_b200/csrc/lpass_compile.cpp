@@ -1507,7 +1507,7 @@ int lpass_run(const LGate *gates, int ng, const LRunConfig &cfg, LPassSink &sink
 // with the stage as a literal LStage and a functor holding its ops as literal
 // LOps (lp_op1 folds to straight-line code); the tile width is a template
 // constant.
-std::string lpass_jit_source(const LPassParams &p, int R, int minb, int nt) {
+std::string lpass_jit_source(const LPassParams &p, int R, int minb, int nt, int ng) {
     std::string s;
     s.reserve(8192);
     s += "#include \"lpass_dev.cuh\"\n";
@@ -1553,8 +1553,8 @@ std::string lpass_jit_source(const LPassParams &p, int R, int minb, int nt) {
                  S.qbit[4], S.needs_xq, S.first_op, S.nops, S.ev_mask);
         s += buf;
         s += ev + "};\n";
-        snprintf(buf, sizeof buf, "      qsim::lp_stage<%d, %d, JitOps%d<%d>, %d>(p, t, S, JitOps%d<%d>{}); }\n", R, p.K,
-                 st, R, nt, st, R);
+        snprintf(buf, sizeof buf, "      qsim::lp_stage<%d, %d, JitOps%d<%d>, %d, %d>(p, t, S, JitOps%d<%d>{}); }\n", R,
+                 p.K, st, R, nt, ng, st, R);
         s += buf;
     }
     s += "  }\n};\n";

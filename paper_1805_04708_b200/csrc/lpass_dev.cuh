@@ -362,7 +362,7 @@ struct LpTile {
 // register basis) is loaded from shared memory, `ops(v, g, xq, full, p,
 // smem, cpool_off)` applies the stage's ops, and it is stored back.  KK: the
 // tile width when known at compile time (0: p.K); NT: threads per CTA.
-template <int R, int KK, class Ops, int NT = LP_THREADS>
+template <int R, int KK, class Ops, int NT = LP_THREADS, int G = 1>
 __device__ __forceinline__ void lp_stage(const LPassParams &p, const LpTile &t, const LStage &st, const Ops &ops) {
     constexpr int NS = 1 << R;
     const int K = KK ? KK : p.K;
@@ -393,6 +393,44 @@ __device__ __forceinline__ void lp_stage(const LPassParams &p, const LpTile &t, 
             a0t ^= (uint32_t)st.grp_phys[i] << 4;
             xqt ^= st.grp_log[i];
         }
+    if constexpr (G == 2) {
+        // two register groups per thread, every op applied to both (independent
+        // work for the scheduler to interleave); needs ngroups == 2 NT
+        uint32_t a0[2], xq[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            a0[k] = a0t;
+            xq[k] = nxq ? xqt : yrest;
+            if (k) {
+                a0[k] ^= (uint32_t)st.grp_phys[TB] << 4;
+                if (nxq) xq[k] ^= st.grp_log[TB];
+            }
+        }
+        double2 v0[NS], v1[NS];
+#pragma unroll
+        for (int j = 0; j < NS; ++j) {
+            uint32_t ad = 0;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (j & (1 << r)) ad ^= rp[r];
+            v0[j] = *reinterpret_cast<const double2 *>(smem_raw + (a0[0] ^ ad));
+            v1[j] = *reinterpret_cast<const double2 *>(smem_raw + (a0[1] ^ ad));
+        }
+        uint32_t g_0 = g0, g_1 = g0;
+        ops(v0, g_0, xq[0], t.full, p, smem_raw, t.cpool_off);
+        ops(v1, g_1, xq[1], t.full, p, smem_raw, t.cpool_off);
+#pragma unroll
+        for (int j = 0; j < NS; ++j) {
+            uint32_t ad = 0;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (j & (1 << r)) ad ^= rp[r];
+            *reinterpret_cast<double2 *>(smem_raw + (a0[0] ^ ad)) = v0[j];
+            *reinterpret_cast<double2 *>(smem_raw + (a0[1] ^ ad)) = v1[j];
+        }
+        __syncthreads();
+        return;
+    }
     for (uint32_t grp = tid; grp < ngroups; grp += NT) {
         uint32_t a0 = a0t, xq = nxq ? xqt : yrest;
         for (int i = TB; i < K - R; ++i)
