@@ -40,7 +40,8 @@ amp_bytes = 2 if enc == q.ENC_ADAPTIVE2 else 16
 shard_bytes = float(2 ** n) * amp_bytes
 kinds = [("dense", U, lambda t: ()), ("cnot", C.mat_X(), lambda t: ((t + 1) % n,)), ("T", C.mat_T(), lambda t: ())]
 if enc == q.ENC_ADAPTIVE2:
-    kinds = [("dense", U, lambda t: ()), ("Rz", C.mat_Rz(0.7), lambda t: ())]
+    kinds = [("dense", U, lambda t: ()), ("Rx", C.mat_Rx(0.7), lambda t: ()), ("H", C.mat_H(), lambda t: ()),
+             ("Rz", C.mat_Rz(0.7), lambda t: ())]
 
 out = {"enc": enc_name, "n": n, "reps": reps, "warmup": warm, "unit": "ms per gate (CUDA events, library stream)",
        "rows": []}
