@@ -1157,6 +1157,9 @@ int lpass_compile(const LGate *gates, int ng, int nl, int K, int R, const int *t
     c.R = R;
     c.max_coef = max_coef;
     c.allow_carry = deferred != nullptr;
+    // the lookahead costs host time per stage: worth it when a pass is long
+    // (2^(nl-K) >= 1024 tiles); small states keep first-come register sets
+    c.lookahead = nl - K >= 10 ? 1 : 0;
     if (const char *e = getenv("LPASS_LOOKAHEAD")) c.lookahead = atoi(e);
     if (const char *e = getenv("LPASS_FLIP_PENALTY")) c.flip_penalty = atoi(e);
     for (int q = 0; q < 64; ++q) c.tbit_of[q] = -1;
@@ -1395,7 +1398,9 @@ int lpass_run(const LGate *gates, int ng, const LRunConfig &cfg, LPassSink &sink
         }
         return score;
     };
-    static const int search = getenv("LPASS_SEARCH") ? atoi(getenv("LPASS_SEARCH")) : 3;
+    // the search costs host time per pass: small states (< 1024 tiles) skip it
+    static const int search_env = getenv("LPASS_SEARCH") ? atoi(getenv("LPASS_SEARCH")) : -1;
+    const int search = search_env >= 0 ? search_env : (nl - K >= 10 ? 3 : 0);
     while (!pend.empty()) {
         std::vector<char> done;
         std::vector<int> high;

@@ -24,19 +24,29 @@ def emu(tmp_path_factory):
     return exe
 
 
+# the register-set lookahead and the pass-former search run by default only on
+# large states (>= 1024 tiles); the emulator's cases are small, so they are
+# also checked with both forced on
+FORCED = {"LPASS_LOOKAHEAD": "1", "LPASS_SEARCH": "3"}
+
+
+@pytest.mark.parametrize("forced", [False, True])
 @pytest.mark.parametrize("seed", [1, 2, 3])
-def test_compiled_program_equals_sequential_application(emu, seed):
-    out = subprocess.run([emu, "300", str(seed)], capture_output=True, text=True, timeout=300)
+def test_compiled_program_equals_sequential_application(emu, seed, forced):
+    env = dict(os.environ, **FORCED) if forced else None
+    out = subprocess.run([emu, "300", str(seed)], capture_output=True, text=True, timeout=300, env=env)
     assert out.returncode == 0, out.stdout + out.stderr
     assert out.stdout.startswith("ok"), out.stdout
 
 
+@pytest.mark.parametrize("forced", [False, True])
 @pytest.mark.parametrize("seed", [1, 2])
-def test_scheduler_whole_circuits(emu, seed):
+def test_scheduler_whole_circuits(emu, seed, forced):
     """lpass_run (the runtime's pass scheduler, with diagonals carried across
     stages and deferred across passes) on whole random and layered circuits:
     terminates and equals sequential application."""
-    out = subprocess.run([emu, "30", str(seed), "run"], capture_output=True, text=True, timeout=300)
+    env = dict(os.environ, **FORCED) if forced else None
+    out = subprocess.run([emu, "30", str(seed), "run"], capture_output=True, text=True, timeout=300, env=env)
     assert out.returncode == 0, out.stdout + out.stderr
     assert out.stdout.startswith("ok"), out.stdout
 
@@ -78,7 +88,7 @@ def test_specialised_kernel_sources_compile(emu, tmp_path):
                "typedef int int32_t;\ntypedef long long int64_t;\n")
     for k in range(2):
         src = prelude + open(tmp_path / f"jit_{k}.cu").read()
-        assert "lp_stage<4, 12, JitOps0<4>, 128>" in src and "constexpr qsim::LOp" in src
+        assert "lp_stage<4, 12, JitOps0<4>, 128, 1>" in src and "constexpr qsim::LOp" in src
         err, prog = nvrtc.nvrtcCreateProgram(src.encode(), b"lpass_jit.cu", 2, hdrs,
                                              [b"lpass_types.h", b"lpass_dev.cuh"])
         opts = [b"--gpu-architecture=sm_100a", b"-std=c++17", b"-default-device"]
