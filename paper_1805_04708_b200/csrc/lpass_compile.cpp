@@ -1362,7 +1362,44 @@ int lpass_run(const LGate *gates, int ng, const LRunConfig &cfg, LPassSink &sink
     static const double w_other = getenv("LPASS_W") ? atof(getenv("LPASS_W")) : 0.3;
     static const int best_impr = getenv("LPASS_BEST") ? atoi(getenv("LPASS_BEST")) : 0;
     static const bool pairs_ok = getenv("LPASS_PAIRS") ? atoi(getenv("LPASS_PAIRS")) != 0 : true;
-    auto select = [&](uint64_t forbid, std::vector<int> &sel_, std::vector<int> &high_, std::vector<char> &done_) {
+    // score of the plain greedy pass over the gates not in `skip` (the pass
+    // that would follow): the search's two-pass lookahead
+    auto next_score = [&](const std::vector<char> &skip) {
+        std::vector<int> hi;
+        uint64_t bx = 0, bz = 0;
+        double score = 0.0;
+        int nsel = 0;
+        for (size_t k = 0; k < pend.size() && nsel < LP_MAX_PASS_GATES; ++k) {
+            if (skip[k]) continue;
+            const Item &it = pend[k];
+            bool ok = !((it.xq & (bx | bz)) || (it.zq & bx));
+            if (ok && it.needs_reg) {
+                const int t = it.g.t;
+                if (t >= LP_LOW && std::find(hi.begin(), hi.end(), t) == hi.end()) {
+                    if ((int)hi.size() >= hmax)
+                        ok = false;
+                    else
+                        hi.push_back(t);
+                }
+                if (ok && it.g.nctl == 1) {
+                    const int c = it.g.ctl[0];
+                    if (c >= LP_LOW && c < nl && (int)hi.size() < hmax &&
+                        std::find(hi.begin(), hi.end(), c) == hi.end())
+                        hi.push_back(c);
+                }
+            }
+            if (ok) {
+                ++nsel;
+                score += it.needs_reg ? 1.0 : w_other;
+            } else {
+                bx |= it.xq;
+                bz |= it.zq;
+            }
+        }
+        return score;
+    };
+    static const double beta = getenv("LPASS_SCORE2") ? atof(getenv("LPASS_SCORE2")) : 0.75;
+    auto select1 = [&](uint64_t forbid, std::vector<int> &sel_, std::vector<int> &high_, std::vector<char> &done_) {
         done_.assign(pend.size(), 0);
         high_.clear();
         sel_.clear();
@@ -1397,6 +1434,10 @@ int lpass_run(const LGate *gates, int ng, const LRunConfig &cfg, LPassSink &sink
             }
         }
         return score;
+    };
+    auto select = [&](uint64_t forbid, std::vector<int> &sel_, std::vector<int> &high_, std::vector<char> &done_) {
+        const double s1 = select1(forbid, sel_, high_, done_);
+        return beta > 0.0 ? s1 + beta * next_score(done_) : s1;
     };
     // the search costs host time per pass: small states (< 1024 tiles) skip it
     static const int search_env = getenv("LPASS_SEARCH") ? atoi(getenv("LPASS_SEARCH")) : -1;
