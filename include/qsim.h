@@ -137,6 +137,16 @@ int qsim_nccl_unique_id(uint8_t out[128]);
  * ENOTUNITARY. */
 int qsim_apply_gate(qsim_state *s, const double u[8], int target, const int *controls, int ncontrols);
 
+/* A k-qubit unitary U (k = 1..3: SPEC's apply_two / apply_three) on logical
+ * qubits[0..k): U is 2^k x 2^k complex, row-major, interleaved (re, im);
+ * qubits[0] is the MOST significant bit of the matrix index (reading A14),
+ * i.e. U[r][c] maps basis state c to r with bit (k-1-b) of r/c = qubit b.
+ * Global qubits of the set are first brought to local bits by half-shard
+ * swap exchanges; one sweep over the shard (32 B per
+ * amplitude).  E encoding only (A: QSIM_EUNSUPPORTED).  Errors: EINVAL (k,
+ * range, duplicates, non-finite), ENOTUNITARY (||U^dagger U - I||_max > 1e-10). */
+int qsim_apply_matrix(qsim_state *s, const double *U, const int *qubits, int k);
+
 /* SWAP(q1, q2) as a qubit-map relabelling (0 bytes moved).  EINVAL. */
 int qsim_apply_swap(qsim_state *s, int q1, int q2);
 

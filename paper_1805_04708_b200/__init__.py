@@ -92,7 +92,7 @@ EXPORTS = (
     "qsim_aux_amplitudes", "qsim_aux_num_vars", "qsim_set_qubit_map",
     "qsim_asm_parse", "qsim_asm_info", "qsim_asm_get_op", "qsim_asm_destroy", "qsim_asm_run",
     "qsim_asm_result_get", "qsim_asm_result_destroy",
-    "qsim_overlap", "qsim_jit_sync", "qsim_jit_shutdown", "qsim_graph_begin", "qsim_graph_end", "qsim_graph_launch", "qsim_graph_destroy",
+    "qsim_overlap", "qsim_apply_matrix", "qsim_jit_sync", "qsim_jit_shutdown", "qsim_graph_begin", "qsim_graph_end", "qsim_graph_launch", "qsim_graph_destroy",
 )
 
 if not os.path.exists(_LIB_PATH):
@@ -145,6 +145,7 @@ _lib.qsim_get_codes.argtypes = [_P, ctypes.POINTER(ctypes.c_int8), _dp, _dp]
 _lib.qsim_set_codes.argtypes = [_P, ctypes.POINTER(ctypes.c_int8), ctypes.c_double, ctypes.c_double]
 _lib.qsim_sync.argtypes = [_P]
 _lib.qsim_overlap.argtypes = [_P, _P, _dp]
+_lib.qsim_apply_matrix.argtypes = [_P, _dp, _ip, ctypes.c_int]
 _lib.qsim_jit_sync.argtypes = []
 _lib.qsim_jit_shutdown.argtypes = []
 # stop the fused-pass compile threads before the C exit handlers run (qsim.h)
@@ -440,6 +441,14 @@ def qsim_jit_sync():
     _check(_lib.qsim_jit_sync())
 
 
+def qsim_apply_matrix(h, u, qubits):
+    """k-qubit unitary (k = len(qubits) <= 3), qubits[0] the most significant matrix index."""
+    k = len(qubits)
+    m = np.ascontiguousarray(np.asarray(u, dtype=np.complex128).reshape(1 << k, 1 << k)).view(np.float64).reshape(-1)
+    q = (ctypes.c_int * k)(*[int(x) for x in qubits])
+    _check(_lib.qsim_apply_matrix(h, m.ctypes.data_as(_dp), q, k))
+
+
 def qsim_overlap(ha, hb) -> complex:
     out = (ctypes.c_double * 2)()
     _check(_lib.qsim_overlap(ha, hb, out))
@@ -608,6 +617,10 @@ class State:
 
     def stream(self):
         return qsim_stream(self.h)
+
+    def apply_matrix(self, u, qubits):
+        qsim_apply_matrix(self.h, u, qubits)
+        return self
 
     def overlap(self, other):
         """<self|other> (qsim_overlap)."""

@@ -1373,6 +1373,90 @@ int qsim_apply_gate(qsim_state *s, const double u[8], int target, const int *con
     return qsim_apply_circuit(s, &g, 1);
 }
 
+int qsim_apply_matrix(qsim_state *s, const double *U, const int *qubits, int k) {
+    if (!s || !U || !qubits || k < 1 || k > 3) {
+        set_error("qsim_apply_matrix: bad arguments (k must be 1..3)");
+        return QSIM_EINVAL;
+    }
+    for (int b = 0; b < k; ++b) {
+        if (qubits[b] < 0 || qubits[b] >= s->n) {
+            set_error("qsim_apply_matrix: qubit out of range");
+            return QSIM_EINVAL;
+        }
+        for (int c = 0; c < b; ++c)
+            if (qubits[c] == qubits[b]) {
+                set_error("qsim_apply_matrix: duplicate qubits");
+                return QSIM_EINVAL;
+            }
+    }
+    const int M = 1 << k;
+    for (int i = 0; i < 2 * M * M; ++i)
+        if (!std::isfinite(U[i])) {
+            set_error("qsim_apply_matrix: non-finite matrix entry");
+            return QSIM_EINVAL;
+        }
+    // ||U^dagger U - I||_max <= 1e-10 (the same bound as qsim_apply_gate)
+    for (int r = 0; r < M; ++r)
+        for (int c = 0; c < M; ++c) {
+            double re = 0.0, im = 0.0;
+            for (int m = 0; m < M; ++m) {
+                const double ar = U[2 * (m * M + r)], ai = -U[2 * (m * M + r) + 1];  // conj(U[m][r])
+                const double br = U[2 * (m * M + c)], bi = U[2 * (m * M + c) + 1];
+                re += ar * br - ai * bi;
+                im += ar * bi + ai * br;
+            }
+            if (std::fabs(re - (r == c ? 1.0 : 0.0)) > 1e-10 || std::fabs(im) > 1e-10) {
+                set_error("qsim_apply_matrix: ||U^dagger U - I||_max > 1e-10");
+                return QSIM_ENOTUNITARY;
+            }
+        }
+    if (s->enc != QSIM_ENC_FP64) {
+        set_error("qsim_apply_matrix: E encoding only");
+        return QSIM_EUNSUPPORTED;
+    }
+    cudaSetDevice(s->dev);
+    // bring every global qubit of the set to a local bit (half-shard swap
+    // exchanges), victims outside the set
+    for (int b = 0; b < k; ++b) {
+        const int pb = s->pl.pos[qubits[b]];
+        if (pb < s->nl) continue;
+        int avoid[3];
+        int na = 0;
+        for (int c = 0; c < k; ++c)
+            if (s->pl.pos[qubits[c]] < s->nl) avoid[na++] = s->pl.pos[qubits[c]];
+        const int l = s->pl.choose_victim(nullptr, 0, 0, avoid, na, false);
+        if (l < 0) {
+            set_error("qsim_apply_matrix: no local bit left for the exchange");
+            return QSIM_EINVAL;
+        }
+        PlanOp x{};
+        x.type = QSIM_OP_EXCHANGE;
+        x.g = pb;
+        x.l = l;
+        RC(exchange(s, x, nullptr, nullptr));
+        s->pl.swap_bits(pb, l);
+    }
+    MatKParams p{};
+    p.k = k;
+    p.ngroups = 1ull << (s->nl - k);
+    for (int b = 0; b < k; ++b) p.phys[b] = p.sorted[b] = s->pl.pos[qubits[b]];
+    std::sort(p.sorted, p.sorted + k);
+    std::memcpy(p.u, U, sizeof(double) * 2 * M * M);
+    for (auto &sh : s->shards) {
+        p.a = sh.amps;
+        prof_begin(s);
+        launch_matk_e(p, s->stream);
+        prof_end(s, QSIM_K_SWEEP, std::ldexp(32.0, s->nl), std::ldexp(8.0 * M, s->nl));
+        s->st.kernels++;
+        s->st.sweeps++;
+        s->st.hbm_bytes += std::ldexp(32.0, s->nl);
+        s->st.gate_bytes += std::ldexp(32.0, s->nl);
+    }
+    s->st.gates++;
+    CU(cudaGetLastError());
+    return QSIM_OK;
+}
+
 int qsim_apply_swap(qsim_state *s, int q1, int q2) {
     if (!s) return QSIM_EINVAL;
     qsim_gate g{};

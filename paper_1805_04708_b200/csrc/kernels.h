@@ -112,6 +112,18 @@ void launch_pass_e(const PassParams &p, int grid, cudaStream_t s);
 int pass_e_max_grid(int R);
 int pass_e_max_k();  // tile qubits of the selected pass-kernel occupancy
 
+// ---- k-qubit dense matrix (qsim_apply_matrix) ---------------------------------
+struct MatKParams {
+    void *a;
+    uint64_t ngroups;   // 2^(nl - k)
+    int32_t k;
+    int32_t phys[3];    // physical bit of matrix index bit k-1-b (qubits[b])
+    int32_t sorted[3];  // the same bits ascending (zero insertion)
+    int32_t pad;
+    double u[128];      // 2^k x 2^k complex, row-major interleaved
+};
+void launch_matk_e(const MatKParams &p, cudaStream_t s);
+
 // ---- exchange-fused gate (a7) ------------------------------------------------
 struct XchgParams {
     void *own;             // this shard

@@ -99,6 +99,53 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_sweep_e(const __grid_constant
     }
 }
 
+// k-qubit dense matrix (qsim_apply_matrix, k = 1..3): every group of 2^k
+// amplitudes that differ only in the k physical bits, matrix index bit
+// (k-1-b) <-> physical bit phys[b] (qubits[0] the most significant, reading
+// A14), y = U x with U row-major 2^k x 2^k complex.
+template <int K>
+__global__ void __launch_bounds__(256) k_matk_e(const __grid_constant__ MatKParams p) {
+    constexpr int M = 1 << K;
+    double2 *__restrict__ a = reinterpret_cast<double2 *>(p.a);
+    for (uint64_t w = (uint64_t)blockIdx.x * 256 + threadIdx.x; w < p.ngroups; w += (uint64_t)gridDim.x * 256) {
+        uint64_t base = w;
+        for (int b = 0; b < K; ++b) base = insert_zero(base, p.sorted[b]);
+        uint64_t idx[M];
+        double2 x[M];
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            uint64_t i = base;
+#pragma unroll
+            for (int b = 0; b < K; ++b)
+                if ((m >> (K - 1 - b)) & 1) i |= 1ull << p.phys[b];
+            idx[m] = i;
+            x[m] = a[i];
+        }
+#pragma unroll
+        for (int r = 0; r < M; ++r) {
+            double yr = 0.0, yi = 0.0;
+#pragma unroll
+            for (int c = 0; c < M; ++c) {
+                const double ur = p.u[2 * (r * M + c)], ui = p.u[2 * (r * M + c) + 1];
+                yr = fma(ur, x[c].x, fma(-ui, x[c].y, yr));
+                yi = fma(ur, x[c].y, fma(ui, x[c].x, yi));
+            }
+            a[idx[r]] = make_double2(yr, yi);
+        }
+    }
+}
+
+void launch_matk_e(const MatKParams &p, cudaStream_t s) {
+    uint64_t cap = (uint64_t)num_sms() * 8, need = (p.ngroups + 255) / 256;
+    const int grid = (int)(need < cap ? (need ? need : 1) : cap);
+    if (p.k == 1)
+        k_matk_e<1><<<grid, 256, 0, s>>>(p);
+    else if (p.k == 2)
+        k_matk_e<2><<<grid, 256, 0, s>>>(p);
+    else
+        k_matk_e<3><<<grid, 256, 0, s>>>(p);
+}
+
 static int sweep_grid(uint64_t nitems) {
     uint64_t per = (uint64_t)SWEEP_THREADS * SWEEP_ILP;
     uint64_t need = (nitems + per - 1) / per;

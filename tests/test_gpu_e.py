@@ -606,3 +606,75 @@ def test_specialised_kernels_with_phase_ops_match_the_oracle(tmp_path, recipe, n
     assert np.max(np.abs(a - b)) <= 1e-14
     circ = eval(recipe, {"C": C, "n": n})
     assert np.max(np.abs(a - oracle.e_simulate(n, circ))) <= TOL
+
+
+def _apply_matrix_ref(psi, n, U, qubits):
+    """Test-side reference: U (2^k x 2^k, qubits[0] the most significant index)
+    on a logical state vector (numpy; bit j of the index = qubit j)."""
+    k = len(qubits)
+    t = psi.reshape((2,) * n)  # axis a <-> qubit n-1-a
+    axes = [n - 1 - q for q in qubits]
+    Ut = U.reshape((2,) * (2 * k))
+    out = np.tensordot(Ut, t, axes=(list(range(k, 2 * k)), axes))
+    # tensordot puts the k output axes first, in qubits order; move them back
+    out = np.moveaxis(out, list(range(k)), axes)
+    return out.reshape(-1)
+
+
+def test_apply_matrix_pins_and_random_unitaries():
+    """qsim_apply_matrix (SPEC apply_two / apply_three): kron(A, B) on
+    (q1, q0) equals A on q1 then B on q0; the 8x8 Toffoli matrix equals the
+    Toffoli gate; Haar 4x4 / 8x8 on a random state equal the test-side
+    tensor contraction; P = 2 loopback with a qubit on the global bit."""
+    n = 9
+    rng = np.random.default_rng(21)
+    A, B = C.mat_haar(rng), C.mat_haar(rng)
+    circ = C.Circuit(n)
+    circ.add("Haar", A, 5)
+    circ.add("Haar", B, 2)
+    with q.State(n, q.ENC_FP64, 1) as s:
+        s.apply_matrix(np.kron(A, B), [5, 2])
+        assert np.max(np.abs(s.get_state() - oracle.e_simulate(n, circ))) <= TOL
+    tof = np.eye(8, dtype=complex)
+    tof[[6, 7]] = tof[[7, 6]]
+    with q.State(n, q.ENC_FP64, 1) as s:
+        s.apply_circuit(C.h_wall(n))
+        s.apply_gate(C.mat_Rz(0.3), 7)
+        s.apply_matrix(tof, [7, 3, 1])  # controls 7, 3 (matrix MSBs), target 1
+        ref = oracle.e_run(oracle.e_simulate(n, C.h_wall(n)).copy(), n, _one(n, "Rz", C.mat_Rz(0.3), 7))
+        ref = oracle.e_run(ref, n, _one(n, "TOFFOLI", C.mat_X(), 1, [7, 3]))
+        assert np.max(np.abs(s.get_state() - ref)) <= TOL
+    n = 11  # sharded states need >= 10 local qubits; qubit 10 is global at P = 2
+    psi = rng.normal(size=2 ** n) + 1j * rng.normal(size=2 ** n)
+    psi /= np.linalg.norm(psi)
+    for k, qs in ((2, [3, 10]), (3, [0, 10, 4]), (1, [10]), (3, [9, 2, 6])):
+        z = rng.normal(size=(2 ** k, 2 ** k)) + 1j * rng.normal(size=(2 ** k, 2 ** k))
+        U, _ = np.linalg.qr(z)
+        for P in (1, 2):
+            with q.State(n, q.ENC_FP64, P) as s:
+                s.set_state(psi)
+                s.apply_matrix(U, qs)
+                assert np.max(np.abs(s.get_state() - _apply_matrix_ref(psi, n, U, qs))) <= TOL
+
+
+def _one(n, name, u, t, ctl=()):
+    c = C.Circuit(n)
+    c.add(name, u, t, list(ctl))
+    return c
+
+
+def test_apply_matrix_errors():
+    with q.State(6, q.ENC_FP64, 1) as s:
+        with pytest.raises(q.QsimError) as e:
+            s.apply_matrix(np.eye(16), [0, 1, 2, 3])
+        assert e.value.code == -1
+        with pytest.raises(q.QsimError) as e:
+            s.apply_matrix(np.eye(4), [1, 1])
+        assert e.value.code == -1
+        with pytest.raises(q.QsimError) as e:
+            s.apply_matrix(np.ones((4, 4)), [0, 1])
+        assert e.value.code == q.QSIM_ENOTUNITARY
+    with q.State(6, q.ENC_ADAPTIVE2, 1) as a:
+        with pytest.raises(q.QsimError) as e:
+            a.apply_matrix(np.eye(4), [0, 1])
+        assert e.value.code == -7
