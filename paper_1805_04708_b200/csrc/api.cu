@@ -909,6 +909,63 @@ static int remap(qsim_state *s, std::vector<std::pair<int, int>> pairs) {
         return phi;
     };
     const uint32_t nt = 1u << m;
+    static const bool via_pack = getenv("QSIM_REMAP_VIA_PACK") != nullptr;
+    if (s->transport == QSIM_TRANSPORT_LOCAL && via_pack) {
+        // test path: the NCCL data flow (chunked pack of every foreign block ->
+        // partner's receive slot -> unpack) with device copies standing in for
+        // ncclSend / ncclRecv, so the pack / unpack kernels and the slot / peer
+        // mapping of the NCCL path run on one GPU
+        uint64_t C = 1;
+        while (C * 2 * (nt - 1) <= s->chunk_amps && C * 2 <= nblock) C *= 2;
+        const uint64_t nch = nblock / C;
+        const size_t slot_bytes = (size_t)C * ab, area = slot_bytes * (nt - 1);
+        char *sendall = nullptr, *recvall = nullptr;
+        CU(cudaMalloc(&sendall, area * s->shards.size()));
+        if (cudaMalloc(&recvall, area * s->shards.size()) != cudaSuccess) {
+            cudaFree(sendall);
+            set_error("remap (pack path): staging allocation failed");
+            return QSIM_ENOMEM;
+        }
+        std::vector<RemapVals> vals(s->shards.size());
+        for (size_t i = 0; i < s->shards.size(); ++i) {
+            const uint32_t ta = jval(shard_phys(s, s->shards[i]));
+            vals[i] = RemapVals{};
+            for (uint32_t t = 0; t < nt; ++t)
+                if (t != ta) vals[i].v[vals[i].n++] = t;
+        }
+        auto slot_of = [&](size_t i, uint32_t t) {  // position of block value t among shard i's slots
+            int k = 0;
+            while (vals[i].v[k] != t) ++k;
+            return k;
+        };
+        for (uint64_t c = 0; c < nch; ++c) {
+            for (size_t i = 0; i < s->shards.size(); ++i)
+                launch_pack_multi(s->shards[i].amps, sendall + i * area, c * C, C, blk, vals[i], ab, s->stream);
+            // "send": shard i's slot for block t goes to the shard with j bits t,
+            // which receives it into its slot for block ta(i)
+            for (size_t i = 0; i < s->shards.size(); ++i) {
+                const uint32_t pa = shard_phys(s, s->shards[i]), ta = jval(pa);
+                for (int k = 0; k < vals[i].n; ++k) {
+                    const uint32_t t = vals[i].v[k];
+                    const uint32_t idx = s->ginv[with_j(pa, t)];
+                    size_t r = 0;
+                    while ((uint32_t)s->shards[r].index != idx) ++r;
+                    CU(cudaMemcpyAsync(recvall + r * area + (size_t)slot_of(r, ta) * slot_bytes,
+                                       sendall + i * area + (size_t)k * slot_bytes, slot_bytes,
+                                       cudaMemcpyDeviceToDevice, s->stream));
+                }
+            }
+            for (size_t i = 0; i < s->shards.size(); ++i)
+                launch_unpack_multi(s->shards[i].amps, recvall + i * area, c * C, C, blk, vals[i], ab, s->stream);
+        }
+        CU(cudaStreamSynchronize(s->stream));
+        cudaFree(sendall);
+        cudaFree(recvall);
+        s->st.exchange_bytes += (double)s->shards.size() * (double)(nt - 1) * (double)nblock * ab;
+        s->st.exchanges++;
+        CU(cudaGetLastError());
+        return QSIM_OK;
+    }
     if (s->transport == QSIM_TRANSPORT_LOCAL) {
         prof_begin(s);
         for (auto &sa : s->shards) {
@@ -939,16 +996,14 @@ static int remap(qsim_state *s, std::vector<std::pair<int, int>> pairs) {
     while (C * 2 * (nt - 1) <= s->chunk_amps && C * 2 <= nblock) C *= 2;
     const uint64_t nch = nblock / C;
     char *sendb = (char *)s->stage[0], *recvb = (char *)s->stage[1];
+    RemapVals vals{};
+    for (uint32_t t = 0; t < nt; ++t)
+        if (t != ta) vals.v[vals.n++] = t;  // slot p <-> block vals.v[p]
     prof_begin(s);
     for (uint64_t c = 0; c < nch; ++c) {
-        int slot = 0;
-        for (uint32_t t = 0; t < nt; ++t) {
-            if (t == ta) continue;
-            launch_pack(sh.amps, sendb + (size_t)slot * C * ab, c * C, C, blk, t, ab, s->stream);
-            ++slot;
-        }
+        launch_pack_multi(sh.amps, sendb, c * C, C, blk, vals, ab, s->stream);
         NC(ncclGroupStart());
-        slot = 0;
+        int slot = 0;
         for (uint32_t t = 0; t < nt; ++t) {
             if (t == ta) continue;
             const int peer = (int)s->ginv[with_j(pa, t)];
@@ -957,13 +1012,8 @@ static int remap(qsim_state *s, std::vector<std::pair<int, int>> pairs) {
             ++slot;
         }
         NC(ncclGroupEnd());
-        slot = 0;
-        for (uint32_t t = 0; t < nt; ++t) {
-            if (t == ta) continue;
-            launch_unpack(sh.amps, recvb + (size_t)slot * C * ab, c * C, C, blk, t, ab, s->stream);
-            ++slot;
-        }
-        s->st.kernels += 2 * (nt - 1);
+        launch_unpack_multi(sh.amps, recvb, c * C, C, blk, vals, ab, s->stream);
+        s->st.kernels += 2;
         s->st.hbm_bytes += 4.0 * (double)(nt - 1) * (double)C * ab;
     }
     prof_end(s, QSIM_K_XCHG, 2.0 * (double)(nt - 1) * (double)nblock * ab);

@@ -156,6 +156,15 @@ void launch_pack(const void *src, void *out, uint64_t base, uint64_t count, cons
                  size_t elem, cudaStream_t s);
 void launch_unpack(void *dst, const void *in, uint64_t base, uint64_t count, const RemapBlock &blk, uint32_t v,
                    size_t elem, cudaStream_t s);
+// every partner in one launch: slot p (count elements) <-> block vals.v[p]
+struct RemapVals {
+    int32_t n;
+    uint32_t v[7];
+};
+void launch_pack_multi(const void *src, void *out, uint64_t base, uint64_t count, const RemapBlock &blk,
+                       const RemapVals &vals, size_t elem, cudaStream_t s);
+void launch_unpack_multi(void *dst, const void *in, uint64_t base, uint64_t count, const RemapBlock &blk,
+                         const RemapVals &vals, size_t elem, cudaStream_t s);
 
 // ---- reductions (a10) ---------------------------------------------------------
 // Per-shard: out[0] = sum |a|^2, out[1 + q] = sum_{bit q = 1} |a|^2 for local q.

@@ -65,6 +65,28 @@ __global__ void __launch_bounds__(256) k_unpack(T *__restrict__ dst, const T *__
         dst[rm_ins(base + x, blk, v)] = in[x];
 }
 
+// all partners at once: slot p of out (count elements each) <- block v[p] of src
+template <typename T>
+__global__ void __launch_bounds__(256) k_pack_multi(const T *__restrict__ src, T *__restrict__ out, uint64_t base,
+                                                    uint64_t count, const __grid_constant__ RemapBlock blk,
+                                                    const __grid_constant__ RemapVals vals) {
+    const uint64_t total = count * (uint64_t)vals.n;
+    for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < total; i += (uint64_t)gridDim.x * 256) {
+        const uint64_t p = i / count, x = i - p * count;
+        out[i] = src[rm_ins(base + x, blk, vals.v[p])];
+    }
+}
+template <typename T>
+__global__ void __launch_bounds__(256) k_unpack_multi(T *__restrict__ dst, const T *__restrict__ in, uint64_t base,
+                                                      uint64_t count, const __grid_constant__ RemapBlock blk,
+                                                      const __grid_constant__ RemapVals vals) {
+    const uint64_t total = count * (uint64_t)vals.n;
+    for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < total; i += (uint64_t)gridDim.x * 256) {
+        const uint64_t p = i / count, x = i - p * count;
+        dst[rm_ins(base + x, blk, vals.v[p])] = in[i];
+    }
+}
+
 static int rm_grid(uint64_t n) {
     const uint64_t cap = (uint64_t)rm_num_sms() * 8, need = (n + 255) / 256;
     return (int)(need < cap ? (need ? need : 1) : cap);
@@ -119,6 +141,40 @@ void launch_unpack(void *dst, const void *in, uint64_t base, uint64_t count, con
         k_unpack<uint16_t><<<rm_grid(count), 256, 0, s>>>((uint16_t *)dst, (const uint16_t *)in, base, count, blk, v);
     } else {
         k_unpack<double2><<<rm_grid(count), 256, 0, s>>>((double2 *)dst, (const double2 *)in, base, count, blk, v);
+    }
+}
+
+void launch_pack_multi(const void *src, void *out, uint64_t base, uint64_t count, const RemapBlock &blk,
+                       const RemapVals &vals, size_t elem, cudaStream_t s) {
+    RemapBlock vb;
+    int sh;
+    if (rm_vec(blk, elem, vb, sh) && ((base | count) & ((1ull << sh) - 1)) == 0) {
+        const uint64_t n = count >> sh;
+        k_pack_multi<uint4><<<rm_grid(n * vals.n), 256, 0, s>>>((const uint4 *)src, (uint4 *)out, base >> sh, n, vb,
+                                                                  vals);
+    } else if (elem == 2) {
+        k_pack_multi<uint16_t><<<rm_grid(count * vals.n), 256, 0, s>>>((const uint16_t *)src, (uint16_t *)out, base,
+                                                                         count, blk, vals);
+    } else {
+        k_pack_multi<double2><<<rm_grid(count * vals.n), 256, 0, s>>>((const double2 *)src, (double2 *)out, base,
+                                                                        count, blk, vals);
+    }
+}
+
+void launch_unpack_multi(void *dst, const void *in, uint64_t base, uint64_t count, const RemapBlock &blk,
+                         const RemapVals &vals, size_t elem, cudaStream_t s) {
+    RemapBlock vb;
+    int sh;
+    if (rm_vec(blk, elem, vb, sh) && ((base | count) & ((1ull << sh) - 1)) == 0) {
+        const uint64_t n = count >> sh;
+        k_unpack_multi<uint4><<<rm_grid(n * vals.n), 256, 0, s>>>((uint4 *)dst, (const uint4 *)in, base >> sh, n, vb,
+                                                                    vals);
+    } else if (elem == 2) {
+        k_unpack_multi<uint16_t><<<rm_grid(count * vals.n), 256, 0, s>>>((uint16_t *)dst, (const uint16_t *)in, base,
+                                                                           count, blk, vals);
+    } else {
+        k_unpack_multi<double2><<<rm_grid(count * vals.n), 256, 0, s>>>((double2 *)dst, (const double2 *)in, base,
+                                                                          count, blk, vals);
     }
 }
 

@@ -678,3 +678,38 @@ def test_apply_matrix_errors():
         with pytest.raises(q.QsimError) as e:
             a.apply_matrix(np.eye(4), [0, 1])
         assert e.value.code == -7
+
+
+@pytest.mark.parametrize("enc", ["E", "A"])
+def test_remap_pack_unpack_path(tmp_path, enc):
+    """The NCCL remap's data flow on one GPU (QSIM_REMAP_VIA_PACK=1: chunked
+    multi-partner pack -> device copies standing in for ncclSend / ncclRecv
+    -> multi-partner unpack, small chunks so every block takes several
+    rounds): E equals the oracle, A equals the single-shard run bit for bit."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    n, P = 13, 8
+    out = str(tmp_path / f"r_{enc}.npy")
+    getter = "s.get_state()" if enc == "E" else "s.get_codes()[0]"
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); import paper_1805_04708_b200 as q, qsim_inputs as C; "
+            "s = q.State(%d, q.ENC_%s, %d, chunk_bytes=2048); c = C.layered(%d, 2, seed=7); "
+            "c.extend(C.rz_rx_cphase(%d, 1, seed=7)); s.apply_circuit(c); st = s.stats(); np.save(%r, %s); "
+            "print(st['exchanges'])" % (root, n, "FP64" if enc == "E" else "ADAPTIVE2", P, n, n, out, getter))
+    env = dict(os.environ, QSIM_REMAP_VIA_PACK="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    assert int(r.stdout.split()[-1]) > 0
+    got = np.load(out)
+    circ = C.layered(n, 2, seed=7)
+    circ.extend(C.rz_rx_cphase(n, 1, seed=7))
+    ops, _ = q.qsim_plan(n, P, circ)
+    assert sum(o["type"] == q.OP_REMAP for o in ops) > 0
+    if enc == "E":
+        assert np.max(np.abs(got - oracle.e_simulate(n, circ))) <= TOL
+    else:
+        with q.State(n, q.ENC_ADAPTIVE2, 1) as s1:
+            s1.apply_circuit(circ)
+            assert np.array_equal(got, s1.get_codes()[0])
