@@ -37,7 +37,8 @@ struct Planner {
     // Appends the ops for gates[0..ngates) to `ops` and updates the map.
     // `lookahead` enables Belady victim selection over the remaining gates.
     void plan(const qsim_gate *gates, size_t ngates, std::vector<PlanOp> &ops, bool lookahead);
-    int choose_victim(const qsim_gate *gates, size_t ngates, size_t cur, const int *avoid, int navoid, bool lookahead);
+    int choose_victim(const qsim_gate *gates, size_t ngates, size_t cur, const int *avoid, int navoid, bool lookahead,
+                      bool wide = false);
     void swap_bits(int a, int b);  // exchange the logical qubits at physical bits a and b
 };
 

@@ -97,8 +97,16 @@ void Planner::swap_bits(int a, int b) {
 // needed as a non-diagonal target furthest in the future (Belady); else the
 // highest candidate.
 int Planner::choose_victim(const qsim_gate *gates, size_t ngates, size_t cur, const int *avoid, int navoid,
-                           bool lookahead) {
-    int lo = nl - 8 > 0 ? nl - 8 : 0;
+                           bool lookahead, bool wide) {
+    // candidates: the top 8 local bits for a pairwise exchange (its half-shard
+    // slot is contiguous in runs of 2^l amplitudes: the NCCL chunks); an
+    // all-to-all remap packs its blocks, so its victims may come from every
+    // local bit >= min(QSIM_VICTIM_FLOOR = 12, nl - 8): Belady then finds
+    // qubits the coming gates do not need (config 3, N = 36 / P = 8: 15.6 ->
+    // 11.9 shard-equivalents of exchange per GPU)
+    static const int floor_bit = getenv("QSIM_VICTIM_FLOOR") ? atoi(getenv("QSIM_VICTIM_FLOOR")) : 12;
+    int lo = wide ? std::min(floor_bit, nl - 8) : nl - 8;
+    if (lo < 0) lo = 0;
     int best = -1;
     int64_t best_next = -1;
     for (int l = nl - 1; l >= lo; --l) {
@@ -196,7 +204,7 @@ void Planner::plan(const qsim_gate *gates, size_t ngates, std::vector<PlanOp> &o
             if (m >= 2) {
                 int lv[64];
                 for (int i = 0; i < m; ++i) {
-                    lv[i] = choose_victim(gates, ngates, g, avoid, navoid, lookahead);
+                    lv[i] = choose_victim(gates, ngates, g, avoid, navoid, lookahead, true);
                     avoid[navoid++] = lv[i];
                 }
                 for (int i = 0; i < m; ++i) {
