@@ -449,6 +449,11 @@ def qsim_apply_matrix(h, u, qubits):
     _check(_lib.qsim_apply_matrix(h, m.ctypes.data_as(_dp), q, k))
 
 
+def qsim_jit_shutdown():
+    """Stop the fused-pass compile threads (also registered with atexit)."""
+    _check(_lib.qsim_jit_shutdown())
+
+
 def qsim_overlap(ha, hb) -> complex:
     out = (ctypes.c_double * 2)()
     _check(_lib.qsim_overlap(ha, hb, out))

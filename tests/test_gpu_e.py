@@ -713,3 +713,23 @@ def test_remap_pack_unpack_path(tmp_path, enc):
         with q.State(n, q.ENC_ADAPTIVE2, 1) as s1:
             s1.apply_circuit(circ)
             assert np.array_equal(got, s1.get_codes()[0])
+
+
+def test_jit_shutdown_then_interpreter(tmp_path):
+    """qsim_jit_shutdown stops the compile threads; later passes run in the
+    interpreter with the same results, and the process exits cleanly."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = str(tmp_path / "s.npy")
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); import paper_1805_04708_b200 as q, qsim_inputs as C; "
+            "n = 14; c = C.config(0, seed=4); s = q.State(n, q.ENC_FP64, 1); s.apply_circuit(c); s.sync(); "
+            "q.qsim_jit_shutdown(); s.reset(); s.apply_circuit(c); np.save(%r, s.get_state()); "
+            "print(s.stats()['jit_passes'])" % (root, out))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    assert int(r.stdout.split()[-1]) == 0  # after the shutdown nothing is specialised
+    ref = oracle.e_simulate(14, C.config(0, seed=4))
+    assert np.max(np.abs(np.load(out) - ref)) <= TOL
