@@ -201,7 +201,8 @@ void Planner::plan(const qsim_gate *gates, size_t ngates, std::vector<PlanOp> &o
                     if (!dup) gl[m++] = py;
                 }
             }
-            if (m >= 2) {
+            static const int remap_min = getenv("QSIM_REMAP_MIN") ? atoi(getenv("QSIM_REMAP_MIN")) : 2;
+            if (remap && m >= remap_min && n - nl >= 1) {
                 int lv[64];
                 for (int i = 0; i < m; ++i) {
                     lv[i] = choose_victim(gates, ngates, g, avoid, navoid, lookahead, true);
