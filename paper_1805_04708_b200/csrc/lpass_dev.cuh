@@ -22,6 +22,19 @@ __device__ __forceinline__ void lp_cp_async16(void *smem, const void *gmem) {
 }
 __device__ __forceinline__ void lp_cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
+// 16-byte shared-memory access of one amplitude (register stages).  Explicit
+// v2.f64: from C++ the compiler splits some stages' double2 accesses into two
+// 8-byte halves (LDS.64 / STS.64 pairs, twice the wavefronts -- measured); the
+// asm is volatile so it stays between the stage's __syncthreads.
+__device__ __forceinline__ double2 lp_lds16(uint32_t sa) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(sa));
+    return v;
+}
+__device__ __forceinline__ void lp_sts16(uint32_t sa, const double2 &v) {
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(sa), "d"(v.x), "d"(v.y));
+}
+
 // x' = x - t y, y' = y + t x  (2 FMAs per amplitude component)
 __device__ __forceinline__ void lp_shear_pair(double2 &x, double2 &y, double t) {
     const double2 x0 = x;
@@ -370,6 +383,7 @@ __device__ __forceinline__ void lp_stage(const LPassParams &p, const LpTile &t, 
     const uint32_t tid = threadIdx.x;
     const uint32_t ngroups = 1u << (K - R);
     unsigned char *smem_raw = t.smem_raw;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_raw);
     uint32_t y = st.y_static;
     // static event indices (a literal stage keeps only its events, no indexed array)
 #pragma unroll
@@ -413,8 +427,8 @@ __device__ __forceinline__ void lp_stage(const LPassParams &p, const LpTile &t, 
 #pragma unroll
             for (int r = 0; r < R; ++r)
                 if (j & (1 << r)) ad ^= rp[r];
-            v0[j] = *reinterpret_cast<const double2 *>(smem_raw + (a0[0] ^ ad));
-            v1[j] = *reinterpret_cast<const double2 *>(smem_raw + (a0[1] ^ ad));
+            v0[j] = lp_lds16(sbase + (a0[0] ^ ad));
+            v1[j] = lp_lds16(sbase + (a0[1] ^ ad));
         }
         uint32_t g_0 = g0, g_1 = g0;
         ops(v0, g_0, xq[0], t.full, p, smem_raw, t.cpool_off);
@@ -425,8 +439,8 @@ __device__ __forceinline__ void lp_stage(const LPassParams &p, const LpTile &t, 
 #pragma unroll
             for (int r = 0; r < R; ++r)
                 if (j & (1 << r)) ad ^= rp[r];
-            *reinterpret_cast<double2 *>(smem_raw + (a0[0] ^ ad)) = v0[j];
-            *reinterpret_cast<double2 *>(smem_raw + (a0[1] ^ ad)) = v1[j];
+            lp_sts16(sbase + (a0[0] ^ ad), v0[j]);
+            lp_sts16(sbase + (a0[1] ^ ad), v1[j]);
         }
         __syncthreads();
         return;
@@ -445,7 +459,7 @@ __device__ __forceinline__ void lp_stage(const LPassParams &p, const LpTile &t, 
 #pragma unroll
             for (int r = 0; r < R; ++r)
                 if (j & (1 << r)) ad ^= rp[r];
-            v[j] = *reinterpret_cast<const double2 *>(smem_raw + ad);
+            v[j] = lp_lds16(sbase + ad);
         }
         uint32_t g = g0;
         ops(v, g, xq, t.full, p, smem_raw, t.cpool_off);
@@ -455,7 +469,7 @@ __device__ __forceinline__ void lp_stage(const LPassParams &p, const LpTile &t, 
 #pragma unroll
             for (int r = 0; r < R; ++r)
                 if (j & (1 << r)) ad ^= rp[r];
-            *reinterpret_cast<double2 *>(smem_raw + ad) = v[j];
+            lp_sts16(sbase + ad, v[j]);
         }
     }
     __syncthreads();

@@ -363,10 +363,28 @@ static int run_circuits(int ncases, uint64_t seed) {
 // local qubits: the program the runtime would launch, without a state
 struct StatSink : LPassSink {
     long passes = 0, sweeps = 0, stages = 0, ops = 0, tables = 0, shears = 0, flips = 0, relabels = 0,
-         tile_free = 0, events = 0;
+         tile_free = 0, events = 0, wf_ideal = 0, wf = 0;
     int nl = 30;
-    int pass(const LPassParams &, const LCompileStats &cs, const std::vector<int> &) override {
+    int pass(const LPassParams &p, const LCompileStats &cs, const std::vector<int> &) override {
         ++passes;
+        // shared-memory wavefronts of one warp's stage load (16-byte elements:
+        // a wavefront serves each 16-byte bank group once)
+        for (int s = 0; s < p.nstages; ++s) {
+            int cnt[8][32] = {};
+            int nb[8] = {};
+            for (int lane = 0; lane < 32; ++lane) {
+                uint32_t a = 0;
+                for (int i = 0; i < 5 && i < p.K - p.R; ++i)
+                    if ((lane >> i) & 1) a ^= p.st[s].grp_phys[i];
+                bool seen = false;
+                for (int k = 0; k < nb[a & 7]; ++k) seen |= cnt[a & 7][k] == (int)a;
+                if (!seen) cnt[a & 7][nb[a & 7]++] = (int)a;
+            }
+            int mx = 0;
+            for (int b = 0; b < 8; ++b) mx = std::max(mx, nb[b]);
+            wf += mx;
+            wf_ideal += 4;
+        }
         stages += cs.stages;
         ops += cs.ops;
         tables += cs.diagt;
@@ -410,9 +428,9 @@ static int stats_file(const char *path, int nl, int R) {
         return 1;
     }
     printf("gates=%zu passes=%ld sweeps=%ld stages=%ld ops=%ld tables=%ld shears=%ld flips=%ld relabels=%ld "
-           "tile_free=%ld events=%ld\n",
+           "tile_free=%ld events=%ld stage_wavefronts=%ld/%ld\n",
            gs.size(), sink.passes, sink.sweeps, sink.stages, sink.ops, sink.tables, sink.shears, sink.flips,
-           sink.relabels, sink.tile_free, sink.events);
+           sink.relabels, sink.tile_free, sink.events, sink.wf, sink.wf_ideal);
     return 0;
 }
 
