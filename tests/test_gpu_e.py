@@ -332,6 +332,41 @@ def test_full_size_config2_vs_oracle_sampled():
     assert abs(nrm - 1) <= 1e-10
 
 
+def _inverse(circ):
+    """The inverse circuit: gates in reverse order, each U replaced by U^dagger
+    (controls kept; SWAP is its own inverse)."""
+    inv = C.Circuit(circ.n)
+    for i in reversed(range(len(circ))):
+        name, kind, t, t2, ctl, u = circ.gate(i)
+        if kind == 1:
+            inv.swap(t, t2)
+        else:
+            inv.add(name + "^dag", u.conj().T, t, ctl)
+    return inv
+
+
+@pytest.mark.slow
+def test_full_size_config2_mirror_returns_to_zero():
+    """The whole bench circuit (config 2: N=30, H wall + 20 layers, CNOTs
+    kept, 930 gates, seed 1) in bench.py's launch configuration, then its
+    inverse: U^dagger U = 1 returns the state to |0...0> at any size -- every
+    fused pass of the timed step checked at full size (the oracle cannot run
+    it): amplitude 0 and 10^5 sampled others, and the norm after each half."""
+    n = 30
+    circ = C.layered(n, 20, seed=1)
+    assert len(circ) == 930
+    with q.State(n) as s:
+        s.apply_circuit(circ)
+        assert abs(s.norm() - 1) <= 1e-10
+        s.apply_circuit(_inverse(circ))
+        idx = np.random.default_rng(8).integers(1, 1 << n, 100000, dtype=np.uint64)
+        a0 = s.get_amplitudes(np.array([0], dtype=np.uint64))[0]
+        assert abs(a0 - 1) <= 1e-10
+        assert np.max(np.abs(s.get_amplitudes(idx))) <= 1e-12
+        assert abs(s.norm() - 1) <= 1e-10
+        assert s.stats()["passes"] > 0
+
+
 @pytest.mark.slow
 def test_max_size_config3_n33_product_pin_and_qft():
     """BASELINE config 3's per-GPU size (2^33 amplitudes = 128 GiB of HBM): the
@@ -726,10 +761,15 @@ def test_jit_shutdown_then_interpreter(tmp_path):
     out = str(tmp_path / "s.npy")
     code = ("import sys, numpy as np; sys.path.insert(0, %r); import paper_1805_04708_b200 as q, qsim_inputs as C; "
             "n = 14; c = C.config(0, seed=4); s = q.State(n, q.ENC_FP64, 1); s.apply_circuit(c); s.sync(); "
-            "q.qsim_jit_shutdown(); s.reset(); s.apply_circuit(c); np.save(%r, s.get_state()); "
-            "print(s.stats()['jit_passes'])" % (root, out))
-    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
-    assert r.returncode == 0, r.stderr
-    assert int(r.stdout.split()[-1]) == 0  # after the shutdown nothing is specialised
+            "q.qsim_jit_sync(); s.reset(); s.reset_stats(); s.apply_circuit(c); s.sync(); "
+            "j1 = s.stats()['jit_passes']; "
+            "q.qsim_jit_shutdown(); s.reset(); s.reset_stats(); s.apply_circuit(c); np.save(%r, s.get_state()); "
+            "print(j1, s.stats()['jit_passes'])" % (root, out))
     ref = oracle.e_simulate(14, C.config(0, seed=4))
-    assert np.max(np.abs(np.load(out) - ref)) <= TOL
+    for mode in ("1", "2"):  # compile in the background / before the first launch
+        env = dict(os.environ, QSIM_LPASS_JIT=mode)
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, env=env)
+        assert r.returncode == 0, r.stderr
+        j1, j2 = (int(x) for x in r.stdout.split()[-2:])
+        assert j1 > 0 and j2 == 0, (mode, j1, j2)  # specialised before the shutdown, interpreted after
+        assert np.max(np.abs(np.load(out) - ref)) <= TOL
