@@ -556,13 +556,25 @@ __device__ __forceinline__ uint32_t a_encode_f(const ASm &sm, const ASmF &f, flo
 }
 
 // fp64 reference for the pairs of a unit whose fp32 decision failed (rare;
-// out of line so the hot loop stays small)
+// out of line so the hot loop stays small), then the unit's store.  Only
+// scalars cross the call (the fp32 codes packed two per word, the gate from
+// the kernel parameters; the input codes are reloaded -- this thread has not
+// stored the unit yet), so the hot loop keeps its arrays in registers.
 template <int TL, int UK>
-__device__ __noinline__ void a_unit_exact(const ASm &sm, const double *u, const uint32_t *c, uint32_t *nc,
-                                          uint32_t fail, uint32_t selm) {
+__device__ __noinline__ void a_unit_exact_store(const ASm &sm, const double *u, uint16_t *a, uint64_t s0, int t,
+                                                uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t w4,
+                                                uint32_t w5, uint32_t w6, uint32_t w7, uint32_t fail, uint32_t selm) {
     double uu[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) uu[i] = u[i];
+    const uint32_t w[8] = {w0, w1, w2, w3, w4, w5, w6, w7};
+    uint32_t c[16], nc[16];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        nc[2 * k] = w[k] & 0xffffu;
+        nc[2 * k + 1] = w[k] >> 16;
+    }
+    AUnit<TL>::load(a, s0, t, c);
     for (int k = 0; k < 8; ++k) {
         if (!((fail >> k) & 1u)) continue;
         const int j0 = AUnit<TL>::j0(k), j1 = AUnit<TL>::j1(k);
@@ -571,6 +583,7 @@ __device__ __noinline__ void a_unit_exact(const ASm &sm, const double *u, const 
         nc[j0] = a_encode(sm, x);
         nc[j1] = a_encode(sm, y);
     }
+    AUnit<TL>::store(a, s0, t, nc);
 }
 
 template <int TL, bool CTRL, int UK>
@@ -736,13 +749,9 @@ __global__ void __launch_bounds__(A_THREADS) k_apply_a(const __grid_constant__ A
     const uint32_t cl = (uint32_t)(p.cmask & lowm);
     __shared__ ASmF f;
     load_asmf(f, sm);
-    double u[8];
     float uf[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        u[i] = p.u[i];
-        uf[i] = (float)p.u[i];
-    }
+    for (int i = 0; i < 8; ++i) uf[i] = (float)p.u[i];
     for (uint64_t v = (uint64_t)blockIdx.x * A_THREADS + threadIdx.x; v < units; v += (uint64_t)gridDim.x * A_THREADS) {
         uint32_t c[16];
         const uint64_t s0 = U::s0(v, p.t);
@@ -764,8 +773,13 @@ __global__ void __launch_bounds__(A_THREADS) k_apply_a(const __grid_constant__ A
             nc[j1] = a_encode_f(sm, f, yf, E, oky);
             fail |= (uint32_t)!(okx && oky) << k;
         }
-        if (fail) a_unit_exact<TL, UK>(sm, u, c, nc, fail, selm);
-        U::store(a, s0, p.t, nc);
+        if (fail)
+            a_unit_exact_store<TL, UK>(sm, p.u, a, s0, p.t, nc[0] | (nc[1] << 16), nc[2] | (nc[3] << 16),
+                                       nc[4] | (nc[5] << 16), nc[6] | (nc[7] << 16), nc[8] | (nc[9] << 16),
+                                       nc[10] | (nc[11] << 16), nc[12] | (nc[13] << 16), nc[14] | (nc[15] << 16),
+                                       fail, selm);
+        else
+            U::store(a, s0, p.t, nc);
     }
 }
 
