@@ -26,13 +26,26 @@ __device__ __forceinline__ void lp_cp_async_wait_all() { asm volatile("cp.async.
 // v2.f64: from C++ the compiler splits some stages' double2 accesses into two
 // 8-byte halves (LDS.64 / STS.64 pairs, twice the wavefronts -- measured); the
 // asm is volatile so it stays between the stage's __syncthreads.
+#ifndef LP_STAGE_ASM
+#define LP_STAGE_ASM 1
+#endif
 __device__ __forceinline__ double2 lp_lds16(uint32_t sa) {
+#if LP_STAGE_ASM
     double2 v;
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(sa));
     return v;
+#else
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    return *reinterpret_cast<const double2 *>(smem_raw + (sa - (uint32_t)__cvta_generic_to_shared(smem_raw)));
+#endif
 }
 __device__ __forceinline__ void lp_sts16(uint32_t sa, const double2 &v) {
+#if LP_STAGE_ASM
     asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(sa), "d"(v.x), "d"(v.y));
+#else
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    *reinterpret_cast<double2 *>(smem_raw + (sa - (uint32_t)__cvta_generic_to_shared(smem_raw))) = v;
+#endif
 }
 
 // x' = x - t y, y' = y + t x  (2 FMAs per amplitude component)
