@@ -7,6 +7,9 @@
 #include <algorithm>
 #include <array>
 #include <deque>
+#include <memory>
+#include <mutex>
+#include <unordered_map>
 #include <cstdlib>
 #include <cmath>
 #include <cstdio>
@@ -696,6 +699,53 @@ struct LaunchSink : LPassSink {
     double gate_bytes(const LGate &g) override { return gate_bytes_alone(s, s->shards[0], plan_op_of(g), g.u); }
 };
 
+// Program cache of the host pass compiler: lpass_run is deterministic in
+// its gate list, its configuration and the state's shape (gate_bytes), so
+// a repeated run (the same circuit applied again, e.g. config 1's repeated
+// calls) replays the recorded pass programs and sweeps instead of compiling
+// them again (~0.2-0.3 ms of host time for 200 gates).  QSIM_PLAN_CACHE=0
+// disables it.
+struct LRecord {
+    bool is_pass;
+    std::unique_ptr<LPassParams> p;
+    LCompileStats cs;
+    std::vector<int> ids;
+    LGate g;
+    int id;
+};
+struct LRecorder : LPassSink {
+    LPassSink *inner;
+    std::vector<LRecord> recs;
+    int pass(const LPassParams &p, const LCompileStats &cs, const std::vector<int> &ids) override {
+        LRecord r{};
+        r.is_pass = true;
+        r.p.reset(new LPassParams(p));
+        r.cs = cs;
+        r.ids = ids;
+        recs.push_back(std::move(r));
+        return inner->pass(p, cs, ids);
+    }
+    int sweep(const LGate &g, int id) override {
+        LRecord r{};
+        r.is_pass = false;
+        r.g = g;
+        r.id = id;
+        recs.push_back(std::move(r));
+        return inner->sweep(g, id);
+    }
+    double gate_bytes(const LGate &g) override { return inner->gate_bytes(g); }
+};
+struct LProgramCache {
+    std::mutex mu;
+    std::unordered_map<std::string, std::shared_ptr<std::vector<LRecord>>> map;
+    std::deque<std::string> order;  // FIFO eviction
+    static constexpr size_t kMax = 64;
+};
+static LProgramCache &lprogram_cache() {
+    static LProgramCache *c = new LProgramCache();  // never destroyed: no exit-order issues
+    return *c;
+}
+
 static int run_gates_lpass(qsim_state *s, const std::vector<PlanOp> &run, const std::vector<const double *> &us) {
     std::vector<LGate> lg(run.size());
     for (size_t k = 0; k < run.size(); ++k) {
@@ -718,11 +768,48 @@ static int run_gates_lpass(qsim_state *s, const std::vector<PlanOp> &run, const 
     sink.s = s;
     sink.run = &run;
     sink.us = &us;
+    static const bool use_cache = !(getenv("QSIM_PLAN_CACHE") && atoi(getenv("QSIM_PLAN_CACHE")) == 0);
+    std::string key;
+    if (use_cache) {
+        // everything lpass_run and gate_bytes read: configuration, state shape, gate records
+        const int shape[8] = {cfg.nl, cfg.K, cfg.R, cfg.max_coef, cfg.defer ? 1 : 0, s->n,
+                              (int)s->shards.size(), (int)s->amp_bytes};
+        // gate_bytes reads shard 0's global bits (global controls / diagonal targets)
+        const uint64_t sb0 = shard_base(s, s->shards[0]);
+        key.assign(reinterpret_cast<const char *>(shape), sizeof(shape));
+        key.append(reinterpret_cast<const char *>(&sb0), sizeof(sb0));
+        key.append(reinterpret_cast<const char *>(lg.data()), lg.size() * sizeof(LGate));
+        std::shared_ptr<std::vector<LRecord>> hit;
+        {
+            LProgramCache &c = lprogram_cache();
+            std::lock_guard<std::mutex> lk(c.mu);
+            auto it = c.map.find(key);
+            if (it != c.map.end()) hit = it->second;
+        }
+        if (hit) {
+            for (const LRecord &r : *hit) RC(r.is_pass ? sink.pass(*r.p, r.cs, r.ids) : sink.sweep(r.g, r.id));
+            return QSIM_OK;
+        }
+    }
+    LRecorder rec;
+    rec.inner = &sink;
     std::string err;
-    const int rc = lpass_run(lg.data(), (int)lg.size(), cfg, sink, &err);
+    const int rc = lpass_run(lg.data(), (int)lg.size(), cfg, use_cache ? (LPassSink &)rec : (LPassSink &)sink, &err);
     if (rc == -1) {
         set_error("lpass: " + err);
         return QSIM_EINVAL;
+    }
+    if (rc == 0 && use_cache) {
+        LProgramCache &c = lprogram_cache();
+        std::lock_guard<std::mutex> lk(c.mu);
+        if (!c.map.count(key)) {
+            if (c.order.size() >= LProgramCache::kMax) {
+                c.map.erase(c.order.front());
+                c.order.pop_front();
+            }
+            c.map.emplace(key, std::make_shared<std::vector<LRecord>>(std::move(rec.recs)));
+            c.order.push_back(key);
+        }
     }
     return rc;
 }

@@ -750,6 +750,24 @@ def test_remap_pack_unpack_path(tmp_path, enc):
             assert np.array_equal(got, s1.get_codes()[0])
 
 
+def test_program_cache_replay_is_identical():
+    """A circuit applied again replays the host compiler's recorded pass
+    programs (api.cu program cache): same state bit for bit, equal to the
+    oracle; sharded states (the key includes shard 0's global bits) too."""
+    n = 14
+    c = C.config(0, seed=9)
+    ref = oracle.e_simulate(n, c)
+    for P in (1, 4):
+        with q.State(n, q.ENC_FP64, P) as s:
+            s.apply_circuit(c)
+            a = s.get_state()
+            s.reset()
+            s.apply_circuit(c)
+            b = s.get_state()
+        assert np.array_equal(a, b), P
+        assert np.max(np.abs(a - ref)) <= TOL, P
+
+
 def test_jit_shutdown_then_interpreter(tmp_path):
     """qsim_jit_shutdown stops the compile threads; later passes run in the
     interpreter with the same results, and the process exits cleanly."""
