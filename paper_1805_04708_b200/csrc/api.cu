@@ -739,7 +739,13 @@ struct LProgramCache {
     std::mutex mu;
     std::unordered_map<std::string, std::shared_ptr<std::vector<LRecord>>> map;
     std::deque<std::string> order;  // FIFO eviction
-    static constexpr size_t kMax = 64;
+    size_t bytes = 0;
+    static constexpr size_t kMax = 64, kMaxBytes = size_t(256) << 20;
+    static size_t entry_bytes(const std::vector<LRecord> &r) {
+        size_t b = 0;
+        for (const LRecord &x : r) b += x.is_pass ? sizeof(LPassParams) : sizeof(LGate);
+        return b;
+    }
 };
 static LProgramCache &lprogram_cache() {
     static LProgramCache *c = new LProgramCache();  // never destroyed: no exit-order issues
@@ -802,13 +808,17 @@ static int run_gates_lpass(qsim_state *s, const std::vector<PlanOp> &run, const 
     if (rc == 0 && use_cache) {
         LProgramCache &c = lprogram_cache();
         std::lock_guard<std::mutex> lk(c.mu);
-        if (!c.map.count(key)) {
-            if (c.order.size() >= LProgramCache::kMax) {
-                c.map.erase(c.order.front());
+        const size_t eb = LProgramCache::entry_bytes(rec.recs);
+        if (!c.map.count(key) && eb <= LProgramCache::kMaxBytes) {
+            while (!c.order.empty() && (c.order.size() >= LProgramCache::kMax || c.bytes + eb > LProgramCache::kMaxBytes)) {
+                auto it = c.map.find(c.order.front());
+                c.bytes -= LProgramCache::entry_bytes(*it->second);
+                c.map.erase(it);
                 c.order.pop_front();
             }
             c.map.emplace(key, std::make_shared<std::vector<LRecord>>(std::move(rec.recs)));
             c.order.push_back(key);
+            c.bytes += eb;
         }
     }
     return rc;

@@ -766,6 +766,17 @@ def test_program_cache_replay_is_identical():
             b = s.get_state()
         assert np.array_equal(a, b), P
         assert np.max(np.abs(a - ref)) <= TOL, P
+    # more distinct gate lists than the cache holds (64): the first is
+    # evicted and compiled again, the last still replays
+    circs = [C.random_circuit(n, 30, seed=1000 + k) for k in range(70)]
+    with q.State(n) as s:
+        for cc in circs:
+            s.reset()
+            s.apply_circuit(cc)
+        for cc in (circs[0], circs[-1]):
+            s.reset()
+            s.apply_circuit(cc)
+            assert np.max(np.abs(s.get_state() - oracle.e_simulate(n, cc))) <= TOL
 
 
 def test_jit_shutdown_then_interpreter(tmp_path):
