@@ -184,6 +184,9 @@ def run_reference(args, rank, world):
     import oracle
     import psutil
 
+    # torchrun sets OMP_NUM_THREADS=1 per rank; only rank 0 works here, so
+    # the oracle gets every host core, as at N=1
+    oracle.set_num_threads(len(os.sched_getaffinity(0)))
     if psutil.virtual_memory().available < (16 << n) * 1.5:
         n = 28
         circ = C.layered(n, 20, seed=1)
