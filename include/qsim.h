@@ -172,6 +172,15 @@ int qsim_norm(qsim_state *s, double *norm2);
  * runs of one circuit have): QSIM_EUNSUPPORTED otherwise.  Synchronous. */
 int qsim_overlap(qsim_state *a, qsim_state *b, double *out);
 
+/* Magnitude range of an E state: *max = max_x |a_x|, *min_nonzero = min over
+ * the x with a_x != 0 of |a_x| (0 if the state is all zero) -- the fp64
+ * counterpart of the A bounds r0 / r1, used to report the
+ * value distribution of the workloads.  A device reduction
+ * (exact: min / max are order-independent); all-reduced over NCCL ranks.
+ * QSIM_EUNSUPPORTED for the A encoding (its range is (r0, r1), qsim_get_codes).
+ * Synchronous. */
+int qsim_magnitude_range(qsim_state *s, double *min_nonzero, double *max);
+
 /* p1[n] = P(qubit n = 1) = sum over |a(..1_n..)|^2, n = 0..N-1,
  * not renormalised.  p1 has N entries. */
 int qsim_probabilities(qsim_state *s, double *p1);
@@ -294,6 +303,11 @@ int qsim_get_amplitudes(qsim_state *s, const uint64_t *logical_idx, size_t n, do
  * small N (N <= 30).  get: E or A (decoded); set: E only (A: EUNSUPPORTED). */
 int qsim_get_state(qsim_state *s, double *out);
 int qsim_set_state(qsim_state *s, const double *amps);
+
+/* The A state's current bounds (r0, r1) (min / max |z| over
+ * the intermediate amplitudes; (0.5, 0.5) before any exists, reading R-A8),
+ * without reading the codes.  QSIM_EUNSUPPORTED for E.  Synchronous. */
+int qsim_get_bounds(qsim_state *s, double *r0, double *r1);
 
 /* A only: raw codes in logical order (2^N pairs (b0, b1) as int8) and the
  * magnitude bounds r0 <= r1.  EUNSUPPORTED for E. */

@@ -341,6 +341,9 @@ void oracle_a_encode(double zr, double zi, double r0, double r1, int *b0_out, in
 void oracle_a_bounds(const double *z, uint64_t dim, double *r0_out, double *r1_out)
 {
     double r0 = INFINITY, r1 = -INFINITY;
+    /* min / max are exact and order-independent: the reduction gives the
+     * same bits for any thread count */
+#pragma omp parallel for schedule(static) reduction(min : r0) reduction(max : r1)
     for (uint64_t i = 0; i < dim; ++i) {
         double m = hypot(z[2 * i], z[2 * i + 1]);
         if (a_class(m) != 2) continue;
@@ -374,6 +377,7 @@ void oracle_a_init(int8_t *code, int n, double *r0, double *r1)
 void oracle_a_decode_state(const int8_t *code, int n, double r0, double r1, double *z)
 {
     uint64_t dim = (uint64_t)1 << n;
+#pragma omp parallel for schedule(static)
     for (uint64_t i = 0; i < dim; ++i) oracle_a_decode(code[2 * i], code[2 * i + 1], r0, r1, &z[2 * i], &z[2 * i + 1]);
 }
 
@@ -382,6 +386,7 @@ void oracle_a_encode_state(const double *z, int n, int8_t *code, double *r0, dou
 {
     uint64_t dim = (uint64_t)1 << n;
     oracle_a_bounds(z, dim, r0, r1);
+#pragma omp parallel for schedule(static)
     for (uint64_t i = 0; i < dim; ++i) {
         int b0, b1;
         oracle_a_encode(z[2 * i], z[2 * i + 1], *r0, *r1, &b0, &b1);

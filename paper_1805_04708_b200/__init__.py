@@ -92,7 +92,7 @@ EXPORTS = (
     "qsim_aux_amplitudes", "qsim_aux_num_vars", "qsim_set_qubit_map",
     "qsim_asm_parse", "qsim_asm_info", "qsim_asm_get_op", "qsim_asm_destroy", "qsim_asm_run",
     "qsim_asm_result_get", "qsim_asm_result_destroy",
-    "qsim_overlap", "qsim_apply_matrix", "qsim_jit_sync", "qsim_jit_shutdown", "qsim_graph_begin", "qsim_graph_end", "qsim_graph_launch", "qsim_graph_destroy",
+    "qsim_overlap", "qsim_magnitude_range", "qsim_get_bounds", "qsim_apply_matrix", "qsim_jit_sync", "qsim_jit_shutdown", "qsim_graph_begin", "qsim_graph_end", "qsim_graph_launch", "qsim_graph_destroy",
 )
 
 if not os.path.exists(_LIB_PATH):
@@ -145,6 +145,8 @@ _lib.qsim_get_codes.argtypes = [_P, ctypes.POINTER(ctypes.c_int8), _dp, _dp]
 _lib.qsim_set_codes.argtypes = [_P, ctypes.POINTER(ctypes.c_int8), ctypes.c_double, ctypes.c_double]
 _lib.qsim_sync.argtypes = [_P]
 _lib.qsim_overlap.argtypes = [_P, _P, _dp]
+_lib.qsim_magnitude_range.argtypes = [_P, _dp, _dp]
+_lib.qsim_get_bounds.argtypes = [_P, _dp, _dp]
 _lib.qsim_apply_matrix.argtypes = [_P, _dp, _ip, ctypes.c_int]
 _lib.qsim_jit_sync.argtypes = []
 _lib.qsim_jit_shutdown.argtypes = []
@@ -460,6 +462,18 @@ def qsim_overlap(ha, hb) -> complex:
     return complex(out[0], out[1])
 
 
+def qsim_magnitude_range(h) -> tuple[float, float]:
+    lo, hi = ctypes.c_double(), ctypes.c_double()
+    _check(_lib.qsim_magnitude_range(h, ctypes.byref(lo), ctypes.byref(hi)))
+    return lo.value, hi.value
+
+
+def qsim_get_bounds(h) -> tuple[float, float]:
+    lo, hi = ctypes.c_double(), ctypes.c_double()
+    _check(_lib.qsim_get_bounds(h, ctypes.byref(lo), ctypes.byref(hi)))
+    return lo.value, hi.value
+
+
 def qsim_graph_begin(h):
     _check(_lib.qsim_graph_begin(h))
 
@@ -626,6 +640,14 @@ class State:
     def apply_matrix(self, u, qubits):
         qsim_apply_matrix(self.h, u, qubits)
         return self
+
+    def magnitude_range(self):
+        """(min non-zero |a|, max |a|) of an E state (qsim_magnitude_range)."""
+        return qsim_magnitude_range(self.h)
+
+    def bounds(self):
+        """(r0, r1) of an A state (qsim_get_bounds)."""
+        return qsim_get_bounds(self.h)
 
     def overlap(self, other):
         """<self|other> (qsim_overlap)."""

@@ -63,8 +63,6 @@ using namespace qsim;
 struct qsim_state {
     int n = 0, enc = 0, P = 1, nl = 0, transport = 0, rank = 0, dev = 0, fuse = 1;
     int pass_r = 4;  // register qubits per pass stage (QSIM_PASS_R=5 selects 32-amplitude groups)
-    int use_mma = 1; // tensor-core (DMMA) pair stages in fused passes (QSIM_PASS_MMA=0 disables)
-    int pass_kernel = 1;  // 1: relabelling pass k_lpass_e (lpass.h); 0: k_pass_e (QSIM_PASS_KERNEL=0)
     int pass_k = LP_MAX_K;  // tile qubits of the relabelling pass (QSIM_LPASS_K = 9..12)
     size_t amp_bytes = 16;
     uint64_t alloc_amps = 0;  // max(2^nl, 256): small shards are padded with zero amplitudes
@@ -254,393 +252,6 @@ static int sweep_gate_e(qsim_state *s, const PlanOp &o, const double *u) {
     return QSIM_OK;
 }
 
-// ============================================================================
-// fused tile passes (a6)
-// ============================================================================
-struct PassBuild {
-    std::vector<int> ops;      // indices into the run, in execution order
-    std::vector<int> high;     // local qubits >= PASS_LOW needed in the tile
-    std::vector<std::vector<int>> stage_q;     // per stage: register qubits, or the pair (type 1)
-    std::vector<std::vector<int>> stage_ops;   // per stage: op indices
-    std::vector<int> stage_type;               // 0 register stage, 1 tensor-core pair stage
-};
-
-// Qubits a gate acts on non-diagonally (X-type: the target of a dense /
-// anti-diagonal gate) and diagonally (Z-type: controls, diagonal targets).
-// Two gates commute if every shared qubit is Z-type for both.
-static void gate_masks(const PlanOp &o, uint64_t &xq, uint64_t &zq) {
-    xq = zq = 0;
-    if (o.cls == CLS_DIAG)
-        zq |= 1ull << o.l;
-    else
-        xq |= 1ull << o.l;
-    for (int c = 0; c < o.nctrl; ++c) zq |= 1ull << o.ctrl[c];
-}
-
-// Try to append op `idx` to the pass (tile capacity only); false (no change)
-// if it does not fit.  Stages are formed afterwards by stage_pass().
-static bool pass_add(PassBuild &pb, const PlanOp &o, int idx, int hmax, int nl, int max_gates = PASS_MAX_GATES) {
-    const bool needs_reg = o.cls != CLS_DIAG;
-    if ((int)pb.ops.size() >= max_gates) return false;
-    bool new_high = needs_reg && o.l >= PASS_LOW && std::find(pb.high.begin(), pb.high.end(), o.l) == pb.high.end();
-    if (new_high && (int)pb.high.size() >= hmax) return false;
-    if (new_high) pb.high.push_back(o.l);
-    // bring a local control into the tile too when there is room: a controlled
-    // gate with all its qubits in the tile can join a tensor-core pair stage
-    if (needs_reg && o.nctrl == 1) {
-        const int c = o.ctrl[0];
-        if (c >= PASS_LOW && c < nl && (int)pb.high.size() < hmax &&
-            std::find(pb.high.begin(), pb.high.end(), c) == pb.high.end())
-            pb.high.push_back(c);
-    }
-    pb.ops.push_back(idx);
-    return true;
-}
-
-// Split a pass into register stages (<= PASS_R register qubits each) with the
-// same commutation-aware greedy as the pass scheduler: each stage takes, in
-// order, every remaining gate that commutes with all skipped earlier gates and
-// whose target fits the register set.  Returns false if more than
-// PASS_MAX_STAGES stages are needed (the caller then shortens the pass).
-static bool in_tile(const PassBuild &pb, int q, int nl) {
-    if (q < 0 || q >= nl) return false;
-    return q < PASS_LOW || std::find(pb.high.begin(), pb.high.end(), q) != pb.high.end();
-}
-// Qubits (target and controls) of a gate if it can join a tensor-core pair
-// stage: at most two, all in the tile.  Returns the count (0 = not pairable).
-static int pair_qubits(const PassBuild &pb, const PlanOp &o, int nl, int *q) {
-    int n = 0;
-    if (!in_tile(pb, o.l, nl)) return 0;
-    q[n++] = o.l;
-    for (int c = 0; c < o.nctrl; ++c) {
-        if (!in_tile(pb, o.ctrl[c], nl) || n >= 2) return 0;
-        q[n++] = o.ctrl[c];
-    }
-    return n;
-}
-
-static bool stage_pass(PassBuild &pb, const std::vector<PlanOp> &run, int RR, bool use_mma, int nl) {
-    pb.stage_q.clear();
-    pb.stage_ops.clear();
-    pb.stage_type.clear();
-    std::vector<int> rem = pb.ops, order;
-    while (!rem.empty()) {
-        if ((int)pb.stage_q.size() >= PASS_MAX_STAGES) return false;
-        std::vector<int> taken, left;
-        uint64_t bx = 0, bz = 0;
-        // ---- tensor-core pair stage: every remaining gate acting only on the pair ----
-        int q0[2];
-        const int n0 = use_mma ? pair_qubits(pb, run[rem[0]], nl, q0) : 0;
-        if (n0 > 0) {
-            int a = q0[0], b = n0 == 2 ? q0[1] : -1;
-            if (b < 0) {  // partner: first commuting 2-qubit gate on a, else another 1-qubit gate's qubit
-                uint64_t sx = 0, sz = 0;
-                int alt = -1;
-                for (int k : rem) {
-                    const PlanOp &o = run[k];
-                    uint64_t xq, zq;
-                    gate_masks(o, xq, zq);
-                    const bool ok = !((xq & (sx | sz)) || (zq & sx));
-                    int q[2];
-                    const int nq = pair_qubits(pb, o, nl, q);
-                    if (ok && nq == 2 && (q[0] == a || q[1] == a)) {
-                        b = q[0] == a ? q[1] : q[0];
-                        break;
-                    }
-                    if (ok && nq == 1 && q[0] != a && alt < 0) alt = q[0];
-                    sx |= xq;
-                    sz |= zq;
-                }
-                if (b < 0) b = alt;
-                for (int t = 0; b < 0 && t < nl; ++t)
-                    if (t != a && in_tile(pb, t, nl)) b = t;
-            }
-            const uint64_t pm = (1ull << a) | (1ull << b);
-            for (int k : rem) {
-                const PlanOp &o = run[k];
-                uint64_t xq, zq;
-                gate_masks(o, xq, zq);
-                bool ok = !((xq & (bx | bz)) || (zq & bx)) && ((xq | zq) & ~pm) == 0 && o.l < nl;
-                if (ok) {
-                    taken.push_back(k);
-                } else {
-                    bx |= xq;
-                    bz |= zq;
-                    left.push_back(k);
-                }
-            }
-            pb.stage_q.push_back({a, b});
-            pb.stage_ops.push_back(taken);
-            pb.stage_type.push_back(1);
-            for (int k : taken) order.push_back(k);
-            rem.swap(left);
-            continue;
-        }
-        // ---- register stage: gates whose targets fit RR register qubits ----
-        std::vector<int> R;
-        for (int k : rem) {
-            const PlanOp &o = run[k];
-            uint64_t xq, zq;
-            gate_masks(o, xq, zq);
-            bool ok = !((xq & (bx | bz)) || (zq & bx));
-            if (ok && o.cls != CLS_DIAG && std::find(R.begin(), R.end(), o.l) == R.end()) {
-                if ((int)R.size() < RR)
-                    R.push_back(o.l);
-                else
-                    ok = false;
-            }
-            if (ok) {
-                taken.push_back(k);
-            } else {
-                bx |= xq;
-                bz |= zq;
-                left.push_back(k);
-            }
-        }
-        pb.stage_q.push_back(R);
-        pb.stage_ops.push_back(taken);
-        pb.stage_type.push_back(0);
-        for (int k : taken) order.push_back(k);
-        rem.swap(left);
-    }
-    pb.ops = order;
-    return true;
-}
-
-static void cmatmul2(const double *a, const double *b, double *c) {  // c = a * b (2x2 complex)
-    for (int r = 0; r < 2; ++r)
-        for (int k = 0; k < 2; ++k) {
-            double re = 0.0, im = 0.0;
-            for (int m = 0; m < 2; ++m) {
-                double ar = a[(r * 2 + m) * 2], ai = a[(r * 2 + m) * 2 + 1];
-                double br = b[(m * 2 + k) * 2], bi = b[(m * 2 + k) * 2 + 1];
-                re += ar * br - ai * bi;
-                im += ar * bi + ai * br;
-            }
-            c[(r * 2 + k) * 2] = re;
-            c[(r * 2 + k) * 2 + 1] = im;
-        }
-}
-
-static int launch_pass(qsim_state *s, const PassBuild &pb, const std::vector<PlanOp> &run,
-                       const std::vector<const double *> &us) {
-    const int K = std::min(pass_e_max_k(), s->nl);
-    const int h = K - PASS_LOW;
-    std::vector<int> high = pb.high;
-    for (int q = PASS_LOW; (int)high.size() < h && q < s->nl; ++q)
-        if (std::find(high.begin(), high.end(), q) == high.end()) high.push_back(q);
-    std::sort(high.begin(), high.end());
-    auto tile_bit = [&](int q) -> int {
-        if (q < PASS_LOW) return q;
-        for (int i = 0; i < h; ++i)
-            if (high[i] == q) return PASS_LOW + i;
-        return -1;
-    };
-    static PassParams p;  // large: keep off the stack
-    std::memset(&p, 0, sizeof(p));
-    p.nl = s->nl;
-    p.K = K;
-    p.ntiles = 1ull << (s->nl - K);
-    for (int i = 0; i < h; ++i) p.high_q[i] = high[i];
-    p.nstages = (int)pb.stage_q.size();
-    const int RR = s->pass_r;
-    p.R = RR;
-    p.noio = getenv("QSIM_DEBUG_PASS_NOIO") ? 1 : 0;
-    int gi = 0;
-    int nops4 = 0;
-    for (int si = 0; si < p.nstages; ++si) {
-        PassStage &st = p.st[si];
-        if (pb.stage_type[si] == 1) {
-            // tensor-core pair stage: lane bits 0,1 = the pair, lane bits 2-4 items,
-            // warp bits, fragment bits
-            const int a = pb.stage_q[si][0], b = pb.stage_q[si][1];
-            const int ta = tile_bit(a), tb = tile_bit(b);
-            std::vector<int> rest;
-            for (int t = 0; t < K; ++t)
-                if (t != ta && t != tb) rest.push_back(t);
-            // first item bit: residue mod 3 distinct from the pair's (conflict-free quarter warps)
-            int pick = 0;
-            for (size_t k2 = 0; k2 < rest.size(); ++k2)
-                if (rest[k2] % 3 != ta % 3 && rest[k2] % 3 != tb % 3) {
-                    pick = (int)k2;
-                    break;
-                }
-            std::vector<int> mb = {ta, tb, rest[pick]};
-            rest.erase(rest.begin() + pick);
-            for (int t : rest) mb.push_back(t);
-            for (int i = 0; i < K; ++i) st.mbits[i] = (int8_t)mb[i];
-            st.type = 1;
-            st.opi = (int8_t)nops4;
-            st.first_gate = (int8_t)gi;
-            st.ngates = 0;
-            // G = product of the stage's gates embedded in the pair basis c = bit(a) + 2 bit(b)
-            double G[4][4][2] = {};
-            for (int c = 0; c < 4; ++c) G[c][c][0] = 1.0;
-            for (int oi : pb.stage_ops[si]) {
-                const PlanOp &o = run[oi];
-                const double *u = us[oi];
-                double M[4][4][2] = {};
-                for (int c = 0; c < 4; ++c) M[c][c][0] = 1.0;
-                const int tm = (o.l == a) ? 1 : 2;
-                int cm = 0;
-                for (int c = 0; c < o.nctrl; ++c) cm |= (o.ctrl[c] == a) ? 1 : 2;
-                for (int c = 0; c < 4; ++c) {
-                    if ((c & tm) || (c & cm) != cm) continue;
-                    const int c1 = c | tm;
-                    M[c][c][0] = u[0]; M[c][c][1] = u[1];
-                    M[c][c1][0] = u[2]; M[c][c1][1] = u[3];
-                    M[c1][c][0] = u[4]; M[c1][c][1] = u[5];
-                    M[c1][c1][0] = u[6]; M[c1][c1][1] = u[7];
-                }
-                double N[4][4][2];
-                for (int r = 0; r < 4; ++r)
-                    for (int c = 0; c < 4; ++c) {
-                        double re = 0.0, im = 0.0;
-                        for (int m = 0; m < 4; ++m) {
-                            re += M[r][m][0] * G[m][c][0] - M[r][m][1] * G[m][c][1];
-                            im += M[r][m][0] * G[m][c][1] + M[r][m][1] * G[m][c][0];
-                        }
-                        N[r][c][0] = re;
-                        N[r][c][1] = im;
-                    }
-                std::memcpy(G, N, sizeof(G));
-            }
-            for (int r = 0; r < 4; ++r)
-                for (int c = 0; c < 4; ++c) p.op4[nops4][r * 4 + c] = make_double2(G[r][c][0], G[r][c][1]);
-            ++nops4;
-            continue;
-        }
-        std::vector<int> R;
-        for (int q : pb.stage_q[si]) R.push_back(tile_bit(q));
-        for (int b = 0; (int)R.size() < RR; ++b)
-            if (std::find(R.begin(), R.end(), b) == R.end()) R.push_back(b);
-        for (int r = 0; r < RR; ++r) st.rbits[r] = (int8_t)R[r];
-        // group bits: three with distinct residues mod 3 first (bank-conflict-free
-        // quarter warps under the XOR-fold swizzle), then the rest ascending.
-        std::vector<int> rest;
-        for (int b = 0; b < K; ++b)
-            if (std::find(R.begin(), R.end(), b) == R.end()) rest.push_back(b);
-        std::vector<int> gb;
-        for (int res = 0; res < 3; ++res)
-            for (size_t k = 0; k < rest.size(); ++k)
-                if (rest[k] % 3 == res) {
-                    gb.push_back(rest[k]);
-                    rest.erase(rest.begin() + k);
-                    break;
-                }
-        std::sort(gb.begin(), gb.end());
-        for (int b : rest) gb.push_back(b);
-        for (int i = 0; i < K - RR; ++i) st.gbits[i] = (int8_t)gb[i];
-        st.first_gate = (int8_t)gi;
-        // last gate (index into p.g) touching each local qubit in this stage, for merging
-        int last_on[64];
-        for (int k2 = 0; k2 < 64; ++k2) last_on[k2] = -1;
-        std::vector<int> merged_ok;  // per gate in this stage: uncontrolled (mergeable)
-        for (int oi : pb.stage_ops[si]) {
-            const PlanOp &o = run[oi];
-            // merge an uncontrolled gate into the previous uncontrolled gate on the
-            // same target when no gate in between touched that qubit
-            if (o.nctrl == 0 && last_on[o.l] >= 0 && merged_ok[last_on[o.l] - st.first_gate]) {
-                PassGate &m = p.g[last_on[o.l]];
-                double prod[8];
-                cmatmul2(us[oi], m.u, prod);
-                std::memcpy(m.u, prod, sizeof(prod));
-                bool off0 = prod[2] == 0.0 && prod[3] == 0.0 && prod[4] == 0.0 && prod[5] == 0.0;
-                bool dia0 = prod[0] == 0.0 && prod[1] == 0.0 && prod[6] == 0.0 && prod[7] == 0.0;
-                if ((m.kind & 3) != PG_DIAG_OUT || m.kind == PG_SWAP || m.kind == PG_SWAP + PG_PARTIAL) {
-                    int base_kind = off0 ? PG_DIAG_IN : (dia0 ? PG_ANTI : PG_DENSE);
-                    if (dia0 && prod[2] == 1.0 && prod[3] == 0.0 && prod[4] == 1.0 && prod[5] == 0.0) base_kind = PG_SWAP;
-                    m.kind = (int8_t)(base_kind | (m.kind & PG_PARTIAL));
-                    m.op = (int8_t)pass_op(m.kind, m.slot, RR);
-                }
-                // a DIAG_OUT gate only merges with diagonal gates (target outside the registers)
-                continue;
-            }
-            PassGate &g = p.g[gi];
-            std::memcpy(g.u, us[oi], sizeof(g.u));
-            int8_t cslot = 0;
-            uint64_t cout = 0;
-            for (int c = 0; c < o.nctrl; ++c) {
-                int tb = (o.ctrl[c] < s->nl) ? tile_bit(o.ctrl[c]) : -1;
-                int slot = -1;
-                for (int r = 0; r < RR; ++r)
-                    if (tb >= 0 && R[r] == tb) slot = r;
-                if (slot >= 0)
-                    cslot |= (int8_t)(1 << slot);
-                else
-                    cout |= 1ull << o.ctrl[c];
-            }
-            g.cslot = cslot;
-            g.cmask_out = cout;
-            if (cout) st.needs_full = 1;
-            int ttb = (o.l < s->nl) ? tile_bit(o.l) : -1;
-            int tslot = -1;
-            for (int r = 0; r < RR; ++r)
-                if (ttb >= 0 && R[r] == ttb) tslot = r;
-            int kind;
-            if (o.cls == CLS_DIAG) {
-                if (tslot >= 0) {
-                    kind = PG_DIAG_IN;
-                    g.slot = (int8_t)tslot;
-                } else {
-                    kind = PG_DIAG_OUT;
-                    g.tmask_out = 1ull << o.l;
-                    st.needs_full = 1;
-                }
-            } else {
-                if (tslot < 0) {
-                    set_error("internal: pass target not in register set");
-                    return QSIM_EINVAL;
-                }
-                kind = (o.cls == CLS_ANTI) ? PG_ANTI : PG_DENSE;
-                const double *uu = us[oi];
-                if (o.cls == CLS_ANTI && uu[2] == 1.0 && uu[3] == 0.0 && uu[4] == 1.0 && uu[5] == 0.0) kind = PG_SWAP;
-                g.slot = (int8_t)tslot;
-            }
-            if (cslot) {
-                // a register permutation under an in-register control cannot be a
-                // slot flip: apply it as (exact) dense arithmetic
-                if (kind == PG_ANTI || kind == PG_SWAP) kind = PG_DENSE;
-                kind |= PG_PARTIAL;
-            }
-            g.kind = (int8_t)kind;
-            g.op = (int8_t)pass_op(kind, g.slot, RR);
-            merged_ok.push_back(o.nctrl == 0 && o.l < s->nl ? 1 : 0);
-            if (o.l < 64) last_on[o.l] = gi;
-            for (int c = 0; c < o.nctrl; ++c)
-                if (o.ctrl[c] < 64) {
-                    // a control use blocks merging across it
-                    if (last_on[o.ctrl[c]] >= 0) merged_ok[last_on[o.ctrl[c]] - st.first_gate] = 0;
-                    last_on[o.ctrl[c]] = -1;
-                }
-            ++gi;
-        }
-        st.ngates = (int8_t)(gi - st.first_gate);
-    }
-    if (getenv("QSIM_DEBUG_PASSES")) {
-        std::string d = "pass: " + std::to_string(pb.ops.size()) + " gates, stages:";
-        for (int si = 0; si < p.nstages; ++si)
-            d += (pb.stage_type[si] ? " M" : " R") + std::to_string(pb.stage_ops[si].size());
-        fprintf(stderr, "%s\n", d.c_str());
-    }
-    int grid = (int)std::min<uint64_t>(p.ntiles, (uint64_t)pass_e_max_grid(RR));
-    s->st.stages += p.nstages;
-    for (auto &sh : s->shards) {
-        p.a = sh.amps;
-        p.shard_base = shard_base(s, sh);
-        double fl = 0.0;
-        for (int k : pb.ops) fl += gate_flops(s, sh, run[k], us[k]);
-        prof_begin(s);
-        launch_pass_e(p, grid, s->stream);
-        prof_end(s, QSIM_K_PASS, std::ldexp(2.0 * (double)s->amp_bytes, s->nl), fl);
-        s->st.kernels++;
-        s->st.passes++;
-        s->st.fused_gates += (int64_t)pb.ops.size();
-        s->st.hbm_bytes += std::ldexp(2.0 * (double)s->amp_bytes, s->nl);
-    }
-    CU(cudaGetLastError());
-    return QSIM_OK;
-}
 
 // ---- relabelling tile pass (lpass.h) ----
 static PlanOp plan_op_of(const LGate &g) {
@@ -671,7 +282,7 @@ struct LaunchSink : LPassSink {
                             "%d carried, %d deferred\n",
                     ids.size(), nreal, cs.stages, cs.ops, cs.diagt, cs.shears, cs.dense, cs.flips, cs.relabels,
                     cs.cswaps, cs.tile_free, cs.events, p.ncoef, cs.carried, cs.deferred);
-        static LPassParams q;  // large: keep off the stack
+        static thread_local LPassParams q;  // large: keep off the stack; one per thread (handles on other threads)
         std::memcpy(&q, &p, sizeof(q));
         q.noio = getenv("QSIM_DEBUG_PASS_NOIO") ? 1 : 0;
         s->st.stages += p.nstages;
@@ -824,57 +435,11 @@ static int run_gates_lpass(qsim_state *s, const std::vector<PlanOp> &run, const 
     return rc;
 }
 
-// Greedy commutation-aware pass scheduler (a6): each pass takes, in circuit
-// order, every not-yet-applied gate that commutes with all earlier skipped
-// gates and fits the tile (<= K - PASS_LOW high target qubits, <= PASS_MAX_*).
+// Local gates of an E state (a3-a6): the relabelling tile pass when the shard
+// holds a tile (lpass.h), single-gate sweeps otherwise (or with fusion off).
 static int run_gates_e(qsim_state *s, const std::vector<PlanOp> &run, const std::vector<const double *> &us) {
-    if (s->pass_kernel == 1 && s->fuse && std::min(LP_MAX_K, s->nl) >= LP_MIN_K) return run_gates_lpass(s, run, us);
-    const int K = std::min(pass_e_max_k(), s->nl);
-    const bool can_fuse = s->fuse && K >= PASS_MIN_K;
-    if (!can_fuse) {
-        for (size_t i = 0; i < run.size(); ++i) RC(sweep_gate_e(s, run[i], us[i]));
-        return QSIM_OK;
-    }
-    std::vector<char> done(run.size(), 0);
-    size_t first = 0;
-    const double pass_bytes = std::ldexp(2.0 * (double)s->amp_bytes, s->nl);
-    while (first < run.size()) {
-        PassBuild pb;
-        uint64_t bx = 0, bz = 0;
-        for (size_t k = first; k < run.size(); ++k) {
-            if (done[k]) continue;
-            uint64_t xq, zq;
-            gate_masks(run[k], xq, zq);
-            const bool conflict = (xq & (bx | bz)) || (zq & bx);
-            if (!conflict && pass_add(pb, run[k], (int)k, K - PASS_LOW, s->nl)) {
-                done[k] = 1;
-            } else {
-                bx |= xq;
-                bz |= zq;
-            }
-            if ((int)pb.ops.size() >= PASS_MAX_GATES) break;
-        }
-        // form register stages; if the pass needs too many, give back its last gates
-        while (!stage_pass(pb, run, s->pass_r, s->use_mma && K >= 11 && s->pass_r == 4, s->nl)) {
-            int k = pb.ops.back();
-            pb.ops.pop_back();
-            done[k] = 0;
-            if (k < (int)first) first = k;
-            pb.high.clear();
-            for (int k2 : pb.ops)
-                if (run[k2].cls != CLS_DIAG && run[k2].l >= PASS_LOW &&
-                    std::find(pb.high.begin(), pb.high.end(), run[k2].l) == pb.high.end())
-                    pb.high.push_back(run[k2].l);
-        }
-        double sweep_bytes = 0.0;
-        for (int k : pb.ops) sweep_bytes += gate_bytes_alone(s, s->shards[0], run[k], us[k]);
-        if (pb.ops.size() >= 2 && pass_bytes < sweep_bytes) {
-            RC(launch_pass(s, pb, run, us));
-        } else {
-            for (int k : pb.ops) RC(sweep_gate_e(s, run[k], us[k]));
-        }
-        while (first < run.size() && done[first]) ++first;
-    }
+    if (s->fuse && std::min(LP_MAX_K, s->nl) >= LP_MIN_K) return run_gates_lpass(s, run, us);
+    for (size_t i = 0; i < run.size(); ++i) RC(sweep_gate_e(s, run[i], us[i]));
     return QSIM_OK;
 }
 
@@ -987,6 +552,10 @@ static int remap(qsim_state *s, std::vector<std::pair<int, int>> pairs) {
         return x.second < y.second;  // by local bit
     });
     const int m = (int)pairs.size();
+    if (m < 1 || m > kRemapMaxBits) {  // RemapVals holds 2^3 - 1 partners (the planner caps groups)
+        set_error("remap: " + std::to_string(m) + " bits in one group (at most " + std::to_string(kRemapMaxBits) + ")");
+        return QSIM_EINVAL;
+    }
     RemapBlock blk{};
     blk.m = m;
     int jb[8];
@@ -1375,8 +944,6 @@ int qsim_create_ex(const qsim_config *cfg, qsim_state **out) {
     s->rank = transport == QSIM_TRANSPORT_NCCL ? cfg->rank : 0;
     s->fuse = cfg->fuse;
     if (const char *pr = getenv("QSIM_PASS_R")) s->pass_r = (atoi(pr) == 4) ? 4 : 5;
-    if (const char *pm = getenv("QSIM_PASS_MMA")) s->use_mma = atoi(pm) != 0;
-    if (const char *pk = getenv("QSIM_PASS_KERNEL")) s->pass_kernel = atoi(pk) != 0 ? 1 : 0;
     if (const char *lk = getenv("QSIM_LPASS_K")) s->pass_k = std::max(LP_MIN_K, std::min(LP_MAX_K, atoi(lk)));
     s->amp_bytes = s->enc == QSIM_ENC_FP64 ? 16 : 2;
     if (cfg->device >= 0) {
@@ -1792,6 +1359,42 @@ int qsim_norm(qsim_state *s, double *norm2) {
     std::vector<double> phys;
     RC(phys_probs(s, phys));
     *norm2 = phys[0];
+    return QSIM_OK;
+}
+
+int qsim_magnitude_range(qsim_state *s, double *min_nonzero, double *max) {
+    if (!s || !min_nonzero || !max) return QSIM_EINVAL;
+    if (s->capturing) {
+        set_error("qsim_magnitude_range: not allowed while a graph capture is open");
+        return QSIM_EINVAL;
+    }
+    if (s->enc != QSIM_ENC_FP64) {
+        set_error("qsim_magnitude_range: E encoding only (an A state's range is its bounds, qsim_get_codes)");
+        return QSIM_EUNSUPPORTED;
+    }
+    cudaSetDevice(s->dev);
+    double mn = INFINITY, mx = 0.0;
+    for (auto &sh : s->shards) {
+        uint64_t init[2] = {0x7ff0000000000000ull, 0ull};  // (+inf, 0) as bit patterns
+        CU(cudaMemcpyAsync(s->d_out, init, sizeof(init), cudaMemcpyHostToDevice, s->stream));
+        launch_absrange_e(sh.amps, 1ull << s->nl, s->d_out, s->stream);
+        s->st.kernels++;
+        CU(cudaMemcpyAsync(s->h_out, s->d_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+        CU(cudaStreamSynchronize(s->stream));
+        mn = std::min(mn, s->h_out[0]);
+        mx = std::max(mx, s->h_out[1]);
+    }
+    if (s->transport == QSIM_TRANSPORT_NCCL && s->P > 1) {
+        double v[2] = {mn, -mx};
+        CU(cudaMemcpyAsync(s->d_out, v, sizeof(v), cudaMemcpyHostToDevice, s->stream));
+        NC(ncclAllReduce(s->d_out, s->d_out, 2, ncclDouble, ncclMin, s->comm, s->stream));
+        CU(cudaMemcpyAsync(s->h_out, s->d_out, sizeof(v), cudaMemcpyDeviceToHost, s->stream));
+        CU(cudaStreamSynchronize(s->stream));
+        mn = s->h_out[0];
+        mx = -s->h_out[1];
+    }
+    *min_nonzero = std::isinf(mn) ? 0.0 : std::sqrt(mn);
+    *max = std::sqrt(mx);
     return QSIM_OK;
 }
 
@@ -2271,6 +1874,23 @@ static int sync_bounds(qsim_state *s) {
     s->r0 = rr[0];
     s->r1 = rr[1];
     s->r_stale = false;
+    return QSIM_OK;
+}
+
+int qsim_get_bounds(qsim_state *s, double *r0, double *r1) {
+    if (!s || !r0 || !r1) return QSIM_EINVAL;
+    if (s->capturing) {
+        set_error("qsim_get_bounds: not allowed while a graph capture is open");
+        return QSIM_EINVAL;
+    }
+    if (s->enc != QSIM_ENC_ADAPTIVE2) {
+        set_error("qsim_get_bounds: A only");
+        return QSIM_EUNSUPPORTED;
+    }
+    cudaSetDevice(s->dev);
+    RC(sync_bounds(s));
+    *r0 = s->r0;
+    *r1 = s->r1;
     return QSIM_OK;
 }
 

@@ -28,6 +28,11 @@ struct PlanOp {
     int32_t gate_index;
 };
 
+// An all-to-all remap swaps at most this many global bits at once: each shard
+// then trades 2^m - 1 blocks (RemapVals holds 7 partners); more global bits
+// than this are remapped in several groups.
+constexpr int kRemapMaxBits = 3;
+
 struct Planner {
     int n = 0, nl = 0;
     std::vector<int> pos, inv;  // logical -> physical bit, physical -> logical

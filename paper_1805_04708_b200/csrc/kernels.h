@@ -38,80 +38,6 @@ struct ScaleParams {
 };
 void launch_scale_e(const ScaleParams &p, cudaStream_t s);
 
-// ---- fused tile pass (a6) ----------------------------------------------------
-constexpr int PASS_LOW = 3;       // tile always holds qubits 0..2 (128 B contiguous runs = one L2 line)
-constexpr int PASS_MAX_K = 12;    // 2^12 amplitudes x 16 B = 64 KiB of shared memory per CTA
-constexpr int PASS_MIN_K = 9;
-constexpr int PASS_R_MAX = 5;     // qubits held in registers per stage: R = 4 (16 amplitudes / thread) or 5 (32)
-constexpr int PASS_THREADS = 128;
-constexpr int PASS_MAX_GATES = 32;
-constexpr int PASS_MAX_STAGES = 12;  // smem: 64 KiB tile + 3 KiB gates + 6 KiB group table < 75 KiB (3 CTAs/SM)
-
-enum PassGateKind : int8_t { PG_DENSE = 0, PG_DIAG_IN = 1, PG_ANTI = 2, PG_DIAG_OUT = 3 };
-constexpr int PG_SWAP = 8;  // kind value: anti-diagonal with u01 = u10 = 1 (X, CNOT, TOFFOLI): a pure register swap
-constexpr int PG_PARTIAL = 4;  // kind flag: some controls sit in the register set (per-slot predicate)
-
-struct PassGate {
-    double u[8];
-    uint64_t cmask_out;  // control bits outside the stage's register set (full physical index)
-    uint64_t tmask_out;  // PG_DIAG_OUT: target bit (full physical index)
-    int8_t kind;
-    int8_t slot;         // target slot (0..3) in the register set
-    int8_t cslot;        // slot bits that must be 1 (controls inside the register set)
-    int8_t op;           // dense dispatch index (pass_op()), computed on the host
-    int8_t pad[4];
-};
-// Dense dispatch index of a pass gate: slot * 6 + {0 dense, 1 dense-partial,
-// 2 diag, 3 diag-partial, 4 anti, 5 swap}, or 6 * R + {0, 1} for a diagonal
-// gate whose target is outside the register set (full / partial).
-__host__ __device__ inline int pass_op(int kind, int slot, int R) {
-    const bool part = (kind & PG_PARTIAL) != 0;
-    if (kind == PG_SWAP) return slot * 6 + 5;
-    switch (kind & 3) {
-        case PG_DENSE: return slot * 6 + (part ? 1 : 0);
-        case PG_DIAG_IN: return slot * 6 + (part ? 3 : 2);
-        case PG_ANTI: return slot * 6 + 4;
-        default: return 6 * R + (part ? 1 : 0);
-    }
-}
-
-// A pass stage is either a register stage (type 0: gates applied with fp64
-// FMAs on 2^R register-resident amplitudes per thread) or a tensor-core pair
-// stage (type 1: one 4x4 complex operator on two tile qubits, applied with
-// mma.sync.m8n8k4.f64 -- lanes = 4 amplitudes of a quad x 8 items).
-struct PassStage {
-    int8_t rbits[PASS_R_MAX];  // type 0: slot s <-> tile bit rbits[s] (first R used)
-    int8_t gbits[PASS_MAX_K];  // type 0: group index bit i <-> tile bit gbits[i] (first K - R used)
-    int8_t mbits[PASS_MAX_K];  // type 1: lane bits 0-4, warp bits 5-6, fragment bits 7.. <-> tile bits
-    int8_t first_gate;
-    int8_t ngates;
-    int8_t needs_full;   // type 0: some gate of the stage tests bits outside the register set
-    int8_t type;
-    int8_t opi;          // type 1: index into PassParams::op4
-    int8_t pad[3];
-};
-
-struct PassParams {
-    void *a;
-    uint64_t shard_base;  // rank bits of this shard (full physical index of local 0)
-    uint64_t ntiles;
-    int32_t nl;
-    int32_t K;            // tile qubits
-    int32_t nstages;
-    int32_t R;            // register qubits per stage (4 or 5)
-    int32_t noio;         // debug: skip the HBM tile load / store (timing experiments only)
-    int32_t pad_noio;
-    int32_t high_q[PASS_MAX_K - PASS_LOW];  // local qubit of tile bit PASS_LOW + i (ascending)
-    int32_t pad2;
-    PassStage st[PASS_MAX_STAGES];
-    PassGate g[PASS_MAX_GATES];
-    double2 op4[PASS_MAX_STAGES][16];  // type-1 operators G[c'][c], c = bit(qa) + 2 bit(qb)
-};
-static_assert(sizeof(PassParams) <= 32000, "kernel parameter block too large");
-void launch_pass_e(const PassParams &p, int grid, cudaStream_t s);
-int pass_e_max_grid(int R);
-int pass_e_max_k();  // tile qubits of the selected pass-kernel occupancy
-
 // ---- k-qubit dense matrix (qsim_apply_matrix) ---------------------------------
 struct MatKParams {
     void *a;
@@ -174,6 +100,7 @@ void launch_probs_e(const void *a, int nl, double *partials, double *out, cudaSt
 // S = sum_{i: bit q = 0} conj(a_i) a_{i | 2^q}  (out[0] = re, out[1] = im)
 void launch_pairdot_e(const void *a, int nl, int q, double *partials, double *out, cudaStream_t s);
 // S = sum_i conj(x_i) y_i over two shards (global-qubit pairs in loopback mode)
+void launch_absrange_e(const void *a, uint64_t n, void *out_u64x2, cudaStream_t s);
 void launch_dot_e(const void *x, const void *y, uint64_t n, double *partials, double *out, cudaStream_t s);
 // Collapse: zero amplitudes whose bit q != keep, scale the others by f.
 void launch_collapse_e(void *a, uint64_t n, int q, int keep, double f, cudaStream_t s);

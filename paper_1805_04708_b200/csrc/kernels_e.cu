@@ -184,385 +184,6 @@ void launch_scale_e(const ScaleParams &p, cudaStream_t s) {
 }
 
 // ============================================================================
-// fused tile pass
-// ============================================================================
-__device__ __forceinline__ uint32_t swz(uint32_t x) { return x ^ (((x >> 3) ^ (x >> 6) ^ (x >> 9)) & 7u); }
-
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-    uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
-
-// In-place pair updates.  Each output's final FMA is the last use of exactly
-// one input, so the register allocator can write every output over its own
-// input: no register copies at the gate-dispatch merge points (the loop over a
-// stage's gates is a runtime switch).
-//   x' = u00 x + u01 y,  y' = u10 x + u11 y   (u = {u00r,u00i,u01r,u01i,u10r,u10i,u11r,u11i})
-__device__ __forceinline__ void pair_dense(double2 &x, double2 &y, const double (&u)[8]) {
-    const double p0 = fma(u[2], y.x, fma(-u[1], x.y, -u[3] * y.y));  // x'.re - u00r x.re
-    const double p1 = fma(u[2], y.y, fma(u[1], x.x, u[3] * y.x));    // x'.im - u00r x.im
-    const double p2 = fma(u[4], x.x, fma(-u[5], x.y, -u[7] * y.y));  // y'.re - u11r y.re
-    const double p3 = fma(u[4], x.y, fma(u[5], x.x, u[7] * y.x));    // y'.im - u11r y.im
-    x.x = fma(u[0], x.x, p0);
-    x.y = fma(u[0], x.y, p1);
-    y.x = fma(u[6], y.x, p2);
-    y.y = fma(u[6], y.y, p3);
-}
-__device__ __forceinline__ void amp_phase(double2 &x, double ur, double ui) {
-    const double p = -ui * x.y, q = ui * x.x;
-    x.x = fma(ur, x.x, p);
-    x.y = fma(ur, x.y, q);
-}
-
-// Gate table entry as staged in shared memory (one LDS.128 per complex entry).
-struct SmGate {
-    double2 u[4];        // u00, u01, u10, u11
-    uint64_t cmask_out;
-    uint64_t tmask_out;
-    int32_t kind, slot, cslot, op;
-};
-
-// Gate application on the NS = 2^R register-resident amplitudes of one group.
-// `f` is the group's slot-flip mask: register j holds the amplitude of
-// logical slot j ^ f.  An uncontrolled X / CNOT-like swap on slot S is applied
-// as f ^= 2^S (no data moves); later gates of the stage select conjugated
-// coefficients for flipped slots and the stage's store XORs f into the
-// (GF(2)-linear) smem address.  Every update is in place, so the register
-// allocator never copies the amplitudes at the gate-dispatch merge points.
-// FULL: no control inside the register set.
-template <int NS, int S, bool FULL>
-__device__ __forceinline__ void pg_dense(double2 (&v)[NS], const SmGate &g, int cslot, uint32_t f) {
-    // flipped target slot: registers hold (y, x): apply X U X (complex entry c -> c ^ 3)
-    const int cx = ((f >> S) & 1u) ? 3 : 0;
-    const double2 e0 = g.u[0 ^ cx], e1 = g.u[1 ^ cx], e2 = g.u[2 ^ cx], e3 = g.u[3 ^ cx];
-    const double u[8] = {e0.x, e0.y, e1.x, e1.y, e2.x, e2.y, e3.x, e3.y};
-#pragma unroll
-    for (int j = 0; j < NS; ++j) {
-        if (j & (1 << S)) continue;
-        if (!FULL && (((uint32_t)j ^ f) & cslot) != (uint32_t)cslot) continue;
-        pair_dense(v[j], v[j | (1 << S)], u);
-    }
-}
-// diagonal on slot S: logical bit 0 -> a0, logical bit 1 -> a1
-template <int NS, int S, bool FULL>
-__device__ __forceinline__ void pg_phase(double2 (&v)[NS], double2 a0, double2 a1, int cslot, uint32_t f) {
-    const bool fl = (f >> S) & 1u;
-    const double2 c0 = fl ? a1 : a0;  // registers with bit S = 0
-    const double2 c1 = fl ? a0 : a1;  // registers with bit S = 1
-#pragma unroll
-    for (int j = 0; j < NS; ++j) {
-        if (!FULL && (((uint32_t)j ^ f) & cslot) != (uint32_t)cslot) continue;
-        if (j & (1 << S))
-            amp_phase(v[j], c1.x, c1.y);
-        else
-            amp_phase(v[j], c0.x, c0.y);
-    }
-}
-template <int NS>
-__device__ __forceinline__ void pg_diag_out(double2 (&v)[NS], double2 c, int cslot, uint32_t f, bool full) {
-    if (full) {
-#pragma unroll
-        for (int j = 0; j < NS; ++j) amp_phase(v[j], c.x, c.y);
-    } else {
-#pragma unroll
-        for (int j = 0; j < NS; ++j)
-            if ((((uint32_t)j ^ f) & cslot) == (uint32_t)cslot) amp_phase(v[j], c.x, c.y);
-    }
-}
-
-// one gate on slot S (compile time) of a group; sub = op % 6
-template <int NS, int S>
-__device__ __forceinline__ void pg_slot(double2 (&v)[NS], const SmGate &g, int sub, int cs, uint32_t &f) {
-    switch (sub) {
-        case 0: pg_dense<NS, S, true>(v, g, cs, f); break;
-        case 1: pg_dense<NS, S, false>(v, g, cs, f); break;
-        case 2: pg_phase<NS, S, true>(v, g.u[0], g.u[3], cs, f); break;
-        case 3: pg_phase<NS, S, false>(v, g.u[0], g.u[3], cs, f); break;
-        case 4:  // x' = u01 y, y' = u10 x: flip slot S, then bit 0 gets u01, bit 1 gets u10
-            f ^= 1u << S;
-            pg_phase<NS, S, true>(v, g.u[1], g.u[2], 0, f);
-            break;
-        default: f ^= 1u << S; break;  // 5: uncontrolled in-register swap = slot flip
-    }
-}
-
-// D = A B + C for one m8n8k4 f64 tile (A: lane (r = lane>>2, k = lane&3);
-// B: lane (k = lane&3, n = lane>>2); D: lane (r, n = 2 (lane&3) + {0,1})).
-__device__ __forceinline__ void dmma_first(double &d0, double &d1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%4};\n"
-                 : "=d"(d0), "=d"(d1) : "d"(a), "d"(b), "d"(0.0));
-}
-__device__ __forceinline__ void dmma_acc(double &d0, double &d1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                 : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
-}
-
-// Shared memory of one CTA: the tile (2^K double2, XOR-swizzled), the
-// two-level deposit tables of the high tile bits, the gate table, and per
-// stage the swizzled base address of every register group.
-struct PassSmemLayout {
-    size_t tile, depA, depB, depJ, gates, gx, fbt, total;
-};
-__host__ __device__ inline PassSmemLayout pass_layout(int K, int R, int nstages) {
-    PassSmemLayout L;
-    L.tile = 0;
-    L.depA = ((size_t)1 << K) * 16;
-    L.depB = L.depA + 32 * 8;
-    L.depJ = L.depB + 32 * 8;
-    L.gates = L.depJ + 32 * 8;
-    L.gx = L.gates + PASS_MAX_GATES * sizeof(SmGate);
-    L.fbt = L.gx + (size_t)nstages * ((size_t)1 << (K - R)) * 2;
-    L.total = L.fbt + (size_t)nstages * 8 * 2;
-    return L;
-}
-
-template <int R, int MINB>
-__global__ void __launch_bounds__(PASS_THREADS, MINB) k_pass_e(const __grid_constant__ PassParams p) {
-    constexpr int NS = 1 << R;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int K = p.K;
-    const PassSmemLayout L = pass_layout(K, R, p.nstages);
-    double2 *tile = reinterpret_cast<double2 *>(smem_raw + L.tile);
-    uint64_t *depA = reinterpret_cast<uint64_t *>(smem_raw + L.depA);  // high tile bits 0..4
-    uint64_t *depB = reinterpret_cast<uint64_t *>(smem_raw + L.depB);  // high tile bits 5..
-    SmGate *gates = reinterpret_cast<SmGate *>(smem_raw + L.gates);
-    uint16_t *gx = reinterpret_cast<uint16_t *>(smem_raw + L.gx);
-    uint16_t *fbt = reinterpret_cast<uint16_t *>(smem_raw + L.fbt);
-    const uint32_t tsize = 1u << K;
-    const int h = K - PASS_LOW;
-    const uint32_t ngroups = tsize >> R;
-    const uint32_t tid = threadIdx.x;
-    // ---- one-time setup per CTA ----
-    if (tid < 64) {
-        const int lo = tid < 32 ? 0 : 5;
-        const uint32_t hi = tid & 31u;
-        uint64_t m = 0;
-        for (int i = 0; i < 5 && lo + i < h; ++i)
-            if (hi & (1u << i)) m |= 1ull << p.high_q[lo + i];
-        (tid < 32 ? depA : depB)[hi] = m;
-    }
-    for (int gi = tid; gi < PASS_MAX_GATES; gi += PASS_THREADS) {
-        const PassGate &g = p.g[gi];
-        SmGate sg;
-        for (int c = 0; c < 4; ++c) sg.u[c] = make_double2(g.u[2 * c], g.u[2 * c + 1]);
-        sg.cmask_out = g.cmask_out;
-        sg.tmask_out = g.tmask_out;
-        sg.kind = g.kind;
-        sg.slot = g.slot;
-        sg.cslot = g.cslot;
-        sg.op = g.op;
-        gates[gi] = sg;
-    }
-    for (int s = 0; s < p.nstages; ++s) {
-        const PassStage &st = p.st[s];
-        if (st.type == 1) {  // pair stage: thread base address (lane, warp bits) + fragment basis
-            uint32_t xl = 0;
-            for (int i = 0; i < 7; ++i) xl |= ((tid >> i) & 1u) << st.mbits[i];
-            gx[s * ngroups + tid] = (uint16_t)swz(xl);
-            if (tid < 8) fbt[s * 8 + tid] = (tid < 5 && 7 + (int)tid < K) ? (uint16_t)swz(1u << st.mbits[7 + tid]) : 0;
-            continue;
-        }
-        for (uint32_t grp = tid; grp < ngroups; grp += PASS_THREADS) {
-            uint32_t x0 = 0;
-            for (int i = 0; i < K - R; ++i) x0 |= ((grp >> i) & 1u) << st.gbits[i];
-            gx[s * ngroups + grp] = (uint16_t)swz(x0);
-        }
-    }
-    __syncthreads();
-    double2 *__restrict__ a = reinterpret_cast<double2 *>(p.a);
-    constexpr uint32_t LOWM = (1u << PASS_LOW) - 1u;
-    auto dep = [&](uint32_t hi) -> uint64_t { return depA[hi & 31u] | depB[hi >> 5]; };
-    static_assert(PASS_THREADS == 128, "load/store addressing assumes x = tid + 128 j");
-    const uint32_t njt = tsize >> 7;  // elements per thread in the load / store loops
-    const uint32_t s_tid = swz(tid);
-    const uint64_t d_tid = (tid & LOWM) | dep(tid >> PASS_LOW);
-    uint64_t *depJ = reinterpret_cast<uint64_t *>(smem_raw + L.depJ);  // dep(16 j): high tile bits >= 4
-    for (uint32_t j = tid; j < njt; j += PASS_THREADS) depJ[j] = dep(j << (7 - PASS_LOW));
-    __syncthreads();
-
-    for (uint64_t T = blockIdx.x; T < p.ntiles; T += gridDim.x) {
-        // base: insert zeros at the tile's qubits (0..PASS_LOW-1 and high_q ascending)
-        uint64_t base = T << PASS_LOW;
-        for (int i = 0; i < h; ++i) base = insert_zero(base, p.high_q[i]);
-        // ---- load the tile (coalesced 128 B runs) ----
-        // x = tid + 128 j: swz and the deposit are GF(2)-linear on disjoint
-        // bits, so address = a[(base | d_tid) + depJ[j]] and smem = s_tid ^ swz(128 j).
-        const double2 *pt = a + (base | d_tid);
-        if (!p.noio) {
-#pragma unroll 8
-            for (uint32_t j = 0; j < njt; ++j) cp_async16(&tile[s_tid ^ swz(j << 7)], pt + depJ[j]);
-        }
-        cp_async_wait_all();
-        __syncthreads();
-        // ---- stages ----
-        for (int s = 0; s < p.nstages; ++s) {
-            const PassStage &st = p.st[s];
-            if (st.type == 1) {
-                // ---- tensor-core pair stage: amp' = G amp on the quad (lane bits 0,1) ----
-                // Real 8x8 form: k = c <-> Re(in_c), k = 4 + c <-> Im(in_c);
-                // n = 2c' <-> Re(out_c'), n = 2c' + 1 <-> Im(out_c').  A lane holds
-                // amp c of item r as (A chunk 0, A chunk 1) and receives amp'_c as (d0, d1).
-                // Per-thread base address and fragment-bit basis come from the
-                // per-CTA tables built at kernel start (GF(2)-linear swizzle).
-                const uint32_t sl = gx[s * ngroups + tid];
-                const uint16_t *fbs = fbt + s * 8;
-                const uint32_t fb0 = fbs[0], fb1 = fbs[1], fb2 = fbs[2], fb3 = fbs[3], fb4 = fbs[4];
-                const uint32_t off[8] = {0u, fb0, fb1, fb0 ^ fb1, fb2, fb0 ^ fb2, fb1 ^ fb2, fb0 ^ fb1 ^ fb2};
-                const uint32_t c = tid & 3u, nn = (tid & 31u) >> 2;
-                const double2 gcc = p.op4[st.opi][(nn >> 1) * 4 + c];  // G[c'][c]
-                const double b0 = (nn & 1u) ? gcc.y : gcc.x;            // B[c][n]
-                const double b1 = (nn & 1u) ? gcc.x : -gcc.y;           // B[4 + c][n]
-                const uint32_t nch = 1u << (K - 10);                     // chunks of 8 fragments
-                for (uint32_t ch = 0; ch < nch; ++ch) {
-                    const uint32_t cb = sl ^ ((ch & 1u) ? fb3 : 0u) ^ ((ch & 2u) ? fb4 : 0u);
-                    double2 v8[8];
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) v8[j] = tile[cb ^ off[j]];
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        double d0, d1;
-                        dmma_first(d0, d1, v8[j].x, b0);
-                        dmma_acc(d0, d1, v8[j].y, b1);
-                        v8[j] = make_double2(d0, d1);
-                    }
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) tile[cb ^ off[j]] = v8[j];
-                }
-                __syncthreads();
-                continue;
-            }
-            // swz is linear over GF(2): swz(x0 | slot bits) = swz(x0) ^ xor of swz(slot bit)
-            uint32_t sb[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r) sb[r] = swz(1u << st.rbits[r]);
-            const int g0 = st.first_gate, g1 = st.first_gate + st.ngates;
-            const bool nf = st.needs_full;
-            for (uint32_t grp = tid; grp < ngroups; grp += PASS_THREADS) {
-                const uint32_t sx0 = gx[s * ngroups + grp];
-                uint64_t full0 = 0;
-                if (nf) {
-                    const uint32_t x0 = swz(sx0);  // swz is an involution
-                    full0 = p.shard_base | base | (x0 & LOWM) | dep(x0 >> PASS_LOW);
-                }
-                double2 v[NS];
-#pragma unroll
-                for (int j = 0; j < NS; ++j) {
-                    uint32_t xs = sx0;
-#pragma unroll
-                    for (int r = 0; r < R; ++r)
-                        if (j & (1 << r)) xs ^= sb[r];
-                    v[j] = tile[xs];
-                }
-                uint32_t f = 0;
-                // software-pipelined dispatch: the next gate's descriptor is
-                // loaded while the current gate's FMA block runs
-                int op_n = g0 < g1 ? gates[g0].op : 0;
-                int cs_n = g0 < g1 ? gates[g0].cslot : 0;
-                uint64_t cm_n = g0 < g1 ? gates[g0].cmask_out : 0;
-                for (int gi = g0; gi < g1; ++gi) {
-                    const SmGate &g = gates[gi];
-                    const int op = op_n, cs = cs_n;
-                    const uint64_t cm = cm_n;
-                    if (gi + 1 < g1) {
-                        op_n = gates[gi + 1].op;
-                        cs_n = gates[gi + 1].cslot;
-                        cm_n = gates[gi + 1].cmask_out;
-                    }
-                    if ((full0 & cm) != cm) continue;
-                    switch (op) {
-#define PG_OPS(S)                                                                            \
-    case (S) * 6 + 0: pg_dense<NS, (S), true>(v, g, cs, f); break;                           \
-    case (S) * 6 + 1: pg_dense<NS, (S), false>(v, g, cs, f); break;                          \
-    case (S) * 6 + 2: pg_phase<NS, (S), true>(v, g.u[0], g.u[3], cs, f); break;              \
-    case (S) * 6 + 3: pg_phase<NS, (S), false>(v, g.u[0], g.u[3], cs, f); break;             \
-    case (S) * 6 + 4:                                                                        \
-        f ^= 1u << (S);                                                                      \
-        pg_phase<NS, (S), true>(v, g.u[1], g.u[2], 0, f);                                    \
-        break;                                                                               \
-    case (S) * 6 + 5: f ^= 1u << (S); break;
-                        PG_OPS(0)
-                        PG_OPS(1)
-                        PG_OPS(2)
-                        PG_OPS(3)
-#undef PG_OPS
-                        default:
-                            if (op >= 6 * R) {  // diagonal gate whose target is outside the registers
-                                const bool bit = (full0 & g.tmask_out) != 0;
-                                pg_diag_out<NS>(v, bit ? g.u[3] : g.u[0], cs, f, op == 6 * R);
-                            } else if constexpr (R > 4) {
-                                pg_slot<NS, (R > 4 ? 4 : 0)>(v, g, op - 24, cs, f);
-                            }
-                            break;
-                    }
-                }
-                // register j holds logical slot j ^ f: store to swz(x0 | slots(j ^ f))
-                uint32_t sxf = sx0;
-#pragma unroll
-                for (int r = 0; r < R; ++r)
-                    if (f & (1u << r)) sxf ^= sb[r];
-#pragma unroll
-                for (int j = 0; j < NS; ++j) {
-                    uint32_t xs = sxf;
-#pragma unroll
-                    for (int r = 0; r < R; ++r)
-                        if (j & (1 << r)) xs ^= sb[r];
-                    tile[xs] = v[j];
-                }
-            }
-            __syncthreads();
-        }
-        // ---- store the tile ----
-        double2 *ps = a + (base | d_tid);
-        if (!p.noio) {
-#pragma unroll 8
-            for (uint32_t j = 0; j < njt; ++j) ps[depJ[j]] = tile[s_tid ^ swz(j << 7)];
-        }
-        __syncthreads();
-    }
-}
-
-static size_t pass_smem(int K, int R, int nstages) { return pass_layout(K, R, nstages).total; }
-
-
-static bool g_pass_attr = false;
-// CTAs per SM of the R = 4 kernel: 3 (164 registers, K = 12 tiles), or 4 / 5
-// (register-capped, K = 11 tiles) -- selected with QSIM_PASS_OCC for tuning.
-static int pass_occ() {
-    static int occ = 0;
-    if (!occ) {
-        const char *e = getenv("QSIM_PASS_OCC");
-        occ = e ? atoi(e) : 3;
-        if (occ < 3 || occ > 5) occ = 3;
-    }
-    return occ;
-}
-int pass_e_max_k() { return pass_occ() == 3 ? 12 : 11; }
-int pass_e_max_grid(int R) { return num_sms() * (R >= 5 ? 2 : pass_occ()); }
-
-void launch_pass_e(const PassParams &p, int grid, cudaStream_t s) {
-    if (!g_pass_attr) {
-        cudaFuncSetAttribute(k_pass_e<4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)pass_smem(PASS_MAX_K, 4, PASS_MAX_STAGES));
-        cudaFuncSetAttribute(k_pass_e<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)pass_smem(PASS_MAX_K, 4, PASS_MAX_STAGES));
-        cudaFuncSetAttribute(k_pass_e<4, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)pass_smem(PASS_MAX_K, 4, PASS_MAX_STAGES));
-        cudaFuncSetAttribute(k_pass_e<5, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)pass_smem(PASS_MAX_K, 5, PASS_MAX_STAGES));
-        g_pass_attr = true;
-    }
-    if (p.R >= 5)
-        k_pass_e<5, 2><<<grid, PASS_THREADS, pass_smem(p.K, 5, p.nstages), s>>>(p);
-    else if (pass_occ() == 4)
-        k_pass_e<4, 4><<<grid, PASS_THREADS, pass_smem(p.K, 4, p.nstages), s>>>(p);
-    else if (pass_occ() == 5)
-        k_pass_e<4, 5><<<grid, PASS_THREADS, pass_smem(p.K, 4, p.nstages), s>>>(p);
-    else
-        k_pass_e<4, 3><<<grid, PASS_THREADS, pass_smem(p.K, 4, p.nstages), s>>>(p);
-}
-
-// ============================================================================
 // exchange-fused gate: (kept half slice, received slice) -> both slots
 // ============================================================================
 template <int MODE, int CLS>
@@ -755,6 +376,36 @@ void launch_dot_e(const void *x, const void *y, uint64_t n, double *partials, do
     k_dot_e<<<nb, RED_THREADS, 0, s>>>(reinterpret_cast<const double2 *>(x), reinterpret_cast<const double2 *>(y), n,
                                        partials);
     k_final_sum<<<1, 32, 0, s>>>(partials, nb, 2, out);
+}
+
+// max |a|^2 and min of the non-zero |a|^2 (the magnitude range of the state:
+// SURVEY.md §8(d) "value distributions", the A bounds' E counterpart).
+// Non-negative doubles order like their bit patterns, so the block results
+// merge with integer atomics (order-independent, exact).
+__global__ void __launch_bounds__(RED_THREADS) k_absrange_e(const double2 *__restrict__ a, uint64_t n,
+                                                            unsigned long long *out) {
+    double mx = 0.0, mn = INFINITY;
+    const uint64_t stride = (uint64_t)gridDim.x * RED_THREADS;
+    for (uint64_t i = (uint64_t)blockIdx.x * RED_THREADS + threadIdx.x; i < n; i += stride) {
+        double2 v = a[i];
+        double m = fma(v.x, v.x, v.y * v.y);
+        mx = fmax(mx, m);
+        if (m > 0.0) mn = fmin(mn, m);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(&out[1], (unsigned long long)__double_as_longlong(mx));
+        atomicMin(&out[0], (unsigned long long)__double_as_longlong(mn));
+    }
+}
+
+void launch_absrange_e(const void *a, uint64_t n, void *out_u64x2, cudaStream_t s) {
+    k_absrange_e<<<red_blocks(), RED_THREADS, 0, s>>>(reinterpret_cast<const double2 *>(a), n,
+                                                      reinterpret_cast<unsigned long long *>(out_u64x2));
 }
 
 __global__ void k_collapse_e(double2 *__restrict__ a, uint64_t n, int q, int keep, double f) {

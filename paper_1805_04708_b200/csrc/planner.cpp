@@ -186,7 +186,7 @@ void Planner::plan(const qsim_gate *gates, size_t ngates, std::vector<PlanOp> &o
             gl[m++] = pt;
             if (remap && n - nl >= 2) {
                 const size_t end = std::min(ngates, g + 1 + 2 * (size_t)n);
-                for (size_t h = g + 1; h < end && m < n - nl; ++h) {
+                for (size_t h = g + 1; h < end && m < std::min(n - nl, kRemapMaxBits); ++h) {
                     const qsim_gate &y = gates[h];
                     if (y.kind == QSIM_GATE_SWAP) break;  // relabels: stop looking (rare)
                     const int32_t yc = classify(y.u);
