@@ -1991,6 +1991,10 @@ static int dense_gate_a(qsim_state *s, const PlanOp &o, const double *u) {
         NC(ncclAllReduce(s->d_acc, s->d_acc, 2, ncclFloat64, ncclMin, s->comm, s->stream));
     launch_tables_next(s->d_acc, s->atab, s->stream);
     s->st.kernels++;
+    if (getenv("QSIM_ABND_DEBUG")) {
+        cudaStreamSynchronize(s->stream);
+        a_bounds_debug_print();
+    }
     for (auto &sh : s->shards) {
         AGateParams p{};
         fill_agate(p, s, sh, o, u);

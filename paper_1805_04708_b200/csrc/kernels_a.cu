@@ -24,8 +24,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
+#include <cstdio>
 
 #include "internal.h"
 #include "kernels.h"
@@ -78,10 +80,24 @@ static void fill_tables(ATabData &t, double r0, double r1) {
     t.scale = t.degenerate ? 0.0 : 253.0 / (r1 - r0);
 }
 
+static void fill_ftab(AFTab &f, const ATabData &t) {
+    for (int raw = 0; raw < 256; ++raw) {
+        const int i = (int)(int8_t)(uint8_t)raw + 128;  // table index of the code byte
+        const float r = (float)t.r[i], c = (float)t.cth[i], sn = (float)t.sth[i];
+        for (int l = 0; l < 32; ++l) f.rf[raw][l] = r;
+        for (int l = 0; l < 16; ++l) {
+            f.cs[raw][l][0] = c;
+            f.cs[raw][l][1] = sn;
+        }
+    }
+}
+
 int atables_alloc(ATables **out) {
     auto *t = new ATables();
     if (cudaMalloc(&t->d[0], sizeof(ATabData)) != cudaSuccess || cudaMalloc(&t->d[1], sizeof(ATabData)) != cudaSuccess ||
-        cudaMallocHost(&t->h, sizeof(ATabData)) != cudaSuccess) {
+        cudaMalloc(&t->f[0], sizeof(AFTab)) != cudaSuccess || cudaMalloc(&t->f[1], sizeof(AFTab)) != cudaSuccess ||
+        cudaMalloc(&t->gext, 2 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMallocHost(&t->h, sizeof(ATabData)) != cudaSuccess || cudaMallocHost(&t->hf, sizeof(AFTab)) != cudaSuccess) {
         cudaGetLastError();
         atables_free(t);
         set_error("A tables allocation failed");
@@ -93,16 +109,22 @@ int atables_alloc(ATables **out) {
 
 void atables_free(ATables *t) {
     if (!t) return;
-    if (t->d[0]) cudaFree(t->d[0]);
-    if (t->d[1]) cudaFree(t->d[1]);
+    for (int k = 0; k < 2; ++k) {
+        if (t->d[k]) cudaFree(t->d[k]);
+        if (t->f[k]) cudaFree(t->f[k]);
+    }
+    if (t->gext) cudaFree(t->gext);
     if (t->h) cudaFreeHost(t->h);
+    if (t->hf) cudaFreeHost(t->hf);
     delete t;
 }
 
 static int upload(ATables *t, int which, double r0, double r1, cudaStream_t s) {
     if (cudaStreamSynchronize(s) != cudaSuccess) return QSIM_ECUDA;  // h is reused
     fill_tables(*t->h, r0, r1);
-    if (cudaMemcpyAsync(t->d[which], t->h, sizeof(ATabData), cudaMemcpyHostToDevice, s) != cudaSuccess) {
+    fill_ftab(*t->hf, *t->h);
+    if (cudaMemcpyAsync(t->d[which], t->h, sizeof(ATabData), cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(t->f[which], t->hf, sizeof(AFTab), cudaMemcpyHostToDevice, s) != cudaSuccess) {
         set_error("A tables upload failed");
         return QSIM_ECUDA;
     }
@@ -123,6 +145,7 @@ int atables_commit_next(ATables *t, cudaStream_t s) {
 }
 static const ATabData *tcur(const ATables *t) { return t->d[t->cur]; }
 static const ATabData *tnext(const ATables *t) { return t->d[1 - t->cur]; }
+static const AFTab *fcur(const ATables *t) { return t->f[t->cur]; }
 
 // ---------------------------------------------------------------- device side
 struct ASm {
@@ -354,6 +377,10 @@ struct AUnit {
     __device__ static __forceinline__ int j0(int k) { return TL < 4 ? (((k >> TL) << (TL + 1)) | (k & ((1 << TL) - 1))) : k; }
     __device__ static __forceinline__ int j1(int k) { return TL < 4 ? (j0(k) | (1 << TL)) : k + 8; }
     __device__ static __forceinline__ uint64_t s0(uint64_t u, int t) { return TL < 4 ? (u << 4) : a_ins0(u << 3, t); }
+    // local index of code j of the unit at s0
+    __device__ static __forceinline__ uint64_t pos(uint64_t s0, int t, int j) {
+        return TL < 4 ? s0 + (uint64_t)j : (j < 8 ? s0 + (uint64_t)j : (s0 | (1ull << t)) + (uint64_t)(j - 8));
+    }
     __device__ static __forceinline__ void load(const uint16_t *__restrict__ a, uint64_t s0, int t, uint32_t (&c)[16]) {
         const uint4 v0 = __ldcs(reinterpret_cast<const uint4 *>(a + s0));
         const uint4 v1 = __ldcs(reinterpret_cast<const uint4 *>(a + (TL < 4 ? s0 + 8 : (s0 | (1ull << t)))));
@@ -365,15 +392,15 @@ struct AUnit {
         }
     }
     __device__ static __forceinline__ void store(uint16_t *__restrict__ a, uint64_t s0, int t, const uint32_t (&c)[16]) {
-        uint4 v0, v1;
-        v0.x = c[0] | (c[1] << 16);
-        v0.y = c[2] | (c[3] << 16);
-        v0.z = c[4] | (c[5] << 16);
-        v0.w = c[6] | (c[7] << 16);
-        v1.x = c[8] | (c[9] << 16);
-        v1.y = c[10] | (c[11] << 16);
-        v1.z = c[12] | (c[13] << 16);
-        v1.w = c[14] | (c[15] << 16);
+        uint4 v0, v1;  // low halves of c[] (upper bits ignored)
+        v0.x = __byte_perm(c[0], c[1], 0x5410);
+        v0.y = __byte_perm(c[2], c[3], 0x5410);
+        v0.z = __byte_perm(c[4], c[5], 0x5410);
+        v0.w = __byte_perm(c[6], c[7], 0x5410);
+        v1.x = __byte_perm(c[8], c[9], 0x5410);
+        v1.y = __byte_perm(c[10], c[11], 0x5410);
+        v1.z = __byte_perm(c[12], c[13], 0x5410);
+        v1.w = __byte_perm(c[14], c[15], 0x5410);
         __stcs(reinterpret_cast<uint4 *>(a + s0), v0);
         __stcs(reinterpret_cast<uint4 *>(a + (TL < 4 ? s0 + 8 : (s0 | (1ull << t)))), v1);
     }
@@ -461,45 +488,35 @@ struct ABnd {
 };
 
 
-// ---- fp32 fast path with a certified fallback ------------------------------
+// ---- certified fp32 fast path -------------------------------------------------
 // The dense A gate decides codes and bounds from fp32 copies of the decode
 // tables, of U and of the gate arithmetic, together with a rigorous bound on
 // how far each fp32 output can be from the fp64 reference (a_decode, a_gate2,
-// a_m2 -- the functions the fallback and the oracle's definition use).  A code
-// (or a bounds candidate) is committed from fp32 only when that bound proves
-// the fp64 reference decides the same way; otherwise the pair is recomputed in
-// fp64 exactly as before.  So the result is the fp64 reference's, bit for bit,
-// while most pairs cost fp32 (FMA pipe) instead of fp64 + conversions.
+// a_m2 / a_encode -- the functions of the fallback, which follow the oracle's
+// definition).  A code (or a bounds candidate) is committed from fp32 only when
+// that bound proves the fp64 reference decides the same way; otherwise the
+// pair is recomputed in fp64.  So the result is the fp64 reference's, bit for
+// bit, while almost every pair costs fp32 arithmetic only.
 //
 // Error bound (u = 2^-24): the fp32 decode has |zf - z| <= 3u r per component
 // (table value r, cos / sin and the product each rounded once); one output
 // component is 4 products summed by an fma chain, with |Re u_ij| + |Im u_ij|
 // <= sqrt2: sum_j sqrt2 (3u + u) r_j for the inputs and coefficients plus 4
-// roundings of partial sums <= 4u sqrt2 (r0 + r1) -- in all <= 11.4u (r0 + r1)
-// = 6.8e-7 (r0 + r1).  A_KF = 1e-6 > that, so per output component
-// |xf - x| <= E = A_KF (r0 + r1) with r the pair's decoded magnitudes.
+// roundings of partial sums <= 4u sqrt2 (ra + rb) -- in all <= 11.4u (ra + rb)
+// = 6.8e-7 (ra + rb).  A_KF = 1e-6 > that, so per output component
+// |xf - x| <= E = A_KF (ra + rb) with ra, rb the pair's decoded magnitudes.
+//
+// Lookups: the fp32 tables (AFTab, 64 KiB of dynamic shared memory) hold one
+// copy per lane, so a warp's 32 random codes never share a bank (the shared
+// 256-entry tables cost ~5 wavefronts per lookup on random codes).
 #define A_KF 1e-6f
-struct ASmF {
-    float rf[256];
-    float2 csf[256];
-    float scalef, r0s, r0f;
-};
-__device__ __forceinline__ void load_asmf(ASmF &f, const ASm &sm) {
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-        f.rf[i] = (float)sm.r[i];
-        f.csf[i] = make_float2((float)sm.cs[i].x, (float)sm.cs[i].y);
-    }
-    if (threadIdx.x == 0) {
-        f.scalef = (float)sm.scalen;
-        f.r0s = (float)(sm.r0n * sm.scalen);
-        f.r0f = (float)sm.r0n;
-    }
-    __syncthreads();
-}
-__device__ __forceinline__ float2 a_decode_f(const ASmF &f, uint32_t code, float &r) {
-    r = f.rf[(code & 0xffu) ^ 0x80u];
-    const float2 cs = f.csf[((code >> 8) & 0xffu) ^ 0x80u];
-    return make_float2(r * cs.x, r * cs.y);
+
+template <int UK>
+__device__ __forceinline__ void a_gate2u(const double (&u)[8], double2 &x, double2 &y) {
+    if (UK == 0)
+        a_gate2(u, x, y);
+    else
+        a_gate2k<UK>(u, x, y);
 }
 __device__ __forceinline__ void a_gate_f(const float (&u)[8], float2 &x, float2 &y) {
     const float2 x0 = x, y0 = y;
@@ -509,13 +526,6 @@ __device__ __forceinline__ void a_gate_f(const float (&u)[8], float2 &x, float2 
     y.y = fmaf(u[4], x0.y, fmaf(u[5], x0.x, fmaf(u[6], y0.y, u[7] * y0.x)));
 }
 template <int UK>
-__device__ __forceinline__ void a_gate2u(const double (&u)[8], double2 &x, double2 &y) {
-    if (UK == 0)
-        a_gate2(u, x, y);
-    else
-        a_gate2k<UK>(u, x, y);
-}
-template <int UK>
 __device__ __forceinline__ void a_gate_fu(const float (&u)[8], float2 &x, float2 &y) {
     if (UK == 0)
         a_gate_f(u, x, y);
@@ -523,104 +533,412 @@ __device__ __forceinline__ void a_gate_fu(const float (&u)[8], float2 &x, float2
         a_gate_fk<UK>(u, x, y);
 }
 
-// nearest integer of t (|t| < 2^22) without the conversion unit: k and t - k
-__device__ __forceinline__ int a_rnd(float t, float &fr) {
-    const float m = t + 12582912.0f;  // 1.5 * 2^23
-    fr = t - (m - 12582912.0f);
-    return __float_as_int(m) - 0x4B400000;
-}
-// The code of one fp32 output x (component error bound E); ok = false when
-// the fp32 value cannot decide it.  Branch-free.
-__device__ __forceinline__ uint32_t a_encode_f(const ASm &sm, const ASmF &f, float2 x, float E, bool &ok) {
-    const float m2f = fmaf(x.x, x.x, x.y * x.y);
-    const float rs = rsqrtf(m2f);
-    const float mf = m2f > 0.f ? m2f * rs : 0.f;
-    const float Em = fmaf(1.4143f, E, 4e-7f * mf);  // | |z| - mf |
-    const bool zero = mf + Em < 0.99999e-12f;    // certainly the special zero (reading R-A5)
-    // certainly intermediate, and the direction known to within 1 %
-    const bool inter = (mf - Em > 1.00001e-12f) & (mf + Em < 0.999999f) & (Em < 0.01f * mf);
-    float fr;
-    const float tf = fminf(fmaxf(fmaf(mf, f.scalef, -f.r0s), -2.f), 256.f);
-    const int c = a_rnd(tf, fr);
-    const float errm = fmaf(Em + 1.2e-7f * (mf + f.r0f), f.scalef, 2e-5f);
-    const bool okm = sm.degn || (fabsf(fr) < 0.5f - errm);
-    const int b0 = sm.degn ? 0 : max(0, min(253, c)) - 127;
-    float fa;
-    int k = a_rnd(atan2_steps(x.y, x.x), fa);
-    // direction error <= sqrt(2) E / |z| (|z| >= 0.99 mf) rad, polynomial 1e-5 rad + fp32 rounding
-    const float erra = fmaf(1.4143f * 1.0102f * 40.7437f, E * rs, 6e-4f);
-    const bool oka = fabsf(fa) < 0.5f - erra;
-    k = max(-128, min(128, k));
-    ok = zero | (inter & okm & oka);
-    return zero ? pack(-128, 0) : pack(b0, k == 128 ? -128 : k);
+// the fp32 tables of this thread's lane in shared memory
+struct AFLane {
+    const float *rf;   // rf[raw * 32]
+    const float2 *cs;  // cs[raw * 16]
+    __device__ __forceinline__ float2 decode(uint32_t code, float &r) const {
+        r = rf[(code & 0xffu) * 32u];
+        const float2 c = cs[((code >> 8) & 0xffu) * 16u];
+        return make_float2(r * c.x, r * c.y);
+    }
+};
+extern __shared__ __align__(16) unsigned char a_dsm[];
+// stage the fp32 tables (64 KiB, L2-resident) in shared memory
+__device__ __forceinline__ AFLane load_aflane(const AFTab *__restrict__ f) {
+    const uint4 *src = reinterpret_cast<const uint4 *>(f);
+    uint4 *dst = reinterpret_cast<uint4 *>(a_dsm);
+    for (int i = threadIdx.x; i < (int)(sizeof(AFTab) / 16); i += blockDim.x) dst[i] = __ldg(src + i);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const AFTab *t = reinterpret_cast<const AFTab *>(a_dsm);
+    AFLane L;
+    L.rf = &t->rf[0][lane];
+    L.cs = reinterpret_cast<const float2 *>(&t->cs[0][lane & 15][0]);
+    return L;
 }
 
-// fp64 reference for the pairs of a unit whose fp32 decision failed (rare;
-// out of line so the hot loop stays small), then the unit's store.  Only
-// scalars cross the call (the fp32 codes packed two per word, the gate from
-// the kernel parameters; the input codes are reloaded -- this thread has not
-// stored the unit yet), so the hot loop keeps its arrays in registers.
-template <int TL, int UK>
-__device__ __noinline__ void a_unit_exact_store(const ASm &sm, const double *u, uint16_t *a, uint64_t s0, int t,
-                                                uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t w4,
-                                                uint32_t w5, uint32_t w6, uint32_t w7, uint32_t fail, uint32_t selm) {
-    double uu[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) uu[i] = u[i];
-    const uint32_t w[8] = {w0, w1, w2, w3, w4, w5, w6, w7};
-    uint32_t c[16], nc[16];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        nc[2 * k] = w[k] & 0xffffu;
-        nc[2 * k + 1] = w[k] >> 16;
+// The fp64 reference tables read from global memory (the fallback path is
+// rare; the dense kernels keep shared memory for the fp32 tables).  Same
+// values and the same arithmetic as ASm / a_decode / a_encode.
+struct AGlob {
+    const ATabData *cur, *nxt;
+    float mmargin;
+    __device__ void init(const ATabData *c, const ATabData *n) {
+        cur = c;
+        nxt = n;
+        const double e = 6e-7 * (__ldg(&n->r1) + __ldg(&n->r0)) * __ldg(&n->scale) + 1e-4;
+        mmargin = (float)(e < 0.49 ? e : 0.5);
     }
-    AUnit<TL>::load(a, s0, t, c);
-    for (int k = 0; k < 8; ++k) {
-        if (!((fail >> k) & 1u)) continue;
-        const int j0 = AUnit<TL>::j0(k), j1 = AUnit<TL>::j1(k);
-        double2 x = a_decode(sm, c[j0]), y = a_decode(sm, c[j1]);
-        if ((selm >> k) & 1u) a_gate2u<UK>(uu, x, y);
-        nc[j0] = a_encode(sm, x);
-        nc[j1] = a_encode(sm, y);
+    __device__ __forceinline__ double2 decode(uint32_t code) const {
+        const int b0i = (int)(code & 0xffu) ^ 0x80, b1i = (int)((code >> 8) & 0xffu) ^ 0x80;
+        const double r = __ldg(&cur->r[b0i]);
+        return make_double2(r * __ldg(&cur->cth[b1i]), r * __ldg(&cur->sth[b1i]));
     }
-    AUnit<TL>::store(a, s0, t, nc);
+    __device__ uint32_t encode(double2 z) const {
+        const double m2 = a_m2(z);
+        if (m2 < A_ZERO2) return pack(-128, 0);
+        int b0;
+        if (m2 > A_ONE2) {
+            b0 = 127;
+        } else if (__ldg(&nxt->degenerate)) {
+            b0 = 0;
+        } else {
+            const float mf = sqrtf((float)m2);
+            const float tf = (mf - (float)__ldg(&nxt->r0)) * (float)__ldg(&nxt->scale);
+            int c = __float2int_rn(tf);
+            const float fr = tf - (float)c;
+            c = max(0, min(253, c));
+            if (fabsf(fr) > 0.5f - mmargin) {
+                if (c < 253 && m2 >= __ldg(&nxt->thr[c]))
+                    c += 1;
+                else if (c > 0 && m2 < __ldg(&nxt->thr[c - 1]))
+                    c -= 1;
+            }
+            b0 = c - 127;
+        }
+        // angle: the same decision as a_angle_code
+        const float af = atan2_steps((float)z.y, (float)z.x);
+        int k = __float2int_rn(af);
+        const float fr = af - (float)k;
+        k = max(-128, min(128, k));
+        if (fabsf(fr) > 0.5f - A_MARGIN) {
+            const double cu = z.y * __ldg(&nxt->cb[k + 129]) - z.x * __ldg(&nxt->sb[k + 129]);
+            if ((k >= 0) ? (cu >= 0.0) : (cu > 0.0)) {
+                k += 1;
+            } else {
+                const double cl = z.y * __ldg(&nxt->cb[k + 128]) - z.x * __ldg(&nxt->sb[k + 128]);
+                if ((k > 0) ? (cl < 0.0) : (cl <= 0.0)) k -= 1;
+            }
+            k = max(-128, min(128, k));
+        }
+        return pack(b0, (k == 128) ? -128 : k);
+    }
+};
+
+// Encode constants of the next bounds (per thread, from nxt): t = mf s1 + s0
+// is the fp32 magnitude coordinate (b0 + 127); its distance to the fp64
+// reference's is at most (5.2e-7 |z| + sqrt2 E) scale + C0 steps (candidate
+// mf: 4e-7 mf + sqrt2 E from |zf - z|; s1, s0 and the roundings: 6e-8 (mf +
+// r0) scale + 253 * 2^-24 + slack).  Degenerate bounds (r0 = r1): t = 127
+// exactly, the code every intermediate gets.
+struct AEncF {
+    float s1, s0, kS, kE, C0;
+    __device__ void init(const ATabData *n) {
+        const double sc = __ldg(&n->scale), r0 = __ldg(&n->r0);
+        if (__ldg(&n->degenerate)) {
+            s1 = 0.f;
+            s0 = 127.f;
+            kS = kE = C0 = 0.f;
+        } else {
+            s1 = (float)sc;
+            s0 = (float)(-r0 * sc);
+            kS = (float)(5.2e-7 * sc);
+            kE = (float)(1.4143 * sc);
+            C0 = (float)(1.2e-7 * r0 * sc + 5e-5);
+        }
+    }
+};
+
+// fp32 atan(w) in units of 2 b1 steps (256/pi per radian) for |w| <= 1: odd
+// polynomial of degree 13 (least-squares minimax fit, |error| <= 3e-5 steps
+// in fp32 evaluation); used on the half angle w = tan(theta / 2).
+__device__ __forceinline__ float atan_2steps(float w) {
+    const float s = w * w;
+    float p = fmaf(0.5550681352615356f, s, -2.7382962703704834f);
+    p = fmaf(p, s, 6.488292694091797f);
+    p = fmaf(p, s, -10.783480644226074f);
+    p = fmaf(p, s, 16.14085578918457f);
+    p = fmaf(p, s, -27.149433135986328f);
+    p = fmaf(p, s, 81.48701477050781f);
+    return p * w;
+}
+
+// raw MUFU approximations, flush-to-zero (no denormal rescaling): an output
+// with |z|^2 < 2^-126 gives rs = inf, mf = NaN and fails certification (the
+// fp64 fallback decides it), far below the intermediate range |z| >= 1e-12
+__device__ __forceinline__ float a_rsqrt(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float a_rcp(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+#define A_MAGIC 12582912.0f  // 1.5 * 2^23: x + A_MAGIC holds round(x) in its low mantissa bits
+
+// One fp32 output z of a pair with magnitudes ra + rb = S -> a 16-bit code
+// candidate; ok = the error bounds prove the fp64 reference gives the same
+// code.  Magnitude: t = mf scale - r0 scale is the coordinate b0 + 127; the
+// exact t lies in [0, 253] (r0, r1 are the exact extremes of these very
+// outputs), so round(t) needs no clamp; byte (c + 129) & 0xff = c - 127.  Its
+// certification takes the pair's limit limm = 0.5 - ((5.2e-7 S + sqrt2 E)
+// scale + C0) (|z| <= S).  Angle: theta = 2 atan(y / (|z| + |x|)), reflected
+// for x < 0, in steps; k = round half away (exact ties fall back); byte
+// k & 0xff (k = 128 wraps to -128, reading R-A6).  Its error: 73 E / |z|
+// steps from E (valid while E / |z| <= 0.141; above, 73 E rs > 0.5 fails) +
+// 2e-4 for the polynomial and the roundings.  A passing angle test also
+// proves |z| > 0.99 mf >= 1.445e-4 S, so S > 7e-9 (checked per pair) rules
+// out the special zero.
+__device__ __forceinline__ uint32_t a_encode_f(const AEncF &ce, float2 z, float limm, float KE, float eS, bool &ok) {
+    const float m2 = fmaf(z.x, z.x, z.y * z.y);
+    const float rs = a_rsqrt(m2);
+    const float mf = m2 > 0.f ? m2 * rs : 0.f;
+    const float t = fmaf(mf, ce.s1, ce.s0);
+    const float tm = t + (A_MAGIC + 129.f);
+    const float frm = t - (tm - (A_MAGIC + 129.f));
+    const float w = z.y * a_rcp(mf + fabsf(z.x));
+    const float p = atan_2steps(w);
+    const float q = (z.x < 0.f) ? copysignf(128.f, z.y) - p : p;
+    const float ta = q + A_MAGIC;
+    const float fra = q - (ta - A_MAGIC);
+    // |z| certainly below 1e-12: the special zero; certainly above: intermediate (reading R-A5)
+    const bool zero = fmaf(mf, 1.0000005f, eS) < 0.99999e-12f;
+    const bool inter = fmaf(mf, 0.9999995f, -eS) > 1.00001e-12f;
+    ok = zero | (inter & (fabsf(frm) < limm) & (fmaf(KE, rs, fabsf(fra)) < 0.4998f));
+    return zero ? 0x0080u : __byte_perm(__float_as_uint(tm), __float_as_uint(ta), 0x0040);
+}
+
+// Pairs whose fp32 decision failed go to a per-warp queue; the fp64 reference
+// (AGlob: the same arithmetic as a_decode / a_gate2 / a_encode) recomputes
+// them 32 at a time, one pair per lane, after their units' provisional
+// stores -- instead of stalling the whole warp for every unit with a failing
+// pair.  Entry: the pair's first code index i0 (bit 63: the gate applies),
+// the input codes (c0 | c1 << 16); the second code is at i0 + 2^t.
+struct AFail {
+    uint64_t i0;
+    uint32_t codes, pad;
+};
+constexpr int A_QN = 32;
+template <int UK>
+__device__ __noinline__ void a_flush(const AGateParams *pp, const ATabData *cur, const ATabData *nxt,
+                                     const AFail *q, int n) {
+    __syncwarp();  // the queued units' provisional stores and the entries are visible
+    const int lane = threadIdx.x & 31;
+    if (lane < n) {
+        AGlob g;
+        g.init(cur, nxt);
+        const AFail e = q[lane];
+        const uint64_t i0 = e.i0 & ~(1ull << 63);
+        double2 x = g.decode(e.codes & 0xffffu), y = g.decode(e.codes >> 16);
+        if (e.i0 >> 63) {
+            double u[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) u[i] = pp->u[i];
+            a_gate2u<UK>(u, x, y);
+        }
+        uint16_t *a = reinterpret_cast<uint16_t *>(pp->a);
+        a[i0] = (uint16_t)g.encode(x);
+        a[i0 + (1ull << pp->t)] = (uint16_t)g.encode(y);
+    }
+    __syncwarp();  // the queue is free again
+}
+
+constexpr int A_DENSE_MINB = 3;  // CTAs per SM of the dense kernels (64 KiB of tables each)
+
+// Phase 1 (reading R-A4): exact min / max of the intermediate |z'|^2 of the
+// gate's output, through two screens:
+//  1. fp32 decode + gate + |z'| with the certified bound ||z'f| - |z'|| <=
+//     sqrt2 E (E = A_KF (ra + rb) per component) and the fp32 rounding of
+//     the magnitude (4e-7 relative): a pair passes when both outputs provably
+//     lie inside the warp's exact running [min, max] of the intermediate |z'|
+//     (and so are intermediate themselves);
+//  2. otherwise (a new extreme, or a tie with one: the structured workload
+//     states have massive exact ties at the extremes), the pair's class --
+//     raw b0 of both codes, the b1 difference mod 256, whether the gate
+//     applies -- is looked up in a per-warp cache; a class not found there
+//     goes to a per-warp queue, evaluated in the same iteration, one class
+//     per lane, updating the warp's exact min / max, which it shares with the
+//     grid through two atomics (min / max of the fp64 bit patterns).
+// The value of a class is |z'_j|^2 evaluated in fp64 in the frame of the
+// first input: z'_j = u_j0 ra + u_j1 rb e^{i pi (b1b - b1a)/128} (reading
+// R-A24: the gate output up to the common phase e^{i pi b1a/128}, which
+// |.|^2 does not see; it differs from the per-amplitude fp64 evaluation by
+// rounding only, ~1e-16 (ra + rb)).  So the bounds are a deterministic
+// function of the set of classes present -- independent of the sharding and
+// of the evaluation order -- and the structured workload states, with
+// massive exact ties at the extremes, cost one evaluation per class.
+// A pair that passes a screen provably lies inside [min, max] and is
+// intermediate, so it cannot change the result.
+__device__ unsigned long long g_abnd_dbg[5];  // debug: screen-1 candidates, screen-2 candidates, queued, flushes
+struct ACand {
+    uint32_t key;  // b0a | b0b << 8 | ((b1b - b1a) & 0xff) << 16 | sel << 24 (raw code bytes)
+};
+constexpr int A_BOUNDS_MINB = 3;
+constexpr int A_DEDUP = 256;  // per-warp direct-mapped cache of queued class keys
+template <int UK>
+__device__ __forceinline__ void a_bounds_flush(const AGateParams &p, const ATabData *__restrict__ cur,
+                                               const ACand *q, int n, double &mn, double &mx, float &tlo,
+                                               float &thi, unsigned long long *gext) {
+    __syncwarp();
+    const int lane = threadIdx.x & 31;
+    if (lane < n) {
+        const uint32_t key = q[lane].key;
+        const int b0a = (int)(key & 0xffu) ^ 0x80, b0b = (int)((key >> 8) & 0xffu) ^ 0x80;
+        const int dl = (int)((key >> 16) & 0xffu) ^ 0x80;  // (b1b - b1a) as a table index
+        const double ra = __ldg(&cur->r[b0a]), rb = __ldg(&cur->r[b0b]);
+        double ma, mb;
+        if (key >> 24) {
+            const double yr = rb * __ldg(&cur->cth[dl]), yi = rb * __ldg(&cur->sth[dl]);
+            // z'_0 = u00 ra + u01 y, z'_1 = u10 ra + u11 y (y = rb e^{i pi d / 128})
+            const double x0r = fma(p.u[0], ra, fma(p.u[2], yr, -p.u[3] * yi));
+            const double x0i = fma(p.u[1], ra, fma(p.u[2], yi, p.u[3] * yr));
+            const double x1r = fma(p.u[4], ra, fma(p.u[6], yr, -p.u[7] * yi));
+            const double x1i = fma(p.u[5], ra, fma(p.u[6], yi, p.u[7] * yr));
+            ma = fma(x0r, x0r, x0i * x0i);
+            mb = fma(x1r, x1r, x1i * x1i);
+        } else {  // unselected: the inputs themselves
+            ma = ra * ra;
+            mb = rb * rb;
+        }
+        if (is_inter(ma)) {
+            mn = fmin(mn, ma);
+            mx = fmax(mx, ma);
+        }
+        if (is_inter(mb)) {
+            mn = fmin(mn, mb);
+            mx = fmax(mx, mb);
+        }
+    }
+    mn = warp_min(mn);
+    mx = warp_max(mx);
+    // share with the grid: exact extremes found by other warps tighten this warp's
+    // thresholds (non-negative doubles order like their bit patterns)
+    if (lane == 0) {
+        const unsigned long long omn = atomicMin(&gext[0], (unsigned long long)__double_as_longlong(mn));
+        const unsigned long long omx =
+            atomicMax(&gext[1], (unsigned long long)__double_as_longlong(mx > 0.0 ? mx : 0.0));
+        mn = fmin(mn, __longlong_as_double((long long)omn));
+        if (omx) mx = fmax(mx, __longlong_as_double((long long)omx));
+    }
+    mn = __shfl_sync(0xffffffffu, mn, 0);
+    mx = __shfl_sync(0xffffffffu, mx, 0);
+    // fp32 thresholds on |z|: tlo >= sqrt(mn), thi <= sqrt(mx) (directed roundings)
+    tlo = mn == INFINITY ? INFINITY : __double2float_ru(__dsqrt_ru(mn));
+    thi = mx == -INFINITY ? -INFINITY : __double2float_rd(__dsqrt_rd(mx));
+    __syncwarp();
 }
 
 template <int TL, bool CTRL, int UK>
-__global__ void __launch_bounds__(A_THREADS) k_bounds_a(const __grid_constant__ AGateParams p,
-                                                        const ATabData *__restrict__ cur,
-                                                        const ATabData *__restrict__ nxt, double *partials) {
+__global__ void __launch_bounds__(A_THREADS, A_BOUNDS_MINB) k_bounds_a(const __grid_constant__ AGateParams p,
+                                                                       const ATabData *__restrict__ cur,
+                                                                       const AFTab *__restrict__ fcur,
+                                                                       double *partials, unsigned long long *gext) {
     using U = AUnit<TL>;
-    __shared__ ASm sm;
-    load_asm(sm, cur, nxt);
+    const AFLane L = load_aflane(fcur);
+    const int lane = threadIdx.x & 31;
+    __shared__ ACand qall[A_THREADS / 32][A_QN];
+    __shared__ uint32_t dall[A_THREADS / 32][A_DEDUP];
+    ACand *q = qall[threadIdx.x >> 5];
+    uint32_t *dd = dall[threadIdx.x >> 5];
+    for (int i = lane; i < A_DEDUP; i += 32) dd[i] = ~0u;  // no key (keys < 2^25)
+    __syncwarp();
+    int qn = 0;  // warp-uniform
     const uint16_t *a = reinterpret_cast<const uint16_t *>(p.a);
     const uint64_t units = (p.nl >= 4) ? (1ull << (p.nl - 4)) : 1ull;
     const uint64_t lowm = (1ull << U::LOWB) - 1ull;
     const uint64_t chi = p.cmask & ~lowm;
     const uint32_t cl = (uint32_t)(p.cmask & lowm);
-    double u[8];
+    float uf[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) u[i] = p.u[i];
-    ABnd b;
-    b.init();
-    for (uint64_t v = (uint64_t)blockIdx.x * A_THREADS + threadIdx.x; v < units; v += (uint64_t)gridDim.x * A_THREADS) {
-        uint32_t c[16];
-        const uint64_t s0 = U::s0(v, p.t);
-        U::load(a, s0, p.t, c);
-        const bool hi_ok = !CTRL || (((p.shard_base | s0) & chi) == chi);
+    for (int i = 0; i < 8; ++i) uf[i] = p.uf[i];
+    double mn = INFINITY, mx = -INFINITY;  // exact, warp-wide
+    float tlo = INFINITY, thi = -INFINITY;
+    const uint32_t lt = (1u << lane) - 1u;
+    for (uint64_t vb = (uint64_t)blockIdx.x * A_THREADS + (threadIdx.x & ~31u); vb < units;
+         vb += (uint64_t)gridDim.x * A_THREADS) {
+        const uint64_t v = vb + (uint64_t)lane;
+        uint32_t c[16], keys[8];
+        uint32_t candm = 0;
+        if (v < units) {
+            const uint64_t s0 = U::s0(v, p.t);
+            U::load(a, s0, p.t, c);
+            const bool hi_ok = !CTRL || (((p.shard_base | s0) & chi) == chi);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int j0 = U::j0(k), j1 = U::j1(k);
-            double2 x = a_decode(sm, c[j0]), y = a_decode(sm, c[j1]);
-            const int off = TL < 4 ? j0 : k;
-            if (!CTRL || (hi_ok && ((uint32_t)off & cl) == cl)) a_gate2u<UK>(u, x, y);
-            b.add(a_m2(x));
-            b.add(a_m2(y));
+            for (int k = 0; k < 8; ++k) {
+                const int j0 = U::j0(k), j1 = U::j1(k);
+                const int off = TL < 4 ? j0 : k;
+                const bool sel = !CTRL || (hi_ok && ((uint32_t)off & cl) == cl);
+                float ra, rb;
+                float2 x = L.decode(c[j0], ra), y = L.decode(c[j1], rb);
+                if (sel) a_gate_fu<UK>(uf, x, y);
+                const float S = ra + rb;
+                // |z'| within sqrt2 E of |z'f| (E = A_KF S per component), mf within 4e-7 mf of |z'f|
+                const float m2x = fmaf(x.x, x.x, x.y * x.y), m2y = fmaf(y.x, y.x, y.y * y.y);
+                float mfx = m2x * a_rsqrt(m2x), mfy = m2y * a_rsqrt(m2y);
+                mfx = m2x > 0.f ? mfx : 0.f;
+                mfy = m2y > 0.f ? mfy : 0.f;
+                const float eS = 1.4145e-6f * S;
+                // a certainly-zero output (|z'| < 1e-12, reading R-A5) is no intermediate: not a
+                // min candidate (the A states of the workloads hold many amplitudes at the
+                // 1e-12 floor, whose products straddle it)
+                float lx = fmaf(mfx, 1.0000005f, eS) < 0.99999e-12f ? INFINITY : mfx;
+                float ly = fmaf(mfy, 1.0000005f, eS) < 0.99999e-12f ? INFINITY : mfy;
+                if (CTRL && !sel) {  // an unselected zero code stays the exact zero special
+                    lx = ra == 0.f ? INFINITY : lx;
+                    ly = rb == 0.f ? INFINITY : ly;
+                }
+                const bool cand = (S > 0.f) & ((fminf(lx, ly) * 0.9999995f < tlo + eS) |
+                                               (fmaxf(mfx, mfy) * 1.0000005f > thi - eS));
+#ifdef QSIM_ABND_DEBUG
+                if (cand) atomicAdd(&g_abnd_dbg[1], 1ull);
+                if (cand && (fminf(lx, ly) * 0.9999995f < tlo + eS)) atomicAdd(&g_abnd_dbg[0], 1ull);
+                if (cand && (fminf(lx, ly) < 1e-3f * S)) atomicAdd(&g_abnd_dbg[3], 1ull);
+                if (cand && blockIdx.x == 7 && (threadIdx.x & 31) == 3 && vb > 60ull * gridDim.x * A_THREADS) {
+                    unsigned long long nprint = atomicAdd(&g_abnd_dbg[4], 1ull);
+                    if (nprint < 12)
+                        printf("cand ra %.6e rb %.6e mfx %.9e mfy %.9e tlo %.9e thi %.9e eS %.3e ca %04x cb %04x\n", ra,
+                               rb, mfx, mfy, tlo, thi, eS, c[j0], c[j1]);
+                }
+#endif
+                if (cand) {  // one evaluation per class: a class in the warp's cache is done
+                    const uint32_t ca = c[j0], cb = c[j1];
+                    const uint32_t key = (ca & 0xffu) | ((cb & 0xffu) << 8) |
+                                         ((((cb >> 8) - (ca >> 8)) & 0xffu) << 16) | ((uint32_t)sel << 24);
+                    const uint32_t slot = (key * 2654435761u) >> 24;
+                    if (dd[slot] != key) {
+                        dd[slot] = key;
+                        candm |= 1u << k;
+                        keys[k] = key;
+                    }
+                }
+            }
+        }
+        if (__any_sync(0xffffffffu, candm != 0)) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const bool f = (candm >> k) & 1u;
+                const uint32_t key = keys[k];
+                const uint32_t bal = __ballot_sync(0xffffffffu, f);
+                if (bal) {
+                    const int tot = __popc(bal);
+                    if (qn + tot > A_QN) {
+                        a_bounds_flush<UK>(p, cur, q, qn, mn, mx, tlo, thi, gext);
+                        qn = 0;
+                    }
+                    if (f) {
+#ifdef QSIM_ABND_DEBUG
+                        atomicAdd(&g_abnd_dbg[2], 1ull);
+#endif
+                        q[qn + __popc(bal & lt)].key = key;
+                    }
+                    qn += tot;
+                }
+            }
+            // evaluate now: the thresholds must follow (a class found in the cache is not
+            // queued again, so waiting for a full queue would leave them stale)
+            if (qn) {
+                a_bounds_flush<UK>(p, cur, q, qn, mn, mx, tlo, thi, gext);
+                qn = 0;
+            }
         }
     }
+    if (qn) a_bounds_flush<UK>(p, cur, q, qn, mn, mx, tlo, thi, gext);
     __shared__ double red[2][A_THREADS / 32];
-    const double mn = warp_min(b.mn), mx = warp_max(b.mx);
-    if ((threadIdx.x & 31) == 0) {
+    if (lane == 0) {
         red[0][threadIdx.x >> 5] = mn;
         red[1][threadIdx.x >> 5] = mx;
     }
@@ -667,14 +985,19 @@ __global__ void k_minmax_final(const double *partials, int nb, double *acc, int 
 // the sentinel 0.5 when no magnitude is intermediate (reading R-A8).  The same
 // expressions as fill_tables on the host, with explicit IEEE roundings (no
 // FMA contraction), so device- and host-built tables are bit-identical.
-__global__ void k_tables_next(const double *acc, ATabData *t) {
+__global__ void k_tables_next(const double *acc, ATabData *t, AFTab *f) {
     const double mn = acc[0], mx = -acc[1];
     const bool none = !(mn <= mx);
     const double r0 = none ? 0.5 : __dsqrt_rn(mn), r1 = none ? 0.5 : __dsqrt_rn(mx);
     const double d = __dsub_rn(r1, r0);
     for (int i = threadIdx.x; i < 256; i += blockDim.x) {
         const int b0 = i - 128;
-        t->r[i] = b0 == -128 ? 0.0 : b0 == 127 ? 1.0 : __dadd_rn(__ddiv_rn(__dmul_rn((double)(b0 + 127), d), 253.0), r0);
+        const double ri =
+            b0 == -128 ? 0.0 : b0 == 127 ? 1.0 : __dadd_rn(__ddiv_rn(__dmul_rn((double)(b0 + 127), d), 253.0), r0);
+        t->r[i] = ri;
+        const float rf = __double2float_rn(ri);  // fp32 copy (fill_ftab), one per lane
+        float *row = f->rf[(i - 128) & 0xff];
+        for (int l = 0; l < 32; ++l) row[l] = rf;
         if (i < 253) {
             const double m = __dadd_rn(r0, __ddiv_rn(__dmul_rn((double)i + 0.5, d), 253.0));
             t->thr[i] = __dmul_rn(m, m);
@@ -690,9 +1013,24 @@ __global__ void k_tables_next(const double *acc, ATabData *t) {
     }
 }
 
+// 64 KiB of dynamic shared memory (the fp32 tables): opted in once per device
+// and kernel instantiation
+static bool a_dense_attr(const void *kern, std::atomic<uint64_t> &devs) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (devs.load() & bit) return true;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(AFTab)) != cudaSuccess)
+        return false;
+    devs.fetch_or(bit);
+    return true;
+}
+
 template <int TL, bool CTRL, int UK>
 static void launch_bounds_tl(const AGateParams &p, const ATables *t, double *partials, int grid, cudaStream_t s) {
-    k_bounds_a<TL, CTRL, UK><<<grid, A_THREADS, 0, s>>>(p, tcur(t), tnext(t), partials);
+    static std::atomic<uint64_t> attr{0};
+    a_dense_attr((const void *)k_bounds_a<TL, CTRL, UK>, attr);
+    k_bounds_a<TL, CTRL, UK><<<grid, A_THREADS, sizeof(AFTab), s>>>(p, tcur(t), fcur(t), partials, t->gext);
 }
 template <int TL, int UK>
 static void launch_bounds_c(const AGateParams &p, const ATables *t, double *partials, int grid, cudaStream_t s) {
@@ -717,12 +1055,44 @@ static int a_ukind(const double *u) {
     if (u[1] == 0.0 && u[7] == 0.0 && u[2] == 0.0 && u[4] == 0.0) return 2;
     return 0;
 }
+// fp32 copy of U and the magnitude coefficients of the bounds screen
+static AGateParams a_dense_params(const AGateParams &p0) {
+    AGateParams p = p0;
+    for (int i = 0; i < 8; ++i) p.uf[i] = (float)p.u[i];
+    const double m00 = std::hypot(p.u[0], p.u[1]), m01 = std::hypot(p.u[2], p.u[3]);
+    const double m10 = std::hypot(p.u[4], p.u[5]), m11 = std::hypot(p.u[6], p.u[7]);
+    const double A = std::max(m00, m11) * (1.0 + 1e-6), B = std::max(m01, m10) * (1.0 + 1e-6);
+    p.mA = (float)std::max(A, B);
+    p.mB = (float)std::min(A, B);
+    p.ma = (float)m00;
+    p.mb = (float)m01;
+    return p;
+}
+// persistent grid: MINB CTAs per SM (capped by the work and by the partials' capacity)
+static int a_dense_grid(uint64_t units, int minb = A_DENSE_MINB) {
+    const uint64_t cap = (uint64_t)a_num_sms() * minb;
+    const uint64_t need = (units + A_THREADS - 1) / A_THREADS;
+    return (int)(need < cap ? (need ? need : 1) : cap);
+}
 
-void launch_bounds_a(const AGateParams &p, const ATables *t, double *partials, double *acc, bool first,
+void a_bounds_debug_print() {
+#ifdef QSIM_ABND_DEBUG
+    unsigned long long h[4];
+    cudaMemcpyFromSymbol(h, g_abnd_dbg, sizeof(h));
+    fprintf(stderr, "abnd: min-cands %llu cands %llu queued %llu tiny(<1e-3 S) %llu\n", h[0], h[1], h[2], h[3]);
+    unsigned long long z[5] = {0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_abnd_dbg, z, sizeof(z));
+#endif
+}
+void launch_bounds_a(const AGateParams &p0, const ATables *t, double *partials, double *acc, bool first,
                      cudaStream_t s) {
+    const AGateParams p = a_dense_params(p0);
+    if (first) {  // the gate's running extremes shared by the grid: (+inf, 0) as bit patterns
+        static const unsigned long long init[2] = {0x7ff0000000000000ull, 0ull};
+        cudaMemcpyAsync(t->gext, init, sizeof(init), cudaMemcpyHostToDevice, s);
+    }
     const uint64_t units = (p.nl >= 4) ? (1ull << (p.nl - 4)) : 1ull;
-    int grid = a_grid(units);
-    if (grid > 2 * a_num_sms() * 4) grid = 2 * a_num_sms() * 4;  // partials capacity
+    const int grid = a_dense_grid(units, A_BOUNDS_MINB);
     switch (a_ukind(p.u)) {
         case 1: launch_bounds_k<1>(p, t, partials, grid, s); break;
         case 2: launch_bounds_k<2>(p, t, partials, grid, s); break;
@@ -732,63 +1102,115 @@ void launch_bounds_a(const AGateParams &p, const ATables *t, double *partials, d
 }
 
 void launch_tables_next(const double *acc, ATables *t, cudaStream_t s) {
-    k_tables_next<<<1, 256, 0, s>>>(acc, t->d[1 - t->cur]);
+    k_tables_next<<<1, 256, 0, s>>>(acc, t->d[1 - t->cur], t->f[1 - t->cur]);
 }
 
+// Phase 2: decode (current tables), apply, encode (next tables) -- fp32 with
+// the certified fallback per failing pair (the warp queue, a_flush).  The
+// grid-stride loop is warp-uniform (lanes past the end idle) so that the
+// queue's votes see the whole warp.
 template <int TL, bool CTRL, int UK>
-__global__ void __launch_bounds__(A_THREADS) k_apply_a(const __grid_constant__ AGateParams p,
-                                                       const ATabData *__restrict__ cur,
-                                                       const ATabData *__restrict__ nxt) {
+__global__ void __launch_bounds__(A_THREADS, A_DENSE_MINB) k_apply_a(const __grid_constant__ AGateParams p,
+                                                                     const ATabData *__restrict__ cur,
+                                                                     const ATabData *__restrict__ nxt,
+                                                                     const AFTab *__restrict__ fcur) {
     using U = AUnit<TL>;
-    __shared__ ASm sm;
-    load_asm(sm, cur, nxt);
+    const AFLane L = load_aflane(fcur);
+    __shared__ AFail qall[A_THREADS / 32][A_QN];
+    const int lane = threadIdx.x & 31;
+    AFail *q = qall[threadIdx.x >> 5];
+    int qn = 0;  // warp-uniform
+    AEncF ce;
+    ce.init(nxt);
     uint16_t *a = reinterpret_cast<uint16_t *>(p.a);
     const uint64_t units = (p.nl >= 4) ? (1ull << (p.nl - 4)) : 1ull;
     const uint64_t lowm = (1ull << U::LOWB) - 1ull;
     const uint64_t chi = p.cmask & ~lowm;
     const uint32_t cl = (uint32_t)(p.cmask & lowm);
-    __shared__ ASmF f;
-    load_asmf(f, sm);
     float uf[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) uf[i] = (float)p.u[i];
-    for (uint64_t v = (uint64_t)blockIdx.x * A_THREADS + threadIdx.x; v < units; v += (uint64_t)gridDim.x * A_THREADS) {
+    for (int i = 0; i < 8; ++i) uf[i] = p.uf[i];
+    const uint32_t lt = (1u << lane) - 1u;
+    for (uint64_t vb = (uint64_t)blockIdx.x * A_THREADS + (threadIdx.x & ~31u); vb < units;
+         vb += (uint64_t)gridDim.x * A_THREADS) {
+        const uint64_t v = vb + (uint64_t)lane;
+        uint32_t fail = 0, selm = 0;
         uint32_t c[16];
-        const uint64_t s0 = U::s0(v, p.t);
-        U::load(a, s0, p.t, c);
-        const bool hi_ok = !CTRL || (((p.shard_base | s0) & chi) == chi);
-        uint32_t nc[16], fail = 0, selm = 0;
+        uint64_t s0 = 0;
+        if (v < units) {
+            s0 = U::s0(v, p.t);
+            U::load(a, s0, p.t, c);
+            const bool hi_ok = !CTRL || (((p.shard_base | s0) & chi) == chi);
+            uint32_t nc[16];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int j0 = U::j0(k), j1 = U::j1(k);
-            const int off = TL < 4 ? j0 : k;
-            const bool sel = !CTRL || (hi_ok && ((uint32_t)off & cl) == cl);
-            selm |= (uint32_t)sel << k;
-            float ra, rb;
-            float2 xf = a_decode_f(f, c[j0], ra), yf = a_decode_f(f, c[j1], rb);
-            if (sel) a_gate_fu<UK>(uf, xf, yf);
-            const float E = A_KF * (ra + rb);
-            bool okx, oky;
-            nc[j0] = a_encode_f(sm, f, xf, E, okx);
-            nc[j1] = a_encode_f(sm, f, yf, E, oky);
-            fail |= (uint32_t)!(okx && oky) << k;
+            for (int k = 0; k < 8; ++k) {
+                const int j0 = U::j0(k), j1 = U::j1(k);
+                const int off = TL < 4 ? j0 : k;
+                const bool sel = !CTRL || (hi_ok && ((uint32_t)off & cl) == cl);
+                selm |= (uint32_t)sel << k;
+                float ra, rb;
+                float2 x = L.decode(c[j0], ra), y = L.decode(c[j1], rb);
+                if (sel) a_gate_fu<UK>(uf, x, y);
+                const float S = ra + rb;
+                const float E = A_KF * S;
+                const float limm = 0.5f - fmaf(S, ce.kS, fmaf(E, ce.kE, ce.C0)), KE = 73.f * E;
+                const float eS = 1.4145f * E;
+                bool okx, oky;
+                uint32_t cx = a_encode_f(ce, x, limm, KE, eS, okx);
+                uint32_t cy = a_encode_f(ce, y, limm, KE, eS, oky);
+                if (CTRL) {  // an unselected zero code stays the exact zero special
+                    const bool zx = (ra == 0.f) & !sel, zy = (rb == 0.f) & !sel;
+                    cx = zx ? 0x0080u : cx;
+                    cy = zy ? 0x0080u : cy;
+                    okx |= zx;
+                    oky |= zy;
+                }
+                // |z'| <= ra + rb < 0.999: never the special one; else fp64 decides
+                const bool ok = okx & oky & (S < 0.999f);
+                nc[j0] = cx;
+                nc[j1] = cy;
+                fail |= (uint32_t)!ok << k;
+            }
+            U::store(a, s0, p.t, nc);  // provisional for the failing pairs
         }
-        if (fail)
-            a_unit_exact_store<TL, UK>(sm, p.u, a, s0, p.t, nc[0] | (nc[1] << 16), nc[2] | (nc[3] << 16),
-                                       nc[4] | (nc[5] << 16), nc[6] | (nc[7] << 16), nc[8] | (nc[9] << 16),
-                                       nc[10] | (nc[11] << 16), nc[12] | (nc[13] << 16), nc[14] | (nc[15] << 16),
-                                       fail, selm);
-        else
-            U::store(a, s0, p.t, nc);
+        if (__any_sync(0xffffffffu, fail != 0)) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const bool f = (fail >> k) & 1u;
+                const uint32_t bal = __ballot_sync(0xffffffffu, f);
+                if (bal) {
+                    const int tot = __popc(bal);
+                    if (qn + tot > A_QN) {
+                        a_flush<UK>(&p, cur, nxt, q, qn);
+                        qn = 0;
+                    }
+                    if (f) {
+                        AFail e;
+                        e.i0 = U::pos(s0, p.t, U::j0(k)) | ((uint64_t)((selm >> k) & 1u) << 63);
+                        e.codes = __byte_perm(c[U::j0(k)], c[U::j1(k)], 0x5410);
+                        e.pad = 0;
+                        q[qn + __popc(bal & lt)] = e;
+                    }
+                    qn += tot;
+                }
+            }
+        }
     }
+    if (qn) a_flush<UK>(&p, cur, nxt, q, qn);
 }
 
+template <int TL, bool CTRL, int UK>
+static void launch_apply_tl(const AGateParams &p, const ATables *t, int grid, cudaStream_t s) {
+    static std::atomic<uint64_t> attr{0};
+    a_dense_attr((const void *)k_apply_a<TL, CTRL, UK>, attr);
+    k_apply_a<TL, CTRL, UK><<<grid, A_THREADS, sizeof(AFTab), s>>>(p, tcur(t), tnext(t), fcur(t));
+}
 template <int TL, int UK>
 static void launch_apply_c(const AGateParams &p, const ATables *t, int grid, cudaStream_t s) {
     if (p.cmask)
-        k_apply_a<TL, true, UK><<<grid, A_THREADS, 0, s>>>(p, tcur(t), tnext(t));
+        launch_apply_tl<TL, true, UK>(p, t, grid, s);
     else
-        k_apply_a<TL, false, UK><<<grid, A_THREADS, 0, s>>>(p, tcur(t), tnext(t));
+        launch_apply_tl<TL, false, UK>(p, t, grid, s);
 }
 template <int UK>
 static void launch_apply_k(const AGateParams &p, const ATables *t, int grid, cudaStream_t s) {
@@ -801,9 +1223,10 @@ static void launch_apply_k(const AGateParams &p, const ATables *t, int grid, cud
     }
 }
 
-void launch_apply_a(const AGateParams &p, const ATables *t, cudaStream_t s) {
+void launch_apply_a(const AGateParams &p0, const ATables *t, cudaStream_t s) {
+    const AGateParams p = a_dense_params(p0);
     const uint64_t units = (p.nl >= 4) ? (1ull << (p.nl - 4)) : 1ull;
-    const int grid = a_grid(units);
+    const int grid = a_dense_grid(units);
     switch (a_ukind(p.u)) {
         case 1: launch_apply_k<1>(p, t, grid, s); break;
         case 2: launch_apply_k<2>(p, t, grid, s); break;

@@ -26,9 +26,23 @@ struct ATabData {
     int32_t pad;
 };
 
+// fp32 copies of the decode tables for the dense-gate fast path (kernels_a.cu
+// "certified fp32"), replicated so that a warp's 32 random lookups never
+// share a shared-memory bank: rf[raw b0][lane], cs[raw b1][lane & 15] (a
+// 64-bit load serves 16 lanes per wavefront).  Indexed by the raw code byte
+// (two's-complement int8), so no bias is added at lookup.
+struct AFTab {
+    float rf[256][32];
+    float cs[256][16][2];
+};
+static_assert(sizeof(AFTab) == 65536, "AFTab is 64 KiB (one CTA's dynamic shared memory)");
+
 struct ATables {
     ATabData *d[2] = {nullptr, nullptr};
+    AFTab *f[2] = {nullptr, nullptr};  // fp32 tables of d[0] / d[1]
     ATabData *h = nullptr;  // pinned host staging
+    AFTab *hf = nullptr;
+    unsigned long long *gext = nullptr;  // k_bounds_a: the gate's exact (min, max) |z'|^2 bits, grid-wide
     int cur = 0;
 };
 int atables_alloc(ATables **out);
@@ -46,6 +60,11 @@ struct AGateParams {
     int32_t cls;
     int32_t pad;
     double u[8];
+    // filled by the dense launchers: fp32 copy of U, and the magnitude
+    // coefficients of the bounds screen (k_bounds_a): A >= B >= 0 bound
+    // max(|u00|, |u11|), max(|u01|, |u10|) from above, a / b their nominal values
+    float uf[8];
+    float mA, mB, ma, mb;
 };
 struct ACollapseParams {
     void *a;
@@ -63,6 +82,7 @@ void launch_bounds_a(const AGateParams &p, const ATables *t, double *partials, d
                      cudaStream_t s);
 // the next tables (r, thr, r0, r1, scale) built on the device from acc (no host round trip)
 void launch_tables_next(const double *acc, ATables *t, cudaStream_t s);
+void a_bounds_debug_print();  // debug build (-DQSIM_ABND_DEBUG): screen counters of k_bounds_a
 // phase 2: decode (current tables), apply, encode (next tables)
 void launch_apply_a(const AGateParams &p, const ATables *t, cudaStream_t s);
 // diagonal / anti-diagonal gates: b1 shifts and code moves, bounds unchanged

@@ -125,11 +125,18 @@ def test_per_gate_full_grid_controlled_n22(ctl):
 
 def test_table5_recipe_in_a_vs_oracle_a_n24():
     """The Table-5 workload (SHORBOX + QFT on the x-register)
-    at the largest size the oracle-A finishes in a test (N = 24: G = 247,
-    y = 2, 16-qubit x-register; the paper's N = 30 instance is checked in E
-    below): the GPU A codes start equal to the oracle's and end within one
-    step; expectations within 1e-12 of those of the decoded state and within
-    the paper's A-vs-exact level (0.011) of E."""
+    at the largest size the oracle-A runs gate by gate in a test (N = 24:
+    G = 247, y = 2, 16-qubit x-register; the paper's N = 30 instance is
+    checked in E below).  SHORBOX codes equal the oracle's; then EVERY gate of
+    the QFT is checked from identical input codes (the GPU's codes before the
+    gate, fed to the oracle-A): decoded amplitudes within one step.  Over the
+    whole circuit the two runs drift apart at rounding ties -- the CPHASE
+    R_9 phase is exactly half a b1 step (SURVEY §8(c) "A on QFT"), which the
+    GPU's phase path rounds away from zero while the oracle's fp64
+    decode-rotate-encode lands on either side of the tie -- so the whole
+    circuit is bounded by the paper's accuracy level instead: expectations
+    within 0.011 of E (Table 4) and fidelity >= 0.99 against
+    the oracle-A."""
     n, nx, G, y = 24, 16, 247, 2
     ze0 = oracle.e_shorbox(n, nx, G, y)
     ref = oracle.AState(n)
@@ -139,13 +146,21 @@ def test_table5_recipe_in_a_vs_oracle_a_n24():
         s.prepare_shorbox(nx, G, y)
         c0, _, _ = s.get_codes()
         assert np.array_equal(c0, ref.codes)
-        s.apply_circuit(circ)
+        for i in range(len(circ)):
+            c, r0, r1 = s.get_codes()
+            one = oracle.AState(n, c, r0, r1)
+            g = circ.slice(i, i + 1)
+            one.run(g)
+            s.apply_circuit(g)
+            zg = s.get_state()
+            ok = within_one_step(zg, one.decoded(), one.r0, one.r1)
+            assert ok.all(), (i, 1 - ok.mean())
         zg = s.get_state()
         ex = s.expectations()
     ref.run(circ)
     zr = ref.decoded()
-    assert within_one_step(zg, zr, ref.r0, ref.r1).mean() >= 0.99
-    assert fidelity(zg, zr) >= 1 - 2e-3
+    f = fidelity(zg, zr)
+    assert f >= 0.99, f
     ee = oracle.e_expectations(oracle.e_run(ze0, n, circ), n)
     assert np.max(np.abs(ex - oracle.e_expectations(zg, n))) <= 1e-12
     assert np.max(np.abs(ex - ee)) <= 0.011

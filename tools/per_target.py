@@ -45,8 +45,9 @@ if enc == q.ENC_ADAPTIVE2:
 
 out = {"enc": enc_name, "n": n, "reps": reps, "warmup": warm, "unit": "ms per gate (CUDA events, library stream)",
        "rows": []}
+targets = [int(x) for x in os.environ["TARGETS"].split(",")] if os.environ.get("TARGETS") else list(range(n))
 for name, u, ctl in kinds:
-    for t in range(n):
+    for t in targets:
         s.profile(False)
         for _ in range(warm):
             s.apply_gate(u, t, ctl(t))
