@@ -740,12 +740,19 @@ __device__ __noinline__ void a_flush(const AGateParams *pp, const ATabData *cur,
 constexpr int A_DENSE_MINB = 3;  // CTAs per SM of the dense kernels (64 KiB of tables each)
 
 // Phase 1 (reading R-A4): exact min / max of the intermediate |z'|^2 of the
-// gate's output, through two screens:
+// gate's output, through screens of increasing cost:
+//  0. magnitudes only (fp32 table ra, rb): rigorous bounds on both outputs
+//       hi = A max(ra, rb) + B min(ra, rb) >= |u_j0| ra + |u_j1| rb >= |z'_j|,
+//       lo = min(|a ra - b rb|, |b ra - a rb|) - 3e-6 (ra + rb) <= |z'_j|
+//     (reverse triangle inequality; a = |u00| ~ |u11|, b = |u01| ~ |u10| for
+//     a unitary U, the margins cover fp32 rounding and the 1e-10 unitarity
+//     tolerance); a pair passes when [lo, hi] lies inside the running
+//     [min |z'|, max |z'|];
 //  1. fp32 decode + gate + |z'| with the certified bound ||z'f| - |z'|| <=
 //     sqrt2 E (E = A_KF (ra + rb) per component) and the fp32 rounding of
 //     the magnitude (4e-7 relative): a pair passes when both outputs provably
-//     lie inside the warp's exact running [min, max] of the intermediate |z'|
-//     (and so are intermediate themselves);
+//     lie inside the running [min, max] of the intermediate |z'| (and so are
+//     intermediate themselves) or are certainly below 1e-12 (special zero);
 //  2. otherwise (a new extreme, or a tie with one: the structured workload
 //     states have massive exact ties at the extremes), the pair's class --
 //     raw b0 of both codes, the b1 difference mod 256, whether the gate
@@ -862,37 +869,40 @@ __global__ void __launch_bounds__(A_THREADS, A_BOUNDS_MINB) k_bounds_a(const __g
                 const int j0 = U::j0(k), j1 = U::j1(k);
                 const int off = TL < 4 ? j0 : k;
                 const bool sel = !CTRL || (hi_ok && ((uint32_t)off & cl) == cl);
-                float ra, rb;
-                float2 x = L.decode(c[j0], ra), y = L.decode(c[j1], rb);
-                if (sel) a_gate_fu<UK>(uf, x, y);
+                const float ra = L.rf[(c[j0] & 0xffu) * 32u], rb = L.rf[(c[j1] & 0xffu) * 32u];
                 const float S = ra + rb;
-                // |z'| within sqrt2 E of |z'f| (E = A_KF S per component), mf within 4e-7 mf of |z'f|
-                const float m2x = fmaf(x.x, x.x, x.y * x.y), m2y = fmaf(y.x, y.x, y.y * y.y);
-                float mfx = m2x * a_rsqrt(m2x), mfy = m2y * a_rsqrt(m2y);
-                mfx = m2x > 0.f ? mfx : 0.f;
-                mfy = m2y > 0.f ? mfy : 0.f;
                 const float eS = 1.4145e-6f * S;
-                // a certainly-zero output (|z'| < 1e-12, reading R-A5) is no intermediate: not a
-                // min candidate (the A states of the workloads hold many amplitudes at the
-                // 1e-12 floor, whose products straddle it)
-                float lx = fmaf(mfx, 1.0000005f, eS) < 0.99999e-12f ? INFINITY : mfx;
-                float ly = fmaf(mfy, 1.0000005f, eS) < 0.99999e-12f ? INFINITY : mfy;
-                if (CTRL && !sel) {  // an unselected zero code stays the exact zero special
-                    lx = ra == 0.f ? INFINITY : lx;
-                    ly = rb == 0.f ? INFINITY : ly;
+                // screen 0, magnitudes only: hi >= |z'_j| >= lo for both outputs
+                float hi, lo;
+                if (!CTRL || sel) {
+                    hi = fmaf(p.mA, fmaxf(ra, rb), p.mB * fminf(ra, rb));
+                    lo = fminf(fabsf(fmaf(p.ma, ra, -p.mb * rb)), fabsf(fmaf(p.mb, ra, -p.ma * rb)));
+                } else {  // unselected: |z'| = (ra, rb); a zero code stays the exact zero special
+                    hi = fmaxf(ra, rb);
+                    lo = fminf(ra == 0.f ? INFINITY : ra, rb == 0.f ? INFINITY : rb);
                 }
-                const bool cand = (S > 0.f) & ((fminf(lx, ly) * 0.9999995f < tlo + eS) |
-                                               (fmaxf(mfx, mfy) * 1.0000005f > thi - eS));
+                bool cand = (S > 0.f) & ((fmaf(-3e-6f, S, lo) < tlo) | (hi > thi));
+                if (cand) {  // screen 1, fp32 gate: |z'| within sqrt2 E of |z'f|, mf within 4e-7 mf
+                    const float2 csa = L.cs[((c[j0] >> 8) & 0xffu) * 16u], csb = L.cs[((c[j1] >> 8) & 0xffu) * 16u];
+                    float2 x = make_float2(ra * csa.x, ra * csa.y), y = make_float2(rb * csb.x, rb * csb.y);
+                    if (sel) a_gate_fu<UK>(uf, x, y);
+                    const float m2x = fmaf(x.x, x.x, x.y * x.y), m2y = fmaf(y.x, y.x, y.y * y.y);
+                    float mfx = m2x * a_rsqrt(m2x), mfy = m2y * a_rsqrt(m2y);
+                    mfx = m2x > 0.f ? mfx : 0.f;
+                    mfy = m2y > 0.f ? mfy : 0.f;
+                    // a certainly-zero output (|z'| < 1e-12, reading R-A5) is no intermediate:
+                    // not a min candidate (the A states of the workloads hold many amplitudes
+                    // at the 1e-12 floor, whose products straddle it)
+                    float lx = fmaf(mfx, 1.0000005f, eS) < 0.99999e-12f ? INFINITY : mfx;
+                    float ly = fmaf(mfy, 1.0000005f, eS) < 0.99999e-12f ? INFINITY : mfy;
+                    if (CTRL && !sel) {
+                        lx = ra == 0.f ? INFINITY : lx;
+                        ly = rb == 0.f ? INFINITY : ly;
+                    }
+                    cand = (fminf(lx, ly) * 0.9999995f < tlo + eS) | (fmaxf(mfx, mfy) * 1.0000005f > thi - eS);
+                }
 #ifdef QSIM_ABND_DEBUG
                 if (cand) atomicAdd(&g_abnd_dbg[1], 1ull);
-                if (cand && (fminf(lx, ly) * 0.9999995f < tlo + eS)) atomicAdd(&g_abnd_dbg[0], 1ull);
-                if (cand && (fminf(lx, ly) < 1e-3f * S)) atomicAdd(&g_abnd_dbg[3], 1ull);
-                if (cand && blockIdx.x == 7 && (threadIdx.x & 31) == 3 && vb > 60ull * gridDim.x * A_THREADS) {
-                    unsigned long long nprint = atomicAdd(&g_abnd_dbg[4], 1ull);
-                    if (nprint < 12)
-                        printf("cand ra %.6e rb %.6e mfx %.9e mfy %.9e tlo %.9e thi %.9e eS %.3e ca %04x cb %04x\n", ra,
-                               rb, mfx, mfy, tlo, thi, eS, c[j0], c[j1]);
-                }
 #endif
                 if (cand) {  // one evaluation per class: a class in the warp's cache is done
                     const uint32_t ca = c[j0], cb = c[j1];
@@ -1257,6 +1267,10 @@ struct AFastParams {
     uint64_t n;  // codes in the shard
     int32_t nl, t, cls;
     int32_t k0, k1;  // DIAG: b1 steps for bit 0 / 1; ANTI: k0 = steps of u01, k1 = steps of u10
+    // ANTI: units visited = units with every local control above the unit's own bits = 1:
+    // unit index bits fixed to 1 (ascending positions), the visited count
+    int32_t ins[2], nins;
+    uint64_t nvis;
 };
 
 // Diagonal gates visit only the 16-byte vectors (8 codes) that hold touched
@@ -1308,11 +1322,16 @@ __global__ void __launch_bounds__(A_THREADS) k_diag_a(const __grid_constant__ AD
     }
 }
 
+// Permutation gates move codes: only the units whose
+// control bits above the unit's own code bits are all 1 are visited (those
+// bits are inserted into the unit index, like the E sweep's control
+// insertion); controls inside a unit are tested per pair.
 template <bool LOWT>
 __global__ void __launch_bounds__(A_THREADS) k_anti_a(const __grid_constant__ AFastParams p) {
     uint16_t *a = reinterpret_cast<uint16_t *>(p.a);
-    const uint64_t units = (p.nl >= 4) ? (1ull << (p.nl - 4)) : 1ull;
-    for (uint64_t u = (uint64_t)blockIdx.x * A_THREADS + threadIdx.x; u < units; u += (uint64_t)gridDim.x * A_THREADS) {
+    for (uint64_t w = (uint64_t)blockIdx.x * A_THREADS + threadIdx.x; w < p.nvis; w += (uint64_t)gridDim.x * A_THREADS) {
+        uint64_t u = w;
+        for (int q = 0; q < p.nins; ++q) u = a_ins0(u, p.ins[q]) | (1ull << p.ins[q]);
         uint32_t c[16];
         uint64_t s0;
         unit_load<LOWT>(a, u, p.t, c, s0);
@@ -1381,10 +1400,20 @@ void launch_fast_a(const AGateParams &g, const ATables *t, cudaStream_t s) {
     } else {
         p.k0 = phase_steps(g.u[2], g.u[3]);
         p.k1 = phase_steps(g.u[4], g.u[5]);
-        if (g.t < 4)
-            k_anti_a<true><<<a_grid(p.n >> 4), A_THREADS, 0, s>>>(p);
+        // local controls above the unit bits become fixed unit-index bits
+        const bool lowt = g.t < 4;
+        const int lowb = lowt ? 4 : 3;
+        const uint64_t units = p.n >> 4;
+        int ub[2], nu = 0;
+        for (int b = lowb; b < g.nl && b < 64; ++b)
+            if (b != g.t && ((g.cmask >> b) & 1ull)) ub[nu++] = lowt ? b - 4 : (b < g.t ? b - 3 : b - 4);
+        p.nins = nu;
+        for (int q = 0; q < nu; ++q) p.ins[q] = ub[q];  // ascending
+        p.nvis = units >> nu;
+        if (lowt)
+            k_anti_a<true><<<a_grid(p.nvis), A_THREADS, 0, s>>>(p);
         else
-            k_anti_a<false><<<a_grid(p.n >> 4), A_THREADS, 0, s>>>(p);
+            k_anti_a<false><<<a_grid(p.nvis), A_THREADS, 0, s>>>(p);
     }
 }
 

@@ -356,6 +356,37 @@ def qft_register(n: int, m: int, swaps: bool = True) -> Circuit:
     return c
 
 
+def draper_adder(k: int, a: int, b: int) -> Circuit:
+    """The QFT adder of PAPER.md section 5.3 (Table 4; Draper's
+    construction, DRAP00) on n = 2k qubits: b on qubits 0..k-1 (bit j on qubit
+    j), a on qubits k..2k-1 in reversed bit order (bit j of a on qubit 2k-1-j:
+    the layout Table 4's a-register column shows, reading R-B12).  X gates
+    prepare |b>|a>; QFT without swaps on the b register (reading A15: for
+    j = k-1..0 { H(j); CPHASE(m -> j, 2pi/2^(j-m+1)), m = j-1..0 }) gives qubit
+    j the phase 2pi (b mod 2^(j+1))/2^(j+1); CPHASE(a_m -> j, 2pi/2^(j-m+1)),
+    m <= j, adds a's; the inverse QFT returns |a + b mod 2^k> on qubits 0..k-1.
+    Gate count: popcount(a) + popcount(b) + 3 k (k + 1)/2."""
+    n = 2 * k
+    c = Circuit(n)
+    for j in range(k):
+        if (b >> j) & 1:
+            c.add("X", mat_X(), j)
+        if (a >> j) & 1:
+            c.add("X", mat_X(), n - 1 - j)
+    for j in range(k - 1, -1, -1):
+        c.add("H", mat_H(), j)
+        for m in range(j - 1, -1, -1):
+            c.add("CPHASE", mat_R(j - m + 1), j, [m])
+    for j in range(k - 1, -1, -1):
+        for m in range(j, -1, -1):
+            c.add("CPHASE", mat_R(j - m + 1), j, [n - 1 - m])
+    for j in range(k):
+        for m in range(j):
+            c.add("CPHASE", mat_R(-(j - m + 1)), j, [m])
+        c.add("H", mat_H(), j)
+    return c
+
+
 def config(idx: int, n: int | None = None, seed: int | None = None, layers: int | None = None) -> Circuit:
     """BASELINE.json configs by index (0-based as in the JSON list)."""
     if idx == 0:

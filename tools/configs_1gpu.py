@@ -135,6 +135,30 @@ def s2_ghz():
     return rows
 
 
+def table4_adder():
+    """NEXT-2: the scaled Table-4 QFT adder, a = 210018 mod 2^k,
+    b = 2^k - 1 - a: E at N = 30 (k = 15) and A at N = 30 and N = 34 (k = 17);
+    max deviation of the expectation values from the closed form."""
+    rows = []
+    for k, enc in ((15, q.ENC_FP64), (15, q.ENC_ADAPTIVE2), (17, q.ENC_ADAPTIVE2)):
+        a = 210018 % (1 << k)
+        b = (1 << k) - 1 - a
+        n = 2 * k
+        circ = C.draper_adder(k, a, b)
+        idx = (a + b) % (1 << k)
+        for j in range(k):
+            if (a >> j) & 1:
+                idx |= 1 << (n - 1 - j)
+        ref = np.array([[0.5, 0.5, float((idx >> qq) & 1)] for qq in range(n)])
+        with q.State(n, enc, 1) as s:
+            dev, wall, prof, st = run(s, circ, warm=enc == q.ENC_FP64)
+            ex = s.expectations()
+        rows.append(summary("table4_adder_" + ("E" if enc == q.ENC_FP64 else "A"), circ, dev, wall, prof, st,
+                            k=k, max_dev_vs_closed_form=float(np.max(np.abs(ex - ref))),
+                            min_sum_bit_Qz=float(np.min(ex[:k, 2]))))
+    return rows
+
+
 def cfg4_trend():
     """Config-4 fidelity and norm drift of A against E as N grows (10 layers)."""
     rows = []
@@ -150,7 +174,7 @@ def cfg4_trend():
     return rows
 
 
-ROWS = {"cfg4_trend": cfg4_trend, "cfg3_n33": cfg3_n33, "cfg4_n33": cfg4_n33, "cfg5_n32": cfg5_n32, "s1_hwall": s1_hwall, "s2_ghz": s2_ghz}
+ROWS = {"table4_adder": table4_adder, "cfg4_trend": cfg4_trend, "cfg3_n33": cfg3_n33, "cfg4_n33": cfg4_n33, "cfg5_n32": cfg5_n32, "s1_hwall": s1_hwall, "s2_ghz": s2_ghz}
 want = sys.argv[1:] or list(ROWS)
 out = []
 for name in want:
