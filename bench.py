@@ -3,16 +3,17 @@
 
 Workload (one "step" = one pass of the whole hot path over one batch of
 synthetic input = the whole circuit applied to the resident state):
-  N GPUs = 1: BASELINE config 2 -- N=30 E (16 GiB), H on all 30 qubits, then
-              20 layers of Haar U(2) on every qubit + CNOTs on a random perfect
-              matching (seed 1, 930 gates).
-  N GPUs = P: weak scaling, the same recipe at n = 30 + log2(P) qubits, 2^30
-              amplitudes per GPU, top log2(P) qubits global (one process per
-              GPU, NCCL exchange), as in BASELINE config 3's series.
+  BASELINE config 3 at every P = 1/2/4/8 GPUs: N = 33 + log2(P) qubits, E
+  fp64, 2^33 amplitudes (128 GiB) per GPU, top log2(P) qubits global; H on
+  all N, then 10 layers of Haar U(2) on every qubit + CNOTs on a random
+  perfect matching (seed 3; 523/544/555/576 gates).  P = 1 is the weak-scaling
+  base point and the largest single-GPU E workload.  Launch: torchrun (one
+  process per GPU, QSIM_TRANSPORT_NCCL) or plain `python bench.py --gpus P`
+  (one process driving P GPUs, QSIM_TRANSPORT_DEVICES).
 value = aggregate effective HBM GB/s = sum over gates of the gate's
 algorithmic bytes (SURVEY.md §8(d) byte-accounting: 32 B x amplitudes touched
 by the gate, 0 for SWAP) over all GPUs / device time (max over ranks).
-Inputs are larger than L2 (16 GiB state >> 126 MB), so no L2 flush is needed.
+Inputs are larger than L2 (128 GiB state >> 126 MB), so no L2 flush is needed.
 Warm-up: the first warm-up step queues the NVRTC specialisation of every pass
 program of the circuit; bench.py waits for them (qsim_jit_sync) before the
 remaining warm-up steps, so the timed steps run the specialised pass kernels
@@ -126,13 +127,16 @@ class ClockSampler:
 
 def workload(world):
     k = int(round(math.log2(world)))
-    n = 30 + k
-    circ = C.layered(n, 20, seed=1)
-    name = ("config2: N=30 E fp64 (16 GiB), H wall + 20 layers (Haar U(2) on every qubit + CNOT perfect "
-            "matching), 930 gates, seed 1" if world == 1 else
-            f"config2 recipe weak-scaled: N={n} E fp64, 2^30 amplitudes per GPU, top {k} qubits global, "
-            f"H wall + 20 layers (Haar U(2) on every qubit + CNOT matching), {len(circ)} gates, seed 1")
+    n = 33 + k
+    circ = C.config(2, n=n)  # layered(n, 10, seed=3)
+    name = (f"config3: N={n} E fp64, 2^33 amplitudes (128 GiB) per GPU, top {k} qubit(s) global, H wall + 10 layers "
+            f"(Haar U(2) on every qubit + CNOT perfect matching), {len(circ)} gates, seed 3")
     return n, circ, name
+
+
+def recipe(n):
+    """The workload recipe at another size (the CPU legs' fallback when the host lacks the RAM)."""
+    return C.config(2, n=n)
 
 
 def cpu_sample(circ_full, budget_s=15.0):
@@ -144,7 +148,7 @@ def cpu_sample(circ_full, budget_s=15.0):
     need = (16 << n) * 1.5
     if psutil.virtual_memory().available < need:
         n = 28
-    circ = C.layered(n, 20, seed=1) if n != circ_full.n else circ_full
+    circ = recipe(n) if n != circ_full.n else circ_full
     a = oracle.e_init(n)
     done, t_all, nbytes = 0, 0.0, 0.0
     while t_all < budget_s and done < len(circ):
@@ -189,7 +193,7 @@ def run_reference(args, rank, world):
     oracle.set_num_threads(len(os.sched_getaffinity(0)))
     if psutil.virtual_memory().available < (16 << n) * 1.5:
         n = 28
-        circ = C.layered(n, 20, seed=1)
+        circ = recipe(n)
     a = oracle.e_init(n)
     # each step: a bounded sample -- the next `g` gates of the circuit (about 2 s of CPU work)
     t0 = time.perf_counter()
@@ -235,9 +239,11 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--fuse", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-cold", action="store_true", help="skip the cold end-to-end leg")
     args = ap.parse_args()
+    torchrun = "RANK" in os.environ and "WORLD_SIZE" in os.environ
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus))) if torchrun else args.gpus
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, rank, world)
@@ -249,9 +255,10 @@ def main():
     import paper_1805_04708_b200 as q
 
     dist = None
-    # BENCH_FORCE_DIST=1 takes the multi-GPU code path (process group, NCCL
-    # transport) even with one rank -- a one-GPU check of the N>1 plumbing.
-    use_dist = world > 1 or os.environ.get("BENCH_FORCE_DIST") == "1"
+    # under torchrun: one process per GPU (NCCL transport); BENCH_FORCE_DIST=1
+    # takes that path even with one rank (a one-GPU check of the plumbing).
+    # Without torchrun, --gpus P > 1: this process drives P GPUs (DEVICES).
+    use_dist = torchrun and (world > 1 or os.environ.get("BENCH_FORCE_DIST") == "1")
     if use_dist:
         import torch.distributed as dist
 
@@ -262,14 +269,27 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         s = q.State(n, q.ENC_FP64, world, transport=q.TRANSPORT_NCCL, rank=rank, device=local,
                     nccl_id=obj[0], fuse=args.fuse)
+        devs = [local]
+        mode = f"{world} processes (torchrun), one GPU each, NCCL exchange"
+    elif world > 1:
+        s = q.State(n, q.ENC_FP64, world, transport=q.TRANSPORT_DEVICES, device=0, fuse=args.fuse)
+        devs = list(range(world))
+        mode = f"one process driving {world} GPUs (QSIM_TRANSPORT_DEVICES), in-process NCCL exchange"
     else:
         s = q.State(n, q.ENC_FP64, 1, fuse=args.fuse, device=local)
+        devs = [local]
+        mode = "one GPU"
     gates = q.pack_gates(circ)  # host gate records (the step's input)
-    stream = torch.cuda.ExternalStream(s.stream())
+    # the library's stream on every device this process drives
+    streams = [torch.cuda.ExternalStream(s.stream(r), device=torch.device("cuda", d)) for r, d in enumerate(devs)]
 
     def barrier():
         if dist:
             dist.barrier()
+
+    def sync_all():
+        for d in devs:
+            torch.cuda.synchronize(d)
 
     for w in range(args.warmup):
         s.apply_circuit(gates)
@@ -285,40 +305,58 @@ def main():
     s.profile_read()
     clocks = ClockSampler(local)
     clocks.start()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = []
+    for d in devs:
+        with torch.cuda.device(d):
+            evs.append((torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)))
     barrier()
-    torch.cuda.synchronize()
+    sync_all()
     s.sync()
-    e0.record(stream)
+    for (e0, _), st_ in zip(evs, streams):
+        e0.record(st_)
     for _ in range(args.steps):
         s.apply_circuit(gates)
-    e1.record(stream)
+    for (_, e1), st_ in zip(evs, streams):
+        e1.record(st_)
     s.sync()
-    torch.cuda.synchronize()
+    sync_all()
     barrier()
     clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
+    ms = max(e0.elapsed_time(e1) for e0, e1 in evs)  # max over the devices this process drives
     st = s.stats()
     prof = s.profile_read()
     s.profile(False)
-    t_dev = torch.tensor([ms, st["gate_bytes"], float(st["kernels"])], dtype=torch.float64, device="cuda")
+    t_dev = torch.tensor([ms, st["gate_bytes"], float(st["kernels"]), st["exchange_bytes"]], dtype=torch.float64,
+                         device="cuda")
     if dist:
         mx = t_dev.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         sm = t_dev.clone()
         dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        ms_max, bytes_all, launches = mx[0].item(), sm[1].item(), int(sm[2].item())
+        ms_max, bytes_all, launches, xbytes = mx[0].item(), sm[1].item(), int(sm[2].item()), sm[3].item()
     else:
-        ms_max, bytes_all, launches = ms, st["gate_bytes"], st["kernels"]
+        ms_max, bytes_all, launches, xbytes = ms, st["gate_bytes"], st["kernels"], st["exchange_bytes"]
     value = bytes_all / (ms_max / 1e3) / 1e9
     gates_per_s = len(circ) * args.steps / (ms_max / 1e3)
+
+    # ---- exchange (a7): bytes sent per direction per GPU over the exchange time ----
+    exchange = None
+    if world > 1:
+        xr = prof.get("xchg")
+        per_gpu = xbytes / world
+        if xr and xr["ms"] > 0:
+            gbs = per_gpu / (xr["ms"] / 1e3) / 1e9
+            exchange = {"GB_per_direction_per_gpu": per_gpu / 1e9, "exchange_ms": xr["ms"],
+                        "GBps_per_direction": gbs, "frac_of_900": gbs / 900.0, "frac_of_measured_770": gbs / 770.0,
+                        "what": "bytes each GPU sent (pairwise half-shard swaps + all-to-all remaps) / time of the "
+                                "exchange launches (CUDA events on the library stream, rank 0)"}
 
     # ---- end to end through the public API with host buffers ----
     # every step: reset to |0...0> (the method's input state), H2D of the host
     # gate records, the circuit, D2H of the result (per-qubit probabilities).
     e2e_steps = max(1, min(args.steps, 3))
     barrier()
-    torch.cuda.synchronize()
+    sync_all()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         s.reset()
@@ -333,6 +371,34 @@ def main():
     e2e = {"value": bytes_all / args.steps * e2e_steps / t_e2e / 1e9, "unit": UNIT,
            "h2d_bytes_per_step": 88 * len(circ), "d2h_bytes_per_step": 8 * len(p1),
            "what": "qsim_reset + qsim_apply_circuit(host gate records) + qsim_probabilities(host buffer), wall clock"}
+
+    # ---- cold end to end: a circuit never seen by this process every step ----
+    # (fresh seed: new CNOT matchings and matrices, so the host plan cache
+    # misses and the pass programs are new: planning + the interpreter while
+    # NVRTC specialises in the background, or the on-disk cubin cache)
+    if not args.no_cold:
+        cold_steps = 2
+        barrier()
+        sync_all()
+        t0 = time.perf_counter()
+        cb = 0.0
+        for i in range(cold_steps):
+            c2 = C.layered(n, 10, seed=1000 + i)
+            g2 = q.pack_gates(c2)
+            s.reset()
+            s.apply_circuit(g2)
+            s.probabilities()
+            cb += gate_bytes(c2)
+        t_cold = time.perf_counter() - t0
+        barrier()
+        if dist:
+            tt = torch.tensor([t_cold], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_cold = tt.item()
+        e2e["cold"] = {"value": cb / t_cold / 1e9, "unit": UNIT, "steps": cold_steps,
+                       "ms_per_step": t_cold / cold_steps * 1e3,
+                       "ratio_to_warm": (t_cold / cold_steps) / (t_e2e / e2e_steps),
+                       "what": "as e2e, but each step a circuit of the same recipe with a fresh seed (seeds 1000+i)"}
 
     # ---- roofline of the dominant kernel ----
     # Each launch has algorithmic bytes (HBM) and algorithmic fp64 flops; the
@@ -390,10 +456,10 @@ def main():
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": name, "n_qubits": n, "gates_per_step": len(circ),
                            "amplitudes_per_gpu": 1 << (n - int(round(math.log2(world)))),
-                           "fuse": args.fuse, "l2": "inputs larger than L2 (16 GiB state per GPU), no flush",
-                           "parallelism": f"state sharded over {world} GPU(s) by the top log2(P) qubits"},
+                           "fuse": args.fuse, "l2": "inputs larger than L2 (128 GiB state per GPU), no flush",
+                           "parallelism": f"state sharded over {world} GPU(s) by the top log2(P) qubits; {mode}"},
                 "gates_per_s": gates_per_s, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches, "clocks": clk, "per_kernel": per_kernel,
+                "exchange": exchange, "gpu_launches": launches, "clocks": clk, "per_kernel": per_kernel,
                 "library": {"passes": st["passes"], "jit_passes": st["jit_passes"], "fused_gates": st["fused_gates"],
                             "sweeps": st["sweeps"],
                             "exchanges": st["exchanges"], "exchange_GB": st["exchange_bytes"] / 1e9}}

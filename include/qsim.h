@@ -60,6 +60,10 @@ extern "C" {
                                   the exchange of a global-qubit gate is a device-to-device copy */
 #define QSIM_TRANSPORT_NCCL 1  /* one process per GPU; this process owns shard `rank`;
                                   the exchange is NCCL send/recv over NVLink */
+#define QSIM_TRANSPORT_DEVICES 2 /* one process drives nshards GPUs (devices `device`.. `device` + P - 1,
+                                  `device` = -1 meaning 0): shard r on device r, an in-process NCCL
+                                  communicator, one host thread per device running each call on its
+                                  shard -- the NCCL code path with every rank in this process */
 
 /* ---- gate records ---------------------------------------------------- */
 #define QSIM_GATE_U 0    /* controlled 2x2 gate: target, controls[0..ncontrols-1], u */
@@ -110,10 +114,15 @@ typedef struct qsim_stats {
 /* ---- lifetime ---------------------------------------------------------- */
 
 /* Create |0...0> (Eq. appa0) with N qubits in `encoding`,
- * split into `ngpus` shards that all live on the CURRENT device
- * (QSIM_TRANSPORT_LOCAL; use qsim_create_ex for one process per GPU).
- * *out receives the handle.  Errors: EINVAL (N, ngpus not a power of two,
- * fewer than 10 local qubits), ENOMEM (message has the byte count), ECUDA. */
+ * sharded over `ngpus` GPUs driven by this process: shard r on device r
+ * (QSIM_TRANSPORT_DEVICES; ngpus = 1: the current device).  The top
+ * log2(ngpus) qubits are global.  Every other call takes
+ * the handle as for one GPU; read-outs are collective and return one result.
+ * Use qsim_create_ex for one process per GPU (QSIM_TRANSPORT_NCCL) or for
+ * several shards on one device (QSIM_TRANSPORT_LOCAL, "loopback").
+ * *out receives the handle.  Errors: EINVAL (N, ngpus not a power of two or
+ * more than the visible GPUs, fewer than 10 local qubits), ENOMEM (message
+ * has the byte count), ECUDA, ECOMM. */
 int qsim_create(int n_qubits, int encoding, int ngpus, qsim_state **out);
 
 /* Full configuration (see qsim_config).  For QSIM_TRANSPORT_NCCL every rank
@@ -229,7 +238,8 @@ int qsim_set_qubit_map(qsim_state *s, const int *pos);
  * Z S S+ T T+ U1 U2 U3 +X -X +Y -Y R CNOT U TOFFOLI with the matrices of
  * App. B; BEGIN MEASUREMENT, GENERATE EVENTS, M, SHORBOX, CLEAR, SET, EXIT.
  * Errors: EINVAL with "line L: ..." in qsim_last_error().  qsim_asm_run
- * executes it on a fresh state (encoding, ngpus as qsim_create): runs of gates
+ * executes it on a fresh state (encoding; ngpus shards on the current device,
+ * QSIM_TRANSPORT_LOCAL): runs of gates
  * go to qsim_apply_circuit; BEGIN MEASUREMENT appends the 3N expectations of
  * qsim_expectations to the result; M n appends (n, outcome) drawn by
  * qsim_measure with seed = seed + (measurement index); GENERATE EVENTS draws

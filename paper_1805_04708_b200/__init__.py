@@ -34,6 +34,7 @@ ENC_FP64 = 0
 ENC_ADAPTIVE2 = 1
 TRANSPORT_LOCAL = 0
 TRANSPORT_NCCL = 1
+TRANSPORT_DEVICES = 2
 GATE_U = 0
 GATE_SWAP = 1
 OP_EXCHANGE = 0
@@ -556,9 +557,12 @@ class State:
     """Convenience wrapper: one handle, methods named after the C-ABI calls."""
 
     def __init__(self, n_qubits, encoding=ENC_FP64, ngpus=1, **ex):
+        """ngpus > 1 without a transport: that many shards on the current
+        device (QSIM_TRANSPORT_LOCAL, loopback); transport=TRANSPORT_DEVICES
+        spreads them over devices 0..ngpus-1 (qsim_create's default)."""
         self.n = n_qubits
         self.encoding = encoding
-        if ex:
+        if ex or ngpus > 1:
             self.h = qsim_create_ex(n_qubits, encoding, ngpus, **ex)
         else:
             self.h = qsim_create(n_qubits, encoding, ngpus)
@@ -634,8 +638,9 @@ class State:
     def sync(self):
         qsim_sync(self.h)
 
-    def stream(self):
-        return qsim_stream(self.h)
+    def stream(self, shard=0):
+        """cudaStream_t of the handle (of member `shard` for the multi-device transport)."""
+        return qsim_stream(self.h, shard)
 
     def apply_matrix(self, u, qubits):
         qsim_apply_matrix(self.h, u, qubits)

@@ -6,7 +6,10 @@
 
 #include <algorithm>
 #include <array>
+#include <condition_variable>
 #include <deque>
+#include <functional>
+#include <thread>
 #include <memory>
 #include <mutex>
 #include <unordered_map>
@@ -60,8 +63,12 @@ struct Shard {
 
 using namespace qsim;
 
+namespace qsim {
+struct QGroup;
+}
 struct qsim_state {
     int n = 0, enc = 0, P = 1, nl = 0, transport = 0, rank = 0, dev = 0, fuse = 1;
+    qsim::QGroup *group = nullptr;  // QSIM_TRANSPORT_DEVICES: this handle drives P member handles
     int pass_r = 4;  // register qubits per pass stage (QSIM_PASS_R=5 selects 32-amplitude groups)
     int pass_k = LP_MAX_K;  // tile qubits of the relabelling pass (QSIM_LPASS_K = 9..12)
     size_t amp_bytes = 16;
@@ -826,6 +833,89 @@ static int phys_probs(qsim_state *s, std::vector<double> &phys) {
 // ============================================================================
 // C-ABI
 // ============================================================================
+// ============================================================================
+// QSIM_TRANSPORT_DEVICES: one process drives P GPUs (SURVEY.md §8(e) process
+// model).  The handle owns P member handles, member r on
+// device base + r with the NCCL transport as rank r of a communicator whose
+// ranks all live in this process; one host thread per device runs every call
+// on its member concurrently (NCCL collectives of one communicator need all
+// ranks to enter them), so the exchange, remap and read-out code is exactly
+// the one-process-per-GPU path.  Results of collective read-outs are
+// identical on every rank; the caller gets member 0's.
+// ============================================================================
+namespace qsim {
+struct QGroup {
+    int P = 0, base = 0;
+    std::vector<qsim_state *> m;
+    std::vector<std::thread> th;
+    std::mutex mu;
+    std::condition_variable cv, cv_done;
+    const std::function<int(int, qsim_state *)> *job = nullptr;
+    uint64_t gen = 0;
+    int pending = 0;
+    bool stop = false;
+    std::vector<int> rc;
+    std::vector<std::string> err;
+};
+
+static void group_worker(QGroup *g, int r) {
+    cudaSetDevice(g->base + r);
+    uint64_t seen = 0;
+    for (;;) {
+        const std::function<int(int, qsim_state *)> *job;
+        {
+            std::unique_lock<std::mutex> lk(g->mu);
+            g->cv.wait(lk, [&] { return g->stop || g->gen != seen; });
+            if (g->stop) return;
+            seen = g->gen;
+            job = g->job;
+        }
+        cudaSetDevice(g->base + r);
+        const int rc = (*job)(r, g->m[r]);
+        std::string e = rc ? std::string(qsim_last_error()) : std::string();
+        std::lock_guard<std::mutex> lk(g->mu);
+        g->rc[r] = rc;
+        g->err[r] = e;
+        if (--g->pending == 0) g->cv_done.notify_all();
+    }
+}
+
+// run f(r, member r) on every member's thread; the first failing rank's code / message
+static int group_run(QGroup *g, const std::function<int(int, qsim_state *)> &f) {
+    {
+        std::unique_lock<std::mutex> lk(g->mu);
+        g->job = &f;
+        g->pending = g->P;
+        ++g->gen;
+        g->cv.notify_all();
+        g->cv_done.wait(lk, [&] { return g->pending == 0; });
+        g->job = nullptr;
+    }
+    for (int r = 0; r < g->P; ++r)
+        if (g->rc[r]) {
+            set_error("device " + std::to_string(g->base + r) + ": " + g->err[r]);
+            return g->rc[r];
+        }
+    return QSIM_OK;
+}
+
+static void group_stop(QGroup *g) {
+    {
+        std::lock_guard<std::mutex> lk(g->mu);
+        g->stop = true;
+        g->cv.notify_all();
+    }
+    for (auto &t : g->th)
+        if (t.joinable()) t.join();
+}
+}  // namespace qsim
+
+#define GROUP_ALL(s, expr)                                                                              \
+    do {                                                                                                \
+        if ((s) && (s)->group)                                                                          \
+            return group_run((s)->group, [&](int r_, qsim_state *m_) -> int { (void)r_; return (expr); }); \
+    } while (0)
+
 extern "C" {
 
 const char *qsim_last_error(void) { return g_err.c_str(); }
@@ -841,6 +931,18 @@ int qsim_nccl_unique_id(uint8_t out[128]) {
 
 int qsim_destroy(qsim_state *s) {
     if (!s) return QSIM_OK;
+    if (s->group) {
+        QGroup *g = s->group;
+        group_run(g, [&](int r, qsim_state *m) {
+            const int rc = qsim_destroy(m);
+            g->m[r] = nullptr;
+            return rc;
+        });
+        group_stop(g);
+        delete g;
+        delete s;
+        return QSIM_OK;
+    }
     if (s->dev >= 0) cudaSetDevice(s->dev);
     if (s->stream) cudaStreamSynchronize(s->stream);
     if (s->comm_stream) cudaStreamSynchronize(s->comm_stream);
@@ -920,7 +1022,65 @@ int qsim_create_ex(const qsim_config *cfg, qsim_state **out) {
     }
     // nshards = 1 defaults to LOCAL; an explicit NCCL request with one rank is honoured
     // (communicator + collective read-out paths, used to test NCCL on one GPU)
-    const int transport = (P == 1 && cfg->transport != QSIM_TRANSPORT_NCCL) ? QSIM_TRANSPORT_LOCAL : cfg->transport;
+    const int transport =
+        (P == 1 && cfg->transport != QSIM_TRANSPORT_NCCL && cfg->transport != QSIM_TRANSPORT_DEVICES)
+            ? QSIM_TRANSPORT_LOCAL
+            : cfg->transport;
+    if (transport == QSIM_TRANSPORT_DEVICES) {
+        // one process, P devices: member r = rank r of an in-process NCCL communicator on device base + r
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess) {
+            cudaGetLastError();
+            ndev = 0;
+        }
+        const int base = cfg->device >= 0 ? cfg->device : 0;
+        if (base + P > ndev) {
+            set_error("QSIM_TRANSPORT_DEVICES: " + std::to_string(P) + " shards need devices " + std::to_string(base) +
+                      ".." + std::to_string(base + P - 1) + ", " + std::to_string(ndev) +
+                      " visible (QSIM_TRANSPORT_LOCAL keeps every shard on one device)");
+            return QSIM_EINVAL;
+        }
+        uint8_t id[128];
+        RC(qsim_nccl_unique_id(id));
+        auto *g = new QGroup();
+        g->P = P;
+        g->base = base;
+        g->m.assign(P, nullptr);
+        g->rc.assign(P, 0);
+        g->err.assign(P, std::string());
+        for (int r = 0; r < P; ++r) g->th.emplace_back(group_worker, g, r);
+        int rc = group_run(g, [&](int r, qsim_state *) {
+            qsim_config c = *cfg;
+            c.transport = QSIM_TRANSPORT_NCCL;
+            c.rank = r;
+            c.device = base + r;
+            c.nccl_id = id;
+            return qsim_create_ex(&c, &g->m[r]);
+        });
+        if (rc) {
+            const std::string msg = qsim_last_error();
+            group_run(g, [&](int r, qsim_state *m) {
+                qsim_destroy(m);
+                g->m[r] = nullptr;
+                return QSIM_OK;
+            });
+            group_stop(g);
+            delete g;
+            set_error(msg);
+            return rc;
+        }
+        auto *s = new qsim_state();
+        s->n = n;
+        s->enc = cfg->encoding;
+        s->P = P;
+        s->nl = nl;
+        s->transport = QSIM_TRANSPORT_DEVICES;
+        s->dev = base;
+        s->fuse = cfg->fuse;
+        s->group = g;
+        *out = s;
+        return QSIM_OK;
+    }
     if (transport != QSIM_TRANSPORT_LOCAL && transport != QSIM_TRANSPORT_NCCL) {
         set_error("unknown transport");
         return QSIM_EINVAL;
@@ -1055,13 +1215,14 @@ int qsim_create(int n_qubits, int encoding, int ngpus, qsim_state **out) {
     c.n_qubits = n_qubits;
     c.encoding = encoding;
     c.nshards = ngpus;
-    c.transport = QSIM_TRANSPORT_LOCAL;
+    c.transport = ngpus > 1 ? QSIM_TRANSPORT_DEVICES : QSIM_TRANSPORT_LOCAL;
     c.device = -1;
     c.fuse = 1;
     return qsim_create_ex(&c, out);
 }
 
 int qsim_apply_circuit(qsim_state *s, const qsim_gate *gates, size_t ngates) {
+    GROUP_ALL(s, qsim_apply_circuit(m_, gates, ngates));
     if (!s || (!gates && ngates)) {
         set_error("null argument");
         return QSIM_EINVAL;
@@ -1074,6 +1235,7 @@ int qsim_apply_circuit(qsim_state *s, const qsim_gate *gates, size_t ngates) {
 }
 
 int qsim_apply_gate(qsim_state *s, const double u[8], int target, const int *controls, int ncontrols) {
+    GROUP_ALL(s, qsim_apply_gate(m_, u, target, controls, ncontrols));
     if (!s || !u || (ncontrols > 0 && !controls) || ncontrols < 0 || ncontrols > 2) {
         set_error("qsim_apply_gate: bad arguments (ncontrols must be 0..2)");
         return QSIM_EINVAL;
@@ -1088,6 +1250,7 @@ int qsim_apply_gate(qsim_state *s, const double u[8], int target, const int *con
 }
 
 int qsim_apply_matrix(qsim_state *s, const double *U, const int *qubits, int k) {
+    GROUP_ALL(s, qsim_apply_matrix(m_, U, qubits, k));
     if (!s || !U || !qubits || k < 1 || k > 3) {
         set_error("qsim_apply_matrix: bad arguments (k must be 1..3)");
         return QSIM_EINVAL;
@@ -1172,6 +1335,7 @@ int qsim_apply_matrix(qsim_state *s, const double *U, const int *qubits, int k) 
 }
 
 int qsim_apply_swap(qsim_state *s, int q1, int q2) {
+    GROUP_ALL(s, qsim_apply_swap(m_, q1, q2));
     if (!s) return QSIM_EINVAL;
     qsim_gate g{};
     g.kind = QSIM_GATE_SWAP;
@@ -1181,6 +1345,7 @@ int qsim_apply_swap(qsim_state *s, int q1, int q2) {
 }
 
 int qsim_reset(qsim_state *s) {
+    GROUP_ALL(s, qsim_reset(m_));
     if (s && s->capturing) {
         set_error("qsim_reset: not allowed while a graph capture is open");
         return QSIM_EINVAL;
@@ -1193,12 +1358,14 @@ int qsim_reset(qsim_state *s) {
 }
 
 int qsim_profile(qsim_state *s, int enable) {
+    GROUP_ALL(s, qsim_profile(m_, enable));
     if (!s) return QSIM_EINVAL;
     s->prof = enable != 0;
     return QSIM_OK;
 }
 
 int qsim_profile_read(qsim_state *s, qsim_kernel_profile *out, int max, int *nout) {
+    GROUP_ALL(s, r_ == 0 ? qsim_profile_read(m_, out, max, nout) : QSIM_OK);  // member 0's records
     if (s && s->capturing) {
         set_error("qsim_profile_read: not allowed while a graph capture is open");
         return QSIM_EINVAL;
@@ -1237,6 +1404,7 @@ int qsim_jit_shutdown(void) {
 }
 
 int qsim_sync(qsim_state *s) {
+    GROUP_ALL(s, qsim_sync(m_));
     if (!s) return QSIM_EINVAL;
     if (s->capturing) {
         set_error("qsim_sync: not allowed while a graph capture is open");
@@ -1254,6 +1422,10 @@ struct qsim_graph {
 };
 
 int qsim_graph_begin(qsim_state *s) {
+    if (s && s->group) {
+        set_error("qsim_graph_begin: not available for the multi-device transport");
+        return QSIM_EUNSUPPORTED;
+    }
     if (!s) return QSIM_EINVAL;
     if (s->capturing) {
         set_error("qsim_graph_begin: a capture is already open");
@@ -1328,28 +1500,55 @@ int qsim_graph_destroy(qsim_graph *g) {
 }
 
 void *qsim_stream(qsim_state *s, int shard) {
-    (void)shard;
+    if (s && s->group) {  // member `shard`'s stream (its device's)
+        const int r = shard >= 0 && shard < s->P ? shard : 0;
+        return (void *)s->group->m[r]->stream;
+    }
     return s ? (void *)s->stream : nullptr;
 }
 
 int qsim_get_stats(qsim_state *s, qsim_stats *out) {
+    if (s && s->group && out) {  // summed over the members (the shards this process owns)
+        std::vector<qsim_stats> v(s->P);
+        RC(group_run(s->group, [&](int r, qsim_state *m) { return qsim_get_stats(m, &v[r]); }));
+        qsim_stats t{};
+        for (const auto &x : v) {
+            t.gates = x.gates;
+            t.kernels += x.kernels;
+            t.sweeps += x.sweeps;
+            t.passes += x.passes;
+            t.fused_gates += x.fused_gates;
+            t.exchanges = std::max(t.exchanges, x.exchanges);
+            t.hbm_bytes += x.hbm_bytes;
+            t.gate_bytes += x.gate_bytes;
+            t.exchange_bytes += x.exchange_bytes;
+            t.stages += x.stages;
+            t.jit_passes += x.jit_passes;
+        }
+        *out = t;
+        return QSIM_OK;
+    }
     if (!s || !out) return QSIM_EINVAL;
     *out = s->st;
     return QSIM_OK;
 }
 int qsim_reset_stats(qsim_state *s) {
+    GROUP_ALL(s, qsim_reset_stats(m_));
     if (!s) return QSIM_EINVAL;
     s->st = qsim_stats{};
     return QSIM_OK;
 }
 
 int qsim_get_qubit_map(qsim_state *s, int *pos) {
+    GROUP_ALL(s, r_ == 0 ? qsim_get_qubit_map(m_, pos) : QSIM_OK);  // identical on every member
     if (!s || !pos) return QSIM_EINVAL;
     for (int q = 0; q < s->n; ++q) pos[q] = s->pl.pos[q];
     return QSIM_OK;
 }
 
 int qsim_norm(qsim_state *s, double *norm2) {
+    std::vector<double> g_sc(s && s->group ? s->P : 0);
+    GROUP_ALL(s, qsim_norm(m_, r_ == 0 ? norm2 : &g_sc[r_]));
     if (s && s->capturing) {
         set_error("qsim_norm: not allowed while a graph capture is open");
         return QSIM_EINVAL;
@@ -1363,6 +1562,8 @@ int qsim_norm(qsim_state *s, double *norm2) {
 }
 
 int qsim_magnitude_range(qsim_state *s, double *min_nonzero, double *max) {
+    std::vector<double> g_sc(s && s->group ? 2 * s->P : 0);
+    GROUP_ALL(s, qsim_magnitude_range(m_, r_ == 0 ? min_nonzero : &g_sc[2 * r_], r_ == 0 ? max : &g_sc[2 * r_ + 1]));
     if (!s || !min_nonzero || !max) return QSIM_EINVAL;
     if (s->capturing) {
         set_error("qsim_magnitude_range: not allowed while a graph capture is open");
@@ -1399,6 +1600,10 @@ int qsim_magnitude_range(qsim_state *s, double *min_nonzero, double *max) {
 }
 
 int qsim_overlap(qsim_state *a, qsim_state *b, double *out) {
+    if ((a && a->group) || (b && b->group)) {
+        set_error("qsim_overlap: not available for the multi-device transport");
+        return QSIM_EUNSUPPORTED;
+    }
     if (!a || !b || !out) return QSIM_EINVAL;
     if (a->capturing || b->capturing) {
         set_error("qsim_overlap: not allowed while a graph capture is open");
@@ -1431,6 +1636,8 @@ int qsim_overlap(qsim_state *a, qsim_state *b, double *out) {
 }
 
 int qsim_probabilities(qsim_state *s, double *p1) {
+    std::vector<double> g_sc(s && s->group ? (size_t)s->P * s->n : 0);
+    GROUP_ALL(s, qsim_probabilities(m_, r_ == 0 ? p1 : &g_sc[(size_t)r_ * s->n]));
     if (s && s->capturing) {
         set_error("qsim_probabilities: not allowed while a graph capture is open");
         return QSIM_EINVAL;
@@ -1460,6 +1667,8 @@ static int pair_sums_local(qsim_state *s, int b, double &sr, double &si) {
 }
 
 int qsim_expectations(qsim_state *s, double *q) {
+    std::vector<double> g_sc(s && s->group ? (size_t)s->P * 3 * s->n : 0);
+    GROUP_ALL(s, qsim_expectations(m_, r_ == 0 ? q : &g_sc[(size_t)r_ * 3 * s->n]));
     if (s && s->capturing) {
         set_error("qsim_expectations: not allowed while a graph capture is open");
         return QSIM_EINVAL;
@@ -1571,6 +1780,9 @@ static int collapse(qsim_state *s, int b, int out, double keep) {
 }
 
 int qsim_measure_u(qsim_state *s, int qubit, double u, int *outcome, double *p0_out) {
+    std::vector<int> g_o(s && s->group ? s->P : 0);
+    std::vector<double> g_p(s && s->group ? s->P : 0);
+    GROUP_ALL(s, qsim_measure_u(m_, qubit, u, r_ == 0 ? outcome : &g_o[r_], r_ == 0 ? p0_out : (p0_out ? &g_p[r_] : nullptr)));
     if (s && s->capturing) {
         set_error("qsim_measure_u: not allowed while a graph capture is open");
         return QSIM_EINVAL;
@@ -1593,6 +1805,7 @@ int qsim_measure_u(qsim_state *s, int qubit, double u, int *outcome, double *p0_
 }
 
 int qsim_project(qsim_state *s, int qubit, int value) {
+    GROUP_ALL(s, qsim_project(m_, qubit, value));
     if (s && s->capturing) {
         set_error("qsim_project: not allowed while a graph capture is open");
         return QSIM_EINVAL;
@@ -1610,6 +1823,8 @@ int qsim_project(qsim_state *s, int qubit, int value) {
 }
 
 int qsim_sample(qsim_state *s, size_t nsamples, uint64_t seed, uint64_t *out) {
+    std::vector<uint64_t> g_sc(s && s->group ? (size_t)s->P * nsamples : 0);
+    GROUP_ALL(s, qsim_sample(m_, nsamples, seed, r_ == 0 ? out : &g_sc[(size_t)r_ * nsamples]));
     if (s && s->capturing) {
         set_error("qsim_sample: not allowed while a graph capture is open");
         return QSIM_EINVAL;
@@ -1636,6 +1851,7 @@ int qsim_sample(qsim_state *s, size_t nsamples, uint64_t seed, uint64_t *out) {
 }
 
 int qsim_set_qubit_map(qsim_state *s, const int *pos) {
+    GROUP_ALL(s, qsim_set_qubit_map(m_, pos));
     if (!s || !pos) return QSIM_EINVAL;
     std::vector<int> seen(s->n, 0);
     for (int q = 0; q < s->n; ++q) {
@@ -1668,6 +1884,7 @@ int qsim_aux_amplitudes(int n_qubits, const qsim_gate *gates, size_t ngates, con
 }
 
 int qsim_prepare_shorbox(qsim_state *s, int nx, uint64_t G, uint64_t y) {
+    GROUP_ALL(s, qsim_prepare_shorbox(m_, nx, G, y));
     if (!s || nx < 0 || nx >= s->n || G < 2 || y < 1 || y >= G) {
         set_error("qsim_prepare_shorbox: need 0 <= nx < N, G >= 2, 1 <= y < G");
         return QSIM_EINVAL;
@@ -1696,6 +1913,8 @@ int qsim_prepare_shorbox(qsim_state *s, int nx, uint64_t G, uint64_t y) {
 }
 
 int qsim_measure(qsim_state *s, int qubit, uint64_t seed, int *outcome) {
+    std::vector<int> g_o(s && s->group ? s->P : 0);
+    GROUP_ALL(s, qsim_measure(m_, qubit, seed, r_ == 0 ? outcome : &g_o[r_]));
     if (s && s->capturing) {
         set_error("qsim_measure: not allowed while a graph capture is open");
         return QSIM_EINVAL;
@@ -1713,6 +1932,8 @@ static uint64_t logical_to_phys(const qsim_state *s, uint64_t L) {
 }
 
 int qsim_get_amplitudes(qsim_state *s, const uint64_t *idx, size_t m, double *out) {
+    std::vector<double> g_sc(s && s->group ? (size_t)(s->P - 1) * 2 * m : 0);
+    GROUP_ALL(s, qsim_get_amplitudes(m_, idx, m, r_ == 0 ? out : &g_sc[(size_t)(r_ - 1) * 2 * m]));
     if (s && s->capturing) {
         set_error("qsim_get_amplitudes: not allowed while a graph capture is open");
         return QSIM_EINVAL;
@@ -1801,6 +2022,7 @@ static int upload_inv(qsim_state *s, int **d_inv) {
 }
 
 int qsim_get_state(qsim_state *s, double *out) {
+    GROUP_ALL(s, qsim_get_state(m_, out));  // collective: every member writes the same bytes
     if (s && s->capturing) {
         set_error("qsim_get_state: not allowed while a graph capture is open");
         return QSIM_EINVAL;
@@ -1834,6 +2056,7 @@ int qsim_get_state(qsim_state *s, double *out) {
 }
 
 int qsim_set_state(qsim_state *s, const double *amps) {
+    GROUP_ALL(s, qsim_set_state(m_, amps));
     if (s && s->capturing) {
         set_error("qsim_set_state: not allowed while a graph capture is open");
         return QSIM_EINVAL;
@@ -1878,6 +2101,8 @@ static int sync_bounds(qsim_state *s) {
 }
 
 int qsim_get_bounds(qsim_state *s, double *r0, double *r1) {
+    std::vector<double> g_sc(s && s->group ? 2 * s->P : 0);
+    GROUP_ALL(s, qsim_get_bounds(m_, r_ == 0 ? r0 : &g_sc[2 * r_], r_ == 0 ? r1 : &g_sc[2 * r_ + 1]));
     if (!s || !r0 || !r1) return QSIM_EINVAL;
     if (s->capturing) {
         set_error("qsim_get_bounds: not allowed while a graph capture is open");
@@ -1895,6 +2120,8 @@ int qsim_get_bounds(qsim_state *s, double *r0, double *r1) {
 }
 
 int qsim_get_codes(qsim_state *s, int8_t *codes, double *r0, double *r1) {
+    std::vector<double> g_sc(s && s->group ? 2 * s->P : 0);
+    GROUP_ALL(s, qsim_get_codes(m_, codes, r_ == 0 ? r0 : &g_sc[2 * r_], r_ == 0 ? r1 : &g_sc[2 * r_ + 1]));
     if (s && s->capturing) {
         set_error("qsim_get_codes: not allowed while a graph capture is open");
         return QSIM_EINVAL;
@@ -1929,6 +2156,7 @@ int qsim_get_codes(qsim_state *s, int8_t *codes, double *r0, double *r1) {
 }
 
 int qsim_set_codes(qsim_state *s, const int8_t *codes, double r0, double r1) {
+    GROUP_ALL(s, qsim_set_codes(m_, codes, r0, r1));
     if (s && s->capturing) {
         set_error("qsim_set_codes: not allowed while a graph capture is open");
         return QSIM_EINVAL;

@@ -316,7 +316,14 @@ int qsim_asm_run(const qsim_asm *a, int encoding, int ngpus, uint64_t seed, qsim
         return QSIM_EINVAL;
     }
     qsim_state *s = nullptr;
-    int rc = qsim_create(a->n, encoding, ngpus, &s);
+    qsim_config cfg{};  // ngpus shards on the current device (QSIM_TRANSPORT_LOCAL)
+    cfg.n_qubits = a->n;
+    cfg.encoding = encoding;
+    cfg.nshards = ngpus;
+    cfg.transport = QSIM_TRANSPORT_LOCAL;
+    cfg.device = -1;
+    cfg.fuse = 1;
+    int rc = qsim_create_ex(&cfg, &s);
     if (rc) return rc;
     auto r = new qsim_asm_result();
     r->n = a->n;
