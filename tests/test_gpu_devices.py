@@ -35,11 +35,10 @@ def test_device_group_of_one(enc):
     if enc == 0:
         ref = oracle.e_simulate(n, circ)
         assert np.max(np.abs(z - ref)) <= TOL
-    else:
-        ra = oracle.AState(n).run(circ)
-        ref = ra.decoded()
-        step = (ra.r1 - ra.r0) / 253.0
-        assert np.mean(np.abs(np.abs(z) - np.abs(ref)) <= step + 1e-12) >= 0.99
+    else:  # A: the same codes as the one-device handle (the oracle-A parity is test_gpu_a*.py's)
+        with q.State(n, enc) as one:
+            one.apply_circuit(circ)
+            assert np.array_equal(z, one.get_state())
     assert np.max(np.abs(ex - oracle.e_expectations(z, n))) <= TOL
     assert np.max(np.abs(p1 - ex[:, 2] * nrm)) <= TOL
     assert np.max(np.abs(amps - z[[0, 5, 1 << 13]])) <= 1e-15
