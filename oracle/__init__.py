@@ -66,6 +66,10 @@ def lib():
                                      ctypes.c_int, _dp]
         L.oracle_a_run.argtypes = [_i8p, ctypes.c_int, _dp, _dp, ctypes.c_int64, _i32p, _i32p, _i32p, _i32p, _i32p,
                                    _dp, _dp]
+        L.oracle_a_apply_lazy.argtypes = L.oracle_a_apply.argtypes
+        L.oracle_a_apply_lazy.restype = ctypes.c_int
+        L.oracle_a_run_lazy.argtypes = L.oracle_a_run.argtypes
+        L.oracle_a_run_lazy.restype = ctypes.c_int64
         L.oracle_num_threads.restype = ctypes.c_int
         L.oracle_set_num_threads.argtypes = [ctypes.c_int]
         L.oracle_set_num_threads.restype = None
@@ -224,6 +228,26 @@ class AState:
         lib().oracle_a_apply(_ptr(self.codes, _i8p), self.n, ctypes.byref(r0c), ctypes.byref(r1c), _ptr(u8, _dp),
                              target, c, len(controls), _ptr(self.work(), _dp))
         self.r0, self.r1 = r0c.value, r1c.value
+
+    def apply_lazy(self, u, target: int, controls=()) -> bool:
+        """One gate under the lazy-bounds policy (reading R-A25); True if it rescaled."""
+        u8 = np.ascontiguousarray(np.asarray(u, dtype=np.complex128).reshape(2, 2)).view(np.float64).reshape(8)
+        c = (ctypes.c_int * 2)(*(list(controls) + [0, 0])[:2])
+        r0c, r1c = ctypes.c_double(self.r0), ctypes.c_double(self.r1)
+        rs = lib().oracle_a_apply_lazy(_ptr(self.codes, _i8p), self.n, ctypes.byref(r0c), ctypes.byref(r1c),
+                                       _ptr(u8, _dp), target, c, len(controls), _ptr(self.work(), _dp))
+        self.r0, self.r1 = r0c.value, r1c.value
+        return bool(rs)
+
+    def run_lazy(self, circuit) -> int:
+        """A circuit under the lazy-bounds policy; returns the number of rescales."""
+        g = circuit
+        r0c, r1c = ctypes.c_double(self.r0), ctypes.c_double(self.r1)
+        rs = lib().oracle_a_run_lazy(_ptr(self.codes, _i8p), self.n, ctypes.byref(r0c), ctypes.byref(r1c),
+                                     len(g.kind), _ptr(g.kind, _i32p), _ptr(g.target, _i32p), _ptr(g.target2, _i32p),
+                                     _ptr(g.nctrl, _i32p), _ptr(g.ctrl, _i32p), _ptr(g.u, _dp), _ptr(self.work(), _dp))
+        self.r0, self.r1 = r0c.value, r1c.value
+        return int(rs)
 
     def run(self, circuit):
         g = circuit

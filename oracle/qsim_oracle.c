@@ -430,6 +430,82 @@ int oracle_a_run(int8_t *code, int n, double *r0, double *r1, int64_t ngates, co
     return 0;
 }
 
+/* ---- A with lazy ("lagged") bounds: SURVEY.md §8(f) NEXT-4, the policy
+ * variant of PAPER.md:455-456 ("the values of r0 and r1 need to be updated")
+ * that updates them only when the circuit leaves the current range, reading
+ * R-A25 (SPEC's lazy rescale):
+ *   decode all with (r0, r1); apply the gate in fp64; if every intermediate
+ *   output magnitude m (reading R-A3/R-A5 classification) lies in
+ *   [r0 - d, r1 + d], d = (r1 - r0)/253 the magnitude step, encode with the
+ *   SAME (r0, r1) (a magnitude within one step outside the range clamps to
+ *   the nearest end code); otherwise recompute r0, r1 exactly over the whole
+ *   state (oracle_a_bounds) and encode with them -- the exact policy's step.
+ * Returns 1 when the gate rescaled, 0 when it kept the bounds.  work: 2*2^n
+ * doubles of scratch.  No fast paths. */
+static int oracle_a_in_range(const double *z, uint64_t dim, double r0, double r1)
+{
+    const double d = (r1 - r0) / 253.0;
+    int in = 1;
+#pragma omp parallel for schedule(static) reduction(&& : in)
+    for (uint64_t i = 0; i < dim; ++i) {
+        const double m = hypot(z[2 * i], z[2 * i + 1]);
+        if (a_class(m) != 2) continue;
+        in = in && (m >= r0 - d) && (m <= r1 + d);
+    }
+    return in;
+}
+
+static void oracle_a_encode_with(const double *z, int n, int8_t *code, double r0, double r1)
+{
+    uint64_t dim = (uint64_t)1 << n;
+#pragma omp parallel for schedule(static)
+    for (uint64_t i = 0; i < dim; ++i) {
+        int b0, b1;
+        oracle_a_encode(z[2 * i], z[2 * i + 1], r0, r1, &b0, &b1);
+        code[2 * i] = (int8_t)b0;
+        code[2 * i + 1] = (int8_t)b1;
+    }
+}
+
+int oracle_a_apply_lazy(int8_t *code, int n, double *r0, double *r1, const double *u, int t, const int *ctrl,
+                        int nctrl, double *work)
+{
+    uint64_t dim = (uint64_t)1 << n;
+    oracle_a_decode_state(code, n, *r0, *r1, work);
+    oracle_e_apply(work, n, u, t, ctrl, nctrl);
+    if (oracle_a_in_range(work, dim, *r0, *r1)) {
+        oracle_a_encode_with(work, n, code, *r0, *r1);
+        return 0;
+    }
+    oracle_a_encode_state(work, n, code, r0, r1);
+    return 1;
+}
+
+/* a circuit under the lazy policy; SWAP records rescale like gates (their
+ * outputs are the inputs, always in range); returns the number of rescales */
+int64_t oracle_a_run_lazy(int8_t *code, int n, double *r0, double *r1, int64_t ngates, const int32_t *kind,
+                          const int32_t *target, const int32_t *target2, const int32_t *nctrl, const int32_t *ctrl,
+                          const double *u, double *work)
+{
+    int64_t rescales = 0;
+    for (int64_t g = 0; g < ngates; ++g) {
+        if (kind[g] == 1) {
+            oracle_a_decode_state(code, n, *r0, *r1, work);
+            oracle_e_swap(work, n, target[g], target2[g]);
+            if (oracle_a_in_range(work, (uint64_t)1 << n, *r0, *r1)) {
+                oracle_a_encode_with(work, n, code, *r0, *r1);
+            } else {
+                oracle_a_encode_state(work, n, code, r0, r1);
+                ++rescales;
+            }
+        } else {
+            int c[2] = {ctrl[2 * g], ctrl[2 * g + 1]};
+            rescales += oracle_a_apply_lazy(code, n, r0, r1, u + 8 * g, target[g], c, nctrl[g], work);
+        }
+    }
+    return rescales;
+}
+
 int oracle_num_threads(void)
 {
 #ifdef _OPENMP
