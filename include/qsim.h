@@ -91,8 +91,14 @@ typedef struct qsim_config {
     int64_t chunk_bytes; /* exchange chunk per transfer; 0 = default (2^{N-3}/P B in
                             total, i.e. 2^{N-4}/P per buffer of a double buffer, capped at 512 MiB) */
     int32_t fuse;        /* 1 = fuse runs of gates into shared-memory tile passes (default), 0 = one sweep per gate */
-    int32_t reserved;
+    int32_t a_policy;    /* A encoding: when (r0, r1) are updated ("need to be updated"):
+                            QSIM_A_POLICY_EXACT (0, default): exact bounds of every dense gate's output
+                            (reading R-A4; two passes, 6 B/amp); QSIM_A_POLICY_LAZY (1): kept while the
+                            outputs stay within one step of them, exact rescale when one leaves (reading
+                            R-A25; one out-of-place pass of 4 B/amp in range, a second code buffer) */
 } qsim_config;
+#define QSIM_A_POLICY_EXACT 0
+#define QSIM_A_POLICY_LAZY 1
 
 /* Counters since creation (or the last qsim_reset_stats). Bytes are ALGORITHMIC
  * bytes (SURVEY.md §8(d) byte-accounting rule), summed over the shards this
@@ -109,6 +115,9 @@ typedef struct qsim_stats {
     double exchange_bytes;    /* bytes sent per direction by this process's shards */
     int64_t stages;           /* register stages summed over fused passes */
     int64_t jit_passes;       /* fused passes run by a run-time specialised kernel (the rest interpreted) */
+    int64_t a_rescales;       /* A: dense gates that (re)computed the bounds (every dense gate for the exact
+                                 policy; the out-of-range ones for the lazy policy) */
+    int64_t a_dense;          /* A: dense gates applied */
 } qsim_stats;
 
 /* ---- lifetime ---------------------------------------------------------- */

@@ -35,6 +35,8 @@ ENC_ADAPTIVE2 = 1
 TRANSPORT_LOCAL = 0
 TRANSPORT_NCCL = 1
 TRANSPORT_DEVICES = 2
+A_POLICY_EXACT = 0
+A_POLICY_LAZY = 1
 GATE_U = 0
 GATE_SWAP = 1
 OP_EXCHANGE = 0
@@ -58,14 +60,15 @@ class qsim_config(ctypes.Structure):
     _fields_ = [("n_qubits", ctypes.c_int32), ("encoding", ctypes.c_int32), ("nshards", ctypes.c_int32),
                 ("transport", ctypes.c_int32), ("rank", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("nccl_id", ctypes.c_void_p), ("chunk_bytes", ctypes.c_int64), ("fuse", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("a_policy", ctypes.c_int32)]
 
 
 class qsim_stats(ctypes.Structure):
     _fields_ = [("gates", ctypes.c_int64), ("kernels", ctypes.c_int64), ("sweeps", ctypes.c_int64),
                 ("passes", ctypes.c_int64), ("fused_gates", ctypes.c_int64), ("exchanges", ctypes.c_int64),
                 ("hbm_bytes", ctypes.c_double), ("gate_bytes", ctypes.c_double),
-                ("exchange_bytes", ctypes.c_double), ("stages", ctypes.c_int64), ("jit_passes", ctypes.c_int64)]
+                ("exchange_bytes", ctypes.c_double), ("stages", ctypes.c_int64), ("jit_passes", ctypes.c_int64),
+                ("a_rescales", ctypes.c_int64), ("a_dense", ctypes.c_int64)]
 
 
 class qsim_kernel_profile(ctypes.Structure):
@@ -241,10 +244,10 @@ def qsim_create(n_qubits: int, encoding: int = ENC_FP64, ngpus: int = 1):
 
 
 def qsim_create_ex(n_qubits, encoding=ENC_FP64, nshards=1, transport=TRANSPORT_LOCAL, rank=0, device=-1,
-                   nccl_id: bytes | None = None, chunk_bytes=0, fuse=1):
+                   nccl_id: bytes | None = None, chunk_bytes=0, fuse=1, a_policy=0):
     cfg = qsim_config()
     cfg.n_qubits, cfg.encoding, cfg.nshards, cfg.transport = n_qubits, encoding, nshards, transport
-    cfg.rank, cfg.device, cfg.chunk_bytes, cfg.fuse = rank, device, chunk_bytes, fuse
+    cfg.rank, cfg.device, cfg.chunk_bytes, cfg.fuse, cfg.a_policy = rank, device, chunk_bytes, fuse, a_policy
     idbuf = None
     if nccl_id is not None:
         idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)

@@ -57,6 +57,7 @@ static inline uint64_t ins0(uint64_t w, int p) { return ((w >> p) << (p + 1)) | 
 struct Shard {
     int index = 0;            // global shard index (rank bits)
     void *amps = nullptr;     // 2^nl amplitudes
+    void *amps2 = nullptr;    // A, lazy bounds: the out-of-place target of a dense gate (swapped after it)
 };
 
 }  // namespace qsim
@@ -69,6 +70,8 @@ struct QGroup;
 struct qsim_state {
     int n = 0, enc = 0, P = 1, nl = 0, transport = 0, rank = 0, dev = 0, fuse = 1;
     qsim::QGroup *group = nullptr;  // QSIM_TRANSPORT_DEVICES: this handle drives P member handles
+    int a_policy = 0;               // QSIM_A_POLICY_*
+    int32_t *d_oor = nullptr;       // lazy policy: "an output left the kept range" flag
     int pass_r = 4;  // register qubits per pass stage (QSIM_PASS_R=5 selects 32-amplitude groups)
     int pass_k = LP_MAX_K;  // tile qubits of the relabelling pass (QSIM_LPASS_K = 9..12)
     size_t amp_bytes = 16;
@@ -947,8 +950,11 @@ int qsim_destroy(qsim_state *s) {
     if (s->stream) cudaStreamSynchronize(s->stream);
     if (s->comm_stream) cudaStreamSynchronize(s->comm_stream);
     if (s->comm) ncclCommDestroy(s->comm);
-    for (auto &sh : s->shards)
+    for (auto &sh : s->shards) {
         if (sh.amps) cudaFree(sh.amps);
+        if (sh.amps2) cudaFree(sh.amps2);
+    }
+    if (s->d_oor) cudaFree(s->d_oor);
     for (int k = 0; k < 2; ++k) {
         if (s->stage[k]) cudaFree(s->stage[k]);
         if (s->ev_recv[k]) cudaEventDestroy(s->ev_recv[k]);
@@ -1103,6 +1109,12 @@ int qsim_create_ex(const qsim_config *cfg, qsim_state **out) {
     s->transport = transport;
     s->rank = transport == QSIM_TRANSPORT_NCCL ? cfg->rank : 0;
     s->fuse = cfg->fuse;
+    s->a_policy = cfg->a_policy == QSIM_A_POLICY_LAZY ? QSIM_A_POLICY_LAZY : QSIM_A_POLICY_EXACT;
+    if (cfg->a_policy != QSIM_A_POLICY_EXACT && cfg->a_policy != QSIM_A_POLICY_LAZY) {
+        delete s;
+        set_error("unknown a_policy");
+        return QSIM_EINVAL;
+    }
     if (const char *pr = getenv("QSIM_PASS_R")) s->pass_r = (atoi(pr) == 4) ? 4 : 5;
     if (const char *lk = getenv("QSIM_LPASS_K")) s->pass_k = std::max(LP_MIN_K, std::min(LP_MAX_K, atoi(lk)));
     s->amp_bytes = s->enc == QSIM_ENC_FP64 ? 16 : 2;
@@ -1524,6 +1536,8 @@ int qsim_get_stats(qsim_state *s, qsim_stats *out) {
             t.exchange_bytes += x.exchange_bytes;
             t.stages += x.stages;
             t.jit_passes += x.jit_passes;
+            t.a_rescales = std::max(t.a_rescales, x.a_rescales);  // per gate, the same on every member
+            t.a_dense = std::max(t.a_dense, x.a_dense);
         }
         *out = t;
         return QSIM_OK;
@@ -2200,7 +2214,9 @@ namespace qsim {
 
 // Exact global bounds of the post-gate magnitudes (reading R-A4), then the
 // decode-apply-encode sweep with those bounds.
-static int dense_gate_a(qsim_state *s, const PlanOp &o, const double *u) {
+// the exact policy's two phases (reading R-A4) from the shards' codes; aout: the
+// out-of-place target (lazy policy) or in place
+static int dense_gate_a_exact(qsim_state *s, const PlanOp &o, const double *u, bool out_of_place) {
     // phase 1 on every shard: (min, -max) of the post-gate |z|^2 merged on the
     // device; across ranks one ncclAllReduce(min); the next tables are built
     // on the device from the result -- no host round trip per gate
@@ -2226,6 +2242,7 @@ static int dense_gate_a(qsim_state *s, const PlanOp &o, const double *u) {
     for (auto &sh : s->shards) {
         AGateParams p{};
         fill_agate(p, s, sh, o, u);
+        if (out_of_place) p.aout = sh.amps2;
         prof_begin(s);
         launch_apply_a(p, s->atab, s->stream);
         prof_end(s, QSIM_K_A_APPLY, std::ldexp(2.0 * (double)s->amp_bytes, s->nl));
@@ -2234,13 +2251,59 @@ static int dense_gate_a(qsim_state *s, const PlanOp &o, const double *u) {
     }
     s->r_stale = true;  // (r0, r1) now live in the device tables only
     RC(atables_commit_next(s->atab, s->stream));
+    s->st.a_rescales++;
     CU(cudaGetLastError());
     return QSIM_OK;
 }
 
-// Consecutive diagonal gates [i, j) as one sweep per shard (k_diag_run_a):
-// each gate contributes the integer b1 steps it would add alone, so the
-// codes equal gate-by-gate application bit for bit (mod 256 addition).
+// Lazy policy (reading R-A25): one out-of-place pass with the kept tables,
+// which also certifies that every output stayed within one step of (r0, r1);
+// if one left, the exact policy runs from the (intact) input codes.  Then the
+// two code buffers swap.
+static int dense_gate_a_lazy(qsim_state *s, const PlanOp &o, const double *u) {
+    for (auto &sh : s->shards)
+        if (!sh.amps2) {
+            if (cudaMalloc(&sh.amps2, s->alloc_amps * s->amp_bytes) != cudaSuccess) {
+                cudaGetLastError();
+                set_error("lazy A policy: the second code buffer (" + std::to_string(s->alloc_amps * s->amp_bytes) +
+                          " B per shard) does not fit");
+                return QSIM_ENOMEM;
+            }
+            CU(cudaMemsetAsync(sh.amps2, 0, s->alloc_amps * s->amp_bytes, s->stream));
+        }
+    if (!s->d_oor) CU(cudaMalloc(&s->d_oor, sizeof(int32_t)));
+    RC(sync_bounds(s));
+    bool rescale = !(s->r1 > s->r0);  // degenerate kept bounds: d = 0, any other magnitude leaves them
+    if (!rescale) {
+        CU(cudaMemsetAsync(s->d_oor, 0, sizeof(int32_t), s->stream));
+        for (auto &sh : s->shards) {
+            AGateParams p{};
+            fill_agate(p, s, sh, o, u);
+            p.aout = sh.amps2;
+            p.oor = s->d_oor;
+            prof_begin(s);
+            launch_apply_a_lazy(p, s->atab, s->stream);
+            prof_end(s, QSIM_K_A_APPLY, std::ldexp(2.0 * (double)s->amp_bytes, s->nl));
+            s->st.kernels++;
+            s->st.hbm_bytes += std::ldexp(2.0 * (double)s->amp_bytes, s->nl);
+        }
+        int32_t h = 0;
+        if (s->transport == QSIM_TRANSPORT_NCCL)
+            NC(ncclAllReduce(s->d_oor, s->d_oor, 1, ncclInt32, ncclMax, s->comm, s->stream));
+        CU(cudaMemcpyAsync(&h, s->d_oor, sizeof(h), cudaMemcpyDeviceToHost, s->stream));
+        CU(cudaStreamSynchronize(s->stream));
+        rescale = h != 0;
+    }
+    if (rescale) RC(dense_gate_a_exact(s, o, u, true));
+    for (auto &sh : s->shards) std::swap(sh.amps, sh.amps2);
+    return QSIM_OK;
+}
+
+static int dense_gate_a(qsim_state *s, const PlanOp &o, const double *u) {
+    s->st.a_dense++;
+    if (s->a_policy == QSIM_A_POLICY_LAZY) return dense_gate_a_lazy(s, o, u);
+    return dense_gate_a_exact(s, o, u, false);
+}
 static int diag_run_a(qsim_state *s, const std::vector<PlanOp> &run, const std::vector<const double *> &us, size_t i,
                       size_t j) {
     for (auto &sh : s->shards) {

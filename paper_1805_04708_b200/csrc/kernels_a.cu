@@ -683,11 +683,24 @@ __device__ __forceinline__ float a_rcp(float x) {
 // 2e-4 for the polynomial and the roundings.  A passing angle test also
 // proves |z| > 0.99 mf >= 1.445e-4 S, so S > 7e-9 (checked per pair) rules
 // out the special zero.
-__device__ __forceinline__ uint32_t a_encode_f(const AEncF &ce, float2 z, float limm, float KE, float eS, bool &ok) {
+template <bool LAZY>
+__device__ __forceinline__ uint32_t a_encode_f(const AEncF &ce, float2 z, float errm, float KE, float eS, bool &ok,
+                                              bool &oor) {
     const float m2 = fmaf(z.x, z.x, z.y * z.y);
     const float rs = a_rsqrt(m2);
     const float mf = m2 > 0.f ? m2 * rs : 0.f;
-    const float t = fmaf(mf, ce.s1, ce.s0);
+    float t = fmaf(mf, ce.s1, ce.s0);
+    bool edge = false;
+    // |z| certainly below 1e-12: the special zero; certainly above: intermediate (reading R-A5)
+    const bool zero = fmaf(mf, 1.0000005f, eS) < 0.99999e-12f;
+    const bool inter = fmaf(mf, 0.9999995f, -eS) > 1.00001e-12f;
+    if (LAZY) {
+        // kept bounds: one step (1 in t) of slack on each side, clamped to the end codes;
+        // certainly outside -> rescale; within errm of the slack's edge -> fp64 decides
+        oor = inter & ((t < -1.f - errm) | (t > 254.f + errm));
+        edge = (fabsf(t + 1.f) <= errm) | (fabsf(t - 254.f) <= errm);
+        t = fminf(fmaxf(t, 0.f), 253.f);
+    }
     const float tm = t + (A_MAGIC + 129.f);
     const float frm = t - (tm - (A_MAGIC + 129.f));
     const float w = z.y * a_rcp(mf + fabsf(z.x));
@@ -695,10 +708,7 @@ __device__ __forceinline__ uint32_t a_encode_f(const AEncF &ce, float2 z, float 
     const float q = (z.x < 0.f) ? copysignf(128.f, z.y) - p : p;
     const float ta = q + A_MAGIC;
     const float fra = q - (ta - A_MAGIC);
-    // |z| certainly below 1e-12: the special zero; certainly above: intermediate (reading R-A5)
-    const bool zero = fmaf(mf, 1.0000005f, eS) < 0.99999e-12f;
-    const bool inter = fmaf(mf, 0.9999995f, -eS) > 1.00001e-12f;
-    ok = zero | (inter & (fabsf(frm) < limm) & (fmaf(KE, rs, fabsf(fra)) < 0.4998f));
+    ok = zero | (inter & !edge & (fabsf(frm) < 0.5f - errm) & (fmaf(KE, rs, fabsf(fra)) < 0.4998f));
     return zero ? 0x0080u : __byte_perm(__float_as_uint(tm), __float_as_uint(ta), 0x0040);
 }
 
@@ -713,7 +723,7 @@ struct AFail {
     uint32_t codes, pad;
 };
 constexpr int A_QN = 32;
-template <int UK>
+template <int UK, bool LAZY>
 __device__ __noinline__ void a_flush(const AGateParams *pp, const ATabData *cur, const ATabData *nxt,
                                      const AFail *q, int n) {
     __syncwarp();  // the queued units' provisional stores and the entries are visible
@@ -730,7 +740,15 @@ __device__ __noinline__ void a_flush(const AGateParams *pp, const ATabData *cur,
             for (int i = 0; i < 8; ++i) u[i] = pp->u[i];
             a_gate2u<UK>(u, x, y);
         }
-        uint16_t *a = reinterpret_cast<uint16_t *>(pp->a);
+        if (LAZY) {  // reading R-A25: outside [r0 - d, r1 + d] -> the gate rescales
+            const double r0 = __ldg(&cur->r0), r1 = __ldg(&cur->r1), d = (r1 - r0) / 253.0;
+            const double lo = r0 - d, hi = r1 + d;
+            const double mx = a_m2(x), my = a_m2(y);
+            const bool ox = is_inter(mx) && (mx < (lo > 0.0 ? lo * lo : 0.0) || mx > hi * hi);
+            const bool oy = is_inter(my) && (my < (lo > 0.0 ? lo * lo : 0.0) || my > hi * hi);
+            if (ox || oy) atomicOr(pp->oor, 1);
+        }
+        uint16_t *a = reinterpret_cast<uint16_t *>(pp->aout ? pp->aout : pp->a);
         a[i0] = (uint16_t)g.encode(x);
         a[i0 + (1ull << pp->t)] = (uint16_t)g.encode(y);
     }
@@ -1119,7 +1137,7 @@ void launch_tables_next(const double *acc, ATables *t, cudaStream_t s) {
 // the certified fallback per failing pair (the warp queue, a_flush).  The
 // grid-stride loop is warp-uniform (lanes past the end idle) so that the
 // queue's votes see the whole warp.
-template <int TL, bool CTRL, int UK>
+template <int TL, bool CTRL, int UK, bool LAZY>
 __global__ void __launch_bounds__(A_THREADS, A_DENSE_MINB) k_apply_a(const __grid_constant__ AGateParams p,
                                                                      const ATabData *__restrict__ cur,
                                                                      const ATabData *__restrict__ nxt,
@@ -1131,8 +1149,10 @@ __global__ void __launch_bounds__(A_THREADS, A_DENSE_MINB) k_apply_a(const __gri
     AFail *q = qall[threadIdx.x >> 5];
     int qn = 0;  // warp-uniform
     AEncF ce;
-    ce.init(nxt);
+    ce.init(nxt);  // LAZY: nxt = cur (the kept bounds)
     uint16_t *a = reinterpret_cast<uint16_t *>(p.a);
+    uint16_t *ao = reinterpret_cast<uint16_t *>(p.aout ? p.aout : p.a);
+    bool oor_any = false;
     const uint64_t units = (p.nl >= 4) ? (1ull << (p.nl - 4)) : 1ull;
     const uint64_t lowm = (1ull << U::LOWB) - 1ull;
     const uint64_t chi = p.cmask & ~lowm;
@@ -1143,6 +1163,10 @@ __global__ void __launch_bounds__(A_THREADS, A_DENSE_MINB) k_apply_a(const __gri
     const uint32_t lt = (1u << lane) - 1u;
     for (uint64_t vb = (uint64_t)blockIdx.x * A_THREADS + (threadIdx.x & ~31u); vb < units;
          vb += (uint64_t)gridDim.x * A_THREADS) {
+        if (LAZY) {  // an output left the kept range somewhere: this pass is discarded, stop early
+            int f = lane == 0 ? *reinterpret_cast<volatile int32_t *>(p.oor) : 0;
+            if (__shfl_sync(0xffffffffu, f, 0)) break;
+        }
         const uint64_t v = vb + (uint64_t)lane;
         uint32_t fail = 0, selm = 0;
         uint32_t c[16];
@@ -1163,11 +1187,12 @@ __global__ void __launch_bounds__(A_THREADS, A_DENSE_MINB) k_apply_a(const __gri
                 if (sel) a_gate_fu<UK>(uf, x, y);
                 const float S = ra + rb;
                 const float E = A_KF * S;
-                const float limm = 0.5f - fmaf(S, ce.kS, fmaf(E, ce.kE, ce.C0)), KE = 73.f * E;
+                const float errm = fmaf(S, ce.kS, fmaf(E, ce.kE, ce.C0)), KE = 73.f * E;
                 const float eS = 1.4145f * E;
-                bool okx, oky;
-                uint32_t cx = a_encode_f(ce, x, limm, KE, eS, okx);
-                uint32_t cy = a_encode_f(ce, y, limm, KE, eS, oky);
+                bool okx, oky, ox, oy;
+                uint32_t cx = a_encode_f<LAZY>(ce, x, errm, KE, eS, okx, ox);
+                uint32_t cy = a_encode_f<LAZY>(ce, y, errm, KE, eS, oky, oy);
+                if (LAZY) oor_any |= (ox & (!CTRL || sel)) | (oy & (!CTRL || sel));
                 if (CTRL) {  // an unselected zero code stays the exact zero special
                     const bool zx = (ra == 0.f) & !sel, zy = (rb == 0.f) & !sel;
                     cx = zx ? 0x0080u : cx;
@@ -1181,7 +1206,11 @@ __global__ void __launch_bounds__(A_THREADS, A_DENSE_MINB) k_apply_a(const __gri
                 nc[j1] = cy;
                 fail |= (uint32_t)!ok << k;
             }
-            U::store(a, s0, p.t, nc);  // provisional for the failing pairs
+            U::store(ao, s0, p.t, nc);  // provisional for the failing pairs
+        }
+        if (LAZY && __any_sync(0xffffffffu, oor_any)) {
+            if (lane == 0) atomicOr(p.oor, 1);
+            break;
         }
         if (__any_sync(0xffffffffu, fail != 0)) {
 #pragma unroll
@@ -1191,7 +1220,7 @@ __global__ void __launch_bounds__(A_THREADS, A_DENSE_MINB) k_apply_a(const __gri
                 if (bal) {
                     const int tot = __popc(bal);
                     if (qn + tot > A_QN) {
-                        a_flush<UK>(&p, cur, nxt, q, qn);
+                        a_flush<UK, LAZY>(&p, cur, nxt, q, qn);
                         qn = 0;
                     }
                     if (f) {
@@ -1206,43 +1235,46 @@ __global__ void __launch_bounds__(A_THREADS, A_DENSE_MINB) k_apply_a(const __gri
             }
         }
     }
-    if (qn) a_flush<UK>(&p, cur, nxt, q, qn);
+    if (qn) a_flush<UK, LAZY>(&p, cur, nxt, q, qn);
 }
 
-template <int TL, bool CTRL, int UK>
+template <int TL, bool CTRL, int UK, bool LAZY>
 static void launch_apply_tl(const AGateParams &p, const ATables *t, int grid, cudaStream_t s) {
     static std::atomic<uint64_t> attr{0};
-    a_dense_attr((const void *)k_apply_a<TL, CTRL, UK>, attr);
-    k_apply_a<TL, CTRL, UK><<<grid, A_THREADS, sizeof(AFTab), s>>>(p, tcur(t), tnext(t), fcur(t));
+    a_dense_attr((const void *)k_apply_a<TL, CTRL, UK, LAZY>, attr);
+    // LAZY: encode with the current tables (the kept bounds)
+    k_apply_a<TL, CTRL, UK, LAZY><<<grid, A_THREADS, sizeof(AFTab), s>>>(p, tcur(t), LAZY ? tcur(t) : tnext(t), fcur(t));
 }
-template <int TL, int UK>
+template <int TL, int UK, bool LAZY>
 static void launch_apply_c(const AGateParams &p, const ATables *t, int grid, cudaStream_t s) {
     if (p.cmask)
-        launch_apply_tl<TL, true, UK>(p, t, grid, s);
+        launch_apply_tl<TL, true, UK, LAZY>(p, t, grid, s);
     else
-        launch_apply_tl<TL, false, UK>(p, t, grid, s);
+        launch_apply_tl<TL, false, UK, LAZY>(p, t, grid, s);
 }
-template <int UK>
+template <int UK, bool LAZY>
 static void launch_apply_k(const AGateParams &p, const ATables *t, int grid, cudaStream_t s) {
     switch (p.t < 4 ? p.t : 4) {
-        case 0: launch_apply_c<0, UK>(p, t, grid, s); break;
-        case 1: launch_apply_c<1, UK>(p, t, grid, s); break;
-        case 2: launch_apply_c<2, UK>(p, t, grid, s); break;
-        case 3: launch_apply_c<3, UK>(p, t, grid, s); break;
-        default: launch_apply_c<4, UK>(p, t, grid, s); break;
+        case 0: launch_apply_c<0, UK, LAZY>(p, t, grid, s); break;
+        case 1: launch_apply_c<1, UK, LAZY>(p, t, grid, s); break;
+        case 2: launch_apply_c<2, UK, LAZY>(p, t, grid, s); break;
+        case 3: launch_apply_c<3, UK, LAZY>(p, t, grid, s); break;
+        default: launch_apply_c<4, UK, LAZY>(p, t, grid, s); break;
     }
 }
-
-void launch_apply_a(const AGateParams &p0, const ATables *t, cudaStream_t s) {
+template <bool LAZY>
+static void launch_apply_any(const AGateParams &p0, const ATables *t, cudaStream_t s) {
     const AGateParams p = a_dense_params(p0);
     const uint64_t units = (p.nl >= 4) ? (1ull << (p.nl - 4)) : 1ull;
     const int grid = a_dense_grid(units);
     switch (a_ukind(p.u)) {
-        case 1: launch_apply_k<1>(p, t, grid, s); break;
-        case 2: launch_apply_k<2>(p, t, grid, s); break;
-        default: launch_apply_k<0>(p, t, grid, s); break;
+        case 1: launch_apply_k<1, LAZY>(p, t, grid, s); break;
+        case 2: launch_apply_k<2, LAZY>(p, t, grid, s); break;
+        default: launch_apply_k<0, LAZY>(p, t, grid, s); break;
     }
 }
+void launch_apply_a(const AGateParams &p, const ATables *t, cudaStream_t s) { launch_apply_any<false>(p, t, s); }
+void launch_apply_a_lazy(const AGateParams &p, const ATables *t, cudaStream_t s) { launch_apply_any<true>(p, t, s); }
 
 // ---------------------------------------------------------------- fast paths
 static int phase_steps(double ur, double ui) {

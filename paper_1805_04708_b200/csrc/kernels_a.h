@@ -65,6 +65,10 @@ struct AGateParams {
     // max(|u00|, |u11|), max(|u01|, |u10|) from above, a / b their nominal values
     float uf[8];
     float mA, mB, ma, mb;
+    // lazy bounds (reading R-A25): codes are written to aout (out of place,
+    // nullptr = in place); an output magnitude outside [r0 - d, r1 + d] sets *oor
+    void *aout;
+    int32_t *oor;
 };
 struct ACollapseParams {
     void *a;
@@ -85,6 +89,9 @@ void launch_tables_next(const double *acc, ATables *t, cudaStream_t s);
 void a_bounds_debug_print();  // debug build (-DQSIM_ABND_DEBUG): screen counters of k_bounds_a
 // phase 2: decode (current tables), apply, encode (next tables)
 void launch_apply_a(const AGateParams &p, const ATables *t, cudaStream_t s);
+// the lazy policy's one pass (reading R-A25): decode, apply, encode with the CURRENT
+// tables into p.aout, *p.oor |= some intermediate output left [r0 - d, r1 + d]
+void launch_apply_a_lazy(const AGateParams &p, const ATables *t, cudaStream_t s);
 // diagonal / anti-diagonal gates: b1 shifts and code moves, bounds unchanged
 void launch_fast_a(const AGateParams &p, const ATables *t, cudaStream_t s);
 // A run of consecutive diagonal gates in one sweep: each gate's b1 step

@@ -159,6 +159,28 @@ def table4_adder():
     return rows
 
 
+def cfg4_lazy():
+    """NEXT-4: config 4 at N = 33 under the lazy-bounds A policy (reading R-A25)
+    vs the exact policy: device time, dense gates that rescaled, fidelity
+    against E (same circuit, E run on the same GPU)."""
+    n = 33
+    circ = C.config(3, n=n)
+    rows = []
+    with q.State(n, q.ENC_FP64, 1) as e:
+        e.apply_circuit(circ)
+        e.sync()
+        for pol in (q.A_POLICY_EXACT, q.A_POLICY_LAZY):
+            with q.State(n, q.ENC_ADAPTIVE2, 1, a_policy=pol) as a:
+                dev, wall, prof, st = run(a, circ, warm=False)
+                ae = a.overlap(e)
+                aa = a.overlap(a).real
+                ee = e.overlap(e).real
+            rows.append(summary("cfg4_" + ("lazy" if pol else "exact"), circ, dev, wall, prof, st,
+                                fidelity_vs_E=abs(ae) ** 2 / (aa * ee), norm_A=aa,
+                                dense=st["a_dense"], rescaled=st["a_rescales"]))
+    return rows
+
+
 def cfg4_trend():
     """Config-4 fidelity and norm drift of A against E as N grows (10 layers)."""
     rows = []
@@ -174,7 +196,7 @@ def cfg4_trend():
     return rows
 
 
-ROWS = {"table4_adder": table4_adder, "cfg4_trend": cfg4_trend, "cfg3_n33": cfg3_n33, "cfg4_n33": cfg4_n33, "cfg5_n32": cfg5_n32, "s1_hwall": s1_hwall, "s2_ghz": s2_ghz}
+ROWS = {"cfg4_lazy": cfg4_lazy, "table4_adder": table4_adder, "cfg4_trend": cfg4_trend, "cfg3_n33": cfg3_n33, "cfg4_n33": cfg4_n33, "cfg5_n32": cfg5_n32, "s1_hwall": s1_hwall, "s2_ghz": s2_ghz}
 want = sys.argv[1:] or list(ROWS)
 out = []
 for name in want:
