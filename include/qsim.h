@@ -176,6 +176,17 @@ int qsim_apply_swap(qsim_state *s, int q1, int q2);
  * validated before any is applied; EINVAL / ENOTUNITARY name the index. */
 int qsim_apply_circuit(qsim_state *s, const qsim_gate *gates, size_t ngates);
 
+/* The whole circuit in ONE kernel launch (the
+ * latency-bound small states): the state lives in the distributed shared
+ * memory of an 8-CTA thread-block cluster, each gate is one sweep over the
+ * pairs (Eq. NUM2 with controls) followed by a cluster
+ * barrier; SWAP records relabel the qubit map.  One launch per 1024 gate
+ * records.  E encoding, one shard on one device, 4 <= N <= 16 (EINVAL /
+ * EUNSUPPORTED otherwise).  Same results as
+ * qsim_apply_circuit up to fp reassociation.  Stream-ordered like
+ * qsim_apply_circuit. */
+int qsim_apply_circuit_persistent(qsim_state *s, const qsim_gate *gates, size_t ngates);
+
 /* ---- read-out (a10, a11) ------------------------------------------------- */
 
 /* Sum_i |a_i|^2 (Eq. STAT1), decoded amplitudes for A. */

@@ -96,7 +96,7 @@ EXPORTS = (
     "qsim_aux_amplitudes", "qsim_aux_num_vars", "qsim_set_qubit_map",
     "qsim_asm_parse", "qsim_asm_info", "qsim_asm_get_op", "qsim_asm_destroy", "qsim_asm_run",
     "qsim_asm_result_get", "qsim_asm_result_destroy",
-    "qsim_overlap", "qsim_magnitude_range", "qsim_get_bounds", "qsim_apply_matrix", "qsim_jit_sync", "qsim_jit_shutdown", "qsim_graph_begin", "qsim_graph_end", "qsim_graph_launch", "qsim_graph_destroy",
+    "qsim_overlap", "qsim_apply_circuit_persistent", "qsim_magnitude_range", "qsim_get_bounds", "qsim_apply_matrix", "qsim_jit_sync", "qsim_jit_shutdown", "qsim_graph_begin", "qsim_graph_end", "qsim_graph_launch", "qsim_graph_destroy",
 )
 
 if not os.path.exists(_LIB_PATH):
@@ -150,6 +150,7 @@ _lib.qsim_set_codes.argtypes = [_P, ctypes.POINTER(ctypes.c_int8), ctypes.c_doub
 _lib.qsim_sync.argtypes = [_P]
 _lib.qsim_overlap.argtypes = [_P, _P, _dp]
 _lib.qsim_magnitude_range.argtypes = [_P, _dp, _dp]
+_lib.qsim_apply_circuit_persistent.argtypes = [_P, ctypes.POINTER(qsim_gate), ctypes.c_size_t]
 _lib.qsim_get_bounds.argtypes = [_P, _dp, _dp]
 _lib.qsim_apply_matrix.argtypes = [_P, _dp, _ip, ctypes.c_int]
 _lib.qsim_jit_sync.argtypes = []
@@ -265,6 +266,11 @@ def qsim_apply_gate(h, u, target, controls=()):
     u8 = np.ascontiguousarray(np.asarray(u, dtype=np.complex128).reshape(2, 2)).view(np.float64).reshape(8)
     c = (ctypes.c_int * 2)(*(list(controls) + [0, 0])[:2])
     _check(_lib.qsim_apply_gate(h, _dptr(u8), target, c, len(controls)))
+
+
+def qsim_apply_circuit_persistent(h, circuit):
+    arr, n = circuit if isinstance(circuit, tuple) else pack_gates(circuit)
+    _check(_lib.qsim_apply_circuit_persistent(h, arr, n))
 
 
 def qsim_apply_swap(h, q1, q2):
@@ -593,6 +599,11 @@ class State:
 
     def apply_circuit(self, circuit):
         qsim_apply_circuit(self.h, circuit)
+        return self
+
+    def apply_circuit_persistent(self, circuit):
+        """The whole circuit in one cluster kernel (qsim_apply_circuit_persistent)."""
+        qsim_apply_circuit_persistent(self.h, circuit)
         return self
 
     def norm(self):

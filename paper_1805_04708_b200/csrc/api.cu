@@ -72,6 +72,8 @@ struct qsim_state {
     qsim::QGroup *group = nullptr;  // QSIM_TRANSPORT_DEVICES: this handle drives P member handles
     int a_policy = 0;               // QSIM_A_POLICY_*
     int32_t *d_oor = nullptr;       // lazy policy: "an output left the kept range" flag
+    PersistGate *d_pg = nullptr, *h_pg = nullptr;  // qsim_apply_circuit_persistent: gate records
+    size_t pg_cap = 0;
     int pass_r = 4;  // register qubits per pass stage (QSIM_PASS_R=5 selects 32-amplitude groups)
     int pass_k = LP_MAX_K;  // tile qubits of the relabelling pass (QSIM_LPASS_K = 9..12)
     size_t amp_bytes = 16;
@@ -955,6 +957,8 @@ int qsim_destroy(qsim_state *s) {
         if (sh.amps2) cudaFree(sh.amps2);
     }
     if (s->d_oor) cudaFree(s->d_oor);
+    if (s->d_pg) cudaFree(s->d_pg);
+    if (s->h_pg) cudaFreeHost(s->h_pg);
     for (int k = 0; k < 2; ++k) {
         if (s->stage[k]) cudaFree(s->stage[k]);
         if (s->ev_recv[k]) cudaEventDestroy(s->ev_recv[k]);
@@ -1244,6 +1248,68 @@ int qsim_apply_circuit(qsim_state *s, const qsim_gate *gates, size_t ngates) {
     std::vector<PlanOp> ops;
     s->pl.plan(gates, ngates, ops, true);
     return execute(s, gates, ngates, ops);
+}
+
+int qsim_apply_circuit_persistent(qsim_state *s, const qsim_gate *gates, size_t ngates) {
+    if (!s || (!gates && ngates)) {
+        set_error("null argument");
+        return QSIM_EINVAL;
+    }
+    if (s->group || s->P != 1 || s->enc != QSIM_ENC_FP64 || s->capturing) {
+        set_error("qsim_apply_circuit_persistent: one E shard on one device, outside graph capture");
+        return QSIM_EUNSUPPORTED;
+    }
+    if (s->n < PERSIST_MIN_N || s->n > PERSIST_MAX_N) {
+        set_error("qsim_apply_circuit_persistent: N must be in [" + std::to_string(PERSIST_MIN_N) + ", " +
+                  std::to_string(PERSIST_MAX_N) + "] (the state lives in one cluster's shared memory)");
+        return QSIM_EINVAL;
+    }
+    RC(validate_gates(s->n, gates, ngates, true));
+    if (!ngates) return QSIM_OK;
+    cudaSetDevice(s->dev);
+    if (ngates > s->pg_cap) {
+        CU(cudaStreamSynchronize(s->stream));
+        if (s->d_pg) cudaFree(s->d_pg);
+        if (s->h_pg) cudaFreeHost(s->h_pg);
+        s->d_pg = nullptr;
+        s->h_pg = nullptr;
+        s->pg_cap = 0;
+        if (cudaMalloc(&s->d_pg, ngates * sizeof(PersistGate)) != cudaSuccess ||
+            cudaMallocHost(&s->h_pg, ngates * sizeof(PersistGate)) != cudaSuccess) {
+            cudaGetLastError();
+            set_error("qsim_apply_circuit_persistent: gate buffer allocation failed");
+            return QSIM_ENOMEM;
+        }
+        s->pg_cap = ngates;
+    }
+    CU(cudaStreamSynchronize(s->stream));  // the pinned staging buffer is reused
+    // logical -> physical through the qubit map; SWAP records relabel it (0 bytes)
+    int ng = 0;
+    for (size_t k = 0; k < ngates; ++k) {
+        const qsim_gate &g = gates[k];
+        if (g.kind == QSIM_GATE_SWAP) {
+            s->pl.swap_bits(s->pl.pos[g.target], s->pl.pos[g.target2]);
+            continue;
+        }
+        PersistGate &p = s->h_pg[ng++];
+        std::memcpy(p.u, g.u, sizeof(p.u));
+        p.t = s->pl.pos[g.target];
+        p.cmask = 0;
+        for (int c = 0; c < g.ncontrols; ++c) p.cmask |= 1u << s->pl.pos[g.controls[c]];
+    }
+    CU(cudaMemcpyAsync(s->d_pg, s->h_pg, ng * sizeof(PersistGate), cudaMemcpyHostToDevice, s->stream));
+    for (int k0 = 0; k0 < ng; k0 += PERSIST_MAX_GATES) {  // one launch per PERSIST_MAX_GATES records
+        const int kn = std::min(ng - k0, PERSIST_MAX_GATES);
+        prof_begin(s);
+        if (launch_persist_e(s->shards[0].amps, s->n, s->d_pg + k0, kn, s->stream)) {
+            set_error("qsim_apply_circuit_persistent: cluster launch failed");
+            return QSIM_ECUDA;
+        }
+        prof_end(s, QSIM_K_PASS, std::ldexp(32.0 * kn, s->n), 14.0 * kn * std::ldexp(1.0, s->n));
+        s->st.kernels++;
+    }
+    s->st.gates += (int64_t)ngates;
+    return QSIM_OK;
 }
 
 int qsim_apply_gate(qsim_state *s, const double u[8], int target, const int *controls, int ncontrols) {

@@ -92,6 +92,16 @@ void launch_pack_multi(const void *src, void *out, uint64_t base, uint64_t count
 void launch_unpack_multi(void *dst, const void *in, uint64_t base, uint64_t count, const RemapBlock &blk,
                          const RemapVals &vals, size_t elem, cudaStream_t s);
 
+// ---- single persistent kernel (config 1, persist.cu) ---------------------------
+struct PersistGate {
+    double u[8];
+    int32_t t;       // physical target bit
+    uint32_t cmask;  // physical control bits (full index)
+};
+constexpr int PERSIST_MIN_N = 4, PERSIST_MAX_N = 16;  // 2^(N-3) amplitudes per CTA of an 8-CTA cluster
+constexpr int PERSIST_MAX_GATES = 1024;  // gate records staged in each CTA's shared memory (72 KiB)
+int launch_persist_e(void *a, int n, const PersistGate *g, int ngates, cudaStream_t s);
+
 // ---- reductions (a10) ---------------------------------------------------------
 // Per-shard: out[0] = sum |a|^2, out[1 + q] = sum_{bit q = 1} |a|^2 for local q.
 constexpr int RED_SLOTS = 64;

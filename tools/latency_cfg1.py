@@ -1,6 +1,7 @@
 """BASELINE config 1 (N=14, 200 gates, 256 KiB state: latency-bound, SURVEY.md
 §8(d)): gates/s with one launch per gate, with the fused relabelling pass,
-and with each replayed from a CUDA graph (qsim_graph_*).
+with each replayed from a CUDA graph (qsim_graph_*), and with the single
+persistent cluster kernel (qsim_apply_circuit_persistent).
 
 Timing: wall clock over REPS back-to-back circuits on the library stream,
 synchronised once at each end (so host planning / compilation overlaps the
@@ -59,6 +60,18 @@ for fuse in (0, 1):
                                           "kernels_per_circuit": st["kernels"]}
     g.close()
     s.close()
+# the whole circuit in one persistent cluster kernel (qsim_apply_circuit_persistent)
+s = q.State(n, q.ENC_FP64, 1)
+wall = timed(lambda: s.apply_circuit_persistent(gates), s, reps)
+s.reset_stats()
+s.profile(True)
+s.profile_read()
+s.apply_circuit_persistent(gates)
+prof = s.profile_read()
+s.profile(False)
+out["modes"]["persistent_kernel"] = {"us_per_circuit": wall * 1e6, "gates_per_s": 200 / wall, "kernels_per_circuit": 1,
+                                     "device_us_per_circuit": sum(v["ms"] for v in prof.values()) * 1e3}
+s.close()
 # one host call per gate (qsim_apply_gate), unfused
 s = q.State(n, q.ENC_FP64, 1, fuse=0)
 idx = list(range(len(circ)))
