@@ -234,7 +234,9 @@ int qsim_measure_u(qsim_state *s, int qubit, double u, int *outcome, double *p0_
  * the state.  Event k uses u_k = (splitmix64(seed + k) >> 11) * 2^-53 and is the
  * smallest logical index L with cumsum_{L' <= L} |a_L'|^2 > u_k * norm^2
  * (inverse CDF in logical order).  Needs 8 B x 2^N of scratch (N <= 34);
- * EUNSUPPORTED for the multi-process NCCL transport; EZERONORM for a zero state. */
+ * for the NCCL transport every rank calls it collectively: the ranks'
+ * probability masses are all-reduced into the full distribution and every
+ * rank draws the same events.  EZERONORM for a zero state. */
 int qsim_sample(qsim_state *s, size_t nsamples, uint64_t seed, uint64_t *out);
 
 /* SHORBOX n_x G y (App. B; §5.4):

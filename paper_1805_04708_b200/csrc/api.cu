@@ -459,7 +459,7 @@ static int run_gates_e(qsim_state *s, const std::vector<PlanOp> &run, const std:
 // exchange (a7): swap physical global bit g with local bit l; optionally apply
 // the triggering gate (now on bit l) to each (kept, received) pair on arrival.
 // ============================================================================
-static int exchange(qsim_state *s, const PlanOp &x, const PlanOp *gop, const double *u) {
+static int exchange_impl(qsim_state *s, const PlanOp &x, const PlanOp *gop, const double *u) {
     const int j = x.g - s->nl;
     const int l = x.l;
     const uint64_t half = 1ull << (s->nl - 1);
@@ -526,6 +526,9 @@ static int exchange(qsim_state *s, const PlanOp &x, const PlanOp *gop, const dou
     Shard &sh = s->shards[0];
     const int b = (shard_phys(s, sh) >> j) & 1;
     const int partner = (int)s->ginv[shard_phys(s, sh) ^ (1u << j)];
+    // one profile record for the whole pipeline (transfers included: the
+    // compute stream waits on every chunk's arrival), bytes = sent per direction
+    prof_begin(s);
     CU(cudaEventRecord(s->ev_start, s->stream));
     CU(cudaStreamWaitEvent(s->comm_stream, s->ev_start, 0));
     for (uint64_t c = 0; c < nchunks; ++c) {
@@ -540,15 +543,14 @@ static int exchange(qsim_state *s, const PlanOp &x, const PlanOp *gop, const dou
         CU(cudaStreamWaitEvent(s->stream, s->ev_recv[k], 0));
         XchgParams p{};
         fill(p, sh, b, c, s->stage[k]);
-        prof_begin(s);
         if (s->enc == QSIM_ENC_FP64)
             launch_xchg_e(p, s->stream);
         else
             launch_xchg_a(p, s->atab, s->stream);
-        prof_end(s, QSIM_K_XCHG, (double)C * ab * (gop ? 4.0 : 2.0));
         account();
         CU(cudaEventRecord(s->ev_comp[k], s->stream));
     }
+    prof_end(s, QSIM_K_XCHG, (double)half * ab);
     s->st.exchange_bytes += (double)half * ab;
     s->st.exchanges++;
     CU(cudaGetLastError());
@@ -559,7 +561,7 @@ static int exchange(qsim_state *s, const PlanOp &x, const PlanOp *gop, const dou
 // local l_i) pairs swapped at once.  Shard phi trades its block B(t) (l bits
 // = t) with block B(phi[j]) of the shard phi with j bits := t, for every
 // t != phi[j].  The qubit map was updated by the planner.
-static int remap(qsim_state *s, std::vector<std::pair<int, int>> pairs) {
+static int remap_impl(qsim_state *s, std::vector<std::pair<int, int>> pairs) {
     std::sort(pairs.begin(), pairs.end(), [](const std::pair<int, int> &x, const std::pair<int, int> &y) {
         return x.second < y.second;  // by local bit
     });
@@ -670,35 +672,85 @@ static int remap(qsim_state *s, std::vector<std::pair<int, int>> pairs) {
     // each of the 2^m - 1 blocks with its partner (grouped sends / receives)
     Shard &sh = s->shards[0];
     const uint32_t pa = shard_phys(s, sh), ta = jval(pa);
-    uint64_t C = 1;
-    while (C * 2 * (nt - 1) <= s->chunk_amps && C * 2 <= nblock) C *= 2;
+    uint64_t C = 1;  // two chunk rounds in flight: each uses half of a staging buffer
+    while (C * 2 * (nt - 1) * 2 <= s->chunk_amps && C * 2 <= nblock) C *= 2;
     const uint64_t nch = nblock / C;
-    char *sendb = (char *)s->stage[0], *recvb = (char *)s->stage[1];
+    // double-buffered pipeline: pack (compute stream) -> grouped sends / receives
+    // with the 2^m - 1 partners (comm stream) -> unpack (compute stream); chunk
+    // c + 2 is packed while chunk c + 1 travels.  Buffer k = c & 1 is one half
+    // of each staging buffer.  Hazards: pack(c + 2) is enqueued after unpack(c),
+    // which waited on the comm group of chunk c (its sends read sendb[k], its
+    // receives wrote recvb[k]); the comm group of chunk c + 2 waits on the event
+    // recorded after pack(c + 2).
+    char *sendb[2] = {(char *)s->stage[0], (char *)s->stage[0] + (size_t)C * (nt - 1) * ab};
+    char *recvb[2] = {(char *)s->stage[1], (char *)s->stage[1] + (size_t)C * (nt - 1) * ab};
     RemapVals vals{};
     for (uint32_t t = 0; t < nt; ++t)
         if (t != ta) vals.v[vals.n++] = t;  // slot p <-> block vals.v[p]
     prof_begin(s);
-    for (uint64_t c = 0; c < nch; ++c) {
-        launch_pack_multi(sh.amps, sendb, c * C, C, blk, vals, ab, s->stream);
+    CU(cudaEventRecord(s->ev_start, s->stream));
+    CU(cudaStreamWaitEvent(s->comm_stream, s->ev_start, 0));
+    auto issue = [&](uint64_t c) -> int {
+        const int k = (int)(c & 1);
+        launch_pack_multi(sh.amps, sendb[k], c * C, C, blk, vals, ab, s->stream);
+        CU(cudaEventRecord(s->ev_comp[k], s->stream));
+        CU(cudaStreamWaitEvent(s->comm_stream, s->ev_comp[k], 0));
         NC(ncclGroupStart());
         int slot = 0;
         for (uint32_t t = 0; t < nt; ++t) {
             if (t == ta) continue;
             const int peer = (int)s->ginv[with_j(pa, t)];
-            NC(ncclSend(sendb + (size_t)slot * C * ab, C * ab, ncclUint8, peer, s->comm, s->stream));
-            NC(ncclRecv(recvb + (size_t)slot * C * ab, C * ab, ncclUint8, peer, s->comm, s->stream));
+            NC(ncclSend(sendb[k] + (size_t)slot * C * ab, C * ab, ncclUint8, peer, s->comm, s->comm_stream));
+            NC(ncclRecv(recvb[k] + (size_t)slot * C * ab, C * ab, ncclUint8, peer, s->comm, s->comm_stream));
             ++slot;
         }
         NC(ncclGroupEnd());
-        launch_unpack_multi(sh.amps, recvb, c * C, C, blk, vals, ab, s->stream);
+        CU(cudaEventRecord(s->ev_recv[k], s->comm_stream));
+        return QSIM_OK;
+    };
+    RC(issue(0));
+    if (nch > 1) RC(issue(1));
+    for (uint64_t c = 0; c < nch; ++c) {
+        const int k = (int)(c & 1);
+        CU(cudaStreamWaitEvent(s->stream, s->ev_recv[k], 0));
+        launch_unpack_multi(sh.amps, recvb[k], c * C, C, blk, vals, ab, s->stream);
         s->st.kernels += 2;
         s->st.hbm_bytes += 4.0 * (double)(nt - 1) * (double)C * ab;
+        if (c + 2 < nch) RC(issue(c + 2));
     }
     prof_end(s, QSIM_K_XCHG, 2.0 * (double)(nt - 1) * (double)nblock * ab);
     s->st.exchange_bytes += (double)(nt - 1) * (double)nblock * ab;
     s->st.exchanges++;
     CU(cudaGetLastError());
     return QSIM_OK;
+}
+
+// A rank that fails inside the exchange pipeline leaves its partners blocked in
+// their sends / receives: abort the communicator so they fail fast;
+// every later collective of this handle then returns QSIM_ECOMM.
+static void comm_abort(qsim_state *s) {
+    if (s->transport == QSIM_TRANSPORT_NCCL && s->comm) {
+        ncclCommAbort(s->comm);
+        s->comm = nullptr;
+    }
+}
+static int exchange(qsim_state *s, const PlanOp &x, const PlanOp *gop, const double *u) {
+    if (s->transport == QSIM_TRANSPORT_NCCL && !s->comm) {
+        set_error("the NCCL communicator was aborted after an earlier error");
+        return QSIM_ECOMM;
+    }
+    const int rc = exchange_impl(s, x, gop, u);
+    if (rc) comm_abort(s);
+    return rc;
+}
+static int remap(qsim_state *s, std::vector<std::pair<int, int>> pairs) {
+    if (s->transport == QSIM_TRANSPORT_NCCL && !s->comm) {
+        set_error("the NCCL communicator was aborted after an earlier error");
+        return QSIM_ECOMM;
+    }
+    const int rc = remap_impl(s, std::move(pairs));
+    if (rc) comm_abort(s);
+    return rc;
 }
 
 // ============================================================================
@@ -1910,9 +1962,9 @@ int qsim_sample(qsim_state *s, size_t nsamples, uint64_t seed, uint64_t *out) {
         return QSIM_EINVAL;
     }
     if (!s || (nsamples && !out)) return QSIM_EINVAL;
-    if (s->transport == QSIM_TRANSPORT_NCCL && s->P > 1) {
-        set_error("qsim_sample: not implemented for the multi-process NCCL transport");
-        return QSIM_EUNSUPPORTED;
+    if (s->transport == QSIM_TRANSPORT_NCCL && !s->comm) {
+        set_error("the NCCL communicator was aborted after an earlier error");
+        return QSIM_ECOMM;
     }
     if (s->n > 34) {
         set_error("qsim_sample needs an 8 B x 2^N probability array (N <= 34)");
@@ -1927,7 +1979,8 @@ int qsim_sample(qsim_state *s, size_t nsamples, uint64_t seed, uint64_t *out) {
     }
     s->st.kernels += 4;
     return sample_logical(amps.data(), bases.data(), (int)amps.size(), s->nl, s->n, s->pl.inv.data(), s->enc, s->atab,
-                          nsamples, seed, out, s->stream);
+                          nsamples, seed, out, s->stream,
+                          s->transport == QSIM_TRANSPORT_NCCL ? (void *)s->comm : nullptr);
 }
 
 int qsim_set_qubit_map(qsim_state *s, const int *pos) {
@@ -2027,21 +2080,22 @@ int qsim_get_amplitudes(qsim_state *s, const uint64_t *idx, size_t m, double *ou
             return QSIM_EINVAL;
         }
     if (!m) return QSIM_OK;
-    // device scratch: offsets + results for m entries
+    // device scratch: offsets + results for m entries.  A local failure must not
+    // skip the NCCL all-reduce the other ranks enter: it is folded
+    // into the reduction as an error count instead.
     uint64_t *d_off = nullptr;
     double *d_val = nullptr;
-    CU(cudaMalloc(&d_off, m * sizeof(uint64_t)));
-    if (cudaMalloc(&d_val, m * 2 * sizeof(double)) != cudaSuccess) {
-        cudaFree(d_off);
-        set_error("cudaMalloc for get_amplitudes");
-        return QSIM_ENOMEM;
-    }
     std::vector<double> res(2 * m, 0.0);
     std::vector<uint64_t> off;
     std::vector<size_t> which;
     int rc = QSIM_OK;
+    if (cudaMalloc(&d_off, m * sizeof(uint64_t)) != cudaSuccess || cudaMalloc(&d_val, m * 2 * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        rc = QSIM_ENOMEM;
+    }
     const uint64_t lmask = (1ull << s->nl) - 1ull;
     for (auto &sh : s->shards) {
+        if (rc) break;
         off.clear();
         which.clear();
         for (size_t k = 0; k < m; ++k) {
@@ -2072,18 +2126,29 @@ int qsim_get_amplitudes(qsim_state *s, const uint64_t *idx, size_t m, double *ou
             res[2 * which[k] + 1] = tmp[2 * k + 1];
         }
     }
-    if (rc == QSIM_OK && s->transport == QSIM_TRANSPORT_NCCL) {
-        double *d_all = nullptr;
-        if (cudaMalloc(&d_all, res.size() * 8) == cudaSuccess) {
-            cudaMemcpyAsync(d_all, res.data(), res.size() * 8, cudaMemcpyHostToDevice, s->stream);
-            if (ncclAllReduce(d_all, d_all, res.size(), ncclFloat64, ncclSum, s->comm, s->stream) != ncclSuccess)
+    if (s->transport == QSIM_TRANSPORT_NCCL) {
+        // chunks of the pre-allocated 4096-double scratch: element 0 = error count,
+        // then up to 4095 values; the same number of chunks on every rank
+        const size_t per = 4095;
+        const size_t nchunk = (res.size() + per - 1) / per;
+        int nerr = 0;
+        for (size_t c = 0; c < std::max<size_t>(nchunk, 1); ++c) {
+            const size_t lo = c * per, cnt = std::min(per, res.size() - std::min(res.size(), lo));
+            s->h_out[0] = rc ? 1.0 : 0.0;
+            std::memcpy(s->h_out + 1, res.data() + lo, cnt * 8);
+            if (!s->comm) {
                 rc = QSIM_ECOMM;
-            cudaMemcpyAsync(res.data(), d_all, res.size() * 8, cudaMemcpyDeviceToHost, s->stream);
+                break;
+            }
+            cudaMemcpyAsync(s->d_out, s->h_out, (cnt + 1) * 8, cudaMemcpyHostToDevice, s->stream);
+            if (ncclAllReduce(s->d_out, s->d_out, cnt + 1, ncclFloat64, ncclSum, s->comm, s->stream) != ncclSuccess)
+                nerr++;
+            cudaMemcpyAsync(s->h_out, s->d_out, (cnt + 1) * 8, cudaMemcpyDeviceToHost, s->stream);
             cudaStreamSynchronize(s->stream);
-            cudaFree(d_all);
-        } else {
-            rc = QSIM_ENOMEM;
+            if (s->h_out[0] != 0.0 && !rc) rc = QSIM_ECOMM;  // another rank failed
+            std::memcpy(res.data() + lo, s->h_out + 1, cnt * 8);
         }
+        if (nerr && !rc) rc = QSIM_ECOMM;
     }
     cudaFree(d_off);
     cudaFree(d_val);

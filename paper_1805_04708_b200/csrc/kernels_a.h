@@ -136,7 +136,8 @@ void launch_codes_from_logical_a(void *a, uint64_t n, uint64_t base, const int *
                                  cudaStream_t s);
 
 int sample_logical(void *const *shard_amps, const uint64_t *shard_base, int nshards, int nl, int nq, const int *inv_host,
-                   int enc, const ATables *at, uint64_t nsamp, uint64_t seed, uint64_t *out_host, cudaStream_t s);
+                   int enc, const ATables *at, uint64_t nsamp, uint64_t seed, uint64_t *out_host, cudaStream_t s,
+                   void *nccl_comm = nullptr);  // NCCL: all-reduce the distribution over the ranks' shards
 
 int shorbox(void *const *shard_amps, const uint64_t *shard_base, int nshards, int nl, int nq, const int *inv_host,
             int enc, int nx, uint64_t G, uint64_t y, cudaStream_t s);

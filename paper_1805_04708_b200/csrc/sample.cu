@@ -10,6 +10,7 @@
 //    running sum exceeds the remaining target.
 // Deterministic for a given state, seed and count.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <cmath>
 #include <cstdint>
@@ -146,7 +147,8 @@ __global__ void __launch_bounds__(256) k_sample(const __grid_constant__ TreeLeve
 }
 
 int sample_logical(void *const *shard_amps, const uint64_t *shard_base, int nshards, int nl, int nq, const int *inv_host,
-                   int enc, const ATables *at, uint64_t nsamp, uint64_t seed, uint64_t *out_host, cudaStream_t s) {
+                   int enc, const ATables *at, uint64_t nsamp, uint64_t seed, uint64_t *out_host, cudaStream_t s,
+                   void *nccl_comm) {
     const uint64_t dim = 1ull << nq;
     std::vector<void *> bufs;
     auto cleanup = [&]() {
@@ -170,6 +172,7 @@ int sample_logical(void *const *shard_amps, const uint64_t *shard_base, int nsha
         return QSIM_ENOMEM;
     }
     cudaMemcpyAsync(d_inv, inv_host, nq * sizeof(int), cudaMemcpyHostToDevice, s);
+    if (nccl_comm) cudaMemsetAsync(p, 0, dim * sizeof(double), s);  // the other ranks' entries stay 0 here
     const uint64_t nshard_amps = 1ull << nl;
     const int grid = 148 * 8;
     for (int r = 0; r < nshards; ++r) {
@@ -179,6 +182,15 @@ int sample_logical(void *const *shard_amps, const uint64_t *shard_base, int nsha
         else
             k_prob_logical_a<<<grid, 256, 0, s>>>((const uint16_t *)shard_amps[r], nshard_amps, shard_base[r], d_inv,
                                                   nq, at->d[at->cur], p);
+    }
+    // NCCL transport: each rank filled its own shard's entries (zeros elsewhere,
+    // the array was cleared); the sum is the whole distribution, exactly, on
+    // every rank -- which then draws the same samples from the same seed
+    if (nccl_comm &&
+        ncclAllReduce(p, p, dim, ncclFloat64, ncclSum, (ncclComm_t)nccl_comm, s) != ncclSuccess) {
+        cleanup();
+        set_error("qsim_sample: ncclAllReduce of the probabilities failed");
+        return QSIM_ECOMM;
     }
     TreeLevels T{};
     T.lv[0] = p;

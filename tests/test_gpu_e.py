@@ -412,6 +412,9 @@ def test_nccl_transport_single_rank():
     assert np.max(np.abs(s.expectations() - oracle.e_expectations(ref, n))) <= TOL
     idx = np.arange(0, 1 << n, 7, dtype=np.uint64)
     assert np.max(np.abs(s.get_amplitudes(idx) - ref[idx.astype(np.int64)])) <= TOL
+    with q.State(n) as loc:  # GENERATE EVENTS through the NCCL path: the same events as one shard
+        loc.apply_circuit(circ)
+        assert np.array_equal(s.sample(500, 9), loc.sample(500, 9))
     out, p0 = s.measure_u(2, 0.4)
     ro, rp0 = oracle.e_measure(ref, n, 2, 0.4)
     assert out == ro and abs(p0 - rp0) <= 1e-12
