@@ -488,7 +488,8 @@ static int exchange_impl(qsim_state *s, const PlanOp &x, const PlanOp *gop, cons
         s->st.kernels++;
         s->st.hbm_bytes += (double)C * ab * (gop ? 4.0 : 2.0);
     };
-    if (s->transport == QSIM_TRANSPORT_LOCAL) {
+    static const bool via_comm = getenv("QSIM_XCHG_VIA_COMM") != nullptr;
+    if (s->transport == QSIM_TRANSPORT_LOCAL && !via_comm) {
         for (auto &sa : s->shards) {
             if ((shard_phys(s, sa) >> j) & 1) continue;
             Shard *sb = nullptr;
@@ -522,36 +523,89 @@ static int exchange_impl(qsim_state *s, const PlanOp &x, const PlanOp *gop, cons
         CU(cudaGetLastError());
         return QSIM_OK;
     }
-    // ---- NCCL: one shard per process, double-buffered chunk pipeline ----
-    Shard &sh = s->shards[0];
-    const int b = (shard_phys(s, sh) >> j) & 1;
-    const int partner = (int)s->ginv[shard_phys(s, sh) ^ (1u << j)];
+    // ---- NCCL (one shard per process): the double-buffered chunk pipeline.
+    // QSIM_XCHG_VIA_COMM=1 runs it with the loopback transport on one GPU --
+    // every shard of this process, device copies on the comm stream standing
+    // in for ncclSend / ncclRecv, per-shard receive buffers -- so its
+    // schedule, events and hazards are tested without a second GPU.
+    // Hazards: a sent chunk's slot is overwritten only by the kernel of that
+    // chunk, which waits on the comm work that sent it; a receive buffer is
+    // reused (chunk c + 2) only after the kernel that read it (ev_comp).
+    const bool nccl = s->transport == QSIM_TRANSPORT_NCCL;
+    const size_t ns = s->shards.size();
+    std::vector<int> bbit(ns);
+    std::vector<size_t> partner_of(ns);
+    for (size_t i = 0; i < ns; ++i) {
+        bbit[i] = (shard_phys(s, s->shards[i]) >> j) & 1;
+        if (!nccl) {
+            const uint32_t want = s->ginv[shard_phys(s, s->shards[i]) ^ (1u << j)];
+            size_t r = 0;
+            while ((uint32_t)s->shards[r].index != want) ++r;
+            partner_of[i] = r;
+        }
+    }
+    char *rbuf = nullptr;  // loopback: per shard and buffer k, one chunk
+    if (!nccl) {
+        if (cudaMalloc(&rbuf, 2 * ns * C * ab) != cudaSuccess) {
+            cudaGetLastError();
+            set_error("exchange (comm path): staging allocation failed");
+            return QSIM_ENOMEM;
+        }
+        if (!s->comm_stream) {
+            CU(cudaStreamCreateWithFlags(&s->comm_stream, cudaStreamNonBlocking));
+            for (int k2 = 0; k2 < 2; ++k2) {
+                CU(cudaEventCreateWithFlags(&s->ev_recv[k2], cudaEventDisableTiming));
+                CU(cudaEventCreateWithFlags(&s->ev_comp[k2], cudaEventDisableTiming));
+            }
+            CU(cudaEventCreateWithFlags(&s->ev_start, cudaEventDisableTiming));
+        }
+    }
+    auto recv_buf = [&](size_t i, int k) -> void * {
+        return nccl ? s->stage[k] : (void *)(rbuf + ((size_t)k * ns + i) * C * ab);
+    };
+    auto send_src = [&](size_t i, uint64_t c) {
+        return (const char *)s->shards[i].amps + ins0(c * C, l) * ab + (bbit[i] ? 0 : ((size_t)1 << l) * ab);
+    };
     // one profile record for the whole pipeline (transfers included: the
     // compute stream waits on every chunk's arrival), bytes = sent per direction
     prof_begin(s);
     CU(cudaEventRecord(s->ev_start, s->stream));
     CU(cudaStreamWaitEvent(s->comm_stream, s->ev_start, 0));
-    for (uint64_t c = 0; c < nchunks; ++c) {
+    int rc = QSIM_OK;
+    for (uint64_t c = 0; c < nchunks && !rc; ++c) {
         const int k = (int)(c & 1);
         if (c >= 2) CU(cudaStreamWaitEvent(s->comm_stream, s->ev_comp[k], 0));
-        const char *src = (const char *)sh.amps + ins0(c * C, l) * ab + (b ? 0 : ((size_t)1 << l) * ab);
-        NC(ncclGroupStart());
-        NC(ncclSend(src, C * ab, ncclUint8, partner, s->comm, s->comm_stream));
-        NC(ncclRecv(s->stage[k], C * ab, ncclUint8, partner, s->comm, s->comm_stream));
-        NC(ncclGroupEnd());
+        if (nccl) {
+            const int partner = (int)s->ginv[shard_phys(s, s->shards[0]) ^ (1u << j)];
+            NC(ncclGroupStart());
+            NC(ncclSend(send_src(0, c), C * ab, ncclUint8, partner, s->comm, s->comm_stream));
+            NC(ncclRecv(s->stage[k], C * ab, ncclUint8, partner, s->comm, s->comm_stream));
+            NC(ncclGroupEnd());
+        } else {
+            for (size_t i = 0; i < ns; ++i)  // shard i's sent half lands in its partner's receive buffer
+                CU(cudaMemcpyAsync(recv_buf(partner_of[i], k), send_src(i, c), C * ab, cudaMemcpyDeviceToDevice,
+                                   s->comm_stream));
+        }
         CU(cudaEventRecord(s->ev_recv[k], s->comm_stream));
         CU(cudaStreamWaitEvent(s->stream, s->ev_recv[k], 0));
-        XchgParams p{};
-        fill(p, sh, b, c, s->stage[k]);
-        if (s->enc == QSIM_ENC_FP64)
-            launch_xchg_e(p, s->stream);
-        else
-            launch_xchg_a(p, s->atab, s->stream);
-        account();
+        for (size_t i = 0; i < ns; ++i) {
+            XchgParams p{};
+            fill(p, s->shards[i], bbit[i], c, recv_buf(i, k));
+            if (s->enc == QSIM_ENC_FP64)
+                launch_xchg_e(p, s->stream);
+            else
+                launch_xchg_a(p, s->atab, s->stream);
+            account();
+        }
         CU(cudaEventRecord(s->ev_comp[k], s->stream));
     }
-    prof_end(s, QSIM_K_XCHG, (double)half * ab);
-    s->st.exchange_bytes += (double)half * ab;
+    if (!nccl) {
+        cudaStreamSynchronize(s->stream);
+        cudaFree(rbuf);
+    }
+    if (rc) return rc;
+    prof_end(s, QSIM_K_XCHG, (double)ns * (double)half * ab);
+    s->st.exchange_bytes += (double)ns * (double)half * ab;
     s->st.exchanges++;
     CU(cudaGetLastError());
     return QSIM_OK;
@@ -590,63 +644,7 @@ static int remap_impl(qsim_state *s, std::vector<std::pair<int, int>> pairs) {
     };
     const uint32_t nt = 1u << m;
     static const bool via_pack = getenv("QSIM_REMAP_VIA_PACK") != nullptr;
-    if (s->transport == QSIM_TRANSPORT_LOCAL && via_pack) {
-        // test path: the NCCL data flow (chunked pack of every foreign block ->
-        // partner's receive slot -> unpack) with device copies standing in for
-        // ncclSend / ncclRecv, so the pack / unpack kernels and the slot / peer
-        // mapping of the NCCL path run on one GPU
-        uint64_t C = 1;
-        while (C * 2 * (nt - 1) <= s->chunk_amps && C * 2 <= nblock) C *= 2;
-        const uint64_t nch = nblock / C;
-        const size_t slot_bytes = (size_t)C * ab, area = slot_bytes * (nt - 1);
-        char *sendall = nullptr, *recvall = nullptr;
-        CU(cudaMalloc(&sendall, area * s->shards.size()));
-        if (cudaMalloc(&recvall, area * s->shards.size()) != cudaSuccess) {
-            cudaFree(sendall);
-            set_error("remap (pack path): staging allocation failed");
-            return QSIM_ENOMEM;
-        }
-        std::vector<RemapVals> vals(s->shards.size());
-        for (size_t i = 0; i < s->shards.size(); ++i) {
-            const uint32_t ta = jval(shard_phys(s, s->shards[i]));
-            vals[i] = RemapVals{};
-            for (uint32_t t = 0; t < nt; ++t)
-                if (t != ta) vals[i].v[vals[i].n++] = t;
-        }
-        auto slot_of = [&](size_t i, uint32_t t) {  // position of block value t among shard i's slots
-            int k = 0;
-            while (vals[i].v[k] != t) ++k;
-            return k;
-        };
-        for (uint64_t c = 0; c < nch; ++c) {
-            for (size_t i = 0; i < s->shards.size(); ++i)
-                launch_pack_multi(s->shards[i].amps, sendall + i * area, c * C, C, blk, vals[i], ab, s->stream);
-            // "send": shard i's slot for block t goes to the shard with j bits t,
-            // which receives it into its slot for block ta(i)
-            for (size_t i = 0; i < s->shards.size(); ++i) {
-                const uint32_t pa = shard_phys(s, s->shards[i]), ta = jval(pa);
-                for (int k = 0; k < vals[i].n; ++k) {
-                    const uint32_t t = vals[i].v[k];
-                    const uint32_t idx = s->ginv[with_j(pa, t)];
-                    size_t r = 0;
-                    while ((uint32_t)s->shards[r].index != idx) ++r;
-                    CU(cudaMemcpyAsync(recvall + r * area + (size_t)slot_of(r, ta) * slot_bytes,
-                                       sendall + i * area + (size_t)k * slot_bytes, slot_bytes,
-                                       cudaMemcpyDeviceToDevice, s->stream));
-                }
-            }
-            for (size_t i = 0; i < s->shards.size(); ++i)
-                launch_unpack_multi(s->shards[i].amps, recvall + i * area, c * C, C, blk, vals[i], ab, s->stream);
-        }
-        CU(cudaStreamSynchronize(s->stream));
-        cudaFree(sendall);
-        cudaFree(recvall);
-        s->st.exchange_bytes += (double)s->shards.size() * (double)(nt - 1) * (double)nblock * ab;
-        s->st.exchanges++;
-        CU(cudaGetLastError());
-        return QSIM_OK;
-    }
-    if (s->transport == QSIM_TRANSPORT_LOCAL) {
+    if (s->transport == QSIM_TRANSPORT_LOCAL && !via_pack) {
         prof_begin(s);
         for (auto &sa : s->shards) {
             const uint32_t pa = shard_phys(s, sa), ta = jval(pa);
@@ -668,58 +666,112 @@ static int remap_impl(qsim_state *s, std::vector<std::pair<int, int>> pairs) {
         CU(cudaGetLastError());
         return QSIM_OK;
     }
-    // ---- NCCL: one shard per process; every chunk round trades one slice of
-    // each of the 2^m - 1 blocks with its partner (grouped sends / receives)
-    Shard &sh = s->shards[0];
-    const uint32_t pa = shard_phys(s, sh), ta = jval(pa);
-    uint64_t C = 1;  // two chunk rounds in flight: each uses half of a staging buffer
+    // ---- the pack / transfer / unpack pipeline: NCCL (one shard per process)
+    // and, as its one-GPU test path (QSIM_REMAP_VIA_PACK with the loopback
+    // transport), every shard of this process with device copies on the comm
+    // stream standing in for the grouped sends / receives -- the same schedule,
+    // buffers, events and slot / peer mapping.  Every chunk round trades one
+    // slice of each of the 2^m - 1 foreign blocks with their owners.
+    // Double-buffered: chunk c + 2 is packed while chunk c + 1 travels; buffer
+    // k = c & 1 is one half of the staging.  Hazards: pack(c + 2) is enqueued on
+    // the compute stream after unpack(c), which waited on the comm work of
+    // chunk c (its sends read sendb[k], its receives wrote recvb[k]); the comm
+    // work of chunk c + 2 waits on the event recorded after pack(c + 2).
+    const bool nccl = s->transport == QSIM_TRANSPORT_NCCL;
+    const size_t ns = s->shards.size();
+    uint64_t C = 1;
     while (C * 2 * (nt - 1) * 2 <= s->chunk_amps && C * 2 <= nblock) C *= 2;
     const uint64_t nch = nblock / C;
-    // double-buffered pipeline: pack (compute stream) -> grouped sends / receives
-    // with the 2^m - 1 partners (comm stream) -> unpack (compute stream); chunk
-    // c + 2 is packed while chunk c + 1 travels.  Buffer k = c & 1 is one half
-    // of each staging buffer.  Hazards: pack(c + 2) is enqueued after unpack(c),
-    // which waited on the comm group of chunk c (its sends read sendb[k], its
-    // receives wrote recvb[k]); the comm group of chunk c + 2 waits on the event
-    // recorded after pack(c + 2).
-    char *sendb[2] = {(char *)s->stage[0], (char *)s->stage[0] + (size_t)C * (nt - 1) * ab};
-    char *recvb[2] = {(char *)s->stage[1], (char *)s->stage[1] + (size_t)C * (nt - 1) * ab};
-    RemapVals vals{};
-    for (uint32_t t = 0; t < nt; ++t)
-        if (t != ta) vals.v[vals.n++] = t;  // slot p <-> block vals.v[p]
-    prof_begin(s);
-    CU(cudaEventRecord(s->ev_start, s->stream));
-    CU(cudaStreamWaitEvent(s->comm_stream, s->ev_start, 0));
+    const size_t slot_bytes = (size_t)C * ab, area = slot_bytes * (nt - 1);
+    char *send_base = nullptr, *recv_base = nullptr;
+    if (nccl) {
+        send_base = (char *)s->stage[0];
+        recv_base = (char *)s->stage[1];
+    } else {
+        if (cudaMalloc(&send_base, 2 * area * ns) != cudaSuccess || cudaMalloc(&recv_base, 2 * area * ns) != cudaSuccess) {
+            cudaGetLastError();
+            if (send_base) cudaFree(send_base);
+            set_error("remap (pack path): staging allocation failed");
+            return QSIM_ENOMEM;
+        }
+        if (!s->comm_stream) {  // the loopback test path borrows the NCCL transport's stream and events
+            CU(cudaStreamCreateWithFlags(&s->comm_stream, cudaStreamNonBlocking));
+            for (int k2 = 0; k2 < 2; ++k2) {
+                CU(cudaEventCreateWithFlags(&s->ev_recv[k2], cudaEventDisableTiming));
+                CU(cudaEventCreateWithFlags(&s->ev_comp[k2], cudaEventDisableTiming));
+            }
+            CU(cudaEventCreateWithFlags(&s->ev_start, cudaEventDisableTiming));
+        }
+    }
+    auto sendb = [&](size_t i, int k) { return send_base + ((size_t)k * ns + i) * area; };
+    auto recvb = [&](size_t i, int k) { return recv_base + ((size_t)k * ns + i) * area; };
+    std::vector<RemapVals> vals(ns);
+    for (size_t i = 0; i < ns; ++i) {
+        const uint32_t ta = jval(shard_phys(s, s->shards[i]));
+        vals[i] = RemapVals{};
+        for (uint32_t t = 0; t < nt; ++t)
+            if (t != ta) vals[i].v[vals[i].n++] = t;  // slot p <-> block vals[i].v[p]
+    }
+    auto slot_of = [&](size_t i, uint32_t t) {  // position of block value t among shard i's slots
+        int k = 0;
+        while (vals[i].v[k] != t) ++k;
+        return k;
+    };
     auto issue = [&](uint64_t c) -> int {
         const int k = (int)(c & 1);
-        launch_pack_multi(sh.amps, sendb[k], c * C, C, blk, vals, ab, s->stream);
+        for (size_t i = 0; i < ns; ++i)
+            launch_pack_multi(s->shards[i].amps, sendb(i, k), c * C, C, blk, vals[i], ab, s->stream);
         CU(cudaEventRecord(s->ev_comp[k], s->stream));
         CU(cudaStreamWaitEvent(s->comm_stream, s->ev_comp[k], 0));
-        NC(ncclGroupStart());
-        int slot = 0;
-        for (uint32_t t = 0; t < nt; ++t) {
-            if (t == ta) continue;
-            const int peer = (int)s->ginv[with_j(pa, t)];
-            NC(ncclSend(sendb[k] + (size_t)slot * C * ab, C * ab, ncclUint8, peer, s->comm, s->comm_stream));
-            NC(ncclRecv(recvb[k] + (size_t)slot * C * ab, C * ab, ncclUint8, peer, s->comm, s->comm_stream));
-            ++slot;
+        if (nccl) {
+            const uint32_t pa = shard_phys(s, s->shards[0]);
+            NC(ncclGroupStart());
+            for (int q = 0; q < vals[0].n; ++q) {
+                const int peer = (int)s->ginv[with_j(pa, vals[0].v[q])];
+                NC(ncclSend(sendb(0, k) + (size_t)q * slot_bytes, slot_bytes, ncclUint8, peer, s->comm, s->comm_stream));
+                NC(ncclRecv(recvb(0, k) + (size_t)q * slot_bytes, slot_bytes, ncclUint8, peer, s->comm, s->comm_stream));
+            }
+            NC(ncclGroupEnd());
+        } else {
+            // shard i's slot for block t goes to the shard with j bits t, which
+            // receives it into its slot for block ta(i)
+            for (size_t i = 0; i < ns; ++i) {
+                const uint32_t pa = shard_phys(s, s->shards[i]), ta = jval(pa);
+                for (int q = 0; q < vals[i].n; ++q) {
+                    const uint32_t idx = s->ginv[with_j(pa, vals[i].v[q])];
+                    size_t r = 0;
+                    while ((uint32_t)s->shards[r].index != idx) ++r;
+                    CU(cudaMemcpyAsync(recvb(r, k) + (size_t)slot_of(r, ta) * slot_bytes,
+                                       sendb(i, k) + (size_t)q * slot_bytes, slot_bytes, cudaMemcpyDeviceToDevice,
+                                       s->comm_stream));
+                }
+            }
         }
-        NC(ncclGroupEnd());
         CU(cudaEventRecord(s->ev_recv[k], s->comm_stream));
         return QSIM_OK;
     };
-    RC(issue(0));
-    if (nch > 1) RC(issue(1));
-    for (uint64_t c = 0; c < nch; ++c) {
+    prof_begin(s);
+    CU(cudaEventRecord(s->ev_start, s->stream));
+    CU(cudaStreamWaitEvent(s->comm_stream, s->ev_start, 0));
+    int rc = issue(0);
+    if (!rc && nch > 1) rc = issue(1);
+    for (uint64_t c = 0; c < nch && !rc; ++c) {
         const int k = (int)(c & 1);
         CU(cudaStreamWaitEvent(s->stream, s->ev_recv[k], 0));
-        launch_unpack_multi(sh.amps, recvb[k], c * C, C, blk, vals, ab, s->stream);
-        s->st.kernels += 2;
-        s->st.hbm_bytes += 4.0 * (double)(nt - 1) * (double)C * ab;
-        if (c + 2 < nch) RC(issue(c + 2));
+        for (size_t i = 0; i < ns; ++i)
+            launch_unpack_multi(s->shards[i].amps, recvb(i, k), c * C, C, blk, vals[i], ab, s->stream);
+        s->st.kernels += 2 * (int64_t)ns;
+        s->st.hbm_bytes += 4.0 * (double)ns * (double)(nt - 1) * (double)C * ab;
+        if (c + 2 < nch) rc = issue(c + 2);
     }
-    prof_end(s, QSIM_K_XCHG, 2.0 * (double)(nt - 1) * (double)nblock * ab);
-    s->st.exchange_bytes += (double)(nt - 1) * (double)nblock * ab;
+    if (!nccl) {
+        cudaStreamSynchronize(s->stream);
+        cudaFree(send_base);
+        cudaFree(recv_base);
+    }
+    if (rc) return rc;
+    prof_end(s, QSIM_K_XCHG, 2.0 * (double)ns * (double)(nt - 1) * (double)nblock * ab);
+    s->st.exchange_bytes += (double)ns * (double)(nt - 1) * (double)nblock * ab;
     s->st.exchanges++;
     CU(cudaGetLastError());
     return QSIM_OK;

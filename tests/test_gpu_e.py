@@ -805,3 +805,39 @@ def test_jit_shutdown_then_interpreter(tmp_path):
         j1, j2 = (int(x) for x in r.stdout.split()[-2:])
         assert j1 > 0 and j2 == 0, (mode, j1, j2)  # specialised before the shutdown, interpreted after
         assert np.max(np.abs(np.load(out) - ref)) <= TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("enc", ["E", "A"])
+def test_exchange_comm_pipeline_path(tmp_path, enc):
+    """The NCCL pairwise exchange's pipeline on one GPU (QSIM_XCHG_VIA_COMM=1:
+    comm stream, double-buffered receive buffers, events; device copies stand
+    in for ncclSend / ncclRecv; QSIM_NO_REMAP=1 so every global gate takes a
+    pairwise exchange; small chunks so each exchange takes many rounds): E
+    equals the oracle, A equals the single-shard run bit for bit."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    n = 13
+    for P in (2, 4):
+        out = str(tmp_path / f"x_{enc}_{P}.npy")
+        getter = "s.get_state()" if enc == "E" else "s.get_codes()[0]"
+        code = ("import sys, numpy as np; sys.path.insert(0, %r); import paper_1805_04708_b200 as q, qsim_inputs as C; "
+                "s = q.State(%d, q.ENC_%s, %d, chunk_bytes=2048); c = C.layered(%d, 2, seed=8); "
+                "c.extend(C.rz_rx_cphase(%d, 1, seed=8)); s.apply_circuit(c); st = s.stats(); np.save(%r, %s); "
+                "print(st['exchanges'])" % (root, n, "FP64" if enc == "E" else "ADAPTIVE2", P, n, n, out, getter))
+        env = dict(os.environ, QSIM_XCHG_VIA_COMM="1", QSIM_NO_REMAP="1")
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        assert int(r.stdout.split()[-1]) > 0
+        got = np.load(out)
+        circ = C.layered(n, 2, seed=8)
+        circ.extend(C.rz_rx_cphase(n, 1, seed=8))
+        if enc == "E":
+            assert np.max(np.abs(got - oracle.e_simulate(n, circ))) <= TOL
+        else:
+            with q.State(n, q.ENC_ADAPTIVE2, 1) as s1:
+                s1.apply_circuit(circ)
+                assert np.array_equal(got, s1.get_codes()[0])
