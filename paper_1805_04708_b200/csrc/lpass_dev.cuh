@@ -21,6 +21,10 @@ __device__ __forceinline__ void lp_cp_async16(void *smem, const void *gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void lp_cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+// bring a 128-byte run into L2 ahead of its cp.async (no completion to wait for)
+__device__ __forceinline__ void lp_prefetch_l2_128(const void *gmem) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], 128;\n" ::"l"(gmem) : "memory");
+}
 
 // 16-byte shared-memory access of one amplitude (register stages).  Explicit
 // v2.f64: from C++ the compiler splits some stages' double2 accesses into two
@@ -28,6 +32,9 @@ __device__ __forceinline__ void lp_cp_async_wait_all() { asm volatile("cp.async.
 // asm is volatile so it stays between the stage's __syncthreads.
 #ifndef LP_STAGE_ASM
 #define LP_STAGE_ASM 1
+#endif
+#ifndef LP_PREFETCH
+#define LP_PREFETCH 0  // L2 prefetch of the next tile (QSIM_LPASS_PREFETCH=1): measured slower, off
 #endif
 __device__ __forceinline__ double2 lp_lds16(uint32_t sa) {
 #if LP_STAGE_ASM
@@ -549,6 +556,24 @@ __device__ __forceinline__ void lp_body(const LPassParams &p, const Stages &stag
         }
         lp_cp_async_wait_all();
         __syncthreads();
+        // ---- L2 prefetch of this CTA's next tile: its HBM reads overlap this
+        // tile's stages, and its cp.async loads then hit L2 (one thread per
+        // 128-byte run: the threads with logical bits 0..2 = 0) ----
+        if (LP_PREFETCH && !p.noio && T + gridDim.x < p.ntiles) {
+            // the runs are (thread bits 3.., j bits); thread tid takes the runs of the
+            // j with j % 8 == tid % 8, i.e. 2^(K-TB)/8 of them
+            uint64_t nb = (T + gridDim.x) << LP_LOW;
+            for (int i = 0; i < K - LP_LOW; ++i) nb = lp_ins0(nb, p.high_q[i]);
+            const char *gp = reinterpret_cast<const char *>(a + (nb | (d_tid & ~7ull)));
+            const int nj = 1 << (K - TB);
+            for (int j = (int)(tid & 7u); j < nj; j += 8) {
+                uint64_t dj = 0;
+#pragma unroll
+                for (int b = 0; b < 5; ++b)
+                    if ((j >> b) & 1) dj ^= d_hi[b];
+                lp_prefetch_l2_128(gp + dj);
+            }
+        }
         // ---- register stages ----
         stages(t);
         // ---- store: logical x = tid + 128 j from S (M x ^ b) ----
