@@ -2395,11 +2395,82 @@ int qsim_set_codes(qsim_state *s, const int8_t *codes, double r0, double r1) {
 // ============================================================================
 namespace qsim {
 
+// The diagonal gates that follow a dense gate, applied as its apply kernel
+// stores the codes (AEpilogue; the same integer b1 steps as diag_run_a, so
+// the result is bit-identical to the separate sweep): run[i..j).
+struct AEpiRun {
+    const std::vector<PlanOp> *run = nullptr;
+    const std::vector<const double *> *us = nullptr;
+    size_t i = 0, j = 0;
+};
+
+// The epilogue of the dense gate o for shard sh; false when the run does not fit.
+// A unit holds 16 codes: local bits 0..3 (target < 4) or bits 0..2 and the
+// target (code index bit 3); a diagonal gate's step for a code depends on its
+// target and control bits -- all inside the unit (a per-code constant), all
+// outside (one value per unit) or both (a per-unit condition on a per-code pattern).
+static bool build_epi(const qsim_state *s, const Shard &sh, const PlanOp &o, const AEpiRun &r, AEpilogue &e) {
+    e = AEpilogue{};
+    const int ib[4] = {0, 1, 2, o.l < 4 ? 3 : o.l};
+    uint64_t imask = 0;
+    for (int q = 0; q < 4; ++q) imask |= 1ull << ib[q];
+    auto jbit = [&](int j, int bit) {
+        for (int q = 0; q < 4; ++q)
+            if (ib[q] == bit) return (j >> q) & 1;
+        return 0;
+    };
+    for (size_t k = r.i; k < r.j; ++k) {
+        const PlanOp &g = (*r.run)[k];
+        const double *u = (*r.us)[k];
+        if (!global_ctrls_ok(s, sh, g)) continue;
+        uint64_t cm = 0;
+        for (int c = 0; c < g.nctrl; ++c)
+            if (g.ctrl[c] < s->nl) cm |= 1ull << g.ctrl[c];
+        int k0 = a_phase_steps(u[0], u[1]), k1 = a_phase_steps(u[6], u[7]);
+        int t = g.l;
+        if (g.l >= s->nl) {
+            t = -1;
+            k0 = k1 = rank_bit(s, sh, g.l) ? k1 : k0;
+        }
+        const uint64_t ci = cm & imask, ce = cm & ~imask;
+        const bool ti = t >= 0 && ((imask >> t) & 1ull);
+        auto step = [&](int j, int sel) {  // the gate's step for code j (sel: an outside target bit)
+            for (int q = 0; q < 4; ++q)
+                if (((ci >> ib[q]) & 1ull) && !((j >> q) & 1)) return 0;
+            return (ti ? jbit(j, t) : sel) ? k1 : k0;
+        };
+        if (!ce && (t < 0 || ti)) {
+            for (int j = 0; j < 16; ++j) e.base[j] = (int8_t)(e.base[j] + step(j, 0));
+        } else if (!ci && !ti) {
+            if (e.nscalar == A_EPI_MAX_SCALAR) return false;
+            AEpiScalar &x = e.s[e.nscalar++];
+            x.cext = ce;
+            x.t = (int16_t)t;
+            x.k0 = (int8_t)k0;
+            x.k1 = (int8_t)k1;
+        } else {
+            if (e.nmixed == A_EPI_MAX_MIXED) return false;
+            AEpiMixed &m = e.m[e.nmixed++];
+            m.cext = ce;
+            m.t = (int16_t)(ti ? -1 : t);
+            for (int sel = 0; sel < 2; ++sel)
+                for (int j = 0; j < 16; ++j) m.pat[sel][j] = (int8_t)step(j, sel);
+        }
+    }
+    return true;
+}
+static void set_epi(const qsim_state *s, const Shard &sh, const PlanOp &o, const AEpiRun &r, AGateParams &p) {
+    if (r.i >= r.j) return;
+    build_epi(s, sh, o, r, p.epi);  // fits: checked on every shard by run_gates_a
+    p.has_epi = 1;
+}
+
 // Exact global bounds of the post-gate magnitudes (reading R-A4), then the
 // decode-apply-encode sweep with those bounds.
 // the exact policy's two phases (reading R-A4) from the shards' codes; aout: the
 // out-of-place target (lazy policy) or in place
-static int dense_gate_a_exact(qsim_state *s, const PlanOp &o, const double *u, bool out_of_place) {
+static int dense_gate_a_exact(qsim_state *s, const PlanOp &o, const double *u, bool out_of_place,
+                              const AEpiRun &r) {
     // phase 1 on every shard: (min, -max) of the post-gate |z|^2 merged on the
     // device; across ranks one ncclAllReduce(min); the next tables are built
     // on the device from the result -- no host round trip per gate
@@ -2425,6 +2496,7 @@ static int dense_gate_a_exact(qsim_state *s, const PlanOp &o, const double *u, b
     for (auto &sh : s->shards) {
         AGateParams p{};
         fill_agate(p, s, sh, o, u);
+        set_epi(s, sh, o, r, p);
         if (out_of_place) p.aout = sh.amps2;
         prof_begin(s);
         launch_apply_a(p, s->atab, s->stream);
@@ -2443,7 +2515,7 @@ static int dense_gate_a_exact(qsim_state *s, const PlanOp &o, const double *u, b
 // which also certifies that every output stayed within one step of (r0, r1);
 // if one left, the exact policy runs from the (intact) input codes.  Then the
 // two code buffers swap.
-static int dense_gate_a_lazy(qsim_state *s, const PlanOp &o, const double *u) {
+static int dense_gate_a_lazy(qsim_state *s, const PlanOp &o, const double *u, const AEpiRun &r) {
     for (auto &sh : s->shards)
         if (!sh.amps2) {
             if (cudaMalloc(&sh.amps2, s->alloc_amps * s->amp_bytes) != cudaSuccess) {
@@ -2462,6 +2534,7 @@ static int dense_gate_a_lazy(qsim_state *s, const PlanOp &o, const double *u) {
         for (auto &sh : s->shards) {
             AGateParams p{};
             fill_agate(p, s, sh, o, u);
+            set_epi(s, sh, o, r, p);
             p.aout = sh.amps2;
             p.oor = s->d_oor;
             prof_begin(s);
@@ -2477,15 +2550,15 @@ static int dense_gate_a_lazy(qsim_state *s, const PlanOp &o, const double *u) {
         CU(cudaStreamSynchronize(s->stream));
         rescale = h != 0;
     }
-    if (rescale) RC(dense_gate_a_exact(s, o, u, true));
+    if (rescale) RC(dense_gate_a_exact(s, o, u, true, r));
     for (auto &sh : s->shards) std::swap(sh.amps, sh.amps2);
     return QSIM_OK;
 }
 
-static int dense_gate_a(qsim_state *s, const PlanOp &o, const double *u) {
+static int dense_gate_a(qsim_state *s, const PlanOp &o, const double *u, const AEpiRun &r = AEpiRun{}) {
     s->st.a_dense++;
-    if (s->a_policy == QSIM_A_POLICY_LAZY) return dense_gate_a_lazy(s, o, u);
-    return dense_gate_a_exact(s, o, u, false);
+    if (s->a_policy == QSIM_A_POLICY_LAZY) return dense_gate_a_lazy(s, o, u, r);
+    return dense_gate_a_exact(s, o, u, false, r);
 }
 static int diag_run_a(qsim_state *s, const std::vector<PlanOp> &run, const std::vector<const double *> &us, size_t i,
                       size_t j) {
@@ -2527,11 +2600,27 @@ static int diag_run_a(qsim_state *s, const std::vector<PlanOp> &run, const std::
 
 static int run_gates_a(qsim_state *s, const std::vector<PlanOp> &run, const std::vector<const double *> &us) {
     static const bool fuse_diag = getenv("QSIM_A_NO_DIAG_RUN") == nullptr;
+    const bool epilogue = getenv("QSIM_A_NO_EPILOGUE") == nullptr;  // read per call: tests compare both
     for (size_t i = 0; i < run.size(); ++i) {
         const PlanOp &o = run[i];
         const double *u = us[i];
         if (o.cls == CLS_DENSE) {
-            RC(dense_gate_a(s, o, u));
+            // the diagonal gates that follow fold into this gate's apply kernel
+            AEpiRun r{&run, &us, i + 1, i + 1};
+            if (epilogue) {
+                AEpilogue e;
+                for (;;) {
+                    if (r.j >= run.size() || run[r.j].cls != CLS_DIAG) break;
+                    AEpiRun t = r;
+                    ++t.j;
+                    bool fits = true;
+                    for (auto &sh : s->shards) fits = fits && build_epi(s, sh, o, t, e);
+                    if (!fits) break;
+                    r = t;
+                }
+            }
+            RC(dense_gate_a(s, o, u, r));
+            i = r.j - 1;
             continue;
         }
         if (fuse_diag && o.cls == CLS_DIAG && s->nl <= 32) {

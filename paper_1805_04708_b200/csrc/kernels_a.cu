@@ -712,15 +712,68 @@ __device__ __forceinline__ uint32_t a_encode_f(const AEncF &ce, float2 z, float 
     return zero ? 0x0080u : __byte_perm(__float_as_uint(tm), __float_as_uint(ta), 0x0040);
 }
 
+// b1 += k8 >> 8 (mod 256) except for the special zero, which keeps b1 = 0
+// (a diagonal gate's phase step); b0 never changes
+__device__ __forceinline__ uint32_t shift_b1_fast(uint32_t code, uint32_t k8) {
+    const uint32_t moved = (code & 0xffu) | ((code + k8) & 0xff00u);
+    return (code & 0xffu) == 0x80u ? code : moved;
+}
+
+// The following diagonal run (AEpilogue): the summed b1 step of code j of the
+// unit at s0 -- the same sum k_diag_run_a forms per code.  The scalar part is
+// one value per unit.
+__device__ __forceinline__ uint32_t a_epi_scalar(const AEpilogue &e, uint64_t s0) {
+    uint32_t acc = 0;
+#pragma unroll 1
+    for (int g = 0; g < e.nscalar; ++g) {
+        const AEpiScalar x = e.s[g];
+        const bool on = (s0 & x.cext) == x.cext;
+        const bool b = x.t >= 0 && ((s0 >> x.t) & 1ull);
+        acc += on ? (uint32_t)(int)(b ? x.k1 : x.k0) : 0u;
+    }
+    return acc;
+}
+// the queue path (rare): the steps of the pair's two codes, sh0 | sh1 << 8
+__device__ __noinline__ uint32_t a_epi_pair(const AEpilogue *e, uint64_t s0, int j0, int j1) {
+    const uint32_t acc = a_epi_scalar(*e, s0);
+    uint32_t s[2] = {acc + (uint32_t)(int)e->base[j0], acc + (uint32_t)(int)e->base[j1]};
+#pragma unroll 1
+    for (int g = 0; g < e->nmixed; ++g) {
+        const AEpiMixed &m = e->m[g];
+        if ((s0 & m.cext) != m.cext) continue;
+        const int sel = m.t >= 0 ? (int)((s0 >> m.t) & 1ull) : 0;
+        s[0] += (uint32_t)(int)m.pat[sel][j0];
+        s[1] += (uint32_t)(int)m.pat[sel][j1];
+    }
+    return (s[0] & 0xffu) | ((s[1] & 0xffu) << 8);
+}
+__device__ __forceinline__ void a_epi_apply(const AEpilogue &e, uint64_t s0, uint32_t (&nc)[16]) {
+    const uint32_t acc = a_epi_scalar(e, s0);
+    uint32_t sh[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) sh[j] = acc + (uint32_t)(int)e.base[j];
+#pragma unroll 1
+    for (int g = 0; g < e.nmixed; ++g) {
+        const AEpiMixed &m = e.m[g];
+        if ((s0 & m.cext) != m.cext) continue;
+        const int sel = m.t >= 0 ? (int)((s0 >> m.t) & 1ull) : 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sh[j] += (uint32_t)(int)m.pat[sel][j];
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) nc[j] = shift_b1_fast(nc[j], (sh[j] & 0xffu) << 8);
+}
+
 // Pairs whose fp32 decision failed go to a per-warp queue; the fp64 reference
 // (AGlob: the same arithmetic as a_decode / a_gate2 / a_encode) recomputes
 // them 32 at a time, one pair per lane, after their units' provisional
 // stores -- instead of stalling the whole warp for every unit with a failing
 // pair.  Entry: the pair's first code index i0 (bit 63: the gate applies),
-// the input codes (c0 | c1 << 16); the second code is at i0 + 2^t.
+// the input codes (c0 | c1 << 16); the second code is at i0 + 2^t; the
+// epilogue's b1 steps of the two codes (sh0 | sh1 << 8).
 struct AFail {
     uint64_t i0;
-    uint32_t codes, pad;
+    uint32_t codes, sh;
 };
 constexpr int A_QN = 32;
 template <int UK, bool LAZY>
@@ -749,8 +802,8 @@ __device__ __noinline__ void a_flush(const AGateParams *pp, const ATabData *cur,
             if (ox || oy) atomicOr(pp->oor, 1);
         }
         uint16_t *a = reinterpret_cast<uint16_t *>(pp->aout ? pp->aout : pp->a);
-        a[i0] = (uint16_t)g.encode(x);
-        a[i0 + (1ull << pp->t)] = (uint16_t)g.encode(y);
+        a[i0] = (uint16_t)shift_b1_fast(g.encode(x), (e.sh & 0xffu) << 8);
+        a[i0 + (1ull << pp->t)] = (uint16_t)shift_b1_fast(g.encode(y), e.sh & 0xff00u);
     }
     __syncwarp();  // the queue is free again
 }
@@ -1206,6 +1259,7 @@ __global__ void __launch_bounds__(A_THREADS, A_DENSE_MINB) k_apply_a(const __gri
                 nc[j1] = cy;
                 fail |= (uint32_t)!ok << k;
             }
+            if (p.has_epi) a_epi_apply(p.epi, s0, nc);
             U::store(ao, s0, p.t, nc);  // provisional for the failing pairs
         }
         if (LAZY && __any_sync(0xffffffffu, oor_any)) {
@@ -1227,7 +1281,8 @@ __global__ void __launch_bounds__(A_THREADS, A_DENSE_MINB) k_apply_a(const __gri
                         AFail e;
                         e.i0 = U::pos(s0, p.t, U::j0(k)) | ((uint64_t)((selm >> k) & 1u) << 63);
                         e.codes = __byte_perm(c[U::j0(k)], c[U::j1(k)], 0x5410);
-                        e.pad = 0;
+                        e.sh = 0;
+                        if (p.has_epi) e.sh = a_epi_pair(&p.epi, s0, U::j0(k), U::j1(k));
                         q[qn + __popc(bal & lt)] = e;
                     }
                     qn += tot;
@@ -1323,10 +1378,6 @@ struct ADiagParams {
     int32_t tconst;     // target bit value when it is neither (fixed or global)
     int32_t k0, k1;
 };
-__device__ __forceinline__ uint32_t shift_b1_fast(uint32_t code, uint32_t k8) {
-    const uint32_t moved = (code & 0xffu) | ((code + k8) & 0xff00u);
-    return (code & 0xffu) == 0x80u ? code : moved;
-}
 __global__ void __launch_bounds__(A_THREADS) k_diag_a(const __grid_constant__ ADiagParams p) {
     uint16_t *a = reinterpret_cast<uint16_t *>(p.a);
     const uint32_t k08 = (uint32_t)p.k0 << 8, k18 = (uint32_t)p.k1 << 8;

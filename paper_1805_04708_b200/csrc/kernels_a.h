@@ -51,6 +51,33 @@ int atables_set(ATables *t, double r0, double r1, cudaStream_t s);       // curr
 int atables_set_next(ATables *t, double r0, double r1, cudaStream_t s);  // tables for the encode bounds
 int atables_commit_next(ATables *t, cudaStream_t s);                     // next becomes current
 
+// A run of diagonal gates that follows a dense gate, applied to the dense
+// gate's output codes as they are stored: the same integer b1 steps the
+// diagonal sweeps add (exact; k_diag_run_a semantics), so the run costs no
+// extra pass.  Per code of a 16-code unit the step is base[j] (gates whose
+// target and controls are all unit-internal bits) + the scalar gates (every
+// bit outside the unit: one value per unit) + the mixed gates (a unit-index
+// condition selecting a per-code pattern).
+constexpr int A_EPI_MAX_SCALAR = 48, A_EPI_MAX_MIXED = 4;
+struct AEpiScalar {
+    uint64_t cext;  // local control bits (all outside the unit)
+    int16_t t;      // local target bit outside the unit, or -1: the constant step k0
+    int8_t k0, k1;  // b1 steps for target bit 0 / 1
+    int32_t pad;
+};
+struct AEpiMixed {
+    uint64_t cext;       // local control bits outside the unit
+    int16_t t;           // local target bit outside the unit (selects pat[1]), or -1 (pat[0])
+    int16_t pad[3];
+    int8_t pat[2][16];   // per code of the unit
+};
+struct AEpilogue {
+    int32_t nscalar, nmixed;
+    int8_t base[16];
+    AEpiScalar s[A_EPI_MAX_SCALAR];
+    AEpiMixed m[A_EPI_MAX_MIXED];
+};
+
 struct AGateParams {
     void *a;              // uint16 codes: low byte b0, high byte b1
     uint64_t shard_base;  // full physical index of local 0
@@ -69,6 +96,9 @@ struct AGateParams {
     // nullptr = in place); an output magnitude outside [r0 - d, r1 + d] sets *oor
     void *aout;
     int32_t *oor;
+    int32_t has_epi;  // the following diagonal run applied at store (AEpilogue)
+    int32_t pad2;
+    AEpilogue epi;
 };
 struct ACollapseParams {
     void *a;
