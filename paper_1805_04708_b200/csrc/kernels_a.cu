@@ -533,6 +533,37 @@ __device__ __forceinline__ void a_gate_fu(const float (&u)[8], float2 &x, float2
         a_gate_fk<UK>(u, x, y);
 }
 
+__device__ __forceinline__ float2 f2s(float v) { return make_float2(v, v); }
+
+// The fp32 gate on Blackwell's packed fp32x2 instructions (FFMA2 / FMUL2, a
+// scalar operand broadcast to both halves): the outputs come out as
+// RE = (Re x', Re y'), IM = (Im x', Im y') -- the layout a_encode_f2 takes --
+// from the decoded inputs A = x, B = y.  Each component is the same sum of at
+// most 4 products by an fma chain as a_gate_f (the error bound A_KF covers
+// any order); the coefficient pairs kf come from a_dense_params:
+//   UK 0: RE = (u0,u4) A.x + (-u1,-u5) A.y + (u2,u6) B.x + (-u3,-u7) B.y,
+//         IM = (u1,u5) A.x + (u0,u4) A.y + (u3,u7) B.x + (u2,u6) B.y;
+//   UK 1: RE = (u0,u4) A.x + (u2,u6) B.x, IM = (u0,u4) A.y + (u2,u6) B.y;
+//   UK 2: RE = (u0,-u5) (A.x,A.y) + (-u3,u6) (B.y,B.x),
+//         IM = (u0,u5) (A.y,A.x) + (u3,u6) (B.x,B.y).
+template <int UK>
+__device__ __forceinline__ void a_gate_f2(const float (&k)[16], float2 A, float2 B, float2 &RE, float2 &IM) {
+    const float2 k0 = make_float2(k[0], k[1]), k1 = make_float2(k[2], k[3]);
+    const float2 k2 = make_float2(k[4], k[5]), k3 = make_float2(k[6], k[7]);
+    if (UK == 0) {
+        const float2 k4 = make_float2(k[8], k[9]), k5 = make_float2(k[10], k[11]);
+        const float2 k6 = make_float2(k[12], k[13]), k7 = make_float2(k[14], k[15]);
+        RE = __ffma2_rn(k3, f2s(B.y), __ffma2_rn(k2, f2s(B.x), __ffma2_rn(k1, f2s(A.y), __fmul2_rn(k0, f2s(A.x)))));
+        IM = __ffma2_rn(k7, f2s(B.y), __ffma2_rn(k6, f2s(B.x), __ffma2_rn(k5, f2s(A.y), __fmul2_rn(k4, f2s(A.x)))));
+    } else if (UK == 1) {
+        RE = __ffma2_rn(k2, f2s(B.x), __fmul2_rn(k0, f2s(A.x)));
+        IM = __ffma2_rn(k2, f2s(B.y), __fmul2_rn(k0, f2s(A.y)));
+    } else {
+        RE = __ffma2_rn(k0, A, __fmul2_rn(k1, make_float2(B.y, B.x)));
+        IM = __ffma2_rn(k2, make_float2(A.y, A.x), __fmul2_rn(k3, B));
+    }
+}
+
 // the fp32 tables of this thread's lane in shared memory
 struct AFLane {
     const float *rf;   // rf[raw * 32]
@@ -541,6 +572,13 @@ struct AFLane {
         r = rf[(code & 0xffu) * 32u];
         const float2 c = cs[((code >> 8) & 0xffu) * 16u];
         return make_float2(r * c.x, r * c.y);
+    }
+    // the same values (one FMUL2); the byte offsets of both tables are raw * 128
+    __device__ __forceinline__ float2 decode2(uint32_t code, float &r) const {
+        r = *reinterpret_cast<const float *>(reinterpret_cast<const char *>(rf) + ((code & 0xffu) << 7));
+        const float2 c = *reinterpret_cast<const float2 *>(reinterpret_cast<const char *>(cs) +
+                                                           (__byte_perm(code, 0u, 0x4441) << 7));
+        return __fmul2_rn(f2s(r), c);
     }
 };
 extern __shared__ __align__(16) unsigned char a_dsm[];
@@ -710,6 +748,58 @@ __device__ __forceinline__ uint32_t a_encode_f(const AEncF &ce, float2 z, float 
     const float fra = q - (ta - A_MAGIC);
     ok = zero | (inter & !edge & (fabsf(frm) < 0.5f - errm) & (fmaf(KE, rs, fabsf(fra)) < 0.4998f));
     return zero ? 0x0080u : __byte_perm(__float_as_uint(tm), __float_as_uint(ta), 0x0040);
+}
+
+// The same encode for the two outputs of a pair at once, on Blackwell's
+// packed fp32x2 instructions (FFMA2 / FADD2 / FMUL2: two IEEE round-to-nearest
+// operations per issue, the same results bit for bit as the scalar ones above,
+// so the certification is unchanged); lane .x = output x, .y = output y.
+__device__ __forceinline__ float2 atan_2steps2(float2 w) {
+    const float2 s = __fmul2_rn(w, w);
+    float2 p = __ffma2_rn(f2s(0.5550681352615356f), s, f2s(-2.7382962703704834f));
+    p = __ffma2_rn(p, s, f2s(6.488292694091797f));
+    p = __ffma2_rn(p, s, f2s(-10.783480644226074f));
+    p = __ffma2_rn(p, s, f2s(16.14085578918457f));
+    p = __ffma2_rn(p, s, f2s(-27.149433135986328f));
+    p = __ffma2_rn(p, s, f2s(81.48701477050781f));
+    return __fmul2_rn(p, w);
+}
+template <bool LAZY>
+__device__ __forceinline__ void a_encode_f2(const AEncF &ce, float2 re, float2 im, float errm, float KE, float eS,
+                                            uint32_t &cx, uint32_t &cy, bool &okx, bool &oky, bool &ox, bool &oy) {
+    const float2 m2 = __ffma2_rn(re, re, __fmul2_rn(im, im));
+    const float2 rs = make_float2(a_rsqrt(m2.x), a_rsqrt(m2.y));
+    float2 mf = __fmul2_rn(m2, rs);
+    mf.x = m2.x > 0.f ? mf.x : 0.f;
+    mf.y = m2.y > 0.f ? mf.y : 0.f;
+    float2 t = __ffma2_rn(mf, f2s(ce.s1), f2s(ce.s0));
+    const float2 zt = __ffma2_rn(mf, f2s(1.0000005f), f2s(eS));
+    const float2 it = __ffma2_rn(mf, f2s(0.9999995f), f2s(-eS));
+    const bool zerox = zt.x < 0.99999e-12f, zeroy = zt.y < 0.99999e-12f;
+    const bool interx = it.x > 1.00001e-12f, intery = it.y > 1.00001e-12f;
+    bool edgex = false, edgey = false;
+    if (LAZY) {
+        ox = interx & ((t.x < -1.f - errm) | (t.x > 254.f + errm));
+        oy = intery & ((t.y < -1.f - errm) | (t.y > 254.f + errm));
+        edgex = (fabsf(t.x + 1.f) <= errm) | (fabsf(t.x - 254.f) <= errm);
+        edgey = (fabsf(t.y + 1.f) <= errm) | (fabsf(t.y - 254.f) <= errm);
+        t.x = fminf(fmaxf(t.x, 0.f), 253.f);
+        t.y = fminf(fmaxf(t.y, 0.f), 253.f);
+    }
+    const float2 tm = __fadd2_rn(t, f2s(A_MAGIC + 129.f));
+    const float2 frm = __fadd2_rn(t, __ffma2_rn(tm, f2s(-1.f), f2s(A_MAGIC + 129.f)));  // t - (tm - M), exact
+    const float2 den = __fadd2_rn(mf, make_float2(fabsf(re.x), fabsf(re.y)));
+    const float2 w = __fmul2_rn(im, make_float2(a_rcp(den.x), a_rcp(den.y)));
+    const float2 p = atan_2steps2(w);
+    const float2 q = make_float2((re.x < 0.f) ? copysignf(128.f, im.x) - p.x : p.x,
+                                 (re.y < 0.f) ? copysignf(128.f, im.y) - p.y : p.y);
+    const float2 ta = __fadd2_rn(q, f2s(A_MAGIC));
+    const float2 fra = __fadd2_rn(q, __ffma2_rn(ta, f2s(-1.f), f2s(A_MAGIC)));  // q - (ta - M), exact
+    const float2 ka = __ffma2_rn(f2s(KE), rs, make_float2(fabsf(fra.x), fabsf(fra.y)));
+    okx = zerox | (interx & !edgex & (fabsf(frm.x) < 0.5f - errm) & (ka.x < 0.4998f));
+    oky = zeroy | (intery & !edgey & (fabsf(frm.y) < 0.5f - errm) & (ka.y < 0.4998f));
+    cx = zerox ? 0x0080u : __byte_perm(__float_as_uint(tm.x), __float_as_uint(ta.x), 0x0040);
+    cy = zeroy ? 0x0080u : __byte_perm(__float_as_uint(tm.y), __float_as_uint(ta.y), 0x0040);
 }
 
 // b1 += k8 >> 8 (mod 256) except for the special zero, which keeps b1 = 0
@@ -1137,9 +1227,31 @@ static int a_ukind(const double *u) {
     return 0;
 }
 // fp32 copy of U and the magnitude coefficients of the bounds screen
+static int a_ukind(const double *u);
 static AGateParams a_dense_params(const AGateParams &p0) {
     AGateParams p = p0;
     for (int i = 0; i < 8; ++i) p.uf[i] = (float)p.u[i];
+    {  // a_gate_f2's coefficient pairs
+        const float *u = p.uf;
+        float *k = p.kf;
+        switch (a_ukind(p.u)) {
+            case 1: {
+                const float v[8] = {u[0], u[4], 0.f, 0.f, u[2], u[6], 0.f, 0.f};
+                for (int i = 0; i < 8; ++i) k[i] = v[i];
+                break;
+            }
+            case 2: {
+                const float v[8] = {u[0], -u[5], -u[3], u[6], u[0], u[5], u[3], u[6]};
+                for (int i = 0; i < 8; ++i) k[i] = v[i];
+                break;
+            }
+            default: {
+                const float v[16] = {u[0], u[4], -u[1], -u[5], u[2], u[6], -u[3], -u[7],
+                                     u[1], u[5], u[0], u[4], u[3], u[7], u[2], u[6]};
+                for (int i = 0; i < 16; ++i) k[i] = v[i];
+            }
+        }
+    }
     const double m00 = std::hypot(p.u[0], p.u[1]), m01 = std::hypot(p.u[2], p.u[3]);
     const double m10 = std::hypot(p.u[4], p.u[5]), m11 = std::hypot(p.u[6], p.u[7]);
     const double A = std::max(m00, m11) * (1.0 + 1e-6), B = std::max(m01, m10) * (1.0 + 1e-6);
@@ -1236,15 +1348,26 @@ __global__ void __launch_bounds__(A_THREADS, A_DENSE_MINB) k_apply_a(const __gri
                 const bool sel = !CTRL || (hi_ok && ((uint32_t)off & cl) == cl);
                 selm |= (uint32_t)sel << k;
                 float ra, rb;
+#ifdef QSIM_A_SCALAR_ENCODE
                 float2 x = L.decode(c[j0], ra), y = L.decode(c[j1], rb);
                 if (sel) a_gate_fu<UK>(uf, x, y);
+#else
+                const float2 A = L.decode2(c[j0], ra), B = L.decode2(c[j1], rb);
+                float2 RE = make_float2(A.x, B.x), IM = make_float2(A.y, B.y);
+                if (sel) a_gate_f2<UK>(p.kf, A, B, RE, IM);
+#endif
                 const float S = ra + rb;
                 const float E = A_KF * S;
                 const float errm = fmaf(S, ce.kS, fmaf(E, ce.kE, ce.C0)), KE = 73.f * E;
                 const float eS = 1.4145f * E;
-                bool okx, oky, ox, oy;
-                uint32_t cx = a_encode_f<LAZY>(ce, x, errm, KE, eS, okx, ox);
-                uint32_t cy = a_encode_f<LAZY>(ce, y, errm, KE, eS, oky, oy);
+                bool okx, oky, ox = false, oy = false;
+                uint32_t cx, cy;
+#ifdef QSIM_A_SCALAR_ENCODE
+                cx = a_encode_f<LAZY>(ce, x, errm, KE, eS, okx, ox);
+                cy = a_encode_f<LAZY>(ce, y, errm, KE, eS, oky, oy);
+#else
+                a_encode_f2<LAZY>(ce, RE, IM, errm, KE, eS, cx, cy, okx, oky, ox, oy);
+#endif
                 if (LAZY) oor_any |= (ox & (!CTRL || sel)) | (oy & (!CTRL || sel));
                 if (CTRL) {  // an unselected zero code stays the exact zero special
                     const bool zx = (ra == 0.f) & !sel, zy = (rb == 0.f) & !sel;

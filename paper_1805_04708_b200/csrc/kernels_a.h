@@ -91,6 +91,7 @@ struct AGateParams {
     // coefficients of the bounds screen (k_bounds_a): A >= B >= 0 bound
     // max(|u00|, |u11|), max(|u01|, |u10|) from above, a / b their nominal values
     float uf[8];
+    float kf[16];  // packed fp32x2 coefficient pairs of a_gate_f2 (a_dense_params, per matrix class)
     float mA, mB, ma, mb;
     // lazy bounds (reading R-A25): codes are written to aout (out of place,
     // nullptr = in place); an output magnitude outside [r0 - d, r1 + d] sets *oor
