@@ -381,15 +381,23 @@ struct AUnit {
     __device__ static __forceinline__ uint64_t pos(uint64_t s0, int t, int j) {
         return TL < 4 ? s0 + (uint64_t)j : (j < 8 ? s0 + (uint64_t)j : (s0 | (1ull << t)) + (uint64_t)(j - 8));
     }
-    __device__ static __forceinline__ void load(const uint16_t *__restrict__ a, uint64_t s0, int t, uint32_t (&c)[16]) {
-        const uint4 v0 = __ldcs(reinterpret_cast<const uint4 *>(a + s0));
-        const uint4 v1 = __ldcs(reinterpret_cast<const uint4 *>(a + (TL < 4 ? s0 + 8 : (s0 | (1ull << t)))));
+    __device__ static __forceinline__ void load_raw(const uint16_t *__restrict__ a, uint64_t s0, int t, uint4 &v0,
+                                                    uint4 &v1) {
+        v0 = __ldcs(reinterpret_cast<const uint4 *>(a + s0));
+        v1 = __ldcs(reinterpret_cast<const uint4 *>(a + (TL < 4 ? s0 + 8 : (s0 | (1ull << t)))));
+    }
+    __device__ static __forceinline__ void unpack(const uint4 &v0, const uint4 &v1, uint32_t (&c)[16]) {
         const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             c[2 * k] = w[k] & 0xffffu;
             c[2 * k + 1] = w[k] >> 16;
         }
+    }
+    __device__ static __forceinline__ void load(const uint16_t *__restrict__ a, uint64_t s0, int t, uint32_t (&c)[16]) {
+        uint4 v0, v1;
+        load_raw(a, s0, t, v0, v1);
+        unpack(v0, v1, c);
     }
     __device__ static __forceinline__ void store(uint16_t *__restrict__ a, uint64_t s0, int t, const uint32_t (&c)[16]) {
         uint4 v0, v1;  // low halves of c[] (upper bits ignored)
@@ -573,12 +581,18 @@ struct AFLane {
         const float2 c = cs[((code >> 8) & 0xffu) * 16u];
         return make_float2(r * c.x, r * c.y);
     }
-    // the same values (one FMUL2); the byte offsets of both tables are raw * 128
+    // the byte offsets of both tables are raw * 128
+    __device__ __forceinline__ float mag(uint32_t code) const {
+        return *reinterpret_cast<const float *>(reinterpret_cast<const char *>(rf) + ((code & 0xffu) << 7));
+    }
+    __device__ __forceinline__ float2 cs2(uint32_t code) const {
+        return *reinterpret_cast<const float2 *>(reinterpret_cast<const char *>(cs) +
+                                                 (__byte_perm(code, 0u, 0x4441) << 7));
+    }
+    // the same values as decode (one FMUL2)
     __device__ __forceinline__ float2 decode2(uint32_t code, float &r) const {
-        r = *reinterpret_cast<const float *>(reinterpret_cast<const char *>(rf) + ((code & 0xffu) << 7));
-        const float2 c = *reinterpret_cast<const float2 *>(reinterpret_cast<const char *>(cs) +
-                                                           (__byte_perm(code, 0u, 0x4441) << 7));
-        return __fmul2_rn(f2s(r), c);
+        r = mag(code);
+        return __fmul2_rn(f2s(r), cs2(code));
     }
 };
 extern __shared__ __align__(16) unsigned char a_dsm[];
@@ -898,7 +912,7 @@ __device__ __noinline__ void a_flush(const AGateParams *pp, const ATabData *cur,
     __syncwarp();  // the queue is free again
 }
 
-constexpr int A_DENSE_MINB = 3;  // CTAs per SM of the dense kernels (64 KiB of tables each)
+constexpr int A_DENSE_MINB = 2;  // CTAs per SM of the dense kernels (64 KiB of tables each)
 
 // Phase 1 (reading R-A4): exact min / max of the intermediate |z'|^2 of the
 // gate's output, through screens of increasing cost:
@@ -1016,41 +1030,51 @@ __global__ void __launch_bounds__(A_THREADS, A_BOUNDS_MINB) k_bounds_a(const __g
     double mn = INFINITY, mx = -INFINITY;  // exact, warp-wide
     float tlo = INFINITY, thi = -INFINITY;
     const uint32_t lt = (1u << lane) - 1u;
-    for (uint64_t vb = (uint64_t)blockIdx.x * A_THREADS + (threadIdx.x & ~31u); vb < units;
-         vb += (uint64_t)gridDim.x * A_THREADS) {
+    // the next unit's codes are loaded one iteration ahead (the loop is latency-bound
+    // on its loads otherwise: few warps per scheduler, a dependent chain per unit)
+    const uint64_t stride = (uint64_t)gridDim.x * A_THREADS;
+    uint4 w0 = make_uint4(0, 0, 0, 0), w1 = w0;
+    {
+        const uint64_t v = (uint64_t)blockIdx.x * A_THREADS + threadIdx.x;
+        if (v < units) U::load_raw(a, U::s0(v, p.t), p.t, w0, w1);
+    }
+    for (uint64_t vb = (uint64_t)blockIdx.x * A_THREADS + (threadIdx.x & ~31u); vb < units; vb += stride) {
         const uint64_t v = vb + (uint64_t)lane;
         uint32_t c[16], keys[8];
         uint32_t candm = 0;
         if (v < units) {
             const uint64_t s0 = U::s0(v, p.t);
-            U::load(a, s0, p.t, c);
+            U::unpack(w0, w1, c);
+            if (v + stride < units) U::load_raw(a, U::s0(v + stride, p.t), p.t, w0, w1);
             const bool hi_ok = !CTRL || (((p.shard_base | s0) & chi) == chi);
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const int j0 = U::j0(k), j1 = U::j1(k);
                 const int off = TL < 4 ? j0 : k;
                 const bool sel = !CTRL || (hi_ok && ((uint32_t)off & cl) == cl);
-                const float ra = L.rf[(c[j0] & 0xffu) * 32u], rb = L.rf[(c[j1] & 0xffu) * 32u];
+                const float ra = L.mag(c[j0]), rb = L.mag(c[j1]);
                 const float S = ra + rb;
                 const float eS = 1.4145e-6f * S;
                 // screen 0, magnitudes only: hi >= |z'_j| >= lo for both outputs
                 float hi, lo;
                 if (!CTRL || sel) {
                     hi = fmaf(p.mA, fmaxf(ra, rb), p.mB * fminf(ra, rb));
-                    lo = fminf(fabsf(fmaf(p.ma, ra, -p.mb * rb)), fabsf(fmaf(p.mb, ra, -p.ma * rb)));
+                    // (ma ra - mb rb, mb ra - ma rb) on one FFMA2
+                    const float2 T = __ffma2_rn(make_float2(p.ma, p.mb), f2s(ra),
+                                                __fmul2_rn(make_float2(-p.mb, -p.ma), f2s(rb)));
+                    lo = fminf(fabsf(T.x), fabsf(T.y));
                 } else {  // unselected: |z'| = (ra, rb); a zero code stays the exact zero special
                     hi = fmaxf(ra, rb);
                     lo = fminf(ra == 0.f ? INFINITY : ra, rb == 0.f ? INFINITY : rb);
                 }
                 bool cand = (S > 0.f) & ((fmaf(-3e-6f, S, lo) < tlo) | (hi > thi));
                 if (cand) {  // screen 1, fp32 gate: |z'| within sqrt2 E of |z'f|, mf within 4e-7 mf
-                    const float2 csa = L.cs[((c[j0] >> 8) & 0xffu) * 16u], csb = L.cs[((c[j1] >> 8) & 0xffu) * 16u];
-                    float2 x = make_float2(ra * csa.x, ra * csa.y), y = make_float2(rb * csb.x, rb * csb.y);
-                    if (sel) a_gate_fu<UK>(uf, x, y);
-                    const float m2x = fmaf(x.x, x.x, x.y * x.y), m2y = fmaf(y.x, y.x, y.y * y.y);
-                    float mfx = m2x * a_rsqrt(m2x), mfy = m2y * a_rsqrt(m2y);
-                    mfx = m2x > 0.f ? mfx : 0.f;
-                    mfy = m2y > 0.f ? mfy : 0.f;
+                    const float2 A = __fmul2_rn(f2s(ra), L.cs2(c[j0])), B = __fmul2_rn(f2s(rb), L.cs2(c[j1]));
+                    float2 RE = make_float2(A.x, B.x), IM = make_float2(A.y, B.y);
+                    if (sel) a_gate_f2<UK>(p.kf, A, B, RE, IM);
+                    const float2 m2 = __ffma2_rn(RE, RE, __fmul2_rn(IM, IM));
+                    const float2 mf2 = __fmul2_rn(m2, make_float2(a_rsqrt(m2.x), a_rsqrt(m2.y)));
+                    const float mfx = m2.x > 0.f ? mf2.x : 0.f, mfy = m2.y > 0.f ? mf2.y : 0.f;
                     // a certainly-zero output (|z'| < 1e-12, reading R-A5) is no intermediate:
                     // not a min candidate (the A states of the workloads hold many amplitudes
                     // at the 1e-12 floor, whose products straddle it)
@@ -1326,8 +1350,14 @@ __global__ void __launch_bounds__(A_THREADS, A_DENSE_MINB) k_apply_a(const __gri
 #pragma unroll
     for (int i = 0; i < 8; ++i) uf[i] = p.uf[i];
     const uint32_t lt = (1u << lane) - 1u;
-    for (uint64_t vb = (uint64_t)blockIdx.x * A_THREADS + (threadIdx.x & ~31u); vb < units;
-         vb += (uint64_t)gridDim.x * A_THREADS) {
+    // the next unit's codes are loaded one iteration ahead (as in k_bounds_a)
+    const uint64_t stride = (uint64_t)gridDim.x * A_THREADS;
+    uint4 w0 = make_uint4(0, 0, 0, 0), w1 = w0;
+    {
+        const uint64_t v = (uint64_t)blockIdx.x * A_THREADS + threadIdx.x;
+        if (v < units) U::load_raw(a, U::s0(v, p.t), p.t, w0, w1);
+    }
+    for (uint64_t vb = (uint64_t)blockIdx.x * A_THREADS + (threadIdx.x & ~31u); vb < units; vb += stride) {
         if (LAZY) {  // an output left the kept range somewhere: this pass is discarded, stop early
             int f = lane == 0 ? *reinterpret_cast<volatile int32_t *>(p.oor) : 0;
             if (__shfl_sync(0xffffffffu, f, 0)) break;
@@ -1338,7 +1368,8 @@ __global__ void __launch_bounds__(A_THREADS, A_DENSE_MINB) k_apply_a(const __gri
         uint64_t s0 = 0;
         if (v < units) {
             s0 = U::s0(v, p.t);
-            U::load(a, s0, p.t, c);
+            U::unpack(w0, w1, c);
+            if (v + stride < units) U::load_raw(a, U::s0(v + stride, p.t), p.t, w0, w1);
             const bool hi_ok = !CTRL || (((p.shard_base | s0) & chi) == chi);
             uint32_t nc[16];
 #pragma unroll
