@@ -72,7 +72,8 @@ struct qsim_state {
     qsim::QGroup *group = nullptr;  // QSIM_TRANSPORT_DEVICES: this handle drives P member handles
     int a_policy = 0;               // QSIM_A_POLICY_*
     int32_t *d_oor = nullptr;       // lazy policy: "an output left the kept range" flag
-    PersistGate *d_pg = nullptr, *h_pg = nullptr;  // qsim_apply_circuit_persistent: gate records
+    PersistGate *h_pg = nullptr;  // qsim_apply_circuit_persistent: gate records (physical bits)
+    void *d_pc = nullptr, *h_pc = nullptr;  // its phase / op records (device, pinned staging)
     size_t pg_cap = 0;
     int pass_r = 4;  // register qubits per pass stage (QSIM_PASS_R=5 selects 32-amplitude groups)
     int pass_k = LP_MAX_K;  // tile qubits of the relabelling pass (QSIM_LPASS_K = 9..12)
@@ -1061,7 +1062,8 @@ int qsim_destroy(qsim_state *s) {
         if (sh.amps2) cudaFree(sh.amps2);
     }
     if (s->d_oor) cudaFree(s->d_oor);
-    if (s->d_pg) cudaFree(s->d_pg);
+    if (s->d_pc) cudaFree(s->d_pc);
+    if (s->h_pc) cudaFreeHost(s->h_pc);
     if (s->h_pg) cudaFreeHost(s->h_pg);
     for (int k = 0; k < 2; ++k) {
         if (s->stage[k]) cudaFree(s->stage[k]);
@@ -1373,13 +1375,15 @@ int qsim_apply_circuit_persistent(qsim_state *s, const qsim_gate *gates, size_t 
     cudaSetDevice(s->dev);
     if (ngates > s->pg_cap) {
         CU(cudaStreamSynchronize(s->stream));
-        if (s->d_pg) cudaFree(s->d_pg);
         if (s->h_pg) cudaFreeHost(s->h_pg);
-        s->d_pg = nullptr;
         s->h_pg = nullptr;
         s->pg_cap = 0;
-        if (cudaMalloc(&s->d_pg, ngates * sizeof(PersistGate)) != cudaSuccess ||
-            cudaMallocHost(&s->h_pg, ngates * sizeof(PersistGate)) != cudaSuccess) {
+        if (s->d_pc) cudaFree(s->d_pc);
+        if (s->h_pc) cudaFreeHost(s->h_pc);
+        s->d_pc = s->h_pc = nullptr;
+        const size_t rec = sizeof(PersistOp) + sizeof(PersistPhase);
+        if (cudaMallocHost(&s->h_pg, ngates * sizeof(PersistGate)) != cudaSuccess ||
+            cudaMalloc(&s->d_pc, ngates * rec) != cudaSuccess || cudaMallocHost(&s->h_pc, ngates * rec) != cudaSuccess) {
             cudaGetLastError();
             set_error("qsim_apply_circuit_persistent: gate buffer allocation failed");
             return QSIM_ENOMEM;
@@ -1401,11 +1405,41 @@ int qsim_apply_circuit_persistent(qsim_state *s, const qsim_gate *gates, size_t 
         p.cmask = 0;
         for (int c = 0; c < g.ncontrols; ++c) p.cmask |= 1u << s->pl.pos[g.controls[c]];
     }
-    CU(cudaMemcpyAsync(s->d_pg, s->h_pg, ng * sizeof(PersistGate), cudaMemcpyHostToDevice, s->stream));
-    for (int k0 = 0; k0 < ng; k0 += PERSIST_MAX_GATES) {  // one launch per PERSIST_MAX_GATES records
+    // phases of gates on <= K qubits (persist.cu); the records go to the device in
+    // the pinned buffer (72 + 16 bytes per gate at most), one launch per
+    // PERSIST_MAX_GATES gates
+    int lcs = std::min(persist_lcs(), s->n - 3);
+    if (const char *e = getenv("QSIM_PERSIST_LCS")) lcs = std::max(1, std::min(atoi(e), std::min(4, s->n - 3)));
+    int K = persist_k(s->n, lcs);
+    if (const char *e = getenv("QSIM_PERSIST_K")) K = std::max(3, std::min(atoi(e), std::min(4, s->n - lcs)));
+    std::vector<PersistPhase> ph;
+    std::vector<PersistOp> ops;
+    std::vector<std::pair<int, int>> lens;  // (phases, ops) per launch
+    size_t bytes = 0;
+    for (int k0 = 0; k0 < ng; k0 += PERSIST_MAX_GATES) {
         const int kn = std::min(ng - k0, PERSIST_MAX_GATES);
+        persist_plan(s->h_pg + k0, kn, s->n, K, lcs, ph, ops);
+        std::memcpy(reinterpret_cast<char *>(s->h_pc) + bytes, ops.data(), ops.size() * sizeof(PersistOp));
+        std::memcpy(reinterpret_cast<char *>(s->h_pc) + bytes + ops.size() * sizeof(PersistOp), ph.data(),
+                    ph.size() * sizeof(PersistPhase));
+        bytes += ops.size() * sizeof(PersistOp) + ph.size() * sizeof(PersistPhase);
+        lens.emplace_back((int)ph.size(), (int)ops.size());
+        if (getenv("QSIM_PERSIST_DEBUG")) {
+            int rem = 0;
+            for (auto &x : ph) rem += x.remote != 0;
+            fprintf(stderr, "persist: n %d cluster %d K %d gates %d phases %zu remote %d\n", s->n, 1 << lcs, K, kn,
+                    ph.size(), rem);
+        }
+    }
+    CU(cudaMemcpyAsync(s->d_pc, s->h_pc, bytes, cudaMemcpyHostToDevice, s->stream));
+    size_t at = 0;
+    for (size_t c = 0; c < lens.size(); ++c) {
+        const int nph = lens[c].first, kn = lens[c].second;
+        const PersistOp *d_ops = reinterpret_cast<const PersistOp *>(reinterpret_cast<char *>(s->d_pc) + at);
+        const PersistPhase *d_ph = reinterpret_cast<const PersistPhase *>(d_ops + kn);
+        at += kn * sizeof(PersistOp) + nph * sizeof(PersistPhase);
         prof_begin(s);
-        if (launch_persist_e(s->shards[0].amps, s->n, s->d_pg + k0, kn, s->stream)) {
+        if (launch_persist_e(s->shards[0].amps, s->n, lcs, K, d_ph, nph, d_ops, kn, s->stream)) {
             set_error("qsim_apply_circuit_persistent: cluster launch failed");
             return QSIM_ECUDA;
         }

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 namespace qsim {
 
@@ -98,9 +99,29 @@ struct PersistGate {
     int32_t t;       // physical target bit
     uint32_t cmask;  // physical control bits (full index)
 };
-constexpr int PERSIST_MIN_N = 4, PERSIST_MAX_N = 16;  // 2^(N-3) amplitudes per CTA of an 8-CTA cluster
-constexpr int PERSIST_MAX_GATES = 1024;  // gate records staged in each CTA's shared memory (72 KiB)
-int launch_persist_e(void *a, int n, const PersistGate *g, int ngates, cudaStream_t s);
+constexpr int PERSIST_MIN_N = 4, PERSIST_MAX_N = 16;  // 2^(N-c) amplitudes per CTA of a 2^c-CTA cluster
+constexpr int PERSIST_MAX_GATES = 1024;  // records staged in each CTA's shared memory (<= 88 KiB)
+// one gate of a phase, in the phase's group coordinates (persist.cu)
+struct PersistOp {
+    double u[8];
+    uint32_t cout;  // control bits outside the phase's qubits (full index)
+    uint8_t m;      // target: its position in the phase's sorted qubit list
+    uint8_t cin;    // controls among the phase's qubits (group-index mask)
+    uint8_t kind;   // 0 dense, 1 diagonal, 2 anti-diagonal
+    uint8_t pad;
+};
+struct PersistPhase {
+    uint8_t q[4];   // the phase's K qubits, ascending
+    int32_t g0, ng; // its ops [g0, g0 + ng)
+    int32_t remote; // a qubit is a cluster-select bit
+};
+static_assert(sizeof(PersistOp) == 72 && sizeof(PersistPhase) == 16, "record layout");
+int persist_lcs();                // log2 of the cluster size this device runs (4 or 3)
+int persist_k(int n, int lcs);    // qubits per phase (4 or 3)
+int persist_plan(const PersistGate *g, int ngates, int n, int K, int lcs, std::vector<PersistPhase> &ph,
+                 std::vector<PersistOp> &ops);
+int launch_persist_e(void *a, int n, int lcs, int K, const PersistPhase *ph, int nph, const PersistOp *ops,
+                     int nops, cudaStream_t s);
 
 // ---- reductions (a10) ---------------------------------------------------------
 // Per-shard: out[0] = sum |a|^2, out[1 + q] = sum_{bit q = 1} |a|^2 for local q.

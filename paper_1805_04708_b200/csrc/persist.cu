@@ -1,19 +1,26 @@
 // persist.cu -- the "single persistent kernel" mode of SURVEY.md §8(d) config 1
 // (latency-bound small states, N <= 16): ONE launch applies a whole circuit.
 // The state lives in the distributed shared memory of a thread-block cluster
-// of 8 CTAs (CTA r holds amplitudes [r 2^(n-3), (r+1) 2^(n-3)), up to 128 KiB
-// each); every gate is one sweep over the pairs (Eq. NUM2, PAPER.md:285-307:
-// (a_i0, a_i1) <- U (a_i0, a_i1) for the pairs whose control bits are 1)
-// followed by a barrier.  A target inside a CTA's block pairs local
-// amplitudes (a CTA barrier suffices between such gates); a target among the
-// top 3 bits pairs a CTA with its partner CTA through DSMEM (the CTA with the
-// bit clear updates both) between two cluster barriers.  No host work between
-// gates and no HBM traffic between them.
+// (16 CTAs where the device allows the non-portable size, else 8; CTA r holds
+// amplitudes [r 2^(n-c), (r+1) 2^(n-c)), c = log2 of the cluster size).
+//
+// The gates are cut into phases: maximal runs of gates whose targets lie in a
+// set Q of K qubits (controls anywhere).  In a phase every thread loads
+// groups of 2^K amplitudes -- the amplitudes that differ only in the Q bits --
+// into registers, applies all of the phase's gates there (Eq. NUM2,
+// (a_i0, a_i1) <- U (a_i0, a_i1) for the pairs whose control
+// bits are 1; a control outside Q is one test per group), and stores them
+// back; one barrier per phase instead of one per gate.  A phase whose Q holds
+// a cluster-select bit reads and writes other CTAs' blocks through DSMEM
+// between two cluster barriers; a phase on local bits only needs the CTA's
+// own barrier.  No host work between gates and no HBM traffic between them.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
+#include <vector>
 
 #include "kernels.h"
 
@@ -21,98 +28,270 @@ namespace cg = cooperative_groups;
 
 namespace qsim {
 
-constexpr int PC_CTAS = 8;  // portable cluster size
-constexpr int PC_THREADS = 512;
+constexpr int PC_THREADS = 256;
 
-__global__ void __cluster_dims__(PC_CTAS, 1, 1) __launch_bounds__(PC_THREADS)
-    k_persist_e(double2 *__restrict__ a, int n, const PersistGate *__restrict__ g, int ngates) {
+// kind of a gate: 0 dense, 1 diagonal (u01 = u10 = 0), 2 anti-diagonal (u00 = u11 = 0);
+// the dropped terms are exact zeros, so every kind evaluates the general formula's value
+template <int K, int M>
+__device__ __forceinline__ void pc_apply(double2 (&v)[1 << K], const PersistOp &op) {
+    const double u0r = op.u[0], u0i = op.u[1], u1r = op.u[2], u1i = op.u[3];
+    const double u2r = op.u[4], u2i = op.u[5], u3r = op.u[6], u3i = op.u[7];
+    const uint32_t cin = op.cin;
+    if (op.kind == 1) {
+#pragma unroll
+        for (int k = 0; k < (1 << (K - 1)); ++k) {
+            const int j0 = ((k >> M) << (M + 1)) | (k & ((1 << M) - 1)), j1 = j0 | (1 << M);
+            if (((uint32_t)j0 & cin) != cin) continue;
+            const double2 x = v[j0], y = v[j1];
+            v[j0] = make_double2(fma(u0r, x.x, -u0i * x.y), fma(u0r, x.y, u0i * x.x));
+            v[j1] = make_double2(fma(u3r, y.x, -u3i * y.y), fma(u3r, y.y, u3i * y.x));
+        }
+    } else if (op.kind == 2) {
+#pragma unroll
+        for (int k = 0; k < (1 << (K - 1)); ++k) {
+            const int j0 = ((k >> M) << (M + 1)) | (k & ((1 << M) - 1)), j1 = j0 | (1 << M);
+            if (((uint32_t)j0 & cin) != cin) continue;
+            const double2 x = v[j0], y = v[j1];
+            v[j0] = make_double2(fma(u1r, y.x, -u1i * y.y), fma(u1r, y.y, u1i * y.x));
+            v[j1] = make_double2(fma(u2r, x.x, -u2i * x.y), fma(u2r, x.y, u2i * x.x));
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < (1 << (K - 1)); ++k) {
+            const int j0 = ((k >> M) << (M + 1)) | (k & ((1 << M) - 1)), j1 = j0 | (1 << M);
+            if (((uint32_t)j0 & cin) != cin) continue;
+            const double2 x = v[j0], y = v[j1];
+            v[j0] = make_double2(fma(u0r, x.x, fma(-u0i, x.y, fma(u1r, y.x, -u1i * y.y))),
+                                 fma(u0r, x.y, fma(u0i, x.x, fma(u1r, y.y, u1i * y.x))));
+            v[j1] = make_double2(fma(u2r, x.x, fma(-u2i, x.y, fma(u3r, y.x, -u3i * y.y))),
+                                 fma(u2r, x.y, fma(u2i, x.x, fma(u3r, y.y, u3i * y.x))));
+        }
+    }
+}
+
+template <int K>
+__global__ void __launch_bounds__(PC_THREADS) k_persist_e(double2 *__restrict__ a, int n, int lcs,
+                                                          const PersistPhase *__restrict__ ph, int nph,
+                                                          const PersistOp *__restrict__ ops, int nops) {
+    constexpr int R = 1 << K;
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ __align__(16) double2 pc_sh[];
     const int rank = (int)cluster.block_rank();
-    const int lb = n - 3;  // local bits of a CTA's block
+    const int cs = 1 << lcs;
+    const int lb = n - lcs;  // local bits of a CTA's block
     const uint32_t S = 1u << lb;
     double2 *mine = pc_sh;
-    PersistGate *gs = reinterpret_cast<PersistGate *>(pc_sh + S);  // the gate records, staged once
+    PersistOp *os = reinterpret_cast<PersistOp *>(pc_sh + S);  // the records, staged once
+    PersistPhase *ps = reinterpret_cast<PersistPhase *>(os + nops);
     for (uint32_t j = threadIdx.x; j < S; j += PC_THREADS) mine[j] = a[(size_t)rank * S + j];
-    for (int k = threadIdx.x; k < ngates * (int)(sizeof(PersistGate) / 8); k += PC_THREADS)
-        reinterpret_cast<double *>(gs)[k] = reinterpret_cast<const double *>(g)[k];
+    for (int k = threadIdx.x; k < nops * (int)(sizeof(PersistOp) / 8); k += PC_THREADS)
+        reinterpret_cast<double *>(os)[k] = reinterpret_cast<const double *>(ops)[k];
+    for (int k = threadIdx.x; k < nph * (int)(sizeof(PersistPhase) / 8); k += PC_THREADS)
+        reinterpret_cast<double *>(ps)[k] = reinterpret_cast<const double *>(ph)[k];
     cluster.sync();
-    bool synced = true;  // the cluster has synchronised since the last gate
-    for (int k = 0; k < ngates; ++k) {
-        const PersistGate &G = gs[k];
-        const int t = G.t;
-        // a gate on a cluster-select bit reads / writes a partner CTA's block: the
-        // whole cluster must be done with the previous gate; a local gate only
-        // needs this CTA done with it
-        if (t >= lb && !synced) cluster.sync();
-        const double u0r = G.u[0], u0i = G.u[1], u1r = G.u[2], u1i = G.u[3];
-        const double u2r = G.u[4], u2i = G.u[5], u3r = G.u[6], u3i = G.u[7];
-        const uint32_t cmask = G.cmask;
-        double2 *p0, *p1;
-        uint32_t base, npairs, q0;
-        if (t < lb) {
-            p0 = p1 = mine;
-            base = (uint32_t)rank * S;
-            npairs = S >> 1;
-            q0 = 0;
-        } else {
-            // the CTA pair (r, r | bit) shares the S pairs: each takes half, with its own
-            // block on one side of every pair and the partner's on the other
-            const int cb = t - lb;
-            const int lo = rank & ~(1 << cb), hi = rank | (1 << cb);
-            p0 = cluster.map_shared_rank(mine, lo);
-            p1 = cluster.map_shared_rank(mine, hi);
-            base = (uint32_t)lo * S;
-            npairs = S >> 1;
-            q0 = (rank >> cb) & 1 ? S >> 1 : 0;
-        }
-        for (uint32_t q = threadIdx.x; q < npairs; q += PC_THREADS) {
-            uint32_t j0, j1;
-            if (t < lb) {
-                j0 = ((q >> t) << (t + 1)) | (q & ((1u << t) - 1u));
-                j1 = j0 | (1u << t);
-            } else {
-                j0 = j1 = q0 + q;
-            }
-            const uint32_t i0 = base | j0;  // full index of the |0> member (controls tested on it)
-            if ((i0 & cmask) != cmask) continue;
-            const double2 x = p0[j0], y = p1[j1];
-            double2 nx, ny;
-            nx.x = fma(u0r, x.x, fma(-u0i, x.y, fma(u1r, y.x, -u1i * y.y)));
-            nx.y = fma(u0r, x.y, fma(u0i, x.x, fma(u1r, y.y, u1i * y.x)));
-            ny.x = fma(u2r, x.x, fma(-u2i, x.y, fma(u3r, y.x, -u3i * y.y)));
-            ny.y = fma(u2r, x.y, fma(u2i, x.x, fma(u3r, y.y, u3i * y.x)));
-            p0[j0] = nx;
-            p1[j1] = ny;
-        }
-        if (t >= lb) {
-            cluster.sync();  // the partner's block is written: visible before anyone's next gate
-            synced = true;
-        } else {
+    const uint32_t G = 1u << (n - K), gpc = G / cs;  // groups, per CTA
+    bool prev_remote = true;                         // the staging above counts as remote
+    for (int p = 0; p < nph; ++p) {
+        const PersistPhase P = ps[p];
+        const bool remote = P.remote != 0;
+        if (remote || prev_remote)
+            cluster.sync();
+        else
             __syncthreads();
-            synced = false;
+        prev_remote = remote;
+        uint32_t off[R];  // member offsets of a group: the Q bits of j
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            uint32_t o = 0;
+#pragma unroll
+            for (int b = 0; b < K; ++b)
+                if ((j >> b) & 1) o |= 1u << P.q[b];
+            off[j] = o;
+        }
+        for (uint32_t gi = (uint32_t)rank * gpc + threadIdx.x; gi < (uint32_t)(rank + 1) * gpc; gi += PC_THREADS) {
+            uint32_t base = gi;  // zeros inserted at the Q positions (ascending)
+#pragma unroll
+            for (int b = 0; b < K; ++b) {
+                const uint32_t q = P.q[b];
+                base = ((base >> q) << (q + 1)) | (base & ((1u << q) - 1u));
+            }
+            double2 v[R];
+            if (!remote) {  // the group lies in this CTA's block
+                const uint32_t lo = base & (S - 1u);
+#pragma unroll
+                for (int j = 0; j < R; ++j) v[j] = mine[lo | off[j]];
+            } else {
+#pragma unroll
+                for (int j = 0; j < R; ++j) {
+                    const uint32_t i = base | off[j];
+                    v[j] = *cluster.map_shared_rank(mine + (i & (S - 1u)), (int)(i >> lb));
+                }
+            }
+            for (int g = P.g0; g < P.g0 + P.ng; ++g) {
+                const PersistOp &op = os[g];
+                if ((base & op.cout) != op.cout) continue;
+                switch (op.m) {
+                    case 0: pc_apply<K, 0>(v, op); break;
+                    case 1: pc_apply<K, 1>(v, op); break;
+                    case 2: pc_apply<K, 2>(v, op); break;
+                    default:
+                        if (K > 3) pc_apply<K, (K > 3 ? 3 : 0)>(v, op);
+                        break;
+                }
+            }
+            if (!remote) {
+                const uint32_t lo = base & (S - 1u);
+#pragma unroll
+                for (int j = 0; j < R; ++j) mine[lo | off[j]] = v[j];
+            } else {
+#pragma unroll
+                for (int j = 0; j < R; ++j) {
+                    const uint32_t i = base | off[j];
+                    *cluster.map_shared_rank(mine + (i & (S - 1u)), (int)(i >> lb)) = v[j];
+                }
+            }
         }
     }
     cluster.sync();
     for (uint32_t j = threadIdx.x; j < S; j += PC_THREADS) a[(size_t)rank * S + j] = mine[j];
 }
 
-int launch_persist_e(void *a, int n, const PersistGate *g, int ngates, cudaStream_t s) {
-    if (n < PERSIST_MIN_N || n > PERSIST_MAX_N || ngates > PERSIST_MAX_GATES) return -1;
-    const size_t smem = (sizeof(double2) << n) / PC_CTAS + (size_t)ngates * sizeof(PersistGate);
-    static std::atomic<uint64_t> attr_devs{0};  // the >48 KiB opt-in is per device
+// Phases (host): a gate whose target is not in the current Q starts a new
+// phase once Q holds K qubits; a closed Q is padded with the lowest unused
+// qubits (preferring local ones) and sorted; each gate becomes an op in the
+// phase's coordinates (target position m, controls inside Q as a group-index
+// mask, controls outside as a full-index mask).
+static int kind_of(const double *u) {
+    if (u[2] == 0.0 && u[3] == 0.0 && u[4] == 0.0 && u[5] == 0.0) return 1;
+    if (u[0] == 0.0 && u[1] == 0.0 && u[6] == 0.0 && u[7] == 0.0) return 2;
+    return 0;
+}
+int persist_plan(const PersistGate *g, int ngates, int n, int K, int lcs, std::vector<PersistPhase> &ph,
+                 std::vector<PersistOp> &ops) {
+    ph.clear();
+    ops.clear();
+    const int lb = n - lcs;
+    int start = 0;
+    std::vector<int> Q;
+    auto close = [&](int end) {
+        if (end <= start) return;
+        std::vector<int> q = Q;
+        for (int b = 0; (int)q.size() < K && b < n; ++b)
+            if (std::find(q.begin(), q.end(), b) == q.end()) q.push_back(b);
+        std::sort(q.begin(), q.end());
+        PersistPhase P{};
+        uint32_t qm = 0;
+        for (int b = 0; b < K; ++b) {
+            P.q[b] = (uint8_t)q[b];
+            qm |= 1u << q[b];
+            if (q[b] >= lb) P.remote = 1;
+        }
+        P.g0 = (int32_t)ops.size();
+        for (int k = start; k < end; ++k) {
+            PersistOp o{};
+            for (int i = 0; i < 8; ++i) o.u[i] = g[k].u[i];
+            o.kind = (uint8_t)kind_of(g[k].u);
+            for (int b = 0; b < K; ++b) {
+                if (q[b] == g[k].t) o.m = (uint8_t)b;
+                if ((g[k].cmask >> q[b]) & 1u) o.cin |= (uint8_t)(1u << b);
+            }
+            o.cout = g[k].cmask & ~qm;
+            ops.push_back(o);
+        }
+        P.ng = (int32_t)(ops.size() - P.g0);
+        ph.push_back(P);
+        start = end;
+        Q.clear();
+    };
+    for (int k = 0; k < ngates; ++k) {
+        const int t = g[k].t;
+        if (std::find(Q.begin(), Q.end(), t) == Q.end()) {
+            if ((int)Q.size() == K) close(k);
+            Q.push_back(t);
+        }
+    }
+    close(ngates);
+    return 0;
+}
+
+template <int K>
+static int launch_k(void *a, int n, int lcs, const PersistPhase *ph, int nph, const PersistOp *ops, int nops,
+                    cudaStream_t s) {
+    const size_t smem = (sizeof(double2) << (n - lcs)) + (size_t)nops * sizeof(PersistOp) +
+                        (size_t)nph * sizeof(PersistPhase);
+    static std::atomic<uint64_t> attr_devs{0};  // the >48 KiB opt-in and the 16-CTA cluster are per device
     int dev = 0;
     cudaGetDevice(&dev);
     const uint64_t bit = 1ull << (dev & 63);
     if (!(attr_devs.load() & bit)) {
-        if (cudaFuncSetAttribute(k_persist_e, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)((sizeof(double2) << PERSIST_MAX_N) / PC_CTAS +
-                                       PERSIST_MAX_GATES * sizeof(PersistGate))) != cudaSuccess)
+        if (cudaFuncSetAttribute(k_persist_e<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
+                cudaSuccess ||
+            cudaFuncSetAttribute(k_persist_e<K>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+            cudaGetLastError();
             return -1;
+        }
         attr_devs.fetch_or(bit);
     }
-    k_persist_e<<<PC_CTAS, PC_THREADS, smem, s>>>(reinterpret_cast<double2 *>(a), n, g, ngates);
-    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(1u << lcs);
+    cfg.blockDim = dim3(PC_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 1u << lcs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, k_persist_e<K>, reinterpret_cast<double2 *>(a), n, lcs, ph, nph, ops, nops) !=
+        cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    return 0;
+}
+
+// the cluster size this device runs (16 if a 16-CTA cluster with the largest
+// block fits, else 8); cached per device
+int persist_lcs() {
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int c = cache[dev & 63].load();
+    if (c) return c;
+    int lcs = 3;
+    if (cudaFuncSetAttribute(k_persist_e<4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+        cudaFuncSetAttribute(k_persist_e<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) ==
+            cudaSuccess) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(16);
+        cfg.blockDim = dim3(PC_THREADS);
+        cfg.dynamicSmemBytes = 200 * 1024;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 16;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int nc = 0;
+        if (cudaOccupancyMaxActiveClusters(&nc, k_persist_e<4>, &cfg) == cudaSuccess && nc > 0) lcs = 4;
+    }
+    cudaGetLastError();
+    cache[dev & 63].store(lcs);
+    return lcs;
+}
+
+// K = 4 (16-amplitude groups) when each CTA still has a full block of groups,
+// else 3
+int persist_k(int n, int lcs) { return (n - 4 - lcs >= 8) ? 4 : 3; }
+
+int launch_persist_e(void *a, int n, int lcs, int K, const PersistPhase *ph, int nph, const PersistOp *ops,
+                     int nops, cudaStream_t s) {
+    if (n < PERSIST_MIN_N || n > PERSIST_MAX_N || nops > PERSIST_MAX_GATES || nph > nops) return -1;
+    if ((K != 3 && K != 4) || n - lcs < K) return -1;
+    return K == 4 ? launch_k<4>(a, n, lcs, ph, nph, ops, nops, s) : launch_k<3>(a, n, lcs, ph, nph, ops, nops, s);
 }
 
 }  // namespace qsim

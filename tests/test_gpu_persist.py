@@ -63,3 +63,19 @@ def test_mixed_with_the_ordinary_path_and_errors():
     with q.State(12, q.ENC_ADAPTIVE2) as s, pytest.raises(q.QsimError) as err:
         s.apply_circuit_persistent(C.h_wall(12))
     assert err.value.code == -7
+
+
+@pytest.mark.parametrize("lcs,K", [(3, 3), (3, 4), (4, 3), (4, 4)])
+def test_cluster_sizes_and_phase_widths(lcs, K, monkeypatch):
+    """Every cluster size (8 / 16 CTAs) and phase width (K = 3 / 4 qubits per
+    register group) the kernel can run, against the oracle: phases on local
+    bits, phases holding cluster-select bits (DSMEM), controls inside and
+    outside a phase's qubits."""
+    monkeypatch.setenv("QSIM_PERSIST_LCS", str(lcs))
+    monkeypatch.setenv("QSIM_PERSIST_K", str(K))
+    for n in (12, 15):
+        circ = C.config(0, n=n, seed=n + K)
+        with q.State(n) as s:
+            s.apply_circuit_persistent(circ)
+            z = s.get_state()
+        assert np.max(np.abs(z - oracle.e_simulate(n, circ))) <= TOL
