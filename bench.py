@@ -78,7 +78,7 @@ class ClockSampler:
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_power_cap,memory.used,memory.total")
 
     def __init__(self, device):
         self.device = device
@@ -107,7 +107,7 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        sm, smax, reasons = [], None, set()
+        sm, smax, reasons, mem, memtot, pw = [], None, set(), [], None, []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
@@ -121,8 +121,20 @@ class ClockSampler:
             for nm, v in zip(names, parts[4:8]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+            try:
+                pw.append(float(parts[3]))
+                mem.append(float(parts[8]))
+                memtot = float(parts[9])
+            except (ValueError, IndexError):
+                pass
+        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+               "samples": len(sm)}
+        if pw:
+            out["power_w_median"] = statistics.median(pw)
+        if mem:  # device memory in use during the timed region (the shard plus buffers fit)
+            out["memory_used_gib_max"] = max(mem) / 1024.0
+            out["memory_total_gib"] = memtot / 1024.0 if memtot else None
+        return out
 
 
 def workload(world):
