@@ -72,8 +72,16 @@ struct qsim_state {
     qsim::QGroup *group = nullptr;  // QSIM_TRANSPORT_DEVICES: this handle drives P member handles
     int a_policy = 0;               // QSIM_A_POLICY_*
     int32_t *d_oor = nullptr;       // lazy policy: "an output left the kept range" flag
-    PersistGate *h_pg = nullptr;  // qsim_apply_circuit_persistent: gate records (physical bits)
-    void *d_pc = nullptr, *h_pc = nullptr;  // its phase / op records (device, pinned staging)
+    std::vector<PersistGate> h_pg;  // qsim_apply_circuit_persistent: gate records (physical bits)
+    void *h_pc = nullptr;           // pinned staging of its phase / op records
+    struct PcEntry {                // planned circuits (device records), keyed by the physical gate list
+        uint64_t key = 0, stamp = 0;
+        int lcs = 0, K = 0;
+        void *d = nullptr;
+        std::vector<std::pair<int, int>> lens;  // (phases, ops) per launch
+    };
+    std::vector<PcEntry> pc_cache;
+    uint64_t pc_clock = 0;
     size_t pg_cap = 0;
     int pass_r = 4;  // register qubits per pass stage (QSIM_PASS_R=5 selects 32-amplitude groups)
     int pass_k = LP_MAX_K;  // tile qubits of the relabelling pass (QSIM_LPASS_K = 9..12)
@@ -1062,9 +1070,9 @@ int qsim_destroy(qsim_state *s) {
         if (sh.amps2) cudaFree(sh.amps2);
     }
     if (s->d_oor) cudaFree(s->d_oor);
-    if (s->d_pc) cudaFree(s->d_pc);
+    for (auto &e : s->pc_cache)
+        if (e.d) cudaFree(e.d);
     if (s->h_pc) cudaFreeHost(s->h_pc);
-    if (s->h_pg) cudaFreeHost(s->h_pg);
     for (int k = 0; k < 2; ++k) {
         if (s->stage[k]) cudaFree(s->stage[k]);
         if (s->ev_recv[k]) cudaEventDestroy(s->ev_recv[k]);
@@ -1373,25 +1381,8 @@ int qsim_apply_circuit_persistent(qsim_state *s, const qsim_gate *gates, size_t 
     RC(validate_gates(s->n, gates, ngates, true));
     if (!ngates) return QSIM_OK;
     cudaSetDevice(s->dev);
-    if (ngates > s->pg_cap) {
-        CU(cudaStreamSynchronize(s->stream));
-        if (s->h_pg) cudaFreeHost(s->h_pg);
-        s->h_pg = nullptr;
-        s->pg_cap = 0;
-        if (s->d_pc) cudaFree(s->d_pc);
-        if (s->h_pc) cudaFreeHost(s->h_pc);
-        s->d_pc = s->h_pc = nullptr;
-        const size_t rec = sizeof(PersistOp) + sizeof(PersistPhase);
-        if (cudaMallocHost(&s->h_pg, ngates * sizeof(PersistGate)) != cudaSuccess ||
-            cudaMalloc(&s->d_pc, ngates * rec) != cudaSuccess || cudaMallocHost(&s->h_pc, ngates * rec) != cudaSuccess) {
-            cudaGetLastError();
-            set_error("qsim_apply_circuit_persistent: gate buffer allocation failed");
-            return QSIM_ENOMEM;
-        }
-        s->pg_cap = ngates;
-    }
-    CU(cudaStreamSynchronize(s->stream));  // the pinned staging buffer is reused
     // logical -> physical through the qubit map; SWAP records relabel it (0 bytes)
+    s->h_pg.resize(ngates);
     int ng = 0;
     for (size_t k = 0; k < ngates; ++k) {
         const qsim_gate &g = gates[k];
@@ -1405,37 +1396,83 @@ int qsim_apply_circuit_persistent(qsim_state *s, const qsim_gate *gates, size_t 
         p.cmask = 0;
         for (int c = 0; c < g.ncontrols; ++c) p.cmask |= 1u << s->pl.pos[g.controls[c]];
     }
-    // phases of gates on <= K qubits (persist.cu); the records go to the device in
-    // the pinned buffer (72 + 16 bytes per gate at most), one launch per
-    // PERSIST_MAX_GATES gates
+    if (!ng) return QSIM_OK;
     int lcs = std::min(persist_lcs(), s->n - 3);
     if (const char *e = getenv("QSIM_PERSIST_LCS")) lcs = std::max(1, std::min(atoi(e), std::min(4, s->n - 3)));
     int K = persist_k(s->n, lcs);
     if (const char *e = getenv("QSIM_PERSIST_K")) K = std::max(3, std::min(atoi(e), std::min(4, s->n - lcs)));
-    std::vector<PersistPhase> ph;
-    std::vector<PersistOp> ops;
-    std::vector<std::pair<int, int>> lens;  // (phases, ops) per launch
-    size_t bytes = 0;
-    for (int k0 = 0; k0 < ng; k0 += PERSIST_MAX_GATES) {
-        const int kn = std::min(ng - k0, PERSIST_MAX_GATES);
-        persist_plan(s->h_pg + k0, kn, s->n, K, lcs, ph, ops);
-        std::memcpy(reinterpret_cast<char *>(s->h_pc) + bytes, ops.data(), ops.size() * sizeof(PersistOp));
-        std::memcpy(reinterpret_cast<char *>(s->h_pc) + bytes + ops.size() * sizeof(PersistOp), ph.data(),
-                    ph.size() * sizeof(PersistPhase));
-        bytes += ops.size() * sizeof(PersistOp) + ph.size() * sizeof(PersistPhase);
-        lens.emplace_back((int)ph.size(), (int)ops.size());
-        if (getenv("QSIM_PERSIST_DEBUG")) {
-            int rem = 0;
-            for (auto &x : ph) rem += x.remote != 0;
-            fprintf(stderr, "persist: n %d cluster %d K %d gates %d phases %zu remote %d\n", s->n, 1 << lcs, K, kn,
-                    ph.size(), rem);
-        }
+    // a circuit seen before (same physical records, size and shape) replays its
+    // device records: no planning, no upload, no host synchronisation
+    uint64_t key = 1469598103934665603ull;
+    {
+        const unsigned char *b = reinterpret_cast<const unsigned char *>(s->h_pg.data());
+        for (size_t i = 0; i < (size_t)ng * sizeof(PersistGate); ++i) key = (key ^ b[i]) * 1099511628211ull;
+        key ^= ((uint64_t)s->n << 48) ^ ((uint64_t)lcs << 40) ^ ((uint64_t)K << 32) ^ (uint64_t)ng;
     }
-    CU(cudaMemcpyAsync(s->d_pc, s->h_pc, bytes, cudaMemcpyHostToDevice, s->stream));
+    qsim_state::PcEntry *ent = nullptr;
+    for (auto &e : s->pc_cache)
+        if (e.d && e.key == key && e.lcs == lcs && e.K == K) ent = &e;
+    if (!ent) {
+        // phases of gates on <= K qubits (persist.cu), one launch per PERSIST_MAX_GATES gates
+        std::vector<PersistPhase> ph;
+        std::vector<PersistOp> ops;
+        std::vector<std::pair<int, int>> lens;
+        std::vector<char> rec;
+        for (int k0 = 0; k0 < ng; k0 += PERSIST_MAX_GATES) {
+            const int kn = std::min(ng - k0, PERSIST_MAX_GATES);
+            if (persist_plan(s->h_pg.data() + k0, kn, s->n, K, lcs, ph, ops)) {
+                set_error("qsim_apply_circuit_persistent: phase planning failed");
+                return QSIM_EINVAL;
+            }
+            const size_t o = rec.size();
+            rec.resize(o + ops.size() * sizeof(PersistOp) + ph.size() * sizeof(PersistPhase));
+            std::memcpy(rec.data() + o, ops.data(), ops.size() * sizeof(PersistOp));
+            std::memcpy(rec.data() + o + ops.size() * sizeof(PersistOp), ph.data(), ph.size() * sizeof(PersistPhase));
+            lens.emplace_back((int)ph.size(), (int)ops.size());
+            if (getenv("QSIM_PERSIST_DEBUG")) {
+                int rem = 0;
+                for (auto &x : ph) rem += x.remote != 0;
+                fprintf(stderr, "persist: n %d cluster %d K %d gates %d phases %zu remote %d\n", s->n, 1 << lcs, K,
+                        kn, ph.size(), rem);
+            }
+        }
+        // the entry to (re)use: a free slot, else the least recently used of 8
+        if (s->pc_cache.size() < 8) s->pc_cache.emplace_back();
+        ent = &s->pc_cache[0];
+        for (auto &e : s->pc_cache)
+            if (!e.d || e.stamp < ent->stamp) ent = &e;
+        CU(cudaStreamSynchronize(s->stream));  // the pinned staging and an evicted entry are free
+        if (ent->d) cudaFree(ent->d);
+        ent->d = nullptr;
+        if (rec.size() > s->pg_cap) {
+            if (s->h_pc) cudaFreeHost(s->h_pc);
+            s->h_pc = nullptr;
+            s->pg_cap = 0;
+            if (cudaMallocHost(&s->h_pc, rec.size()) != cudaSuccess) {
+                cudaGetLastError();
+                set_error("qsim_apply_circuit_persistent: staging allocation failed");
+                return QSIM_ENOMEM;
+            }
+            s->pg_cap = rec.size();
+        }
+        if (cudaMalloc(&ent->d, rec.size()) != cudaSuccess) {
+            cudaGetLastError();
+            ent->d = nullptr;
+            set_error("qsim_apply_circuit_persistent: record buffer allocation failed");
+            return QSIM_ENOMEM;
+        }
+        std::memcpy(s->h_pc, rec.data(), rec.size());
+        CU(cudaMemcpyAsync(ent->d, s->h_pc, rec.size(), cudaMemcpyHostToDevice, s->stream));
+        ent->key = key;
+        ent->lcs = lcs;
+        ent->K = K;
+        ent->lens = lens;
+    }
+    ent->stamp = ++s->pc_clock;
     size_t at = 0;
-    for (size_t c = 0; c < lens.size(); ++c) {
-        const int nph = lens[c].first, kn = lens[c].second;
-        const PersistOp *d_ops = reinterpret_cast<const PersistOp *>(reinterpret_cast<char *>(s->d_pc) + at);
+    for (size_t c = 0; c < ent->lens.size(); ++c) {
+        const int nph = ent->lens[c].first, kn = ent->lens[c].second;
+        const PersistOp *d_ops = reinterpret_cast<const PersistOp *>(reinterpret_cast<char *>(ent->d) + at);
         const PersistPhase *d_ph = reinterpret_cast<const PersistPhase *>(d_ops + kn);
         at += kn * sizeof(PersistOp) + nph * sizeof(PersistPhase);
         prof_begin(s);

@@ -156,11 +156,18 @@ __global__ void __launch_bounds__(PC_THREADS) k_persist_e(double2 *__restrict__ 
     for (uint32_t j = threadIdx.x; j < S; j += PC_THREADS) a[(size_t)rank * S + j] = mine[j];
 }
 
-// Phases (host): a gate whose target is not in the current Q starts a new
-// phase once Q holds K qubits; a closed Q is padded with the lowest unused
-// qubits (preferring local ones) and sorted; each gate becomes an op in the
-// phase's coordinates (target position m, controls inside Q as a group-index
-// mask, controls outside as a full-index mask).
+// Phases (host).  Gates on disjoint qubit sets commute, so the host may
+// reorder them: each qubit keeps the queue of its gates (target and
+// controls) in program order, and a gate is ready when it heads the queues
+// of all its qubits.  A phase takes ready gates whose target is in its set Q
+// (<= K qubits) or can join it.  Remote phases (Q holding a cluster-select
+// bit) cost DSMEM traffic and cluster barriers, so a phase stays local while
+// a ready gate with a local target exists, and a remote phase then takes the
+// ready remote gates first -- batching them.  A closed Q is padded with the
+// lowest unused qubits and sorted; each gate becomes an op in the phase's
+// coordinates (target position m, controls inside Q as a group-index mask,
+// controls outside as a full-index mask).  The reordering changes only the
+// rounding order (products of commuting 2x2 factors).
 static int kind_of(const double *u) {
     if (u[2] == 0.0 && u[3] == 0.0 && u[4] == 0.0 && u[5] == 0.0) return 1;
     if (u[0] == 0.0 && u[1] == 0.0 && u[6] == 0.0 && u[7] == 0.0) return 2;
@@ -171,10 +178,58 @@ int persist_plan(const PersistGate *g, int ngates, int n, int K, int lcs, std::v
     ph.clear();
     ops.clear();
     const int lb = n - lcs;
-    int start = 0;
-    std::vector<int> Q;
-    auto close = [&](int end) {
-        if (end <= start) return;
+    std::vector<std::vector<int>> qq(n);  // per qubit: its gates in program order
+    std::vector<size_t> head(n, 0);
+    auto touches = [&](int k) { return g[k].cmask | (1u << g[k].t); };
+    for (int k = 0; k < ngates; ++k)
+        for (int b = 0; b < n; ++b)
+            if ((touches(k) >> b) & 1u) qq[b].push_back(k);
+    auto ready = [&](int k) {
+        const uint32_t m = touches(k);
+        for (int b = 0; b < n; ++b)
+            if (((m >> b) & 1u) && (head[b] >= qq[b].size() || qq[b][head[b]] != k)) return false;
+        return true;
+    };
+    int left = ngates;
+    std::vector<int> Q, sel;
+    while (left > 0) {
+        Q.clear();
+        sel.clear();
+        // the phase is local if some ready gate has a local target
+        bool remote_phase = true;
+        for (int b = 0; b < n && remote_phase; ++b)
+            if (head[b] < qq[b].size()) {
+                const int k = qq[b][head[b]];
+                if (g[k].t < lb && ready(k)) remote_phase = false;
+            }
+        for (;;) {
+            // the next gate: ready, target in Q (lowest program index), else one that can
+            // join Q (remote targets first in a remote phase, none in a local one)
+            int best = -1, bestjoin = -1;
+            for (int b = 0; b < n; ++b) {
+                if (head[b] >= qq[b].size()) continue;
+                const int k = qq[b][head[b]];
+                if (!ready(k)) continue;
+                const int t = g[k].t;
+                const bool inq = std::find(Q.begin(), Q.end(), t) != Q.end();
+                if (inq) {
+                    if (best < 0 || k < best) best = k;
+                } else if ((int)Q.size() < K && (remote_phase || t < lb)) {
+                    const bool pref = remote_phase ? t >= lb : true;
+                    const bool bpref = bestjoin >= 0 && (remote_phase ? g[bestjoin].t >= lb : true);
+                    if (bestjoin < 0 || (pref && !bpref) || (pref == bpref && k < bestjoin)) bestjoin = k;
+                }
+            }
+            const int k = best >= 0 ? best : bestjoin;
+            if (k < 0) break;
+            if (best < 0) Q.push_back(g[k].t);
+            sel.push_back(k);
+            const uint32_t m = touches(k);
+            for (int b = 0; b < n; ++b)
+                if ((m >> b) & 1u) ++head[b];
+            --left;
+        }
+        if (sel.empty()) return -1;  // cannot happen: the lowest unscheduled gate is always ready
         std::vector<int> q = Q;
         for (int b = 0; (int)q.size() < K && b < n; ++b)
             if (std::find(q.begin(), q.end(), b) == q.end()) q.push_back(b);
@@ -187,7 +242,7 @@ int persist_plan(const PersistGate *g, int ngates, int n, int K, int lcs, std::v
             if (q[b] >= lb) P.remote = 1;
         }
         P.g0 = (int32_t)ops.size();
-        for (int k = start; k < end; ++k) {
+        for (int k : sel) {
             PersistOp o{};
             for (int i = 0; i < 8; ++i) o.u[i] = g[k].u[i];
             o.kind = (uint8_t)kind_of(g[k].u);
@@ -200,17 +255,7 @@ int persist_plan(const PersistGate *g, int ngates, int n, int K, int lcs, std::v
         }
         P.ng = (int32_t)(ops.size() - P.g0);
         ph.push_back(P);
-        start = end;
-        Q.clear();
-    };
-    for (int k = 0; k < ngates; ++k) {
-        const int t = g[k].t;
-        if (std::find(Q.begin(), Q.end(), t) == Q.end()) {
-            if ((int)Q.size() == K) close(k);
-            Q.push_back(t);
-        }
     }
-    close(ngates);
     return 0;
 }
 

@@ -79,3 +79,23 @@ def test_cluster_sizes_and_phase_widths(lcs, K, monkeypatch):
             s.apply_circuit_persistent(circ)
             z = s.get_state()
         assert np.max(np.abs(z - oracle.e_simulate(n, circ))) <= TOL
+
+
+def test_planned_circuit_cache():
+    """A gate list seen before replays its device records (no planning, no
+    upload): the same circuit twice, another in between, more circuits than
+    the cache holds, and a relabel (SWAP) changing the physical records."""
+    n = 13
+    cs = [C.config(0, n=n, seed=20 + i) for i in range(10)]
+    order = [0, 0, 1, 0, 2, 3, 4, 5, 6, 7, 8, 9, 0, 1]
+    ref = oracle.e_init(n)
+    with q.State(n) as s:
+        for i in order:
+            s.apply_circuit_persistent(cs[i])
+            ref = oracle.e_run(ref, n, cs[i])
+        sw = C.Circuit(n).swap(0, n - 1)
+        s.apply_circuit_persistent(sw)
+        s.apply_circuit_persistent(cs[0])
+        ref = oracle.e_run(oracle.e_run(ref, n, sw), n, cs[0])
+        z = s.get_state()
+    assert np.max(np.abs(z - ref)) <= TOL
