@@ -583,7 +583,8 @@ struct AFLane {
     }
     // the byte offsets of both tables are raw * 128
     __device__ __forceinline__ float mag(uint32_t code) const {
-        return *reinterpret_cast<const float *>(reinterpret_cast<const char *>(rf) + ((code & 0xffu) << 7));
+        return *reinterpret_cast<const float *>(reinterpret_cast<const char *>(rf) +
+                                                (__byte_perm(code, 0u, 0x4440) << 7));
     }
     __device__ __forceinline__ float2 cs2(uint32_t code) const {
         return *reinterpret_cast<const float2 *>(reinterpret_cast<const char *>(cs) +
@@ -782,10 +783,11 @@ template <bool LAZY>
 __device__ __forceinline__ void a_encode_f2(const AEncF &ce, float2 re, float2 im, float errm, float KE, float eS,
                                             uint32_t &cx, uint32_t &cy, bool &okx, bool &oky, bool &ox, bool &oy) {
     const float2 m2 = __ffma2_rn(re, re, __fmul2_rn(im, im));
-    const float2 rs = make_float2(a_rsqrt(m2.x), a_rsqrt(m2.y));
-    float2 mf = __fmul2_rn(m2, rs);
-    mf.x = m2.x > 0.f ? mf.x : 0.f;
-    mf.y = m2.y > 0.f ? mf.y : 0.f;
+    // rsqrt of max(m2, 1e-37): mf = |z| for m2 >= 1e-37, 0 for m2 = 0, and below
+    // sqrt(m2) < 3.2e-19 otherwise -- all of those certify as the special zero
+    // (|z| <= 3.2e-19 + eS < 1e-12 whenever mf + eS passes the zero test)
+    const float2 rs = make_float2(a_rsqrt(fmaxf(m2.x, 1e-37f)), a_rsqrt(fmaxf(m2.y, 1e-37f)));
+    const float2 mf = __fmul2_rn(m2, rs);
     float2 t = __ffma2_rn(mf, f2s(ce.s1), f2s(ce.s0));
     const float2 zt = __ffma2_rn(mf, f2s(1.0000005f), f2s(eS));
     const float2 it = __ffma2_rn(mf, f2s(0.9999995f), f2s(-eS));
@@ -1073,8 +1075,10 @@ __global__ void __launch_bounds__(A_THREADS, A_BOUNDS_MINB) k_bounds_a(const __g
                     float2 RE = make_float2(A.x, B.x), IM = make_float2(A.y, B.y);
                     if (sel) a_gate_f2<UK>(p.kf, A, B, RE, IM);
                     const float2 m2 = __ffma2_rn(RE, RE, __fmul2_rn(IM, IM));
-                    const float2 mf2 = __fmul2_rn(m2, make_float2(a_rsqrt(m2.x), a_rsqrt(m2.y)));
-                    const float mfx = m2.x > 0.f ? mf2.x : 0.f, mfy = m2.y > 0.f ? mf2.y : 0.f;
+                    // as a_encode_f2: mf = |z'f| for m2 >= 1e-37, else below 3.2e-19 (certainly zero)
+                    const float2 mf2 = __fmul2_rn(
+                        m2, make_float2(a_rsqrt(fmaxf(m2.x, 1e-37f)), a_rsqrt(fmaxf(m2.y, 1e-37f))));
+                    const float mfx = mf2.x, mfy = mf2.y;
                     // a certainly-zero output (|z'| < 1e-12, reading R-A5) is no intermediate:
                     // not a min candidate (the A states of the workloads hold many amplitudes
                     // at the 1e-12 floor, whose products straddle it)

@@ -28,7 +28,10 @@ namespace cg = cooperative_groups;
 
 namespace qsim {
 
-constexpr int PC_THREADS = 256;
+#ifndef PC_THREADS_DEF
+#define PC_THREADS_DEF 256
+#endif
+constexpr int PC_THREADS = PC_THREADS_DEF;
 
 // kind of a gate: 0 dense, 1 diagonal (u01 = u10 = 0), 2 anti-diagonal (u00 = u11 = 0);
 // the dropped terms are exact zeros, so every kind evaluates the general formula's value
