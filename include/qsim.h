@@ -95,10 +95,14 @@ typedef struct qsim_config {
                             QSIM_A_POLICY_EXACT (0, default): exact bounds of every dense gate's output
                             (reading R-A4; two passes, 6 B/amp); QSIM_A_POLICY_LAZY (1): kept while the
                             outputs stay within one step of them, exact rescale when one leaves (reading
-                            R-A25; one out-of-place pass of 4 B/amp in range, a second code buffer) */
+                            R-A25; one out-of-place pass of 4 B/amp in range, a second code buffer);
+                            QSIM_A_POLICY_FP32 (2): exact bounds, the decode / apply / encode in fp32
+                            without the certified fp64 fallback (reading R-A26, SURVEY 8(f) NEXT-4 "fp32
+                            decode/apply"): codes within one step of the fp64 reference's */
 } qsim_config;
 #define QSIM_A_POLICY_EXACT 0
 #define QSIM_A_POLICY_LAZY 1
+#define QSIM_A_POLICY_FP32 2
 
 /* Counters since creation (or the last qsim_reset_stats). Bytes are ALGORITHMIC
  * bytes (SURVEY.md §8(d) byte-accounting rule), summed over the shards this

@@ -37,6 +37,7 @@ TRANSPORT_NCCL = 1
 TRANSPORT_DEVICES = 2
 A_POLICY_EXACT = 0
 A_POLICY_LAZY = 1
+A_POLICY_FP32 = 2
 GATE_U = 0
 GATE_SWAP = 1
 OP_EXCHANGE = 0

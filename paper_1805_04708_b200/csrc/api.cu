@@ -1227,8 +1227,9 @@ int qsim_create_ex(const qsim_config *cfg, qsim_state **out) {
     s->transport = transport;
     s->rank = transport == QSIM_TRANSPORT_NCCL ? cfg->rank : 0;
     s->fuse = cfg->fuse;
-    s->a_policy = cfg->a_policy == QSIM_A_POLICY_LAZY ? QSIM_A_POLICY_LAZY : QSIM_A_POLICY_EXACT;
-    if (cfg->a_policy != QSIM_A_POLICY_EXACT && cfg->a_policy != QSIM_A_POLICY_LAZY) {
+    s->a_policy = cfg->a_policy;
+    if (cfg->a_policy != QSIM_A_POLICY_EXACT && cfg->a_policy != QSIM_A_POLICY_LAZY &&
+        cfg->a_policy != QSIM_A_POLICY_FP32) {
         delete s;
         set_error("unknown a_policy");
         return QSIM_EINVAL;
@@ -2570,7 +2571,10 @@ static int dense_gate_a_exact(qsim_state *s, const PlanOp &o, const double *u, b
         set_epi(s, sh, o, r, p);
         if (out_of_place) p.aout = sh.amps2;
         prof_begin(s);
-        launch_apply_a(p, s->atab, s->stream);
+        if (s->a_policy == QSIM_A_POLICY_FP32)
+            launch_apply_a_fp32(p, s->atab, s->stream);
+        else
+            launch_apply_a(p, s->atab, s->stream);
         prof_end(s, QSIM_K_A_APPLY, std::ldexp(2.0 * (double)s->amp_bytes, s->nl));
         s->st.kernels++;
         s->st.hbm_bytes += std::ldexp(2.0 * (double)s->amp_bytes, s->nl);

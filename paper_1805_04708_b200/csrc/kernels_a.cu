@@ -779,7 +779,12 @@ __device__ __forceinline__ float2 atan_2steps2(float2 w) {
     p = __ffma2_rn(p, s, f2s(81.48701477050781f));
     return __fmul2_rn(p, w);
 }
-template <bool LAZY>
+// FAST (the fp32 arithmetic variant, reading R-A26): the same fp32 values,
+// no certification -- the magnitude coordinate clamped to the end codes, the
+// special zero decided in fp32 (|zf| < 1e-12); the codes differ from the fp64
+// reference's only where the fp32 error (~1e-6 relative) crosses a rounding
+// boundary, i.e. by one step.
+template <bool LAZY, bool FAST = false>
 __device__ __forceinline__ void a_encode_f2(const AEncF &ce, float2 re, float2 im, float errm, float KE, float eS,
                                             uint32_t &cx, uint32_t &cy, bool &okx, bool &oky, bool &ox, bool &oy) {
     const float2 m2 = __ffma2_rn(re, re, __fmul2_rn(im, im));
@@ -789,10 +794,22 @@ __device__ __forceinline__ void a_encode_f2(const AEncF &ce, float2 re, float2 i
     const float2 rs = make_float2(a_rsqrt(fmaxf(m2.x, 1e-37f)), a_rsqrt(fmaxf(m2.y, 1e-37f)));
     const float2 mf = __fmul2_rn(m2, rs);
     float2 t = __ffma2_rn(mf, f2s(ce.s1), f2s(ce.s0));
-    const float2 zt = __ffma2_rn(mf, f2s(1.0000005f), f2s(eS));
-    const float2 it = __ffma2_rn(mf, f2s(0.9999995f), f2s(-eS));
-    const bool zerox = zt.x < 0.99999e-12f, zeroy = zt.y < 0.99999e-12f;
-    const bool interx = it.x > 1.00001e-12f, intery = it.y > 1.00001e-12f;
+    bool zerox, zeroy, interx, intery;
+    if (FAST) {
+        zerox = mf.x < 1e-12f;
+        zeroy = mf.y < 1e-12f;
+        interx = !zerox;
+        intery = !zeroy;
+        t.x = fminf(fmaxf(t.x, 0.f), 253.f);
+        t.y = fminf(fmaxf(t.y, 0.f), 253.f);
+    } else {
+        const float2 zt = __ffma2_rn(mf, f2s(1.0000005f), f2s(eS));
+        const float2 it = __ffma2_rn(mf, f2s(0.9999995f), f2s(-eS));
+        zerox = zt.x < 0.99999e-12f;
+        zeroy = zt.y < 0.99999e-12f;
+        interx = it.x > 1.00001e-12f;
+        intery = it.y > 1.00001e-12f;
+    }
     bool edgex = false, edgey = false;
     if (LAZY) {
         ox = interx & ((t.x < -1.f - errm) | (t.x > 254.f + errm));
@@ -811,9 +828,13 @@ __device__ __forceinline__ void a_encode_f2(const AEncF &ce, float2 re, float2 i
                                  (re.y < 0.f) ? copysignf(128.f, im.y) - p.y : p.y);
     const float2 ta = __fadd2_rn(q, f2s(A_MAGIC));
     const float2 fra = __fadd2_rn(q, __ffma2_rn(ta, f2s(-1.f), f2s(A_MAGIC)));  // q - (ta - M), exact
-    const float2 ka = __ffma2_rn(f2s(KE), rs, make_float2(fabsf(fra.x), fabsf(fra.y)));
-    okx = zerox | (interx & !edgex & (fabsf(frm.x) < 0.5f - errm) & (ka.x < 0.4998f));
-    oky = zeroy | (intery & !edgey & (fabsf(frm.y) < 0.5f - errm) & (ka.y < 0.4998f));
+    if (FAST) {
+        okx = oky = true;
+    } else {
+        const float2 ka = __ffma2_rn(f2s(KE), rs, make_float2(fabsf(fra.x), fabsf(fra.y)));
+        okx = zerox | (interx & !edgex & (fabsf(frm.x) < 0.5f - errm) & (ka.x < 0.4998f));
+        oky = zeroy | (intery & !edgey & (fabsf(frm.y) < 0.5f - errm) & (ka.y < 0.4998f));
+    }
     cx = zerox ? 0x0080u : __byte_perm(__float_as_uint(tm.x), __float_as_uint(ta.x), 0x0040);
     cy = zeroy ? 0x0080u : __byte_perm(__float_as_uint(tm.y), __float_as_uint(ta.y), 0x0040);
 }
@@ -1330,12 +1351,14 @@ void launch_tables_next(const double *acc, ATables *t, cudaStream_t s) {
 // the certified fallback per failing pair (the warp queue, a_flush).  The
 // grid-stride loop is warp-uniform (lanes past the end idle) so that the
 // queue's votes see the whole warp.
-template <int TL, bool CTRL, int UK, bool LAZY>
+// MODE 0: exact bounds, certified; 1: lazy (reading R-A25); 2: exact bounds, fp32 arithmetic (R-A26)
+template <int TL, bool CTRL, int UK, int MODE>
 __global__ void __launch_bounds__(A_THREADS, A_DENSE_MINB) k_apply_a(const __grid_constant__ AGateParams p,
                                                                      const ATabData *__restrict__ cur,
                                                                      const ATabData *__restrict__ nxt,
                                                                      const AFTab *__restrict__ fcur) {
     using U = AUnit<TL>;
+    constexpr bool LAZY = MODE == 1, FAST = MODE == 2;
     const AFLane L = load_aflane(fcur);
     __shared__ AFail qall[A_THREADS / 32][A_QN];
     const int lane = threadIdx.x & 31;
@@ -1401,7 +1424,7 @@ __global__ void __launch_bounds__(A_THREADS, A_DENSE_MINB) k_apply_a(const __gri
                 cx = a_encode_f<LAZY>(ce, x, errm, KE, eS, okx, ox);
                 cy = a_encode_f<LAZY>(ce, y, errm, KE, eS, oky, oy);
 #else
-                a_encode_f2<LAZY>(ce, RE, IM, errm, KE, eS, cx, cy, okx, oky, ox, oy);
+                a_encode_f2<LAZY, FAST>(ce, RE, IM, errm, KE, eS, cx, cy, okx, oky, ox, oy);
 #endif
                 if (LAZY) oor_any |= (ox & (!CTRL || sel)) | (oy & (!CTRL || sel));
                 if (CTRL) {  // an unselected zero code stays the exact zero special
@@ -1451,43 +1474,45 @@ __global__ void __launch_bounds__(A_THREADS, A_DENSE_MINB) k_apply_a(const __gri
     if (qn) a_flush<UK, LAZY>(&p, cur, nxt, q, qn);
 }
 
-template <int TL, bool CTRL, int UK, bool LAZY>
+template <int TL, bool CTRL, int UK, int MODE>
 static void launch_apply_tl(const AGateParams &p, const ATables *t, int grid, cudaStream_t s) {
     static std::atomic<uint64_t> attr{0};
-    a_dense_attr((const void *)k_apply_a<TL, CTRL, UK, LAZY>, attr);
+    a_dense_attr((const void *)k_apply_a<TL, CTRL, UK, MODE>, attr);
     // LAZY: encode with the current tables (the kept bounds)
-    k_apply_a<TL, CTRL, UK, LAZY><<<grid, A_THREADS, sizeof(AFTab), s>>>(p, tcur(t), LAZY ? tcur(t) : tnext(t), fcur(t));
+    k_apply_a<TL, CTRL, UK, MODE><<<grid, A_THREADS, sizeof(AFTab), s>>>(p, tcur(t), MODE == 1 ? tcur(t) : tnext(t),
+                                                                         fcur(t));
 }
-template <int TL, int UK, bool LAZY>
+template <int TL, int UK, int MODE>
 static void launch_apply_c(const AGateParams &p, const ATables *t, int grid, cudaStream_t s) {
     if (p.cmask)
-        launch_apply_tl<TL, true, UK, LAZY>(p, t, grid, s);
+        launch_apply_tl<TL, true, UK, MODE>(p, t, grid, s);
     else
-        launch_apply_tl<TL, false, UK, LAZY>(p, t, grid, s);
+        launch_apply_tl<TL, false, UK, MODE>(p, t, grid, s);
 }
-template <int UK, bool LAZY>
+template <int UK, int MODE>
 static void launch_apply_k(const AGateParams &p, const ATables *t, int grid, cudaStream_t s) {
     switch (p.t < 4 ? p.t : 4) {
-        case 0: launch_apply_c<0, UK, LAZY>(p, t, grid, s); break;
-        case 1: launch_apply_c<1, UK, LAZY>(p, t, grid, s); break;
-        case 2: launch_apply_c<2, UK, LAZY>(p, t, grid, s); break;
-        case 3: launch_apply_c<3, UK, LAZY>(p, t, grid, s); break;
-        default: launch_apply_c<4, UK, LAZY>(p, t, grid, s); break;
+        case 0: launch_apply_c<0, UK, MODE>(p, t, grid, s); break;
+        case 1: launch_apply_c<1, UK, MODE>(p, t, grid, s); break;
+        case 2: launch_apply_c<2, UK, MODE>(p, t, grid, s); break;
+        case 3: launch_apply_c<3, UK, MODE>(p, t, grid, s); break;
+        default: launch_apply_c<4, UK, MODE>(p, t, grid, s); break;
     }
 }
-template <bool LAZY>
+template <int MODE>
 static void launch_apply_any(const AGateParams &p0, const ATables *t, cudaStream_t s) {
     const AGateParams p = a_dense_params(p0);
     const uint64_t units = (p.nl >= 4) ? (1ull << (p.nl - 4)) : 1ull;
     const int grid = a_dense_grid(units);
     switch (a_ukind(p.u)) {
-        case 1: launch_apply_k<1, LAZY>(p, t, grid, s); break;
-        case 2: launch_apply_k<2, LAZY>(p, t, grid, s); break;
-        default: launch_apply_k<0, LAZY>(p, t, grid, s); break;
+        case 1: launch_apply_k<1, MODE>(p, t, grid, s); break;
+        case 2: launch_apply_k<2, MODE>(p, t, grid, s); break;
+        default: launch_apply_k<0, MODE>(p, t, grid, s); break;
     }
 }
-void launch_apply_a(const AGateParams &p, const ATables *t, cudaStream_t s) { launch_apply_any<false>(p, t, s); }
-void launch_apply_a_lazy(const AGateParams &p, const ATables *t, cudaStream_t s) { launch_apply_any<true>(p, t, s); }
+void launch_apply_a(const AGateParams &p, const ATables *t, cudaStream_t s) { launch_apply_any<0>(p, t, s); }
+void launch_apply_a_fp32(const AGateParams &p, const ATables *t, cudaStream_t s) { launch_apply_any<2>(p, t, s); }
+void launch_apply_a_lazy(const AGateParams &p, const ATables *t, cudaStream_t s) { launch_apply_any<1>(p, t, s); }
 
 // ---------------------------------------------------------------- fast paths
 static int phase_steps(double ur, double ui) {

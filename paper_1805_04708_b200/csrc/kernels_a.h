@@ -123,6 +123,8 @@ void launch_apply_a(const AGateParams &p, const ATables *t, cudaStream_t s);
 // the lazy policy's one pass (reading R-A25): decode, apply, encode with the CURRENT
 // tables into p.aout, *p.oor |= some intermediate output left [r0 - d, r1 + d]
 void launch_apply_a_lazy(const AGateParams &p, const ATables *t, cudaStream_t s);
+// exact bounds, fp32 arithmetic without certification (reading R-A26; QSIM_A_POLICY_FP32)
+void launch_apply_a_fp32(const AGateParams &p, const ATables *t, cudaStream_t s);
 // diagonal / anti-diagonal gates: b1 shifts and code moves, bounds unchanged
 void launch_fast_a(const AGateParams &p, const ATables *t, cudaStream_t s);
 // A run of consecutive diagonal gates in one sweep: each gate's b1 step

@@ -161,21 +161,22 @@ def table4_adder():
 
 def cfg4_lazy():
     """NEXT-4: config 4 at N = 33 under the lazy-bounds A policy (reading R-A25)
-    vs the exact policy: device time, dense gates that rescaled, fidelity
-    against E (same circuit, E run on the same GPU)."""
+    and the fp32-arithmetic variant (reading R-A26) vs the exact policy:
+    device time, dense gates that rescaled, fidelity against E (same circuit,
+    E run on the same GPU)."""
     n = 33
     circ = C.config(3, n=n)
     rows = []
     with q.State(n, q.ENC_FP64, 1) as e:
         e.apply_circuit(circ)
         e.sync()
-        for pol in (q.A_POLICY_EXACT, q.A_POLICY_LAZY):
+        for pol in (q.A_POLICY_EXACT, q.A_POLICY_LAZY, q.A_POLICY_FP32):
             with q.State(n, q.ENC_ADAPTIVE2, 1, a_policy=pol) as a:
                 dev, wall, prof, st = run(a, circ, warm=False)
                 ae = a.overlap(e)
                 aa = a.overlap(a).real
                 ee = e.overlap(e).real
-            rows.append(summary("cfg4_" + ("lazy" if pol else "exact"), circ, dev, wall, prof, st,
+            rows.append(summary("cfg4_" + {0: "exact", 1: "lazy", 2: "fp32"}[pol], circ, dev, wall, prof, st,
                                 fidelity_vs_E=abs(ae) ** 2 / (aa * ee), norm_A=aa,
                                 dense=st["a_dense"], rescaled=st["a_rescales"]))
     return rows
