@@ -11,6 +11,7 @@ the E timing; for A it is a config-4 style state (H wall + one Rz/Rx/CPHASE
 layer) so that the bounds are non-degenerate.
 
 Usage: python tools/per_target.py {E|A} N [REPS] > per_target_{E|A}.json
+(A_POLICY=lazy|fp32 selects the A policy; default exact.)
 """
 import json
 import os
@@ -28,7 +29,8 @@ n = int(sys.argv[2]) if len(sys.argv) > 2 else 30
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 10
 warm = 3
 enc = q.ENC_ADAPTIVE2 if enc_name == "A" else q.ENC_FP64
-s = q.State(n, enc, 1, fuse=0)
+pol = {"exact": q.A_POLICY_EXACT, "lazy": q.A_POLICY_LAZY, "fp32": q.A_POLICY_FP32}[os.environ.get("A_POLICY", "exact")]
+s = q.State(n, enc, 1, fuse=0, a_policy=pol)
 if enc == q.ENC_ADAPTIVE2:
     s.apply_circuit(C.rz_rx_cphase(n, 1, seed=4))
 else:
@@ -43,7 +45,7 @@ if enc == q.ENC_ADAPTIVE2:
     kinds = [("dense", U, lambda t: ()), ("Rx", C.mat_Rx(0.7), lambda t: ()), ("H", C.mat_H(), lambda t: ()),
              ("Rz", C.mat_Rz(0.7), lambda t: ())]
 
-out = {"enc": enc_name, "n": n, "reps": reps, "warmup": warm, "unit": "ms per gate (CUDA events, library stream)",
+out = {"enc": enc_name, "a_policy": os.environ.get("A_POLICY", "exact"), "n": n, "reps": reps, "warmup": warm, "unit": "ms per gate (CUDA events, library stream)",
        "rows": []}
 targets = [int(x) for x in os.environ["TARGETS"].split(",")] if os.environ.get("TARGETS") else list(range(n))
 for name, u, ctl in kinds:
