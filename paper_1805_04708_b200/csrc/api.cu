@@ -79,6 +79,7 @@ struct qsim_state {
         int lcs = 0, K = 0;
         void *d = nullptr;
         std::vector<std::pair<int, int>> lens;  // (phases, ops) per launch
+        std::vector<PersistGate> recs;          // the records it was planned from (a hit compares them)
     };
     std::vector<PcEntry> pc_cache;
     uint64_t pc_clock = 0;
@@ -1412,7 +1413,9 @@ int qsim_apply_circuit_persistent(qsim_state *s, const qsim_gate *gates, size_t 
     }
     qsim_state::PcEntry *ent = nullptr;
     for (auto &e : s->pc_cache)
-        if (e.d && e.key == key && e.lcs == lcs && e.K == K) ent = &e;
+        if (e.d && e.key == key && e.lcs == lcs && e.K == K && e.recs.size() == (size_t)ng &&
+            std::memcmp(e.recs.data(), s->h_pg.data(), (size_t)ng * sizeof(PersistGate)) == 0)
+            ent = &e;
     if (!ent) {
         // phases of gates on <= K qubits (persist.cu), one launch per PERSIST_MAX_GATES gates
         std::vector<PersistPhase> ph;
@@ -1468,6 +1471,7 @@ int qsim_apply_circuit_persistent(qsim_state *s, const qsim_gate *gates, size_t 
         ent->lcs = lcs;
         ent->K = K;
         ent->lens = lens;
+        ent->recs.assign(s->h_pg.begin(), s->h_pg.begin() + ng);
     }
     ent->stamp = ++s->pc_clock;
     size_t at = 0;
