@@ -719,18 +719,19 @@ def test_apply_matrix_errors():
 
 
 @pytest.mark.parametrize("enc", ["E", "A"])
-def test_remap_pack_unpack_path(tmp_path, enc):
+@pytest.mark.parametrize("n,P", [(13, 8), (14, 16)])
+def test_remap_pack_unpack_path(tmp_path, enc, n, P):
     """The NCCL remap's data flow on one GPU (QSIM_REMAP_VIA_PACK=1: chunked
     multi-partner pack -> device copies standing in for ncclSend / ncclRecv
     -> multi-partner unpack, small chunks so every block takes several
-    rounds): E equals the oracle, A equals the single-shard run bit for bit."""
+    rounds): E equals the oracle, A equals the single-shard run bit for bit;
+    P = 16 (4 global qubits) exercises remaps split into groups of <= 3 bits."""
     import os
     import subprocess
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    n, P = 13, 8
-    out = str(tmp_path / f"r_{enc}.npy")
+    out = str(tmp_path / f"r_{enc}_{P}.npy")
     getter = "s.get_state()" if enc == "E" else "s.get_codes()[0]"
     code = ("import sys, numpy as np; sys.path.insert(0, %r); import paper_1805_04708_b200 as q, qsim_inputs as C; "
             "s = q.State(%d, q.ENC_%s, %d, chunk_bytes=2048); c = C.layered(%d, 2, seed=7); "
