@@ -86,6 +86,7 @@ struct qsim_state {
     size_t pg_cap = 0;
     int pass_r = 4;  // register qubits per pass stage (QSIM_PASS_R=5 selects 32-amplitude groups)
     int pass_k = LP_MAX_K;  // tile qubits of the relabelling pass (QSIM_LPASS_K = 9..12)
+    bool pass_k_env = false;  // QSIM_LPASS_K given: no small-shard reduction
     size_t amp_bytes = 16;
     uint64_t alloc_amps = 0;  // max(2^nl, 256): small shards are padded with zero amplitudes
     Planner pl;
@@ -398,7 +399,11 @@ static int run_gates_lpass(qsim_state *s, const std::vector<PlanOp> &run, const 
     }
     LRunConfig cfg;
     cfg.nl = s->nl;
+    // small shards: tiles of at most nl - 3 qubits (>= 8 tiles, i.e. CTAs) where that
+    // keeps K >= LP_MIN_K -- a latency-bound pass of 4 tiles ran on 4 SMs (config 1,
+    // N = 14: 39 -> 28.5 us per circuit with a graph at K = 11); QSIM_LPASS_K overrides
     cfg.K = std::min(s->pass_k, s->nl);
+    if (!s->pass_k_env) cfg.K = std::min(cfg.K, std::max(std::min(s->nl, LP_MIN_K), s->nl - 3));
     cfg.R = s->pass_r;
     cfg.max_coef = lpass_max_coef(cfg.R);
     cfg.defer = getenv("QSIM_LPASS_NODEFER") == nullptr;
@@ -1236,7 +1241,10 @@ int qsim_create_ex(const qsim_config *cfg, qsim_state **out) {
         return QSIM_EINVAL;
     }
     if (const char *pr = getenv("QSIM_PASS_R")) s->pass_r = (atoi(pr) == 4) ? 4 : 5;
-    if (const char *lk = getenv("QSIM_LPASS_K")) s->pass_k = std::max(LP_MIN_K, std::min(LP_MAX_K, atoi(lk)));
+    if (const char *lk = getenv("QSIM_LPASS_K")) {
+        s->pass_k = std::max(LP_MIN_K, std::min(LP_MAX_K, atoi(lk)));
+        s->pass_k_env = true;
+    }
     s->amp_bytes = s->enc == QSIM_ENC_FP64 ? 16 : 2;
     if (cfg->device >= 0) {
         if (cudaSetDevice(cfg->device) != cudaSuccess) {
