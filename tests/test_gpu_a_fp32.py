@@ -81,3 +81,19 @@ def test_special_codes_and_whole_circuit():
             z = s.get_state()
         f[pol] = abs(np.vdot(z, e)) ** 2 / (np.vdot(z, z).real * np.vdot(e, e).real)
     assert abs(f[q.A_POLICY_FP32] - f[q.A_POLICY_EXACT]) <= 2e-3, f
+
+
+def test_shard_count_independent():
+    """As for the certified policy, the fp32 variant's codes do not depend on
+    the sharding: the bounds are the exact global extremes and each pair's
+    fp32 arithmetic is the same wherever it runs (1 vs 4 loopback shards,
+    dense gates on global qubits through the exchange path)."""
+    n = 14
+    circ = C.rz_rx_cphase(n, 3, seed=8)
+    out = []
+    for P in (1, 4):
+        with q.State(n, q.ENC_ADAPTIVE2, P, a_policy=q.A_POLICY_FP32) as s:
+            s.apply_circuit(circ)
+            out.append(s.get_codes())
+    assert out[0][1:] == out[1][1:]
+    assert np.array_equal(out[0][0], out[1][0])
