@@ -1193,9 +1193,69 @@ int lpass_compile(const LGate *gates, int ng, int nl, int K, int R, const int *t
     }
     int rc = c.run();
     if (rc == 0 && (int)c.coef.size() > max_coef) rc = 1;
+    int p_ts_off = 0, p_nts = 0, p_ts_slot = 0;
     if (rc) {
         if (err) *err = c.err;
         return rc;
+    }
+    // PHASES terms conditioned on full-index bits (outside the tile) have one
+    // product per tile: move them to the front of the op's term list (stable;
+    // the phases commute) and give the op a 2-double slot at the end of the
+    // coefficient pool, which the kernel fills once per tile (lp_body);
+    // the op then multiplies only its tile-bit terms per group.
+    // pmc[0] = slot offset in coef (doubles), pmc[1] = number of hoisted terms.
+    // Conditional scalars (a DIAG1 with T0 == T1 whose condition is on full-index
+    // bits only: a CPHASE with both qubits outside the tile) commute with every
+    // op of the pass: they become one product per tile (terms (omask, oval, e)
+    // in sc, formed in lp_body into a coefficient-pool slot) applied at the
+    // tile store, and the op a no-op (FLIP with gvec 0).
+    std::vector<size_t> ts_ops;
+    for (size_t i = 0; i < c.ops.size(); ++i) {
+        const LOp &o = c.ops[i];
+        if (o.code != LOP_CODE_DIAG1 || !(o.flags & LF_COND) || o.tmask || !o.omask) continue;
+        const double *T = &c.sc[o.coef];
+        if (T[0] == T[2] && T[1] == T[3]) ts_ops.push_back(i);
+    }
+    if (!ts_ops.empty() && (int)c.sc.size() + 4 * (int)ts_ops.size() <= LP_MAX_SC &&
+        (int)((c.coef.size() + 1) & ~(size_t)1) + 2 <= max_coef) {  // else they stay DIAG1 ops
+        p_ts_off = (int)c.sc.size();
+        p_nts = (int)ts_ops.size();
+        for (size_t i : ts_ops) {
+            LOp &o = c.ops[i];
+            double term[4];
+            std::memcpy(&term[0], &o.omask, 8);
+            std::memcpy(&term[1], &o.oval, 8);
+            term[2] = c.sc[o.coef];
+            term[3] = c.sc[o.coef + 1];
+            c.sc.insert(c.sc.end(), term, term + 4);
+            o.code = LOP_CODE_FLIP;
+            o.flags = 0;
+            o.gvec = 0;
+        }
+        if (c.coef.size() & 1) c.coef.push_back(0.0);
+        p_ts_slot = (int)c.coef.size();
+        c.coef.push_back(1.0);
+        c.coef.push_back(0.0);
+    }
+    int nops_ph = 0;
+    for (size_t i = 0; i < c.ops.size(); ++i) {
+        LOp &o = c.ops[i];
+        if (o.code != LOP_CODE_PHASES) continue;
+        std::vector<double> full_t, tile_t;
+        for (int k = 0; k < o.nctl; ++k) {
+            std::vector<double> &dst = c.sc[o.coef + 3 * k] >= 64.0 ? full_t : tile_t;
+            for (int j = 0; j < 3; ++j) dst.push_back(c.sc[o.coef + 3 * k + j]);
+        }
+        if (full_t.empty() || (int)((c.coef.size() + 1) & ~(size_t)1) + 2 > max_coef) continue;
+        if (c.coef.size() & 1) c.coef.push_back(0.0);  // 16-byte aligned slot
+        const size_t nfull = full_t.size() / 3;
+        for (double x : tile_t) full_t.push_back(x);
+        std::memcpy(&c.sc[o.coef], full_t.data(), full_t.size() * sizeof(double));
+        o.pmc[0] = (uint32_t)c.coef.size();
+        o.pmc[1] = (uint32_t)nfull;
+        c.coef.push_back(1.0);
+        c.coef.push_back(0.0);
+        nops_ph = (int)i + 1;
     }
     if (deferred) {
         // still-carried diagonals: the caller applies them right after the pass
@@ -1320,6 +1380,10 @@ int lpass_compile(const LGate *gates, int ng, int nl, int K, int R, const int *t
     }
     p.ncoef = (int)c.coef.size();
     p.nsc = (int)c.sc.size();
+    p.nops_ph = nops_ph;
+    p.nts = p_nts;
+    p.ts_off = p_ts_off;
+    p.ts_slot = p_ts_slot;
     std::memcpy(p.op, c.ops.data(), c.ops.size() * sizeof(LOp));
     std::memcpy(p.coef, c.coef.data(), c.coef.size() * sizeof(double));
     std::memcpy(p.sc, c.sc.data(), c.sc.size() * sizeof(double));

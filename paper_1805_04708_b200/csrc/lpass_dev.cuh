@@ -219,6 +219,22 @@ __device__ __forceinline__ void lp_tile_store(const unsigned char *smem, char *g
         *reinterpret_cast<double2 *>(gp + dj) = *reinterpret_cast<const double2 *>(smem + mo);
     }
 }
+// the same, every amplitude times the tile scalar c (LPassParams::nts)
+template <int NJ>
+__device__ __forceinline__ void lp_tile_store_scaled(const unsigned char *smem, char *gp, uint32_t mo,
+                                                     const uint32_t *m_hi, const uint64_t *d_hi, double2 c) {
+    uint64_t dj = 0;
+#pragma unroll
+    for (int i = 0; i < NJ; ++i) {
+        if (i) {
+            mo ^= m_hi[lp_ctz5(i)];
+            dj ^= d_hi[lp_ctz5(i)];
+        }
+        const double2 v = *reinterpret_cast<const double2 *>(smem + mo);
+        const double pp = c.y * v.y, qq = c.y * v.x;
+        *reinterpret_cast<double2 *>(gp + dj) = make_double2(fma(c.x, v.x, -pp), fma(c.x, v.y, qq));
+    }
+}
 
 // table variant offset (bytes in shared memory) of a group: the group's
 // values of up to 2 condition bits select among the op's consecutive tables
@@ -302,7 +318,13 @@ __device__ __forceinline__ void lp_op1(double2 (&v)[1 << R], uint32_t &g, uint32
         const double *T = p.sc + coef;
         const int nt = (int)((h >> 48) & 0xffu);
         double cr = 1.0, ci = 0.0;
-        for (int k = 0; k < nt; ++k) {
+        const int nf = (int)o.pmc[1];  // leading full-index-bit terms: this tile's product (lp_body)
+        if (nf) {
+            const double2 c = *reinterpret_cast<const double2 *>(smem_raw + cpool_off + o.pmc[0] * 8u);
+            cr = c.x;
+            ci = c.y;
+        }
+        for (int k = nf; k < nt; ++k) {
             const int c = (int)T[3 * k];
             const uint32_t bit = c < 64 ? (xq >> c) & 1u : (uint32_t)(full >> (c - 64)) & 1u;
             if (bit) {
@@ -554,6 +576,39 @@ __device__ __forceinline__ void lp_body(const LPassParams &p, const Stages &stag
                 default: lp_tile_load<2>(smem_raw, gp, s_tid, s_hi, d_hi); break;
             }
         }
+        // ---- per-tile products of the PHASES terms on full-index bits (op slots
+        // in the coefficient pool; read after the barrier below) ----
+        for (int i = (int)tid; i < p.nops_ph; i += NT) {
+            const LOp &o = p.op[i];
+            if (o.code != LOP_CODE_PHASES || !o.pmc[1]) continue;
+            const double *T = p.sc + o.coef;
+            double cr = 1.0, ci = 0.0;
+            for (int k = 0; k < (int)o.pmc[1]; ++k) {
+                const int c = (int)T[3 * k];
+                if ((t.full >> (c - 64)) & 1u) {
+                    const double er = T[3 * k + 1], ei = T[3 * k + 2];
+                    const double nr = fma(cr, er, -ci * ei);
+                    ci = fma(cr, ei, ci * er);
+                    cr = nr;
+                }
+            }
+            *reinterpret_cast<double2 *>(smem_raw + L.cpool + o.pmc[0] * 8u) = make_double2(cr, ci);
+        }
+        // ---- the tile scalar (conditional scalars on full-index bits, applied at the store) ----
+        if (p.nts && tid == 0) {
+            double cr = 1.0, ci = 0.0;
+            for (int k = 0; k < p.nts; ++k) {
+                const double *T = p.sc + p.ts_off + 4 * k;
+                const uint64_t m = (uint64_t)__double_as_longlong(T[0]), v = (uint64_t)__double_as_longlong(T[1]);
+                if ((t.full & m) == v) {
+                    const double er = T[2], ei = T[3];
+                    const double nr = fma(cr, er, -ci * ei);
+                    ci = fma(cr, ei, ci * er);
+                    cr = nr;
+                }
+            }
+            *reinterpret_cast<double2 *>(smem_raw + L.cpool + (uint32_t)p.ts_slot * 8u) = make_double2(cr, ci);
+        }
         lp_cp_async_wait_all();
         __syncthreads();
         // ---- L2 prefetch of this CTA's next tile: its HBM reads overlap this
@@ -579,15 +634,27 @@ __device__ __forceinline__ void lp_body(const LPassParams &p, const Stages &stag
         // ---- store: logical x = tid + 128 j from S (M x ^ b) ----
         uint32_t sbt = p.sb_static;
         for (uint32_t m = t.fired; m; m &= m - 1) sbt ^= p.sv_ev[__ffs(m) - 1];
+        double2 tsc = make_double2(1.0, 0.0);
+        if (p.nts) tsc = *reinterpret_cast<const double2 *>(smem_raw + L.cpool + (uint32_t)p.ts_slot * 8u);
         if (!p.noio) {
             char *gp = reinterpret_cast<char *>(a + (base | d_tid));
             const uint32_t mo = m_tid ^ (sbt << 4);
-            switch (K - TB) {
-                case 5: lp_tile_store<32>(smem_raw, gp, mo, m_hi, d_hi); break;
-                case 4: lp_tile_store<16>(smem_raw, gp, mo, m_hi, d_hi); break;
-                case 3: lp_tile_store<8>(smem_raw, gp, mo, m_hi, d_hi); break;
-                case 2: lp_tile_store<4>(smem_raw, gp, mo, m_hi, d_hi); break;
-                default: lp_tile_store<2>(smem_raw, gp, mo, m_hi, d_hi); break;
+            if (tsc.x == 1.0 && tsc.y == 0.0) {
+                switch (K - TB) {
+                    case 5: lp_tile_store<32>(smem_raw, gp, mo, m_hi, d_hi); break;
+                    case 4: lp_tile_store<16>(smem_raw, gp, mo, m_hi, d_hi); break;
+                    case 3: lp_tile_store<8>(smem_raw, gp, mo, m_hi, d_hi); break;
+                    case 2: lp_tile_store<4>(smem_raw, gp, mo, m_hi, d_hi); break;
+                    default: lp_tile_store<2>(smem_raw, gp, mo, m_hi, d_hi); break;
+                }
+            } else {
+                switch (K - TB) {
+                    case 5: lp_tile_store_scaled<32>(smem_raw, gp, mo, m_hi, d_hi, tsc); break;
+                    case 4: lp_tile_store_scaled<16>(smem_raw, gp, mo, m_hi, d_hi, tsc); break;
+                    case 3: lp_tile_store_scaled<8>(smem_raw, gp, mo, m_hi, d_hi, tsc); break;
+                    case 2: lp_tile_store_scaled<4>(smem_raw, gp, mo, m_hi, d_hi, tsc); break;
+                    default: lp_tile_store_scaled<2>(smem_raw, gp, mo, m_hi, d_hi, tsc); break;
+                }
             }
         }
         __syncthreads();

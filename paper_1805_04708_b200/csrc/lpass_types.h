@@ -50,7 +50,9 @@ constexpr uint8_t LOP_CODE_DIAG1 = 253;
 // c = prod_k (bit_k ? e_k : 1) over the nctl terms at sc[coef + 3k] = (code,
 // re, im) (code: tile bit b -> b, full-index bit b -> 64 + b), then v[j] *= c
 // where par(rowS & (j ^ g)) = 1 -- one complex multiply per term per group
-// instead of per amplitude (the QFT's CPHASE ladders)
+// instead of per amplitude (the QFT's CPHASE ladders).  Terms on full-index
+// bits come first; when pmc[1] = m > 0 their product is formed once per tile
+// into coef[pmc[0] .. pmc[0] + 2) (shared memory) and the group starts from it
 constexpr uint8_t LOP_CODE_PHASES = 254;
 // ROUND: v[j] *= T[j ^ g] (T at coef, 2^R complex), then for every register bit
 // r in gvec (ascending) a lifted shear on the pairs (j0, j0 | 2^r) with
@@ -115,7 +117,8 @@ struct LPassParams {
     void *a;
     uint64_t shard_base;   // full physical index of local amplitude 0 (rank bits)
     uint64_t ntiles;
-    int32_t nl, K, R, nstages, nevents, ncoef, noio, pad;
+    int32_t nl, K, R, nstages, nevents, ncoef, noio;
+    int32_t nops_ph;                   // ops [0, nops_ph) hold every PHASES op with hoisted terms
     int32_t high_q[LP_MAX_K];          // tile bit LP_LOW + i <-> local qubit (ascending)
     uint16_t scol[LP_MAX_K];           // load: swizzled position of logical tile bit i
     uint16_t smcol[LP_MAX_K];          // store: S M_final e_i
@@ -127,7 +130,11 @@ struct LPassParams {
     LOp op[LP_MAX_OPS];
     double coef[LP_MAX_COEF];  // diagonal tables, 2^(R+1) doubles each, table-aligned
     double sc[LP_MAX_SC];
-    int32_t nsc, pad3;
+    int32_t nsc;
+    // tile scalars: nts terms (omask, oval as bit patterns, re, im) at sc[ts_off];
+    // the product of the terms with (full & omask) == oval multiplies the tile at
+    // its store (formed per tile into coef[ts_slot .. ts_slot + 2))
+    int32_t nts, ts_off, ts_slot;
 };
 
 }  // namespace qsim

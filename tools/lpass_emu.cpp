@@ -195,11 +195,19 @@ static void emu_pass(const LPassParams &p, cd *a) {
         uint32_t sbt = p.sb_static;
         for (int e = 0; e < p.nevents; ++e)
             if ((fired >> e) & 1) sbt ^= p.sv_ev[e];
+        cd tsc(1.0, 0.0);  // the tile scalar (LPassParams::nts), applied at the store
+        for (int k = 0; k < p.nts; ++k) {
+            const double *T = p.sc + p.ts_off + 4 * k;
+            uint64_t m, v;
+            std::memcpy(&m, &T[0], 8);
+            std::memcpy(&v, &T[1], 8);
+            if ((full & m) == v) tsc *= cd(T[2], T[3]);
+        }
         for (uint32_t x = 0; x < (1u << K); ++x) {
             uint32_t ad = sbt;
             for (int i = 0; i < K; ++i)
                 if ((x >> i) & 1) ad ^= p.smcol[i];
-            a[base | dep(x)] = tile[ad];
+            a[base | dep(x)] = tsc == cd(1.0, 0.0) ? tile[ad] : tile[ad] * tsc;
         }
     }
 }
@@ -318,6 +326,23 @@ static int run_circuits(int ncases, uint64_t seed) {
             const bool diag = g.u[2] == 0 && g.u[3] == 0 && g.u[4] == 0 && g.u[5] == 0;
             if (!diag && g.t >= nl) continue;  // global non-diagonal targets go through the exchange
             gs.push_back(g);
+        }
+        if (cs % 5 == 4) {  // QFT-like ladders: PHASES ops mixing tile-bit and full-index-bit terms
+            for (int j = nl - 1; j >= 0; --j) {
+                LGate h{};
+                h.t = j;
+                set_u(h.u, M_SQRT1_2, M_SQRT1_2, M_SQRT1_2, -M_SQRT1_2);
+                gs.push_back(h);
+                for (int m = n - 1; m >= 0; --m) {
+                    if (m == j) continue;
+                    LGate g{};
+                    g.t = j;
+                    g.nctl = 1;
+                    g.ctl[0] = m;
+                    set_u(g.u, 1, 0, 0, std::polar(1.0, 2 * M_PI * rng.uni()));
+                    gs.push_back(g);
+                }
+            }
         }
         std::vector<cd> a(1ull << n), b;
         for (auto &z : a) z = cd(rng.uni() - 0.5, rng.uni() - 0.5);
