@@ -49,6 +49,10 @@ def test_scheduler_whole_circuits(emu, seed, forced):
     out = subprocess.run([emu, "30", str(seed), "run"], capture_output=True, text=True, timeout=300, env=env)
     assert out.returncode == 0, out.stdout + out.stderr
     assert out.stdout.startswith("ok"), out.stdout
+    # the QFT-like ladders exercise the per-tile hoisting (phase terms on
+    # full-index bits, tile scalars applied at the store)
+    stats = dict(kv.split("=") for kv in out.stdout.split()[1:])
+    assert int(stats["hoisted"]) > 0 and int(stats["tile_scalars"]) > 0, out.stdout
 
 
 def test_specialised_kernel_sources_compile(emu, tmp_path):

@@ -244,10 +244,14 @@ static void set_u(double *u, cd a, cd b, cd c, cd d) {
 struct EmuSink : LPassSink {
     std::vector<cd> *st;
     int n, nl, nglob;
-    long passes = 0, sweeps = 0, synth = 0;
+    long passes = 0, sweeps = 0, synth = 0, hoisted = 0, tscal = 0;
     int pass(const LPassParams &p0, const LCompileStats &, const std::vector<int> &ids) override {
         static LPassParams p;
         p = p0;
+        // per-tile hoisting: PHASES ops with full-index-bit terms, tile-scalar terms
+        for (int i = 0; i < p.nops_ph; ++i)
+            if (p.op[i].code == LOP_CODE_PHASES) hoisted += p.op[i].pmc[1];
+        tscal += p.nts;
         for (int sh = 0; sh < (1 << nglob); ++sh) {
             p.shard_base = (uint64_t)sh << nl;
             emu_pass(p, st->data() + ((size_t)sh << nl));
@@ -270,7 +274,7 @@ struct EmuSink : LPassSink {
 static int run_circuits(int ncases, uint64_t seed) {
     Rng rng(seed);
     double worst = 0.0;
-    long passes = 0, sweeps = 0, synth = 0, gates = 0;
+    long passes = 0, sweeps = 0, synth = 0, gates = 0, hoisted = 0, tscal = 0;
     for (int cs = 0; cs < ncases; ++cs) {
         const int nl = 12 + rng.below(3), nglob = rng.below(2), n = nl + nglob;
         const int K = std::min(LP_MAX_K, nl), R = (cs % 3 == 2) ? 5 : 4;
@@ -372,6 +376,8 @@ static int run_circuits(int ncases, uint64_t seed) {
         passes += sink.passes;
         sweeps += sink.sweeps;
         synth += sink.synth;
+        hoisted += sink.hoisted;
+        tscal += sink.tscal;
         gates += (long)gs.size();
         if (e > 1e-12) {
             printf("FAIL circuit %d: nl=%d nglob=%d R=%d layered=%d gates=%zu err=%.3e\n", cs, nl, nglob, R, layered,
@@ -379,8 +385,8 @@ static int run_circuits(int ncases, uint64_t seed) {
             return 1;
         }
     }
-    printf("ok circuits=%d gates=%ld passes=%ld sweeps=%ld synthetic=%ld worst=%.3e\n", ncases, gates, passes, sweeps,
-           synth, worst);
+    printf("ok circuits=%d gates=%ld passes=%ld sweeps=%ld synthetic=%ld hoisted=%ld tile_scalars=%ld worst=%.3e\n",
+           ncases, gates, passes, sweeps, synth, hoisted, tscal, worst);
     return 0;
 }
 
