@@ -239,11 +239,30 @@ def run_reference(args, rank, world):
                              "sample": f"{K} steps x {g} gates of the workload circuit at N={n}"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gates_per_s": gg / tt}
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
+# stdout carries exactly the one JSON line: everything else written to file
+# descriptor 1 -- NCCL's version banner at communicator init, library or
+# Python prints -- goes to stderr; the line is written to the saved stdout.
+_OUT_FD = None
+
+
+def emit(line: dict) -> None:
+    data = (json.dumps(line) + "\n").encode()
+    if _OUT_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_OUT_FD, data)
+
+
 def main():
+    global _OUT_FD
+    sys.stdout.flush()
+    _OUT_FD = os.dup(1)
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -475,7 +494,7 @@ def main():
                 "library": {"passes": st["passes"], "jit_passes": st["jit_passes"], "fused_gates": st["fused_gates"],
                             "sweeps": st["sweeps"],
                             "exchanges": st["exchanges"], "exchange_GB": st["exchange_bytes"] / 1e9}}
-        print(json.dumps(line), flush=True)
+        emit(line)
     s.close()
     if dist:
         dist.destroy_process_group()
