@@ -33,6 +33,26 @@ __device__ __forceinline__ void lp_prefetch_l2_128(const void *gmem) {
 #ifndef LP_STAGE_ASM
 #define LP_STAGE_ASM 1
 #endif
+// LP_CHECK (QSIM_LPASS_CHECK=1, specialised kernels): bounds checks of every
+// shared-memory and HBM address the pass forms -- tile slots, table and slot
+// reads in the coefficient pool, the tile's runs in the shard; a violation
+// prints and traps (the pool has no compute-sanitizer; PAPER-independent)
+#ifndef LP_CHECK
+#define LP_CHECK 0
+#endif
+#if LP_CHECK
+#define LP_ASSERT(c)                                                                                       \
+    do {                                                                                                   \
+        if (!(c)) {                                                                                        \
+            printf("lpass check failed: %s (block %d thread %d)\n", #c, (int)blockIdx.x, (int)threadIdx.x); \
+            __trap();                                                                                      \
+        }                                                                                                  \
+    } while (0)
+#else
+#define LP_ASSERT(c) \
+    do {             \
+    } while (0)
+#endif
 #ifndef LP_PREFETCH
 #define LP_PREFETCH 0  // L2 prefetch of the next tile (QSIM_LPASS_PREFETCH=1): measured slower, off
 #endif
@@ -193,9 +213,11 @@ __device__ __forceinline__ void lp_table(double2 (&v)[NS], const unsigned char *
 
 // tile load (cp.async) / store of the NJ = 2^(K-7) elements of this thread:
 // logical x = tid + NT j, j in Gray-code order (one column changes per step)
+// (slim, glo, ghi: the tile's shared-memory bytes and the shard's byte range, LP_CHECK only)
 template <int NJ>
 __device__ __forceinline__ void lp_tile_load(unsigned char *smem, const char *gp, uint32_t so, const uint32_t *s_hi,
-                                             const uint64_t *d_hi) {
+                                             const uint64_t *d_hi, uint32_t slim = 0, const char *glo = nullptr,
+                                             const char *ghi = nullptr) {
     uint64_t dj = 0;
 #pragma unroll
     for (int i = 0; i < NJ; ++i) {
@@ -203,12 +225,14 @@ __device__ __forceinline__ void lp_tile_load(unsigned char *smem, const char *gp
             so ^= s_hi[lp_ctz5(i)];
             dj ^= d_hi[lp_ctz5(i)];
         }
+        LP_ASSERT(so + 16u <= slim && gp + dj >= glo && gp + dj + 16 <= ghi);
         lp_cp_async16(smem + so, gp + dj);
     }
 }
 template <int NJ>
 __device__ __forceinline__ void lp_tile_store(const unsigned char *smem, char *gp, uint32_t mo, const uint32_t *m_hi,
-                                              const uint64_t *d_hi) {
+                                              const uint64_t *d_hi, uint32_t slim = 0, const char *glo = nullptr,
+                                              const char *ghi = nullptr) {
     uint64_t dj = 0;
 #pragma unroll
     for (int i = 0; i < NJ; ++i) {
@@ -216,13 +240,16 @@ __device__ __forceinline__ void lp_tile_store(const unsigned char *smem, char *g
             mo ^= m_hi[lp_ctz5(i)];
             dj ^= d_hi[lp_ctz5(i)];
         }
+        LP_ASSERT(mo + 16u <= slim && gp + dj >= glo && gp + dj + 16 <= ghi);
         *reinterpret_cast<double2 *>(gp + dj) = *reinterpret_cast<const double2 *>(smem + mo);
     }
 }
 // the same, every amplitude times the tile scalar c (LPassParams::nts)
 template <int NJ>
 __device__ __forceinline__ void lp_tile_store_scaled(const unsigned char *smem, char *gp, uint32_t mo,
-                                                     const uint32_t *m_hi, const uint64_t *d_hi, double2 c) {
+                                                     const uint32_t *m_hi, const uint64_t *d_hi, double2 c,
+                                                     uint32_t slim = 0, const char *glo = nullptr,
+                                                     const char *ghi = nullptr) {
     uint64_t dj = 0;
 #pragma unroll
     for (int i = 0; i < NJ; ++i) {
@@ -230,6 +257,7 @@ __device__ __forceinline__ void lp_tile_store_scaled(const unsigned char *smem, 
             mo ^= m_hi[lp_ctz5(i)];
             dj ^= d_hi[lp_ctz5(i)];
         }
+        LP_ASSERT(mo + 16u <= slim && gp + dj >= glo && gp + dj + 16 <= ghi);
         const double2 v = *reinterpret_cast<const double2 *>(smem + mo);
         const double pp = c.y * v.y, qq = c.y * v.x;
         *reinterpret_cast<double2 *>(gp + dj) = make_double2(fma(c.x, v.x, -pp), fma(c.x, v.y, qq));
@@ -301,6 +329,8 @@ __device__ __forceinline__ void lp_op1(double2 (&v)[1 << R], uint32_t &g, uint32
     }
     if (code == LOP_CODE_ROUND || code == LOP_CODE_DIAGT) lp_preflip(g, o, xq, full);
     const uint32_t toff = lp_toff<R>(h, o, xq, full, cpool_off);
+    LP_ASSERT(!(code == LOP_CODE_ROUND || code == LOP_CODE_DIAGT) ||
+              (toff >= cpool_off && toff + (uint32_t)NS * 16u <= cpool_off + (uint32_t)p.ncoef * 8u));
     if (code == LOP_CODE_ROUND) {
         lp_table<NS>(v, smem_raw, toff | (g << 4));
         lp_lifts<R>(v, g, (uint32_t)(h >> 24) & 0xffu, p.sc + o.pm);
@@ -320,6 +350,7 @@ __device__ __forceinline__ void lp_op1(double2 (&v)[1 << R], uint32_t &g, uint32
         double cr = 1.0, ci = 0.0;
         const int nf = (int)o.pmc[1];  // leading full-index-bit terms: this tile's product (lp_body)
         if (nf) {
+            LP_ASSERT(o.pmc[0] * 8u + 16u <= (uint32_t)p.ncoef * 8u && nf <= nt);
             const double2 c = *reinterpret_cast<const double2 *>(smem_raw + cpool_off + o.pmc[0] * 8u);
             cr = c.x;
             ci = c.y;
@@ -469,6 +500,7 @@ __device__ __forceinline__ void lp_stage(const LPassParams &p, const LpTile &t, 
 #pragma unroll
             for (int r = 0; r < R; ++r)
                 if (j & (1 << r)) ad ^= rp[r];
+            LP_ASSERT((a0[0] ^ ad) + 16u <= (16u << K) && (a0[1] ^ ad) + 16u <= (16u << K));
             v0[j] = lp_lds16(sbase + (a0[0] ^ ad));
             v1[j] = lp_lds16(sbase + (a0[1] ^ ad));
         }
@@ -501,6 +533,7 @@ __device__ __forceinline__ void lp_stage(const LPassParams &p, const LpTile &t, 
 #pragma unroll
             for (int r = 0; r < R; ++r)
                 if (j & (1 << r)) ad ^= rp[r];
+            LP_ASSERT(ad + 16u <= (16u << K));
             v[j] = lp_lds16(sbase + ad);
         }
         uint32_t g = g0;
@@ -554,6 +587,11 @@ __device__ __forceinline__ void lp_body(const LPassParams &p, const Stages &stag
     }
     __syncthreads();
     double2 *__restrict__ a = reinterpret_cast<double2 *>(p.a);
+#if LP_CHECK  // the tile's shared-memory bytes, the shard's bytes
+#define LP_LIMS , (uint32_t)L.cpool, reinterpret_cast<const char *>(a), reinterpret_cast<const char *>(a + (1ull << p.nl))
+#else
+#define LP_LIMS
+#endif
 
     for (uint64_t T = blockIdx.x; T < p.ntiles; T += gridDim.x) {
         uint64_t base = T << LP_LOW;
@@ -569,11 +607,11 @@ __device__ __forceinline__ void lp_body(const LPassParams &p, const Stages &stag
         if (!p.noio) {
             const char *gp = reinterpret_cast<const char *>(a + (base | d_tid));
             switch (K - TB) {
-                case 5: lp_tile_load<32>(smem_raw, gp, s_tid, s_hi, d_hi); break;
-                case 4: lp_tile_load<16>(smem_raw, gp, s_tid, s_hi, d_hi); break;
-                case 3: lp_tile_load<8>(smem_raw, gp, s_tid, s_hi, d_hi); break;
-                case 2: lp_tile_load<4>(smem_raw, gp, s_tid, s_hi, d_hi); break;
-                default: lp_tile_load<2>(smem_raw, gp, s_tid, s_hi, d_hi); break;
+                case 5: lp_tile_load<32>(smem_raw, gp, s_tid, s_hi, d_hi LP_LIMS); break;
+                case 4: lp_tile_load<16>(smem_raw, gp, s_tid, s_hi, d_hi LP_LIMS); break;
+                case 3: lp_tile_load<8>(smem_raw, gp, s_tid, s_hi, d_hi LP_LIMS); break;
+                case 2: lp_tile_load<4>(smem_raw, gp, s_tid, s_hi, d_hi LP_LIMS); break;
+                default: lp_tile_load<2>(smem_raw, gp, s_tid, s_hi, d_hi LP_LIMS); break;
             }
         }
         // ---- per-tile products of the PHASES terms on full-index bits (op slots
@@ -592,6 +630,7 @@ __device__ __forceinline__ void lp_body(const LPassParams &p, const Stages &stag
                     cr = nr;
                 }
             }
+            LP_ASSERT(o.pmc[0] * 8u + 16u <= (uint32_t)p.ncoef * 8u && T + 3 * o.pmc[1] <= p.sc + p.nsc);
             *reinterpret_cast<double2 *>(smem_raw + L.cpool + o.pmc[0] * 8u) = make_double2(cr, ci);
         }
         // ---- the tile scalar (conditional scalars on full-index bits, applied at the store) ----
@@ -607,6 +646,7 @@ __device__ __forceinline__ void lp_body(const LPassParams &p, const Stages &stag
                     cr = nr;
                 }
             }
+            LP_ASSERT((uint32_t)p.ts_slot * 8u + 16u <= (uint32_t)p.ncoef * 8u && p.ts_off + 4 * p.nts <= p.nsc);
             *reinterpret_cast<double2 *>(smem_raw + L.cpool + (uint32_t)p.ts_slot * 8u) = make_double2(cr, ci);
         }
         lp_cp_async_wait_all();
@@ -641,19 +681,19 @@ __device__ __forceinline__ void lp_body(const LPassParams &p, const Stages &stag
             const uint32_t mo = m_tid ^ (sbt << 4);
             if (tsc.x == 1.0 && tsc.y == 0.0) {
                 switch (K - TB) {
-                    case 5: lp_tile_store<32>(smem_raw, gp, mo, m_hi, d_hi); break;
-                    case 4: lp_tile_store<16>(smem_raw, gp, mo, m_hi, d_hi); break;
-                    case 3: lp_tile_store<8>(smem_raw, gp, mo, m_hi, d_hi); break;
-                    case 2: lp_tile_store<4>(smem_raw, gp, mo, m_hi, d_hi); break;
-                    default: lp_tile_store<2>(smem_raw, gp, mo, m_hi, d_hi); break;
+                    case 5: lp_tile_store<32>(smem_raw, gp, mo, m_hi, d_hi LP_LIMS); break;
+                    case 4: lp_tile_store<16>(smem_raw, gp, mo, m_hi, d_hi LP_LIMS); break;
+                    case 3: lp_tile_store<8>(smem_raw, gp, mo, m_hi, d_hi LP_LIMS); break;
+                    case 2: lp_tile_store<4>(smem_raw, gp, mo, m_hi, d_hi LP_LIMS); break;
+                    default: lp_tile_store<2>(smem_raw, gp, mo, m_hi, d_hi LP_LIMS); break;
                 }
             } else {
                 switch (K - TB) {
-                    case 5: lp_tile_store_scaled<32>(smem_raw, gp, mo, m_hi, d_hi, tsc); break;
-                    case 4: lp_tile_store_scaled<16>(smem_raw, gp, mo, m_hi, d_hi, tsc); break;
-                    case 3: lp_tile_store_scaled<8>(smem_raw, gp, mo, m_hi, d_hi, tsc); break;
-                    case 2: lp_tile_store_scaled<4>(smem_raw, gp, mo, m_hi, d_hi, tsc); break;
-                    default: lp_tile_store_scaled<2>(smem_raw, gp, mo, m_hi, d_hi, tsc); break;
+                    case 5: lp_tile_store_scaled<32>(smem_raw, gp, mo, m_hi, d_hi, tsc LP_LIMS); break;
+                    case 4: lp_tile_store_scaled<16>(smem_raw, gp, mo, m_hi, d_hi, tsc LP_LIMS); break;
+                    case 3: lp_tile_store_scaled<8>(smem_raw, gp, mo, m_hi, d_hi, tsc LP_LIMS); break;
+                    case 2: lp_tile_store_scaled<4>(smem_raw, gp, mo, m_hi, d_hi, tsc LP_LIMS); break;
+                    default: lp_tile_store_scaled<2>(smem_raw, gp, mo, m_hi, d_hi, tsc LP_LIMS); break;
                 }
             }
         }
