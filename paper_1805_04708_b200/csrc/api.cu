@@ -482,6 +482,17 @@ static int exchange_impl(qsim_state *s, const PlanOp &x, const PlanOp *gop, cons
     C = std::min<uint64_t>(C, 1ull << l);
     const uint64_t nchunks = half / C;
     const size_t ab = s->amp_bytes;
+    // bounds of every chunk the kernels and copies touch (checked, not assumed:
+    // no compute-sanitizer on the GPU pool): the exchanged global bit and the
+    // victim are in range, a chunk is a power of two that divides the half
+    // shard and fits under bit l (so its source run ins0(c C, l) .. + C is
+    // contiguous and inside the shard), and the staging buffers hold it
+    if (j < 0 || (s->P > 1 && (1 << j) >= s->P) || l < 0 || l >= s->nl || C == 0 || (C & (C - 1)) ||
+        half % C || C > (1ull << l) || C > s->chunk_amps) {
+        set_error("exchange: internal bounds check failed (g " + std::to_string(x.g) + ", l " + std::to_string(l) +
+                  ", chunk " + std::to_string(C) + ")");
+        return QSIM_EINVAL;
+    }
     auto fill = [&](XchgParams &p, const Shard &sh, int b, uint64_t c, const void *stg) {
         p.own = sh.amps;
         p.stage = stg;
