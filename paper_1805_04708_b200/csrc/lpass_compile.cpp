@@ -1198,17 +1198,12 @@ int lpass_compile(const LGate *gates, int ng, int nl, int K, int R, const int *t
         if (err) *err = c.err;
         return rc;
     }
-    // PHASES terms conditioned on full-index bits (outside the tile) have one
-    // product per tile: move them to the front of the op's term list (stable;
-    // the phases commute) and give the op a 2-double slot at the end of the
-    // coefficient pool, which the kernel fills once per tile (lp_body);
-    // the op then multiplies only its tile-bit terms per group.
-    // pmc[0] = slot offset in coef (doubles), pmc[1] = number of hoisted terms.
-    // Conditional scalars (a DIAG1 with T0 == T1 whose condition is on full-index
-    // bits only: a CPHASE with both qubits outside the tile) commute with every
-    // op of the pass: they become one product per tile (terms (omask, oval, e)
-    // in sc, formed in lp_body into a coefficient-pool slot) applied at the
-    // tile store, and the op a no-op (FLIP with gvec 0).
+    // Per-tile hoisting (values that are the same for every group of a tile).
+    // (1) Conditional scalars (a DIAG1 with T0 == T1 whose condition is on
+    // full-index bits only: a CPHASE with both qubits outside the tile) commute
+    // with every op of the pass: they become one product per tile (terms
+    // (omask, oval, e) in sc, formed in lp_body into a coefficient-pool slot)
+    // applied at the tile store, and the op a no-op (FLIP with gvec 0).
     std::vector<size_t> ts_ops;
     for (size_t i = 0; i < c.ops.size(); ++i) {
         const LOp &o = c.ops[i];
@@ -1237,6 +1232,12 @@ int lpass_compile(const LGate *gates, int ng, int nl, int K, int R, const int *t
         c.coef.push_back(1.0);
         c.coef.push_back(0.0);
     }
+    // (2) PHASES terms conditioned on full-index bits (outside the tile): move
+    // them to the front of the op's term list (stable; the phases commute) and
+    // give the op a 2-double slot at the end of the coefficient pool, which the
+    // kernel fills once per tile (lp_body); the op then multiplies only its
+    // tile-bit terms per group.  pmc[0] = slot offset in coef (doubles),
+    // pmc[1] = number of hoisted terms.
     int nops_ph = 0;
     for (size_t i = 0; i < c.ops.size(); ++i) {
         LOp &o = c.ops[i];
