@@ -1204,8 +1204,14 @@ int lpass_compile(const LGate *gates, int ng, int nl, int K, int R, const int *t
     // with every op of the pass: they become one product per tile (terms
     // (omask, oval, e) in sc, formed in lp_body into a coefficient-pool slot)
     // applied at the tile store, and the op a no-op (FLIP with gvec 0).
+    // the per-tile products are formed serially while the tile loads: worth it
+    // when a pass has many tiles (>= 1024, as the lookahead); on small,
+    // latency-bound passes it measured 2 us slower per config-1 circuit
+    // (LPASS_HOIST=1 / 0 forces it on / off)
+    static const int hoist_env = getenv("LPASS_HOIST") ? atoi(getenv("LPASS_HOIST")) : -1;
+    const bool hoist = hoist_env < 0 ? nl - K >= 10 : hoist_env != 0;
     std::vector<size_t> ts_ops;
-    for (size_t i = 0; i < c.ops.size(); ++i) {
+    for (size_t i = 0; i < c.ops.size() && hoist; ++i) {
         const LOp &o = c.ops[i];
         if (o.code != LOP_CODE_DIAG1 || !(o.flags & LF_COND) || o.tmask || !o.omask) continue;
         const double *T = &c.sc[o.coef];
@@ -1239,7 +1245,7 @@ int lpass_compile(const LGate *gates, int ng, int nl, int K, int R, const int *t
     // tile-bit terms per group.  pmc[0] = slot offset in coef (doubles),
     // pmc[1] = number of hoisted terms.
     int nops_ph = 0;
-    for (size_t i = 0; i < c.ops.size(); ++i) {
+    for (size_t i = 0; i < c.ops.size() && hoist; ++i) {
         LOp &o = c.ops[i];
         if (o.code != LOP_CODE_PHASES) continue;
         std::vector<double> full_t, tile_t;

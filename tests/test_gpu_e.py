@@ -661,17 +661,19 @@ def test_specialised_kernel_variants_match_the_oracle(tmp_path, knob):
         assert np.max(np.abs(a - oracle.e_simulate(20, circ))) <= TOL
 
 
+@pytest.mark.parametrize("hoist", ["1", "0"])
 @pytest.mark.parametrize("recipe,n,P", [("C.config(0, n=n, seed=3)", 14, 1), ("C.config(2, n=n)", 20, 1),
                                         ("C.qft(n, seed=5)[0]", 20, 1), ("C.random_circuit(n, 400, seed=11)", 16, 1),
                                         ("C.config(3, n=n)", 18, 4), ("C.config(2, n=n)", 19, 2)])
-def test_bounds_checked_pass_kernels(tmp_path, recipe, n, P):
+def test_bounds_checked_pass_kernels(tmp_path, recipe, n, P, hoist):
     """compute-sanitizer is closed on the GPU pool, so the specialised pass
     kernels have a checked build of their own (QSIM_LPASS_CHECK=1, LP_CHECK in
     lpass_dev.cuh): every shared-memory slot, table and coefficient-pool read
     and every HBM run of a tile is asserted in range (a violation traps and
     the process fails).  Small shards, the config-3/4 recipes, QFT ladders
-    (hoisted terms, tile scalars), random gate mixes, and sharded loopback
-    states (shard bits in the full index); results vs the oracle."""
+    (hoisted terms, tile scalars -- forced on with LPASS_HOIST=1 at these sizes,
+    and off), random gate mixes, and sharded loopback states (shard bits in
+    the full index); results vs the oracle."""
     import os
     import subprocess
     import sys
@@ -681,7 +683,7 @@ def test_bounds_checked_pass_kernels(tmp_path, recipe, n, P):
     code = ("import sys, numpy as np; sys.path.insert(0, %r); import paper_1805_04708_b200 as q, qsim_inputs as C; "
             "n = %d; s = q.State(n, q.ENC_FP64, %d); s.apply_circuit(%s); q.qsim_jit_sync(); st = s.stats(); "
             "np.save(%r, s.get_state()); print(st['jit_passes'], st['passes'])" % (root, n, P, recipe, out))
-    env = dict(os.environ, QSIM_LPASS_JIT="2", QSIM_LPASS_CHECK="1", QSIM_JIT_DISK_CACHE="0")
+    env = dict(os.environ, QSIM_LPASS_JIT="2", QSIM_LPASS_CHECK="1", QSIM_JIT_DISK_CACHE="0", LPASS_HOIST=hoist)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and "lpass check failed" not in r.stdout + r.stderr, r.stdout + r.stderr
     jit, passes = (int(x) for x in r.stdout.split()[-2:])

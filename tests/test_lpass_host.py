@@ -45,7 +45,8 @@ def test_scheduler_whole_circuits(emu, seed, forced):
     """lpass_run (the runtime's pass scheduler, with diagonals carried across
     stages and deferred across passes) on whole random and layered circuits:
     terminates and equals sequential application."""
-    env = dict(os.environ, **FORCED) if forced else None
+    # LPASS_HOIST=1: the per-tile hoisting on these small states too (auto: >= 1024 tiles)
+    env = dict(os.environ, LPASS_HOIST="1", **(FORCED if forced else {}))
     out = subprocess.run([emu, "30", str(seed), "run"], capture_output=True, text=True, timeout=300, env=env)
     assert out.returncode == 0, out.stdout + out.stderr
     assert out.stdout.startswith("ok"), out.stdout
