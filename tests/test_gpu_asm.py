@@ -44,27 +44,40 @@ GENERATE EVENTS 4096 77
 """
 
 
+# the instructions EC uses, read here independently of the library's parser:
+# matrices from the App. B table (qsim_inputs), CNOT /
+# TOFFOLI = X on the last operand controlled by the others
+_GATES = {"H": C.mat_H, "T": C.mat_T, "X": C.mat_X}
+
+
 def _oracle_run(text, seed):
     """The instruction semantics of App. B on the state-vector oracle."""
-    d = q.asm_parse(text)
-    n = d["n"]
+    lines = [ln.split("!")[0].split() for ln in text.splitlines()]
+    lines = [ln for ln in lines if ln]
+    assert lines[0][0] == "QUBITS" and not any(ln[0] == "BIT" for ln in lines)
+    n = int(lines[0][1])
     a = oracle.e_init(n)
     tables, outcomes = [], []
     u = C.splitmix_uniform(seed, 64)
     k = 0
-    for o in d["ops"]:
-        if o["type"] == q.ASM_GATE:
-            a = oracle.e_apply(a, n, o["u"], o["target"], o["controls"])
-        elif o["type"] == q.ASM_MEASURE_ALL:
+    for ln in lines[1:]:
+        op, args = ln[0], [int(x) for x in ln[1:] if x.lstrip("-").isdigit()]
+        if op in _GATES:
+            a = oracle.e_apply(a, n, _GATES[op](), args[0], [])
+        elif op in ("CNOT", "TOFFOLI"):
+            a = oracle.e_apply(a, n, C.mat_X(), args[-1], args[:-1])
+        elif op == "BEGIN":
             tables.append(oracle.e_expectations(a, n))
-        elif o["type"] == q.ASM_M:
-            out, _ = oracle.e_measure(a, n, o["args"][0], u[k])
-            outcomes.append((o["args"][0], out))
+        elif op == "M":
+            out, _ = oracle.e_measure(a, n, args[0], u[k])
+            outcomes.append((args[0], out))
             k += 1
-        elif o["type"] in (q.ASM_CLEAR, q.ASM_SET):
-            assert oracle.e_project(a, n, o["args"][0], 1 if o["type"] == q.ASM_SET else 0) == 0
-        elif o["type"] == q.ASM_EVENTS:
+        elif op in ("CLEAR", "SET"):
+            assert oracle.e_project(a, n, args[0], 1 if op == "SET" else 0) == 0
+        elif op == "GENERATE":
             break
+        else:
+            raise AssertionError(f"instruction not modelled here: {op}")
     return np.array(tables), outcomes, a
 
 
