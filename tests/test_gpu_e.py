@@ -638,12 +638,14 @@ def test_specialised_kernels_with_phase_ops_match_the_oracle(tmp_path, recipe, n
     (QSIM_LPASS_JIT=2) on programs with DIAG1 / PHASES ops (QFT ladders,
     controlled phases with outside controls, random gate mixes, the config-4
     recipe in E): the state equals the interpreter's and the oracle's."""
-    a, jit, passes = _run_n22(2, tmp_path, recipe, n)
-    b, jit0, _ = _run_n22(0, tmp_path, recipe, n)
-    assert passes > 0 and jit == passes and jit0 == 0
-    assert np.max(np.abs(a - b)) <= 1e-14
     circ = eval(recipe, {"C": C, "n": n})
-    assert np.max(np.abs(a - oracle.e_simulate(n, circ))) <= TOL
+    ref = oracle.e_simulate(n, circ)
+    for hoist in ("1", "0"):  # per-tile hoisting forced on (auto: off below 1024 tiles) and off
+        a, jit, passes = _run_n22(2, tmp_path, recipe, n, {"LPASS_HOIST": hoist})
+        b, jit0, _ = _run_n22(0, tmp_path, recipe, n, {"LPASS_HOIST": hoist})
+        assert passes > 0 and jit == passes and jit0 == 0
+        assert np.max(np.abs(a - b)) <= 1e-14
+        assert np.max(np.abs(a - ref)) <= TOL
 
 
 @pytest.mark.parametrize("knob", [{"QSIM_LPASS_G": "2"}, {"QSIM_LPASS_NT": "256"}, {"QSIM_LPASS_PREFETCH": "1"},
