@@ -356,6 +356,13 @@ int qsim_set_codes(qsim_state *s, const int8_t *codes, double r0, double r1);
  * allocations (so a benchmark step can start from the method's input state). */
 int qsim_reset(qsim_state *s);
 
+/* Re-initialise to the basis state |x> (logical index x, bit q = qubit q,
+ * PAPER.md:255-258): a(x) = 1, every other amplitude 0 -- the state X on the
+ * set bits of x makes from |0...0>, prepared without a pass over the state
+ * beyond the reset (config 5's input |x>).  Resets the qubit map like
+ * qsim_reset.  EINVAL unless x < 2^N or while a graph capture is open. */
+int qsim_reset_basis(qsim_state *s, uint64_t x);
+
 /* Per-kernel-class timing: while enabled, every library kernel launch is
  * bracketed by CUDA events on the launching stream.  qsim_profile_read
  * synchronises, aggregates the finished records per class into out[0..max)

@@ -92,7 +92,7 @@ EXPORTS = (
     "qsim_create", "qsim_create_ex", "qsim_destroy", "qsim_nccl_unique_id", "qsim_apply_gate", "qsim_apply_swap",
     "qsim_apply_circuit", "qsim_norm", "qsim_probabilities", "qsim_expectations", "qsim_measure", "qsim_measure_u",
     "qsim_get_amplitudes", "qsim_get_state", "qsim_set_state", "qsim_get_codes", "qsim_set_codes", "qsim_sync",
-    "qsim_project", "qsim_sample", "qsim_prepare_shorbox", "qsim_stream", "qsim_get_stats", "qsim_reset", "qsim_profile", "qsim_profile_read", "qsim_reset_stats", "qsim_get_qubit_map", "qsim_last_error",
+    "qsim_project", "qsim_sample", "qsim_prepare_shorbox", "qsim_stream", "qsim_get_stats", "qsim_reset", "qsim_reset_basis", "qsim_profile", "qsim_profile_read", "qsim_reset_stats", "qsim_get_qubit_map", "qsim_last_error",
     "qsim_plan_create", "qsim_plan_num_ops", "qsim_plan_get_op", "qsim_plan_final_map", "qsim_plan_destroy",
     "qsim_aux_amplitudes", "qsim_aux_num_vars", "qsim_set_qubit_map",
     "qsim_asm_parse", "qsim_asm_info", "qsim_asm_get_op", "qsim_asm_destroy", "qsim_asm_run",
@@ -168,6 +168,7 @@ _lib.qsim_get_stats.argtypes = [_P, ctypes.POINTER(qsim_stats)]
 _lib.qsim_reset_stats.argtypes = [_P]
 _lib.qsim_get_qubit_map.argtypes = [_P, _ip]
 _lib.qsim_reset.argtypes = [_P]
+_lib.qsim_reset_basis.argtypes = [_P, ctypes.c_uint64]
 _lib.qsim_profile.argtypes = [_P, ctypes.c_int]
 _lib.qsim_profile_read.argtypes = [_P, ctypes.POINTER(qsim_kernel_profile), ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
 _lib.qsim_plan_create.argtypes = [ctypes.c_int, ctypes.c_int, _ip, ctypes.POINTER(qsim_gate), ctypes.c_size_t,
@@ -521,6 +522,10 @@ def qsim_reset(h):
     _check(_lib.qsim_reset(h))
 
 
+def qsim_reset_basis(h, x):
+    _check(_lib.qsim_reset_basis(h, int(x)))
+
+
 def qsim_profile(h, enable=True):
     _check(_lib.qsim_profile(h, 1 if enable else 0))
 
@@ -695,6 +700,11 @@ class State:
 
     def reset(self):
         qsim_reset(self.h)
+        return self
+
+    def reset_basis(self, x):
+        """|x> (logical index x): the state X on the set bits of x makes from |0...0>."""
+        qsim_reset_basis(self.h, x)
         return self
 
     def profile(self, enable=True):

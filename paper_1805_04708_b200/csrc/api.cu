@@ -1634,6 +1634,42 @@ int qsim_reset(qsim_state *s) {
     return init_state(s);
 }
 
+int qsim_reset_basis(qsim_state *s, uint64_t x) {
+    GROUP_ALL(s, qsim_reset_basis(m_, x));
+    if (!s) return QSIM_EINVAL;
+    if (s->n < 64 && (x >> s->n)) {
+        set_error("qsim_reset_basis: x must be < 2^N");
+        return QSIM_EINVAL;
+    }
+    RC(qsim_reset(s));  // |0...0>, identity qubit map
+    if (!x) return QSIM_OK;
+    // move the single 1 from physical index 0 to physical index x (the map is the identity)
+    const uint64_t lmask = (1ull << s->nl) - 1ull;
+    for (auto &sh : s->shards) {
+        const uint64_t base = shard_base(s, sh);
+        if (base == 0) {  // holds index 0: back to zero
+            if (s->enc == QSIM_ENC_FP64) {
+                CU(cudaMemsetAsync(sh.amps, 0, 16, s->stream));
+            } else {
+                static const uint16_t zero_code = 0x0080u;  // (b0, b1) = (-128, 0)
+                CU(cudaMemcpyAsync(sh.amps, &zero_code, 2, cudaMemcpyHostToDevice, s->stream));
+            }
+        }
+        if (base == (x & ~lmask)) {
+            char *dst = static_cast<char *>(sh.amps) + (x & lmask) * s->amp_bytes;
+            if (s->enc == QSIM_ENC_FP64) {
+                static const double one[2] = {1.0, 0.0};
+                CU(cudaMemcpyAsync(dst, one, 16, cudaMemcpyHostToDevice, s->stream));
+            } else {
+                static const uint16_t one_code = 0x007fu;  // (b0, b1) = (127, 0): r = 1 exactly
+                CU(cudaMemcpyAsync(dst, &one_code, 2, cudaMemcpyHostToDevice, s->stream));
+            }
+        }
+    }
+    CU(cudaStreamSynchronize(s->stream));
+    return QSIM_OK;
+}
+
 int qsim_profile(qsim_state *s, int enable) {
     GROUP_ALL(s, qsim_profile(m_, enable));
     if (!s) return QSIM_EINVAL;

@@ -694,6 +694,42 @@ def test_bounds_checked_pass_kernels(tmp_path, recipe, n, P, hoist):
     assert np.max(np.abs(np.load(out) - oracle.e_simulate(n, circ))) <= TOL
 
 
+@pytest.mark.parametrize("P", [1, 4])
+def test_reset_basis_is_the_x_prepared_state(P):
+    """qsim_reset_basis(x): the basis state X on the set bits of x makes from
+    |0...0> (config 5's input |x>); the QFT from it equals the oracle's QFT of
+    the X-prepared state, and the closed form 2^{-N/2} e^{2 pi i x y / 2^N}."""
+    n = 16
+    circ, x = C.qft(n, seed=7)
+    core = C.qft_register(n, n)
+    assert len(circ) == len(core) + bin(x).count("1")
+    ref = oracle.e_simulate(n, circ)
+    with q.State(n, q.ENC_FP64, P) as s:
+        s.reset_basis(x)
+        basis = s.get_state()
+        assert basis[x] == 1.0 and np.count_nonzero(basis) == 1
+        s.apply_circuit(core)
+        got = s.get_state()
+        assert np.max(np.abs(got - ref)) <= TOL
+        y = np.arange(1 << n)
+        closed = np.exp(2j * np.pi * ((x * y) % (1 << n)) / (1 << n)) / 2 ** (n / 2)
+        assert np.max(np.abs(got - closed)) <= TOL
+        s.reset_basis(0)
+        z = s.get_state()
+        assert z[0] == 1.0 and np.count_nonzero(z) == 1
+        with pytest.raises(q.QsimError):
+            s.reset_basis(1 << n)
+    # A: the same codes as the X-prepared state (X moves codes, PAPER.md:442-444)
+    xs = C.Circuit(n)
+    for b in range(n):
+        if (x >> b) & 1:
+            xs.add("X", C.mat_X(), b)
+    with q.State(n, q.ENC_ADAPTIVE2, P) as a, q.State(n, q.ENC_ADAPTIVE2, P) as b:
+        a.reset_basis(x)
+        b.apply_circuit(xs)
+        assert np.array_equal(a.get_codes()[0], b.get_codes()[0])
+
+
 def _apply_matrix_ref(psi, n, U, qubits):
     """Test-side reference: U (2^k x 2^k, qubits[0] the most significant index)
     on a logical state vector (numpy; bit j of the index = qubit j)."""
