@@ -14,6 +14,8 @@ check the config names, computed here on the GPU results:
   cfg5_n32   E QFT, N=32 (config 5's 2^32 amplitudes per GPU) of a seeded basis
              state; closed form 2^{-N/2} e^{2 pi i x y / 2^N} on 2^20 sampled y,
              marginals = 1/2.
+  cfg5_n32_basis  the same with |x> from qsim_reset_basis and the 544-gate QFT
+             circuit alone timed.
   s1_hwall   H wall, E N=32 and A N=35 (64 GiB each); closed form.
   s2_ghz     CNOT chain (H + CNOT(i -> i+1)), E N=32 and A N=35; closed form.
 
@@ -109,6 +111,42 @@ def cfg5_n32():
                    max_marginal_err=float(np.max(np.abs(p1 - 0.5))))
 
 
+def cfg5_n32_basis():
+    """Config 5 with the input |x> prepared by qsim_reset_basis (outside the
+    timed region, like the reset of every row) and the standard QFT circuit
+    timed: 544 gates at N = 32 (no X gates, so no relabel-only pass)."""
+    n = 32
+    _, x = C.qft(n, seed=5)
+    circ = C.qft_register(n, n)
+    rng = np.random.default_rng(55)
+    ys = rng.integers(0, 2 ** n, size=2 ** 20, dtype=np.uint64)
+    gates = q.pack_gates(circ)
+    with q.State(n, q.ENC_FP64, 1) as s:
+        s.reset_basis(x)
+        s.apply_circuit(gates)
+        s.sync()
+        q.qsim_jit_sync()
+        s.reset_basis(x)
+        s.sync()
+        s.reset_stats()
+        s.profile(True)
+        s.profile_read()
+        t0 = time.perf_counter()
+        s.apply_circuit(gates)
+        s.sync()
+        wall = time.perf_counter() - t0
+        prof = s.profile_read()
+        s.profile(False)
+        st = s.stats()
+        dev = sum(v["ms"] for v in prof.values())
+        z = s.get_amplitudes(ys)
+        p1 = s.probabilities()
+    ph = (int(x) * ys.astype(object)) % (2 ** n)
+    ref = 2.0 ** (-n / 2) * np.exp(2j * math.pi * np.array([float(v) for v in ph]) / 2.0 ** n)
+    return summary("cfg5_basis", circ, dev, wall, prof, st, x=int(x), max_err_sampled=float(np.max(np.abs(z - ref))),
+                   max_marginal_err=float(np.max(np.abs(p1 - 0.5))))
+
+
 def s1_hwall():
     rows = []
     for n, enc in ((32, q.ENC_FP64), (35, q.ENC_ADAPTIVE2)):
@@ -197,7 +235,7 @@ def cfg4_trend():
     return rows
 
 
-ROWS = {"cfg4_lazy": cfg4_lazy, "table4_adder": table4_adder, "cfg4_trend": cfg4_trend, "cfg3_n33": cfg3_n33, "cfg4_n33": cfg4_n33, "cfg5_n32": cfg5_n32, "s1_hwall": s1_hwall, "s2_ghz": s2_ghz}
+ROWS = {"cfg4_lazy": cfg4_lazy, "table4_adder": table4_adder, "cfg4_trend": cfg4_trend, "cfg3_n33": cfg3_n33, "cfg4_n33": cfg4_n33, "cfg5_n32": cfg5_n32, "cfg5_n32_basis": cfg5_n32_basis, "s1_hwall": s1_hwall, "s2_ghz": s2_ghz}
 want = sys.argv[1:] or list(ROWS)
 out = []
 for name in want:
