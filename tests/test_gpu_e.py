@@ -730,6 +730,47 @@ def test_reset_basis_is_the_x_prepared_state(P):
         assert np.array_equal(a.get_codes()[0], b.get_codes()[0])
 
 
+@pytest.mark.parametrize("enc", ["E", "A"])
+@pytest.mark.parametrize("P", [1, 4])
+def test_empty_inputs_and_smallest_states(enc, P):
+    """Degenerate inputs: an empty circuit leaves |0...0> (and the stats at
+    zero gates), an empty index list reads nothing, zero samples draw nothing;
+    the smallest states (N = 2, and the smallest sharded N = 10 + log2 P) run
+    a circuit equal to the oracle's."""
+    e = q.ENC_FP64 if enc == "E" else q.ENC_ADAPTIVE2
+    n = 10 + int(math.log2(P)) if P > 1 else 2
+    with q.State(n, e, P) as s:
+        s.apply_circuit(C.Circuit(n))
+        z = s.get_state()
+        assert z[0] == 1.0 and np.count_nonzero(z) == 1
+        assert s.stats()["gates"] == 0
+        assert s.get_amplitudes(np.array([], dtype=np.uint64)).size == 0
+        assert s.sample(0, 1).size == 0
+        if enc == "E":
+            kinds = tuple(k for k in C.CFG1_KINDS if k != "TOFFOLI") if n < 3 else C.CFG1_KINDS
+            circ = C.random_circuit(n, 60, seed=n + P, kinds=kinds)
+        else:  # H wall, a CNOT, phases, X: codes equal to the oracle-A's
+            circ = C.h_wall(n)
+            circ.add("CNOT", C.mat_X(), n - 1, [0])
+            circ.add("T", C.mat_T(), 1)
+            circ.add("Z", C.mat_Z(), n - 1)
+            circ.add("X", C.mat_X(), 0)
+        s.apply_circuit(circ)
+        got = s.get_state()
+        codes = s.get_codes()[0] if enc == "A" else None
+    if enc == "E":
+        assert np.max(np.abs(got - oracle.e_simulate(n, circ))) <= TOL
+    else:  # decoded amplitudes equal the oracle-A's within one step (the codes themselves
+        # may differ where every magnitude ties: degenerate bounds r0 = r1 decided by an ulp)
+        ra = oracle.AState(n).run(circ)
+        zr = ra.decoded()
+        step = (ra.r1 - ra.r0) / 253.0
+        assert codes.size == 2 << n
+        assert np.max(np.abs(np.abs(got) - np.abs(zr))) <= step + 1e-12
+        both = (np.abs(got) > 0) & (np.abs(zr) > 0)
+        assert np.all(np.abs(np.angle(got[both] * np.conj(zr[both]))) <= math.pi / 128 + 1e-12)
+
+
 def _apply_matrix_ref(psi, n, U, qubits):
     """Test-side reference: U (2^k x 2^k, qubits[0] the most significant index)
     on a logical state vector (numpy; bit j of the index = qubit j)."""
