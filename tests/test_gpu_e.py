@@ -771,6 +771,33 @@ def test_empty_inputs_and_smallest_states(enc, P):
         assert np.all(np.abs(np.angle(got[both] * np.conj(zr[both]))) <= math.pi / 128 + 1e-12)
 
 
+@pytest.mark.parametrize("enc,P", [("E", 1), ("E", 4), ("A", 1), ("A", 2)])
+def test_repeated_runs_are_bit_identical(enc, P):
+    """A race detector by determinism (compute-sanitizer's racecheck is closed
+    on the pool): every kernel's arithmetic and every reduction here has a
+    fixed order (the A bounds are exact extremes, order-free), so the same
+    circuit run again from |0...0> must give the same bits -- a shared-memory
+    race in the tile pass, the exchange or the A kernels' warp queues would
+    show up as run-to-run differences.  Four runs, states / codes and
+    probabilities compared bit for bit."""
+    n = 22 if enc == "E" else 18
+    e = q.ENC_FP64 if enc == "E" else q.ENC_ADAPTIVE2
+    circ = C.config(2, n=n) if enc == "E" else C.config(3, n=n)
+    gates = q.pack_gates(circ)
+    outs = []
+    with q.State(n, e, P) as s:
+        s.apply_circuit(gates)  # warm-up: the pass specialisations it queues are ready below
+        s.sync()
+        q.qsim_jit_sync()
+        for _ in range(4):
+            s.reset()
+            s.apply_circuit(gates)
+            st = s.get_codes()[0] if enc == "A" else s.get_state()
+            outs.append((st, s.probabilities()))
+    for st, pr in outs[1:]:
+        assert np.array_equal(st, outs[0][0]) and np.array_equal(pr, outs[0][1])
+
+
 def _apply_matrix_ref(psi, n, U, qubits):
     """Test-side reference: U (2^k x 2^k, qubits[0] the most significant index)
     on a logical state vector (numpy; bit j of the index = qubit j)."""
